@@ -1,0 +1,51 @@
+# Build of the B200-native IC(k) path and of its CPU checkers.
+#   make lib     -> paper_1601_05871_b200/lib/libtacho_b200.so (sm_100a)
+#   make oracle  -> oracle/_build/liboracle.so   (plain-C restatement, test-only)
+#   make ref     -> oracle/_ref/libtaskchol_ref.so (reference headers, only
+#                   where /root/reference exists)
+NVCC ?= /usr/local/cuda/bin/nvcc
+CXX ?= g++
+CC ?= gcc
+
+PKG := paper_1601_05871_b200
+SRC := $(PKG)/csrc
+OUT := $(PKG)/lib
+OBJ := build/obj
+
+ARCH := -gencode arch=compute_100a,code=sm_100a
+# -fmad=false: no FMA contraction anywhere (bitwise parity with the reference);
+# the kernel also spells every product/difference with __dmul_rn/__dsub_rn.
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v
+CXXFLAGS := -O2 -std=c++17 -fPIC -pthread -Wall -Wextra -ffp-contract=off
+
+HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generators.cpp \
+             $(SRC)/host/plan.cpp $(SRC)/capi.cpp
+HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
+DEV_OBJS := $(OBJ)/device/factor_kernel.o
+
+.PHONY: all lib oracle ref clean
+all: lib oracle
+
+lib: $(OUT)/libtacho_b200.so
+
+$(OBJ)/%.o: $(SRC)/%.cpp $(wildcard $(SRC)/host/*.hpp) include/tacho_b200.h
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -I/usr/local/cuda/include -c $< -o $@
+
+$(OBJ)/device/factor_kernel.o: $(SRC)/device/factor_kernel.cu $(SRC)/device/factor_kernel.cuh
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_factor_kernel.txt || (cat build/ptxas_factor_kernel.txt; false)
+
+$(OUT)/libtacho_b200.so: $(HOST_OBJS) $(DEV_OBJS)
+	@mkdir -p $(OUT)
+	$(NVCC) $(ARCH) -shared -o $@ $^ -Xcompiler -pthread
+
+oracle:
+	$(MAKE) -C oracle
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf build $(OUT)/*.so
+	$(MAKE) -C oracle clean

@@ -1,0 +1,186 @@
+/*
+ * tacho_b200.h — C ABI of the B200-native numeric IC(k) Cholesky-by-blocks.
+ *
+ * The reference (arXiv 1601.05871, "Tacho" re-implementation `taskchol`) has
+ * no FFI: its replaceable unit on the hot path is the C++ function
+ *
+ *   FactorResult factor_by_blocks(const CsrMatrix& a_permuted,
+ *                                 const FillPattern& fp,
+ *                                 const RangeList& ranges,
+ *                                 TaskPolicy& policy);
+ *   (reference proj/include/taskchol/factorize.hpp:134-137)
+ *
+ * This header is the plain-pointer boundary below a C++ drop-in with the same
+ * semantics (include/tacho_b200.hpp: factor_by_blocks_gpu). No exception
+ * crosses it; every call returns a tcg_status. One context per host thread.
+ *
+ * Entry points and the reference interface each one replaces:
+ *   tcg_plan_build    build_block_matrix + the generation walk of
+ *                     factor_by_blocks/export_task_dag, flattened
+ *                     (block_layout.hpp:98-181, factorize.hpp:169-225,260-302)
+ *   tcg_upload        the one-arena upload of U values, block-CSR work
+ *                     tables, the task DAG and dependence counters
+ *                     (replaces the TaskView/Future state, block_layout.hpp:66-93)
+ *   tcg_factor        spawn-all + wait(policy) over the whole DAG, executing
+ *                     chol/trsm/herk/gemm_block (kernels.hpp:40-132) on the
+ *                     GPU; breakdown latch and rethrow (factorize.hpp:146-167,229)
+ *   tcg_download      the factored FactorResult::factor.values
+ *   tcg_last_error    message of BreakdownError / invalid_argument / CUDA
+ */
+#ifndef TACHO_B200_H_
+#define TACHO_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TCG_OK = 0,
+  TCG_BREAKDOWN = 1,   /* non-positive pivot: reference BreakdownError(row, pivot) */
+  TCG_INVALID = 2,     /* malformed input: reference std::invalid_argument / logic_error */
+  TCG_CUDA = 3,        /* CUDA runtime failure */
+  TCG_TIMEOUT = 4      /* device watchdog expired (stalled DAG; reference SchedulerError) */
+} tcg_status;
+
+typedef enum { TCG_CHOL = 0, TCG_TRSM = 1, TCG_HERK = 2, TCG_GEMM = 3 } tcg_task_kind;
+
+typedef struct tcg_ctx tcg_ctx;
+typedef struct tcg_plan tcg_plan;
+
+/* CSR view with the reference's index types (csr_matrix.hpp:16-28). */
+typedef struct {
+  int32_t n;
+  int64_t nnz;
+  const int64_t* row_ptr; /* n + 1 */
+  const int32_t* col_idx; /* nnz, strictly increasing per row */
+  const double* values;   /* nnz (may be NULL for a pattern) */
+} tcg_csr_view;
+
+/* Flattened problem image (what tcg_upload copies into the device arena). */
+typedef struct {
+  int32_t n;
+  int64_t nnz;
+  const int32_t* col_idx;      /* U columns */
+  const double* values;        /* initialised U values (init_factor_values) */
+  int64_t ntasks;
+  const int32_t* task_rec;     /* 8 words per task */
+  int64_t nitems;
+  const int32_t* item_rec;     /* 8 words per item */
+  int64_t nsources;
+  const int32_t* src_rec;      /* 4 words per source */
+  int64_t nedges;
+  const int32_t* succ;         /* successor lists, grouped per task */
+  const int32_t* indeg;        /* dependence counters per task */
+  int64_t nroots;
+  const int32_t* roots;        /* tasks with no predecessor, ascending */
+  int32_t max_target_len;
+  int32_t max_flag_rows;
+} tcg_problem;
+
+typedef struct {
+  int32_t threads_per_cta;  /* 128, 256 or 512; 0 = default (256) */
+  int32_t ctas_per_sm;      /* 0 = occupancy maximum */
+  int32_t staging_cap;      /* target-row entries staged per warp; 0 = auto */
+  double timeout_s;         /* device watchdog; 0 = default (30 s) */
+  int32_t trace;            /* 1 = record per-task start/end globaltimer stamps */
+} tcg_options;
+
+typedef struct {
+  double device_ms;          /* persistent kernel, CUDA events on the launch stream */
+  int64_t tasks_completed;
+  int64_t tasks_executed;    /* bodies run (a breakdown skips the rest) */
+  int32_t breakdown_row;     /* -1 when none */
+  double breakdown_pivot;
+  int32_t grid_ctas;
+  int32_t threads_per_cta;
+  int32_t staging_cap;
+  int64_t smem_bytes;
+  int32_t kernel_launches;   /* device launches issued by the call */
+} tcg_stats;
+
+typedef struct {
+  int64_t tasks[4];          /* chol, trsm, herk, gemm */
+  int64_t edges, items, sources, pairs, empty_tasks;
+  int32_t max_target_len, max_flag_rows, dag_depth;
+  int32_t nblocks_rows;      /* block rows m (= number of ranges) */
+  int64_t nblocks;
+  double block_build_seconds, plan_seconds;
+} tcg_plan_stats;
+
+/* ---- host flattener ---------------------------------------------------- */
+/* a_permuted: PᵀAP (full symmetric CSR with values); pattern: fp.pattern
+ * (upper, full diagonal); range_bounds: nranges + 1 ascending row bounds. */
+tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pattern,
+                          int32_t nranges, const int32_t* range_bounds, tcg_plan** out);
+void tcg_plan_free(tcg_plan* plan);
+const char* tcg_plan_error(void); /* message of the last failed tcg_plan_build (thread-local) */
+tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* out);
+tcg_status tcg_plan_get_stats(const tcg_plan* plan, tcg_plan_stats* out);
+/* DAG in generation order, the export_task_dag contract (factorize.hpp:260-302):
+ * node kind/block_row/block_col and edges (before, after) in emission order.
+ * Pointers stay valid until tcg_plan_free. */
+tcg_status tcg_plan_dag(const tcg_plan* plan, int64_t* nnodes, const int32_t** kind,
+                        const int32_t** block_row, const int32_t** block_col, int64_t* nedges,
+                        const int32_t** edge_from, const int32_t** edge_to);
+/* Block structure (brow_ptr m+1, bcol_idx nblocks), reference BlockMatrix. */
+tcg_status tcg_plan_blocks(const tcg_plan* plan, int32_t* m, const int64_t** brow_ptr,
+                           int64_t* nblocks, const int32_t** bcol_idx);
+
+/* ---- device context ---------------------------------------------------- */
+tcg_status tcg_create(int device, tcg_ctx** out);
+void tcg_destroy(tcg_ctx* ctx);
+const char* tcg_last_error(const tcg_ctx* ctx);
+tcg_status tcg_set_options(tcg_ctx* ctx, const tcg_options* opt);
+/* One cudaMalloc arena; replaces any previous upload. */
+tcg_status tcg_upload(tcg_ctx* ctx, const tcg_problem* problem);
+/* Replace the initial values (host pointer, nnz doubles) of the uploaded problem. */
+tcg_status tcg_set_values(tcg_ctx* ctx, const double* values);
+/* Restore the working values from the device copy of the initial values. */
+tcg_status tcg_restore(tcg_ctx* ctx);
+/* Factor the working values in place. TCG_BREAKDOWN sets stats->breakdown_*. */
+tcg_status tcg_factor(tcg_ctx* ctx, tcg_stats* stats);
+tcg_status tcg_download(tcg_ctx* ctx, double* values);
+/* Per-task {start, end} globaltimer stamps of the last traced factor (2*ntasks). */
+tcg_status tcg_download_trace(tcg_ctx* ctx, uint64_t* stamps);
+/* Device pointer to the working values and their count (for in-process users
+ * that keep U resident, e.g. a preconditioner apply on the same stream). */
+tcg_status tcg_device_values(tcg_ctx* ctx, double** dptr, int64_t* nnz);
+/* Bytes of the device arena. */
+int64_t tcg_arena_bytes(const tcg_ctx* ctx);
+
+/* ---- host input side (analysis) ---------------------------------------- */
+/* Own implementations of the reference's analysis chain (pipeline.hpp:35-55),
+ * kept bit-exact with it; they produce the inputs of tcg_plan_build. */
+typedef struct tch_matrix tch_matrix;
+typedef struct tch_analysis tch_analysis;
+
+/* kind: "grid2d" (p0 x p1), "lap7" (p0^3), "stencil27" (p0^3, seed),
+ * "elasticity" (p0^3 x 3, seed), "diffusion" (p0^3, seed, sigma = p1 / 1000),
+ * "path" (p0, diag = 2), "random_spd" (p0, density = p1 / 1e6, seed). */
+tch_matrix* tch_generate(const char* kind, int64_t p0, int64_t p1, uint64_t seed);
+tch_matrix* tch_matrix_from_csr(const tcg_csr_view* view);
+void tch_matrix_free(tch_matrix* m);
+void tch_matrix_view(const tch_matrix* m, tcg_csr_view* out);
+
+tch_analysis* tch_analyze(const tch_matrix* a, int32_t level, int32_t treecut,
+                          int32_t leaf_size, int32_t max_depth, int32_t threads);
+void tch_analysis_free(tch_analysis* an);
+const char* tch_error(void); /* thread-local message of the last tch_* failure */
+void tch_analysis_perm(const tch_analysis* an, const int32_t** perm, const int32_t** iperm);
+int32_t tch_analysis_ranges(const tch_analysis* an, const int32_t** bounds); /* returns count */
+void tch_analysis_permuted(const tch_analysis* an, tcg_csr_view* out);
+void tch_analysis_pattern(const tch_analysis* an, tcg_csr_view* out);
+void tch_analysis_times(const tch_analysis* an, double* ordering_s, double* symbolic_s);
+/* Fill pattern for an arbitrary permuted matrix (levelk_pattern_bfs). */
+tch_matrix* tch_levelk_pattern(const tch_matrix* a_permuted, int32_t level, int32_t threads);
+/* init_factor_values (factorize.hpp:71-89): out has pattern->nnz doubles. */
+tcg_status tch_init_values(const tcg_csr_view* a_permuted, const tcg_csr_view* pattern, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TACHO_B200_H_ */

@@ -1,0 +1,154 @@
+"""ctypes binding of the C ABI in include/tacho_b200.h.
+
+The shared library is built in-tree (``make lib`` / ``__graft_entry__.build()``)
+into ``paper_1601_05871_b200/lib/libtacho_b200.so``. There is no fallback:
+if the library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libtacho_b200.so")
+
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+u64p = C.POINTER(C.c_uint64)
+
+TCG_OK, TCG_BREAKDOWN, TCG_INVALID, TCG_CUDA, TCG_TIMEOUT = range(5)
+
+
+class CsrView(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32),
+        ("nnz", C.c_int64),
+        ("row_ptr", i64p),
+        ("col_idx", i32p),
+        ("values", f64p),
+    ]
+
+
+class Problem(C.Structure):
+    _fields_ = [
+        ("n", C.c_int32),
+        ("nnz", C.c_int64),
+        ("col_idx", i32p),
+        ("values", f64p),
+        ("ntasks", C.c_int64),
+        ("task_rec", i32p),
+        ("nitems", C.c_int64),
+        ("item_rec", i32p),
+        ("nsources", C.c_int64),
+        ("src_rec", i32p),
+        ("nedges", C.c_int64),
+        ("succ", i32p),
+        ("indeg", i32p),
+        ("nroots", C.c_int64),
+        ("roots", i32p),
+        ("max_target_len", C.c_int32),
+        ("max_flag_rows", C.c_int32),
+    ]
+
+
+class Options(C.Structure):
+    _fields_ = [
+        ("threads_per_cta", C.c_int32),
+        ("ctas_per_sm", C.c_int32),
+        ("staging_cap", C.c_int32),
+        ("timeout_s", C.c_double),
+        ("trace", C.c_int32),
+    ]
+
+
+class Stats(C.Structure):
+    _fields_ = [
+        ("device_ms", C.c_double),
+        ("tasks_completed", C.c_int64),
+        ("tasks_executed", C.c_int64),
+        ("breakdown_row", C.c_int32),
+        ("breakdown_pivot", C.c_double),
+        ("grid_ctas", C.c_int32),
+        ("threads_per_cta", C.c_int32),
+        ("staging_cap", C.c_int32),
+        ("smem_bytes", C.c_int64),
+        ("kernel_launches", C.c_int32),
+    ]
+
+
+class PlanStats(C.Structure):
+    _fields_ = [
+        ("tasks", C.c_int64 * 4),
+        ("edges", C.c_int64),
+        ("items", C.c_int64),
+        ("sources", C.c_int64),
+        ("pairs", C.c_int64),
+        ("empty_tasks", C.c_int64),
+        ("max_target_len", C.c_int32),
+        ("max_flag_rows", C.c_int32),
+        ("dag_depth", C.c_int32),
+        ("nblocks_rows", C.c_int32),
+        ("nblocks", C.c_int64),
+        ("block_build_seconds", C.c_double),
+        ("plan_seconds", C.c_double),
+    ]
+
+
+# (name, restype, argtypes) for every symbol declared in include/tacho_b200.h
+SIGNATURES = [
+    ("tcg_plan_build", C.c_int, [C.POINTER(CsrView), C.POINTER(CsrView), C.c_int32, i32p, C.POINTER(C.c_void_p)]),
+    ("tcg_plan_free", None, [C.c_void_p]),
+    ("tcg_plan_error", C.c_char_p, []),
+    ("tcg_plan_problem", C.c_int, [C.c_void_p, C.POINTER(Problem)]),
+    ("tcg_plan_get_stats", C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
+    ("tcg_plan_dag", C.c_int, [C.c_void_p, i64p, C.POINTER(i32p), C.POINTER(i32p), C.POINTER(i32p),
+                                i64p, C.POINTER(i32p), C.POINTER(i32p)]),
+    ("tcg_plan_blocks", C.c_int, [C.c_void_p, i32p, C.POINTER(i64p), i64p, C.POINTER(i32p)]),
+    ("tcg_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("tcg_destroy", None, [C.c_void_p]),
+    ("tcg_last_error", C.c_char_p, [C.c_void_p]),
+    ("tcg_set_options", C.c_int, [C.c_void_p, C.POINTER(Options)]),
+    ("tcg_upload", C.c_int, [C.c_void_p, C.POINTER(Problem)]),
+    ("tcg_set_values", C.c_int, [C.c_void_p, f64p]),
+    ("tcg_restore", C.c_int, [C.c_void_p]),
+    ("tcg_factor", C.c_int, [C.c_void_p, C.POINTER(Stats)]),
+    ("tcg_download", C.c_int, [C.c_void_p, f64p]),
+    ("tcg_download_trace", C.c_int, [C.c_void_p, u64p]),
+    ("tcg_device_values", C.c_int, [C.c_void_p, C.POINTER(f64p), i64p]),
+    ("tcg_arena_bytes", C.c_int64, [C.c_void_p]),
+    ("tch_generate", C.c_void_p, [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]),
+    ("tch_matrix_from_csr", C.c_void_p, [C.POINTER(CsrView)]),
+    ("tch_matrix_free", None, [C.c_void_p]),
+    ("tch_matrix_view", None, [C.c_void_p, C.POINTER(CsrView)]),
+    ("tch_analyze", C.c_void_p, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
+    ("tch_analysis_free", None, [C.c_void_p]),
+    ("tch_error", C.c_char_p, []),
+    ("tch_analysis_perm", None, [C.c_void_p, C.POINTER(i32p), C.POINTER(i32p)]),
+    ("tch_analysis_ranges", C.c_int32, [C.c_void_p, C.POINTER(i32p)]),
+    ("tch_analysis_permuted", None, [C.c_void_p, C.POINTER(CsrView)]),
+    ("tch_analysis_pattern", None, [C.c_void_p, C.POINTER(CsrView)]),
+    ("tch_analysis_times", None, [C.c_void_p, f64p, f64p]),
+    ("tch_levelk_pattern", C.c_void_p, [C.c_void_p, C.c_int32, C.c_int32]),
+    ("tch_init_values", C.c_int, [C.POINTER(CsrView), C.POINTER(CsrView), f64p]),
+]
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load the in-tree library (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: build it with `make lib` or __graft_entry__.build(); "
+            "there is no CPU fallback for the factorization path")
+    lib = C.CDLL(LIB_PATH)
+    for name, res, args in SIGNATURES:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

@@ -1,0 +1,474 @@
+"""Python mirror of the reference's factorization interface, over the C ABI.
+
+Names follow the reference (`taskchol`, /root/reference/proj/include):
+``CsrMatrix``, ``RangeList``, ``FillPattern``, ``FactorStats``,
+``FactorResult``, ``BreakdownError``, ``analyze``, ``export_task_dag`` and
+the drop-in ``factor_by_blocks_gpu`` (the GPU replacement of
+``factor_by_blocks(a_permuted, fp, ranges, policy)``, factorize.hpp:134-137).
+Every numeric call runs on the GPU through libtacho_b200.so; nothing here
+computes a factor on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _native as N
+
+KIND_NAMES = ("CHOL", "TRSM", "HERK", "GEMM")
+
+
+class BreakdownError(RuntimeError):
+    """Non-positive pivot (reference kernels.hpp:21-36)."""
+
+    def __init__(self, row: int, pivot: float, msg: str = ""):
+        super().__init__(msg or f"factorization breakdown at row {row}: pivot {pivot} is not positive")
+        self.row = row
+        self.pivot = pivot
+
+
+class SchedulerError(RuntimeError):
+    """Stalled task graph (reference scheduler.hpp:298-309); here the device watchdog."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA runtime failure inside the C ABI."""
+
+
+@dataclass
+class CsrMatrix:
+    nrows: int
+    ncols: int
+    row_ptr: np.ndarray  # int64, nrows + 1
+    col_idx: np.ndarray  # int32
+    values: np.ndarray   # float64
+
+    def nnz(self) -> int:
+        return int(self.col_idx.shape[0])
+
+    def view(self) -> N.CsrView:
+        v = N.CsrView()
+        v.n = self.nrows
+        v.nnz = self.nnz()
+        v.row_ptr = self.row_ptr.ctypes.data_as(N.i64p)
+        v.col_idx = self.col_idx.ctypes.data_as(N.i32p)
+        v.values = self.values.ctypes.data_as(N.f64p)
+        return v
+
+    @staticmethod
+    def from_arrays(n: int, row_ptr, col_idx, values=None) -> "CsrMatrix":
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        ci = np.ascontiguousarray(col_idx, dtype=np.int32)
+        va = (np.ones(ci.shape[0]) if values is None
+              else np.ascontiguousarray(values, dtype=np.float64))
+        return CsrMatrix(int(n), int(n), rp, ci, va)
+
+    def at(self, i: int, j: int) -> float:
+        b, e = int(self.row_ptr[i]), int(self.row_ptr[i + 1])
+        k = b + int(np.searchsorted(self.col_idx[b:e], j))
+        return float(self.values[k]) if k < e and self.col_idx[k] == j else 0.0
+
+    def has_entry(self, i: int, j: int) -> bool:
+        b, e = int(self.row_ptr[i]), int(self.row_ptr[i + 1])
+        k = b + int(np.searchsorted(self.col_idx[b:e], j))
+        return k < e and self.col_idx[k] == j
+
+
+@dataclass
+class RangeList:
+    bounds: np.ndarray  # int32, count + 1 ascending row bounds
+
+    @staticmethod
+    def from_ranges(ranges: List[Tuple[int, int]]) -> "RangeList":
+        if not ranges:
+            return RangeList(np.zeros(1, dtype=np.int32))
+        b = [ranges[0][0]] + [r[1] for r in ranges]
+        # keep malformed lists (gaps, inversions) visible to the validator
+        if any(ranges[k][0] != ranges[k - 1][1] for k in range(1, len(ranges))):
+            raise ValueError("ranges not contiguous")
+        return RangeList(np.asarray(b, dtype=np.int32))
+
+    def count(self) -> int:
+        return int(self.bounds.shape[0]) - 1
+
+    @property
+    def ranges(self) -> List[Tuple[int, int]]:
+        return [(int(self.bounds[k]), int(self.bounds[k + 1])) for k in range(self.count())]
+
+
+@dataclass
+class FillPattern:
+    pattern: CsrMatrix
+    level_cap: int = 0
+    nnz_triu_input: int = 0
+
+
+@dataclass
+class Analysis:
+    perm: np.ndarray
+    iperm: np.ndarray
+    ranges: RangeList
+    a_permuted: CsrMatrix
+    pattern: FillPattern
+    ordering_seconds: float = 0.0
+    symbolic_seconds: float = 0.0
+
+
+@dataclass
+class FactorStats:
+    """Reference FactorStats (factorize.hpp:37-54) plus device figures."""
+    ordering_seconds: float = 0.0
+    symbolic_seconds: float = 0.0
+    block_build_seconds: float = 0.0
+    numeric_seconds: float = 0.0
+    chol_tasks: int = 0
+    trsm_tasks: int = 0
+    herk_tasks: int = 0
+    gemm_tasks: int = 0
+    workers: int = 0
+    backend: str = "gpu"
+    nnz_u: int = 0
+    relative_overhead: Optional[float] = None
+    device_ms: float = 0.0
+    plan_seconds: float = 0.0
+    grid_ctas: int = 0
+    threads_per_cta: int = 0
+
+    def total_tasks(self) -> int:
+        return self.chol_tasks + self.trsm_tasks + self.herk_tasks + self.gemm_tasks
+
+
+@dataclass
+class FactorResult:
+    factor: CsrMatrix
+    stats: FactorStats
+
+
+@dataclass
+class TaskDag:
+    """Static DAG in generation order (reference factorize.hpp:240-302)."""
+    kind: np.ndarray
+    block_row: np.ndarray
+    block_col: np.ndarray
+    edge_from: np.ndarray
+    edge_to: np.ndarray
+
+    @property
+    def labels(self) -> List[str]:
+        return [f"{KIND_NAMES[k]}({i},{j})" for k, i, j in zip(self.kind, self.block_row, self.block_col)]
+
+    def to_dot(self) -> str:
+        out = ["digraph tasks {"]
+        out += [f'  t{i} [label="{lab}"];' for i, lab in enumerate(self.labels)]
+        out += [f"  t{a} -> t{b};" for a, b in zip(self.edge_from, self.edge_to)]
+        return "\n".join(out) + "\n}\n"
+
+
+def _lib():
+    return N.load()
+
+
+def _copy(ptr, n, dtype) -> np.ndarray:
+    if n == 0:
+        return np.zeros(0, dtype=dtype)
+    return np.ctypeslib.as_array(ptr, shape=(int(n),)).astype(dtype, copy=True)
+
+
+def _from_view(v: N.CsrView) -> CsrMatrix:
+    n = int(v.n)
+    return CsrMatrix(n, n, _copy(v.row_ptr, n + 1, np.int64), _copy(v.col_idx, v.nnz, np.int32),
+                     _copy(v.values, v.nnz, np.float64))
+
+
+# ------------------------------------------------------------------ inputs --
+
+def generate(kind: str, p0: int, p1: int = 0, seed: int = 0) -> CsrMatrix:
+    """Seeded synthetic matrices; see tacho_b200.h."""
+    lib = _lib()
+    h = lib.tch_generate(kind.encode(), int(p0), int(p1), int(seed))
+    if not h:
+        raise ValueError(lib.tch_error().decode())
+    try:
+        v = N.CsrView()
+        lib.tch_matrix_view(h, C.byref(v))
+        return _from_view(v)
+    finally:
+        lib.tch_matrix_free(h)
+
+
+CONFIGS = {
+    # name: (generator kind, p0, p1, seed, level)  — BASELINE.json configs
+    "c1": ("grid2d", 100, 100, 0, 0),
+    "c2": ("lap7", 64, 0, 0, 1),
+    "c3": ("stencil27", 48, 0, 1, 2),
+    "c4": ("elasticity", 40, 0, 1, 0),
+    "c5": ("diffusion", 32, 1000, 1, 1),   # batch member b uses seed b + 1
+    "c6": ("lap7", 128, 0, 0, 1),
+}
+
+
+def config_matrix(name: str, member: int = 0) -> Tuple[CsrMatrix, int]:
+    kind, p0, p1, seed, level = CONFIGS[name]
+    if name == "c5":
+        seed = member + 1
+    return generate(kind, p0, p1, seed), level
+
+
+def analyze(a: CsrMatrix, level: int = 0, treecut: int = 0, leaf_size: int = 64,
+            max_depth: int = 100, threads: int = 0) -> Analysis:
+    """ND ordering -> prune -> PᵀAP -> level-k pattern (reference pipeline.hpp:35-55)."""
+    lib = _lib()
+    m = lib.tch_matrix_from_csr(C.byref(a.view()))
+    if not m:
+        raise ValueError(lib.tch_error().decode())
+    try:
+        h = lib.tch_analyze(m, level, treecut, leaf_size, max_depth, threads)
+        if not h:
+            raise ValueError(lib.tch_error().decode())
+        try:
+            perm, iperm = N.i32p(), N.i32p()
+            lib.tch_analysis_perm(h, C.byref(perm), C.byref(iperm))
+            bounds = N.i32p()
+            cnt = lib.tch_analysis_ranges(h, C.byref(bounds))
+            ap, pat = N.CsrView(), N.CsrView()
+            lib.tch_analysis_permuted(h, C.byref(ap))
+            lib.tch_analysis_pattern(h, C.byref(pat))
+            t_ord, t_sym = C.c_double(), C.c_double()
+            lib.tch_analysis_times(h, C.byref(t_ord), C.byref(t_sym))
+            a_perm = _from_view(ap)
+            pattern = _from_view(pat)
+            nnz_triu = int(np.count_nonzero(
+                a_perm.col_idx >= np.repeat(np.arange(a_perm.nrows, dtype=np.int64),
+                                            np.diff(a_perm.row_ptr))))
+            return Analysis(perm=_copy(perm, a.nrows, np.int32), iperm=_copy(iperm, a.nrows, np.int32),
+                            ranges=RangeList(_copy(bounds, cnt + 1, np.int32)), a_permuted=a_perm,
+                            pattern=FillPattern(pattern, level, nnz_triu),
+                            ordering_seconds=t_ord.value, symbolic_seconds=t_sym.value)
+        finally:
+            lib.tch_analysis_free(h)
+    finally:
+        lib.tch_matrix_free(m)
+
+
+def levelk_pattern(a_permuted: CsrMatrix, level: int, threads: int = 0) -> FillPattern:
+    lib = _lib()
+    m = lib.tch_matrix_from_csr(C.byref(a_permuted.view()))
+    if not m:
+        raise ValueError(lib.tch_error().decode())
+    try:
+        h = lib.tch_levelk_pattern(m, level, threads)
+        if not h:
+            raise ValueError(lib.tch_error().decode())
+        try:
+            v = N.CsrView()
+            lib.tch_matrix_view(h, C.byref(v))
+            return FillPattern(_from_view(v), level)
+        finally:
+            lib.tch_matrix_free(h)
+    finally:
+        lib.tch_matrix_free(m)
+
+
+def init_factor_values(a_permuted: CsrMatrix, fp: FillPattern) -> np.ndarray:
+    lib = _lib()
+    out = np.zeros(fp.pattern.nnz(), dtype=np.float64)
+    st = lib.tch_init_values(C.byref(a_permuted.view()), C.byref(fp.pattern.view()),
+                             out.ctypes.data_as(N.f64p))
+    if st != N.TCG_OK:
+        raise ValueError(lib.tch_error().decode())
+    return out
+
+
+# -------------------------------------------------------------------- plan --
+
+class Plan:
+    """Host-flattened DAG + work tables (tcg_plan)."""
+
+    def __init__(self, a_permuted: CsrMatrix, fp: FillPattern, ranges: RangeList):
+        lib = _lib()
+        self._lib = lib
+        h = C.c_void_p()
+        b = np.ascontiguousarray(ranges.bounds, dtype=np.int32)
+        t0 = time.perf_counter()
+        st = lib.tcg_plan_build(C.byref(a_permuted.view()), C.byref(fp.pattern.view()),
+                                ranges.count(), b.ctypes.data_as(N.i32p), C.byref(h))
+        self.build_seconds = time.perf_counter() - t0
+        if st != N.TCG_OK:
+            msg = lib.tcg_plan_error().decode()
+            if "diagonal block missing" in msg:
+                raise RuntimeError(msg)  # reference: std::logic_error
+            raise ValueError(msg)
+        self.handle = h
+        self.n = a_permuted.nrows
+        self.pattern = fp.pattern
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self._lib.tcg_plan_free(h)
+            self.handle = None
+
+    def stats(self) -> N.PlanStats:
+        s = N.PlanStats()
+        self._lib.tcg_plan_get_stats(self.handle, C.byref(s))
+        return s
+
+    def problem(self) -> N.Problem:
+        p = N.Problem()
+        self._lib.tcg_plan_problem(self.handle, C.byref(p))
+        return p
+
+    def dag(self) -> TaskDag:
+        nn, ne = C.c_int64(), C.c_int64()
+        k, bi, bj, ef, et = N.i32p(), N.i32p(), N.i32p(), N.i32p(), N.i32p()
+        self._lib.tcg_plan_dag(self.handle, C.byref(nn), C.byref(k), C.byref(bi), C.byref(bj),
+                               C.byref(ne), C.byref(ef), C.byref(et))
+        return TaskDag(_copy(k, nn.value, np.int32), _copy(bi, nn.value, np.int32),
+                       _copy(bj, nn.value, np.int32), _copy(ef, ne.value, np.int32),
+                       _copy(et, ne.value, np.int32))
+
+    def blocks(self) -> Tuple[np.ndarray, np.ndarray]:
+        m, nb = C.c_int32(), C.c_int64()
+        bp, bc = N.i64p(), N.i32p()
+        self._lib.tcg_plan_blocks(self.handle, C.byref(m), C.byref(bp), C.byref(nb), C.byref(bc))
+        return _copy(bp, m.value + 1, np.int64), _copy(bc, nb.value, np.int32)
+
+    def tables(self) -> dict:
+        """Copies of the device tables (for host-side inspection in tests)."""
+        p = self.problem()
+        return {
+            "task": _copy(p.task_rec, 8 * p.ntasks, np.int32).reshape(-1, 8),
+            "item": _copy(p.item_rec, 8 * p.nitems, np.int32).reshape(-1, 8),
+            "src": _copy(p.src_rec, 4 * p.nsources, np.int32).reshape(-1, 4),
+            "succ": _copy(p.succ, p.nedges, np.int32),
+            "indeg": _copy(p.indeg, p.ntasks, np.int32),
+            "roots": _copy(p.roots, p.nroots, np.int32),
+            "values": _copy(p.values, p.nnz, np.float64),
+            "cols": _copy(p.col_idx, p.nnz, np.int32),
+        }
+
+
+def export_task_dag(fp: FillPattern, ranges: RangeList) -> TaskDag:
+    """Dry-run DAG (no execution), as export_task_dag (factorize.hpp:260-302)."""
+    a = CsrMatrix(fp.pattern.nrows, fp.pattern.ncols, fp.pattern.row_ptr, fp.pattern.col_idx,
+                  np.ones(fp.pattern.nnz()))
+    return Plan(a, fp, ranges).dag()
+
+
+# ------------------------------------------------------------------ device --
+
+@dataclass
+class GpuOptions:
+    device: int = 0
+    threads_per_cta: int = 0
+    ctas_per_sm: int = 0
+    staging_cap: int = 0
+    timeout_s: float = 0.0
+    trace: bool = False
+
+
+class GpuFactorizer:
+    """A device context holding one uploaded plan (tcg_ctx)."""
+
+    def __init__(self, plan: Plan, options: Optional[GpuOptions] = None):
+        self.opt = options or GpuOptions()
+        lib = _lib()
+        self._lib = lib
+        h = C.c_void_p()
+        st = lib.tcg_create(self.opt.device, C.byref(h))
+        if st != N.TCG_OK:
+            raise DeviceError(lib.tcg_last_error(None).decode())
+        self.ctx = h
+        o = N.Options(self.opt.threads_per_cta, self.opt.ctas_per_sm, self.opt.staging_cap,
+                      self.opt.timeout_s, 1 if self.opt.trace else 0)
+        self._check(lib.tcg_set_options(self.ctx, C.byref(o)))
+        self.plan = plan
+        self._problem = plan.problem()
+        self.nnz = int(self._problem.nnz)
+        self.ntasks = int(self._problem.ntasks)
+        self._check(lib.tcg_upload(self.ctx, C.byref(self._problem)))
+        self.last = N.Stats()
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self._lib.tcg_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, st):
+        if st == N.TCG_OK:
+            return
+        msg = self._lib.tcg_last_error(self.ctx).decode()
+        if st == N.TCG_BREAKDOWN:
+            raise BreakdownError(self.last.breakdown_row, self.last.breakdown_pivot, msg)
+        if st == N.TCG_TIMEOUT:
+            raise SchedulerError(msg)
+        if st == N.TCG_INVALID:
+            raise ValueError(msg)
+        raise DeviceError(msg)
+
+    def set_values(self, values: np.ndarray):
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        self._check(self._lib.tcg_set_values(self.ctx, v.ctypes.data_as(N.f64p)))
+
+    def set_values_ptr(self, host_ptr: int):
+        self._check(self._lib.tcg_set_values(self.ctx, C.cast(C.c_void_p(host_ptr), N.f64p)))
+
+    def restore(self):
+        self._check(self._lib.tcg_restore(self.ctx))
+
+    def factor(self) -> N.Stats:
+        self.last = N.Stats()
+        st = self._lib.tcg_factor(self.ctx, C.byref(self.last))
+        self._check(st)
+        return self.last
+
+    def download(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.nnz, dtype=np.float64)
+        self._check(self._lib.tcg_download(self.ctx, out.ctypes.data_as(N.f64p)))
+        return out
+
+    def download_ptr(self, host_ptr: int):
+        self._check(self._lib.tcg_download(self.ctx, C.cast(C.c_void_p(host_ptr), N.f64p)))
+
+    def trace(self) -> np.ndarray:
+        out = np.zeros(2 * self.ntasks, dtype=np.uint64)
+        self._check(self._lib.tcg_download_trace(self.ctx, out.ctypes.data_as(N.u64p)))
+        return out.reshape(-1, 2)
+
+    def arena_bytes(self) -> int:
+        return int(self._lib.tcg_arena_bytes(self.ctx))
+
+
+def factor_by_blocks_gpu(a_permuted: CsrMatrix, fp: FillPattern, ranges: RangeList,
+                         options: Optional[GpuOptions] = None) -> FactorResult:
+    """GPU drop-in for ``factor_by_blocks`` (reference factorize.hpp:134-235).
+
+    Same inputs and result semantics: a fresh factor on ``fp.pattern``'s
+    arrays; ``BreakdownError(row, pivot)`` on a non-positive pivot;
+    ``ValueError`` for invalid ranges / missing diagonals and
+    ``RuntimeError`` for a missing diagonal block (logic_error).
+    """
+    plan = Plan(a_permuted, fp, ranges)
+    ps = plan.stats()
+    fz = GpuFactorizer(plan, options)
+    try:
+        st = fz.factor()
+        vals = fz.download()
+    finally:
+        fz.close()
+    stats = FactorStats(
+        block_build_seconds=ps.block_build_seconds, numeric_seconds=st.device_ms / 1e3,
+        chol_tasks=ps.tasks[0], trsm_tasks=ps.tasks[1], herk_tasks=ps.tasks[2], gemm_tasks=ps.tasks[3],
+        workers=int(st.grid_ctas), backend="gpu", nnz_u=fp.pattern.nnz(), device_ms=st.device_ms,
+        plan_seconds=ps.plan_seconds, grid_ctas=int(st.grid_ctas), threads_per_cta=int(st.threads_per_cta))
+    factor = CsrMatrix(fp.pattern.nrows, fp.pattern.ncols, fp.pattern.row_ptr.copy(),
+                       fp.pattern.col_idx.copy(), vals)
+    return FactorResult(factor, stats)

@@ -1,0 +1,602 @@
+// C ABI (include/tacho_b200.h): host flattener, device context and the
+// analysis helpers. No exception crosses this file's extern "C" functions.
+#include "../../include/tacho_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+#include "device/device_api.hpp"
+#include "host/plan.hpp"
+#include "host/sparse.hpp"
+
+namespace {
+
+thread_local std::string g_plan_error;
+thread_local std::string g_tch_error;
+
+tcb::CsrMatrix csr_from_view(const tcg_csr_view* v, bool need_values) {
+  if (!v || v->n < 0 || v->nnz < 0 || (!v->row_ptr && v->n > 0))
+    throw std::invalid_argument("csr view: null or negative sizes");
+  tcb::CsrMatrix m;
+  m.nrows = m.ncols = v->n;
+  m.row_ptr.assign(v->row_ptr, v->row_ptr + v->n + 1);
+  if (v->nnz > 0) {
+    if (!v->col_idx) throw std::invalid_argument("csr view: null col_idx");
+    m.col_idx.assign(v->col_idx, v->col_idx + v->nnz);
+  }
+  if (v->values && v->nnz > 0)
+    m.values.assign(v->values, v->values + v->nnz);
+  else if (need_values)
+    throw std::invalid_argument("csr view: values required");
+  else
+    m.values.assign(static_cast<std::size_t>(v->nnz), 1.0);
+  if (v->n == 0 && m.row_ptr.empty()) m.row_ptr.assign(1, 0);
+  tcb::validate_csr(m);
+  return m;
+}
+
+void view_of(const tcb::CsrMatrix& m, tcg_csr_view* out) {
+  out->n = m.nrows;
+  out->nnz = m.nnz();
+  out->row_ptr = m.row_ptr.data();
+  out->col_idx = m.col_idx.data();
+  out->values = m.values.data();
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct tcg_plan {
+  tcb::Plan plan;
+  std::vector<std::int32_t> brow_ptr32;  // unused, kept for ABI symmetry
+};
+
+struct tcg_ctx {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void* arena = nullptr;
+  size_t arena_bytes = 0;
+  tcbdev::Ctrl* host_ctrl = nullptr;
+  // arena carve-out
+  int* cols = nullptr;
+  double* vals = nullptr;
+  double* vals0 = nullptr;
+  int4* tasks = nullptr;
+  int4* items = nullptr;
+  int4* srcs = nullptr;
+  int* succ = nullptr;
+  int* indeg = nullptr;
+  int* indeg0 = nullptr;
+  int* queue = nullptr;
+  int* roots = nullptr;
+  tcbdev::Ctrl* ctrl = nullptr;
+  unsigned long long* trace = nullptr;
+  // problem shape
+  std::int64_t n = 0, nnz = 0, ntasks = 0, nitems = 0, nsrc = 0, nedges = 0, nroots = 0;
+  int max_target_len = 0, max_flag_rows = 0;
+  bool uploaded = false;
+  tcg_options opt{};
+  std::string err;
+};
+
+#define TCG_CUDA_TRY(ctx, call)                                              \
+  do {                                                                       \
+    cudaError_t e__ = (call);                                                \
+    if (e__ != cudaSuccess) {                                                \
+      (ctx)->err = std::string(#call) + ": " + cudaGetErrorString(e__);      \
+      return TCG_CUDA;                                                       \
+    }                                                                        \
+  } while (0)
+
+extern "C" {
+
+// ---------------------------------------------------------------- plan ----
+
+tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pattern,
+                          int32_t nranges, const int32_t* range_bounds, tcg_plan** out) {
+  if (!out) return TCG_INVALID;
+  *out = nullptr;
+  try {
+    const tcb::CsrMatrix a = csr_from_view(a_permuted, true);
+    const tcb::CsrMatrix u = csr_from_view(pattern, false);
+    if (a.nrows != u.nrows) throw std::invalid_argument("a_permuted and pattern sizes differ");
+    if (nranges < 0 || (nranges > 0 && !range_bounds))
+      throw std::invalid_argument("range list: null bounds");
+    tcb::RangeList rl;
+    for (int32_t r = 0; r < nranges; ++r) rl.ranges.push_back({range_bounds[r], range_bounds[r + 1]});
+    const std::vector<double> init = tcb::init_factor_values(a, u);
+    auto p = std::make_unique<tcg_plan>();
+    p->plan = tcb::build_plan(u, init, rl, true);
+    *out = p.release();
+    return TCG_OK;
+  } catch (const std::bad_alloc&) {
+    g_plan_error = "out of host memory";
+    return TCG_INVALID;
+  } catch (const std::exception& e) {
+    g_plan_error = e.what();
+    return TCG_INVALID;
+  }
+}
+
+void tcg_plan_free(tcg_plan* plan) { delete plan; }
+const char* tcg_plan_error(void) { return g_plan_error.c_str(); }
+
+tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
+  if (!plan || !o) return TCG_INVALID;
+  const tcb::Plan& P = plan->plan;
+  o->n = P.n;
+  o->nnz = P.nnz;
+  o->col_idx = P.cols.data();
+  o->values = P.values.data();
+  o->ntasks = static_cast<int64_t>(P.node_kind.size());
+  o->task_rec = P.task_rec.data();
+  o->nitems = static_cast<int64_t>(P.item_rec.size() / tcb::kItemWords);
+  o->item_rec = P.item_rec.data();
+  o->nsources = static_cast<int64_t>(P.src_rec.size() / tcb::kSrcWords);
+  o->src_rec = P.src_rec.data();
+  o->nedges = static_cast<int64_t>(P.succ.size());
+  o->succ = P.succ.data();
+  o->indeg = P.indeg.data();
+  o->nroots = static_cast<int64_t>(P.roots.size());
+  o->roots = P.roots.data();
+  o->max_target_len = P.stats.max_target_len;
+  o->max_flag_rows = P.stats.max_flag_rows;
+  return TCG_OK;
+}
+
+tcg_status tcg_plan_get_stats(const tcg_plan* plan, tcg_plan_stats* o) {
+  if (!plan || !o) return TCG_INVALID;
+  const tcb::PlanStats& s = plan->plan.stats;
+  for (int k = 0; k < 4; ++k) o->tasks[k] = s.tasks[k];
+  o->edges = s.edges;
+  o->items = s.items;
+  o->sources = s.sources;
+  o->pairs = s.pairs;
+  o->empty_tasks = s.empty_tasks;
+  o->max_target_len = s.max_target_len;
+  o->max_flag_rows = s.max_flag_rows;
+  o->dag_depth = s.dag_depth;
+  o->nblocks_rows = plan->plan.blocks.m;
+  o->nblocks = plan->plan.blocks.nblocks();
+  o->block_build_seconds = s.block_build_seconds;
+  o->plan_seconds = s.plan_seconds;
+  return TCG_OK;
+}
+
+tcg_status tcg_plan_dag(const tcg_plan* plan, int64_t* nnodes, const int32_t** kind,
+                        const int32_t** block_row, const int32_t** block_col, int64_t* nedges,
+                        const int32_t** edge_from, const int32_t** edge_to) {
+  if (!plan) return TCG_INVALID;
+  const tcb::Plan& P = plan->plan;
+  if (nnodes) *nnodes = static_cast<int64_t>(P.node_kind.size());
+  if (kind) *kind = P.node_kind.data();
+  if (block_row) *block_row = P.node_i.data();
+  if (block_col) *block_col = P.node_j.data();
+  if (nedges) *nedges = static_cast<int64_t>(P.edge_from.size());
+  if (edge_from) *edge_from = P.edge_from.data();
+  if (edge_to) *edge_to = P.edge_to.data();
+  return TCG_OK;
+}
+
+tcg_status tcg_plan_blocks(const tcg_plan* plan, int32_t* m, const int64_t** brow_ptr,
+                           int64_t* nblocks, const int32_t** bcol_idx) {
+  if (!plan) return TCG_INVALID;
+  const tcb::BlockLayout& B = plan->plan.blocks;
+  if (m) *m = B.m;
+  if (brow_ptr) *brow_ptr = B.brow_ptr.data();
+  if (nblocks) *nblocks = B.nblocks();
+  if (bcol_idx) *bcol_idx = B.bcol_idx.data();
+  return TCG_OK;
+}
+
+// -------------------------------------------------------------- device ----
+
+tcg_status tcg_create(int device, tcg_ctx** out) {
+  if (!out) return TCG_INVALID;
+  *out = nullptr;
+  auto c = std::make_unique<tcg_ctx>();
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c->host_ctrl), sizeof(tcbdev::Ctrl));
+  if (e != cudaSuccess) {
+    g_plan_error = std::string("tcg_create: ") + cudaGetErrorString(e);
+    tcg_destroy(c.release());
+    return TCG_CUDA;
+  }
+  *out = c.release();
+  return TCG_OK;
+}
+
+void tcg_destroy(tcg_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->arena) cudaFree(c->arena);
+  if (c->host_ctrl) cudaFreeHost(c->host_ctrl);
+  if (c->ev0) cudaEventDestroy(c->ev0);
+  if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* tcg_last_error(const tcg_ctx* c) {
+  if (!c) return g_plan_error.c_str();
+  return c->err.c_str();
+}
+
+tcg_status tcg_set_options(tcg_ctx* c, const tcg_options* opt) {
+  if (!c || !opt) return TCG_INVALID;
+  if (opt->threads_per_cta != 0 && opt->threads_per_cta != 128 && opt->threads_per_cta != 256 &&
+      opt->threads_per_cta != 512) {
+    c->err = "threads_per_cta must be 128, 256 or 512";
+    return TCG_INVALID;
+  }
+  c->opt = *opt;
+  return TCG_OK;
+}
+
+tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
+  if (!c || !p) return TCG_INVALID;
+  if (p->n < 0 || p->nnz < 0 || p->ntasks < 0 || p->nitems < 0 || p->nsources < 0 ||
+      p->nedges < 0 || p->nroots < 0 || p->nnz > 0x7fffffffLL || p->ntasks > 0x7fffffffLL) {
+    c->err = "tcg_upload: invalid problem sizes";
+    return TCG_INVALID;
+  }
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->arena) {
+    TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    TCG_CUDA_TRY(c, cudaFree(c->arena));
+    c->arena = nullptr;
+    c->uploaded = false;
+  }
+  // one arena: [cols][vals][vals0][tasks][items][srcs][succ][indeg][indeg0][queue][roots][ctrl][trace]
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = off;
+    off = align_up(off + std::max<size_t>(bytes, 1), 256);
+    return at;
+  };
+  const size_t o_cols = take(sizeof(int) * p->nnz);
+  const size_t o_vals = take(sizeof(double) * p->nnz);
+  const size_t o_vals0 = take(sizeof(double) * p->nnz);
+  const size_t o_tasks = take(sizeof(int) * 8 * p->ntasks);
+  const size_t o_items = take(sizeof(int) * 8 * p->nitems);
+  const size_t o_srcs = take(sizeof(int) * 4 * p->nsources);
+  const size_t o_succ = take(sizeof(int) * p->nedges);
+  const size_t o_indeg = take(sizeof(int) * p->ntasks);
+  const size_t o_indeg0 = take(sizeof(int) * p->ntasks);
+  const size_t o_queue = take(sizeof(int) * p->ntasks);
+  const size_t o_roots = take(sizeof(int) * p->nroots);
+  const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
+  const size_t o_trace = take(sizeof(unsigned long long) * 2 * p->ntasks);
+  TCG_CUDA_TRY(c, cudaMalloc(&c->arena, off));
+  c->arena_bytes = off;
+  char* base = static_cast<char*>(c->arena);
+  c->cols = reinterpret_cast<int*>(base + o_cols);
+  c->vals = reinterpret_cast<double*>(base + o_vals);
+  c->vals0 = reinterpret_cast<double*>(base + o_vals0);
+  c->tasks = reinterpret_cast<int4*>(base + o_tasks);
+  c->items = reinterpret_cast<int4*>(base + o_items);
+  c->srcs = reinterpret_cast<int4*>(base + o_srcs);
+  c->succ = reinterpret_cast<int*>(base + o_succ);
+  c->indeg = reinterpret_cast<int*>(base + o_indeg);
+  c->indeg0 = reinterpret_cast<int*>(base + o_indeg0);
+  c->queue = reinterpret_cast<int*>(base + o_queue);
+  c->roots = reinterpret_cast<int*>(base + o_roots);
+  c->ctrl = reinterpret_cast<tcbdev::Ctrl*>(base + o_ctrl);
+  c->trace = reinterpret_cast<unsigned long long*>(base + o_trace);
+  auto put = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+    if (bytes == 0) return cudaSuccess;
+    return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
+  };
+  TCG_CUDA_TRY(c, put(c->cols, p->col_idx, sizeof(int) * p->nnz));
+  TCG_CUDA_TRY(c, put(c->vals0, p->values, sizeof(double) * p->nnz));
+  TCG_CUDA_TRY(c, put(c->tasks, p->task_rec, sizeof(int) * 8 * p->ntasks));
+  TCG_CUDA_TRY(c, put(c->items, p->item_rec, sizeof(int) * 8 * p->nitems));
+  TCG_CUDA_TRY(c, put(c->srcs, p->src_rec, sizeof(int) * 4 * p->nsources));
+  TCG_CUDA_TRY(c, put(c->succ, p->succ, sizeof(int) * p->nedges));
+  TCG_CUDA_TRY(c, put(c->indeg0, p->indeg, sizeof(int) * p->ntasks));
+  TCG_CUDA_TRY(c, put(c->roots, p->roots, sizeof(int) * p->nroots));
+  if (p->nnz > 0)
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals, c->vals0, sizeof(double) * p->nnz,
+                                    cudaMemcpyDeviceToDevice, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->n = p->n;
+  c->nnz = p->nnz;
+  c->ntasks = p->ntasks;
+  c->nitems = p->nitems;
+  c->nsrc = p->nsources;
+  c->nedges = p->nedges;
+  c->nroots = p->nroots;
+  c->max_target_len = p->max_target_len;
+  c->max_flag_rows = p->max_flag_rows;
+  c->uploaded = true;
+  return TCG_OK;
+}
+
+tcg_status tcg_set_values(tcg_ctx* c, const double* values) {
+  if (!c || !c->uploaded || (!values && c->nnz > 0)) return TCG_INVALID;
+  if (c->nnz == 0) return TCG_OK;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals0, values, sizeof(double) * c->nnz,
+                                  cudaMemcpyHostToDevice, c->stream));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals, c->vals0, sizeof(double) * c->nnz,
+                                  cudaMemcpyDeviceToDevice, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_restore(tcg_ctx* c) {
+  if (!c || !c->uploaded) return TCG_INVALID;
+  if (c->nnz == 0) return TCG_OK;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals, c->vals0, sizeof(double) * c->nnz,
+                                  cudaMemcpyDeviceToDevice, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
+  if (!c || !c->uploaded) return TCG_INVALID;
+  tcg_stats local{};
+  tcg_stats& S = st ? *st : local;
+  S = tcg_stats{};
+  S.breakdown_row = -1;
+  if (c->ntasks == 0) return TCG_OK;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+
+  const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
+  int flag_words = (c->max_flag_rows + 31) / 32;
+  flag_words += flag_words & 1;
+  int cap = c->opt.staging_cap;
+  if (cap <= 0) cap = std::min(256, std::max(32, (c->max_target_len + 31) / 32 * 32));
+  cap = (cap + 1) & ~1;
+  size_t smem = tcbdev::factor_smem_bytes(threads, cap, flag_words);
+  const size_t kMaxSmem = 227 * 1024;
+  while (smem > kMaxSmem && cap > 32) {
+    cap = std::max(32, cap / 2);
+    smem = tcbdev::factor_smem_bytes(threads, cap, flag_words);
+  }
+  if (smem > kMaxSmem) {
+    c->err = "diagonal range too large for the shared-memory row flags (" +
+             std::to_string(c->max_flag_rows) + " rows)";
+    return TCG_INVALID;
+  }
+  int occ = 0;
+  TCG_CUDA_TRY(c, tcbdev::factor_occupancy(threads, smem, &occ));
+  if (occ < 1) {
+    c->err = "persistent kernel does not fit on an SM";
+    return TCG_INVALID;
+  }
+  if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
+  const int grid = std::max(1, occ * c->sm_count);
+
+  tcbdev::PrepParams q{};
+  q.indeg0 = c->indeg0;
+  q.roots = c->roots;
+  q.indeg = c->indeg;
+  q.queue = c->queue;
+  q.ctrl = c->ctrl;
+  q.ntasks = static_cast<int>(c->ntasks);
+  q.nroots = static_cast<int>(c->nroots);
+  TCG_CUDA_TRY(c, tcbdev::launch_prepare(q, c->stream));
+
+  tcbdev::Params P{};
+  P.tasks = c->tasks;
+  P.items = c->items;
+  P.srcs = c->srcs;
+  P.succ = c->succ;
+  P.cols = c->cols;
+  P.vals = c->vals;
+  P.indeg = c->indeg;
+  P.queue = c->queue;
+  P.ctrl = c->ctrl;
+  P.trace = c->opt.trace ? c->trace : nullptr;
+  P.ntasks = static_cast<int>(c->ntasks);
+  P.cap = cap;
+  P.flag_words = flag_words;
+  const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
+  P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  TCG_CUDA_TRY(c, tcbdev::launch_factor(P, grid, threads, smem, c->stream));
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
+                                  cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  const tcbdev::Ctrl& h = *c->host_ctrl;
+  S.device_ms = ms;
+  S.tasks_completed = h.done;
+  S.tasks_executed = h.executed;
+  S.grid_ctas = grid;
+  S.threads_per_cta = threads;
+  S.staging_cap = cap;
+  S.smem_bytes = static_cast<int64_t>(smem);
+  S.kernel_launches = 2;
+  if (h.error) {
+    c->err = h.error == 1 ? "device watchdog expired: the task DAG stalled" : "device capacity error";
+    return TCG_TIMEOUT;
+  }
+  if (h.done != c->ntasks) {
+    c->err = "scheduler finished with " + std::to_string(h.done) + " of " +
+             std::to_string(c->ntasks) + " tasks";
+    return TCG_TIMEOUT;
+  }
+  if (h.failed) {
+    S.breakdown_row = h.fail_row;
+    S.breakdown_pivot = h.fail_pivot;
+    c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
+             std::to_string(h.fail_pivot) + " is not positive";
+    return TCG_BREAKDOWN;
+  }
+  return TCG_OK;
+}
+
+tcg_status tcg_download(tcg_ctx* c, double* values) {
+  if (!c || !c->uploaded || (!values && c->nnz > 0)) return TCG_INVALID;
+  if (c->nnz == 0) return TCG_OK;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(values, c->vals, sizeof(double) * c->nnz,
+                                  cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_download_trace(tcg_ctx* c, uint64_t* stamps) {
+  if (!c || !c->uploaded || !stamps) return TCG_INVALID;
+  if (c->ntasks == 0) return TCG_OK;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(stamps, c->trace, sizeof(uint64_t) * 2 * c->ntasks,
+                                  cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_device_values(tcg_ctx* c, double** dptr, int64_t* nnz) {
+  if (!c || !c->uploaded) return TCG_INVALID;
+  if (dptr) *dptr = c->vals;
+  if (nnz) *nnz = c->nnz;
+  return TCG_OK;
+}
+
+int64_t tcg_arena_bytes(const tcg_ctx* c) { return c ? static_cast<int64_t>(c->arena_bytes) : 0; }
+
+// ------------------------------------------------------------ analysis ----
+
+struct tch_matrix {
+  tcb::CsrMatrix m;
+};
+struct tch_analysis {
+  tcb::Analysis an;
+  std::vector<int32_t> bounds;
+};
+
+tch_matrix* tch_generate(const char* kind, int64_t p0, int64_t p1, uint64_t seed) {
+  try {
+    if (!kind) throw std::invalid_argument("null kind");
+    const std::string k(kind);
+    auto out = std::make_unique<tch_matrix>();
+    const auto i0 = static_cast<tcb::index_t>(p0);
+    if (p0 < 0 || p0 > (1LL << 24)) throw std::invalid_argument("size out of range");
+    if (k == "grid2d") out->m = tcb::grid_laplacian_2d(i0, static_cast<tcb::index_t>(p1));
+    else if (k == "lap7") out->m = tcb::laplacian_7pt(i0);
+    else if (k == "stencil27") out->m = tcb::stencil27_variable(i0, seed);
+    else if (k == "elasticity") out->m = tcb::elasticity27(i0, seed);
+    else if (k == "diffusion") out->m = tcb::diffusion_7pt_lognormal(i0, seed, static_cast<double>(p1) / 1000.0);
+    else if (k == "path") out->m = tcb::path_matrix(i0, 2.0);
+    else if (k == "random_spd")
+      out->m = tcb::random_spd(i0, static_cast<double>(p1) / 1e6, static_cast<std::uint32_t>(seed));
+    else throw std::invalid_argument("unknown generator '" + k + "'");
+    return out.release();
+  } catch (const std::exception& e) {
+    g_tch_error = e.what();
+    return nullptr;
+  }
+}
+
+tch_matrix* tch_matrix_from_csr(const tcg_csr_view* view) {
+  try {
+    auto out = std::make_unique<tch_matrix>();
+    out->m = csr_from_view(view, true);
+    return out.release();
+  } catch (const std::exception& e) {
+    g_tch_error = e.what();
+    return nullptr;
+  }
+}
+
+void tch_matrix_free(tch_matrix* m) { delete m; }
+void tch_matrix_view(const tch_matrix* m, tcg_csr_view* out) {
+  if (m && out) view_of(m->m, out);
+}
+
+tch_analysis* tch_analyze(const tch_matrix* a, int32_t level, int32_t treecut, int32_t leaf_size,
+                          int32_t max_depth, int32_t threads) {
+  try {
+    if (!a) throw std::invalid_argument("null matrix");
+    tcb::AnalyzeOptions opt;
+    opt.level = level;
+    opt.treecut = treecut;
+    opt.leaf_size = leaf_size;
+    opt.max_depth = max_depth;
+    auto out = std::make_unique<tch_analysis>();
+    out->an = tcb::analyze(a->m, opt, threads);
+    out->bounds.clear();
+    for (const tcb::Range& r : out->an.ranges.ranges) {
+      if (out->bounds.empty()) out->bounds.push_back(r.begin);
+      out->bounds.push_back(r.end);
+    }
+    if (out->bounds.empty()) out->bounds.push_back(0);
+    return out.release();
+  } catch (const std::exception& e) {
+    g_tch_error = e.what();
+    return nullptr;
+  }
+}
+
+void tch_analysis_free(tch_analysis* an) { delete an; }
+const char* tch_error(void) { return g_tch_error.c_str(); }
+
+void tch_analysis_perm(const tch_analysis* an, const int32_t** perm, const int32_t** iperm) {
+  if (!an) return;
+  if (perm) *perm = an->an.perm.perm.data();
+  if (iperm) *iperm = an->an.perm.iperm.data();
+}
+
+int32_t tch_analysis_ranges(const tch_analysis* an, const int32_t** bounds) {
+  if (!an) return -1;
+  if (bounds) *bounds = an->bounds.data();
+  return an->an.ranges.count();
+}
+
+void tch_analysis_permuted(const tch_analysis* an, tcg_csr_view* out) {
+  if (an && out) view_of(an->an.a_permuted, out);
+}
+void tch_analysis_pattern(const tch_analysis* an, tcg_csr_view* out) {
+  if (an && out) view_of(an->an.pattern.pattern, out);
+}
+void tch_analysis_times(const tch_analysis* an, double* ordering_s, double* symbolic_s) {
+  if (!an) return;
+  if (ordering_s) *ordering_s = an->an.ordering_seconds;
+  if (symbolic_s) *symbolic_s = an->an.symbolic_seconds;
+}
+
+tch_matrix* tch_levelk_pattern(const tch_matrix* a, int32_t level, int32_t threads) {
+  try {
+    if (!a) throw std::invalid_argument("null matrix");
+    auto out = std::make_unique<tch_matrix>();
+    out->m = tcb::levelk_pattern(a->m, level, threads).pattern;
+    return out.release();
+  } catch (const std::exception& e) {
+    g_tch_error = e.what();
+    return nullptr;
+  }
+}
+
+tcg_status tch_init_values(const tcg_csr_view* a_permuted, const tcg_csr_view* pattern, double* out) {
+  try {
+    const tcb::CsrMatrix a = csr_from_view(a_permuted, true);
+    const tcb::CsrMatrix u = csr_from_view(pattern, false);
+    const std::vector<double> v = tcb::init_factor_values(a, u);
+    std::copy(v.begin(), v.end(), out);
+    return TCG_OK;
+  } catch (const std::exception& e) {
+    g_tch_error = e.what();
+    return TCG_INVALID;
+  }
+}
+
+}  // extern "C"

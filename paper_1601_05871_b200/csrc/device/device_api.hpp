@@ -1,0 +1,17 @@
+// Host-callable launch helpers of factor_kernel.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+
+#include "factor_kernel.cuh"
+
+namespace tcbdev {
+
+size_t factor_smem_bytes(int threads, int cap, int flag_words);
+cudaError_t factor_occupancy(int threads, size_t smem, int* ctas_per_sm);
+cudaError_t launch_prepare(const PrepParams& q, cudaStream_t st);
+cudaError_t launch_factor(const Params& p, int grid, int threads, size_t smem, cudaStream_t st);
+
+}  // namespace tcbdev
