@@ -21,7 +21,7 @@ CXXFLAGS := -O2 -std=c++17 -fPIC -pthread -Wall -Wextra -ffp-contract=off
 HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generators.cpp \
              $(SRC)/host/plan.cpp $(SRC)/capi.cpp
 HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
-DEV_OBJS := $(OBJ)/device/factor_kernel.o
+DEV_OBJS := $(OBJ)/device/factor_kernel.o $(OBJ)/device/row_kernel.o
 
 .PHONY: all lib oracle ref clean
 all: lib oracle
@@ -32,7 +32,7 @@ $(OBJ)/%.o: $(SRC)/%.cpp $(wildcard $(SRC)/host/*.hpp) include/tacho_b200.h
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -I/usr/local/cuda/include -c $< -o $@
 
-$(OBJ)/device/factor_kernel.o: $(SRC)/device/factor_kernel.cu $(SRC)/device/factor_kernel.cuh
+$(OBJ)/device/factor_kernel.o: $(SRC)/device/factor_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_factor_kernel.txt || (cat build/ptxas_factor_kernel.txt; false)
 
@@ -49,3 +49,7 @@ ref:
 clean:
 	rm -rf build $(OUT)/*.so
 	$(MAKE) -C oracle clean
+
+$(OBJ)/device/row_kernel.o: $(SRC)/device/row_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_row_kernel.txt || (cat build/ptxas_row_kernel.txt; false)

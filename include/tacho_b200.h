@@ -66,18 +66,31 @@ typedef struct {
   const int32_t* col_idx;      /* U columns */
   const double* values;        /* initialised U values (init_factor_values) */
   int64_t ntasks;
-  const int32_t* task_rec;     /* 8 words per task */
+  const int32_t* task_rec;     /* 12 words per task */
   int64_t nitems;
   const int32_t* item_rec;     /* 8 words per item */
   int64_t nsources;
   const int32_t* src_rec;      /* 4 words per source */
   int64_t nedges;
   const int32_t* succ;         /* successor lists, grouped per task */
+  const int32_t* succ_rec;     /* per edge 16 words: successor, 0, 0, 0, its task record */
   const int32_t* indeg;        /* dependence counters per task */
   int64_t nroots;
   const int32_t* roots;        /* tasks with no predecessor, ascending */
   int32_t max_target_len;
   int32_t max_flag_rows;
+  int64_t nhelpers;            /* extra ready-queue entries of multi-CTA tasks */
+  int64_t nslots;              /* update programs (optional; 0 when absent): */
+  const int32_t* slot_rec;     /*   per target slot {u_b, u_e, m0, o0}; item word 6 = first slot */
+  int64_t nupdates;
+  const int32_t* upd;          /*   (m, o) pairs: U[tb+k] -= U[m] * U[o] */
+  /* row-level execution (optional; requires the update programs): */
+  const int32_t* row_rec;      /*   8 words per item: tb, te, dpos, slot_off, kind, t, succ_b, succ_e */
+  int64_t nrow_edges;
+  const int32_t* row_succ;     /*   successor items, grouped per item */
+  const int32_t* row_indeg;    /*   dependence counters per item */
+  int64_t nrow_roots;
+  const int32_t* row_roots;
 } tcg_problem;
 
 typedef struct {
@@ -86,6 +99,9 @@ typedef struct {
   int32_t staging_cap;      /* target-row entries staged per warp; 0 = auto */
   double timeout_s;         /* device watchdog; 0 = default (30 s) */
   int32_t trace;            /* 1 = record per-task start/end globaltimer stamps */
+  int32_t mode;             /* 0 = auto (3 when available), task-level DAG execution with
+                               1 = device merge of sorted indices or 2 = precomputed update
+                               programs; 3 = row-level execution of the same DAG */
 } tcg_options;
 
 typedef struct {
@@ -99,12 +115,19 @@ typedef struct {
   int32_t staging_cap;
   int64_t smem_bytes;
   int32_t kernel_launches;   /* device launches issued by the call */
+  int64_t helpers_run;       /* helper tickets that joined a multi-CTA task */
+  int32_t mode;              /* execution mode used (1 merge, 2 programs) */
 } tcg_stats;
 
 typedef struct {
   int64_t tasks[4];          /* chol, trsm, herk, gemm */
   int64_t edges, items, sources, pairs, empty_tasks;
   int32_t max_target_len, max_flag_rows, dag_depth;
+  int32_t max_width;         /* most CTAs cooperating on one task */
+  int64_t helpers;           /* helper tickets over all multi-CTA tasks */
+  int64_t updates;           /* products in the update programs (0 if not built) */
+  int64_t item_edges;        /* row-level dependences */
+  int32_t item_depth;        /* longest row-level chain, in items */
   int32_t nblocks_rows;      /* block rows m (= number of ranges) */
   int64_t nblocks;
   double block_build_seconds, plan_seconds;
@@ -143,7 +166,8 @@ tcg_status tcg_restore(tcg_ctx* ctx);
 /* Factor the working values in place. TCG_BREAKDOWN sets stats->breakdown_*. */
 tcg_status tcg_factor(tcg_ctx* ctx, tcg_stats* stats);
 tcg_status tcg_download(tcg_ctx* ctx, double* values);
-/* Per-task {start, end} globaltimer stamps of the last traced factor (2*ntasks). */
+/* Stamps of the last traced factor: per task {start, end} (2*ntasks words), then per
+ * item {claimed, sources ready, merged, published} (4*nitems words); globaltimer ns. */
 tcg_status tcg_download_trace(tcg_ctx* ctx, uint64_t* stamps);
 /* Device pointer to the working values and their count (for in-process users
  * that keep U resident, e.g. a preconditioner apply on the same stream). */

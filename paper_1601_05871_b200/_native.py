@@ -44,11 +44,23 @@ class Problem(C.Structure):
         ("src_rec", i32p),
         ("nedges", C.c_int64),
         ("succ", i32p),
+        ("succ_rec", i32p),
         ("indeg", i32p),
         ("nroots", C.c_int64),
         ("roots", i32p),
         ("max_target_len", C.c_int32),
         ("max_flag_rows", C.c_int32),
+        ("nhelpers", C.c_int64),
+        ("nslots", C.c_int64),
+        ("slot_rec", i32p),
+        ("nupdates", C.c_int64),
+        ("upd", i32p),
+        ("row_rec", i32p),
+        ("nrow_edges", C.c_int64),
+        ("row_succ", i32p),
+        ("row_indeg", i32p),
+        ("nrow_roots", C.c_int64),
+        ("row_roots", i32p),
     ]
 
 
@@ -59,6 +71,7 @@ class Options(C.Structure):
         ("staging_cap", C.c_int32),
         ("timeout_s", C.c_double),
         ("trace", C.c_int32),
+        ("mode", C.c_int32),
     ]
 
 
@@ -74,6 +87,8 @@ class Stats(C.Structure):
         ("staging_cap", C.c_int32),
         ("smem_bytes", C.c_int64),
         ("kernel_launches", C.c_int32),
+        ("helpers_run", C.c_int64),
+        ("mode", C.c_int32),
     ]
 
 
@@ -88,6 +103,11 @@ class PlanStats(C.Structure):
         ("max_target_len", C.c_int32),
         ("max_flag_rows", C.c_int32),
         ("dag_depth", C.c_int32),
+        ("max_width", C.c_int32),
+        ("helpers", C.c_int64),
+        ("updates", C.c_int64),
+        ("item_edges", C.c_int64),
+        ("item_depth", C.c_int32),
         ("nblocks_rows", C.c_int32),
         ("nblocks", C.c_int64),
         ("block_build_seconds", C.c_double),

@@ -341,7 +341,7 @@ class Plan:
         """Copies of the device tables (for host-side inspection in tests)."""
         p = self.problem()
         return {
-            "task": _copy(p.task_rec, 8 * p.ntasks, np.int32).reshape(-1, 8),
+            "task": _copy(p.task_rec, 12 * p.ntasks, np.int32).reshape(-1, 12),
             "item": _copy(p.item_rec, 8 * p.nitems, np.int32).reshape(-1, 8),
             "src": _copy(p.src_rec, 4 * p.nsources, np.int32).reshape(-1, 4),
             "succ": _copy(p.succ, p.nedges, np.int32),
@@ -349,6 +349,13 @@ class Plan:
             "roots": _copy(p.roots, p.nroots, np.int32),
             "values": _copy(p.values, p.nnz, np.float64),
             "cols": _copy(p.col_idx, p.nnz, np.int32),
+            "slot_rec": _copy(p.slot_rec, 4 * p.nslots, np.int32).reshape(-1, 4),
+            "upd": _copy(p.upd, 2 * p.nupdates, np.int32).reshape(-1, 2),
+            "row_rec": (_copy(p.row_rec, 8 * p.nitems, np.int32).reshape(-1, 8)
+                        if p.row_rec else np.zeros((0, 8), np.int32)),
+            "row_succ": _copy(p.row_succ, p.nrow_edges, np.int32) if p.row_succ else np.zeros(0, np.int32),
+            "row_indeg": _copy(p.row_indeg, p.nitems, np.int32) if p.row_indeg else np.zeros(0, np.int32),
+            "row_roots": _copy(p.row_roots, p.nrow_roots, np.int32) if p.row_roots else np.zeros(0, np.int32),
         }
 
 
@@ -369,6 +376,7 @@ class GpuOptions:
     staging_cap: int = 0
     timeout_s: float = 0.0
     trace: bool = False
+    mode: int = 0  # 0 auto, 1 device merge, 2 host-precomputed update programs
 
 
 class GpuFactorizer:
@@ -384,7 +392,7 @@ class GpuFactorizer:
             raise DeviceError(lib.tcg_last_error(None).decode())
         self.ctx = h
         o = N.Options(self.opt.threads_per_cta, self.opt.ctas_per_sm, self.opt.staging_cap,
-                      self.opt.timeout_s, 1 if self.opt.trace else 0)
+                      self.opt.timeout_s, 1 if self.opt.trace else 0, self.opt.mode)
         self._check(lib.tcg_set_options(self.ctx, C.byref(o)))
         self.plan = plan
         self._problem = plan.problem()
@@ -438,10 +446,12 @@ class GpuFactorizer:
     def download_ptr(self, host_ptr: int):
         self._check(self._lib.tcg_download(self.ctx, C.cast(C.c_void_p(host_ptr), N.f64p)))
 
-    def trace(self) -> np.ndarray:
-        out = np.zeros(2 * self.ntasks, dtype=np.uint64)
+    def trace(self):
+        """(task stamps [ntasks, 2], item stamps [nitems, 4]) of the last traced factor."""
+        ni = int(self._problem.nitems)
+        out = np.zeros(2 * self.ntasks + 4 * ni, dtype=np.uint64)
         self._check(self._lib.tcg_download_trace(self.ctx, out.ctypes.data_as(N.u64p)))
-        return out.reshape(-1, 2)
+        return out[:2 * self.ntasks].reshape(-1, 2), out[2 * self.ntasks:].reshape(-1, 4)
 
     def arena_bytes(self) -> int:
         return int(self._lib.tcg_arena_bytes(self.ctx))

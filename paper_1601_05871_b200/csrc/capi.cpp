@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -72,15 +73,32 @@ struct tcg_ctx {
   int4* tasks = nullptr;
   int4* items = nullptr;
   int4* srcs = nullptr;
-  int* succ = nullptr;
+  int4* succ = nullptr;  // 4 int4 per edge (kSuccWords)
   int* indeg = nullptr;
   int* indeg0 = nullptr;
   int* queue = nullptr;
   int* roots = nullptr;
+  int* claim = nullptr;
+  int* fin = nullptr;
+  int* iflag = nullptr;
+  int4* slot_rec = nullptr;
+  int2* upd = nullptr;
+  bool has_programs = false;
+  // row-level mode
+  int4* rows = nullptr;
+  int* row_succ = nullptr;
+  int* row_indeg = nullptr;
+  int* row_indeg0 = nullptr;
+  int* row_queue = nullptr;
+  int* row_roots = nullptr;
+  std::int64_t nrow_roots = 0;
+  bool has_rows = false;
   tcbdev::Ctrl* ctrl = nullptr;
   unsigned long long* trace = nullptr;
   // problem shape
   std::int64_t n = 0, nnz = 0, ntasks = 0, nitems = 0, nsrc = 0, nedges = 0, nroots = 0;
+  std::int64_t qcap = 0;
+  int epoch = 0;
   int max_target_len = 0, max_flag_rows = 0;
   bool uploaded = false;
   tcg_options opt{};
@@ -114,7 +132,11 @@ tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pa
     for (int32_t r = 0; r < nranges; ++r) rl.ranges.push_back({range_bounds[r], range_bounds[r + 1]});
     const std::vector<double> init = tcb::init_factor_values(a, u);
     auto p = std::make_unique<tcg_plan>();
-    p->plan = tcb::build_plan(u, init, rl, true);
+    tcb::PlanOptions po;
+    if (const char* e = std::getenv("TCG_CTA_COST")) po.cta_cost = std::max(1.0, std::atof(e));
+    if (const char* e = std::getenv("TCG_MAX_WIDTH")) po.max_width = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("TCG_DEP_WIDE_COST")) po.dep_wide_cost = std::max(1.0, std::atof(e));
+    p->plan = tcb::build_plan(u, init, rl, true, po);
     *out = p.release();
     return TCG_OK;
   } catch (const std::bad_alloc&) {
@@ -144,11 +166,24 @@ tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   o->src_rec = P.src_rec.data();
   o->nedges = static_cast<int64_t>(P.succ.size());
   o->succ = P.succ.data();
+  o->succ_rec = P.succ_rec.data();
   o->indeg = P.indeg.data();
   o->nroots = static_cast<int64_t>(P.roots.size());
   o->roots = P.roots.data();
   o->max_target_len = P.stats.max_target_len;
   o->max_flag_rows = P.stats.max_flag_rows;
+  o->nhelpers = P.stats.helpers;
+  o->nslots = static_cast<int64_t>(P.slot_rec.size() / 4);
+  o->slot_rec = P.slot_rec.data();
+  o->nupdates = static_cast<int64_t>(P.upd.size() / 2);
+  o->upd = P.upd.data();
+  const bool rows = !P.row_rec.empty() && !P.slot_rec.empty();
+  o->row_rec = rows ? P.row_rec.data() : nullptr;
+  o->nrow_edges = rows ? static_cast<int64_t>(P.row_succ.size()) : 0;
+  o->row_succ = rows ? P.row_succ.data() : nullptr;
+  o->row_indeg = rows ? P.row_indeg.data() : nullptr;
+  o->nrow_roots = rows ? static_cast<int64_t>(P.row_roots.size()) : 0;
+  o->row_roots = rows ? P.row_roots.data() : nullptr;
   return TCG_OK;
 }
 
@@ -164,6 +199,11 @@ tcg_status tcg_plan_get_stats(const tcg_plan* plan, tcg_plan_stats* o) {
   o->max_target_len = s.max_target_len;
   o->max_flag_rows = s.max_flag_rows;
   o->dag_depth = s.dag_depth;
+  o->max_width = s.max_width;
+  o->helpers = s.helpers;
+  o->updates = s.updates;
+  o->item_edges = s.item_edges;
+  o->item_depth = s.item_depth;
   o->nblocks_rows = plan->plan.blocks.m;
   o->nblocks = plan->plan.blocks.nblocks();
   o->block_build_seconds = s.block_build_seconds;
@@ -250,7 +290,8 @@ tcg_status tcg_set_options(tcg_ctx* c, const tcg_options* opt) {
 tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   if (!c || !p) return TCG_INVALID;
   if (p->n < 0 || p->nnz < 0 || p->ntasks < 0 || p->nitems < 0 || p->nsources < 0 ||
-      p->nedges < 0 || p->nroots < 0 || p->nnz > 0x7fffffffLL || p->ntasks > 0x7fffffffLL) {
+      p->nedges < 0 || p->nroots < 0 || p->nhelpers < 0 || p->nnz > 0x7fffffffLL ||
+      p->ntasks + p->nhelpers >= 0x40000000LL) {
     c->err = "tcg_upload: invalid problem sizes";
     return TCG_INVALID;
   }
@@ -261,7 +302,9 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     c->arena = nullptr;
     c->uploaded = false;
   }
-  // one arena: [cols][vals][vals0][tasks][items][srcs][succ][indeg][indeg0][queue][roots][ctrl][trace]
+  // one arena: [cols][vals][vals0][tasks][items][srcs][succ][indeg][indeg0][queue][roots]
+  //            [claim][fin][iflag][ctrl][trace]
+  const std::int64_t qcap = p->ntasks + p->nhelpers;
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t at = off;
@@ -271,16 +314,30 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_cols = take(sizeof(int) * p->nnz);
   const size_t o_vals = take(sizeof(double) * p->nnz);
   const size_t o_vals0 = take(sizeof(double) * p->nnz);
-  const size_t o_tasks = take(sizeof(int) * 8 * p->ntasks);
+  const size_t o_tasks = take(sizeof(int) * 12 * p->ntasks);
   const size_t o_items = take(sizeof(int) * 8 * p->nitems);
   const size_t o_srcs = take(sizeof(int) * 4 * p->nsources);
-  const size_t o_succ = take(sizeof(int) * p->nedges);
+  const size_t o_succ = take(sizeof(int4) * 4 * p->nedges);
   const size_t o_indeg = take(sizeof(int) * p->ntasks);
   const size_t o_indeg0 = take(sizeof(int) * p->ntasks);
-  const size_t o_queue = take(sizeof(int) * p->ntasks);
+  const size_t o_queue = take(sizeof(int) * qcap);
   const size_t o_roots = take(sizeof(int) * p->nroots);
+  const size_t o_claim = take(sizeof(int) * p->ntasks);
+  const size_t o_fin = take(sizeof(int) * p->ntasks);
+  const size_t o_iflag = take(sizeof(int) * p->nitems);
+  const bool programs = p->nslots > 0 && p->slot_rec && (p->nupdates == 0 || p->upd);
+  const size_t o_slot = take(programs ? sizeof(int4) * p->nslots : 0);
+  const size_t o_upd = take(programs ? sizeof(int) * 2 * p->nupdates : 0);
+  const bool rows = programs && p->row_rec && p->row_indeg && (p->nrow_edges == 0 || p->row_succ) &&
+                    (p->nrow_roots == 0 || p->row_roots);
+  const size_t o_rows = take(rows ? sizeof(int4) * 2 * p->nitems : 0);
+  const size_t o_rsucc = take(rows ? sizeof(int) * p->nrow_edges : 0);
+  const size_t o_rindeg = take(rows ? sizeof(int) * p->nitems : 0);
+  const size_t o_rindeg0 = take(rows ? sizeof(int) * p->nitems : 0);
+  const size_t o_rqueue = take(rows ? sizeof(int) * p->nitems : 0);
+  const size_t o_rroots = take(rows ? sizeof(int) * p->nrow_roots : 0);
   const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
-  const size_t o_trace = take(sizeof(unsigned long long) * 2 * p->ntasks);
+  const size_t o_trace = take(sizeof(unsigned long long) * (2 * p->ntasks + 4 * p->nitems));
   TCG_CUDA_TRY(c, cudaMalloc(&c->arena, off));
   c->arena_bytes = off;
   char* base = static_cast<char*>(c->arena);
@@ -290,11 +347,25 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->tasks = reinterpret_cast<int4*>(base + o_tasks);
   c->items = reinterpret_cast<int4*>(base + o_items);
   c->srcs = reinterpret_cast<int4*>(base + o_srcs);
-  c->succ = reinterpret_cast<int*>(base + o_succ);
+  c->succ = reinterpret_cast<int4*>(base + o_succ);
   c->indeg = reinterpret_cast<int*>(base + o_indeg);
   c->indeg0 = reinterpret_cast<int*>(base + o_indeg0);
   c->queue = reinterpret_cast<int*>(base + o_queue);
   c->roots = reinterpret_cast<int*>(base + o_roots);
+  c->claim = reinterpret_cast<int*>(base + o_claim);
+  c->fin = reinterpret_cast<int*>(base + o_fin);
+  c->iflag = reinterpret_cast<int*>(base + o_iflag);
+  c->slot_rec = reinterpret_cast<int4*>(base + o_slot);
+  c->upd = reinterpret_cast<int2*>(base + o_upd);
+  c->has_programs = programs;
+  c->rows = reinterpret_cast<int4*>(base + o_rows);
+  c->row_succ = reinterpret_cast<int*>(base + o_rsucc);
+  c->row_indeg = reinterpret_cast<int*>(base + o_rindeg);
+  c->row_indeg0 = reinterpret_cast<int*>(base + o_rindeg0);
+  c->row_queue = reinterpret_cast<int*>(base + o_rqueue);
+  c->row_roots = reinterpret_cast<int*>(base + o_rroots);
+  c->nrow_roots = rows ? p->nrow_roots : 0;
+  c->has_rows = rows;
   c->ctrl = reinterpret_cast<tcbdev::Ctrl*>(base + o_ctrl);
   c->trace = reinterpret_cast<unsigned long long*>(base + o_trace);
   auto put = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
@@ -303,12 +374,28 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   };
   TCG_CUDA_TRY(c, put(c->cols, p->col_idx, sizeof(int) * p->nnz));
   TCG_CUDA_TRY(c, put(c->vals0, p->values, sizeof(double) * p->nnz));
-  TCG_CUDA_TRY(c, put(c->tasks, p->task_rec, sizeof(int) * 8 * p->ntasks));
+  TCG_CUDA_TRY(c, put(c->tasks, p->task_rec, sizeof(int) * 12 * p->ntasks));
   TCG_CUDA_TRY(c, put(c->items, p->item_rec, sizeof(int) * 8 * p->nitems));
   TCG_CUDA_TRY(c, put(c->srcs, p->src_rec, sizeof(int) * 4 * p->nsources));
-  TCG_CUDA_TRY(c, put(c->succ, p->succ, sizeof(int) * p->nedges));
+  if (p->nedges > 0 && !p->succ_rec) {
+    c->err = "tcg_upload: succ_rec is required";
+    return TCG_INVALID;
+  }
+  TCG_CUDA_TRY(c, put(c->succ, p->succ_rec, sizeof(int4) * 4 * p->nedges));
   TCG_CUDA_TRY(c, put(c->indeg0, p->indeg, sizeof(int) * p->ntasks));
   TCG_CUDA_TRY(c, put(c->roots, p->roots, sizeof(int) * p->nroots));
+  if (programs) {
+    TCG_CUDA_TRY(c, put(c->slot_rec, p->slot_rec, sizeof(int4) * p->nslots));
+    TCG_CUDA_TRY(c, put(c->upd, p->upd, sizeof(int) * 2 * p->nupdates));
+  }
+  if (rows) {
+    TCG_CUDA_TRY(c, put(c->rows, p->row_rec, sizeof(int4) * 2 * p->nitems));
+    TCG_CUDA_TRY(c, put(c->row_succ, p->row_succ, sizeof(int) * p->nrow_edges));
+    TCG_CUDA_TRY(c, put(c->row_indeg0, p->row_indeg, sizeof(int) * p->nitems));
+    TCG_CUDA_TRY(c, put(c->row_roots, p->row_roots, sizeof(int) * p->nrow_roots));
+  }
+  if (p->nitems > 0)
+    TCG_CUDA_TRY(c, cudaMemsetAsync(c->iflag, 0, sizeof(int) * p->nitems, c->stream));
   if (p->nnz > 0)
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals, c->vals0, sizeof(double) * p->nnz,
                                     cudaMemcpyDeviceToDevice, c->stream));
@@ -320,6 +407,8 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->nsrc = p->nsources;
   c->nedges = p->nedges;
   c->nroots = p->nroots;
+  c->qcap = qcap;
+  c->epoch = 0;
   c->max_target_len = p->max_target_len;
   c->max_flag_rows = p->max_flag_rows;
   c->uploaded = true;
@@ -348,6 +437,80 @@ tcg_status tcg_restore(tcg_ctx* c) {
   return TCG_OK;
 }
 
+// Row-level execution (mode 3): one warp-granular persistent launch over the
+// items of the same DAG (row_kernel.cu).
+static tcg_status run_rows(tcg_ctx* c, tcg_stats& S, int threads) {
+  int occ = 0;
+  TCG_CUDA_TRY(c, tcbdev::rows_occupancy(threads, &occ));
+  if (occ < 1) {
+    c->err = "row kernel does not fit on an SM";
+    return TCG_INVALID;
+  }
+  if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
+  const int grid = std::max(1, occ * c->sm_count);
+
+  tcbdev::PrepParams q{};
+  q.indeg0 = c->row_indeg0;
+  q.roots = c->row_roots;
+  q.indeg = c->row_indeg;
+  q.queue = c->row_queue;
+  q.claim = nullptr;
+  q.fin = nullptr;
+  q.ctrl = c->ctrl;
+  q.qcap = static_cast<int>(c->nitems);
+  q.ntasks = static_cast<int>(c->nitems);
+  q.nroots = static_cast<int>(c->nrow_roots);
+  TCG_CUDA_TRY(c, tcbdev::launch_prepare(q, c->stream));
+
+  tcbdev::RowParams P{};
+  P.rows = c->rows;
+  P.succ = c->row_succ;
+  P.slot_rec = c->slot_rec;
+  P.upd = c->upd;
+  P.vals = c->vals;
+  P.indeg = c->row_indeg;
+  P.queue = c->row_queue;
+  P.ctrl = c->ctrl;
+  P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;  // the item-stamp region
+  P.nitems = static_cast<int>(c->nitems);
+  const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
+  P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  if (c->nitems > 0) TCG_CUDA_TRY(c, tcbdev::launch_rows(P, grid, threads, c->stream));
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
+                                  cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  const tcbdev::Ctrl& h = *c->host_ctrl;
+  S.device_ms = ms;
+  S.grid_ctas = grid;
+  S.threads_per_cta = threads;
+  S.kernel_launches = c->nitems > 0 ? 2 : 1;
+  S.mode = 3;
+  // every task's rows ran (a task with no rows has no numeric work)
+  S.tasks_completed = (h.done == c->nitems) ? c->ntasks : 0;
+  S.tasks_executed = h.executed;  // rows whose body ran
+  if (h.error) {
+    c->err = "device watchdog expired: the row dataflow stalled";
+    return TCG_TIMEOUT;
+  }
+  if (h.done != c->nitems) {
+    c->err = "row scheduler finished with " + std::to_string(h.done) + " of " +
+             std::to_string(c->nitems) + " rows";
+    return TCG_TIMEOUT;
+  }
+  if (h.failed) {
+    S.breakdown_row = h.fail_row;
+    S.breakdown_pivot = h.fail_pivot;
+    c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
+             std::to_string(h.fail_pivot) + " is not positive";
+    return TCG_BREAKDOWN;
+  }
+  return TCG_OK;
+}
+
 tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   if (!c || !c->uploaded) return TCG_INVALID;
   tcg_stats local{};
@@ -358,16 +521,32 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   TCG_CUDA_TRY(c, cudaSetDevice(c->device));
 
   const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
+  int mode = c->opt.mode;
+  if (mode == 0) mode = c->has_rows ? 3 : (c->has_programs ? 2 : 1);
+  if ((mode == 2 && !c->has_programs) || (mode == 3 && !c->has_rows) || mode < 0 || mode > 3) {
+    c->err = "requested execution mode is not available for the uploaded problem";
+    return TCG_INVALID;
+  }
+  if (mode == 3) return run_rows(c, S, threads);
   int flag_words = (c->max_flag_rows + 31) / 32;
-  flag_words += flag_words & 1;
+  flag_words = (flag_words + 3) & ~3;
   int cap = c->opt.staging_cap;
   if (cap <= 0) cap = std::min(256, std::max(32, (c->max_target_len + 31) / 32 * 32));
-  cap = (cap + 1) & ~1;
-  size_t smem = tcbdev::factor_smem_bytes(threads, cap, flag_words);
+  cap = (cap + 3) & ~3;
+  // task metadata staged per single-CTA task (items x 32 B, sources x 16 B)
+  int icap = 256, scap = 1024;
+  if (const char* e = std::getenv("TCG_ICAP")) icap = std::max(0, std::atoi(e));
+  if (const char* e = std::getenv("TCG_SCAP")) scap = std::max(0, std::atoi(e));
+  size_t smem = tcbdev::factor_smem_bytes(threads, cap, flag_words, icap, scap);
   const size_t kMaxSmem = 227 * 1024;
-  while (smem > kMaxSmem && cap > 32) {
-    cap = std::max(32, cap / 2);
-    smem = tcbdev::factor_smem_bytes(threads, cap, flag_words);
+  while (smem > kMaxSmem && (cap > 32 || scap > 0)) {
+    if (scap > 0) {
+      scap /= 2;
+      icap /= 2;
+    } else {
+      cap = std::max(32, cap / 2);
+    }
+    smem = tcbdev::factor_smem_bytes(threads, cap, flag_words, icap, scap);
   }
   if (smem > kMaxSmem) {
     c->err = "diagonal range too large for the shared-memory row flags (" +
@@ -388,7 +567,10 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   q.roots = c->roots;
   q.indeg = c->indeg;
   q.queue = c->queue;
+  q.claim = c->claim;
+  q.fin = c->fin;
   q.ctrl = c->ctrl;
+  q.qcap = static_cast<int>(c->qcap);
   q.ntasks = static_cast<int>(c->ntasks);
   q.nroots = static_cast<int>(c->nroots);
   TCG_CUDA_TRY(c, tcbdev::launch_prepare(q, c->stream));
@@ -402,11 +584,22 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   P.vals = c->vals;
   P.indeg = c->indeg;
   P.queue = c->queue;
+  P.claim = c->claim;
+  P.fin = c->fin;
+  P.iflag = c->iflag;
   P.ctrl = c->ctrl;
+  P.qcap = static_cast<int>(c->qcap);
+  P.epoch = ++c->epoch;
   P.trace = c->opt.trace ? c->trace : nullptr;
+  P.itrace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
   P.ntasks = static_cast<int>(c->ntasks);
   P.cap = cap;
   P.flag_words = flag_words;
+  P.icap = icap;
+  P.slot_rec = c->slot_rec;
+  P.upd = c->upd;
+  P.mode = mode;
+  P.scap = scap;
   const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
@@ -426,6 +619,8 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   S.staging_cap = cap;
   S.smem_bytes = static_cast<int64_t>(smem);
   S.kernel_launches = 2;
+  S.helpers_run = h.helpers_run;
+  S.mode = mode;
   if (h.error) {
     c->err = h.error == 1 ? "device watchdog expired: the task DAG stalled" : "device capacity error";
     return TCG_TIMEOUT;
@@ -459,7 +654,7 @@ tcg_status tcg_download_trace(tcg_ctx* c, uint64_t* stamps) {
   if (!c || !c->uploaded || !stamps) return TCG_INVALID;
   if (c->ntasks == 0) return TCG_OK;
   TCG_CUDA_TRY(c, cudaSetDevice(c->device));
-  TCG_CUDA_TRY(c, cudaMemcpyAsync(stamps, c->trace, sizeof(uint64_t) * 2 * c->ntasks,
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(stamps, c->trace, sizeof(uint64_t) * (2 * c->ntasks + 4 * c->nitems),
                                   cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return TCG_OK;

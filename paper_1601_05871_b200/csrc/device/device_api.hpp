@@ -1,4 +1,4 @@
-// Host-callable launch helpers of factor_kernel.cu.
+// Host-callable launch helpers of factor_kernel.cu and row_kernel.cu.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -9,9 +9,12 @@
 
 namespace tcbdev {
 
-size_t factor_smem_bytes(int threads, int cap, int flag_words);
+size_t factor_smem_bytes(int threads, int cap, int flag_words, int icap, int scap);
 cudaError_t factor_occupancy(int threads, size_t smem, int* ctas_per_sm);
 cudaError_t launch_prepare(const PrepParams& q, cudaStream_t st);
 cudaError_t launch_factor(const Params& p, int grid, int threads, size_t smem, cudaStream_t st);
+
+cudaError_t rows_occupancy(int threads, int* ctas_per_sm);
+cudaError_t launch_rows(const RowParams& p, int grid, int threads, cudaStream_t st);
 
 }  // namespace tcbdev

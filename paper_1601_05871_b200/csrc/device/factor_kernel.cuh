@@ -7,6 +7,10 @@
 namespace tcbdev {
 
 constexpr int kChol = 0, kTrsm = 1, kHerk = 2, kGemm = 3;
+// Queue entries with this bit set are helper tickets of a multi-CTA task.
+constexpr int kHelperBit = 0x40000000;
+// Task records are three int4 (plan.hpp kTaskWords = 12).
+constexpr int kTaskInt4 = 3;
 
 // Scheduler / status words, one per factorization (reset before each run).
 struct Ctrl {
@@ -15,27 +19,53 @@ struct Ctrl {
   int done;          // tasks completed (released)
   int failed;        // breakdown latch (reference factorize.hpp:146-167)
   int fail_row;
-  int error;         // 1 = watchdog expired, 2 = staging/flag capacity exceeded
+  int error;         // 1 = watchdog expired
   int executed;      // task bodies actually run (skipped after a breakdown)
-  int pad0;
+  int helpers_run;   // helper tickets that joined a multi-CTA task
   double fail_pivot;
   unsigned long long pad1;
 };
 
 struct Params {
-  const int4* tasks;   // 2 x int4 per task (plan.hpp kTaskWords)
+  const int4* tasks;   // 3 x int4 per task
   const int4* items;   // 2 x int4 per item (kItemWords)
   const int4* srcs;    // 1 x int4 per source (kSrcWords)
-  const int* succ;
+  const int4* succ;    // 4 x int4 per edge: {successor, 0, 0, 0} + its task record
   const int* cols;
   double* vals;
   int* indeg;
   int* queue;
+  int* claim;          // per task: next item of a multi-CTA task
+  int* fin;            // per task: items finished of a multi-CTA task
+  int* iflag;          // per item: epoch stamp when the row is final (multi-CTA Chol/Trsm)
   Ctrl* ctrl;
   unsigned long long* trace;  // optional: {start, end} globaltimer per task
+  unsigned long long* itrace; // optional: {claimed, sources ready, merged, published} per item
   int ntasks;
-  int cap;             // per-warp staging capacity (target row entries)
-  int flag_words;      // 32-bit words of the per-CTA row-done bitmask
+  int qcap;            // ready-queue capacity (tasks + helper tickets)
+  int cap;             // per-warp staging capacity (target row entries), multiple of 4
+  int flag_words;      // 32-bit words of the per-CTA row-done bitmask, multiple of 4
+  int icap;            // items staged in shared memory per single-CTA task
+  int scap;            // sources staged in shared memory per single-CTA task
+  int epoch;           // factorization counter (iflag stamps)
+  int mode;            // 1 = device merge of sorted indices, 2 = update programs
+  const int4* slot_rec;  // update programs (mode 2): {u_b, u_e, m0, o0} per target slot
+  const int2* upd;
+  unsigned long long timeout_ns;
+};
+
+// Row-level mode (row_kernel.cu).
+struct RowParams {
+  const int4* rows;      // 2 x int4 per item: {tb, te, dpos, slot_off}, {kind, t, succ_b, succ_e}
+  const int* succ;       // successor items
+  const int4* slot_rec;  // update programs
+  const int2* upd;
+  double* vals;
+  int* indeg;
+  int* queue;
+  Ctrl* ctrl;            // q_head/q_tail/done/executed count rows in this mode
+  unsigned long long* trace;  // optional: {start, end} per item
+  int nitems;
   unsigned long long timeout_ns;
 };
 
@@ -44,8 +74,11 @@ struct PrepParams {
   const int* roots;
   int* indeg;
   int* queue;
+  int* claim;
+  int* fin;
   Ctrl* ctrl;
   int ntasks;
+  int qcap;
   int nroots;
 };
 

@@ -3,7 +3,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <atomic>
 #include <limits>
+#include <thread>
 #include <stdexcept>
 
 namespace tcb {
@@ -159,10 +162,192 @@ BlockColumns transpose_blocks(const CsrMatrix& u, const RangeList& ranges,
   return bc;
 }
 
+// Update programs: the sorted-index merge of every (item, source) pair done
+// once on the host. For item i with target slice [tb, te) (L slots), slot k
+// has the record slot_rec[off_i + k] = {u_b, u_e, m0, o0}: its updates are
+// the (m, o) position pairs upd[u_b .. u_e), each meaning U[tb + k] -= U[m] *
+// U[o], in ascending source row (the reference's per-coordinate order), and
+// (m0, o0) repeats the first of them so the device can start gathering right
+// after one load. Entries whose column is absent from the target row are
+// dropped here (kernels.hpp:62-63).
+void build_programs(Plan& P, int threads) {
+  const std::size_t I = P.item_rec.size() / kItemWords;
+  std::vector<std::int64_t> slot_off(I + 1, 0), upd_off(I + 1, 0);
+  for (std::size_t i = 0; i < I; ++i) {
+    const std::int32_t* r = &P.item_rec[i * kItemWords];
+    slot_off[i + 1] = slot_off[i] + (r[1] - r[0]);
+  }
+  if (slot_off[I] > std::numeric_limits<std::int32_t>::max())
+    throw std::invalid_argument("plan: update-program slot table exceeds 2^31 entries");
+  const int nt = std::max(1, threads > 0 ? threads
+                                         : static_cast<int>(std::thread::hardware_concurrency()));
+  auto parallel = [&](auto&& body) {
+    std::atomic<std::size_t> next{0};
+    auto run = [&]() {
+      constexpr std::size_t kChunk = 512;
+      while (true) {
+        const std::size_t b = next.fetch_add(kChunk);
+        if (b >= I) break;
+        for (std::size_t i = b; i < std::min(I, b + kChunk); ++i) body(i);
+      }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(run);
+    run();
+    for (auto& th : pool) th.join();
+  };
+  // merge one item: calls hit(slot, m, o) for every surviving update, in order
+  auto merge_item = [&](std::size_t i, auto&& hit) {
+    const std::int32_t* r = &P.item_rec[i * kItemWords];
+    const std::int32_t* tc = P.cols.data() + r[0];
+    const std::int32_t L = r[1] - r[0];
+    for (std::int32_t s = r[4]; s < r[5]; ++s) {
+      const std::int32_t* sr = &P.src_rec[static_cast<std::size_t>(s) * kSrcWords];
+      std::int32_t k = 0;
+      for (std::int32_t e = sr[2]; e < sr[3] && k < L; ++e) {
+        k = static_cast<std::int32_t>(std::lower_bound(tc + k, tc + L, P.cols[e]) - tc);
+        if (k < L && tc[k] == P.cols[e]) hit(k, sr[1], e);
+      }
+    }
+  };
+  std::vector<std::int64_t> count(I, 0);
+  parallel([&](std::size_t i) {
+    std::int64_t c = 0;
+    merge_item(i, [&](std::int32_t, std::int32_t, std::int32_t) { ++c; });
+    count[i] = c;
+  });
+  for (std::size_t i = 0; i < I; ++i) upd_off[i + 1] = upd_off[i] + count[i];
+  if (upd_off[I] > std::numeric_limits<std::int32_t>::max())
+    throw std::invalid_argument("plan: update program exceeds 2^31 updates");
+  P.slot_rec.assign(static_cast<std::size_t>(4 * slot_off[I]), 0);
+  P.upd.assign(static_cast<std::size_t>(2 * upd_off[I]), 0);
+  parallel([&](std::size_t i) {
+    std::int32_t* r = &P.item_rec[i * kItemWords];
+    const std::int32_t L = r[1] - r[0];
+    std::vector<std::int32_t> sp(static_cast<std::size_t>(L) + 1, 0);
+    merge_item(i, [&](std::int32_t k, std::int32_t, std::int32_t) { ++sp[k + 1]; });
+    for (std::int32_t k = 0; k < L; ++k) sp[k + 1] += sp[k];
+    std::vector<std::int32_t> fill(sp.begin(), sp.end() - 1);
+    const std::int64_t base = upd_off[i];
+    merge_item(i, [&](std::int32_t k, std::int32_t m, std::int32_t o) {
+      const std::int64_t at = base + fill[k]++;
+      P.upd[2 * at] = m;
+      P.upd[2 * at + 1] = o;
+    });
+    std::int32_t* sr = &P.slot_rec[static_cast<std::size_t>(4 * slot_off[i])];
+    for (std::int32_t k = 0; k < L; ++k) {
+      const std::int64_t ub = base + sp[k], ue = base + sp[k + 1];
+      sr[4 * k] = static_cast<std::int32_t>(ub);
+      sr[4 * k + 1] = static_cast<std::int32_t>(ue);
+      sr[4 * k + 2] = ub < ue ? P.upd[2 * ub] : 0;
+      sr[4 * k + 3] = ub < ue ? P.upd[2 * ub + 1] : 0;
+    }
+    r[6] = static_cast<std::int32_t>(slot_off[i]);
+  });
+  P.stats.updates = upd_off[I];
+}
+
+// Row-level dependences. Every coordinate of U receives its updates in
+// ascending source row as long as (a) the items writing the same (block,
+// row) slice run in generation order and (b) an item reads only slices that
+// are final. So an item follows: the previous item writing its own slice,
+// and the last writer of every slice it reads (multipliers U(r,t), operand
+// rows U(r,:), the Trsm divisor U(t,t)). These are exactly the block-level
+// edges of the generation walk (factorize.hpp:175-224) restricted to the
+// rows that actually interact.
+void build_item_deps(Plan& P, const RangeList& ranges) {
+  const BlockLayout& bl = P.blocks;
+  const std::size_t I = P.item_rec.size() / kItemWords;
+  const std::size_t T = P.node_kind.size();
+  std::vector<std::int32_t> row0(static_cast<std::size_t>(bl.nblocks()));
+  for (index_t bi = 0; bi < bl.m; ++bi)
+    for (offset_t q = bl.brow_ptr[bi]; q < bl.brow_ptr[bi + 1]; ++q) row0[q] = ranges.ranges[bi].begin;
+  std::vector<std::int32_t> last(static_cast<std::size_t>(bl.span_off.back()), -1);
+  auto slot = [&](std::int32_t blk, std::int32_t row) -> std::int32_t& {
+    return last[static_cast<std::size_t>(bl.span_off[blk] + (row - row0[blk]))];
+  };
+  P.item_dep_ptr.assign(I + 1, 0);
+  P.item_dep.clear();
+  P.item_dep.reserve(3 * I);
+  std::vector<std::int32_t> depth(I, 1), deps;
+  for (std::size_t tk = 0; tk < T; ++tk) {
+    const std::int32_t* rec = &P.task_rec[tk * kTaskWords];
+    const std::int32_t kind = rec[0], ib = rec[2], ie = rec[3];
+    const std::int32_t tgt = P.task_blk[4 * tk], mult = P.task_blk[4 * tk + 1],
+                       oper = P.task_blk[4 * tk + 2];
+    for (std::int32_t k = ib; k < ie; ++k) {
+      const std::int32_t* it = &P.item_rec[static_cast<std::size_t>(k) * kItemWords];
+      const std::int32_t t = it[7];
+      deps.clear();
+      if (slot(tgt, t) >= 0) deps.push_back(slot(tgt, t));
+      if (kind == kTrsm) deps.push_back(slot(mult, t));  // U(t,t)
+      for (std::int32_t s = it[4]; s < it[5]; ++s) {
+        const std::int32_t d = P.src_rec[static_cast<std::size_t>(s) * kSrcWords];
+        if (kind == kChol) {
+          deps.push_back(ib + d);
+        } else if (kind == kTrsm) {
+          const std::int32_t r = row0[mult] + P.item_rec[static_cast<std::size_t>(ib + d) * kItemWords + 2];
+          deps.push_back(slot(mult, r));  // U(r,t), written by Chol(p)
+          deps.push_back(ib + d);         // row r of this panel
+        } else {
+          const std::int32_t rg = row0[oper] + d;  // d: row within block row p
+          deps.push_back(slot(mult, rg));
+          if (oper != mult) deps.push_back(slot(oper, rg));
+        }
+      }
+      std::sort(deps.begin(), deps.end());
+      deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+      std::int32_t dp = 1;
+      for (std::int32_t d : deps) {
+        if (d < 0 || d >= k) throw std::logic_error("plan: row dependence out of order");
+        P.item_dep.push_back(d);
+        dp = std::max(dp, depth[d] + 1);
+      }
+      depth[k] = dp;
+      P.item_dep_ptr[k + 1] = static_cast<std::int64_t>(P.item_dep.size());
+      slot(tgt, t) = k;
+    }
+  }
+  P.stats.item_edges = static_cast<std::int64_t>(P.item_dep.size());
+  P.stats.item_depth = I ? *std::max_element(depth.begin(), depth.end()) : 0;
+
+  // device tables of the row-level mode: successor CSR, counters, roots and
+  // a self-contained record per row {tb, te, dpos, slot_off | kind, t, succ_b, succ_e}
+  std::vector<std::int32_t> cnt(I + 1, 0);
+  for (std::int32_t d : P.item_dep) ++cnt[d + 1];
+  for (std::size_t k = 0; k < I; ++k) cnt[k + 1] += cnt[k];
+  P.row_succ.assign(P.item_dep.size(), 0);
+  P.row_indeg.assign(I, 0);
+  std::vector<std::int32_t> fill(cnt.begin(), cnt.end() - 1);
+  for (std::size_t k = 0; k < I; ++k)
+    for (std::int64_t e = P.item_dep_ptr[k]; e < P.item_dep_ptr[k + 1]; ++e) {
+      P.row_succ[fill[P.item_dep[e]]++] = static_cast<std::int32_t>(k);
+      ++P.row_indeg[k];
+    }
+  P.row_rec.assign(I * kRowWords, 0);
+  P.row_roots.clear();
+  for (std::size_t tk = 0; tk < T; ++tk) {
+    const std::int32_t* rec = &P.task_rec[tk * kTaskWords];
+    for (std::int32_t k = rec[2]; k < rec[3]; ++k) {
+      const std::int32_t* it = &P.item_rec[static_cast<std::size_t>(k) * kItemWords];
+      std::int32_t* r = &P.row_rec[static_cast<std::size_t>(k) * kRowWords];
+      r[0] = it[0];
+      r[1] = it[1];
+      r[2] = it[3];
+      r[3] = it[6];
+      r[4] = rec[0];
+      r[5] = it[7];
+      r[6] = cnt[k];
+      r[7] = cnt[k + 1];
+      if (P.row_indeg[k] == 0) P.row_roots.push_back(k);
+    }
+  }
+}
+
 }  // namespace
 
 Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
-                const RangeList& ranges, bool with_work) {
+                const RangeList& ranges, bool with_work, const PlanOptions& opt) {
   if (u.nrows != u.ncols) throw std::invalid_argument("factor pattern not square");
   if (static_cast<offset_t>(init_values.size()) != u.nnz())
     throw std::invalid_argument("initial values do not match the pattern");
@@ -214,14 +399,22 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
     std::int32_t* rec = &tr[static_cast<std::size_t>(id) * kTaskWords];
     rec[0] = kind;
     rec[2] = rec[3] = static_cast<std::int32_t>(ir.size() / kItemWords);
-    rec[7] = static_cast<std::int32_t>(writes);
+    rec[8] = rec[9] = static_cast<std::int32_t>(sr.size() / kSrcWords);
+    rec[10] = static_cast<std::int32_t>(writes);
+    // blocks the rows of this task read: multipliers U(r,t) and operands U(r,c)
+    const offset_t* rd = reads.begin();
+    const offset_t mult = rd[0];
+    const offset_t oper = (kind == kTrsm || kind == kGemm) ? rd[1] : rd[0];
+    P.task_blk.insert(P.task_blk.end(), {static_cast<std::int32_t>(writes),
+                                         static_cast<std::int32_t>(mult),
+                                         static_cast<std::int32_t>(oper), 0});
     return id;
   };
   auto add_item = [&](std::int32_t tb, std::int32_t te, std::int32_t local, std::int32_t dpos,
-                      std::int64_t src_begin) {
+                      std::int64_t src_begin, std::int32_t t) {
     const std::int64_t src_end = static_cast<std::int64_t>(sr.size() / kSrcWords);
     ir.insert(ir.end(), {tb, te, local, dpos, static_cast<std::int32_t>(src_begin),
-                         static_cast<std::int32_t>(src_end), 0, 0});
+                         static_cast<std::int32_t>(src_end), 0, t});
     P.stats.max_target_len = std::max(P.stats.max_target_len, te - tb);
     ++P.stats.items;
   };
@@ -230,10 +423,87 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
     ++P.stats.sources;
     P.stats.pairs += se - sb;
   };
+  // Per-task finishing pass:
+  //  * Chol/Trsm rows depend on earlier rows of the same task. Items are
+  //    re-ordered by intra-task level (stable, so ascending t inside a level)
+  //    and each source's wait field is rewritten from "row r" to "position of
+  //    row r's item", so that warps claiming items in order never wait on a
+  //    row that is claimed later and rows of one level run concurrently.
+  //  * the CTA width (how many CTAs cooperate on the task) from its size.
+  std::vector<std::int32_t> item_of_row, level, order, tmp_items;
   auto close_task = [&](std::int32_t id) {
-    tr[static_cast<std::size_t>(id) * kTaskWords + 3] = static_cast<std::int32_t>(ir.size() / kItemWords);
+    std::int32_t* rec = &tr[static_cast<std::size_t>(id) * kTaskWords];
+    const std::int32_t ib = rec[2];
+    const auto ie = static_cast<std::int32_t>(ir.size() / kItemWords);
+    rec[3] = ie;
+    rec[9] = static_cast<std::int32_t>(sr.size() / kSrcWords);
     if (sr.size() / kSrcWords > static_cast<std::size_t>(std::numeric_limits<std::int32_t>::max()))
       throw std::invalid_argument("plan: source table exceeds 2^31 records");
+    const std::int32_t ni = ie - ib;
+    double cost = 0.0;
+    std::int32_t nlev = ni > 0 ? 1 : 0, widest = ni;
+    for (std::int32_t it = ib; it < ie; ++it) {
+      const std::int32_t* r = &ir[static_cast<std::size_t>(it) * kItemWords];
+      std::int64_t pairs = 0;
+      for (std::int32_t s = r[4]; s < r[5]; ++s)
+        pairs += sr[static_cast<std::size_t>(s) * kSrcWords + 3] - sr[static_cast<std::size_t>(s) * kSrcWords + 2];
+      cost += 2.0 + (r[5] - r[4]) / 8.0 + static_cast<double>(pairs) / 32.0 + (r[1] - r[0]) / 32.0;
+    }
+    if ((rec[0] == kChol || rec[0] == kTrsm) && ni > 0) {
+      const std::int32_t nrows = rec[1];
+      item_of_row.assign(static_cast<std::size_t>(nrows), -1);
+      for (std::int32_t it = ib; it < ie; ++it)
+        item_of_row[ir[static_cast<std::size_t>(it) * kItemWords + 2]] = it - ib;
+      level.assign(static_cast<std::size_t>(ni), 0);
+      for (std::int32_t k = 0; k < ni; ++k) {  // items ascend in t: sources precede
+        const std::int32_t* r = &ir[static_cast<std::size_t>(ib + k) * kItemWords];
+        std::int32_t lv = 0;
+        for (std::int32_t s = r[4]; s < r[5]; ++s) {
+          const std::int32_t dep = item_of_row[sr[static_cast<std::size_t>(s) * kSrcWords]];
+          if (dep < 0) throw std::logic_error("plan: source row without an item");
+          lv = std::max(lv, level[dep] + 1);
+        }
+        level[k] = lv;
+      }
+      order.resize(static_cast<std::size_t>(ni));
+      for (std::int32_t k = 0; k < ni; ++k) order[k] = k;
+      std::stable_sort(order.begin(), order.end(),
+                       [&](std::int32_t x, std::int32_t y) { return level[x] < level[y]; });
+      std::vector<std::int32_t> pos(static_cast<std::size_t>(ni));
+      for (std::int32_t k = 0; k < ni; ++k) pos[order[k]] = k;
+      for (std::int32_t k = 0; k < ni; ++k) {
+        const std::int32_t* r = &ir[static_cast<std::size_t>(ib + k) * kItemWords];
+        for (std::int32_t s = r[4]; s < r[5]; ++s) {
+          std::int32_t& w = sr[static_cast<std::size_t>(s) * kSrcWords];
+          w = pos[item_of_row[w]];
+        }
+      }
+      tmp_items.assign(ir.begin() + static_cast<std::ptrdiff_t>(ib) * kItemWords, ir.end());
+      for (std::int32_t k = 0; k < ni; ++k)
+        std::copy_n(&tmp_items[static_cast<std::size_t>(order[k]) * kItemWords], kItemWords,
+                    &ir[static_cast<std::size_t>(ib + k) * kItemWords]);
+      std::vector<std::int32_t> per_level;
+      for (std::int32_t k = 0; k < ni; ++k) {
+        if (level[k] >= static_cast<std::int32_t>(per_level.size())) per_level.resize(level[k] + 1, 0);
+        ++per_level[level[k]];
+      }
+      nlev = static_cast<std::int32_t>(per_level.size());
+      widest = *std::max_element(per_level.begin(), per_level.end());
+    }
+    // CTA width: enough CTAs to give each warp ~kCtaCost/8 steps, never more
+    // warps than the widest level offers rows.
+    std::int32_t width = static_cast<std::int32_t>(std::ceil(cost / opt.cta_cost));
+    width = std::min(width, (widest + 7) / 8);
+    // rows of a Chol/Trsm chain hand off through shared memory inside one
+    // CTA (~0.3 us) but through global flags across CTAs (~1.4 us): spread
+    // such a task only when a level carries more work than one CTA clears
+    // in about one hand-off time
+    if ((rec[0] == kChol || rec[0] == kTrsm) && cost < opt.dep_wide_cost * nlev) width = 1;
+    width = std::max(1, std::min(width, opt.max_width));
+    rec[1] = width;
+    rec[7] = nlev;
+    P.stats.max_width = std::max(P.stats.max_width, width);
+    P.stats.helpers += width - 1;
   };
 
   for (index_t p = 0; p < m; ++p) {
@@ -262,7 +532,7 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
             span(rb, r - Rp.begin, sb, se);
             add_src(r - Rp.begin, bc.csc_pos[c], bc.csc_pos[c], se);
           }
-          add_item(tb, te, t - Rp.begin, tb, s0);
+          add_item(tb, te, t - Rp.begin, tb, s0, t);
         }
       }
       close_task(id);
@@ -288,7 +558,7 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
             if (sb == se) continue;
             add_src(r - Rp.begin, bc.csc_pos[c], sb, se);
           }
-          add_item(tb, te, t - Rp.begin, static_cast<std::int32_t>(u.row_begin(t)), s0);
+          add_item(tb, te, t - Rp.begin, static_cast<std::int32_t>(u.row_begin(t)), s0, t);
         }
       }
       close_task(id);
@@ -320,10 +590,10 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
               span(qj, r - Rp.begin, sb, se);
               if (herk) sb = pos;  // Herk: entries c2 >= c1 = t of row r
               if (sb == se) continue;
-              add_src(-1, pos, sb, se);
+              add_src(r - Rp.begin, pos, sb, se);  // row in the panel (no wait)
             }
             if (static_cast<std::int64_t>(sr.size() / kSrcWords) == s0) continue;
-            add_item(tb, te, -1, -1, s0);
+            add_item(tb, te, -1, -1, s0, t);
           }
           const std::int32_t* rec = &tr[static_cast<std::size_t>(id) * kTaskWords];
           if (static_cast<std::int32_t>(ir.size() / kItemWords) == rec[2]) ++P.stats.empty_tasks;
@@ -332,6 +602,9 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
       }
     }
   }
+
+  if (with_work && opt.programs) build_programs(P, opt.threads);
+  if (with_work) build_item_deps(P, ranges);
 
   // successors + in-degrees (edge multiplicity preserved)
   const std::size_t T = P.node_kind.size();
@@ -351,6 +624,15 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
     tr[t * kTaskWords + 4] = cnt[t];
     tr[t * kTaskWords + 5] = cnt[t + 1];
     if (P.indeg[t] == 0) P.roots.push_back(static_cast<std::int32_t>(t));
+  }
+  // edge records for the device: {successor, 0, 0, 0} followed by a copy of
+  // the successor's task record, so a CTA that readies a successor already
+  // holds everything it needs to start it (no dependent load on the hop)
+  P.succ_rec.assign(P.succ.size() * kSuccWords, 0);
+  for (std::size_t e = 0; e < P.succ.size(); ++e) {
+    std::int32_t* r = &P.succ_rec[e * kSuccWords];
+    r[0] = P.succ[e];
+    std::copy_n(&tr[static_cast<std::size_t>(P.succ[e]) * kTaskWords], kTaskWords, r + 4);
   }
   P.stats.edges = static_cast<std::int64_t>(P.edge_from.size());
   std::vector<std::int32_t> depth(T, 1);

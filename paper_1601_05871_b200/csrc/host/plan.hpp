@@ -10,11 +10,11 @@
 //
 //   item   = one target row of the task's output block
 //            {tb, te}   : the row's slice of U (positions) inside the block
-//            local      : row index inside the diagonal range (Chol/Trsm flags)
+//            local      : row index inside the diagonal range (breakdown row)
 //            dpos       : position of U(t,t) (Trsm divisor; Chol pivot)
 //            [sbeg,send): its source list
 //   source = one row r of the task's panel that couples to t through U(r,t)
-//            {r_local, pos_rt, sb, se}: wait flag (Chol/Trsm, else -1), the
+//            {dep, pos_rt, sb, se}: item position to wait for (Chol/Trsm, else -1), the
 //            multiplier's position, and the slice of row r whose entries
 //            update row t (sorted columns; entries absent from the target
 //            are dropped by the device merge).
@@ -32,9 +32,21 @@ namespace tcb {
 enum TaskKind : std::int32_t { kChol = 0, kTrsm = 1, kHerk = 2, kGemm = 3 };
 
 // Integer words per record in the device tables.
-constexpr int kTaskWords = 8;  // kind, flag_rows, item_b, item_e, succ_b, succ_e, row_begin, out_block
-constexpr int kItemWords = 8;  // tb, te, local, dpos, src_b, src_e, 0, 0
-constexpr int kSrcWords = 4;   // r_local, pos_rt, sb, se
+// task: kind, width, item_b, item_e | succ_b, succ_e, row_begin, nlevels |
+//       src_b, src_e, out_block, 0   (three int4 loads)
+constexpr int kTaskWords = 12;
+constexpr int kItemWords = 8;  // tb, te, local, dpos, src_b, src_e, slot_off, 0
+constexpr int kSrcWords = 4;   // dep (item position in task, Chol/Trsm; else -1), pos_rt, sb, se
+constexpr int kSuccWords = 16; // successor id, 0, 0, 0, then its 12-word task record
+constexpr int kRowWords = 8;   // row-level record: tb, te, dpos, slot_off | kind, t, succ_b, succ_e
+
+struct PlanOptions {
+  double cta_cost = 64.0;  // estimated warp-steps one CTA should get before a helper joins
+  int max_width = 64;      // most CTAs cooperating on one task
+  double dep_wide_cost = 64.0;  // Chol/Trsm go multi-CTA only above this cost per level
+  bool programs = true;    // precompute per-row update programs (slot_rec / upd)
+  int threads = 0;         // host threads for the program build (0 = all)
+};
 
 struct BlockLayout {
   index_t m = 0;
@@ -56,6 +68,11 @@ struct PlanStats {
   std::int32_t max_target_len = 0; // longest target row slice
   std::int32_t max_flag_rows = 0;  // largest Chol/Trsm diagonal range
   std::int32_t dag_depth = 0;      // longest path, in tasks
+  std::int32_t max_width = 1;      // widest task, in CTAs
+  std::int64_t helpers = 0;        // extra queue entries for multi-CTA tasks
+  std::int64_t updates = 0;        // (m, o) products in the update programs
+  std::int64_t item_edges = 0;     // row-level dependences
+  std::int32_t item_depth = 0;     // longest row-level chain, in items
   double block_build_seconds = 0.0;
   double plan_seconds = 0.0;
 };
@@ -71,7 +88,19 @@ struct Plan {
   std::vector<std::int32_t> edge_from, edge_to;  // emission order
   // device tables
   std::vector<std::int32_t> task_rec, item_rec, src_rec;
+  std::vector<std::int32_t> task_blk;  // per task: target, multiplier, operand block, 0
+  // row-level execution: per item, the items it must follow (rows it reads
+  // and the previous writer of its own row), derived from the same walk
+  std::vector<std::int64_t> item_dep_ptr;
+  std::vector<std::int32_t> item_dep;
+  std::vector<std::int32_t> row_rec;    // kRowWords per item
+  std::vector<std::int32_t> row_succ;   // successor items, grouped per item
+  std::vector<std::int32_t> row_indeg;  // dependence counters per item
+  std::vector<std::int32_t> row_roots;  // items with no dependence, ascending
+  std::vector<std::int32_t> slot_rec;  // update-program slots {u_b, u_e, m0, o0} (per item: L)
+  std::vector<std::int32_t> upd;       // update-program (m, o) pairs
   std::vector<std::int32_t> succ;      // successors grouped per task
+  std::vector<std::int32_t> succ_rec;  // per edge: successor + copy of its task record
   std::vector<std::int32_t> indeg;     // predecessors per task (edge multiplicity)
   std::vector<std::int32_t> roots;     // tasks with indeg 0, ascending
   PlanStats stats;
@@ -83,6 +112,7 @@ BlockLayout build_block_layout(const CsrMatrix& u, const RangeList& ranges);
 // block_layout.hpp:100, kernels.hpp:46-48) and std::logic_error when a
 // diagonal block is missing (factorize.hpp:173-174).
 Plan build_plan(const CsrMatrix& pattern, const std::vector<double>& init_values,
-                const RangeList& ranges, bool with_work = true);
+                const RangeList& ranges, bool with_work = true,
+                const PlanOptions& opt = PlanOptions());
 
 }  // namespace tcb

@@ -286,3 +286,67 @@ def emulate_plan(plan) -> np.ndarray:
                 tv = tv / vals[dpos]
             vals[tb:te] = tv
     return vals
+
+
+def emulate_program(plan) -> np.ndarray:
+    """Sequential host replay of the update-program mode (small matrices)."""
+    T = plan.tables()
+    vals = T["values"].copy()
+    srec, upd = T["slot_rec"], T["upd"]
+    items = T["item"]
+    for rec in T["task"]:
+        kind, ib, ie = rec[0], rec[2], rec[3]
+        for it in range(ib, ie):
+            tb, te, _, dpos, _, _, soff, _ = items[it]
+            L = te - tb
+            tv = vals[tb:te].copy()
+            for k in range(L):
+                ub, ue, m0, o0 = srec[soff + k]
+                assert ub == ue or (upd[ub][0] == m0 and upd[ub][1] == o0)
+                for u in range(ub, ue):
+                    m, o = upd[u]
+                    tv[k] = tv[k] - vals[m] * vals[o]
+            if kind == 0:
+                d = np.sqrt(tv[0])
+                tv[1:] = tv[1:] / d
+                tv[0] = d
+            elif kind == 1:
+                tv = tv / vals[dpos]
+            vals[tb:te] = tv
+    return vals
+
+
+def emulate_rows(plan, seed: int = 0) -> np.ndarray:
+    """Replay of the row-level mode in a random topological order of the row
+    DAG (a missing row dependence shows up as a value mismatch)."""
+    import random
+    T = plan.tables()
+    vals = T["values"].copy()
+    srec, upd, rows = T["slot_rec"], T["upd"], T["row_rec"]
+    succ, indeg = T["row_succ"], T["row_indeg"].copy()
+    ready = list(T["row_roots"])
+    rng = random.Random(seed)
+    done = 0
+    while ready:
+        k = ready.pop(rng.randrange(len(ready)))
+        tb, te, dpos, soff, kind, _, sb, se = rows[k]
+        tv = vals[tb:te].copy()
+        for j in range(te - tb):
+            ub, ue, _, _ = srec[soff + j]
+            for u in range(ub, ue):
+                m, o = upd[u]
+                tv[j] = tv[j] - vals[m] * vals[o]
+        if kind == 0:
+            d = np.sqrt(tv[0])
+            tv[1:] = tv[1:] / d
+            tv[0] = d
+        elif kind == 1:
+            tv = tv / vals[dpos]
+        vals[tb:te] = tv
+        done += 1
+        for s in succ[sb:se]:
+            indeg[s] -= 1
+            if indeg[s] == 0:
+                ready.append(int(s))
+    assert done == len(rows), "row DAG did not drain"
+    return vals
