@@ -90,6 +90,7 @@ struct tcg_ctx {
   int* row_indeg = nullptr;
   int* row_indeg0 = nullptr;
   int* row_queue = nullptr;
+  int* row_hiq = nullptr;
   int* row_roots = nullptr;
   std::int64_t nrow_roots = 0;
   bool has_rows = false;
@@ -136,6 +137,7 @@ tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pa
     if (const char* e = std::getenv("TCG_CTA_COST")) po.cta_cost = std::max(1.0, std::atof(e));
     if (const char* e = std::getenv("TCG_MAX_WIDTH")) po.max_width = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("TCG_DEP_WIDE_COST")) po.dep_wide_cost = std::max(1.0, std::atof(e));
+    if (const char* e = std::getenv("TCG_HOT_FRACTION")) po.hot_fraction = std::atof(e);
     p->plan = tcb::build_plan(u, init, rl, true, po);
     *out = p.release();
     return TCG_OK;
@@ -335,6 +337,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_rindeg = take(rows ? sizeof(int) * p->nitems : 0);
   const size_t o_rindeg0 = take(rows ? sizeof(int) * p->nitems : 0);
   const size_t o_rqueue = take(rows ? sizeof(int) * p->nitems : 0);
+  const size_t o_rhiq = take(rows ? sizeof(int) * p->nitems : 0);
   const size_t o_rroots = take(rows ? sizeof(int) * p->nrow_roots : 0);
   const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
   const size_t o_trace = take(sizeof(unsigned long long) * (2 * p->ntasks + 4 * p->nitems));
@@ -363,6 +366,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->row_indeg = reinterpret_cast<int*>(base + o_rindeg);
   c->row_indeg0 = reinterpret_cast<int*>(base + o_rindeg0);
   c->row_queue = reinterpret_cast<int*>(base + o_rqueue);
+  c->row_hiq = reinterpret_cast<int*>(base + o_rhiq);
   c->row_roots = reinterpret_cast<int*>(base + o_rroots);
   c->nrow_roots = rows ? p->nrow_roots : 0;
   c->has_rows = rows;
@@ -455,6 +459,7 @@ static tcg_status run_rows(tcg_ctx* c, tcg_stats& S, int threads) {
   q.indeg = c->row_indeg;
   q.queue = c->row_queue;
   q.claim = nullptr;
+  q.queue2 = c->row_hiq;
   q.fin = nullptr;
   q.ctrl = c->ctrl;
   q.qcap = static_cast<int>(c->nitems);
@@ -470,6 +475,7 @@ static tcg_status run_rows(tcg_ctx* c, tcg_stats& S, int threads) {
   P.vals = c->vals;
   P.indeg = c->row_indeg;
   P.queue = c->row_queue;
+  P.hiq = c->row_hiq;
   P.ctrl = c->ctrl;
   P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;  // the item-stamp region
   P.nitems = static_cast<int>(c->nitems);
@@ -490,18 +496,18 @@ static tcg_status run_rows(tcg_ctx* c, tcg_stats& S, int threads) {
   S.kernel_launches = c->nitems > 0 ? 2 : 1;
   S.mode = 3;
   // every task's rows ran (a task with no rows has no numeric work)
-  S.tasks_completed = (h.done == c->nitems) ? c->ntasks : 0;
-  S.tasks_executed = h.executed;  // rows whose body ran
-  if (h.error) {
+  S.tasks_completed = (h.done.v == c->nitems) ? c->ntasks : 0;
+  S.tasks_executed = h.executed.v;  // rows whose body ran
+  if (h.error.v) {
     c->err = "device watchdog expired: the row dataflow stalled";
     return TCG_TIMEOUT;
   }
-  if (h.done != c->nitems) {
-    c->err = "row scheduler finished with " + std::to_string(h.done) + " of " +
+  if (h.done.v != c->nitems) {
+    c->err = "row scheduler finished with " + std::to_string(h.done.v) + " of " +
              std::to_string(c->nitems) + " rows";
     return TCG_TIMEOUT;
   }
-  if (h.failed) {
+  if (h.failed.v) {
     S.breakdown_row = h.fail_row;
     S.breakdown_pivot = h.fail_pivot;
     c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
@@ -567,6 +573,7 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   q.roots = c->roots;
   q.indeg = c->indeg;
   q.queue = c->queue;
+  q.queue2 = nullptr;
   q.claim = c->claim;
   q.fin = c->fin;
   q.ctrl = c->ctrl;
@@ -612,25 +619,25 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
   const tcbdev::Ctrl& h = *c->host_ctrl;
   S.device_ms = ms;
-  S.tasks_completed = h.done;
-  S.tasks_executed = h.executed;
+  S.tasks_completed = h.done.v;
+  S.tasks_executed = h.executed.v;
   S.grid_ctas = grid;
   S.threads_per_cta = threads;
   S.staging_cap = cap;
   S.smem_bytes = static_cast<int64_t>(smem);
   S.kernel_launches = 2;
-  S.helpers_run = h.helpers_run;
+  S.helpers_run = h.helpers_run.v;
   S.mode = mode;
-  if (h.error) {
-    c->err = h.error == 1 ? "device watchdog expired: the task DAG stalled" : "device capacity error";
+  if (h.error.v) {
+    c->err = h.error.v == 1 ? "device watchdog expired: the task DAG stalled" : "device capacity error";
     return TCG_TIMEOUT;
   }
-  if (h.done != c->ntasks) {
-    c->err = "scheduler finished with " + std::to_string(h.done) + " of " +
+  if (h.done.v != c->ntasks) {
+    c->err = "scheduler finished with " + std::to_string(h.done.v) + " of " +
              std::to_string(c->ntasks) + " tasks";
     return TCG_TIMEOUT;
   }
-  if (h.failed) {
+  if (h.failed.v) {
     S.breakdown_row = h.fail_row;
     S.breakdown_pivot = h.fail_pivot;
     c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +

@@ -48,7 +48,7 @@ namespace tcbdev {
 
 namespace {
 
-__device__ __forceinline__ void raise_error(Ctrl* c, int code) { atomicCAS(&c->error, 0, code); }
+__device__ __forceinline__ void raise_error(Ctrl* c, int code) { atomicCAS(&c->error.v, 0, code); }
 
 // lower_bound over a sorted int array; returns the index of `key` or -1.
 template <typename IntPtr>
@@ -67,7 +67,7 @@ __device__ __forceinline__ int find_col(IntPtr cols, int len, int key) {
 }
 
 __device__ __forceinline__ bool timed_out(const Params& P, unsigned long long t0) {
-  if (ld_relaxed(&P.ctrl->error)) return true;
+  if (ld_relaxed(&P.ctrl->error.v)) return true;
   if (gtimer() - t0 > P.timeout_ns) {
     raise_error(P.ctrl, 1);
     return true;
@@ -229,7 +229,7 @@ __device__ __forceinline__ void run_item(const Params& P, const int4 ia, const i
     const double piv = tval[0];
     __syncwarp();
     if (!(piv > 0.0) && lane == 0) {
-      if (atomicCAS(&P.ctrl->failed, 0, 1) == 0) {
+      if (atomicCAS(&P.ctrl->failed.v, 0, 1) == 0) {
         P.ctrl->fail_row = row_begin + local;
         P.ctrl->fail_pivot = piv;
       }
@@ -329,7 +329,7 @@ __device__ __forceinline__ void run_item_prog(const Params& P, const int4 ia, co
     // kernels.hpp:49-53: pivot test, square root, row scaling
     const double piv = __shfl_sync(kFull, v, 0);
     if (!(piv > 0.0) && lane == 0) {
-      if (atomicCAS(&P.ctrl->failed, 0, 1) == 0) {
+      if (atomicCAS(&P.ctrl->failed.v, 0, 1) == 0) {
         P.ctrl->fail_row = row_begin + local;
         P.ctrl->fail_pivot = piv;
       }
@@ -424,7 +424,7 @@ __device__ __forceinline__ int work_items(const Params& P, int kind, int t, int 
 // Ticket-based pop: returns a queue entry (task id, possibly with the helper
 // bit), or -1 once all tasks are done (or the run was aborted).
 __device__ __forceinline__ int pop_entry(const Params& P, unsigned long long t0) {
-  const int ticket = atomicAdd(&P.ctrl->q_head, 1);
+  const int ticket = atomicAdd(&P.ctrl->q_head.v, 1);
   unsigned spins = 0;
   unsigned ns = 32;
   while (true) {
@@ -433,8 +433,8 @@ __device__ __forceinline__ int pop_entry(const Params& P, unsigned long long t0)
       if (v >= 0) return v;
     }
     if ((spins & 7u) == 0) {
-      if (ld_relaxed(&P.ctrl->done) >= P.ntasks) return -1;
-      if (ld_relaxed(&P.ctrl->error)) return -1;
+      if (ld_relaxed(&P.ctrl->done.v) >= P.ntasks) return -1;
+      if (ld_relaxed(&P.ctrl->error.v)) return -1;
     }
     if (++spins == 1024u) {
       spins = 0;
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(THREADS) factor_persistent(Params P) {
       s_cont = -1;
       if (e < 0) {
         e = pop_entry(P, t0);
-        latched = ld_relaxed(&P.ctrl->failed) | ld_relaxed(&P.ctrl->error);
+        latched = ld_relaxed(&P.ctrl->failed.v) | ld_relaxed(&P.ctrl->error.v);
       }
       s_entry = e;
       if (e >= 0) {
@@ -525,11 +525,11 @@ __global__ void __launch_bounds__(THREADS) factor_persistent(Params P) {
     if (width > 1 && !(skip && !helper) && nitems > 0) {
       // ---- multi-CTA task -------------------------------------------------
       if (!helper) {
-        if (tid == 0) s_next = atomicAdd(&P.ctrl->q_tail, width - 1);
+        if (tid == 0) s_next = atomicAdd(&P.ctrl->q_tail.v, width - 1);
         __syncthreads();
         if (tid < width - 1) st_release(P.queue + s_next + tid, t | kHelperBit);
       } else if (tid == 0) {
-        atomicAdd(&P.ctrl->helpers_run, 1);
+        atomicAdd(&P.ctrl->helpers_run.v, 1);
       }
       const int mine = work_items<true>(P, kind, t, item_b, nitems, P.items + 2 * item_b, P.srcs, 0,
                                         &s_next, lane, scol, sval, flags, row_begin, t0);
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(THREADS) factor_persistent(Params P) {
       if (tid == 0) {
         const int n = s_done;
         s_release = (n > 0 && atom_add_acq_rel(P.fin + t, n) + n == nitems) ? 1 : 0;
-        if (s_release && !skip) atomicAdd(&P.ctrl->executed, 1);
+        if (s_release && !skip) atomicAdd(&P.ctrl->executed.v, 1);
       }
       __syncthreads();
       release = s_release != 0;
@@ -562,13 +562,13 @@ __global__ void __launch_bounds__(THREADS) factor_persistent(Params P) {
         work_items<false>(P, kind, t, item_b, nitems, stage ? s_items : P.items + 2 * item_b,
                           stage ? s_srcs : P.srcs, stage ? src_b : 0, &s_next, lane, scol, sval,
                           flags, row_begin, t0);
-        if (tid == 0) atomicAdd(&P.ctrl->executed, 1);
+        if (tid == 0) atomicAdd(&P.ctrl->executed.v, 1);
       }
       __syncthreads();
       release = true;
     }
 
-    if (tid == 0) latched = ld_relaxed(&P.ctrl->failed) | ld_relaxed(&P.ctrl->error);
+    if (tid == 0) latched = ld_relaxed(&P.ctrl->failed.v) | ld_relaxed(&P.ctrl->error.v);
     if (release) {
       // release successors (acq_rel: publishes the writes ordered before
       // this thread by the barrier, and acquires the other predecessors'
@@ -585,14 +585,14 @@ __global__ void __launch_bounds__(THREADS) factor_persistent(Params P) {
               s_h[w] = pre ? s_succ[k - succ_b][1 + w] : P.succ[4 * k + 1 + w];
             s_pref = 1;
           } else {
-            const int slot = atomicAdd(&P.ctrl->q_tail, 1);
+            const int slot = atomicAdd(&P.ctrl->q_tail.v, 1);
             st_release(P.queue + slot, s);
           }
         }
       }
       if (tid == 0) {
         if (P.trace) P.trace[2 * t + 1] = gtimer();
-        atomicAdd(&P.ctrl->done, 1);
+        atomicAdd(&P.ctrl->done.v, 1);
       }
     } else {
       cp_async_wait_all();  // helper CTAs: retire the prefetch before smem reuse
@@ -610,10 +610,11 @@ __global__ void prepare_kernel(PrepParams Q) {
       if (Q.fin) Q.fin[k] = 0;
     }
     Q.queue[k] = k < Q.nroots ? Q.roots[k] : -1;
+    if (Q.queue2) Q.queue2[k] = -1;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     Ctrl c = {};
-    c.q_tail = Q.nroots;
+    c.q_tail.v = Q.nroots;
     c.fail_row = -1;
     *Q.ctrl = c;
   }

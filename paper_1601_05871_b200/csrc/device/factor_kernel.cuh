@@ -9,21 +9,32 @@ namespace tcbdev {
 constexpr int kChol = 0, kTrsm = 1, kHerk = 2, kGemm = 3;
 // Queue entries with this bit set are helper tickets of a multi-CTA task.
 constexpr int kHelperBit = 0x40000000;
+// Row successor entries with this bit set go to the priority queue (plan.hpp kRowHot).
+constexpr int kRowHotBit = 0x40000000;
 // Task records are three int4 (plan.hpp kTaskWords = 12).
 constexpr int kTaskInt4 = 3;
 
 // Scheduler / status words, one per factorization (reset before each run).
+// Every word that is polled or updated by many warps sits on its own
+// 128-byte line: idle pollers of one counter must not slow down the
+// atomics on another.
+struct alignas(128) Line {
+  int v;
+  int pad[31];
+};
 struct Ctrl {
-  int q_head;        // next ticket handed to a polling CTA
-  int q_tail;        // next free ready-queue slot
-  int done;          // tasks completed (released)
-  int failed;        // breakdown latch (reference factorize.hpp:146-167)
+  Line q_head;       // next ticket handed to a polling CTA / warp
+  Line q_tail;       // next free ready-queue slot
+  Line hi_head;      // row mode: priority queue tickets
+  Line hi_tail;
+  Line done;         // tasks (rows) completed
+  Line failed;       // breakdown latch (reference factorize.hpp:146-167), plus error below
+  Line error;        // 1 = watchdog expired
+  Line executed;     // task (row) bodies actually run (skipped after a breakdown)
+  Line helpers_run;  // helper tickets that joined a multi-CTA task
   int fail_row;
-  int error;         // 1 = watchdog expired
-  int executed;      // task bodies actually run (skipped after a breakdown)
-  int helpers_run;   // helper tickets that joined a multi-CTA task
+  int pad0;
   double fail_pivot;
-  unsigned long long pad1;
 };
 
 struct Params {
@@ -62,7 +73,8 @@ struct RowParams {
   const int2* upd;
   double* vals;
   int* indeg;
-  int* queue;
+  int* queue;            // FIFO of ready rows (ticket pop)
+  int* hiq;              // priority rows (rows flagged hot by the host), CAS pop
   Ctrl* ctrl;            // q_head/q_tail/done/executed count rows in this mode
   unsigned long long* trace;  // optional: {start, end} per item
   int nitems;
@@ -76,6 +88,7 @@ struct PrepParams {
   int* queue;
   int* claim;
   int* fin;
+  int* queue2;     // optional second queue (row mode priority queue), set to -1
   Ctrl* ctrl;
   int ntasks;
   int qcap;

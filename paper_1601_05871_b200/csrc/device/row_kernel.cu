@@ -72,7 +72,7 @@ __device__ __forceinline__ void row_compute(const RowParams& P, int tb, int L, i
     // kernels.hpp:49-53: pivot test, square root, row scaling
     const double piv = __shfl_sync(kFull, v, 0);
     if (!(piv > 0.0) && lane == 0) {
-      if (atomicCAS(&P.ctrl->failed, 0, 1) == 0) {
+      if (atomicCAS(&P.ctrl->failed.v, 0, 1) == 0) {
         P.ctrl->fail_row = t;
         P.ctrl->fail_pivot = piv;
       }
@@ -91,23 +91,41 @@ __device__ __forceinline__ void row_compute(const RowParams& P, int tb, int L, i
   }
 }
 
-// lane 0 only: ticket pop; -1 once every row is done or the run aborted
-__device__ __forceinline__ int pop_row(const RowParams& P, unsigned long long t0) {
-  const int ticket = atomicAdd(&P.ctrl->q_head, 1);
+// lane 0 only: next ready row, -1 once every row is done or the run aborted.
+// Rows flagged hot by the host (high on the critical path) sit in a
+// priority queue that is tried first; the bulk goes through a FIFO. Both
+// are ticket queues: a warp holds at most one ticket of each (taking a
+// priority ticket only when that queue looks non-empty) and returns
+// whichever of its two slots fills first, keeping the other ticket.
+__device__ __forceinline__ int pop_row(const RowParams& P, unsigned long long t0, int& ticket,
+                                       int& hticket) {
+  if (ticket < 0) ticket = atomicAdd(&P.ctrl->q_head.v, 1);
   unsigned spins = 0, ns = 32;
   while (true) {
+    if (hticket < 0 && ld_relaxed(&P.ctrl->hi_head.v) < ld_relaxed(&P.ctrl->hi_tail.v))
+      hticket = atomicAdd(&P.ctrl->hi_head.v, 1);
+    if (hticket >= 0 && hticket < P.nitems) {
+      const int v = ld_acquire(P.hiq + hticket);
+      if (v >= 0) {
+        hticket = -1;
+        return v;
+      }
+    }
     if (ticket < P.nitems) {
       const int v = ld_acquire(P.queue + ticket);
-      if (v >= 0) return v;
+      if (v >= 0) {
+        ticket = -1;
+        return v;
+      }
     }
     if ((spins & 7u) == 0) {
-      if (ld_relaxed(&P.ctrl->done) >= P.nitems) return -1;
-      if (ld_relaxed(&P.ctrl->error)) return -1;
+      if (ld_relaxed(&P.ctrl->done.v) >= P.nitems) return -1;
+      if (ld_relaxed(&P.ctrl->error.v)) return -1;
     }
     if (++spins == 1024u) {
       spins = 0;
       if (gtimer() - t0 > P.timeout_ns) {
-        atomicCAS(&P.ctrl->error, 0, 1);
+        atomicCAS(&P.ctrl->error.v, 0, 1);
         return -1;
       }
     }
@@ -122,19 +140,22 @@ template <int THREADS>
 __global__ void __launch_bounds__(THREADS) factor_rows(RowParams P) {
   const int lane = threadIdx.x & 31;
   const unsigned long long t0 = gtimer();
-  int cont = -1, pending_done = 0, latched = 0;
+  int cont = -1, pending_done = 0, pending_exec = 0, latched = 0, ticket = -1, hticket = -1;
   while (true) {
     int k = cont;
     cont = -1;
     if (k < 0) {
-      // going idle: publish this warp's completions first (termination test)
+      // going idle: publish this warp's completions first (termination test);
+      // the counters are per-warp sums so no global address is hit per row
       int e = 0;
       if (lane == 0) {
-        if (pending_done) atomicAdd(&P.ctrl->done, pending_done);
-        e = pop_row(P, t0);
-        latched = ld_relaxed(&P.ctrl->failed) | ld_relaxed(&P.ctrl->error);
+        if (pending_exec) atomicAdd(&P.ctrl->executed.v, pending_exec);
+        if (pending_done) atomicAdd(&P.ctrl->done.v, pending_done);
+        e = pop_row(P, t0, ticket, hticket);
+        latched = ld_relaxed(&P.ctrl->failed.v) | ld_relaxed(&P.ctrl->error.v);
       }
       pending_done = 0;
+      pending_exec = 0;
       k = __shfl_sync(kFull, e, 0);
       latched = __shfl_sync(kFull, latched, 0);
       if (k < 0) break;
@@ -153,29 +174,45 @@ __global__ void __launch_bounds__(THREADS) factor_rows(RowParams P) {
         case kTrsm: row_compute<kTrsm>(P, tb, L, dpos, soff, t, lane); break;
         default: row_compute<kHerk>(P, tb, L, dpos, soff, t, lane); break;
       }
-      if (lane == 0) atomicAdd(&P.ctrl->executed, 1);
+      ++pending_exec;
     }
-    // publish this row, then release its successors: the fence orders every
-    // lane's stores before the warp's acq_rel decrements
+    // publish this row, then release its successors. One release fence per
+    // row (fence.acq_rel + relaxed decrements form the release pattern), and
+    // one acquire fence when some successor became ready (relaxed RMW + fence
+    // is the acquire pattern; the same fence releases the queue stores).
     __threadfence();
     __syncwarp();
     int mine = -1;
     for (int j0 = sb; j0 < se; j0 += 32) {
       const int s = (j0 == sb) ? s_own : ((j0 + lane < se) ? P.succ[j0 + lane] : -1);
-      const bool ready = (s >= 0) && atom_add_acq_rel(P.indeg + s, -1) == 1;
+      const bool ready = (s >= 0) && atom_add_relaxed(P.indeg + (s & ~kRowHotBit), -1) == 1;
       unsigned m = __ballot_sync(kFull, ready);
-      if (m && mine < 0) {
+      if (!m) continue;
+      __threadfence();
+      __syncwarp();
+      if (mine < 0) {  // successor lists are sorted by falling height
         const int leader = __ffs(m) - 1;
         mine = __shfl_sync(kFull, s, leader);
         m &= m - 1;
       }
-      if (m) {
+      const unsigned hot = m & __ballot_sync(kFull, (s & kRowHotBit) != 0);
+      const unsigned cold = m & ~hot;
+      if (hot) {
         int base = 0;
-        if (lane == 0) base = atomicAdd(&P.ctrl->q_tail, __popc(m));
+        if (lane == 0) base = atomicAdd(&P.ctrl->hi_tail.v, __popc(hot));
         base = __shfl_sync(kFull, base, 0);
-        if ((m >> lane) & 1u) st_release(P.queue + base + __popc(m & ((1u << lane) - 1u)), s);
+        if ((hot >> lane) & 1u)
+          st_relaxed(P.hiq + base + __popc(hot & ((1u << lane) - 1u)), s & ~kRowHotBit);
+      }
+      if (cold) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&P.ctrl->q_tail.v, __popc(cold));
+        base = __shfl_sync(kFull, base, 0);
+        if ((cold >> lane) & 1u)
+          st_relaxed(P.queue + base + __popc(cold & ((1u << lane) - 1u)), s & ~kRowHotBit);
       }
     }
+    mine &= ~kRowHotBit;
     cont = mine;
     ++pending_done;
     if (P.trace && lane == 0) P.trace[2 * static_cast<long long>(k) + 1] = gtimer();

@@ -255,7 +255,7 @@ void build_programs(Plan& P, int threads) {
 // rows U(r,:), the Trsm divisor U(t,t)). These are exactly the block-level
 // edges of the generation walk (factorize.hpp:175-224) restricted to the
 // rows that actually interact.
-void build_item_deps(Plan& P, const RangeList& ranges) {
+void build_item_deps(Plan& P, const RangeList& ranges, double opt_hot_fraction) {
   const BlockLayout& bl = P.blocks;
   const std::size_t I = P.item_rec.size() / kItemWords;
   const std::size_t T = P.node_kind.size();
@@ -324,6 +324,25 @@ void build_item_deps(Plan& P, const RangeList& ranges) {
       P.row_succ[fill[P.item_dep[e]]++] = static_cast<std::int32_t>(k);
       ++P.row_indeg[k];
     }
+  // Scheduling priority: the height of a row (longest chain of rows still
+  // to run after it). Successor lists are sorted by falling height so that
+  // the continuation a warp keeps is the most critical ready row, and rows
+  // in the top part of the height range are flagged (kRowHot) for the
+  // device's priority queue.
+  P.row_height.assign(I, 1);
+  for (std::size_t k = I; k-- > 0;)
+    for (std::int32_t e = cnt[k]; e < cnt[k + 1]; ++e)
+      P.row_height[k] = std::max(P.row_height[k], P.row_height[P.row_succ[e]] + 1);
+  const std::int32_t hmax = I ? *std::max_element(P.row_height.begin(), P.row_height.end()) : 0;
+  const std::int32_t hot = std::max<std::int32_t>(1, static_cast<std::int32_t>(hmax * opt_hot_fraction));
+  for (std::size_t k = 0; k < I; ++k) {
+    std::sort(P.row_succ.begin() + cnt[k], P.row_succ.begin() + cnt[k + 1],
+              [&](std::int32_t x, std::int32_t y) {
+                return P.row_height[x] != P.row_height[y] ? P.row_height[x] > P.row_height[y] : x < y;
+              });
+    for (std::int32_t e = cnt[k]; e < cnt[k + 1]; ++e)
+      if (P.row_height[P.row_succ[e]] >= hot) P.row_succ[e] |= kRowHot;
+  }
   P.row_rec.assign(I * kRowWords, 0);
   P.row_roots.clear();
   for (std::size_t tk = 0; tk < T; ++tk) {
@@ -342,6 +361,9 @@ void build_item_deps(Plan& P, const RangeList& ranges) {
       if (P.row_indeg[k] == 0) P.row_roots.push_back(k);
     }
   }
+  std::stable_sort(P.row_roots.begin(), P.row_roots.end(), [&](std::int32_t x, std::int32_t y) {
+    return P.row_height[x] > P.row_height[y];
+  });
 }
 
 }  // namespace
@@ -604,7 +626,7 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
   }
 
   if (with_work && opt.programs) build_programs(P, opt.threads);
-  if (with_work) build_item_deps(P, ranges);
+  if (with_work) build_item_deps(P, ranges, opt.hot_fraction);
 
   // successors + in-degrees (edge multiplicity preserved)
   const std::size_t T = P.node_kind.size();

@@ -39,11 +39,13 @@ constexpr int kItemWords = 8;  // tb, te, local, dpos, src_b, src_e, slot_off, 0
 constexpr int kSrcWords = 4;   // dep (item position in task, Chol/Trsm; else -1), pos_rt, sb, se
 constexpr int kSuccWords = 16; // successor id, 0, 0, 0, then its 12-word task record
 constexpr int kRowWords = 8;   // row-level record: tb, te, dpos, slot_off | kind, t, succ_b, succ_e
+constexpr std::int32_t kRowHot = 0x40000000;  // row_succ flag: push to the priority queue
 
 struct PlanOptions {
   double cta_cost = 64.0;  // estimated warp-steps one CTA should get before a helper joins
   int max_width = 64;      // most CTAs cooperating on one task
   double dep_wide_cost = 64.0;  // Chol/Trsm go multi-CTA only above this cost per level
+  double hot_fraction = 0.6;    // rows with height >= this fraction of the max are "hot"
   bool programs = true;    // precompute per-row update programs (slot_rec / upd)
   int threads = 0;         // host threads for the program build (0 = all)
 };
@@ -96,7 +98,8 @@ struct Plan {
   std::vector<std::int32_t> row_rec;    // kRowWords per item
   std::vector<std::int32_t> row_succ;   // successor items, grouped per item
   std::vector<std::int32_t> row_indeg;  // dependence counters per item
-  std::vector<std::int32_t> row_roots;  // items with no dependence, ascending
+  std::vector<std::int32_t> row_roots;  // items with no dependence, by falling height
+  std::vector<std::int32_t> row_height; // longest row chain from an item to the end
   std::vector<std::int32_t> slot_rec;  // update-program slots {u_b, u_e, m0, o0} (per item: L)
   std::vector<std::int32_t> upd;       // update-program (m, o) pairs
   std::vector<std::int32_t> succ;      // successors grouped per task

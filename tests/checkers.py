@@ -345,6 +345,7 @@ def emulate_rows(plan, seed: int = 0) -> np.ndarray:
         vals[tb:te] = tv
         done += 1
         for s in succ[sb:se]:
+            s = int(s) & 0x3FFFFFFF  # drop the priority flag
             indeg[s] -= 1
             if indeg[s] == 0:
                 ready.append(int(s))

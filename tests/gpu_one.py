@@ -10,7 +10,8 @@ threads = int(sys.argv[3]) if len(sys.argv) > 3 else 256
 a, level = T.config_matrix(name)
 an = T.analyze(a, level=level)
 plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
-fz = T.GpuFactorizer(plan, T.GpuOptions(threads_per_cta=threads, timeout_s=60))
+mode = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+fz = T.GpuFactorizer(plan, T.GpuOptions(threads_per_cta=threads, timeout_s=60, mode=mode))
 for r in range(reps):
     fz.restore()
     s = fz.factor()
