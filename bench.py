@@ -1,0 +1,340 @@
+"""Benchmark of the GPU IC(k) numeric factorization (the reference's
+factor_by_blocks hot path) -- prints ONE JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one numeric factorization of the configuration's matrix, starting
+from the initialised factor U resident in HBM (the reference's
+numeric_seconds region, factorize.hpp:169-227). Between steps U is restored
+from its device copy and L2 is flushed (256 MiB write), both untimed.
+
+  value  factor-nnz/s over the whole job = N * nnz_u / (max over ranks of the
+         device time of one step); device time = CUDA events around the
+         persistent kernel on the stream it is launched on.
+  e2e    the same metric through the C ABI with host buffers: H2D of the
+         initial values from pinned memory, factor, D2H of the factor; the
+         symbolic structure (plan) stays resident, as in a refactorization.
+  roofline  algorithmic bytes 20*nnz_u + 8*(n+1) per
+         launch / kernel time, against the measured HBM copy bandwidth.
+
+N > 1 (torchrun, one process per GPU): the single-matrix configs do not
+shard, so every rank factors its own replica (weak scaling, no collective on
+the data path); timing is the max over ranks.
+
+--impl reference: times the reference's own CPU factor_by_blocks
+(oracle/_ref, compiled from the unmodified reference headers) with a pooled
+policy over all host threads, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+WORKLOADS = {
+    "c1": "C1: 2D 5-point Laplacian 100x100 (n=10,000), IC(0), fp64, ND leaf 64",
+    "c2": "C2: 3D 7-point Laplacian 64^3 (n=262,144), IC(1), fp64, ND leaf 64",
+    "c3": "C3: 3D 27-point variable-coefficient 48^3 (n=110,592), IC(2), fp64, ND leaf 64",
+    "c4": "C4: elasticity-like 40^3 x 3 dofs (n=192,000), IC(0), fp64, ND leaf 64",
+    "c5": "C5 member: 3D 7-point log-normal diffusion 32^3 (n=32,768), IC(1), fp64",
+    "c6": "C6: 3D 7-point Laplacian 128^3 (n=2,097,152), IC(1), fp64, ND leaf 64",
+}
+METRIC = "ic_numeric_factor_nnz_per_s"
+UNIT = "nnz/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(config: str):
+    """Per-launch DRAM bytes of the factor kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", f"ncu_{config}_factor.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dram_bytes_per_launch")
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def build_problem(config: str, member: int = 0):
+    import paper_1601_05871_b200 as T
+    name = "c5" if config == "c5" else config
+    a, level = T.config_matrix(name, member)
+    t0 = time.perf_counter()
+    an = T.analyze(a, level=level)
+    t_an = time.perf_counter() - t0
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    return a, an, plan, t_an
+
+
+def cpu_reference_times(an, workers: int, reps: int):
+    from checkers import Reference, reference_available
+    if not reference_available():
+        return None
+    R = Reference()
+    u = an.pattern.pattern
+    out = {"serial": [], "pool": []}
+    for _ in range(reps):
+        _, st, secs, _, _ = R.factor_serial(an.a_permuted, u)
+        out["serial"].append(secs)
+    for _ in range(reps):
+        _, st, secs, _, _, _ = R.factor_by_blocks(an.a_permuted, u, an.ranges.bounds, workers=workers,
+                                                  want_values=False)
+        out["pool"].append(secs)
+    return out
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from checkers import Reference, reference_available
+    if not reference_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref (reference compiled from /root/reference) was not built"}))
+        return
+    a, an, plan, _ = build_problem(args.config)
+    u = an.pattern.pattern
+    R = Reference()
+    cores = os.cpu_count() or 1
+    times = []
+    for i in range(args.warmup + args.steps):
+        _, st, secs, _, _, _ = R.factor_by_blocks(an.a_permuted, u, an.ranges.bounds, workers=cores,
+                                                  want_values=False)
+        if st != 0:
+            raise RuntimeError(f"reference factor_by_blocks status {st}")
+        if i >= args.warmup:
+            times.append(secs)
+    serial = [R.factor_serial(an.a_permuted, u)[2] for _ in range(3)]
+    t = statistics.mean(times)
+    nnz = u.nnz()
+    value = nnz / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config], "n": a.nrows, "nnz_u": nnz,
+                   "policy": f"TaskPolicy::pooled({cores})"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                         "sample": f"{args.steps} full factor_by_blocks runs (pooled, {cores} threads)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_factor_serial_s_median": statistics.median(serial),
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_1601_05871_b200 as T
+
+    rank, local_rank, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+
+    a, an, plan, t_an = build_problem(args.config)
+    ps = plan.stats()
+    u = an.pattern.pattern
+    nnz, n = u.nnz(), a.nrows
+    fz = T.GpuFactorizer(plan, T.GpuOptions(device=dev, mode=args.mode, timeout_s=60))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up
+    for _ in range(args.warmup):
+        fz.restore()
+        fz.factor()
+    # timed region: device time of the factor kernel per step
+    dev_ms = []
+    barrier()
+    with ClockSampler(dev) as clocks:
+        for _ in range(args.steps):
+            fz.restore()            # untimed: U <- initialised values (D2D)
+            flush.fill_(1.0)        # untimed: 256 MiB write evicts L2
+            torch.cuda.synchronize()
+            st = fz.factor()        # CUDA events around the persistent kernel
+            dev_ms.append(st.device_ms)
+    barrier()
+    step_ms = statistics.mean(dev_ms)
+    if world > 1:
+        t = torch.tensor([step_ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        step_ms = float(t.item())
+
+    # end to end through the C ABI with host buffers (pinned)
+    host_in = torch.from_numpy(plan.tables()["values"]).pin_memory()
+    host_out = torch.empty(nnz, dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    barrier()
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        fz.set_values_ptr(host_in.data_ptr())   # H2D 8*nnz_u
+        fz.factor()
+        fz.download_ptr(host_out.data_ptr())    # D2H 8*nnz_u
+        if i >= args.warmup:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    barrier()
+    e2e = statistics.mean(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(t.item())
+
+    # parity of the last factor against the oracle (small configs only, rank 0)
+    parity = None
+    if rank == 0 and nnz <= 3_000_000:
+        from checkers import Oracle
+        ref, status, _, _ = Oracle().factor_serial(an.a_permuted, u)
+        parity = "bitwise" if np.array_equal(ref.view(np.int64), host_out.numpy().view(np.int64)) \
+            else f"max_rel={float(np.max(np.abs(host_out.numpy() - ref) / (np.abs(ref) + 1e-300))):.3e}"
+
+    # CPU baseline (rank 0, N = 1): the reference's own serial factorization
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        times = cpu_reference_times(an, workers=min(os.cpu_count() or 1, 64), reps=3)
+        if times:
+            s_med = statistics.median(times["serial"])
+            cpu = {"value": nnz / s_med, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": "3 x factor_serial on the full matrix (reference's fastest CPU path), median",
+                   "factor_by_blocks_pooled_s": statistics.median(times["pool"]),
+                   "pooled_workers": min(os.cpu_count() or 1, 64)}
+    peak, peak_kind = measured_peak()
+    bytes_alg = 20 * nnz + 8 * (n + 1)
+    achieved = bytes_alg / (step_ms / 1e3) / 1e9
+    launches_per_step = st.kernel_launches
+    line = {
+        "metric": METRIC, "value": world * nnz / (step_ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md Appendix B)",
+        "config": {"workload": WORKLOADS[args.config], "n": n, "nnz_u": nnz,
+                   "tasks": int(sum(ps.tasks)), "dag_depth": int(ps.dag_depth),
+                   "rows": int(ps.items), "row_depth": int(ps.item_depth),
+                   "mode": {1: "task DAG / device merge", 2: "task DAG / update programs",
+                            3: "row-level DAG / update programs"}[st.mode],
+                   "grid_ctas": int(st.grid_ctas), "threads_per_cta": int(st.threads_per_cta),
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2": "flushed between steps (256 MiB write), U restored from device copy (untimed)",
+                   "analysis_s": round(t_an, 3), "plan_s": round(ps.plan_seconds + ps.block_build_seconds, 3),
+                   "parity_vs_oracle": parity},
+        "e2e": {"value": world * nnz / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz,
+                "d2h_bytes_per_step": 8 * nnz, "ms_per_step": e2e},
+        "gpu_launches": launches_per_step * args.steps,
+        "launches_per_step": {"prepare (untimed)": 1, "factor": 1},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(args.config),
+                     "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_alg},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    fz.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", type=int, default=0, help="0 auto, 1/2 task DAG, 3 row DAG")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warm-up raised to 3 (timing rule)")
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

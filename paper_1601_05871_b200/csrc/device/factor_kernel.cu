@@ -574,6 +574,7 @@ __global__ void __launch_bounds__(THREADS) factor_persistent(Params P) {
       // this thread by the barrier, and acquires the other predecessors'
       // writes for the thread that readies the successor)
       cp_async_wait_all();
+      if (tid == 0 && P.trace) P.trace[2 * t + 1] = gtimer();  // finished, before any release
       for (int k = succ_b + tid; k < succ_e; k += THREADS) {
         const bool pre = (k - succ_b) < kPre;
         const int s = pre ? s_succ[k - succ_b][0].x : P.succ[4 * k].x;
@@ -590,10 +591,7 @@ __global__ void __launch_bounds__(THREADS) factor_persistent(Params P) {
           }
         }
       }
-      if (tid == 0) {
-        if (P.trace) P.trace[2 * t + 1] = gtimer();
-        atomicAdd(&P.ctrl->done.v, 1);
-      }
+      if (tid == 0) atomicAdd(&P.ctrl->done.v, 1);
     } else {
       cp_async_wait_all();  // helper CTAs: retire the prefetch before smem reuse
     }

@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(THREADS) factor_rows(RowParams P) {
     // is the acquire pattern; the same fence releases the queue stores).
     __threadfence();
     __syncwarp();
+    if (P.trace && lane == 0) P.trace[2 * static_cast<long long>(k) + 1] = gtimer();  // finished
     int mine = -1;
     for (int j0 = sb; j0 < se; j0 += 32) {
       const int s = (j0 == sb) ? s_own : ((j0 + lane < se) ? P.succ[j0 + lane] : -1);
@@ -215,7 +216,6 @@ __global__ void __launch_bounds__(THREADS) factor_rows(RowParams P) {
     mine &= ~kRowHotBit;
     cont = mine;
     ++pending_done;
-    if (P.trace && lane == 0) P.trace[2 * static_cast<long long>(k) + 1] = gtimer();
   }
 }
 

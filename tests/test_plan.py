@@ -1,0 +1,126 @@
+"""Host flattener (tcg_plan_build): the DAG is bit-exact with the reference's
+export_task_dag, the block structure with build_block_matrix, and the work
+tables reproduce factor_serial bit for bit when replayed on the CPU in any
+order the dependences allow (task order, row order, random row orders)."""
+import numpy as np
+import pytest
+
+from checkers import Reference, emulate_plan, emulate_program, emulate_rows, reference_available
+from conftest import analyzed, bitwise_equal, planned
+
+FAST = ["c1", "c5_m0", "s27_16_k2", "grid20_k2_leaf4", "rand_spd_200", "elast6_k1"]
+
+
+@pytest.mark.parametrize("name", FAST + ["c2", "c3", "c4"])
+def test_plan_dag_and_blocks_match_reference(name, golden, oracle):
+    g = golden[name]
+    plan = planned(name)
+    d = plan.dag()
+    assert len(d.kind) == g["dag"]["nodes"] and len(d.edge_from) == g["dag"]["edges"]
+    for arr, key in ((d.kind, "kind"), (d.block_row, "block_row"), (d.block_col, "block_col"),
+                     (d.edge_from, "edge_from"), (d.edge_to, "edge_to")):
+        assert oracle.hash(arr) == g["dag"][key], key
+    bp, bc = plan.blocks()
+    assert len(bc) == g["blocks"]["nblocks"]
+    assert oracle.hash(bp) == g["blocks"]["brow_ptr"]
+    assert oracle.hash(bc) == g["blocks"]["bcol_idx"]
+    s = plan.stats()
+    assert list(s.tasks) == g["dag"]["tasks"]
+
+
+@pytest.mark.parametrize("name", ["c1", "s27_16_k2", "grid20_k2_leaf4", "rand_spd_200"])
+def test_replays_are_bitwise_serial(name, golden, oracle):
+    plan = planned(name)
+    _, an = analyzed(name)
+    ref, st, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
+    assert oracle.hash(ref) == golden[name]["factor_values"]
+    assert bitwise_equal(emulate_plan(plan), ref)       # device merge mode, task order
+    assert bitwise_equal(emulate_program(plan), ref)    # update programs, task order
+    for seed in range(3):                               # row-level DAG, random orders
+        assert bitwise_equal(emulate_rows(plan, seed), ref)
+
+
+def test_dag_edges_point_forward_and_task_count_formula(T):
+    # test_factorize.cpp:262-311
+    a = T.generate("grid2d", 6, 6)
+    an = T.analyze(a, level=1, leaf_size=3, treecut=1)
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    d = plan.dag()
+    assert np.all(d.edge_from < d.edge_to)
+    bp, bc = plan.blocks()
+    present = {(i, int(c)) for i in range(len(bp) - 1) for c in bc[bp[i]:bp[i + 1]]}
+    expected = 0
+    for p in range(len(bp) - 1):
+        cols = bc[bp[p]:bp[p + 1]]
+        expected += 1 + (len(cols) - 1)
+        for x in range(1, len(cols)):
+            for y in range(x, len(cols)):
+                expected += (int(cols[x]), int(cols[y])) in present
+    assert len(d.kind) == expected
+    # every TRSM(p, j) has CHOL(p, p) among its ancestors (direct edge here)
+    chol_of = {int(d.block_row[t]): t for t in range(len(d.kind)) if d.kind[t] == 0}
+    preds = {}
+    for f, t in zip(d.edge_from, d.edge_to):
+        preds.setdefault(int(t), set()).add(int(f))
+    for t in range(len(d.kind)):
+        if d.kind[t] == 1:
+            assert chol_of[int(d.block_row[t])] in preds[t]
+
+
+def test_row_dependences_are_acyclic_and_shorter(T):
+    plan = planned("c5_m0")
+    s = plan.stats()
+    assert s.item_depth < s.dag_depth  # rows shorten the critical path
+    t = plan.tables()
+    rows, succ = t["row_rec"], t["row_succ"] & 0x3FFFFFFF
+    for k in range(0, len(rows), 97):
+        assert np.all(succ[rows[k, 6]:rows[k, 7]] > k)  # generation order is topological
+    assert t["row_indeg"].sum() == len(succ)
+
+
+def test_single_range_and_diagonal_only(T, oracle):
+    a = T.generate("grid2d", 5, 5)
+    fp = T.levelk_pattern(a, 1)
+    one = T.RangeList(np.array([0, 25], dtype=np.int32))
+    plan = T.Plan(a, fp, one)
+    assert list(plan.stats().tasks) == [1, 0, 0, 0]
+    ref, _, _, _ = oracle.factor_serial(a, fp.pattern)
+    assert bitwise_equal(emulate_rows(plan), ref)
+    d = T.generate("grid2d", 1, 8)  # path-like, blocks of one vertex each
+    fp = T.levelk_pattern(d, 0)
+    plan = T.Plan(d, fp, T.RangeList(np.arange(9, dtype=np.int32)))
+    assert plan.stats().tasks[0] == 8
+
+
+def test_invalid_inputs_raise(T):
+    a = T.generate("grid2d", 4, 4)
+    an = T.analyze(a)
+    with pytest.raises(ValueError):
+        T.Plan(an.a_permuted, an.pattern, T.RangeList(np.array([0, 5, 5, 16], dtype=np.int32)))
+    # missing diagonal entry in the pattern (kernels.hpp:46-48)
+    u = an.pattern.pattern
+    cut = T.CsrMatrix.from_arrays(16, np.concatenate([[0], u.row_ptr[1:] - 1]), u.col_idx[1:])
+    with pytest.raises(ValueError):
+        T.Plan(an.a_permuted, T.FillPattern(cut), an.ranges)
+
+
+@pytest.mark.skipif(not reference_available(), reason="oracle/_ref not built here")
+@pytest.mark.parametrize("seed", range(4))
+def test_random_blockings_against_live_reference(T, oracle, seed):
+    # test_factorize.cpp:125-155 style: several blockings of one matrix
+    R = Reference()
+    rng = np.random.default_rng(seed)
+    a = T.generate("random_spd", int(rng.integers(40, 120)), 60000, seed + 3)
+    an = T.analyze(a, level=int(rng.integers(0, 3)), leaf_size=4)
+    n = a.nrows
+    for nr in (1, 3, 7):
+        step = max(1, -(-n // nr))
+        b = np.array(list(range(0, n, step)) + [n], dtype=np.int32)
+        plan = T.Plan(an.a_permuted, an.pattern, T.RangeList(b))
+        kinds, bi, bj, ef, et = R.export_dag(an.pattern.pattern, b)
+        d = plan.dag()
+        assert np.array_equal(d.kind, kinds) and np.array_equal(d.edge_from, ef)
+        assert np.array_equal(d.edge_to, et) and np.array_equal(d.block_row, bi)
+        vals, st, _, _, _, _ = R.factor_by_blocks(an.a_permuted, an.pattern.pattern, b, workers=2)
+        assert st == 0
+        assert bitwise_equal(emulate_rows(plan, seed), vals)
