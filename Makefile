@@ -21,7 +21,7 @@ CXXFLAGS := -O2 -std=c++17 -fPIC -pthread -Wall -Wextra -ffp-contract=off
 HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generators.cpp \
              $(SRC)/host/plan.cpp $(SRC)/capi.cpp
 HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
-DEV_OBJS := $(OBJ)/device/factor_kernel.o $(OBJ)/device/row_kernel.o
+DEV_OBJS := $(OBJ)/device/factor_kernel.o $(OBJ)/device/row_kernel.o $(OBJ)/device/static_kernel.o
 
 .PHONY: all lib oracle ref clean
 all: lib oracle
@@ -50,6 +50,10 @@ clean:
 	rm -rf build $(OUT)/*.so
 	$(MAKE) -C oracle clean
 
-$(OBJ)/device/row_kernel.o: $(SRC)/device/row_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh
+$(OBJ)/device/row_kernel.o: $(SRC)/device/row_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh $(SRC)/device/row_compute.cuh
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_row_kernel.txt || (cat build/ptxas_row_kernel.txt; false)
+
+$(OBJ)/device/static_kernel.o: $(SRC)/device/static_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh $(SRC)/device/row_compute.cuh
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_static_kernel.txt || (cat build/ptxas_static_kernel.txt; false)

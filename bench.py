@@ -95,7 +95,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -221,6 +221,7 @@ def run_ours(args):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(dev).__enter__()  # nvidia-smi sampling spans every measured loop
     # warm-up
     for _ in range(args.warmup):
         fz.restore()
@@ -228,13 +229,12 @@ def run_ours(args):
     # timed region: device time of the factor kernel per step
     dev_ms = []
     barrier()
-    with ClockSampler(dev) as clocks:
-        for _ in range(args.steps):
-            fz.restore()            # untimed: U <- initialised values (D2D)
-            flush.fill_(1.0)        # untimed: 256 MiB write evicts L2
-            torch.cuda.synchronize()
-            st = fz.factor()        # CUDA events around the persistent kernel
-            dev_ms.append(st.device_ms)
+    for _ in range(args.steps):
+        fz.restore()            # untimed: U <- initialised values (D2D)
+        flush.fill_(1.0)        # untimed: 256 MiB write evicts L2
+        torch.cuda.synchronize()
+        st = fz.factor()        # CUDA events around the persistent kernel
+        dev_ms.append(st.device_ms)
     barrier()
     step_ms = statistics.mean(dev_ms)
     if world > 1:
@@ -257,6 +257,7 @@ def run_ours(args):
         if i >= args.warmup:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
     barrier()
+    clocks.__exit__(None, None, None)
     e2e = statistics.mean(e2e_ms)
     if world > 1:
         t = torch.tensor([e2e], device=f"cuda:{dev}")
@@ -294,7 +295,7 @@ def run_ours(args):
                    "tasks": int(sum(ps.tasks)), "dag_depth": int(ps.dag_depth),
                    "rows": int(ps.items), "row_depth": int(ps.item_depth),
                    "mode": {1: "task DAG / device merge", 2: "task DAG / update programs",
-                            3: "row-level DAG / update programs"}[st.mode],
+                            3: "row-level DAG / ready queues", 4: "row-level DAG / static level schedule"}[st.mode],
                    "grid_ctas": int(st.grid_ctas), "threads_per_cta": int(st.threads_per_cta),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "flushed between steps (256 MiB write), U restored from device copy (untimed)",

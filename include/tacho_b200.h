@@ -91,6 +91,13 @@ typedef struct {
   const int32_t* row_indeg;    /*   dependence counters per item */
   int64_t nrow_roots;
   const int32_t* row_roots;
+  const int32_t* row_order;    /*   static schedule: items by (level, falling height) */
+  const int32_t* row_pred_ptr; /*   nitems + 1 offsets into row_pred */
+  const int32_t* row_pred;     /*   predecessor items (nrow_edges) */
+  const int32_t* pos_rec;      /*   per schedule position, 16 words: tb, L, dpos, slot_off, kind,
+                                    t, npred, pred_off, 4 inline predecessor items, item, 0,0,0 */
+  int64_t npos_pred;
+  const int32_t* pos_pred;     /*   predecessor items beyond the inline four */
 } tcg_problem;
 
 typedef struct {
@@ -99,9 +106,12 @@ typedef struct {
   int32_t staging_cap;      /* target-row entries staged per warp; 0 = auto */
   double timeout_s;         /* device watchdog; 0 = default (30 s) */
   int32_t trace;            /* 1 = record per-task start/end globaltimer stamps */
-  int32_t mode;             /* 0 = auto (3 when available), task-level DAG execution with
+  int32_t mode;             /* 0 = auto (4 when available), task-level DAG execution with
                                1 = device merge of sorted indices or 2 = precomputed update
-                               programs; 3 = row-level execution of the same DAG */
+                               programs; row-level execution of the same DAG with 3 = ready
+                               queues + counters or 4 = static level schedule + row flags */
+  int32_t lanes_per_row;    /* mode 4: lanes working on one row (4, 8, 16, 32); 0 = auto from
+                               the 90th percentile of the target row lengths */
 } tcg_options;
 
 typedef struct {
@@ -116,7 +126,9 @@ typedef struct {
   int64_t smem_bytes;
   int32_t kernel_launches;   /* device launches issued by the call */
   int64_t helpers_run;       /* helper tickets that joined a multi-CTA task */
-  int32_t mode;              /* execution mode used (1 merge, 2 programs) */
+  int32_t mode;              /* execution mode used (1 merge, 2 programs, 3 rows) */
+  uint64_t profile[7];       /* trace mode, rows: SM cycles in {pop wait, row body, publish
+                                fence, release} summed over warps; rows, pops, pushes */
 } tcg_stats;
 
 typedef struct {

@@ -61,6 +61,12 @@ class Problem(C.Structure):
         ("row_indeg", i32p),
         ("nrow_roots", C.c_int64),
         ("row_roots", i32p),
+        ("row_order", i32p),
+        ("row_pred_ptr", i32p),
+        ("row_pred", i32p),
+        ("pos_rec", i32p),
+        ("npos_pred", C.c_int64),
+        ("pos_pred", i32p),
     ]
 
 
@@ -72,6 +78,7 @@ class Options(C.Structure):
         ("timeout_s", C.c_double),
         ("trace", C.c_int32),
         ("mode", C.c_int32),
+        ("lanes_per_row", C.c_int32),
     ]
 
 
@@ -89,6 +96,7 @@ class Stats(C.Structure):
         ("kernel_launches", C.c_int32),
         ("helpers_run", C.c_int64),
         ("mode", C.c_int32),
+        ("profile", C.c_uint64 * 7),
     ]
 
 

@@ -356,6 +356,10 @@ class Plan:
             "row_succ": _copy(p.row_succ, p.nrow_edges, np.int32) if p.row_succ else np.zeros(0, np.int32),
             "row_indeg": _copy(p.row_indeg, p.nitems, np.int32) if p.row_indeg else np.zeros(0, np.int32),
             "row_roots": _copy(p.row_roots, p.nrow_roots, np.int32) if p.row_roots else np.zeros(0, np.int32),
+            "row_order": _copy(p.row_order, p.nitems, np.int32) if p.row_order else np.zeros(0, np.int32),
+            "pos_rec": (_copy(p.pos_rec, 16 * p.nitems, np.int32).reshape(-1, 16)
+                        if p.pos_rec else np.zeros((0, 16), np.int32)),
+            "pos_pred": _copy(p.pos_pred, p.npos_pred, np.int32) if p.pos_pred else np.zeros(0, np.int32),
         }
 
 
@@ -376,7 +380,8 @@ class GpuOptions:
     staging_cap: int = 0
     timeout_s: float = 0.0
     trace: bool = False
-    mode: int = 0  # 0 auto, 1 device merge, 2 host-precomputed update programs
+    mode: int = 0  # 0 auto; task DAG: 1 device merge, 2 update programs; rows: 3 queues, 4 static
+    lanes_per_row: int = 0  # mode 4 row-group width (4/8/16/32), 0 = auto
 
 
 class GpuFactorizer:
@@ -392,7 +397,8 @@ class GpuFactorizer:
             raise DeviceError(lib.tcg_last_error(None).decode())
         self.ctx = h
         o = N.Options(self.opt.threads_per_cta, self.opt.ctas_per_sm, self.opt.staging_cap,
-                      self.opt.timeout_s, 1 if self.opt.trace else 0, self.opt.mode)
+                      self.opt.timeout_s, 1 if self.opt.trace else 0, self.opt.mode,
+                      self.opt.lanes_per_row)
         self._check(lib.tcg_set_options(self.ctx, C.byref(o)))
         self.plan = plan
         self._problem = plan.problem()

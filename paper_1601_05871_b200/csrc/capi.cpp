@@ -94,6 +94,11 @@ struct tcg_ctx {
   int* row_roots = nullptr;
   std::int64_t nrow_roots = 0;
   bool has_rows = false;
+  int4* pos_rec = nullptr;  // static schedule (mode 4)
+  int* pos_pred = nullptr;
+  int* row_flag = nullptr;
+  bool has_static = false;
+  std::int64_t nslots = 0, nupdates = 0;
   tcbdev::Ctrl* ctrl = nullptr;
   unsigned long long* trace = nullptr;
   // problem shape
@@ -186,6 +191,12 @@ tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   o->row_indeg = rows ? P.row_indeg.data() : nullptr;
   o->nrow_roots = rows ? static_cast<int64_t>(P.row_roots.size()) : 0;
   o->row_roots = rows ? P.row_roots.data() : nullptr;
+  o->row_order = rows ? P.row_order.data() : nullptr;
+  o->row_pred_ptr = rows ? P.row_pred_ptr.data() : nullptr;
+  o->row_pred = rows ? P.item_dep.data() : nullptr;
+  o->pos_rec = rows ? P.pos_rec.data() : nullptr;
+  o->npos_pred = rows ? static_cast<int64_t>(P.pos_pred.size()) : 0;
+  o->pos_pred = rows ? P.pos_pred.data() : nullptr;
   return TCG_OK;
 }
 
@@ -339,6 +350,10 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_rqueue = take(rows ? sizeof(int) * p->nitems : 0);
   const size_t o_rhiq = take(rows ? sizeof(int) * p->nitems : 0);
   const size_t o_rroots = take(rows ? sizeof(int) * p->nrow_roots : 0);
+  const bool stat = rows && p->pos_rec && (p->npos_pred == 0 || p->pos_pred);
+  const size_t o_prec = take(stat ? sizeof(int4) * 4 * p->nitems : 0);
+  const size_t o_ppred = take(stat ? sizeof(int) * p->npos_pred : 0);
+  const size_t o_rflag = take(stat ? sizeof(int) * p->nitems : 0);
   const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
   const size_t o_trace = take(sizeof(unsigned long long) * (2 * p->ntasks + 4 * p->nitems));
   TCG_CUDA_TRY(c, cudaMalloc(&c->arena, off));
@@ -370,6 +385,12 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->row_roots = reinterpret_cast<int*>(base + o_rroots);
   c->nrow_roots = rows ? p->nrow_roots : 0;
   c->has_rows = rows;
+  c->pos_rec = reinterpret_cast<int4*>(base + o_prec);
+  c->pos_pred = reinterpret_cast<int*>(base + o_ppred);
+  c->row_flag = reinterpret_cast<int*>(base + o_rflag);
+  c->has_static = stat;
+  c->nslots = programs ? p->nslots : 0;
+  c->nupdates = programs ? p->nupdates : 0;
   c->ctrl = reinterpret_cast<tcbdev::Ctrl*>(base + o_ctrl);
   c->trace = reinterpret_cast<unsigned long long*>(base + o_trace);
   auto put = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
@@ -397,6 +418,11 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     TCG_CUDA_TRY(c, put(c->row_succ, p->row_succ, sizeof(int) * p->nrow_edges));
     TCG_CUDA_TRY(c, put(c->row_indeg0, p->row_indeg, sizeof(int) * p->nitems));
     TCG_CUDA_TRY(c, put(c->row_roots, p->row_roots, sizeof(int) * p->nrow_roots));
+  }
+  if (stat) {
+    TCG_CUDA_TRY(c, put(c->pos_rec, p->pos_rec, sizeof(int4) * 4 * p->nitems));
+    TCG_CUDA_TRY(c, put(c->pos_pred, p->pos_pred, sizeof(int) * p->npos_pred));
+    TCG_CUDA_TRY(c, cudaMemsetAsync(c->row_flag, 0, sizeof(int) * p->nitems, c->stream));
   }
   if (p->nitems > 0)
     TCG_CUDA_TRY(c, cudaMemsetAsync(c->iflag, 0, sizeof(int) * p->nitems, c->stream));
@@ -441,11 +467,83 @@ tcg_status tcg_restore(tcg_ctx* c) {
   return TCG_OK;
 }
 
+// Row-level execution on a static level schedule (mode 4, static_kernel.cu).
+static tcg_status run_static(tcg_ctx* c, tcg_stats& S, int threads) {
+  // gather batch: 8 products in flight per slot when slots carry several
+  // products on average, else 4 (fewer registers)
+  const int group = c->nslots > 0 && c->nupdates > 3 * c->nslots ? 8 : 4;
+  int occ = 0;
+  TCG_CUDA_TRY(c, tcbdev::static_occupancy(threads, group, &occ));
+  if (occ < 1) {
+    c->err = "static row kernel does not fit on an SM";
+    return TCG_INVALID;
+  }
+  if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
+  const int grid = std::max(1, occ * c->sm_count);
+  // counters only (no queues): reuse the prepare kernel with an empty task set
+  tcbdev::PrepParams q{};
+  q.ctrl = c->ctrl;
+  q.qcap = 0;
+  q.ntasks = 0;
+  q.nroots = 0;
+  TCG_CUDA_TRY(c, tcbdev::launch_prepare(q, c->stream));
+  tcbdev::StaticParams P{};
+  P.pos = c->pos_rec;
+  P.pos_pred = c->pos_pred;
+  P.slot_rec = c->slot_rec;
+  P.upd = c->upd;
+  P.vals = c->vals;
+  P.flag = c->row_flag;
+  P.ctrl = c->ctrl;
+  P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
+  P.nitems = static_cast<int>(c->nitems);
+  P.epoch = ++c->epoch;
+  const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
+  P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  if (c->nitems > 0) TCG_CUDA_TRY(c, tcbdev::launch_static(P, grid, threads, group, c->stream));
+  S.staging_cap = group;  // reported: gather batch
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
+                                  cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  const tcbdev::Ctrl& h = *c->host_ctrl;
+  S.device_ms = ms;
+  S.grid_ctas = grid;
+  S.threads_per_cta = threads;
+  S.kernel_launches = c->nitems > 0 ? 2 : 1;
+  S.mode = 4;
+  S.tasks_completed = (h.done.v == c->nitems) ? c->ntasks : 0;
+  S.tasks_executed = h.executed.v;
+  if (h.error.v) {
+    c->err = "device watchdog expired: the static row schedule stalled";
+    return TCG_TIMEOUT;
+  }
+  if (h.done.v != c->nitems) {
+    c->err = "static schedule finished " + std::to_string(h.done.v) + " of " +
+             std::to_string(c->nitems) + " rows";
+    return TCG_TIMEOUT;
+  }
+  if (h.failed.v) {
+    S.breakdown_row = h.fail_row;
+    S.breakdown_pivot = h.fail_pivot;
+    c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
+             std::to_string(h.fail_pivot) + " is not positive";
+    return TCG_BREAKDOWN;
+  }
+  return TCG_OK;
+}
+
 // Row-level execution (mode 3): one warp-granular persistent launch over the
 // items of the same DAG (row_kernel.cu).
 static tcg_status run_rows(tcg_ctx* c, tcg_stats& S, int threads) {
+  int minb = 0;  // register budget variant (row_kernel.cu TCG_ROW_VARIANTS)
+  if (const char* e = std::getenv("TCG_ROW_MINB")) minb = std::atoi(e);
+  else if (threads == 256) minb = 4;
   int occ = 0;
-  TCG_CUDA_TRY(c, tcbdev::rows_occupancy(threads, &occ));
+  TCG_CUDA_TRY(c, tcbdev::rows_occupancy(threads, minb, c->opt.trace != 0, &occ));
   if (occ < 1) {
     c->err = "row kernel does not fit on an SM";
     return TCG_INVALID;
@@ -482,7 +580,7 @@ static tcg_status run_rows(tcg_ctx* c, tcg_stats& S, int threads) {
   const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
-  if (c->nitems > 0) TCG_CUDA_TRY(c, tcbdev::launch_rows(P, grid, threads, c->stream));
+  if (c->nitems > 0) TCG_CUDA_TRY(c, tcbdev::launch_rows(P, grid, threads, minb, c->stream));
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
                                   cudaMemcpyDeviceToHost, c->stream));
@@ -495,6 +593,7 @@ static tcg_status run_rows(tcg_ctx* c, tcg_stats& S, int threads) {
   S.threads_per_cta = threads;
   S.kernel_launches = c->nitems > 0 ? 2 : 1;
   S.mode = 3;
+  for (int i = 0; i < 7; ++i) S.profile[i] = h.prof[i];
   // every task's rows ran (a task with no rows has no numeric work)
   S.tasks_completed = (h.done.v == c->nitems) ? c->ntasks : 0;
   S.tasks_executed = h.executed.v;  // rows whose body ran
@@ -528,12 +627,14 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
 
   const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
   int mode = c->opt.mode;
-  if (mode == 0) mode = c->has_rows ? 3 : (c->has_programs ? 2 : 1);
-  if ((mode == 2 && !c->has_programs) || (mode == 3 && !c->has_rows) || mode < 0 || mode > 3) {
+  if (mode == 0) mode = c->has_static ? 4 : c->has_rows ? 3 : (c->has_programs ? 2 : 1);
+  if ((mode == 2 && !c->has_programs) || (mode == 3 && !c->has_rows) ||
+      (mode == 4 && !c->has_static) || mode < 0 || mode > 4) {
     c->err = "requested execution mode is not available for the uploaded problem";
     return TCG_INVALID;
   }
   if (mode == 3) return run_rows(c, S, threads);
+  if (mode == 4) return run_static(c, S, threads);
   int flag_words = (c->max_flag_rows + 31) / 32;
   flag_words = (flag_words + 3) & ~3;
   int cap = c->opt.staging_cap;

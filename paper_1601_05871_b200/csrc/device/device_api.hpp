@@ -14,7 +14,10 @@ cudaError_t factor_occupancy(int threads, size_t smem, int* ctas_per_sm);
 cudaError_t launch_prepare(const PrepParams& q, cudaStream_t st);
 cudaError_t launch_factor(const Params& p, int grid, int threads, size_t smem, cudaStream_t st);
 
-cudaError_t rows_occupancy(int threads, int* ctas_per_sm);
-cudaError_t launch_rows(const RowParams& p, int grid, int threads, cudaStream_t st);
+cudaError_t rows_occupancy(int threads, int minb, bool prof, int* ctas_per_sm);
+cudaError_t launch_rows(const RowParams& p, int grid, int threads, int minb, cudaStream_t st);
+
+cudaError_t static_occupancy(int threads, int group, int* ctas_per_sm);
+cudaError_t launch_static(const StaticParams& p, int grid, int threads, int group, cudaStream_t st);
 
 }  // namespace tcbdev

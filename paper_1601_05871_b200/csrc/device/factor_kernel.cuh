@@ -35,6 +35,9 @@ struct Ctrl {
   int fail_row;
   int pad0;
   double fail_pivot;
+  // trace mode, row kernel: per-phase SM cycles summed over warps
+  // {pop wait, row body, publish fence, release, rows, pops, pushes, 0}
+  unsigned long long prof[8];
 };
 
 struct Params {
@@ -78,6 +81,22 @@ struct RowParams {
   Ctrl* ctrl;            // q_head/q_tail/done/executed count rows in this mode
   unsigned long long* trace;  // optional: {start, end} per item
   int nitems;
+  unsigned long long timeout_ns;
+};
+
+// Static row schedule (mode 4, static_kernel.cu).
+struct StaticParams {
+  const int4* pos;       // 4 x int4 per schedule position (plan.hpp kPosWords); positions are
+                         // rows by (level, falling height): a topological order
+  const int* pos_pred;   // predecessor items beyond the 4 inline ones
+  const int4* slot_rec;
+  const int2* upd;
+  double* vals;
+  int* flag;             // per item: epoch stamp once its row is final
+  Ctrl* ctrl;
+  unsigned long long* trace;  // optional: {start, end} per item
+  int nitems;
+  int epoch;
   unsigned long long timeout_ns;
 };
 

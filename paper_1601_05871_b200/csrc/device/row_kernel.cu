@@ -22,74 +22,12 @@
 #include <cuda_runtime.h>
 
 #include "factor_kernel.cuh"
+#include "row_compute.cuh"
 #include "sync.cuh"
 
 namespace tcbdev {
 
 namespace {
-
-__device__ __forceinline__ double row_slot(const RowParams& P, double v, const int4 sr) {
-  const int ub = sr.x, ue = sr.y;
-  if (ub >= ue) return v;
-  const double a0 = P.vals[sr.z], b0 = P.vals[sr.w];
-  constexpr int kB = 8;
-  int u = ub + 1;
-  int2 p[kB];
-#pragma unroll
-  for (int j = 0; j < kB; ++j) p[j] = (u + j < ue) ? P.upd[u + j] : make_int2(0, 0);
-  v = __dsub_rn(v, __dmul_rn(a0, b0));
-  while (u < ue) {
-    const int n = min(kB, ue - u);
-    double a[kB], b[kB];
-#pragma unroll
-    for (int j = 0; j < kB; ++j) {
-      a[j] = (j < n) ? P.vals[p[j].x] : 0.0;
-      b[j] = (j < n) ? P.vals[p[j].y] : 0.0;
-    }
-    u += kB;
-#pragma unroll
-    for (int j = 0; j < kB; ++j) p[j] = (u + j < ue) ? P.upd[u + j] : make_int2(0, 0);
-#pragma unroll
-    for (int j = 0; j < kB; ++j)
-      if (j < n) v = __dsub_rn(v, __dmul_rn(a[j], b[j]));
-  }
-  return v;
-}
-
-template <int KIND>
-__device__ __forceinline__ void row_compute(const RowParams& P, int tb, int L, int dpos, int soff,
-                                            int t, int lane) {
-  double v = 0.0;
-  int4 sr = make_int4(0, 0, 0, 0);
-  if (lane < L) {
-    v = P.vals[tb + lane];
-    sr = P.slot_rec[soff + lane];
-  }
-  double d = 1.0;
-  if (KIND == kTrsm) d = P.vals[dpos];
-  if (lane < L) v = row_slot(P, v, sr);
-  if (KIND == kChol) {
-    // kernels.hpp:49-53: pivot test, square root, row scaling
-    const double piv = __shfl_sync(kFull, v, 0);
-    if (!(piv > 0.0) && lane == 0) {
-      if (atomicCAS(&P.ctrl->failed.v, 0, 1) == 0) {
-        P.ctrl->fail_row = t;
-        P.ctrl->fail_pivot = piv;
-      }
-    }
-    d = __dsqrt_rn(piv);
-  }
-  auto finish = [&](int k, double x) {
-    if (KIND == kChol) return k == 0 ? d : __ddiv_rn(x, d);
-    if (KIND == kTrsm) return __ddiv_rn(x, d);  // kernels.hpp:76-78
-    return x;
-  };
-  if (lane < L) P.vals[tb + lane] = finish(lane, v);
-  for (int k = lane + 32; k < L; k += 32) {
-    const double w = row_slot(P, P.vals[tb + k], P.slot_rec[soff + k]);
-    P.vals[tb + k] = finish(k, w);
-  }
-}
 
 // lane 0 only: next ready row, -1 once every row is done or the run aborted.
 // Rows flagged hot by the host (high on the critical path) sit in a
@@ -136,14 +74,17 @@ __device__ __forceinline__ int pop_row(const RowParams& P, unsigned long long t0
 
 }  // namespace
 
-template <int THREADS>
-__global__ void __launch_bounds__(THREADS) factor_rows(RowParams P) {
+template <int THREADS, int MINB, bool PROF>
+__global__ void __launch_bounds__(THREADS, MINB) factor_rows(RowParams P) {
   const int lane = threadIdx.x & 31;
   const unsigned long long t0 = gtimer();
   int cont = -1, pending_done = 0, pending_exec = 0, latched = 0, ticket = -1, hticket = -1;
+  constexpr bool prof = PROF;
+  unsigned long long acc[7] = {0, 0, 0, 0, 0, 0, 0}, c0 = 0, c1 = 0;
   while (true) {
     int k = cont;
     cont = -1;
+    if (prof) c0 = clock64();
     if (k < 0) {
       // going idle: publish this warp's completions first (termination test);
       // the counters are per-warp sums so no global address is hit per row
@@ -158,6 +99,12 @@ __global__ void __launch_bounds__(THREADS) factor_rows(RowParams P) {
       pending_exec = 0;
       k = __shfl_sync(kFull, e, 0);
       latched = __shfl_sync(kFull, latched, 0);
+      if (prof) {
+        acc[5] += 1;
+        c1 = clock64();
+        acc[0] += c1 - c0;
+        c0 = c1;
+      }
       if (k < 0) break;
     }
     __syncwarp();  // lane 0's acquire (pop) or the readying lane's (continuation) covers the warp
@@ -165,16 +112,24 @@ __global__ void __launch_bounds__(THREADS) factor_rows(RowParams P) {
     const int4 b = P.rows[2 * k + 1];
     const int tb = a.x, L = a.y - a.x, dpos = a.z, soff = a.w;
     const int kind = b.x, t = b.y, sb = b.z, se = b.w;
-    // successor ids stream in while the row is computed
+    // successor ids and the first slot record stream in together
     int s_own = (sb + lane < se) ? P.succ[sb + lane] : -1;
+    int4 sr0 = make_int4(0, 0, 0, 0);
+    if (lane < L) sr0 = P.slot_rec[soff + lane];
     if (P.trace && lane == 0) P.trace[2 * static_cast<long long>(k)] = gtimer();
     if (!latched) {
       switch (kind) {
-        case kChol: row_compute<kChol>(P, tb, L, dpos, soff, t, lane); break;
-        case kTrsm: row_compute<kTrsm>(P, tb, L, dpos, soff, t, lane); break;
-        default: row_compute<kHerk>(P, tb, L, dpos, soff, t, lane); break;
+        case kChol: row_compute<kChol>(P.slot_rec, P.upd, P.vals, P.ctrl, tb, L, dpos, soff, t, lane, sr0); break;
+        case kTrsm: row_compute<kTrsm>(P.slot_rec, P.upd, P.vals, P.ctrl, tb, L, dpos, soff, t, lane, sr0); break;
+        default: row_compute<kHerk>(P.slot_rec, P.upd, P.vals, P.ctrl, tb, L, dpos, soff, t, lane, sr0); break;
       }
       ++pending_exec;
+    }
+    if (prof) {
+      __syncwarp();
+      c1 = clock64();
+      acc[1] += c1 - c0;
+      c0 = c1;
     }
     // publish this row, then release its successors. One release fence per
     // row (fence.acq_rel + relaxed decrements form the release pattern), and
@@ -182,6 +137,11 @@ __global__ void __launch_bounds__(THREADS) factor_rows(RowParams P) {
     // is the acquire pattern; the same fence releases the queue stores).
     __threadfence();
     __syncwarp();
+    if (prof) {
+      c1 = clock64();
+      acc[2] += c1 - c0;
+      c0 = c1;
+    }
     if (P.trace && lane == 0) P.trace[2 * static_cast<long long>(k) + 1] = gtimer();  // finished
     int mine = -1;
     for (int j0 = sb; j0 < se; j0 += 32) {
@@ -212,36 +172,55 @@ __global__ void __launch_bounds__(THREADS) factor_rows(RowParams P) {
         if ((cold >> lane) & 1u)
           st_relaxed(P.queue + base + __popc(cold & ((1u << lane) - 1u)), s & ~kRowHotBit);
       }
+      if (prof) acc[6] += __popc(hot) + __popc(cold);
     }
     mine &= ~kRowHotBit;
     cont = mine;
     ++pending_done;
+    if (prof) {
+      c1 = clock64();
+      acc[3] += c1 - c0;
+      acc[4] += 1;
+    }
   }
+  if (prof && lane == 0)
+    for (int i = 0; i < 7; ++i) atomicAdd(&P.ctrl->prof[i], acc[i]);
 }
 
-static const void* row_kernel_for(int threads) {
-  switch (threads) {
-    case 128: return reinterpret_cast<const void*>(&factor_rows<128>);
-    case 256: return reinterpret_cast<const void*>(&factor_rows<256>);
-    case 512: return reinterpret_cast<const void*>(&factor_rows<512>);
-    default: return nullptr;
-  }
+// Variants: block size x register budget (MINB = CTAs per SM the register
+// allocation must allow; 0 = compiler's choice) x phase profiling.
+#define TCG_ROW_VARIANTS(X) \
+  X(128, 0) X(256, 0) X(256, 3) X(256, 4) X(256, 5) X(256, 6) X(512, 0)
+
+static const void* row_kernel_for(int threads, int minb, bool prof) {
+#define X(T, M)                                                                       \
+  if (threads == T && minb == M)                                                      \
+    return prof ? reinterpret_cast<const void*>(&factor_rows<T, M, true>)             \
+                : reinterpret_cast<const void*>(&factor_rows<T, M, false>);
+  TCG_ROW_VARIANTS(X)
+#undef X
+  return nullptr;
 }
 
-cudaError_t rows_occupancy(int threads, int* ctas_per_sm) {
-  const void* k = row_kernel_for(threads);
+cudaError_t rows_occupancy(int threads, int minb, bool prof, int* ctas_per_sm) {
+  const void* k = row_kernel_for(threads, minb, prof);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
 }
 
-cudaError_t launch_rows(const RowParams& p, int grid, int threads, cudaStream_t st) {
-  switch (threads) {
-    case 128: factor_rows<128><<<grid, 128, 0, st>>>(p); break;
-    case 256: factor_rows<256><<<grid, 256, 0, st>>>(p); break;
-    case 512: factor_rows<512><<<grid, 512, 0, st>>>(p); break;
-    default: return cudaErrorInvalidValue;
+cudaError_t launch_rows(const RowParams& p, int grid, int threads, int minb, cudaStream_t st) {
+  const bool prof = p.trace != nullptr;
+#define X(T, M)                                                      \
+  if (threads == T && minb == M) {                                   \
+    if (prof)                                                        \
+      factor_rows<T, M, true><<<grid, T, 0, st>>>(p);                \
+    else                                                             \
+      factor_rows<T, M, false><<<grid, T, 0, st>>>(p);               \
+    return cudaGetLastError();                                       \
   }
-  return cudaGetLastError();
+  TCG_ROW_VARIANTS(X)
+#undef X
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace tcbdev

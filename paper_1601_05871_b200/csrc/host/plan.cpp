@@ -310,6 +310,7 @@ void build_item_deps(Plan& P, const RangeList& ranges, double opt_hot_fraction) 
   }
   P.stats.item_edges = static_cast<std::int64_t>(P.item_dep.size());
   P.stats.item_depth = I ? *std::max_element(depth.begin(), depth.end()) : 0;
+  P.row_level = depth;
 
   // device tables of the row-level mode: successor CSR, counters, roots and
   // a self-contained record per row {tb, te, dpos, slot_off | kind, t, succ_b, succ_e}
@@ -364,6 +365,51 @@ void build_item_deps(Plan& P, const RangeList& ranges, double opt_hot_fraction) 
   std::stable_sort(P.row_roots.begin(), P.row_roots.end(), [&](std::int32_t x, std::int32_t y) {
     return P.row_height[x] > P.row_height[y];
   });
+
+  // static schedule (mode 4): rows by level (a topological order), most
+  // critical first within a level; warp w of W takes positions w, w+W, ...
+  P.row_order.resize(I);
+  for (std::size_t k = 0; k < I; ++k) P.row_order[k] = static_cast<std::int32_t>(k);
+  std::stable_sort(P.row_order.begin(), P.row_order.end(), [&](std::int32_t x, std::int32_t y) {
+    if (P.row_level[x] != P.row_level[y]) return P.row_level[x] < P.row_level[y];
+    return P.row_height[x] > P.row_height[y];
+  });
+  P.row_pred_ptr.resize(I + 1);
+  for (std::size_t k = 0; k <= I; ++k) P.row_pred_ptr[k] = static_cast<std::int32_t>(P.item_dep_ptr[k]);
+
+  // Position-ordered records for the static schedule: everything a warp
+  // needs for the row at position q in one 64-byte record. Predecessors are
+  // named by item id (the first kPosInline inline, the rest in pos_pred):
+  // the row stamps are indexed by item, which scatters the stamps of rows
+  // that run at the same time over different cache lines (positions would
+  // pack 32 concurrently written stamps into one line).
+  std::vector<std::int32_t> pos_of(I);
+  for (std::size_t q = 0; q < I; ++q) pos_of[P.row_order[q]] = static_cast<std::int32_t>(q);
+  P.pos_rec.assign(I * kPosWords, -1);
+  P.pos_pred.clear();
+  for (std::size_t q = 0; q < I; ++q) {
+    const std::int32_t k = P.row_order[q];
+    const std::int32_t* r = &P.row_rec[static_cast<std::size_t>(k) * kRowWords];
+    std::int32_t* o = &P.pos_rec[q * kPosWords];
+    o[0] = r[0];
+    o[1] = r[1] - r[0];
+    o[2] = r[2];
+    o[3] = r[3];
+    o[4] = r[4];
+    o[5] = r[5];
+    const std::int64_t pb = P.item_dep_ptr[k], pe = P.item_dep_ptr[k + 1];
+    o[6] = static_cast<std::int32_t>(pe - pb);
+    o[7] = static_cast<std::int32_t>(P.pos_pred.size());
+    o[12] = k;
+    for (std::int64_t e = pb; e < pe; ++e) {
+      const std::int32_t d = P.item_dep[e];
+      if (pos_of[d] >= static_cast<std::int32_t>(q)) throw std::logic_error("plan: schedule not topological");
+      if (e - pb < kPosInline)
+        o[8 + (e - pb)] = d;
+      else
+        P.pos_pred.push_back(d);
+    }
+  }
 }
 
 }  // namespace

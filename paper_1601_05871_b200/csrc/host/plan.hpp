@@ -40,6 +40,10 @@ constexpr int kSrcWords = 4;   // dep (item position in task, Chol/Trsm; else -1
 constexpr int kSuccWords = 16; // successor id, 0, 0, 0, then its 12-word task record
 constexpr int kRowWords = 8;   // row-level record: tb, te, dpos, slot_off | kind, t, succ_b, succ_e
 constexpr std::int32_t kRowHot = 0x40000000;  // row_succ flag: push to the priority queue
+// static schedule record per position: tb, L, dpos, slot_off | kind, t, npred, pred_off |
+// first kPosInline predecessor items (-1 = none) | item id, 0, 0, 0
+constexpr int kPosWords = 16;
+constexpr int kPosInline = 4;
 
 struct PlanOptions {
   double cta_cost = 64.0;  // estimated warp-steps one CTA should get before a helper joins
@@ -100,6 +104,11 @@ struct Plan {
   std::vector<std::int32_t> row_indeg;  // dependence counters per item
   std::vector<std::int32_t> row_roots;  // items with no dependence, by falling height
   std::vector<std::int32_t> row_height; // longest row chain from an item to the end
+  std::vector<std::int32_t> row_level;  // longest row chain from a root to the item (1-based)
+  std::vector<std::int32_t> row_order;  // static schedule: rows by (level, falling height)
+  std::vector<std::int32_t> row_pred_ptr;  // int32 copy of item_dep_ptr (preds = item_dep)
+  std::vector<std::int32_t> pos_rec;   // kPosWords per schedule position
+  std::vector<std::int32_t> pos_pred;  // predecessor items beyond the inline ones
   std::vector<std::int32_t> slot_rec;  // update-program slots {u_b, u_e, m0, o0} (per item: L)
   std::vector<std::int32_t> upd;       // update-program (m, o) pairs
   std::vector<std::int32_t> succ;      // successors grouped per task

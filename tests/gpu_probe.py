@@ -9,8 +9,8 @@ from checkers import Oracle
 
 kv = dict(a.split("=") for a in sys.argv[1:] if "=" in a)
 names = [a for a in sys.argv[1:] if "=" not in a] or ["c1", "c2"]
-threads, ctas, cap, reps, mode = (int(kv.get(k, d)) for k, d in
-                            (("threads", 256), ("ctas", 0), ("cap", 0), ("reps", 6), ("mode", 0)))
+threads, ctas, cap, reps, mode, lanes = (int(kv.get(k, d)) for k, d in
+                            (("threads", 256), ("ctas", 0), ("cap", 0), ("reps", 6), ("mode", 0), ("lanes", 0)))
 O = Oracle()
 for name in names:
     a, level = T.config_matrix(name)
@@ -19,7 +19,7 @@ for name in names:
     plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
     ref, st, _, _ = O.factor_serial(an.a_permuted, u)
     fz = T.GpuFactorizer(plan, T.GpuOptions(threads_per_cta=threads, ctas_per_sm=ctas,
-                                            staging_cap=cap, timeout_s=20, mode=mode))
+                                            staging_cap=cap, timeout_s=20, mode=mode, lanes_per_row=lanes))
     times = []
     for rep in range(reps):
         fz.restore()

@@ -40,10 +40,31 @@ def check_against_oracle(name, vals, golden, oracle):
 
 @pytest.mark.parametrize("name", ["c1", "c5_m0", "c5_m63", "s27_16_k2", "grid20_k2_leaf4",
                                   "rand_spd_200", "elast6_k1", "c2", "c3", "c4"])
-def test_configs_row_mode(T, golden, oracle, name):
-    vals, st = gpu_factor(T, planned(name), mode=3)
-    assert st.mode == 3
+@pytest.mark.parametrize("mode", [3, 4])
+def test_configs_row_modes(T, golden, oracle, name, mode):  # noqa: D103
+    vals, st = gpu_factor(T, planned(name), mode=mode)
+    assert st.mode == mode
     check_against_oracle(name, vals, golden, oracle)
+
+
+def test_default_mode_is_static_rows(T):
+    _, st = gpu_factor(T, planned("c1"))
+    assert st.mode == 4
+
+
+def test_static_trace_respects_every_row_edge(T):
+    # mode 4: stamps per row; every predecessor finishes before the row starts
+    plan = planned("c5_m0")
+    fz = T.GpuFactorizer(plan, T.GpuOptions(mode=4, trace=True))
+    fz.factor()
+    _, items = fz.trace()
+    fz.close()
+    t = plan.tables()
+    ni = len(t["row_rec"])
+    st = items.reshape(-1)[:2 * ni].reshape(-1, 2)
+    rows, succ = t["row_rec"], t["row_succ"] & 0x3FFFFFFF
+    src = np.repeat(np.arange(ni), rows[:, 7] - rows[:, 6])
+    assert np.all(st[src, 1] <= st[succ, 0])
 
 
 @pytest.mark.parametrize("mode", [1, 2])
@@ -91,7 +112,7 @@ def sym(entries):
     return entries + [(j, i, v) for i, j, v in entries if i != j]
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
 def test_known_answers(T, mode):
     # test_factorize.cpp:78-97 and test_kernels.cpp:36-57
     opt = T.GpuOptions(mode=mode)
@@ -108,7 +129,7 @@ def test_known_answers(T, mode):
     assert v[0] == 2.0 and v[1] == 1.0 and v[2] == math.sqrt(2.0)
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
 def test_breakdown_reports_row_and_pivot(T, mode):
     # test_factorize.cpp:99-108,157-165 and test_kernels.cpp:62-76
     opt = T.GpuOptions(mode=mode)
@@ -137,7 +158,7 @@ def test_random_spd_many_blockings(T, oracle, seed):
         step = max(1, -(-n // nr))
         b = np.array(list(range(0, n, step)) + [n], dtype=np.int32)
         plan = T.Plan(an.a_permuted, an.pattern, T.RangeList(b))
-        for mode in (1, 2, 3):
+        for mode in (1, 2, 3, 4):
             vals, _ = gpu_factor(T, plan, mode=mode)
             assert bitwise_equal(vals, ref), (nr, mode)
 
@@ -220,7 +241,7 @@ def test_refactor_with_new_values_and_determinism(T, oracle):
 def test_cta_sizes_agree(T, threads):
     plan = planned("s27_16_k2")
     base, _ = gpu_factor(T, plan)
-    for mode in (1, 2, 3):
+    for mode in (1, 2, 3, 4):
         vals, st = gpu_factor(T, plan, mode=mode, threads_per_cta=threads)
         assert st.threads_per_cta == threads
         assert bitwise_equal(vals, base)

@@ -40,6 +40,42 @@ def test_replays_are_bitwise_serial(name, golden, oracle):
         assert bitwise_equal(emulate_rows(plan, seed), ref)
 
 
+@pytest.mark.parametrize("name", ["c1", "s27_16_k2", "rand_spd_200"])
+def test_static_schedule_is_topological_and_replays_bitwise(name, oracle):
+    # mode 4: rows in position order; every predecessor sits at an earlier position
+    plan = planned(name)
+    t = plan.tables()
+    order, pos, extra = t["row_order"], t["pos_rec"], t["pos_pred"]
+    pos_of = np.empty(len(order), np.int64)
+    pos_of[order] = np.arange(len(order))
+    for q in range(len(order)):
+        rec = pos[q]
+        assert rec[12] == order[q]
+        preds = [p for p in rec[8:8 + min(4, rec[6])]] + list(extra[rec[7]:rec[7] + max(0, rec[6] - 4)])
+        assert len(preds) == rec[6]
+        assert all(pos_of[p] < q for p in preds)
+    # replay in position order == serial
+    _, an = analyzed(name)
+    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
+    vals = t["values"].copy()
+    srec, upd, rows = t["slot_rec"], t["upd"], t["row_rec"]
+    for k in order:
+        tb, te, dpos, soff, kind = rows[k][:5]
+        tv = vals[tb:te].copy()
+        for j in range(te - tb):
+            ub, ue, _, _ = srec[soff + j]
+            for u in range(ub, ue):
+                tv[j] = tv[j] - vals[upd[u][0]] * vals[upd[u][1]]
+        if kind == 0:
+            d = np.sqrt(tv[0])
+            tv[1:] = tv[1:] / d
+            tv[0] = d
+        elif kind == 1:
+            tv = tv / vals[dpos]
+        vals[tb:te] = tv
+    assert bitwise_equal(vals, ref)
+
+
 def test_dag_edges_point_forward_and_task_count_formula(T):
     # test_factorize.cpp:262-311
     a = T.generate("grid2d", 6, 6)
