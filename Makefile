@@ -21,14 +21,16 @@ CXXFLAGS := -O2 -std=c++17 -fPIC -pthread -Wall -Wextra -ffp-contract=off
 HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generators.cpp \
              $(SRC)/host/plan.cpp $(SRC)/capi.cpp
 HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
-DEV_OBJS := $(OBJ)/device/factor_kernel.o $(OBJ)/device/row_kernel.o $(OBJ)/device/static_kernel.o
+DEV_OBJS := $(OBJ)/device/factor_kernel.o $(OBJ)/device/row_kernel.o $(OBJ)/device/static_kernel.o \
+            $(OBJ)/device/flow_kernel.o
 
 .PHONY: all lib oracle ref clean
 all: lib oracle
 
 lib: $(OUT)/libtacho_b200.so
 
-$(OBJ)/%.o: $(SRC)/%.cpp $(wildcard $(SRC)/host/*.hpp) include/tacho_b200.h
+$(OBJ)/%.o: $(SRC)/%.cpp $(wildcard $(SRC)/host/*.hpp) $(SRC)/device/device_api.hpp \
+            $(SRC)/device/factor_kernel.cuh include/tacho_b200.h
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -I/usr/local/cuda/include -c $< -o $@
 
@@ -57,3 +59,7 @@ $(OBJ)/device/row_kernel.o: $(SRC)/device/row_kernel.cu $(SRC)/device/factor_ker
 $(OBJ)/device/static_kernel.o: $(SRC)/device/static_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh $(SRC)/device/row_compute.cuh
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_static_kernel.txt || (cat build/ptxas_static_kernel.txt; false)
+
+$(OBJ)/device/flow_kernel.o: $(SRC)/device/flow_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_flow_kernel.txt || (cat build/ptxas_flow_kernel.txt; false)

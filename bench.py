@@ -295,7 +295,9 @@ def run_ours(args):
                    "tasks": int(sum(ps.tasks)), "dag_depth": int(ps.dag_depth),
                    "rows": int(ps.items), "row_depth": int(ps.item_depth),
                    "mode": {1: "task DAG / device merge", 2: "task DAG / update programs",
-                            3: "row-level DAG / ready queues", 4: "row-level DAG / static level schedule"}[st.mode],
+                            3: "row-level DAG / ready queues", 4: "row-level DAG / static level schedule",
+                            5: "value flow / static schedule of the finalising rows"}[st.mode],
+                   "flow_rows": int(ps.flow_rows), "flow_depth": int(ps.flow_depth),
                    "grid_ctas": int(st.grid_ctas), "threads_per_cta": int(st.threads_per_cta),
                    "parallelism": f"replicas{world}" if world > 1 else "single",
                    "l2": "flushed between steps (256 MiB write), U restored from device copy (untimed)",

@@ -98,6 +98,14 @@ typedef struct {
                                     t, npred, pred_off, 4 inline predecessor items, item, 0,0,0 */
   int64_t npos_pred;
   const int32_t* pos_pred;     /*   predecessor items beyond the inline four */
+  /* value-flow execution (optional; mode 5): the Chol/Trsm items, each applying every
+   * update of its slice, in a static (level, falling height) order */
+  int64_t nflow;
+  const int32_t* flow_rec;     /*   4 words per position: tb, L | kind << 30, dpos, t */
+  const int32_t* flow_item;    /*   per position: its item (trace stamps are per item) */
+  const int32_t* flow_slot;    /*   4 words per coordinate of U: u_b, u_e, m0, o0 */
+  int64_t nflow_upd;
+  const int32_t* flow_upd;     /*   (m, o) pairs */
 } tcg_problem;
 
 typedef struct {
@@ -106,12 +114,14 @@ typedef struct {
   int32_t staging_cap;      /* target-row entries staged per warp; 0 = auto */
   double timeout_s;         /* device watchdog; 0 = default (30 s) */
   int32_t trace;            /* 1 = record per-task start/end globaltimer stamps */
-  int32_t mode;             /* 0 = auto (4 when available), task-level DAG execution with
+  int32_t mode;             /* 0 = auto (5 when available), task-level DAG execution with
                                1 = device merge of sorted indices or 2 = precomputed update
                                programs; row-level execution of the same DAG with 3 = ready
-                               queues + counters or 4 = static level schedule + row flags */
-  int32_t lanes_per_row;    /* mode 4: lanes working on one row (4, 8, 16, 32); 0 = auto from
-                               the 90th percentile of the target row lengths */
+                               queues + counters, 4 = static level schedule + row flags or
+                               5 = static schedule of the finalising rows, readers polling
+                               the values themselves (no flags, no fences) */
+  int32_t lanes_per_row;    /* mode 5: lanes working on one row (32, or 8 with 256 threads);
+                               0 = default (32) */
 } tcg_options;
 
 typedef struct {
@@ -126,9 +136,10 @@ typedef struct {
   int64_t smem_bytes;
   int32_t kernel_launches;   /* device launches issued by the call */
   int64_t helpers_run;       /* helper tickets that joined a multi-CTA task */
-  int32_t mode;              /* execution mode used (1 merge, 2 programs, 3 rows) */
+  int32_t mode;              /* execution mode used (1 .. 5, see tcg_options.mode) */
   uint64_t profile[7];       /* trace mode, rows: SM cycles in {pop wait, row body, publish
                                 fence, release} summed over warps; rows, pops, pushes */
+  int32_t lanes_per_row;     /* mode 5: lanes per row used */
 } tcg_stats;
 
 typedef struct {
@@ -143,6 +154,8 @@ typedef struct {
   int32_t nblocks_rows;      /* block rows m (= number of ranges) */
   int64_t nblocks;
   double block_build_seconds, plan_seconds;
+  int64_t flow_rows;         /* value-flow rows (mode 5) */
+  int32_t flow_depth;        /* longest value-flow chain, in rows */
 } tcg_plan_stats;
 
 /* ---- host flattener ---------------------------------------------------- */

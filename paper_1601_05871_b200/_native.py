@@ -67,6 +67,12 @@ class Problem(C.Structure):
         ("pos_rec", i32p),
         ("npos_pred", C.c_int64),
         ("pos_pred", i32p),
+        ("nflow", C.c_int64),
+        ("flow_rec", i32p),
+        ("flow_item", i32p),
+        ("flow_slot", i32p),
+        ("nflow_upd", C.c_int64),
+        ("flow_upd", i32p),
     ]
 
 
@@ -97,6 +103,7 @@ class Stats(C.Structure):
         ("helpers_run", C.c_int64),
         ("mode", C.c_int32),
         ("profile", C.c_uint64 * 7),
+        ("lanes_per_row", C.c_int32),
     ]
 
 
@@ -120,6 +127,8 @@ class PlanStats(C.Structure):
         ("nblocks", C.c_int64),
         ("block_build_seconds", C.c_double),
         ("plan_seconds", C.c_double),
+        ("flow_rows", C.c_int64),
+        ("flow_depth", C.c_int32),
     ]
 
 

@@ -360,6 +360,13 @@ class Plan:
             "pos_rec": (_copy(p.pos_rec, 16 * p.nitems, np.int32).reshape(-1, 16)
                         if p.pos_rec else np.zeros((0, 16), np.int32)),
             "pos_pred": _copy(p.pos_pred, p.npos_pred, np.int32) if p.pos_pred else np.zeros(0, np.int32),
+            "flow_rec": (_copy(p.flow_rec, 4 * p.nflow, np.int32).reshape(-1, 4)
+                         if p.flow_rec else np.zeros((0, 4), np.int32)),
+            "flow_item": _copy(p.flow_item, p.nflow, np.int32) if p.flow_item else np.zeros(0, np.int32),
+            "flow_slot": (_copy(p.flow_slot, 4 * p.nnz, np.int32).reshape(-1, 4)
+                          if p.flow_slot else np.zeros((0, 4), np.int32)),
+            "flow_upd": (_copy(p.flow_upd, 2 * p.nflow_upd, np.int32).reshape(-1, 2)
+                         if p.flow_upd else np.zeros((0, 2), np.int32)),
         }
 
 
@@ -380,7 +387,8 @@ class GpuOptions:
     staging_cap: int = 0
     timeout_s: float = 0.0
     trace: bool = False
-    mode: int = 0  # 0 auto; task DAG: 1 device merge, 2 update programs; rows: 3 queues, 4 static
+    mode: int = 0  # 0 auto; task DAG: 1 device merge, 2 update programs; rows: 3 queues,
+    #                4 static + flags, 5 static value flow (finalising rows, no flags)
     lanes_per_row: int = 0  # mode 4 row-group width (4/8/16/32), 0 = auto
 
 

@@ -98,6 +98,13 @@ struct tcg_ctx {
   int* pos_pred = nullptr;
   int* row_flag = nullptr;
   bool has_static = false;
+  int4* flow_rec = nullptr;  // value-flow schedule (mode 5)
+  int* flow_item = nullptr;
+  int4* flow_slot = nullptr;
+  int2* flow_upd = nullptr;
+  double* flow_a = nullptr;  // snapshot of the input values
+  std::int64_t nflow = 0;
+  bool has_flow = false;
   std::int64_t nslots = 0, nupdates = 0;
   tcbdev::Ctrl* ctrl = nullptr;
   unsigned long long* trace = nullptr;
@@ -197,6 +204,13 @@ tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   o->pos_rec = rows ? P.pos_rec.data() : nullptr;
   o->npos_pred = rows ? static_cast<int64_t>(P.pos_pred.size()) : 0;
   o->pos_pred = rows ? P.pos_pred.data() : nullptr;
+  const bool flow = !P.flow_rec.empty();
+  o->nflow = flow ? static_cast<int64_t>(P.flow_rec.size() / tcb::kFlowWords) : 0;
+  o->flow_rec = flow ? P.flow_rec.data() : nullptr;
+  o->flow_item = flow ? P.flow_item.data() : nullptr;
+  o->flow_slot = flow ? P.flow_slot.data() : nullptr;
+  o->nflow_upd = flow ? static_cast<int64_t>(P.flow_upd.size() / 2) : 0;
+  o->flow_upd = flow ? P.flow_upd.data() : nullptr;
   return TCG_OK;
 }
 
@@ -221,6 +235,8 @@ tcg_status tcg_plan_get_stats(const tcg_plan* plan, tcg_plan_stats* o) {
   o->nblocks = plan->plan.blocks.nblocks();
   o->block_build_seconds = s.block_build_seconds;
   o->plan_seconds = s.plan_seconds;
+  o->flow_rows = s.flow_rows;
+  o->flow_depth = s.flow_depth;
   return TCG_OK;
 }
 
@@ -354,6 +370,13 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_prec = take(stat ? sizeof(int4) * 4 * p->nitems : 0);
   const size_t o_ppred = take(stat ? sizeof(int) * p->npos_pred : 0);
   const size_t o_rflag = take(stat ? sizeof(int) * p->nitems : 0);
+  const bool flow = p->nflow > 0 && p->flow_rec && p->flow_item && p->flow_slot &&
+                    (p->nflow_upd == 0 || p->flow_upd);
+  const size_t o_frec = take(flow ? sizeof(int4) * p->nflow : 0);
+  const size_t o_fitem = take(flow ? sizeof(int) * p->nflow : 0);
+  const size_t o_fslot = take(flow ? sizeof(int4) * p->nnz : 0);
+  const size_t o_fupd = take(flow ? sizeof(int2) * p->nflow_upd : 0);
+  const size_t o_fa = take(flow ? sizeof(double) * p->nnz : 0);
   const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
   const size_t o_trace = take(sizeof(unsigned long long) * (2 * p->ntasks + 4 * p->nitems));
   TCG_CUDA_TRY(c, cudaMalloc(&c->arena, off));
@@ -389,6 +412,14 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->pos_pred = reinterpret_cast<int*>(base + o_ppred);
   c->row_flag = reinterpret_cast<int*>(base + o_rflag);
   c->has_static = stat;
+  c->flow_rec = reinterpret_cast<int4*>(base + o_frec);
+  c->flow_item = reinterpret_cast<int*>(base + o_fitem);
+  c->flow_slot = reinterpret_cast<int4*>(base + o_fslot);
+  c->flow_upd = reinterpret_cast<int2*>(base + o_fupd);
+  c->flow_a = reinterpret_cast<double*>(base + o_fa);
+  c->nflow = flow ? p->nflow : 0;
+  c->has_flow = flow;
+
   c->nslots = programs ? p->nslots : 0;
   c->nupdates = programs ? p->nupdates : 0;
   c->ctrl = reinterpret_cast<tcbdev::Ctrl*>(base + o_ctrl);
@@ -423,6 +454,12 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     TCG_CUDA_TRY(c, put(c->pos_rec, p->pos_rec, sizeof(int4) * 4 * p->nitems));
     TCG_CUDA_TRY(c, put(c->pos_pred, p->pos_pred, sizeof(int) * p->npos_pred));
     TCG_CUDA_TRY(c, cudaMemsetAsync(c->row_flag, 0, sizeof(int) * p->nitems, c->stream));
+  }
+  if (flow) {
+    TCG_CUDA_TRY(c, put(c->flow_rec, p->flow_rec, sizeof(int4) * p->nflow));
+    TCG_CUDA_TRY(c, put(c->flow_item, p->flow_item, sizeof(int) * p->nflow));
+    TCG_CUDA_TRY(c, put(c->flow_slot, p->flow_slot, sizeof(int4) * p->nnz));
+    TCG_CUDA_TRY(c, put(c->flow_upd, p->flow_upd, sizeof(int2) * p->nflow_upd));
   }
   if (p->nitems > 0)
     TCG_CUDA_TRY(c, cudaMemsetAsync(c->iflag, 0, sizeof(int) * p->nitems, c->stream));
@@ -464,6 +501,81 @@ tcg_status tcg_restore(tcg_ctx* c) {
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals, c->vals0, sizeof(double) * c->nnz,
                                   cudaMemcpyDeviceToDevice, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+// Value-flow execution (mode 5, flow_kernel.cu): prelude (snapshot the
+// input, mark the output unwritten, reset the status words) + one persistent
+// launch; both inside the timed region.
+static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads) {
+  int kb = 4, minb = threads == 128 ? 6 : threads == 512 ? 1 : 3;
+  if (const char* e = std::getenv("TCG_FLOW_KB")) kb = std::atoi(e);
+  if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
+  // lanes per row: a whole warp unless asked otherwise (flow_kernel.cu)
+  const int g = c->opt.lanes_per_row > 0 ? c->opt.lanes_per_row : 32;
+  int weak = 0;
+  if (const char* e = std::getenv("TCG_FLOW_WEAK")) weak = std::atoi(e);
+  int occ = 0;
+  TCG_CUDA_TRY(c, tcbdev::flow_occupancy(threads, kb, minb, g, weak, &occ));
+  if (occ < 1) {
+    c->err = "value-flow kernel does not fit on an SM";
+    return TCG_INVALID;
+  }
+  if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
+  const int grid = std::max(1, occ * c->sm_count);
+  tcbdev::FlowPrepParams q{};
+  q.vals = c->vals;
+  q.a = c->flow_a;
+  q.out = c->vals;
+  q.nnz = c->nnz;
+  q.ctrl = c->ctrl;
+  tcbdev::FlowParams P{};
+  P.rec = c->flow_rec;
+  P.item = c->flow_item;
+  P.slot = c->flow_slot;
+  P.upd = c->flow_upd;
+  P.a = c->flow_a;
+  P.vals = c->vals;
+  P.ctrl = c->ctrl;
+  P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
+  P.nrows = static_cast<int>(c->nflow);
+  const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
+  P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
+  if (c->nflow > 0) TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, c->stream));
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
+                                  cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  const tcbdev::Ctrl& h = *c->host_ctrl;
+  S.device_ms = ms;
+  S.grid_ctas = grid;
+  S.threads_per_cta = threads;
+  S.staging_cap = kb;  // reported: gather batch
+  S.kernel_launches = c->nflow > 0 ? 2 : 1;
+  S.mode = 5;
+  S.lanes_per_row = g;
+  S.tasks_completed = (h.done.v == c->nflow) ? c->ntasks : 0;
+  S.tasks_executed = h.executed.v;
+  if (h.error.v) {
+    c->err = "device watchdog expired: the value-flow schedule stalled";
+    return TCG_TIMEOUT;
+  }
+  if (h.done.v != c->nflow) {
+    c->err = "value-flow schedule finished " + std::to_string(h.done.v) + " of " +
+             std::to_string(c->nflow) + " rows";
+    return TCG_TIMEOUT;
+  }
+  if (h.failed.v) {
+    S.breakdown_row = h.fail_row;
+    S.breakdown_pivot = h.fail_pivot;
+    c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
+             std::to_string(h.fail_pivot) + " is not positive";
+    return TCG_BREAKDOWN;
+  }
   return TCG_OK;
 }
 
@@ -627,14 +739,22 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
 
   const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
   int mode = c->opt.mode;
-  if (mode == 0) mode = c->has_static ? 4 : c->has_rows ? 3 : (c->has_programs ? 2 : 1);
+  if (mode == 0) {
+    // value flow unless the programs are long (mean products per coordinate
+    // above 16, e.g. C3): there the finalising rows' serial gathers dominate
+    // and the flag schedule, which runs Herk/Gemm rows early, measured faster
+    const bool long_programs = c->nupdates > 16 * c->nnz;
+    mode = c->has_flow && !(long_programs && c->has_static) ? 5
+           : c->has_static ? 4 : c->has_rows ? 3 : (c->has_programs ? 2 : 1);
+  }
   if ((mode == 2 && !c->has_programs) || (mode == 3 && !c->has_rows) ||
-      (mode == 4 && !c->has_static) || mode < 0 || mode > 4) {
+      (mode == 4 && !c->has_static) || (mode == 5 && !c->has_flow) || mode < 0 || mode > 5) {
     c->err = "requested execution mode is not available for the uploaded problem";
     return TCG_INVALID;
   }
   if (mode == 3) return run_rows(c, S, threads);
   if (mode == 4) return run_static(c, S, threads);
+  if (mode == 5) return run_flow(c, S, threads);
   int flag_words = (c->max_flag_rows + 31) / 32;
   flag_words = (flag_words + 3) & ~3;
   int cap = c->opt.staging_cap;

@@ -100,6 +100,32 @@ struct StaticParams {
   unsigned long long timeout_ns;
 };
 
+// Value-flow schedule (mode 5, flow_kernel.cu): the finalising rows only,
+// readers polling the values they gather until they are no longer kUnset.
+// kUnset is a signalling NaN: arithmetic never produces one.
+constexpr unsigned long long kUnset = 0x7FF40000DEADBEEFull;
+
+struct FlowParams {
+  const int4* rec;       // per position {tb, L | kind << 30, dpos, t} (plan.hpp kFlowWords)
+  const int* item;       // per position: its item (trace only)
+  const int4* slot;      // per coordinate of U: {u_b, u_e, m0, o0}
+  const int2* upd;       // (m, o) pairs
+  const double* a;       // input values (snapshot taken by the prelude)
+  double* vals;          // output; kUnset until the owning row writes it
+  Ctrl* ctrl;
+  unsigned long long* trace;  // optional: {start, end} per item
+  int nrows;
+  unsigned long long timeout_ns;
+};
+
+struct FlowPrepParams {
+  const double* vals;    // working values (input of the factorization)
+  double* a;             // snapshot of them
+  double* out;           // = vals in place: set to kUnset
+  long long nnz;
+  Ctrl* ctrl;
+};
+
 struct PrepParams {
   const int* indeg0;
   const int* roots;

@@ -1,0 +1,280 @@
+// Value-flow schedule (mode 5): the static row schedule of mode 4 without
+// flags, fences or any per-row synchronisation.
+//
+// Only the finalising rows run (the Chol/Trsm items; plan.cpp build_flow
+// folds every Herk/Gemm product of a slice into the row that finalises it,
+// in generation order), so every coordinate of U is written exactly once.
+// The prelude snapshots the input values and sets the output to kUnset (a
+// signalling NaN, which arithmetic never produces); a row gathers its
+// operands with 64-bit strong loads and re-polls any that still read kUnset.
+// A value is single-copy atomic, so a reader sees either kUnset or the final
+// value: the data is its own flag, and a hand-off between rows costs one
+// store reaching L2 plus one load, instead of store + release fence + flag
+// store + flag poll + acquire + load.
+//
+// Warp w of the W co-resident warps runs positions w, w+W, ... The order is
+// topological (level, then falling height), so the row at the smallest
+// unfinished position only reads values that are final: the schedule cannot
+// deadlock while all warps are resident (grid = occupancy; a watchdog ends
+// the kernel otherwise). Per coordinate the products arrive in ascending
+// source row, so the factor is bitwise equal to factor_serial
+// (factorize.hpp:94-130; kernels.hpp:40-132 for one target row).
+#include <cuda_runtime.h>
+
+#include "factor_kernel.cuh"
+#include "sync.cuh"
+
+namespace tcbdev {
+
+namespace {
+
+constexpr unsigned long long kCanonicalNaN = 0x7FFFFFFFFFFFFFFFull;
+
+// Slow path of a gather: the value is not written yet.
+__device__ __forceinline__ unsigned long long wait_value(const double* p, Ctrl* ctrl,
+                                                      unsigned long long t0,
+                                                      unsigned long long tmo) {
+  unsigned spins = 0;
+  for (;;) {
+    const unsigned long long x = ld_relaxed_u64(p);
+    if (x != kUnset) return x;
+    if (++spins == 1024u) {
+      spins = 0;
+      if (ld_relaxed(&ctrl->error.v) || gtimer() - t0 > tmo) {
+        atomicCAS(&ctrl->error.v, 0, 1);
+        return 0ull;  // abandoned: the host reports TCG_TIMEOUT
+      }
+    }
+  }
+}
+
+// WEAK: first attempt of every gather is a plain (L1-cached) load; only a
+// kUnset answer falls back to strong polling. Sound because a location
+// holds kUnset until its single final value is written: any other bits a
+// load returns are the final value (8-byte aligned accesses do not tear),
+// and a stale L1 copy can only show kUnset, which the strong path re-reads.
+template <int WEAK>
+struct Ctx {
+  const FlowParams& P;
+  unsigned long long t0;
+  __device__ __forceinline__ double settle(const double* p, unsigned long long x) const {
+    if (x == kUnset) x = wait_value(p, P.ctrl, t0, P.timeout_ns);
+    return __longlong_as_double(static_cast<long long>(x));
+  }
+  __device__ __forceinline__ unsigned long long ld(int pos) const {
+    if (WEAK) return ld_weak_u64(P.vals + pos);
+    return ld_relaxed_u64(P.vals + pos);
+  }
+};
+
+// One coordinate: v -= U[m]*U[o] over its merged program, in order. The
+// first pair rides in the slot record; the rest are fetched a batch ahead.
+template <int KB, class Cx>
+__device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr) {
+  const int ub = sr.x, ue = sr.y;
+  if (ub >= ue) return v;
+  const unsigned long long xa0 = C.ld(sr.z), xb0 = C.ld(sr.w);
+  int u = ub + 1;
+  int2 p[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
+  v = __dsub_rn(v, __dmul_rn(C.settle(C.P.vals + sr.z, xa0), C.settle(C.P.vals + sr.w, xb0)));
+  while (u < ue) {
+    const int n = min(KB, ue - u);
+    unsigned long long xa[KB], xb[KB];
+    int2 c[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      c[j] = p[j];
+      xa[j] = (j < n) ? C.ld(c[j].x) : 0ull;
+      xb[j] = (j < n) ? C.ld(c[j].y) : 0ull;
+    }
+    u += KB;
+#pragma unroll
+    for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
+#pragma unroll
+    for (int j = 0; j < KB; ++j)
+      if (j < n)
+        v = __dsub_rn(v, __dmul_rn(C.settle(C.P.vals + c[j].x, xa[j]),
+                                   C.settle(C.P.vals + c[j].y, xb[j])));
+  }
+  return v;
+}
+
+// One finalising row on a group of G lanes: group lane j owns coordinates
+// tb+j, tb+j+G, ... Chol: pivot test (latch), sqrt, scale
+// (kernels.hpp:49-53); Trsm: divide by U(t,t) (kernels.hpp:76-78). `a0`/`sr0`:
+// the lane's first input value and slot record, prefetched by the caller;
+// `gmask` the group's lanes, `lead` its first lane.
+template <int KIND, int KB, int G, class Cx>
+__device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, int t, int gl,
+                                         unsigned gmask, int lead, double a0, int4 sr0) {
+  const FlowParams& P = C.P;
+  unsigned long long xd = 0;
+  if (KIND == kTrsm) xd = C.ld(dpos);
+  double v = 0.0;
+  if (gl < L) v = flow_slot<KB>(C, a0, sr0);
+  double d;
+  if (KIND == kChol) {
+    const double piv = __shfl_sync(gmask, v, lead);
+    if (!(piv > 0.0) && gl == 0) {
+      if (atomicCAS(&P.ctrl->failed.v, 0, 1) == 0) {
+        P.ctrl->fail_row = t;
+        P.ctrl->fail_pivot = piv;
+      }
+    }
+    d = __dsqrt_rn(piv);
+  } else {
+    d = C.settle(P.vals + dpos, xd);
+  }
+  auto finish = [&](int k, double x) {
+    const double y = (KIND == kChol && k == 0) ? d : __ddiv_rn(x, d);
+    return static_cast<unsigned long long>(__double_as_longlong(y));
+  };
+  if (gl < L) st_relaxed_u64(P.vals + tb + gl, finish(gl, v));
+  for (int k = gl + G; k < L; k += G) {
+    const double w = flow_slot<KB>(C, __ldg(P.a + tb + k), __ldg(P.slot + tb + k));
+    st_relaxed_u64(P.vals + tb + k, finish(k, w));
+  }
+}
+
+}  // namespace
+
+// G lanes per row: a warp runs 32 / G rows side by side.
+template <int THREADS, int KB, int MINB, int G, int WEAK>
+__global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
+  constexpr int kGroups = THREADS / G;
+  constexpr int kLenMask = (1 << 30) - 1;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int lead = lane & ~(G - 1);
+  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << lead);
+  const int W = gridDim.x * kGroups;
+  const Ctx<WEAK> C{P, gtimer()};
+  int ran = 0, executed = 0, latched = 0;
+  int pos = blockIdx.x * kGroups + threadIdx.x / G;
+  // two-deep pipeline of the immutable inputs: the record of the position
+  // after next, and the next position's first slot record and input value,
+  // are in flight while the current row gathers
+  const int4 z = make_int4(0, 0, 0, 0);
+  int4 a = z, na = z, sr0 = z;
+  double a0 = 0.0;
+  if (pos < P.nrows) {
+    a = __ldg(P.rec + pos);
+    if (gl < (a.y & kLenMask)) {
+      sr0 = __ldg(P.slot + a.x + gl);
+      a0 = __ldg(P.a + a.x + gl);
+    }
+  }
+  if (pos + W < P.nrows) na = __ldg(P.rec + pos + W);
+  while (pos < P.nrows) {
+    const int nxt = pos + W, nn = pos + 2 * W;
+    const int4 nna = nn < P.nrows ? __ldg(P.rec + nn) : z;
+    int4 nsr0 = z;
+    double na0 = 0.0;
+    if (nxt < P.nrows && gl < (na.y & kLenMask)) {
+      nsr0 = __ldg(P.slot + na.x + gl);
+      na0 = __ldg(P.a + na.x + gl);
+    }
+    const int tb = a.x, L = a.y & kLenMask, dpos = a.z, t = a.w;
+    const bool chol = (static_cast<unsigned>(a.y) >> 30) == kChol;
+    if (P.trace && gl == 0) P.trace[2 * static_cast<long long>(P.item[pos])] = gtimer();
+    if ((ran & 15) == 0) {  // breakdown: skip the rest (one decision per group)
+      latched = gl == 0 ? ld_relaxed(&P.ctrl->failed.v) : 0;
+      latched = __shfl_sync(gmask, latched, lead);
+    }
+    if (!latched) {
+      if (chol)
+        flow_row<kChol, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0);
+      else
+        flow_row<kTrsm, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0);
+      ++executed;
+    } else {
+      // skipped rows keep their input values (readers must not wait forever)
+      for (int k = gl; k < L; k += G) {
+        unsigned long long x = static_cast<unsigned long long>(__double_as_longlong(P.a[tb + k]));
+        st_relaxed_u64(P.vals + tb + k, x == kUnset ? kCanonicalNaN : x);
+      }
+    }
+    if (P.trace && gl == 0) P.trace[2 * static_cast<long long>(P.item[pos]) + 1] = gtimer();
+    ++ran;
+    pos = nxt;
+    a = na;
+    na = nna;
+    sr0 = nsr0;
+    a0 = na0;
+  }
+  if (gl == 0) {
+    if (ran) atomicAdd(&P.ctrl->done.v, ran);
+    if (executed) atomicAdd(&P.ctrl->executed.v, executed);
+  }
+}
+
+// Prelude: snapshot the working values, mark the output unwritten, reset
+// the status words.
+__global__ void flow_prepare(FlowPrepParams Q) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long h = Q.nnz / 2;
+  const double2* in2 = reinterpret_cast<const double2*>(Q.vals);
+  double2* a2 = reinterpret_cast<double2*>(Q.a);
+  double2* o2 = reinterpret_cast<double2*>(Q.out);
+  const double unset = __longlong_as_double(static_cast<long long>(kUnset));
+  for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < h; x += stride) {
+    a2[x] = in2[x];
+    o2[x] = make_double2(unset, unset);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (Q.nnz & 1) {
+      Q.a[Q.nnz - 1] = Q.vals[Q.nnz - 1];
+      Q.out[Q.nnz - 1] = unset;
+    }
+    Ctrl c = {};
+    c.fail_row = -1;
+    *Q.ctrl = c;
+  }
+}
+
+// KB: products gathered per batch; MINB: CTAs per SM the register budget
+// targets; G: lanes per row. Measured on B200 (C1-C5): whole warps per row
+// win everywhere -- the groups of a warp diverge on their polls and product
+// counts, and their rows serialise; G = 8 is kept for experiments.
+#define TCG_FLOW_VARIANTS(X)                                                     \
+  X(256, 4, 3, 32, 0) X(256, 4, 3, 32, 1) X(128, 4, 6, 32, 0) X(512, 4, 1, 32, 0) \
+  X(256, 8, 3, 32, 0) X(256, 4, 3, 8, 0)
+
+static const void* flow_kernel_for(int threads, int kb, int minb, int g, int weak) {
+#define X(T, K, M, GG, WK)                                                \
+  if (threads == T && kb == K && minb == M && g == GG && weak == WK)      \
+    return reinterpret_cast<const void*>(&factor_flow<T, K, M, GG, WK>);
+  TCG_FLOW_VARIANTS(X)
+#undef X
+  return nullptr;
+}
+
+cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int* ctas_per_sm) {
+  const void* k = flow_kernel_for(threads, kb, minb, g, weak);
+  if (!k) return cudaErrorInvalidValue;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
+}
+
+cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStream_t st) {
+  const long long h = q.nnz / 2;
+  long long blocks = (h + 255) / 256;
+  blocks = blocks < 1 ? 1 : (blocks > 4LL * sm_count ? 4LL * sm_count : blocks);
+  flow_prepare<<<static_cast<int>(blocks), 256, 0, st>>>(q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flow(const FlowParams& p, int grid, int threads, int kb, int minb, int g,
+                        int weak, cudaStream_t st) {
+#define X(T, K, M, GG, WK)                                                 \
+  if (threads == T && kb == K && minb == M && g == GG && weak == WK) {     \
+    factor_flow<T, K, M, GG, WK><<<grid, T, 0, st>>>(p);                   \
+    return cudaGetLastError();                                             \
+  }
+  TCG_FLOW_VARIANTS(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace tcbdev

@@ -412,6 +412,118 @@ void build_item_deps(Plan& P, const RangeList& ranges, double opt_hot_fraction) 
   }
 }
 
+// Value-flow schedule (mode 5). The Chol/Trsm items partition U: each
+// coordinate is finalised by exactly one of them, and every Herk/Gemm item
+// on the same slice runs before it (the own-slice chain above). Folding the
+// Herk/Gemm products into the finaliser's program, in item (generation)
+// order, keeps the per-coordinate product order ascending in source row, so
+// the result stays bitwise equal to factor_serial while every coordinate is
+// written once. A reader then needs no flag: it polls the value itself
+// until the writer has replaced the "not yet written" marker (flow_kernel.cu).
+// Schedule: finalisers by (level, falling height) over the dependences
+// "reads a coordinate owned by", which point to earlier items.
+//
+// (Measured alternative, not kept: cutting the chains into several
+// segments that hand partial values on through scratch, so heavy Herk/Gemm
+// work runs early. On B200 it lost on every acceptance config -- C2 0.69 ->
+// 0.83 ms, C3 7.6 -> 17 ms -- the extra rows cost more than the shorter
+// finaliser programs saved.)
+void build_flow(Plan& P) {
+  const std::size_t I = P.item_rec.size() / kItemWords;
+  const std::size_t N = static_cast<std::size_t>(P.nnz);
+  auto R = [&](std::size_t k, int w) { return P.row_rec[k * kRowWords + w]; };
+  P.flow_owner.assign(N, -1);
+  std::int64_t nfin = 0;
+  for (std::size_t k = 0; k < I; ++k)
+    if (R(k, 4) <= kTrsm) {
+      ++nfin;
+      for (std::int32_t x = R(k, 0); x < R(k, 1); ++x) {
+        if (P.flow_owner[x] >= 0) throw std::logic_error("flow: coordinate finalised twice");
+        P.flow_owner[x] = static_cast<std::int32_t>(k);
+      }
+    }
+  for (std::size_t x = 0; x < N; ++x)
+    if (P.flow_owner[x] < 0) throw std::logic_error("flow: coordinate without a finaliser");
+  // merged programs: per coordinate, the products of every item on it in item order
+  std::vector<std::int64_t> cnt(N + 1, 0);
+  for (std::size_t k = 0; k < I; ++k)
+    for (std::int32_t j = 0; j < R(k, 1) - R(k, 0); ++j) {
+      const std::int32_t* s = &P.slot_rec[static_cast<std::size_t>(R(k, 3) + j) * 4];
+      cnt[R(k, 0) + j + 1] += s[1] - s[0];
+    }
+  for (std::size_t x = 0; x < N; ++x) cnt[x + 1] += cnt[x];
+  if (cnt[N] > 0x7fffffffLL) throw std::length_error("flow: more than 2^31 products");
+  P.flow_upd.assign(static_cast<std::size_t>(2 * cnt[N]), 0);
+  std::vector<std::int64_t> fill(cnt.begin(), cnt.end() - 1);
+  for (std::size_t k = 0; k < I; ++k)
+    for (std::int32_t j = 0; j < R(k, 1) - R(k, 0); ++j) {
+      const std::int32_t* s = &P.slot_rec[static_cast<std::size_t>(R(k, 3) + j) * 4];
+      std::int64_t& f = fill[R(k, 0) + j];
+      for (std::int32_t u = s[0]; u < s[1]; ++u, ++f) {
+        P.flow_upd[2 * f] = P.upd[2 * static_cast<std::size_t>(u)];
+        P.flow_upd[2 * f + 1] = P.upd[2 * static_cast<std::size_t>(u) + 1];
+      }
+    }
+  P.flow_slot.assign(4 * N, 0);
+  for (std::size_t x = 0; x < N; ++x) {
+    std::int32_t* s = &P.flow_slot[4 * x];
+    s[0] = static_cast<std::int32_t>(cnt[x]);
+    s[1] = static_cast<std::int32_t>(cnt[x + 1]);
+    if (s[0] < s[1]) {
+      s[2] = P.flow_upd[2 * static_cast<std::size_t>(s[0])];
+      s[3] = P.flow_upd[2 * static_cast<std::size_t>(s[0]) + 1];
+    }
+  }
+  // levels (forward) and heights (backward) over "reads a coordinate owned by"
+  std::vector<std::int32_t> level(I, 0), height(I, 0);
+  auto each_src = [&](std::size_t k, auto&& fn) {
+    if (R(k, 4) == kTrsm) fn(P.flow_owner[R(k, 2)]);  // divisor U(t,t)
+    for (std::int32_t x = R(k, 0); x < R(k, 1); ++x)
+      for (std::int64_t u = cnt[x]; u < cnt[x + 1]; ++u) {
+        fn(P.flow_owner[P.flow_upd[2 * u]]);
+        fn(P.flow_owner[P.flow_upd[2 * u + 1]]);
+      }
+  };
+  std::int32_t depth = 0;
+  for (std::size_t k = 0; k < I; ++k) {
+    if (R(k, 4) > kTrsm) continue;
+    std::int32_t lv = 1;
+    each_src(k, [&](std::int32_t s) {
+      if (s < 0 || static_cast<std::size_t>(s) >= k) throw std::logic_error("flow: dependence out of order");
+      lv = std::max(lv, level[s] + 1);
+    });
+    level[k] = lv;
+    depth = std::max(depth, lv);
+  }
+  for (std::size_t k = I; k-- > 0;) {
+    if (R(k, 4) > kTrsm) continue;
+    height[k] = std::max(height[k], 1);
+    const std::int32_t h = height[k] + 1;
+    each_src(k, [&](std::int32_t s) { height[s] = std::max(height[s], h); });
+  }
+  std::vector<std::int32_t> order;
+  order.reserve(static_cast<std::size_t>(nfin));
+  for (std::size_t k = 0; k < I; ++k)
+    if (R(k, 4) <= kTrsm) order.push_back(static_cast<std::int32_t>(k));
+  std::stable_sort(order.begin(), order.end(), [&](std::int32_t x, std::int32_t y) {
+    if (level[x] != level[y]) return level[x] < level[y];
+    return height[x] > height[y];
+  });
+  P.flow_rec.assign(order.size() * kFlowWords, 0);
+  P.flow_item = order;
+  for (std::size_t q = 0; q < order.size(); ++q) {
+    const std::size_t k = static_cast<std::size_t>(order[q]);
+    std::int32_t* o = &P.flow_rec[q * kFlowWords];
+    if (R(k, 1) - R(k, 0) >= (1 << kFlowKindShift)) throw std::length_error("flow: row slice too long");
+    o[0] = R(k, 0);
+    o[1] = (R(k, 1) - R(k, 0)) | (R(k, 4) << kFlowKindShift);
+    o[2] = R(k, 2);
+    o[3] = R(k, 5);
+  }
+  P.stats.flow_rows = nfin;
+  P.stats.flow_depth = depth;
+}
+
 }  // namespace
 
 Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
@@ -673,6 +785,7 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
 
   if (with_work && opt.programs) build_programs(P, opt.threads);
   if (with_work) build_item_deps(P, ranges, opt.hot_fraction);
+  if (with_work && opt.programs) build_flow(P);
 
   // successors + in-degrees (edge multiplicity preserved)
   const std::size_t T = P.node_kind.size();

@@ -44,6 +44,9 @@ constexpr std::int32_t kRowHot = 0x40000000;  // row_succ flag: push to the prio
 // first kPosInline predecessor items (-1 = none) | item id, 0, 0, 0
 constexpr int kPosWords = 16;
 constexpr int kPosInline = 4;
+// value-flow schedule (mode 5) record per position: tb, L | kind << 30, dpos, t
+constexpr int kFlowWords = 4;
+constexpr int kFlowKindShift = 30;
 
 struct PlanOptions {
   double cta_cost = 64.0;  // estimated warp-steps one CTA should get before a helper joins
@@ -79,6 +82,8 @@ struct PlanStats {
   std::int64_t updates = 0;        // (m, o) products in the update programs
   std::int64_t item_edges = 0;     // row-level dependences
   std::int32_t item_depth = 0;     // longest row-level chain, in items
+  std::int64_t flow_rows = 0;      // value-flow rows (Chol/Trsm items; they partition U)
+  std::int32_t flow_depth = 0;     // longest value-flow chain, in rows
   double block_build_seconds = 0.0;
   double plan_seconds = 0.0;
 };
@@ -109,6 +114,14 @@ struct Plan {
   std::vector<std::int32_t> row_pred_ptr;  // int32 copy of item_dep_ptr (preds = item_dep)
   std::vector<std::int32_t> pos_rec;   // kPosWords per schedule position
   std::vector<std::int32_t> pos_pred;  // predecessor items beyond the inline ones
+  // value-flow schedule (mode 5): every coordinate of U is written once, by
+  // the Chol/Trsm item owning it, which applies all of its updates (the
+  // Herk/Gemm items' products folded in, generation order kept)
+  std::vector<std::int32_t> flow_rec;   // kFlowWords per schedule position
+  std::vector<std::int32_t> flow_item;  // per schedule position: its item
+  std::vector<std::int32_t> flow_slot;  // per coordinate of U: {u_b, u_e, m0, o0}
+  std::vector<std::int32_t> flow_upd;   // (m, o) pairs
+  std::vector<std::int32_t> flow_owner; // per coordinate of U: the item writing it
   std::vector<std::int32_t> slot_rec;  // update-program slots {u_b, u_e, m0, o0} (per item: L)
   std::vector<std::int32_t> upd;       // update-program (m, o) pairs
   std::vector<std::int32_t> succ;      // successors grouped per task

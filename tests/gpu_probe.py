@@ -29,6 +29,6 @@ for name in names:
     bit = np.array_equal(v.view(np.int64), ref.view(np.int64))
     rel = float(np.max(np.abs(v - ref) / (np.abs(ref) + 1e-300)))
     print(f"{name} mode={s.mode} thr={threads} ctas/sm={ctas} grid={s.grid_ctas} cap={s.staging_cap} smem={s.smem_bytes} "
-          f"helpers={s.helpers_run} med_ms={np.median(times):.3f} min_ms={min(times):.3f} "
+          f"lanes={s.lanes_per_row} helpers={s.helpers_run} med_ms={np.median(times):.3f} min_ms={min(times):.3f} "
           f"bitwise={bit} maxrel={rel:.2e}", flush=True)
     fz.close()

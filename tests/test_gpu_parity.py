@@ -40,16 +40,38 @@ def check_against_oracle(name, vals, golden, oracle):
 
 @pytest.mark.parametrize("name", ["c1", "c5_m0", "c5_m63", "s27_16_k2", "grid20_k2_leaf4",
                                   "rand_spd_200", "elast6_k1", "c2", "c3", "c4"])
-@pytest.mark.parametrize("mode", [3, 4])
+@pytest.mark.parametrize("mode", [3, 4, 5])
 def test_configs_row_modes(T, golden, oracle, name, mode):  # noqa: D103
     vals, st = gpu_factor(T, planned(name), mode=mode)
     assert st.mode == mode
     check_against_oracle(name, vals, golden, oracle)
 
 
-def test_default_mode_is_static_rows(T):
+@pytest.mark.parametrize("name", ["c1", "c5_m0", "s27_16_k2", "c3"])
+def test_flow_weak_first_loads(T, golden, oracle, name, monkeypatch):
+    # mode 5 with L1-cached first gathers (validated against kUnset)
+    monkeypatch.setenv("TCG_FLOW_WEAK", "1")
+    vals, st = gpu_factor(T, planned(name), mode=5)
+    assert st.mode == 5
+    check_against_oracle(name, vals, golden, oracle)
+
+
+def test_default_mode_is_value_flow(T):
     _, st = gpu_factor(T, planned("c1"))
-    assert st.mode == 4
+    assert st.mode == 5
+
+
+def test_flow_trace_stamps_every_finalising_row(T):
+    # mode 5 has no row flags (a row starts and polls its operands), so the
+    # stamps only bracket each finalising row
+    plan = planned("c5_m0")
+    fz = T.GpuFactorizer(plan, T.GpuOptions(mode=5, trace=True))
+    fz.factor()
+    _, items = fz.trace()
+    fz.close()
+    t = plan.tables()
+    st = items.reshape(-1)[:2 * len(t["row_rec"])].reshape(-1, 2)[t["flow_item"]]
+    assert np.all(st[:, 0] > 0) and np.all(st[:, 0] <= st[:, 1])
 
 
 def test_static_trace_respects_every_row_edge(T):
@@ -112,7 +134,7 @@ def sym(entries):
     return entries + [(j, i, v) for i, j, v in entries if i != j]
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4, 5])
 def test_known_answers(T, mode):
     # test_factorize.cpp:78-97 and test_kernels.cpp:36-57
     opt = T.GpuOptions(mode=mode)
@@ -129,7 +151,7 @@ def test_known_answers(T, mode):
     assert v[0] == 2.0 and v[1] == 1.0 and v[2] == math.sqrt(2.0)
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [1, 2, 3, 4, 5])
 def test_breakdown_reports_row_and_pivot(T, mode):
     # test_factorize.cpp:99-108,157-165 and test_kernels.cpp:62-76
     opt = T.GpuOptions(mode=mode)
@@ -158,7 +180,7 @@ def test_random_spd_many_blockings(T, oracle, seed):
         step = max(1, -(-n // nr))
         b = np.array(list(range(0, n, step)) + [n], dtype=np.int32)
         plan = T.Plan(an.a_permuted, an.pattern, T.RangeList(b))
-        for mode in (1, 2, 3, 4):
+        for mode in (1, 2, 3, 4, 5):
             vals, _ = gpu_factor(T, plan, mode=mode)
             assert bitwise_equal(vals, ref), (nr, mode)
 
@@ -241,7 +263,7 @@ def test_refactor_with_new_values_and_determinism(T, oracle):
 def test_cta_sizes_agree(T, threads):
     plan = planned("s27_16_k2")
     base, _ = gpu_factor(T, plan)
-    for mode in (1, 2, 3, 4):
+    for mode in (1, 2, 3, 4, 5):
         vals, st = gpu_factor(T, plan, mode=mode, threads_per_cta=threads)
         assert st.threads_per_cta == threads
         assert bitwise_equal(vals, base)

@@ -160,3 +160,53 @@ def test_random_blockings_against_live_reference(T, oracle, seed):
         vals, st, _, _, _, _ = R.factor_by_blocks(an.a_permuted, an.pattern.pattern, b, workers=2)
         assert st == 0
         assert bitwise_equal(emulate_rows(plan, seed), vals)
+
+
+def replay_flow(t, order=None):
+    """Mode 5 on the CPU: finalising rows in schedule order (or `order`), each
+    coordinate applying its merged program once, reading only final values."""
+    rec, slot, upd = t["flow_rec"], t["flow_slot"], t["flow_upd"]
+    a = t["values"]
+    out = np.full(len(a), np.nan)
+    done = np.zeros(len(a), bool)
+    for q in (range(len(rec)) if order is None else order):
+        tb, lk, dpos, _ = rec[q]
+        L, kind = lk & ((1 << 30) - 1), (lk >> 30) & 3
+        v = a[tb:tb + L].copy()
+        for j in range(L):
+            ub, ue = slot[tb + j, :2]
+            for m, o in upd[ub:ue]:
+                assert done[m] and done[o], "read before written"
+                v[j] = v[j] - out[m] * out[o]
+        if kind == 0:
+            d = np.sqrt(v[0])
+            v[1:] = v[1:] / d
+            v[0] = d
+        else:
+            assert done[dpos]
+            v = v / out[dpos]
+        assert not done[tb:tb + L].any(), "written twice"
+        out[tb:tb + L] = v
+        done[tb:tb + L] = True
+    assert done.all()
+    return out
+
+
+@pytest.mark.parametrize("name", ["c1", "s27_16_k2", "rand_spd_200", "grid20_k2_leaf4", "elast6_k1"])
+def test_flow_schedule_partitions_u_and_replays_bitwise(name, oracle):
+    # mode 5: the Chol/Trsm rows own every coordinate once; merged programs
+    # keep the per-coordinate product order, so replays equal factor_serial
+    plan = planned(name)
+    t = plan.tables()
+    s = plan.stats()
+    assert s.flow_rows == len(t["flow_rec"]) == int((t["row_rec"][:, 4] <= 1).sum())
+    assert len(t["flow_upd"]) == len(t["upd"])  # every product folded in exactly once
+    assert s.flow_depth <= s.item_depth
+    items = t["flow_item"]
+    assert np.array_equal(np.sort(items), np.flatnonzero(t["row_rec"][:, 4] <= 1))
+    _, an = analyzed(name)
+    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
+    assert bitwise_equal(replay_flow(t), ref)
+    # any order that respects "reads only written values" gives the same bits:
+    # item order (generation order) is one
+    assert bitwise_equal(replay_flow(t, np.argsort(items, kind="stable")), ref)
