@@ -307,9 +307,9 @@ const char* tcg_last_error(const tcg_ctx* c) {
 
 tcg_status tcg_set_options(tcg_ctx* c, const tcg_options* opt) {
   if (!c || !opt) return TCG_INVALID;
-  if (opt->threads_per_cta != 0 && opt->threads_per_cta != 128 && opt->threads_per_cta != 256 &&
-      opt->threads_per_cta != 512) {
-    c->err = "threads_per_cta must be 128, 256 or 512";
+  const int t = opt->threads_per_cta;
+  if (t != 0 && t != 128 && t != 256 && t != 512 && t != 384 && t != 768) {
+    c->err = "threads_per_cta must be 128, 256 or 512 (or 384, 768 in mode 5)";
     return TCG_INVALID;
   }
   c->opt = *opt;
@@ -508,15 +508,16 @@ tcg_status tcg_restore(tcg_ctx* c) {
 // input, mark the output unwritten, reset the status words) + one persistent
 // launch; both inside the timed region.
 static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads) {
-  int kb = 4, minb = threads == 128 ? 6 : threads == 512 ? 1 : 3;
+  int kb = 4, minb = threads == 128 ? 6 : threads == 384 ? 2 : threads == 256 ? 3 : 1;
   if (const char* e = std::getenv("TCG_FLOW_KB")) kb = std::atoi(e);
   if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
   // lanes per row: a whole warp unless asked otherwise (flow_kernel.cu)
   const int g = c->opt.lanes_per_row > 0 ? c->opt.lanes_per_row : 32;
-  int weak = 0;
+  int weak = 0, dyn = 0;
   if (const char* e = std::getenv("TCG_FLOW_WEAK")) weak = std::atoi(e);
+  if (const char* e = std::getenv("TCG_FLOW_DYN")) dyn = std::atoi(e);
   int occ = 0;
-  TCG_CUDA_TRY(c, tcbdev::flow_occupancy(threads, kb, minb, g, weak, &occ));
+  TCG_CUDA_TRY(c, tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, &occ));
   if (occ < 1) {
     c->err = "value-flow kernel does not fit on an SM";
     return TCG_INVALID;
@@ -543,7 +544,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads) {
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
   TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
-  if (c->nflow > 0) TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, c->stream));
+  if (c->nflow > 0) TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, c->stream));
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
                                   cudaMemcpyDeviceToHost, c->stream));
@@ -750,6 +751,10 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   if ((mode == 2 && !c->has_programs) || (mode == 3 && !c->has_rows) ||
       (mode == 4 && !c->has_static) || (mode == 5 && !c->has_flow) || mode < 0 || mode > 5) {
     c->err = "requested execution mode is not available for the uploaded problem";
+    return TCG_INVALID;
+  }
+  if (mode != 5 && (threads == 384 || threads == 768)) {
+    c->err = "threads_per_cta 384 and 768 are for mode 5 only";
     return TCG_INVALID;
   }
   if (mode == 3) return run_rows(c, S, threads);

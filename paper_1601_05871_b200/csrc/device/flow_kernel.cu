@@ -69,6 +69,8 @@ struct Ctx {
 
 // One coordinate: v -= U[m]*U[o] over its merged program, in order. The
 // first pair rides in the slot record; the rest are fetched a batch ahead.
+// (Issuing the first batch's operand loads before settling the first pair
+// measured slower on B200: C2 0.63 -> 0.68 ms.)
 template <int KB, class Cx>
 __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr) {
   const int ub = sr.x, ue = sr.y;
@@ -141,7 +143,15 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
 }  // namespace
 
 // G lanes per row: a warp runs 32 / G rows side by side.
-template <int THREADS, int KB, int MINB, int G, int WEAK>
+// DYN = 0: row group g of the W co-resident groups runs positions g, g+W, ...
+// DYN = 1: CTA c owns the positions c, c+grid, c+2*grid, ... and its row
+//   groups take them in that order from a shared-memory counter, each
+//   holding at most the row it runs plus two it prefetches; a row blocked on
+//   an operand then holds up only its own group, not the rows dealt after it.
+//   Still deadlock-free: the lowest unfinished position is either some
+//   group's current row (its operands are final) or was never handed out,
+//   which cannot be while every group of its CTA holds lower rows.
+template <int THREADS, int KB, int MINB, int G, int WEAK, int DYN>
 __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
   constexpr int kGroups = THREADS / G;
   constexpr int kLenMask = (1 << 30) - 1;
@@ -152,7 +162,20 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
   const int W = gridDim.x * kGroups;
   const Ctx<WEAK> C{P, gtimer()};
   int ran = 0, executed = 0, latched = 0;
-  int pos = blockIdx.x * kGroups + threadIdx.x / G;
+  __shared__ int s_next;
+  if (DYN) {
+    if (threadIdx.x == 0) s_next = 0;
+    __syncthreads();
+  }
+  auto grab = [&](int prev) -> int {
+    if (!DYN) return prev + W;
+    int k = 0;
+    if (gl == 0) k = atomicAdd(&s_next, 1);
+    k = __shfl_sync(gmask, k, lead);
+    return blockIdx.x + k * static_cast<int>(gridDim.x);
+  };
+  int pos = DYN ? grab(0) : blockIdx.x * kGroups + threadIdx.x / G;
+  int npos = grab(pos);
   // two-deep pipeline of the immutable inputs: the record of the position
   // after next, and the next position's first slot record and input value,
   // are in flight while the current row gathers
@@ -166,13 +189,13 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
       a0 = __ldg(P.a + a.x + gl);
     }
   }
-  if (pos + W < P.nrows) na = __ldg(P.rec + pos + W);
+  if (npos < P.nrows) na = __ldg(P.rec + npos);
   while (pos < P.nrows) {
-    const int nxt = pos + W, nn = pos + 2 * W;
-    const int4 nna = nn < P.nrows ? __ldg(P.rec + nn) : z;
+    const int nnpos = npos < P.nrows ? grab(npos) : npos;
+    const int4 nna = nnpos < P.nrows ? __ldg(P.rec + nnpos) : z;
     int4 nsr0 = z;
     double na0 = 0.0;
-    if (nxt < P.nrows && gl < (na.y & kLenMask)) {
+    if (npos < P.nrows && gl < (na.y & kLenMask)) {
       nsr0 = __ldg(P.slot + na.x + gl);
       na0 = __ldg(P.a + na.x + gl);
     }
@@ -198,7 +221,8 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
     }
     if (P.trace && gl == 0) P.trace[2 * static_cast<long long>(P.item[pos]) + 1] = gtimer();
     ++ran;
-    pos = nxt;
+    pos = npos;
+    npos = nnpos;
     a = na;
     na = nna;
     sr0 = nsr0;
@@ -238,21 +262,21 @@ __global__ void flow_prepare(FlowPrepParams Q) {
 // targets; G: lanes per row. Measured on B200 (C1-C5): whole warps per row
 // win everywhere -- the groups of a warp diverge on their polls and product
 // counts, and their rows serialise; G = 8 is kept for experiments.
-#define TCG_FLOW_VARIANTS(X)                                                     \
-  X(256, 4, 3, 32, 0) X(256, 4, 3, 32, 1) X(128, 4, 6, 32, 0) X(512, 4, 1, 32, 0) \
-  X(256, 8, 3, 32, 0) X(256, 4, 3, 8, 0)
+#define TCG_FLOW_VARIANTS(X)                                                             \
+  X(256, 4, 3, 32, 0, 0) X(256, 4, 3, 32, 1, 0) X(128, 4, 6, 32, 0, 0) X(512, 4, 1, 32, 0, 0) \
+  X(256, 4, 3, 32, 0, 1) X(768, 4, 1, 32, 0, 1) X(768, 4, 1, 32, 0, 0) X(384, 4, 2, 32, 0, 1)
 
-static const void* flow_kernel_for(int threads, int kb, int minb, int g, int weak) {
-#define X(T, K, M, GG, WK)                                                \
-  if (threads == T && kb == K && minb == M && g == GG && weak == WK)      \
-    return reinterpret_cast<const void*>(&factor_flow<T, K, M, GG, WK>);
+static const void* flow_kernel_for(int threads, int kb, int minb, int g, int weak, int dyn) {
+#define X(T, K, M, GG, WK, D)                                                         \
+  if (threads == T && kb == K && minb == M && g == GG && weak == WK && dyn == D)      \
+    return reinterpret_cast<const void*>(&factor_flow<T, K, M, GG, WK, D>);
   TCG_FLOW_VARIANTS(X)
 #undef X
   return nullptr;
 }
 
-cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int* ctas_per_sm) {
-  const void* k = flow_kernel_for(threads, kb, minb, g, weak);
+cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int dyn, int* ctas_per_sm) {
+  const void* k = flow_kernel_for(threads, kb, minb, g, weak, dyn);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
 }
@@ -266,11 +290,11 @@ cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStrea
 }
 
 cudaError_t launch_flow(const FlowParams& p, int grid, int threads, int kb, int minb, int g,
-                        int weak, cudaStream_t st) {
-#define X(T, K, M, GG, WK)                                                 \
-  if (threads == T && kb == K && minb == M && g == GG && weak == WK) {     \
-    factor_flow<T, K, M, GG, WK><<<grid, T, 0, st>>>(p);                   \
-    return cudaGetLastError();                                             \
+                        int weak, int dyn, cudaStream_t st) {
+#define X(T, K, M, GG, WK, D)                                                          \
+  if (threads == T && kb == K && minb == M && g == GG && weak == WK && dyn == D) {     \
+    factor_flow<T, K, M, GG, WK, D><<<grid, T, 0, st>>>(p);                            \
+    return cudaGetLastError();                                                         \
   }
   TCG_FLOW_VARIANTS(X)
 #undef X
