@@ -19,7 +19,10 @@ from its device copy and L2 is flushed (256 MiB write), both untimed.
 
 N > 1 (torchrun, one process per GPU): the single-matrix configs do not
 shard, so every rank factors its own replica (weak scaling, no collective on
-the data path); timing is the max over ranks.
+the data path); timing is the max over ranks. --config c5b is the sharded
+C5 batch: the 64 members are split over the ranks (paper_1601_05871_b200/
+batch.py), each rank factors its members in one launch, value = 64 * nnz_u /
+max-over-ranks time (strong scaling over the fixed batch).
 
 --impl reference: times the reference's own CPU factor_by_blocks
 (oracle/_ref, compiled from the unmodified reference headers) with a pooled
@@ -46,6 +49,8 @@ WORKLOADS = {
     "c3": "C3: 3D 27-point variable-coefficient 48^3 (n=110,592), IC(2), fp64, ND leaf 64",
     "c4": "C4: elasticity-like 40^3 x 3 dofs (n=192,000), IC(0), fp64, ND leaf 64",
     "c5": "C5 member: 3D 7-point log-normal diffusion 32^3 (n=32,768), IC(1), fp64",
+    "c5b": "C5: batch of 64 3D 7-point log-normal diffusion 32^3 matrices (n=32,768 each), IC(1), fp64, "
+           "members sharded over ranks, one launch per rank",
     "c6": "C6: 3D 7-point Laplacian 128^3 (n=2,097,152), IC(1), fp64, ND leaf 64",
 }
 METRIC = "ic_numeric_factor_nnz_per_s"
@@ -131,7 +136,7 @@ class ClockSampler:
 
 def build_problem(config: str, member: int = 0):
     import paper_1601_05871_b200 as T
-    name = "c5" if config == "c5" else config
+    name = "c5" if config in ("c5", "c5b") else config
     a, level = T.config_matrix(name, member)
     t0 = time.perf_counter()
     an = T.analyze(a, level=level)
@@ -214,6 +219,15 @@ def run_ours(args):
     u = an.pattern.pattern
     nnz, n = u.nnz(), a.nrows
     fz = T.GpuFactorizer(plan, T.GpuOptions(device=dev, mode=args.mode, timeout_s=60))
+    batched = args.config == "c5b"
+    nmembers_total, mine, batch_vals = 1, range(1), None
+    if batched:
+        from paper_1601_05871_b200 import batch as B
+        nmembers_total = 64
+        mine = B.shard(nmembers_total, rank, world)
+        _, batch_vals, batch_perms = B.member_values(list(mine))
+        fz.set_batch(batch_vals)
+    per_rank = len(mine)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
 
     def barrier():
@@ -243,17 +257,25 @@ def run_ours(args):
         step_ms = float(t.item())
 
     # end to end through the C ABI with host buffers (pinned)
-    host_in = torch.from_numpy(plan.tables()["values"]).pin_memory()
-    host_out = torch.empty(nnz, dtype=torch.float64).pin_memory()
+    if batched:
+        host_in = torch.from_numpy(batch_vals.reshape(-1)).pin_memory()
+    else:
+        host_in = torch.from_numpy(plan.tables()["values"]).pin_memory()
+    host_out = torch.empty(nnz * per_rank, dtype=torch.float64).pin_memory()
     e2e_ms = []
     barrier()
     for i in range(args.warmup + args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        fz.set_values_ptr(host_in.data_ptr())   # H2D 8*nnz_u
-        fz.factor()
-        fz.download_ptr(host_out.data_ptr())    # D2H 8*nnz_u
+        if batched:
+            fz.set_batch_values_ptr(host_in.data_ptr())   # H2D 8*nnz_u per member
+            fz.factor()
+            fz.download_batch_ptr(host_out.data_ptr())    # D2H 8*nnz_u per member
+        else:
+            fz.set_values_ptr(host_in.data_ptr())   # H2D 8*nnz_u
+            fz.factor()
+            fz.download_ptr(host_out.data_ptr())    # D2H 8*nnz_u
         if i >= args.warmup:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
     barrier()
@@ -268,9 +290,12 @@ def run_ours(args):
     parity = None
     if rank == 0 and nnz <= 3_000_000:
         from checkers import Oracle
-        ref, status, _, _ = Oracle().factor_serial(an.a_permuted, u)
-        parity = "bitwise" if np.array_equal(ref.view(np.int64), host_out.numpy().view(np.int64)) \
-            else f"max_rel={float(np.max(np.abs(host_out.numpy() - ref) / (np.abs(ref) + 1e-300))):.3e}"
+        O = Oracle()
+        got = host_out.numpy().reshape(per_rank, nnz)
+        refs = [O.factor_serial(ap, u)[0] for ap in (batch_perms if batched else [an.a_permuted])]
+        bad = [float(np.max(np.abs(g - r) / (np.abs(r) + 1e-300))) for g, r in zip(got, refs)
+               if not np.array_equal(g.view(np.int64), r.view(np.int64))]
+        parity = "bitwise" if not bad else f"max_rel={max(bad):.3e}"
 
     # CPU baseline (rank 0, N = 1): the reference's own serial factorization
     cpu = None
@@ -279,17 +304,20 @@ def run_ours(args):
         if times:
             s_med = statistics.median(times["serial"])
             cpu = {"value": nnz / s_med, "unit": UNIT, "cores": 1, "kind": "reference",
-                   "sample": "3 x factor_serial on the full matrix (reference's fastest CPU path), median",
+                   "sample": ("3 x factor_serial on one member (reference's fastest CPU path), median; "
+                              "the batch rate on 1 core is the same per member") if batched else
+                             "3 x factor_serial on the full matrix (reference's fastest CPU path), median",
                    "factor_by_blocks_pooled_s": statistics.median(times["pool"]),
                    "pooled_workers": min(os.cpu_count() or 1, 64)}
     peak, peak_kind = measured_peak()
-    bytes_alg = 20 * nnz + 8 * (n + 1)
+    bytes_alg = (20 * nnz + 8 * (n + 1)) * per_rank
     achieved = bytes_alg / (step_ms / 1e3) / 1e9
     launches_per_step = st.kernel_launches
+    units = nmembers_total * nnz if batched else world * nnz   # factor entries per step, whole job
     line = {
-        "metric": METRIC, "value": world * nnz / (step_ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "metric": METRIC, "value": units / (step_ms / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if batched else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, SURVEY.md Appendix B)",
         "config": {"workload": WORKLOADS[args.config], "n": n, "nnz_u": nnz,
                    "tasks": int(sum(ps.tasks)), "dag_depth": int(ps.dag_depth),
@@ -299,14 +327,17 @@ def run_ours(args):
                             5: "value flow / static schedule of the finalising rows"}[st.mode],
                    "flow_rows": int(ps.flow_rows), "flow_depth": int(ps.flow_depth),
                    "grid_ctas": int(st.grid_ctas), "threads_per_cta": int(st.threads_per_cta),
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "parallelism": (f"batch: {nmembers_total} members, {per_rank} on rank 0, one launch "
+                                   f"per rank" if batched else
+                                   f"replicas{world}" if world > 1 else "single"),
                    "l2": "flushed between steps (256 MiB write), U restored from device copy (untimed)",
                    "analysis_s": round(t_an, 3), "plan_s": round(ps.plan_seconds + ps.block_build_seconds, 3),
                    "parity_vs_oracle": parity},
-        "e2e": {"value": world * nnz / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz,
-                "d2h_bytes_per_step": 8 * nnz, "ms_per_step": e2e},
+        "e2e": {"value": units / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz * per_rank,
+                "d2h_bytes_per_step": 8 * nnz * per_rank, "ms_per_step": e2e},
         "gpu_launches": launches_per_step * args.steps,
-        "launches_per_step": {"prepare (untimed)": 1, "factor": 1},
+        "launches_per_step": ({"flow_prepare (timed)": 1, "factor_flow (timed)": 1} if st.mode == 5 else
+                              {"prepare (untimed)": 1, "factor": 1}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_alg},

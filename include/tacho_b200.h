@@ -140,6 +140,8 @@ typedef struct {
   uint64_t profile[7];       /* trace mode, rows: SM cycles in {pop wait, row body, publish
                                 fence, release} summed over warps; rows, pops, pushes */
   int32_t lanes_per_row;     /* mode 5: lanes per row used */
+  int32_t batch;             /* mode 5: value sets factored by the call */
+  int32_t breakdown_member;  /* batch: member of breakdown_row (-1 when none) */
 } tcg_stats;
 
 typedef struct {
@@ -197,6 +199,16 @@ tcg_status tcg_download_trace(tcg_ctx* ctx, uint64_t* stamps);
 /* Device pointer to the working values and their count (for in-process users
  * that keep U resident, e.g. a preconditioner apply on the same stream). */
 tcg_status tcg_device_values(tcg_ctx* ctx, double** dptr, int64_t* nnz);
+/* Batch of value sets sharing the uploaded pattern (mode 5; C5-style refactorization of
+ * many matrices with one structure). `values`: nbatch x nnz host doubles, member-major.
+ * nbatch = 1 returns to the single-matrix state. tcg_factor then factors every member in
+ * one launch; a breakdown skips the rest of that member only (TCG_BREAKDOWN reports the
+ * first; tcg_batch_breakdown gives each member's row, -1 = none, and pivot). */
+tcg_status tcg_set_batch(tcg_ctx* ctx, int32_t nbatch, const double* values);
+tcg_status tcg_set_batch_values(tcg_ctx* ctx, const double* values); /* same nbatch */
+int32_t tcg_batch_size(const tcg_ctx* ctx);
+tcg_status tcg_download_batch(tcg_ctx* ctx, double* values);
+tcg_status tcg_batch_breakdown(tcg_ctx* ctx, int32_t* rows, double* pivots);
 /* Bytes of the device arena. */
 int64_t tcg_arena_bytes(const tcg_ctx* ctx);
 

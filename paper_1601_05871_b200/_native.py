@@ -104,6 +104,8 @@ class Stats(C.Structure):
         ("mode", C.c_int32),
         ("profile", C.c_uint64 * 7),
         ("lanes_per_row", C.c_int32),
+        ("batch", C.c_int32),
+        ("breakdown_member", C.c_int32),
     ]
 
 
@@ -152,6 +154,11 @@ SIGNATURES = [
     ("tcg_factor", C.c_int, [C.c_void_p, C.POINTER(Stats)]),
     ("tcg_download", C.c_int, [C.c_void_p, f64p]),
     ("tcg_download_trace", C.c_int, [C.c_void_p, u64p]),
+    ("tcg_set_batch", C.c_int, [C.c_void_p, C.c_int32, f64p]),
+    ("tcg_set_batch_values", C.c_int, [C.c_void_p, f64p]),
+    ("tcg_batch_size", C.c_int32, [C.c_void_p]),
+    ("tcg_download_batch", C.c_int, [C.c_void_p, f64p]),
+    ("tcg_batch_breakdown", C.c_int, [C.c_void_p, i32p, f64p]),
     ("tcg_device_values", C.c_int, [C.c_void_p, C.POINTER(f64p), i64p]),
     ("tcg_arena_bytes", C.c_int64, [C.c_void_p]),
     ("tch_generate", C.c_void_p, [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]),

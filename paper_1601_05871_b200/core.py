@@ -460,6 +460,39 @@ class GpuFactorizer:
     def download_ptr(self, host_ptr: int):
         self._check(self._lib.tcg_download(self.ctx, C.cast(C.c_void_p(host_ptr), N.f64p)))
 
+    # ---- batch of value sets sharing the pattern (mode 5; C5) ----
+    def set_batch(self, values: np.ndarray):
+        """values: [nbatch, nnz] initial U values, one row per member."""
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        if v.ndim != 2 or v.shape[1] != self.nnz:
+            raise ValueError(f"batch values must be [nbatch, {self.nnz}]")
+        self._check(self._lib.tcg_set_batch(self.ctx, v.shape[0], v.ctypes.data_as(N.f64p)))
+
+    def set_batch_values_ptr(self, host_ptr: int):
+        self._check(self._lib.tcg_set_batch_values(self.ctx, C.cast(C.c_void_p(host_ptr), N.f64p)))
+
+    @property
+    def batch(self) -> int:
+        return int(self._lib.tcg_batch_size(self.ctx))
+
+    def download_batch(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty((self.batch, self.nnz), dtype=np.float64)
+        self._check(self._lib.tcg_download_batch(self.ctx, out.ctypes.data_as(N.f64p)))
+        return out
+
+    def download_batch_ptr(self, host_ptr: int):
+        self._check(self._lib.tcg_download_batch(self.ctx, C.cast(C.c_void_p(host_ptr), N.f64p)))
+
+    def batch_breakdown(self):
+        """Per member of the last factor: (row or -1, pivot)."""
+        b = self.batch
+        rows = np.zeros(b, np.int32)
+        piv = np.zeros(b, np.float64)
+        self._check(self._lib.tcg_batch_breakdown(self.ctx, rows.ctypes.data_as(N.i32p),
+                                                  piv.ctypes.data_as(N.f64p)))
+        return rows, piv
+
     def trace(self):
         """(task stamps [ntasks, 2], item stamps [nitems, 4]) of the last traced factor."""
         ni = int(self._problem.nitems)

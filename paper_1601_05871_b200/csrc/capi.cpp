@@ -100,6 +100,16 @@ struct tcg_ctx {
   bool has_static = false;
   int4* flow_rec = nullptr;  // value-flow schedule (mode 5)
   int* flow_item = nullptr;
+  int* m_flags = nullptr;    // per member: breakdown latch, row (2 ints) + pivot (below)
+  double* m_pivot = nullptr;
+  // batch of value sets sharing the pattern (mode 5); separate allocation
+  int nbatch = 1;
+  void* batch_arena = nullptr;
+  double* bvals = nullptr;   // nbatch x nnz working values
+  double* bvals0 = nullptr;  // nbatch x nnz initial values
+  double* ba = nullptr;      // nbatch x nnz prelude snapshot
+  int* bm_flags = nullptr;
+  double* bm_pivot = nullptr;
   int4* flow_slot = nullptr;
   int2* flow_upd = nullptr;
   double* flow_a = nullptr;  // snapshot of the input values
@@ -289,6 +299,7 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
 }
 
 void tcg_destroy(tcg_ctx* c) {
+  if (c && c->batch_arena) cudaFree(c->batch_arena);
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
@@ -331,6 +342,11 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     c->arena = nullptr;
     c->uploaded = false;
   }
+  if (c->batch_arena) {
+    TCG_CUDA_TRY(c, cudaFree(c->batch_arena));
+    c->batch_arena = nullptr;
+  }
+  c->nbatch = 1;
   // one arena: [cols][vals][vals0][tasks][items][srcs][succ][indeg][indeg0][queue][roots]
   //            [claim][fin][iflag][ctrl][trace]
   const std::int64_t qcap = p->ntasks + p->nhelpers;
@@ -377,6 +393,8 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_fslot = take(flow ? sizeof(int4) * p->nnz : 0);
   const size_t o_fupd = take(flow ? sizeof(int2) * p->nflow_upd : 0);
   const size_t o_fa = take(flow ? sizeof(double) * p->nnz : 0);
+  const size_t o_mflags = take(sizeof(int) * 2);
+  const size_t o_mpivot = take(sizeof(double));
   const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
   const size_t o_trace = take(sizeof(unsigned long long) * (2 * p->ntasks + 4 * p->nitems));
   TCG_CUDA_TRY(c, cudaMalloc(&c->arena, off));
@@ -414,6 +432,8 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->has_static = stat;
   c->flow_rec = reinterpret_cast<int4*>(base + o_frec);
   c->flow_item = reinterpret_cast<int*>(base + o_fitem);
+  c->m_flags = reinterpret_cast<int*>(base + o_mflags);
+  c->m_pivot = reinterpret_cast<double*>(base + o_mpivot);
   c->flow_slot = reinterpret_cast<int4*>(base + o_fslot);
   c->flow_upd = reinterpret_cast<int2*>(base + o_fupd);
   c->flow_a = reinterpret_cast<double*>(base + o_fa);
@@ -498,6 +518,9 @@ tcg_status tcg_restore(tcg_ctx* c) {
   if (!c || !c->uploaded) return TCG_INVALID;
   if (c->nnz == 0) return TCG_OK;
   TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->nbatch > 1)
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals, c->bvals0, sizeof(double) * c->nnz * c->nbatch,
+                                    cudaMemcpyDeviceToDevice, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals, c->vals0, sizeof(double) * c->nnz,
                                   cudaMemcpyDeviceToDevice, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -524,21 +547,36 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads) {
   }
   if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
   const int grid = std::max(1, occ * c->sm_count);
+  const bool batch = c->nbatch > 1;
+  if (static_cast<int64_t>(c->nflow) * c->nbatch > 0x7fffffffLL) {
+    c->err = "value-flow batch: rows x members beyond 2^31";
+    return TCG_INVALID;
+  }
+  double* const vals = batch ? c->bvals : c->vals;
   tcbdev::FlowPrepParams q{};
-  q.vals = c->vals;
-  q.a = c->flow_a;
-  q.out = c->vals;
-  q.nnz = c->nnz;
+  q.vals = vals;
+  q.a = batch ? c->ba : c->flow_a;
+  q.out = vals;
+  q.nnz = c->nnz * c->nbatch;
   q.ctrl = c->ctrl;
+  q.m_failed = batch ? c->bm_flags : c->m_flags;
+  q.m_row = q.m_failed + c->nbatch;
+  q.m_pivot = batch ? c->bm_pivot : c->m_pivot;
+  q.nbatch = c->nbatch;
   tcbdev::FlowParams P{};
   P.rec = c->flow_rec;
   P.item = c->flow_item;
   P.slot = c->flow_slot;
   P.upd = c->flow_upd;
-  P.a = c->flow_a;
-  P.vals = c->vals;
+  P.a = q.a;
+  P.vals = vals;
   P.ctrl = c->ctrl;
   P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
+  P.m_failed = q.m_failed;
+  P.m_row = q.m_row;
+  P.m_pivot = q.m_pivot;
+  P.nnz = c->nnz;
+  P.nbatch = c->nbatch;
   P.nrows = static_cast<int>(c->nflow);
   const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
@@ -559,22 +597,26 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads) {
   S.kernel_launches = c->nflow > 0 ? 2 : 1;
   S.mode = 5;
   S.lanes_per_row = g;
-  S.tasks_completed = (h.done.v == c->nflow) ? c->ntasks : 0;
+  const int64_t rows = c->nflow * c->nbatch;
+  S.tasks_completed = (h.done.v == rows) ? c->ntasks * c->nbatch : 0;
   S.tasks_executed = h.executed.v;
+  S.batch = c->nbatch;
   if (h.error.v) {
     c->err = "device watchdog expired: the value-flow schedule stalled";
     return TCG_TIMEOUT;
   }
-  if (h.done.v != c->nflow) {
+  if (h.done.v != rows) {
     c->err = "value-flow schedule finished " + std::to_string(h.done.v) + " of " +
-             std::to_string(c->nflow) + " rows";
+             std::to_string(rows) + " rows";
     return TCG_TIMEOUT;
   }
   if (h.failed.v) {
     S.breakdown_row = h.fail_row;
     S.breakdown_pivot = h.fail_pivot;
+    S.breakdown_member = h.fail_member;
     c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
-             std::to_string(h.fail_pivot) + " is not positive";
+             std::to_string(h.fail_pivot) + " is not positive" +
+             (batch ? " (member " + std::to_string(h.fail_member) + ")" : std::string());
     return TCG_BREAKDOWN;
   }
   return TCG_OK;
@@ -735,11 +777,14 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   tcg_stats& S = st ? *st : local;
   S = tcg_stats{};
   S.breakdown_row = -1;
+  S.breakdown_member = -1;
+  S.batch = 1;
   if (c->ntasks == 0) return TCG_OK;
   TCG_CUDA_TRY(c, cudaSetDevice(c->device));
 
   const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
   int mode = c->opt.mode;
+  if (mode == 0 && c->nbatch > 1 && c->has_flow) mode = 5;
   if (mode == 0) {
     // value flow unless the programs are long (mean products per coordinate
     // above 16, e.g. C3): there the finalising rows' serial gathers dominate
@@ -751,6 +796,10 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   if ((mode == 2 && !c->has_programs) || (mode == 3 && !c->has_rows) ||
       (mode == 4 && !c->has_static) || (mode == 5 && !c->has_flow) || mode < 0 || mode > 5) {
     c->err = "requested execution mode is not available for the uploaded problem";
+    return TCG_INVALID;
+  }
+  if (mode != 5 && c->nbatch > 1) {
+    c->err = "a batch of value sets needs mode 5 (value flow)";
     return TCG_INVALID;
   }
   if (mode != 5 && (threads == 384 || threads == 768)) {
@@ -879,6 +928,75 @@ tcg_status tcg_download(tcg_ctx* c, double* values) {
   TCG_CUDA_TRY(c, cudaSetDevice(c->device));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(values, c->vals, sizeof(double) * c->nnz,
                                   cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {
+  if (!c || !c->uploaded || nbatch < 1 || (!values && c->nnz > 0)) return TCG_INVALID;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (c->batch_arena) {
+    TCG_CUDA_TRY(c, cudaFree(c->batch_arena));
+    c->batch_arena = nullptr;
+  }
+  c->nbatch = 1;
+  if (nbatch == 1) return tcg_set_values(c, values);
+  if (!c->has_flow) {
+    c->err = "tcg_set_batch: the plan has no value-flow tables (mode 5)";
+    return TCG_INVALID;
+  }
+  const size_t vb = sizeof(double) * static_cast<size_t>(c->nnz) * nbatch;
+  const size_t fb = align_up(sizeof(int) * 2 * nbatch, 256);
+  const size_t bytes = 3 * align_up(vb, 256) + fb + sizeof(double) * nbatch;
+  TCG_CUDA_TRY(c, cudaMalloc(&c->batch_arena, bytes));
+  char* base = static_cast<char*>(c->batch_arena);
+  c->bvals = reinterpret_cast<double*>(base);
+  c->bvals0 = reinterpret_cast<double*>(base + align_up(vb, 256));
+  c->ba = reinterpret_cast<double*>(base + 2 * align_up(vb, 256));
+  c->bm_flags = reinterpret_cast<int*>(base + 3 * align_up(vb, 256));
+  c->bm_pivot = reinterpret_cast<double*>(base + 3 * align_up(vb, 256) + fb);
+  c->nbatch = nbatch;
+  if (vb) {
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals0, values, vb, cudaMemcpyHostToDevice, c->stream));
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals, c->bvals0, vb, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_set_batch_values(tcg_ctx* c, const double* values) {
+  if (!c || !c->uploaded || (!values && c->nnz > 0)) return TCG_INVALID;
+  if (c->nbatch == 1) return tcg_set_values(c, values);
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  const size_t vb = sizeof(double) * static_cast<size_t>(c->nnz) * c->nbatch;
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals0, values, vb, cudaMemcpyHostToDevice, c->stream));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals, c->bvals0, vb, cudaMemcpyDeviceToDevice, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+int32_t tcg_batch_size(const tcg_ctx* c) { return c ? c->nbatch : 0; }
+
+tcg_status tcg_download_batch(tcg_ctx* c, double* values) {
+  if (!c || !c->uploaded || (!values && c->nnz > 0)) return TCG_INVALID;
+  if (c->nbatch == 1) return tcg_download(c, values);
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(values, c->bvals, sizeof(double) * c->nnz * c->nbatch,
+                                  cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_batch_breakdown(tcg_ctx* c, int32_t* rows, double* pivots) {
+  if (!c || !c->uploaded || !rows || !pivots) return TCG_INVALID;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  const int* flags = c->nbatch > 1 ? c->bm_flags : c->m_flags;
+  const double* piv = c->nbatch > 1 ? c->bm_pivot : c->m_pivot;
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(rows, flags + c->nbatch, sizeof(int) * c->nbatch,
+                                  cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(pivots, piv, sizeof(double) * c->nbatch, cudaMemcpyDeviceToHost,
+                                  c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return TCG_OK;
 }

@@ -33,7 +33,7 @@ struct Ctrl {
   Line executed;     // task (row) bodies actually run (skipped after a breakdown)
   Line helpers_run;  // helper tickets that joined a multi-CTA task
   int fail_row;
-  int pad0;
+  int fail_member;   // mode 5 batch: member of the first breakdown
   double fail_pivot;
   // trace mode, row kernel: per-phase SM cycles summed over warps
   // {pop wait, row body, publish fence, release, rows, pops, pushes, 0}
@@ -110,11 +110,16 @@ struct FlowParams {
   const int* item;       // per position: its item (trace only)
   const int4* slot;      // per coordinate of U: {u_b, u_e, m0, o0}
   const int2* upd;       // (m, o) pairs
-  const double* a;       // input values (snapshot taken by the prelude)
-  double* vals;          // output; kUnset until the owning row writes it
+  const double* a;       // input values (snapshot taken by the prelude), nbatch x nnz
+  double* vals;          // output; kUnset until the owning row writes it; nbatch x nnz
   Ctrl* ctrl;
-  unsigned long long* trace;  // optional: {start, end} per item
-  int nrows;
+  unsigned long long* trace;  // optional: {start, end} per item (member 0)
+  int* m_failed;         // per member: breakdown latch, row, pivot
+  int* m_row;
+  double* m_pivot;
+  long long nnz;         // values per member
+  int nrows;             // schedule rows (per member)
+  int nbatch;            // members sharing the pattern
   unsigned long long timeout_ns;
 };
 
@@ -122,7 +127,11 @@ struct FlowPrepParams {
   const double* vals;    // working values (input of the factorization)
   double* a;             // snapshot of them
   double* out;           // = vals in place: set to kUnset
-  long long nnz;
+  long long nnz;         // all members
+  int* m_failed;         // reset per member
+  int* m_row;
+  double* m_pivot;
+  int nbatch;
   Ctrl* ctrl;
 };
 

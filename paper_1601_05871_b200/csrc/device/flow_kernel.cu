@@ -53,17 +53,22 @@ __device__ __forceinline__ unsigned long long wait_value(const double* p, Ctrl* 
 // holds kUnset until its single final value is written: any other bits a
 // load returns are the final value (8-byte aligned accesses do not tear),
 // and a stale L1 copy can only show kUnset, which the strong path re-reads.
+// `vals`/`a`/`member`: the current row's member of a batch (its value sets
+// are nnz apart; the pattern, records and programs are shared).
 template <int WEAK>
 struct Ctx {
   const FlowParams& P;
   unsigned long long t0;
+  double* vals;
+  const double* a;
+  int member;
   __device__ __forceinline__ double settle(const double* p, unsigned long long x) const {
     if (x == kUnset) x = wait_value(p, P.ctrl, t0, P.timeout_ns);
     return __longlong_as_double(static_cast<long long>(x));
   }
   __device__ __forceinline__ unsigned long long ld(int pos) const {
-    if (WEAK) return ld_weak_u64(P.vals + pos);
-    return ld_relaxed_u64(P.vals + pos);
+    if (WEAK) return ld_weak_u64(vals + pos);
+    return ld_relaxed_u64(vals + pos);
   }
 };
 
@@ -80,7 +85,7 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
   int2 p[KB];
 #pragma unroll
   for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
-  v = __dsub_rn(v, __dmul_rn(C.settle(C.P.vals + sr.z, xa0), C.settle(C.P.vals + sr.w, xb0)));
+  v = __dsub_rn(v, __dmul_rn(C.settle(C.vals + sr.z, xa0), C.settle(C.vals + sr.w, xb0)));
   while (u < ue) {
     const int n = min(KB, ue - u);
     unsigned long long xa[KB], xb[KB];
@@ -97,8 +102,8 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 #pragma unroll
     for (int j = 0; j < KB; ++j)
       if (j < n)
-        v = __dsub_rn(v, __dmul_rn(C.settle(C.P.vals + c[j].x, xa[j]),
-                                   C.settle(C.P.vals + c[j].y, xb[j])));
+        v = __dsub_rn(v, __dmul_rn(C.settle(C.vals + c[j].x, xa[j]),
+                                   C.settle(C.vals + c[j].y, xb[j])));
   }
   return v;
 }
@@ -119,24 +124,29 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
   double d;
   if (KIND == kChol) {
     const double piv = __shfl_sync(gmask, v, lead);
-    if (!(piv > 0.0) && gl == 0) {
+    if (!(piv > 0.0) && gl == 0) {  // first breakdown of the member, and of the launch
+      if (atomicCAS(P.m_failed + C.member, 0, 1) == 0) {
+        P.m_row[C.member] = t;
+        P.m_pivot[C.member] = piv;
+      }
       if (atomicCAS(&P.ctrl->failed.v, 0, 1) == 0) {
         P.ctrl->fail_row = t;
         P.ctrl->fail_pivot = piv;
+        P.ctrl->fail_member = C.member;
       }
     }
     d = __dsqrt_rn(piv);
   } else {
-    d = C.settle(P.vals + dpos, xd);
+    d = C.settle(C.vals + dpos, xd);
   }
   auto finish = [&](int k, double x) {
     const double y = (KIND == kChol && k == 0) ? d : __ddiv_rn(x, d);
     return static_cast<unsigned long long>(__double_as_longlong(y));
   };
-  if (gl < L) st_relaxed_u64(P.vals + tb + gl, finish(gl, v));
+  if (gl < L) st_relaxed_u64(C.vals + tb + gl, finish(gl, v));
   for (int k = gl + G; k < L; k += G) {
-    const double w = flow_slot<KB>(C, __ldg(P.a + tb + k), __ldg(P.slot + tb + k));
-    st_relaxed_u64(P.vals + tb + k, finish(k, w));
+    const double w = flow_slot<KB>(C, __ldg(C.a + tb + k), __ldg(P.slot + tb + k));
+    st_relaxed_u64(C.vals + tb + k, finish(k, w));
   }
 }
 
@@ -160,8 +170,15 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
   const int lead = lane & ~(G - 1);
   const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << lead);
   const int W = gridDim.x * kGroups;
-  const Ctx<WEAK> C{P, gtimer()};
-  int ran = 0, executed = 0, latched = 0;
+  Ctx<WEAK> C{P, gtimer(), P.vals, P.a, 0};
+  int ran = 0, executed = 0, anyfail = 0;
+  // batch: position pos is schedule row pos / nbatch of member pos % nbatch
+  // (the members of one row sit side by side, so level order is kept)
+  const int nrows = P.nrows * P.nbatch;
+  auto member_of = [&](int p, int& q) {
+    q = P.nbatch == 1 ? p : p / P.nbatch;
+    return p - q * P.nbatch;
+  };
   __shared__ int s_next;
   if (DYN) {
     if (threadIdx.x == 0) s_next = 0;
@@ -182,28 +199,49 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
   const int4 z = make_int4(0, 0, 0, 0);
   int4 a = z, na = z, sr0 = z;
   double a0 = 0.0;
-  if (pos < P.nrows) {
-    a = __ldg(P.rec + pos);
+  auto rec_of = [&](int p) {
+    int q;
+    member_of(p, q);
+    return __ldg(P.rec + q);
+  };
+  auto input_of = [&](int p) {
+    int q;
+    return P.a + static_cast<long long>(member_of(p, q)) * P.nnz;
+  };
+  if (pos < nrows) {
+    a = rec_of(pos);
     if (gl < (a.y & kLenMask)) {
       sr0 = __ldg(P.slot + a.x + gl);
-      a0 = __ldg(P.a + a.x + gl);
+      a0 = __ldg(input_of(pos) + a.x + gl);
     }
   }
-  if (npos < P.nrows) na = __ldg(P.rec + npos);
-  while (pos < P.nrows) {
-    const int nnpos = npos < P.nrows ? grab(npos) : npos;
-    const int4 nna = nnpos < P.nrows ? __ldg(P.rec + nnpos) : z;
+  if (npos < nrows) na = rec_of(npos);
+  while (pos < nrows) {
+    const int nnpos = npos < nrows ? grab(npos) : npos;
+    const int4 nna = nnpos < nrows ? rec_of(nnpos) : z;
     int4 nsr0 = z;
     double na0 = 0.0;
-    if (npos < P.nrows && gl < (na.y & kLenMask)) {
+    if (npos < nrows && gl < (na.y & kLenMask)) {
       nsr0 = __ldg(P.slot + na.x + gl);
-      na0 = __ldg(P.a + na.x + gl);
+      na0 = __ldg(input_of(npos) + na.x + gl);
     }
     const int tb = a.x, L = a.y & kLenMask, dpos = a.z, t = a.w;
     const bool chol = (static_cast<unsigned>(a.y) >> 30) == kChol;
-    if (P.trace && gl == 0) P.trace[2 * static_cast<long long>(P.item[pos])] = gtimer();
-    if ((ran & 15) == 0) {  // breakdown: skip the rest (one decision per group)
-      latched = gl == 0 ? ld_relaxed(&P.ctrl->failed.v) : 0;
+    int q;
+    C.member = member_of(pos, q);
+    C.vals = P.vals + static_cast<long long>(C.member) * P.nnz;
+    C.a = P.a + static_cast<long long>(C.member) * P.nnz;
+    const bool traced = P.trace && gl == 0 && C.member == 0;
+    if (traced) P.trace[2 * static_cast<long long>(P.item[q])] = gtimer();
+    // breakdown (reference factorize.hpp:146-167): the member's later rows
+    // are skipped; one decision per group
+    if ((ran & 15) == 0) {
+      anyfail = gl == 0 ? ld_relaxed(&P.ctrl->failed.v) : 0;
+      anyfail = __shfl_sync(gmask, anyfail, lead);
+    }
+    int latched = 0;
+    if (anyfail) {
+      latched = gl == 0 ? ld_relaxed(P.m_failed + C.member) : 0;
       latched = __shfl_sync(gmask, latched, lead);
     }
     if (!latched) {
@@ -215,11 +253,11 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
     } else {
       // skipped rows keep their input values (readers must not wait forever)
       for (int k = gl; k < L; k += G) {
-        unsigned long long x = static_cast<unsigned long long>(__double_as_longlong(P.a[tb + k]));
-        st_relaxed_u64(P.vals + tb + k, x == kUnset ? kCanonicalNaN : x);
+        unsigned long long x = static_cast<unsigned long long>(__double_as_longlong(C.a[tb + k]));
+        st_relaxed_u64(C.vals + tb + k, x == kUnset ? kCanonicalNaN : x);
       }
     }
-    if (P.trace && gl == 0) P.trace[2 * static_cast<long long>(P.item[pos]) + 1] = gtimer();
+    if (traced) P.trace[2 * static_cast<long long>(P.item[q]) + 1] = gtimer();
     ++ran;
     pos = npos;
     npos = nnpos;
@@ -247,6 +285,11 @@ __global__ void flow_prepare(FlowPrepParams Q) {
     a2[x] = in2[x];
     o2[x] = make_double2(unset, unset);
   }
+  for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < Q.nbatch; x += stride) {
+    Q.m_failed[x] = 0;
+    Q.m_row[x] = -1;
+    Q.m_pivot[x] = 0.0;
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (Q.nnz & 1) {
       Q.a[Q.nnz - 1] = Q.vals[Q.nnz - 1];
@@ -254,6 +297,7 @@ __global__ void flow_prepare(FlowPrepParams Q) {
     }
     Ctrl c = {};
     c.fail_row = -1;
+    c.fail_member = -1;
     *Q.ctrl = c;
   }
 }

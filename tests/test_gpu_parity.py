@@ -283,3 +283,66 @@ def test_cpp_dropin_with_reference_types():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "bitwise=1" in r.stdout
+
+
+def c5_members(T, members):
+    """Initial U values of C5 members (shared ordering, pattern and plan)."""
+    _, an = analyzed("c5_m0")
+    vals, perms = [], []
+    for m in members:
+        a, _ = T.config_matrix("c5", m)
+        ap = T.analyze(a, level=1).a_permuted
+        assert np.array_equal(ap.col_idx, an.a_permuted.col_idx)
+        vals.append(T.init_factor_values(ap, an.pattern))
+        perms.append(ap)
+    return an, np.stack(vals), perms
+
+
+def test_c5_batch_one_launch_bitwise(T, oracle):
+    # C5: many matrices with one structure, factored in one launch (mode 5)
+    members = list(range(6))
+    an, vals, perms = c5_members(T, members)
+    fz = T.GpuFactorizer(planned("c5_m0"), T.GpuOptions(timeout_s=30))
+    try:
+        fz.set_batch(vals)
+        assert fz.batch == len(members)
+        st = fz.factor()
+        assert st.mode == 5 and st.batch == len(members) and st.kernel_launches == 2
+        out = fz.download_batch()
+        for i, ap in enumerate(perms):
+            ref, status, _, _ = oracle.factor_serial(ap, an.pattern.pattern)
+            assert status == 0
+            assert bitwise_equal(out[i], ref), i
+        rows, _ = fz.batch_breakdown()
+        assert np.all(rows == -1)
+        # refactor after restore gives the same bits; back to one matrix works
+        fz.restore()
+        fz.factor()
+        assert bitwise_equal(fz.download_batch(), out)
+        fz.set_batch(vals[:1])
+        assert fz.batch == 1
+        fz.factor()
+        assert bitwise_equal(fz.download(), out[0])
+    finally:
+        fz.close()
+
+
+def test_c5_batch_breakdown_is_per_member(T, oracle):
+    an, vals, perms = c5_members(T, [0, 1, 2])
+    u = an.pattern.pattern
+    row = 1000
+    vals[1, u.row_ptr[row]] = -1.0  # member 1: negative pivot at `row`
+    fz = T.GpuFactorizer(planned("c5_m0"), T.GpuOptions(timeout_s=30))
+    try:
+        fz.set_batch(vals)
+        with pytest.raises(T.BreakdownError) as e:
+            fz.factor()
+        assert e.value.row == row and fz.last.breakdown_member == 1
+        rows, piv = fz.batch_breakdown()
+        assert list(rows) == [-1, row, -1] and piv[1] < 0
+        out = fz.download_batch()
+        for i in (0, 2):
+            ref, _, _, _ = oracle.factor_serial(perms[i], u)
+            assert bitwise_equal(out[i], ref), i
+    finally:
+        fz.close()

@@ -1,0 +1,79 @@
+"""N > 1 host logic on CPU: two `gloo` ranks run the C5 batch sharding of
+bench.py (`--config c5b`) -- member split, per-rank value sets on the shared
+structure, max-over-ranks timing -- with the CPU oracle standing in for the
+device factorization (test-only; the product path has no CPU fallback)."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def worker(rank, world, port, nmembers, out_dir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, HERE)
+    import torch.distributed as dist
+
+    from checkers import Oracle
+    from paper_1601_05871_b200 import batch
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    mine = batch.shard(nmembers, rank, world)
+    an, vals, perms = batch.member_values(list(mine))
+    O = Oracle()
+    hashes = {}
+    for m, ap, v in zip(mine, perms, vals):
+        ref, st, _, _ = O.factor_serial(ap, an.pattern.pattern)
+        assert st == 0
+        hashes[m] = O.hash(ref)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (list(mine), hashes))
+    t = batch.max_over_ranks(1.0 + rank)
+    if rank == 0:
+        with open(os.path.join(out_dir, "result.txt"), "w") as f:
+            f.write(repr((gathered, t)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("nmembers", [5])
+def test_two_rank_c5_batch_sharding(tmp_path, nmembers):
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(worker, args=(world, free_port(), nmembers, str(tmp_path)), nprocs=world, join=True)
+    gathered, t = eval(open(tmp_path / "result.txt").read())
+    assert t == 2.0  # max over ranks
+    owned = [m for ms, _ in gathered for m in ms]
+    assert sorted(owned) == list(range(nmembers))  # disjoint and complete
+    assert [len(ms) for ms, _ in gathered] == [3, 2]
+    # every rank's factors equal the single-process ones
+    sys.path.insert(0, HERE)
+    from checkers import Oracle
+    from paper_1601_05871_b200 import batch
+    an, _, perms = batch.member_values(range(nmembers))
+    O = Oracle()
+    merged = {m: h for _, hs in gathered for m, h in hs.items()}
+    for m, ap in enumerate(perms):
+        assert merged[m] == O.hash(O.factor_serial(ap, an.pattern.pattern)[0])
+
+
+def test_shard_sizes():
+    from paper_1601_05871_b200 import batch
+    for n, w in [(64, 1), (64, 2), (64, 8), (10, 3), (3, 8)]:
+        parts = [batch.shard(n, r, w) for r in range(w)]
+        assert sum(len(p) for p in parts) == n
+        assert max(len(p) for p in parts) - min(len(p) for p in parts) <= 1
+        assert [x for p in parts for x in p] == list(range(n))
+    with pytest.raises(ValueError):
+        batch.shard(4, 2, 2)
