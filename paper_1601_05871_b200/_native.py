@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtacho_b200.so")
+# TCG_LIB_DIR: load an alternative in-tree build (A/B experiments under tools/)
+LIB_PATH = os.path.join(os.environ.get("TCG_LIB_DIR") or os.path.join(_HERE, "lib"), "libtacho_b200.so")
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)

@@ -115,7 +115,8 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 // `gmask` the group's lanes, `lead` its first lane.
 template <int KIND, int KB, int G, class Cx>
 __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, int t, int gl,
-                                         unsigned gmask, int lead, double a0, int4 sr0) {
+                                         unsigned gmask, int lead, double a0, int4 sr0,
+                                         unsigned long long* stamp) {
   const FlowParams& P = C.P;
   unsigned long long xd = 0;
   if (KIND == kTrsm) xd = C.ld(dpos);
@@ -138,6 +139,10 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
     d = __dsqrt_rn(piv);
   } else {
     d = C.settle(C.vals + dpos, xd);
+  }
+  if (stamp) {  // trace: every operand of the first G coordinates is final
+    __syncwarp(gmask);
+    if (gl == 0) *stamp = gtimer();
   }
   auto finish = [&](int k, double x) {
     const double y = (KIND == kChol && k == 0) ? d : __ddiv_rn(x, d);
@@ -232,7 +237,9 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
     C.vals = P.vals + static_cast<long long>(C.member) * P.nnz;
     C.a = P.a + static_cast<long long>(C.member) * P.nnz;
     const bool traced = P.trace && gl == 0 && C.member == 0;
-    if (traced) P.trace[2 * static_cast<long long>(P.item[q])] = gtimer();
+    // trace: per item {start, operands final, 0, end} (4 words, member 0)
+    unsigned long long* stamp = P.trace && C.member == 0 ? P.trace + 4 * static_cast<long long>(P.item[q]) : nullptr;
+    if (traced) stamp[0] = gtimer();
     // breakdown (reference factorize.hpp:146-167): the member's later rows
     // are skipped; one decision per group
     if ((ran & 15) == 0) {
@@ -246,9 +253,9 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
     }
     if (!latched) {
       if (chol)
-        flow_row<kChol, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0);
+        flow_row<kChol, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr);
       else
-        flow_row<kTrsm, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0);
+        flow_row<kTrsm, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr);
       ++executed;
     } else {
       // skipped rows keep their input values (readers must not wait forever)
@@ -257,7 +264,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
         st_relaxed_u64(C.vals + tb + k, x == kUnset ? kCanonicalNaN : x);
       }
     }
-    if (traced) P.trace[2 * static_cast<long long>(P.item[q]) + 1] = gtimer();
+    if (traced) stamp[3] = gtimer();
     ++ran;
     pos = npos;
     npos = nnpos;

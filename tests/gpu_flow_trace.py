@@ -24,10 +24,9 @@ _, items = fz.trace()
 fz.close()
 t = plan.tables()
 rec, order, slot, upd = t["flow_rec"], t["flow_item"], t["flow_slot"], t["flow_upd"]
-ni = len(t["row_rec"])
-stamps = items.reshape(-1)[:2 * ni].reshape(-1, 2)[order].astype(np.int64)  # per position
+stamps = items[order].astype(np.int64)  # per schedule position: start, operands final, -, end
 t0 = stamps[:, 0].min()
-s, e = stamps[:, 0] - t0, stamps[:, 1] - t0
+s, r, e = stamps[:, 0] - t0, stamps[:, 1] - t0, stamps[:, 3] - t0
 npos = len(rec)
 W = st.grid_ctas * st.threads_per_cta // 32
 L = rec[:, 1] & ((1 << 30) - 1)
@@ -35,8 +34,7 @@ kind = (rec[:, 1] >> 30) & 3
 owner = np.full(len(t["values"]), -1, np.int64)
 for q in range(npos):
     owner[rec[q, 0]:rec[q, 0] + L[q]] = q
-# ready time of each position: latest end among the positions it reads
-ready = np.zeros(npos, np.int64)
+ready = np.zeros(npos, np.int64)  # latest end among the rows it reads
 src_of = np.full(npos, -1, np.int64)
 for q in range(npos):
     tb = rec[q, 0]
@@ -47,41 +45,35 @@ for q in range(npos):
     if len(srcs):
         m = srcs[np.argmax(e[srcs])]
         ready[q], src_of[q] = e[m], m
-wp, order_w, makespan = plan.flow_schedule(W)  # the assignment tcg_factor laid out
-prev = np.full(npos, -1, np.int64)  # previous position of the same warp
-for w in range(W):
-    seq = order_w[wp[w]:wp[w + 1]]
-    prev[seq[1:]] = seq[:-1]
-busy = np.where(prev >= 0, e[np.maximum(prev, 0)], 0)
-print(f"simulated makespan {makespan:.1f} us")
-print(f"{name}: kernel {st.device_ms:.3f} ms, {npos} rows, {W} warps, span {(e.max()) / 1e3:.1f} us")
-dur = e - s
-print(f"row time (start..end) us: median {np.median(dur) / 1e3:.2f}  p90 {np.percentile(dur, 90) / 1e3:.2f}  "
-      f"mean {dur.mean() / 1e3:.2f}")
-after_ready = e - np.maximum(ready, s)
-print(f"end - max(ready, start) us: median {np.median(after_ready) / 1e3:.2f}  p90 "
-      f"{np.percentile(after_ready, 90) / 1e3:.2f}")
+prev = np.arange(npos) - W
+print(f"{name}: kernel {st.device_ms:.3f} ms, {npos} rows, {W} warps, span {e.max() / 1e3:.1f} us")
+pct = lambda x: f"median {np.median(x) / 1e3:.2f} p90 {np.percentile(x, 90) / 1e3:.2f} us"
+print("start -> operands final:", pct(r - s))
+print("operands final -> end:  ", pct(e - r))
+late = ready > s
+print(f"rows whose last producer ended after they started: {late.mean():.1%}; "
+      f"producer end -> operands final {pct((r - ready)[late])}")
 # walk the realised critical path back from the last row
 q = int(np.argmax(e))
-data = warp = 0
-tdata = twarp = 0
-steps = []
+acc = {"hop (producer end -> operands final)": 0, "row tail (operands final -> end)": 0,
+       "gather after start (operands already final)": 0, "warp busy (previous row of the warp)": 0}
+n = {k: 0 for k in acc}
 while q >= 0:
-    if src_of[q] >= 0 and ready[q] >= busy[q]:
-        nq, kind_step = src_of[q], "data"
-    elif prev[q] >= 0:
-        nq, kind_step = prev[q], "warp"
+    acc["row tail (operands final -> end)"] += e[q] - r[q]
+    if src_of[q] >= 0 and ready[q] > s[q]:
+        acc["hop (producer end -> operands final)"] += r[q] - ready[q]
+        n["hop (producer end -> operands final)"] += 1
+        q = src_of[q]
     else:
-        break
-    dt = e[q] - e[nq]
-    if kind_step == "data":
-        data += 1
-        tdata += dt
-    else:
-        warp += 1
-        twarp += dt
-    steps.append((kind_step, int(kind[q]), dt))
-    q = nq
-print(f"critical path: {data} data hops ({tdata / 1e3:.1f} us), {warp} warp-order hops ({twarp / 1e3:.1f} us)")
+        acc["gather after start (operands already final)"] += r[q] - s[q]
+        n["gather after start (operands already final)"] += 1
+        if prev[q] >= 0 and e[prev[q]] <= s[q] + 2000:
+            acc["warp busy (previous row of the warp)"] += s[q] - e[prev[q]]
+            n["warp busy (previous row of the warp)"] += 1
+            q = prev[q]
+        else:
+            break
+for k in acc:
+    print(f"  {k:48s} {acc[k] / 1e3:8.1f} us  ({n[k]} steps)")
 if len(sys.argv) > 2:
-    np.savez_compressed(sys.argv[2], s=s, e=e, ready=ready, src=src_of, kind=kind, L=L, W=W)
+    np.savez_compressed(sys.argv[2], s=s, r=r, e=e, ready=ready, src=src_of, kind=kind, L=L, W=W)

@@ -110,6 +110,39 @@ __global__ void st_ld(double* data, int n, unsigned long long* out) {
   if (acc == -1) data[0] = acc;
 }
 
+// 7. cross-SM hand-off through the value itself (mode 5): round r's consumer
+// polls data[r-1] with 64-bit ld.relaxed.gpu until it is no longer the
+// marker, then stores data[r] with st.relaxed.gpu. One round = one hand-off.
+__global__ void flow_pingpong(unsigned long long* data, int rounds, unsigned long long* out) {
+  const int b = blockIdx.x;
+  unsigned long long t0 = clk();
+  unsigned long long acc = 0;
+  for (int r = 0; r < rounds; ++r) {
+    if (b == (r & 1) && threadIdx.x == 0) {
+      if (r > 0) {
+        unsigned long long v;
+        do { asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(data + r - 1)); } while (v == ~0ull);
+        acc += v;
+      }
+      asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(data + r), "l"(acc + r) : "memory");
+    }
+  }
+  unsigned long long t1 = clk();
+  if (threadIdx.x == 0 && b == 0) out[0] = (t1 - t0) / rounds;
+  if (acc == 12345) data[0] = acc;
+}
+
+// 8. dependent chase with 64-bit ld.relaxed.gpu (the mode-5 gather load)
+__global__ void chase_strong(const unsigned long long* next, int steps, unsigned long long* out, int* sink) {
+  unsigned long long p = 0;
+  unsigned long long t0 = clk();
+  for (int i = 0; i < steps; ++i)
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(p) : "l"(next + p));
+  unsigned long long t1 = clk();
+  out[0] = (t1 - t0) / steps;
+  sink[0] = static_cast<int>(p);
+}
+
 int main() {
   unsigned long long* out;
   cudaMallocManaged(&out, 64);
@@ -144,6 +177,24 @@ int main() {
   pingpong_gpu<<<2, 32>>>(data, flags, 2000, out);
   cudaDeviceSynchronize();
   printf("cross-SM write->fence->flag->read round: %llu cycles\n", out[0]);
+  {
+    const int R = 4000;
+    unsigned long long* d;
+    cudaMalloc(&d, sizeof(unsigned long long) * R);
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaMemset(d, 0xff, sizeof(unsigned long long) * R);
+      flow_pingpong<<<2, 32>>>(d, R, out);
+      cudaDeviceSynchronize();
+    }
+    printf("cross-SM value hand-off (st.relaxed -> ld.relaxed poll): %llu cycles/round\n", out[0]);
+    unsigned long long* nx;
+    cudaMallocManaged(&nx, sizeof(unsigned long long) * M);
+    for (int i = 0; i < M; ++i) nx[i] = (unsigned long long)((i * 2654435761u + 12345) % M);
+    chase_strong<<<1, 1>>>(nx, 20000, out, sink);
+    chase_strong<<<1, 1>>>(nx, 20000, out, sink);
+    cudaDeviceSynchronize();
+    printf("L2 pointer chase (512 KB, ld.relaxed.gpu.b64): %llu cycles/load\n", out[0]);
+  }
   int* x;
   cudaMalloc(&x, 64);
   atom_lat<<<1, 1>>>(x, 10000, out);

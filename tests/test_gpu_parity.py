@@ -70,8 +70,8 @@ def test_flow_trace_stamps_every_finalising_row(T):
     _, items = fz.trace()
     fz.close()
     t = plan.tables()
-    st = items.reshape(-1)[:2 * len(t["row_rec"])].reshape(-1, 2)[t["flow_item"]]
-    assert np.all(st[:, 0] > 0) and np.all(st[:, 0] <= st[:, 1])
+    st = items[t["flow_item"]]  # {start, operands final, -, end}
+    assert np.all(st[:, 0] > 0) and np.all(st[:, 0] <= st[:, 1]) and np.all(st[:, 1] <= st[:, 3])
 
 
 def test_static_trace_respects_every_row_edge(T):
