@@ -106,6 +106,22 @@ typedef struct {
   const int32_t* flow_slot;    /*   4 words per coordinate of U: u_b, u_e, m0, o0 */
   int64_t nflow_upd;
   const int32_t* flow_upd;     /*   (m, o) pairs */
+  /* block units (optional; mode 6): large diagonal blocks run as CTA-wide units with their
+   * values in shared memory; rows outside units as in mode 5 */
+  int64_t m6_nrows;
+  const int32_t* m6_row_rec;   /*   4 words per row outside units, in schedule order */
+  const int32_t* m6_row_item;
+  int64_t m6_nunits;
+  const int32_t* m6_unit_rec;  /*   4 words per unit: level slot begin, end, first row, order */
+  int64_t m6_nurows;
+  const int32_t* m6_urow_rec;  /*   4 words per unit row, by intra-unit level */
+  const int32_t* m6_urow_lbase;/*   first shared-memory index of the row's values */
+  const int32_t* m6_urow_item;
+  int64_t m6_nlev;
+  const int32_t* m6_ulev;      /*   per level slot: end of its rows */
+  const int32_t* m6_slot;      /*   flow_slot with intra-unit operands as 0x80000000|index */
+  const int32_t* m6_upd;       /*   nflow_upd pairs, same rewrite */
+  int64_t m6_smem;             /*   bytes of the largest unit */
 } tcg_problem;
 
 typedef struct {
@@ -158,6 +174,9 @@ typedef struct {
   double block_build_seconds, plan_seconds;
   int64_t flow_rows;         /* value-flow rows (mode 5) */
   int32_t flow_depth;        /* longest value-flow chain, in rows */
+  int64_t unit_count, unit_rows;   /* mode 6 block units and the rows inside them */
+  int32_t unit_depth;        /* longest chain of units and rows */
+  int32_t unit_max_levels;   /* most intra-unit levels */
 } tcg_plan_stats;
 
 /* ---- host flattener ---------------------------------------------------- */

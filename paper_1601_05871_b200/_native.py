@@ -74,6 +74,20 @@ class Problem(C.Structure):
         ("flow_slot", i32p),
         ("nflow_upd", C.c_int64),
         ("flow_upd", i32p),
+        ("m6_nrows", C.c_int64),
+        ("m6_row_rec", i32p),
+        ("m6_row_item", i32p),
+        ("m6_nunits", C.c_int64),
+        ("m6_unit_rec", i32p),
+        ("m6_nurows", C.c_int64),
+        ("m6_urow_rec", i32p),
+        ("m6_urow_lbase", i32p),
+        ("m6_urow_item", i32p),
+        ("m6_nlev", C.c_int64),
+        ("m6_ulev", i32p),
+        ("m6_slot", i32p),
+        ("m6_upd", i32p),
+        ("m6_smem", C.c_int64),
     ]
 
 
@@ -132,6 +146,10 @@ class PlanStats(C.Structure):
         ("plan_seconds", C.c_double),
         ("flow_rows", C.c_int64),
         ("flow_depth", C.c_int32),
+        ("unit_count", C.c_int64),
+        ("unit_rows", C.c_int64),
+        ("unit_depth", C.c_int32),
+        ("unit_max_levels", C.c_int32),
     ]
 
 

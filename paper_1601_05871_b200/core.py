@@ -363,6 +363,23 @@ class Plan:
             "flow_rec": (_copy(p.flow_rec, 4 * p.nflow, np.int32).reshape(-1, 4)
                          if p.flow_rec else np.zeros((0, 4), np.int32)),
             "flow_item": _copy(p.flow_item, p.nflow, np.int32) if p.flow_item else np.zeros(0, np.int32),
+            "m6_row_rec": _copy(p.m6_row_rec, 4 * p.m6_nrows, np.int32).reshape(-1, 4) if p.m6_row_rec
+            else np.zeros((0, 4), np.int32),
+            "m6_row_item": _copy(p.m6_row_item, p.m6_nrows, np.int32) if p.m6_row_item else np.zeros(0, np.int32),
+            "m6_unit_rec": _copy(p.m6_unit_rec, 4 * p.m6_nunits, np.int32).reshape(-1, 4) if p.m6_unit_rec
+            else np.zeros((0, 4), np.int32),
+            "m6_urow_rec": _copy(p.m6_urow_rec, 4 * p.m6_nurows, np.int32).reshape(-1, 4) if p.m6_urow_rec
+            else np.zeros((0, 4), np.int32),
+            "m6_urow_lbase": _copy(p.m6_urow_lbase, p.m6_nurows, np.int32) if p.m6_urow_lbase
+            else np.zeros(0, np.int32),
+            "m6_urow_item": _copy(p.m6_urow_item, p.m6_nurows, np.int32) if p.m6_urow_item
+            else np.zeros(0, np.int32),
+            "m6_ulev": _copy(p.m6_ulev, p.m6_nlev, np.int32) if p.m6_ulev else np.zeros(0, np.int32),
+            "m6_slot": (_copy(p.m6_slot, 4 * p.nnz, np.int32).reshape(-1, 4) if p.m6_slot
+                        else np.zeros((0, 4), np.int32)),
+            "m6_upd": (_copy(p.m6_upd, 2 * p.nflow_upd, np.int32).reshape(-1, 2) if p.m6_upd
+                       else np.zeros((0, 2), np.int32)),
+            "m6_smem": int(p.m6_smem),
             "flow_slot": (_copy(p.flow_slot, 4 * p.nnz, np.int32).reshape(-1, 4)
                           if p.flow_slot else np.zeros((0, 4), np.int32)),
             "flow_upd": (_copy(p.flow_upd, 2 * p.nflow_upd, np.int32).reshape(-1, 2)

@@ -100,6 +100,18 @@ struct tcg_ctx {
   bool has_static = false;
   int4* flow_rec = nullptr;  // value-flow schedule (mode 5)
   int* flow_item = nullptr;
+  // block units (mode 6)
+  int4* m6_row_rec = nullptr;
+  int* m6_row_item = nullptr;
+  int4* m6_unit_rec = nullptr;
+  int4* m6_urow_rec = nullptr;
+  int* m6_urow_lbase = nullptr;
+  int* m6_urow_item = nullptr;
+  int* m6_ulev = nullptr;
+  int4* m6_slot = nullptr;
+  int2* m6_upd = nullptr;
+  std::int64_t m6_nrows = 0, m6_nunits = 0, m6_smem = 0;
+  bool has_units = false;
   int* m_flags = nullptr;    // per member: breakdown latch, row (2 ints) + pivot (below)
   double* m_pivot = nullptr;
   // batch of value sets sharing the pattern (mode 5); separate allocation
@@ -160,6 +172,8 @@ tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pa
     if (const char* e = std::getenv("TCG_MAX_WIDTH")) po.max_width = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("TCG_DEP_WIDE_COST")) po.dep_wide_cost = std::max(1.0, std::atof(e));
     if (const char* e = std::getenv("TCG_HOT_FRACTION")) po.hot_fraction = std::atof(e);
+    if (const char* e = std::getenv("TCG_UNIT_MIN_ROWS")) po.unit_min_rows = std::atoi(e);
+    if (const char* e = std::getenv("TCG_UNIT_SMEM")) po.unit_smem_cap = std::atoll(e);
     p->plan = tcb::build_plan(u, init, rl, true, po);
     *out = p.release();
     return TCG_OK;
@@ -221,6 +235,21 @@ tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   o->flow_slot = flow ? P.flow_slot.data() : nullptr;
   o->nflow_upd = flow ? static_cast<int64_t>(P.flow_upd.size() / 2) : 0;
   o->flow_upd = flow ? P.flow_upd.data() : nullptr;
+  const bool m6 = flow && !P.m6_slot.empty();
+  o->m6_nrows = m6 ? static_cast<int64_t>(P.m6_row_item.size()) : 0;
+  o->m6_row_rec = m6 ? P.m6_row_rec.data() : nullptr;
+  o->m6_row_item = m6 ? P.m6_row_item.data() : nullptr;
+  o->m6_nunits = m6 ? P.m6_units : 0;
+  o->m6_unit_rec = m6 ? P.m6_unit_rec.data() : nullptr;
+  o->m6_nurows = m6 ? static_cast<int64_t>(P.m6_urow_item.size()) : 0;
+  o->m6_urow_rec = m6 ? P.m6_urow_rec.data() : nullptr;
+  o->m6_urow_lbase = m6 ? P.m6_urow_lbase.data() : nullptr;
+  o->m6_urow_item = m6 ? P.m6_urow_item.data() : nullptr;
+  o->m6_nlev = m6 ? static_cast<int64_t>(P.m6_ulev.size()) : 0;
+  o->m6_ulev = m6 ? P.m6_ulev.data() : nullptr;
+  o->m6_slot = m6 ? P.m6_slot.data() : nullptr;
+  o->m6_upd = m6 ? P.m6_upd.data() : nullptr;
+  o->m6_smem = m6 ? P.m6_smem : 0;
   return TCG_OK;
 }
 
@@ -247,6 +276,10 @@ tcg_status tcg_plan_get_stats(const tcg_plan* plan, tcg_plan_stats* o) {
   o->plan_seconds = s.plan_seconds;
   o->flow_rows = s.flow_rows;
   o->flow_depth = s.flow_depth;
+  o->unit_count = s.unit_count;
+  o->unit_rows = s.unit_rows;
+  o->unit_depth = s.unit_depth;
+  o->unit_max_levels = s.unit_max_levels;
   return TCG_OK;
 }
 
@@ -393,6 +426,18 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_fslot = take(flow ? sizeof(int4) * p->nnz : 0);
   const size_t o_fupd = take(flow ? sizeof(int2) * p->nflow_upd : 0);
   const size_t o_fa = take(flow ? sizeof(double) * p->nnz : 0);
+  const bool units = flow && p->m6_nunits > 0 && (p->m6_nrows == 0 || (p->m6_row_rec && p->m6_row_item)) &&
+                     p->m6_unit_rec && p->m6_urow_rec && p->m6_urow_lbase && p->m6_urow_item && p->m6_ulev &&
+                     p->m6_slot && (p->nflow_upd == 0 || p->m6_upd);
+  const size_t o_m6rr = take(units ? sizeof(int4) * p->m6_nrows : 0);
+  const size_t o_m6ri = take(units ? sizeof(int) * p->m6_nrows : 0);
+  const size_t o_m6ur = take(units ? sizeof(int4) * p->m6_nunits : 0);
+  const size_t o_m6wr = take(units ? sizeof(int4) * p->m6_nurows : 0);
+  const size_t o_m6lb = take(units ? sizeof(int) * p->m6_nurows : 0);
+  const size_t o_m6wi = take(units ? sizeof(int) * p->m6_nurows : 0);
+  const size_t o_m6lv = take(units ? sizeof(int) * p->m6_nlev : 0);
+  const size_t o_m6sl = take(units ? sizeof(int4) * p->nnz : 0);
+  const size_t o_m6up = take(units ? sizeof(int2) * p->nflow_upd : 0);
   const size_t o_mflags = take(sizeof(int) * 2);
   const size_t o_mpivot = take(sizeof(double));
   const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
@@ -432,6 +477,19 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->has_static = stat;
   c->flow_rec = reinterpret_cast<int4*>(base + o_frec);
   c->flow_item = reinterpret_cast<int*>(base + o_fitem);
+  c->m6_row_rec = reinterpret_cast<int4*>(base + o_m6rr);
+  c->m6_row_item = reinterpret_cast<int*>(base + o_m6ri);
+  c->m6_unit_rec = reinterpret_cast<int4*>(base + o_m6ur);
+  c->m6_urow_rec = reinterpret_cast<int4*>(base + o_m6wr);
+  c->m6_urow_lbase = reinterpret_cast<int*>(base + o_m6lb);
+  c->m6_urow_item = reinterpret_cast<int*>(base + o_m6wi);
+  c->m6_ulev = reinterpret_cast<int*>(base + o_m6lv);
+  c->m6_slot = reinterpret_cast<int4*>(base + o_m6sl);
+  c->m6_upd = reinterpret_cast<int2*>(base + o_m6up);
+  c->m6_nrows = units ? p->m6_nrows : 0;
+  c->m6_nunits = units ? p->m6_nunits : 0;
+  c->m6_smem = units ? p->m6_smem : 0;
+  c->has_units = units;
   c->m_flags = reinterpret_cast<int*>(base + o_mflags);
   c->m_pivot = reinterpret_cast<double*>(base + o_mpivot);
   c->flow_slot = reinterpret_cast<int4*>(base + o_fslot);
@@ -480,6 +538,17 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     TCG_CUDA_TRY(c, put(c->flow_item, p->flow_item, sizeof(int) * p->nflow));
     TCG_CUDA_TRY(c, put(c->flow_slot, p->flow_slot, sizeof(int4) * p->nnz));
     TCG_CUDA_TRY(c, put(c->flow_upd, p->flow_upd, sizeof(int2) * p->nflow_upd));
+  }
+  if (units) {
+    TCG_CUDA_TRY(c, put(c->m6_row_rec, p->m6_row_rec, sizeof(int4) * p->m6_nrows));
+    TCG_CUDA_TRY(c, put(c->m6_row_item, p->m6_row_item, sizeof(int) * p->m6_nrows));
+    TCG_CUDA_TRY(c, put(c->m6_unit_rec, p->m6_unit_rec, sizeof(int4) * p->m6_nunits));
+    TCG_CUDA_TRY(c, put(c->m6_urow_rec, p->m6_urow_rec, sizeof(int4) * p->m6_nurows));
+    TCG_CUDA_TRY(c, put(c->m6_urow_lbase, p->m6_urow_lbase, sizeof(int) * p->m6_nurows));
+    TCG_CUDA_TRY(c, put(c->m6_urow_item, p->m6_urow_item, sizeof(int) * p->m6_nurows));
+    TCG_CUDA_TRY(c, put(c->m6_ulev, p->m6_ulev, sizeof(int) * p->m6_nlev));
+    TCG_CUDA_TRY(c, put(c->m6_slot, p->m6_slot, sizeof(int4) * p->nnz));
+    TCG_CUDA_TRY(c, put(c->m6_upd, p->m6_upd, sizeof(int2) * p->nflow_upd));
   }
   if (p->nitems > 0)
     TCG_CUDA_TRY(c, cudaMemsetAsync(c->iflag, 0, sizeof(int) * p->nitems, c->stream));
@@ -617,6 +686,100 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads) {
     c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
              std::to_string(h.fail_pivot) + " is not positive" +
              (batch ? " (member " + std::to_string(h.fail_member) + ")" : std::string());
+    return TCG_BREAKDOWN;
+  }
+  return TCG_OK;
+}
+
+// Block units (mode 6, flow_kernel.cu factor_units): prelude + one launch.
+static tcg_status run_units(tcg_ctx* c, tcg_stats& S, int threads) {
+  int kb = 4, minb = threads == 128 ? 6 : threads == 256 ? 3 : 1;
+  if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
+  int weak = 0;
+  if (const char* e = std::getenv("TCG_FLOW_WEAK")) weak = std::atoi(e);
+  const size_t smem = static_cast<size_t>(std::max<std::int64_t>(c->m6_smem, 16));
+  int occ = 0;
+  TCG_CUDA_TRY(c, tcbdev::unit_occupancy(threads, kb, minb, weak, smem, &occ));
+  if (occ < 1) {
+    c->err = "block-unit kernel does not fit on an SM";
+    return TCG_INVALID;
+  }
+  if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
+  const int grid = std::max(2, occ * c->sm_count);
+  int nu = static_cast<int>(std::min<std::int64_t>(c->m6_nunits, c->sm_count));
+  if (const char* e = std::getenv("TCG_UNIT_CTAS")) nu = std::max(1, std::atoi(e));
+  nu = std::min(nu, grid - 1);
+  tcbdev::FlowPrepParams q{};
+  q.vals = c->vals;
+  q.a = c->flow_a;
+  q.out = c->vals;
+  q.nnz = c->nnz;
+  q.ctrl = c->ctrl;
+  q.m_failed = c->m_flags;
+  q.m_row = c->m_flags + 1;
+  q.m_pivot = c->m_pivot;
+  q.nbatch = 1;
+  tcbdev::FlowParams P{};
+  P.rec = c->m6_row_rec;
+  P.item = c->m6_row_item;
+  P.slot = c->m6_slot;
+  P.upd = c->m6_upd;
+  P.a = c->flow_a;
+  P.vals = c->vals;
+  P.ctrl = c->ctrl;
+  P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
+  P.m_failed = q.m_failed;
+  P.m_row = q.m_row;
+  P.m_pivot = q.m_pivot;
+  P.nnz = c->nnz;
+  P.nbatch = 1;
+  P.nrows = static_cast<int>(c->m6_nrows);
+  const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
+  P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+  tcbdev::UnitParams U{};
+  U.unit_rec = c->m6_unit_rec;
+  U.urow_rec = c->m6_urow_rec;
+  U.urow_lbase = c->m6_urow_lbase;
+  U.urow_item = c->m6_urow_item;
+  U.ulev = c->m6_ulev;
+  U.nunits = static_cast<int>(c->m6_nunits);
+  U.nu_ctas = nu;
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
+  TCG_CUDA_TRY(c, tcbdev::launch_units(P, U, grid, threads, kb, minb, weak, smem, c->stream));
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
+                                  cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  const tcbdev::Ctrl& h = *c->host_ctrl;
+  S.device_ms = ms;
+  S.grid_ctas = grid;
+  S.threads_per_cta = threads;
+  S.staging_cap = kb;
+  S.smem_bytes = static_cast<int64_t>(smem);
+  S.kernel_launches = 2;
+  S.mode = 6;
+  S.helpers_run = nu;  // reported: CTAs running units
+  S.lanes_per_row = 32;
+  S.tasks_completed = (h.done.v == c->nflow) ? c->ntasks : 0;
+  S.tasks_executed = h.executed.v;
+  if (h.error.v) {
+    c->err = "device watchdog expired: the block-unit schedule stalled";
+    return TCG_TIMEOUT;
+  }
+  if (h.done.v != c->nflow) {
+    c->err = "block-unit schedule finished " + std::to_string(h.done.v) + " of " +
+             std::to_string(c->nflow) + " rows";
+    return TCG_TIMEOUT;
+  }
+  if (h.failed.v) {
+    S.breakdown_row = h.fail_row;
+    S.breakdown_pivot = h.fail_pivot;
+    S.breakdown_member = 0;
+    c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
+             std::to_string(h.fail_pivot) + " is not positive";
     return TCG_BREAKDOWN;
   }
   return TCG_OK;
@@ -794,7 +957,8 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
            : c->has_static ? 4 : c->has_rows ? 3 : (c->has_programs ? 2 : 1);
   }
   if ((mode == 2 && !c->has_programs) || (mode == 3 && !c->has_rows) ||
-      (mode == 4 && !c->has_static) || (mode == 5 && !c->has_flow) || mode < 0 || mode > 5) {
+      (mode == 4 && !c->has_static) || (mode == 5 && !c->has_flow) || (mode == 6 && !c->has_units) ||
+      mode < 0 || mode > 6) {
     c->err = "requested execution mode is not available for the uploaded problem";
     return TCG_INVALID;
   }
@@ -809,6 +973,7 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   if (mode == 3) return run_rows(c, S, threads);
   if (mode == 4) return run_static(c, S, threads);
   if (mode == 5) return run_flow(c, S, threads);
+  if (mode == 6) return run_units(c, S, threads);
   int flag_words = (c->max_flag_rows + 31) / 32;
   flag_words = (flag_words + 3) & ~3;
   int cap = c->opt.staging_cap;

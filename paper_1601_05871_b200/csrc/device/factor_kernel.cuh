@@ -123,6 +123,18 @@ struct FlowParams {
   unsigned long long timeout_ns;
 };
 
+// Block units (mode 6, flow_kernel.cu factor_units); rows outside units use
+// FlowParams (rec/item/nrows = that list, slot/upd = the rewritten programs).
+struct UnitParams {
+  const int4* unit_rec;    // per unit: {level slot begin, end, first row, order}
+  const int4* urow_rec;    // per unit row: {tb, L | kind << 30, dpos, t}
+  const int* urow_lbase;   // per unit row: first shared-memory index of its values
+  const int* urow_item;
+  const int* ulev;         // per level slot: end of its rows
+  int nunits;
+  int nu_ctas;             // CTAs [0, nu_ctas) run units
+};
+
 struct FlowPrepParams {
   const double* vals;    // working values (input of the factorization)
   double* a;             // snapshot of them

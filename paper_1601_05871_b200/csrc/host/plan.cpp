@@ -524,6 +524,190 @@ void build_flow(Plan& P) {
   P.stats.flow_depth = depth;
 }
 
+// Block units (mode 6). A chain of Chol rows inside one large diagonal
+// block (an ND separator) is most of the critical path in mode 5: every link
+// costs a cross-SM hand-off through L2 (C2: ~190 of the 214 steps of the
+// longest chain sit in diagonal blocks of 114-3,072 rows). Here such a block
+// becomes a unit executed by one CTA: its rows in intra-block level order,
+// one __syncthreads between levels, and the block's own values kept in shared
+// memory, so an intra-block operand costs a shared-memory load instead of a
+// hand-off. Operands from other blocks are still polled in global memory.
+// Programs are the mode-5 merged programs with every intra-unit operand
+// position rewritten to kLocalBit | (its index in the unit's shared array).
+// Everything that is not in a unit runs as in mode 5. The schedule orders
+// units and rows by level over "reads a value written by" (a unit counts as
+// one node); unit CTAs take the units and the other warps the rows, each
+// list in that topological order, which keeps the launch deadlock-free.
+void build_units(Plan& P, const RangeList& ranges, std::int32_t min_rows, std::int64_t smem_cap) {
+  const std::size_t R = P.flow_item.size();
+  const std::size_t N = static_cast<std::size_t>(P.nnz);
+  const std::size_t I = P.item_rec.size() / kItemWords;
+  auto F = [&](std::size_t q, int w) { return P.flow_rec[q * kFlowWords + w]; };
+  auto len = [&](std::size_t q) { return F(q, 1) & ((1 << kFlowKindShift) - 1); };
+  auto kind = [&](std::size_t q) { return static_cast<std::int32_t>(static_cast<std::uint32_t>(F(q, 1)) >> kFlowKindShift); };
+  std::vector<std::int32_t> range_of(static_cast<std::size_t>(P.n));
+  for (index_t r = 0; r < ranges.count(); ++r)
+    for (index_t c = ranges.ranges[r].begin; c < ranges.ranges[r].end; ++c) range_of[c] = r;
+  std::vector<std::int32_t> pos_of_item(I, -1);
+  for (std::size_t q = 0; q < R; ++q) pos_of_item[P.flow_item[q]] = static_cast<std::int32_t>(q);
+  // candidate units: Chol rows of large diagonal blocks whose values fit
+  std::vector<std::int64_t> nloc(static_cast<std::size_t>(ranges.count()), 0);
+  for (std::size_t q = 0; q < R; ++q)
+    if (kind(q) == kChol) nloc[range_of[F(q, 3)]] += len(q);
+  std::vector<std::int32_t> unit_of_range(static_cast<std::size_t>(ranges.count()), -1);
+  std::int32_t nunits = 0;
+  for (index_t r = 0; r < ranges.count(); ++r)
+    if (min_rows > 0 && ranges.ranges[r].size() > min_rows && nloc[r] > 0 && nloc[r] * 8 <= smem_cap)
+      unit_of_range[r] = nunits++;
+  std::vector<std::int32_t> unit_of_pos(R, -1);
+  for (std::size_t q = 0; q < R; ++q)
+    if (kind(q) == kChol) unit_of_pos[q] = unit_of_range[range_of[F(q, 3)]];
+  // local indices: unit rows in flow order, coordinates consecutive
+  std::vector<std::int32_t> loc_of(N, -1), lbase(R, -1);
+  std::vector<std::int64_t> ucount(static_cast<std::size_t>(nunits), 0);
+  for (std::size_t q = 0; q < R; ++q) {
+    const std::int32_t u = unit_of_pos[q];
+    if (u < 0) continue;
+    lbase[q] = static_cast<std::int32_t>(ucount[u]);
+    for (std::int32_t j = 0; j < len(q); ++j) loc_of[F(q, 0) + j] = static_cast<std::int32_t>(ucount[u] + j);
+    ucount[u] += len(q);
+  }
+  // programs with intra-unit operands rewritten
+  P.m6_slot = P.flow_slot;
+  P.m6_upd = P.flow_upd;
+  auto unit_of_value = [&](std::int32_t pos) { return unit_of_pos[pos_of_item[P.flow_owner[pos]]]; };
+  for (std::size_t q = 0; q < R; ++q) {
+    const std::int32_t u = unit_of_pos[q];
+    if (u < 0) continue;
+    for (std::int32_t j = 0; j < len(q); ++j) {
+      std::int32_t* sl = &P.m6_slot[4 * static_cast<std::size_t>(F(q, 0) + j)];
+      for (std::int32_t e = sl[0]; e < sl[1]; ++e)
+        for (int h = 0; h < 2; ++h) {
+          std::int32_t& x = P.m6_upd[2 * static_cast<std::size_t>(e) + h];
+          if (unit_of_value(x) == u) x = static_cast<std::int32_t>(kLocalBit | static_cast<std::uint32_t>(loc_of[x]));
+        }
+      if (sl[0] < sl[1]) {
+        sl[2] = P.m6_upd[2 * static_cast<std::size_t>(sl[0])];
+        sl[3] = P.m6_upd[2 * static_cast<std::size_t>(sl[0]) + 1];
+      }
+    }
+  }
+  // nodes: units 0..nunits-1, then rows outside units
+  std::vector<std::int32_t> node_of_pos(R, -1);
+  std::int32_t nn = nunits;
+  for (std::size_t q = 0; q < R; ++q) node_of_pos[q] = unit_of_pos[q] >= 0 ? unit_of_pos[q] : nn++;
+  // node dependences (unique), intra-unit levels
+  std::vector<std::vector<std::int32_t>> deps(static_cast<std::size_t>(nn));
+  std::vector<std::int32_t> ulevel(R, 0);
+  for (std::size_t q = 0; q < R; ++q) {
+    const std::int32_t me = node_of_pos[q];
+    std::int32_t lv = 1;
+    auto src = [&](std::int32_t pos) {
+      const std::int32_t sq = pos_of_item[P.flow_owner[pos]];
+      const std::int32_t sn = node_of_pos[sq];
+      if (sn == me) lv = std::max(lv, ulevel[sq] + 1);
+      else deps[me].push_back(sn);
+    };
+    if (kind(q) == kTrsm) src(F(q, 2));
+    for (std::int32_t j = 0; j < len(q); ++j) {
+      const std::int32_t* sl = &P.flow_slot[4 * static_cast<std::size_t>(F(q, 0) + j)];
+      for (std::int32_t e = sl[0]; e < sl[1]; ++e) {
+        src(P.flow_upd[2 * static_cast<std::size_t>(e)]);
+        src(P.flow_upd[2 * static_cast<std::size_t>(e) + 1]);
+      }
+    }
+    ulevel[q] = lv;
+  }
+  std::vector<std::int32_t> indeg(static_cast<std::size_t>(nn), 0), level(static_cast<std::size_t>(nn), 1);
+  std::vector<std::vector<std::int32_t>> succ(static_cast<std::size_t>(nn));
+  for (std::int32_t v = 0; v < nn; ++v) {
+    auto& d = deps[v];
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    indeg[v] = static_cast<std::int32_t>(d.size());
+    for (std::int32_t x : d) succ[x].push_back(v);
+  }
+  std::vector<std::int32_t> ready, topo;
+  for (std::int32_t v = 0; v < nn; ++v)
+    if (indeg[v] == 0) ready.push_back(v);
+  while (!ready.empty()) {
+    const std::int32_t v = ready.back();
+    ready.pop_back();
+    topo.push_back(v);
+    for (std::int32_t w : succ[v]) {
+      level[w] = std::max(level[w], level[v] + 1);
+      if (--indeg[w] == 0) ready.push_back(w);
+    }
+  }
+  if (static_cast<std::int32_t>(topo.size()) != nn) throw std::logic_error("units: dependence cycle");
+  // first flow position of every node, for a stable order inside a level
+  std::vector<std::int32_t> first(static_cast<std::size_t>(nn), std::numeric_limits<std::int32_t>::max());
+  for (std::size_t q = 0; q < R; ++q)
+    first[node_of_pos[q]] = std::min(first[node_of_pos[q]], static_cast<std::int32_t>(q));
+  std::vector<std::int32_t> order(static_cast<std::size_t>(nn));
+  for (std::int32_t v = 0; v < nn; ++v) order[v] = v;
+  std::stable_sort(order.begin(), order.end(), [&](std::int32_t x, std::int32_t y) {
+    return level[x] != level[y] ? level[x] < level[y] : first[x] < first[y];
+  });
+  std::vector<std::int32_t> pos_of_node(static_cast<std::size_t>(nn));
+  for (std::int32_t k = 0; k < nn; ++k) pos_of_node[order[k]] = k;
+  // rows: records in node order; units: rows by intra-unit level
+  P.m6_row_rec.clear();
+  P.m6_row_item.clear();
+  P.m6_row_node.clear();
+  std::vector<std::vector<std::int32_t>> urows(static_cast<std::size_t>(nunits));
+  std::vector<std::int32_t> row_at_node(static_cast<std::size_t>(nn), -1);
+  for (std::size_t q = 0; q < R; ++q) {
+    if (unit_of_pos[q] >= 0) urows[unit_of_pos[q]].push_back(static_cast<std::int32_t>(q));
+    else row_at_node[node_of_pos[q]] = static_cast<std::int32_t>(q);
+  }
+  P.m6_unit_rec.clear();
+  P.m6_urow_rec.clear();
+  P.m6_urow_lbase.clear();
+  P.m6_urow_item.clear();
+  P.m6_ulev.clear();
+  std::int64_t smem_max = 0;
+  std::int32_t depth_max = 0;
+  for (std::int32_t k = 0; k < nn; ++k) {
+    const std::int32_t v = order[k];
+    if (v >= nunits) {
+      const std::size_t q = static_cast<std::size_t>(row_at_node[v]);
+      P.m6_row_rec.insert(P.m6_row_rec.end(), &P.flow_rec[q * kFlowWords], &P.flow_rec[q * kFlowWords] + kFlowWords);
+      P.m6_row_item.push_back(P.flow_item[q]);
+      P.m6_row_node.push_back(k);
+      continue;
+    }
+    auto& rows = urows[v];
+    std::stable_sort(rows.begin(), rows.end(), [&](std::int32_t x, std::int32_t y) { return ulevel[x] < ulevel[y]; });
+    const auto rb = static_cast<std::int32_t>(P.m6_urow_item.size());
+    const auto lb = static_cast<std::int32_t>(P.m6_ulev.size());
+    std::int32_t cur = 0;
+    for (std::int32_t q : rows) {
+      if (ulevel[q] != cur) {
+        P.m6_ulev.push_back(static_cast<std::int32_t>(P.m6_urow_item.size()));
+        cur = ulevel[q];
+      }
+      P.m6_urow_rec.insert(P.m6_urow_rec.end(), &P.flow_rec[static_cast<std::size_t>(q) * kFlowWords],
+                           &P.flow_rec[static_cast<std::size_t>(q) * kFlowWords] + kFlowWords);
+      P.m6_urow_lbase.push_back(lbase[q]);
+      P.m6_urow_item.push_back(P.flow_item[q]);
+    }
+    P.m6_ulev.push_back(static_cast<std::int32_t>(P.m6_urow_item.size()));
+    const auto le = static_cast<std::int32_t>(P.m6_ulev.size());
+    // {first level slot, end level slot, first row, node position}; level slot
+    // l covers rows [ulev[l-1] or rb, ulev[l])
+    P.m6_unit_rec.insert(P.m6_unit_rec.end(), {lb, le, rb, k});
+    smem_max = std::max(smem_max, ucount[v] * 8);
+    depth_max = std::max(depth_max, le - lb);
+  }
+  P.m6_units = nunits;
+  P.m6_smem = smem_max;
+  P.stats.unit_count = nunits;
+  P.stats.unit_rows = static_cast<std::int64_t>(P.m6_urow_item.size());
+  P.stats.unit_depth = level.empty() ? 0 : *std::max_element(level.begin(), level.end());
+  P.stats.unit_max_levels = depth_max;
+}
+
 }  // namespace
 
 Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
@@ -786,6 +970,7 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
   if (with_work && opt.programs) build_programs(P, opt.threads);
   if (with_work) build_item_deps(P, ranges, opt.hot_fraction);
   if (with_work && opt.programs) build_flow(P);
+  if (with_work && opt.programs) build_units(P, ranges, opt.unit_min_rows, opt.unit_smem_cap);
 
   // successors + in-degrees (edge multiplicity preserved)
   const std::size_t T = P.node_kind.size();

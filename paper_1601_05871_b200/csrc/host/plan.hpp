@@ -47,6 +47,8 @@ constexpr int kPosInline = 4;
 // value-flow schedule (mode 5) record per position: tb, L | kind << 30, dpos, t
 constexpr int kFlowWords = 4;
 constexpr int kFlowKindShift = 30;
+// mode 6: operand positions with this bit index the unit's shared-memory values
+constexpr std::uint32_t kLocalBit = 0x80000000u;
 
 struct PlanOptions {
   double cta_cost = 64.0;  // estimated warp-steps one CTA should get before a helper joins
@@ -54,6 +56,8 @@ struct PlanOptions {
   double dep_wide_cost = 64.0;  // Chol/Trsm go multi-CTA only above this cost per level
   double hot_fraction = 0.6;    // rows with height >= this fraction of the max are "hot"
   bool programs = true;    // precompute per-row update programs (slot_rec / upd)
+  int unit_min_rows = 64;  // mode 6: diagonal blocks above this many rows become units
+  std::int64_t unit_smem_cap = 72 * 1024;  // ... if their values fit in this many bytes
   int threads = 0;         // host threads for the program build (0 = all)
 };
 
@@ -84,6 +88,10 @@ struct PlanStats {
   std::int32_t item_depth = 0;     // longest row-level chain, in items
   std::int64_t flow_rows = 0;      // value-flow rows (Chol/Trsm items; they partition U)
   std::int32_t flow_depth = 0;     // longest value-flow chain, in rows
+  std::int64_t unit_count = 0;     // mode 6 block units
+  std::int64_t unit_rows = 0;      // rows inside units
+  std::int32_t unit_depth = 0;     // longest chain of units and rows
+  std::int32_t unit_max_levels = 0;  // most intra-unit levels
   double block_build_seconds = 0.0;
   double plan_seconds = 0.0;
 };
@@ -122,6 +130,20 @@ struct Plan {
   std::vector<std::int32_t> flow_slot;  // per coordinate of U: {u_b, u_e, m0, o0}
   std::vector<std::int32_t> flow_upd;   // (m, o) pairs
   std::vector<std::int32_t> flow_owner; // per coordinate of U: the item writing it
+  // mode 6 (block units): rows outside units in schedule order; units with
+  // their rows by intra-unit level; programs with local operands rewritten
+  std::vector<std::int32_t> m6_row_rec;   // kFlowWords per row
+  std::vector<std::int32_t> m6_row_item;
+  std::vector<std::int32_t> m6_row_node;  // position of the row in the joint order
+  std::vector<std::int32_t> m6_unit_rec;  // per unit: level slot begin/end, first row, node position
+  std::vector<std::int32_t> m6_urow_rec;  // kFlowWords per unit row
+  std::vector<std::int32_t> m6_urow_lbase;  // first shared-memory index of the row's values
+  std::vector<std::int32_t> m6_urow_item;
+  std::vector<std::int32_t> m6_ulev;      // per level slot: end of its rows
+  std::vector<std::int32_t> m6_slot;      // like flow_slot / flow_upd, local operands rewritten
+  std::vector<std::int32_t> m6_upd;
+  std::int32_t m6_units = 0;
+  std::int64_t m6_smem = 0;               // largest unit, bytes
   std::vector<std::int32_t> slot_rec;  // update-program slots {u_b, u_e, m0, o0} (per item: L)
   std::vector<std::int32_t> upd;       // update-program (m, o) pairs
   std::vector<std::int32_t> succ;      // successors grouped per task

@@ -40,8 +40,10 @@ def check_against_oracle(name, vals, golden, oracle):
 
 @pytest.mark.parametrize("name", ["c1", "c5_m0", "c5_m63", "s27_16_k2", "grid20_k2_leaf4",
                                   "rand_spd_200", "elast6_k1", "c2", "c3", "c4"])
-@pytest.mark.parametrize("mode", [3, 4, 5])
+@pytest.mark.parametrize("mode", [3, 4, 5, 6])
 def test_configs_row_modes(T, golden, oracle, name, mode):  # noqa: D103
+    if mode == 6 and planned(name).stats().unit_count == 0:
+        pytest.skip("no diagonal block large enough for a unit")
     vals, st = gpu_factor(T, planned(name), mode=mode)
     assert st.mode == mode
     check_against_oracle(name, vals, golden, oracle)
@@ -344,5 +346,38 @@ def test_c5_batch_breakdown_is_per_member(T, oracle):
         for i in (0, 2):
             ref, _, _, _ = oracle.factor_serial(perms[i], u)
             assert bitwise_equal(out[i], ref), i
+    finally:
+        fz.close()
+
+
+@pytest.mark.parametrize("min_rows", [4, 16, 64])
+@pytest.mark.parametrize("name", ["c5_m0", "s27_16_k2", "grid20_k2_leaf4", "rand_spd_200"])
+def test_block_units(T, golden, oracle, name, min_rows, monkeypatch):
+    # mode 6: diagonal blocks above min_rows run as CTA units (shared-memory values)
+    monkeypatch.setenv("TCG_UNIT_MIN_ROWS", str(min_rows))
+    _, an = analyzed(name)
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    if plan.stats().unit_count == 0:
+        pytest.skip("no block above min_rows")
+    vals, st = gpu_factor(T, plan, mode=6)
+    assert st.mode == 6
+    check_against_oracle(name, vals, golden, oracle)
+
+
+def test_block_units_breakdown(T):
+    a, fp, rl = small(T, 4, sym([(0, 0, 1.0), (1, 1, 1.0), (2, 2, 1.0), (2, 3, 4.0), (3, 3, 1.0)]),
+                      bounds=[0, 4])
+    import os
+    os.environ["TCG_UNIT_MIN_ROWS"] = "1"
+    try:
+        plan = T.Plan(a, fp, rl)
+    finally:
+        del os.environ["TCG_UNIT_MIN_ROWS"]
+    assert plan.stats().unit_count == 1
+    fz = T.GpuFactorizer(plan, T.GpuOptions(mode=6))
+    try:
+        with pytest.raises(T.BreakdownError) as e:
+            fz.factor()
+        assert e.value.row == 3
     finally:
         fz.close()

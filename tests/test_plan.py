@@ -210,3 +210,91 @@ def test_flow_schedule_partitions_u_and_replays_bitwise(name, oracle):
     # any order that respects "reads only written values" gives the same bits:
     # item order (generation order) is one
     assert bitwise_equal(replay_flow(t, np.argsort(items, kind="stable")), ref)
+
+
+LOCAL = 0x80000000
+
+
+def replay_units(t):
+    """Mode 6 on the CPU: units and rows in the joint schedule order; a unit
+    runs its rows level by level with its own values in a local array
+    (operands flagged LOCAL), everything else reads the global factor."""
+    rows, rows_item = t["m6_row_rec"], t["m6_row_item"]
+    units, urec, ulb, ulev = t["m6_unit_rec"], t["m6_urow_rec"], t["m6_urow_lbase"], t["m6_ulev"]
+    slot, upd = t["m6_slot"], t["m6_upd"]
+    a = t["values"]
+    out = np.full(len(a), np.nan)
+    done = np.zeros(len(a), bool)
+    m6_node = t["m6_row_node"] if "m6_row_node" in t else None
+
+    def run_row(rec, local=None, lb=None):
+        tb, lk, dpos, _ = rec
+        L, kind = lk & ((1 << 30) - 1), (lk >> 30) & 3
+        v = a[tb:tb + L].copy()
+        for j in range(L):
+            ub, ue = slot[tb + j, :2]
+            for m, o in upd[ub:ue]:
+                vals = []
+                for x in (int(m) & 0xFFFFFFFF, int(o) & 0xFFFFFFFF):
+                    if x & LOCAL:
+                        assert local is not None and not np.isnan(local[x & ~LOCAL]), "local read before written"
+                        vals.append(local[x & ~LOCAL])
+                    else:
+                        assert done[x], "read before written"
+                        vals.append(out[x])
+                v[j] = v[j] - vals[0] * vals[1]
+        if kind == 0:
+            d = np.sqrt(v[0])
+            v[1:] = v[1:] / d
+            v[0] = d
+        else:
+            assert done[dpos]
+            v = v / out[dpos]
+        assert not done[tb:tb + L].any(), "written twice"
+        out[tb:tb + L] = v
+        done[tb:tb + L] = True
+        if local is not None:
+            local[lb:lb + L] = v
+
+    # joint order: unit k sits at order position units[k, 3]; rows fill the rest in order
+    nodes = len(rows) + len(units)
+    unit_at = {int(u[3]): k for k, u in enumerate(units)}
+    r = 0
+    for pos in range(nodes):
+        if pos in unit_at:
+            lb, le, rb, _ = units[unit_at[pos]]
+            n_local = 0
+            start = rb
+            bounds = []
+            for s in range(lb, le):
+                bounds.append((start, ulev[s]))
+                start = ulev[s]
+            for b0, b1 in bounds:
+                for q in range(b0, b1):
+                    n_local = max(n_local, ulb[q] + (urec[q, 1] & ((1 << 30) - 1)))
+            local = np.full(n_local, np.nan)
+            for b0, b1 in bounds:
+                # rows of one level are independent: run them in reverse to prove it
+                for q in reversed(range(b0, b1)):
+                    run_row(urec[q], local, ulb[q])
+        else:
+            run_row(rows[r])
+            r += 1
+    assert r == len(rows) and done.all()
+    return out
+
+
+@pytest.mark.parametrize("name,min_rows", [("c5_m0", 64), ("c5_m0", 16), ("grid20_k2_leaf4", 8),
+                                           ("s27_16_k2", 32), ("rand_spd_200", 4)])
+def test_unit_schedule_replays_bitwise(T, name, min_rows, oracle, monkeypatch):
+    monkeypatch.setenv("TCG_UNIT_MIN_ROWS", str(min_rows))
+    _, an = analyzed(name)
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    t = plan.tables()
+    s = plan.stats()
+    assert s.unit_count == len(t["m6_unit_rec"]) > 0
+    assert len(t["m6_row_rec"]) + s.unit_rows == s.flow_rows
+    assert sorted(np.concatenate([t["m6_row_item"], t["m6_urow_item"]])) == sorted(t["flow_item"])
+    assert t["m6_smem"] <= 72 * 1024
+    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
+    assert bitwise_equal(replay_units(t), ref)
