@@ -1,4 +1,3 @@
 set -x
-P="timeout 600 python tests/gpu_probe.py c5 c2 c4 reps=5 mode=5"
-$P
-for b in 20 50 100 200 400; do TCG_FLOW_BACKOFF=$b $P; done
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "row_modes or flow or batch or known or breakdown or unit" 2>&1 | tail -2
+bash tools/ab_probe.sh S0 S2
