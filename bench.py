@@ -11,9 +11,11 @@ from its device copy and L2 is flushed (256 MiB write), both untimed.
   value  factor-nnz/s over the whole job = N * nnz_u / (max over ranks of the
          device time of one step); device time = CUDA events around the
          persistent kernel on the stream it is launched on.
-  e2e    the same metric through the C ABI with host buffers: H2D of the
-         initial values from pinned memory, factor, D2H of the factor; the
-         symbolic structure (plan) stays resident, as in a refactorization.
+  e2e    the same metric through the C ABI with host buffers
+         (tcg_factor_host): H2D of the initial values from pinned memory --
+         in mode 5 on a second stream beside the kernel, which polls the
+         inputs as they land --, factor, D2H of the factor; the symbolic
+         structure (plan) stays resident, as in a refactorization.
   roofline  algorithmic bytes 20*nnz_u + 8*(n+1) per
          launch / kernel time, against the measured HBM copy bandwidth.
 
@@ -268,14 +270,9 @@ def run_ours(args):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        if batched:
-            fz.set_batch_values_ptr(host_in.data_ptr())   # H2D 8*nnz_u per member
-            fz.factor()
-            fz.download_batch_ptr(host_out.data_ptr())    # D2H 8*nnz_u per member
-        else:
-            fz.set_values_ptr(host_in.data_ptr())   # H2D 8*nnz_u
-            fz.factor()
-            fz.download_ptr(host_out.data_ptr())    # D2H 8*nnz_u
+        # tcg_factor_host: H2D of the initial values (8*nnz_u per member, overlapped with
+        # the mode-5 kernel, which polls them), factor, D2H of the factor (8*nnz_u per member)
+        fz.factor_host_ptr(host_in.data_ptr(), host_out.data_ptr())
         if i >= args.warmup:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
     barrier()

@@ -468,6 +468,22 @@ class GpuFactorizer:
         self._check(st)
         return self.last
 
+    def factor_host_ptr(self, in_ptr: int, out_ptr: int) -> N.Stats:
+        """Host buffers in, factor out (tcg_factor_host): in mode 5 the upload
+        overlaps the factorization. Pointers to nnz x batch doubles (pinned)."""
+        self.last = N.Stats()
+        st = self._lib.tcg_factor_host(self.ctx, C.cast(C.c_void_p(in_ptr), N.f64p),
+                                       C.cast(C.c_void_p(out_ptr), N.f64p), C.byref(self.last))
+        self._check(st)
+        return self.last
+
+    def factor_host(self, values: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        if out is None:
+            out = np.empty_like(v)
+        self.factor_host_ptr(v.ctypes.data, out.ctypes.data)
+        return out
+
     def download(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:
             out = np.empty(self.nnz, dtype=np.float64)

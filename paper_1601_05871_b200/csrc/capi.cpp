@@ -63,6 +63,8 @@ struct tcg_ctx {
   int sm_count = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t copy_stream = nullptr;  // host-buffer factorization: H2D beside the kernel
+  cudaEvent_t ev_prep = nullptr, ev_copy = nullptr;
   void* arena = nullptr;
   size_t arena_bytes = 0;
   tcbdev::Ctrl* host_ctrl = nullptr;
@@ -321,6 +323,9 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_prep, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c->host_ctrl), sizeof(tcbdev::Ctrl));
   if (e != cudaSuccess) {
     g_plan_error = std::string("tcg_create: ") + cudaGetErrorString(e);
@@ -340,6 +345,10 @@ void tcg_destroy(tcg_ctx* c) {
   if (c->host_ctrl) cudaFreeHost(c->host_ctrl);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  if (c->ev_prep) cudaEventDestroy(c->ev_prep);
+  if (c->ev_copy) cudaEventDestroy(c->ev_copy);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -599,7 +608,11 @@ tcg_status tcg_restore(tcg_ctx* c) {
 // Value-flow execution (mode 5, flow_kernel.cu): prelude (snapshot the
 // input, mark the output unwritten, reset the status words) + one persistent
 // launch; both inside the timed region.
-static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads) {
+// host_in/host_out (tcg_factor_host): the inputs arrive by a copy on
+// copy_stream that runs beside the kernel (the kernel polls them, as it
+// polls operands), and the factor is copied back on the launch stream.
+static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* host_in = nullptr,
+                           double* host_out = nullptr) {
   int kb = 4, minb = threads == 128 ? 6 : threads == 384 ? 2 : threads == 256 ? 3 : 1;
   if (const char* e = std::getenv("TCG_FLOW_KB")) kb = std::atoi(e);
   if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
@@ -632,7 +645,9 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads) {
   q.m_row = q.m_failed + c->nbatch;
   q.m_pivot = batch ? c->bm_pivot : c->m_pivot;
   q.nbatch = c->nbatch;
+  q.input_async = host_in != nullptr;
   tcbdev::FlowParams P{};
+  P.input_async = host_in != nullptr;
   P.rec = c->flow_rec;
   P.item = c->flow_item;
   P.slot = c->flow_slot;
@@ -649,10 +664,21 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads) {
   P.nrows = static_cast<int>(c->nflow);
   const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+  const size_t vbytes = sizeof(double) * static_cast<size_t>(c->nnz) * c->nbatch;
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
   TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
+  if (host_in) {  // inputs stream in while the kernel runs
+    TCG_CUDA_TRY(c, cudaEventRecord(c->ev_prep, c->stream));
+    TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_prep, 0));
+  }
   if (c->nflow > 0) TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, c->stream));
+  if (host_in) {
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(q.a, host_in, vbytes, cudaMemcpyHostToDevice, c->copy_stream));
+    TCG_CUDA_TRY(c, cudaEventRecord(c->ev_copy, c->copy_stream));
+    TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_copy, 0));
+  }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  if (host_out) TCG_CUDA_TRY(c, cudaMemcpyAsync(host_out, vals, vbytes, cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
                                   cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -1095,6 +1121,29 @@ tcg_status tcg_download(tcg_ctx* c, double* values) {
                                   cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return TCG_OK;
+}
+
+tcg_status tcg_factor_host(tcg_ctx* c, const double* values_in, double* values_out, tcg_stats* st) {
+  if (!c || !c->uploaded || ((!values_in || !values_out) && c->nnz > 0)) return TCG_INVALID;
+  int mode = c->opt.mode;
+  const bool flow = c->has_flow && c->nnz > 0 && c->ntasks > 0 && (mode == 0 || mode == 5) &&
+                    !(mode == 0 && c->nbatch == 1 && c->nupdates > 16 * c->nnz && c->has_static);
+  if (!flow) {  // other modes: the same three steps, one after the other
+    tcg_status r = c->nbatch > 1 ? tcg_set_batch_values(c, values_in) : tcg_set_values(c, values_in);
+    if (r != TCG_OK) return r;
+    const tcg_status f = tcg_factor(c, st);
+    r = c->nbatch > 1 ? tcg_download_batch(c, values_out) : tcg_download(c, values_out);
+    return f != TCG_OK ? f : r;
+  }
+  tcg_stats local{};
+  tcg_stats& S = st ? *st : local;
+  S = tcg_stats{};
+  S.breakdown_row = -1;
+  S.breakdown_member = -1;
+  S.batch = 1;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
+  return run_flow(c, S, threads, values_in, values_out);
 }
 
 tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {

@@ -120,6 +120,7 @@ struct FlowParams {
   long long nnz;         // values per member
   int nrows;             // schedule rows (per member)
   int nbatch;            // members sharing the pattern
+  int input_async;       // the inputs `a` arrive during the launch (kUnset until copied): poll them
   unsigned long long timeout_ns;
 };
 
@@ -144,6 +145,7 @@ struct FlowPrepParams {
   int* m_row;
   double* m_pivot;
   int nbatch;
+  int input_async;       // mark `a` kUnset (a copy fills it beside the kernel) instead of snapshotting
   Ctrl* ctrl;
 };
 

@@ -76,6 +76,20 @@ struct Ctx {
   }
 };
 
+// An input value: immutable during the launch (read-only path), or, when
+// the inputs are still being copied in (input_async), polled like an operand.
+__device__ __forceinline__ double input_ld(const FlowParams& P, const double* p) {
+  if (!P.input_async) return __ldg(p);
+  return __longlong_as_double(static_cast<long long>(ld_relaxed_u64(p)));
+}
+__device__ __forceinline__ double input_settle(const FlowParams& P, const double* p, double x,
+                                               unsigned long long t0) {
+  if (!P.input_async) return x;
+  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  if (b == kUnset) b = wait_value(p, P.ctrl, t0, P.timeout_ns);
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
 // One coordinate: v -= U[m]*U[o] over its merged program, in order. The
 // first pair rides in the slot record; the rest are fetched a batch ahead.
 // (Issuing the first batch's operand loads before settling the first pair
@@ -125,7 +139,7 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
   unsigned long long xd = 0;
   if (KIND == kTrsm) xd = C.ld(dpos);
   double v = 0.0;
-  if (gl < L) v = flow_slot<KB>(C, a0, sr0);
+  if (gl < L) v = flow_slot<KB>(C, input_settle(P, C.a + tb + gl, a0, C.t0), sr0);
   double d;
   if (KIND == kChol) {
     const double piv = __shfl_sync(gmask, v, lead);
@@ -155,7 +169,8 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
   };
   if (gl < L) st_relaxed_u64(C.vals + tb + gl, finish(gl, v));
   for (int k = gl + G; k < L; k += G) {
-    const double w = flow_slot<KB>(C, __ldg(C.a + tb + k), __ldg(P.slot + tb + k));
+    const double w = flow_slot<KB>(C, input_settle(P, C.a + tb + k, input_ld(P, C.a + tb + k), C.t0),
+                                   __ldg(P.slot + tb + k));
     st_relaxed_u64(C.vals + tb + k, finish(k, w));
   }
 }
@@ -222,7 +237,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
     a = rec_of(pos);
     if (gl < (a.y & kLenMask)) {
       sr0 = __ldg(P.slot + a.x + gl);
-      a0 = __ldg(input_of(pos) + a.x + gl);
+      a0 = input_ld(P, input_of(pos) + a.x + gl);
     }
   }
   if (npos < nrows) na = rec_of(npos);
@@ -233,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
     double na0 = 0.0;
     if (npos < nrows && gl < (na.y & kLenMask)) {
       nsr0 = __ldg(P.slot + na.x + gl);
-      na0 = __ldg(input_of(npos) + na.x + gl);
+      na0 = input_ld(P, input_of(npos) + na.x + gl);
     }
     const int tb = a.x, L = a.y & kLenMask, dpos = a.z, t = a.w;
     const bool chol = (static_cast<unsigned>(a.y) >> 30) == kChol;
@@ -265,8 +280,11 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
     } else {
       // skipped rows keep their input values (readers must not wait forever)
       for (int k = gl; k < L; k += G) {
-        unsigned long long x = static_cast<unsigned long long>(__double_as_longlong(C.a[tb + k]));
-        st_relaxed_u64(C.vals + tb + k, x == kUnset ? kCanonicalNaN : x);
+        const double* ap = C.a + tb + k;
+        unsigned long long x = static_cast<unsigned long long>(
+            __double_as_longlong(input_settle(P, ap, input_ld(P, ap), C.t0)));
+        if (x == kUnset) x = kCanonicalNaN;
+        st_relaxed_u64(C.vals + tb + k, x);
       }
     }
     if (traced) stamp[3] = gtimer();
@@ -406,7 +424,7 @@ __global__ void flow_prepare(FlowPrepParams Q) {
   double2* o2 = reinterpret_cast<double2*>(Q.out);
   const double unset = __longlong_as_double(static_cast<long long>(kUnset));
   for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < h; x += stride) {
-    a2[x] = in2[x];
+    a2[x] = Q.input_async ? make_double2(unset, unset) : in2[x];
     o2[x] = make_double2(unset, unset);
   }
   for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < Q.nbatch; x += stride) {
@@ -416,7 +434,7 @@ __global__ void flow_prepare(FlowPrepParams Q) {
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (Q.nnz & 1) {
-      Q.a[Q.nnz - 1] = Q.vals[Q.nnz - 1];
+      Q.a[Q.nnz - 1] = Q.input_async ? unset : Q.vals[Q.nnz - 1];
       Q.out[Q.nnz - 1] = unset;
     }
     Ctrl c = {};

@@ -381,3 +381,38 @@ def test_block_units_breakdown(T):
         assert e.value.row == 3
     finally:
         fz.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c5_m0", "c2", "c4"])
+def test_factor_host_overlapped_upload(T, golden, oracle, name):
+    # tcg_factor_host: the input copy runs beside the mode-5 kernel, which
+    # polls the inputs; the result is the same bits
+    import torch
+    plan = planned(name)
+    vals = plan.tables()["values"]
+    fz = T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30))
+    try:
+        host_in = torch.from_numpy(vals.copy()).pin_memory()
+        host_out = torch.empty(len(vals), dtype=torch.float64).pin_memory()
+        for _ in range(2):
+            host_out.fill_(0.0)
+            st = fz.factor_host_ptr(host_in.data_ptr(), host_out.data_ptr())
+            check_against_oracle(name, host_out.numpy(), golden, oracle)
+        assert st.mode in (4, 5)
+        out = fz.factor_host(vals)  # pageable buffers work too
+        check_against_oracle(name, out, golden, oracle)
+    finally:
+        fz.close()
+
+
+def test_factor_host_batch(T, oracle):
+    an, vals, perms = c5_members(T, [0, 3, 9])
+    fz = T.GpuFactorizer(planned("c5_m0"), T.GpuOptions(timeout_s=30))
+    try:
+        fz.set_batch(vals)
+        out = fz.factor_host(vals)
+        for i, ap in enumerate(perms):
+            ref, _, _, _ = oracle.factor_serial(ap, an.pattern.pattern)
+            assert bitwise_equal(out[i], ref), i
+    finally:
+        fz.close()
