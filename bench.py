@@ -348,6 +348,122 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def run_sharded(args):
+    """C6 over N GPUs (BASELINE.json configs[4], second half): rank r owns the
+    rows of the r-th level-log2(N) ND subtree, rank 0 also the separators above
+    them; each rank runs its rows (mode 5) and reads the few operands other
+    ranks own straight from their U through CUDA IPC peer mappings over
+    NVLink (tcg_plan_part_problem / tcg_set_peers). Every rank resets its U
+    (phase 1) before any rank's kernel starts (phase 2). value = nnz_u of the
+    one matrix / max-over-ranks time (strong scaling)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1601_05871_b200 as T
+
+    rank, local_rank, world = dist_env()
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    a, an, plan, t_an = build_problem(args.config)
+    ps = plan.stats()
+    u = an.pattern.pattern
+    nnz, n = u.nnz(), a.nrows
+    owners = an.subtree_owners(world, separators=0)
+    problem = plan.part_problem(world, owners, rank)
+    fz = T.GpuFactorizer(plan, T.GpuOptions(device=dev, mode=5, timeout_s=60), problem=problem)
+    handle, offset = fz.ipc_handle()
+    table = [None] * world
+    dist.all_gather_object(table, (handle, offset))
+    ptrs = [fz.values_device_ptr() if r == rank else fz.ipc_open(h, off) for r, (h, off) in enumerate(table)]
+    fz.set_peers(ptrs)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def barrier():
+        torch.cuda.synchronize()
+        dist.barrier()
+
+    def step():
+        fz.factor_phase(1)      # this part's U <- marker
+        barrier()               # ... on every part before any kernel reads it
+        return fz.factor_phase(2)
+
+    clocks = ClockSampler(dev).__enter__()
+    for _ in range(args.warmup):
+        fz.restore()
+        step()
+    dev_ms = []
+    for _ in range(args.steps):
+        fz.restore()
+        flush.fill_(1.0)
+        st = step()
+        dev_ms.append(st.device_ms)
+    barrier()
+    step_ms = max_over(statistics.mean(dev_ms), dev)
+    host_in = torch.from_numpy(plan.tables()["values"]).pin_memory()
+    host_out = torch.empty(nnz, dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1.0)
+        barrier()
+        t0 = time.perf_counter()
+        fz.set_values_ptr(host_in.data_ptr())   # H2D 8*nnz_u
+        step()
+        fz.download_ptr(host_out.data_ptr())    # D2H 8*nnz_u (this rank's rows valid)
+        if i >= args.warmup:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    clocks.__exit__(None, None, None)
+    e2e = max_over(statistics.mean(e2e_ms), dev)
+    # parity: every rank contributes its rows, rank 0 compares with the oracle
+    own = np.repeat(owners, np.diff(u.row_ptr)) == rank
+    mine = torch.from_numpy(np.where(own, host_out.numpy(), 0.0)).to(f"cuda:{dev}")
+    dist.all_reduce(mine)  # rows are disjoint: the sum is the whole factor
+    parity = None
+    if rank == 0:
+        from checkers import Oracle
+        ref, _, _, _ = Oracle().factor_serial(an.a_permuted, u)
+        got = mine.cpu().numpy()
+        parity = "bitwise" if np.array_equal(ref.view(np.int64), got.view(np.int64)) else \
+            f"max_rel={float(np.max(np.abs(got - ref) / (np.abs(ref) + 1e-300))):.3e}"
+    peak, peak_kind = measured_peak()
+    bytes_alg = 20 * nnz + 8 * (n + 1)
+    line = {
+        "metric": METRIC, "value": nnz / (step_ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md Appendix B)",
+        "config": {"workload": WORKLOADS[args.config] + f", ND subtrees sharded over {world} GPUs",
+                   "n": n, "nnz_u": nnz, "flow_rows": int(ps.flow_rows), "flow_depth": int(ps.flow_depth),
+                   "rows_rank0": int(problem.nflow), "remote_operands_rank0": int(problem.remote_operands),
+                   "parallelism": f"ND subtrees over {world} ranks, peer reads over NVLink (CUDA IPC)",
+                   "l2": "flushed between steps (256 MiB write), U restored from device copy (untimed)",
+                   "analysis_s": round(t_an, 3), "parity_vs_oracle": parity},
+        "e2e": {"value": nnz / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz,
+                "d2h_bytes_per_step": 8 * nnz, "ms_per_step": e2e},
+        "gpu_launches": args.steps,
+        "launches_per_step": {"flow_prepare (untimed, before the barrier)": 1, "factor_flow (timed)": 1},
+        "roofline": {"bound": "hbm", "achieved": bytes_alg / (step_ms / 1e3) / 1e9, "peak": peak * world,
+                     "unit": "GB/s", "frac": bytes_alg / (step_ms / 1e3) / 1e9 / (peak * world),
+                     "traffic": None, "peak_kind": peak_kind + f" x {world}",
+                     "algorithmic_bytes_per_launch": bytes_alg},
+        "cpu_baseline": None,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    fz.close()
+    dist.destroy_process_group()
+
+
+def max_over(x, dev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -363,6 +479,8 @@ def main():
         args.warmup = 3
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c6" and dist_env()[2] > 1:
+        run_sharded(args)
     else:
         run_ours(args)
 

@@ -198,6 +198,13 @@ tcg_status tcg_plan_dag(const tcg_plan* plan, int64_t* nnodes, const int32_t** k
 tcg_status tcg_plan_blocks(const tcg_plan* plan, int32_t* m, const int64_t** brow_ptr,
                            int64_t* nblocks, const int32_t** bcol_idx);
 
+/* Sharded value flow (C6: ND subtrees on different GPUs). part_of_row: owner part of every
+ * row of U (n entries, < nparts <= 64). Fills `out` like tcg_plan_problem but with only the
+ * rows of `part` (mode 5 only); operands owned by other parts are read from their copies of
+ * U, set with tcg_set_peers. Valid until the next call for the same part or tcg_plan_free. */
+tcg_status tcg_plan_part_problem(tcg_plan* plan, int32_t nparts, const int32_t* part_of_row, int32_t part,
+                                 tcg_problem* out, int64_t* remote_operands);
+
 /* ---- device context ---------------------------------------------------- */
 tcg_status tcg_create(int device, tcg_ctx** out);
 void tcg_destroy(tcg_ctx* ctx);
@@ -234,6 +241,16 @@ tcg_status tcg_set_batch_values(tcg_ctx* ctx, const double* values); /* same nba
 int32_t tcg_batch_size(const tcg_ctx* ctx);
 tcg_status tcg_download_batch(tcg_ctx* ctx, double* values);
 tcg_status tcg_batch_breakdown(tcg_ctx* ctx, int32_t* rows, double* pivots);
+/* Mode 5 in two steps (sharded runs): phase 1 resets the output (and waits for it), phase 2
+ * launches the factorization; 0 = both, as tcg_factor. Between them the caller makes sure
+ * every part has finished phase 1, since parts read each other's U. */
+tcg_status tcg_factor_phase(tcg_ctx* ctx, int32_t phase, tcg_stats* stats);
+/* Sharded runs: device pointers of every part's working values (index = part; own included,
+ * from tcg_device_values, or tcg_ipc_open for parts in other processes). */
+tcg_status tcg_set_peers(tcg_ctx* ctx, int32_t nparts, const uint64_t* values_ptrs);
+/* CUDA IPC of the working values: a 64-byte handle of the arena plus the values' offset. */
+tcg_status tcg_ipc_values_handle(tcg_ctx* ctx, void* handle, int64_t* offset);
+tcg_status tcg_ipc_open(tcg_ctx* ctx, const void* handle, int64_t offset, uint64_t* values_ptr);
 /* Bytes of the device arena. */
 int64_t tcg_arena_bytes(const tcg_ctx* ctx);
 
@@ -257,6 +274,10 @@ void tch_analysis_free(tch_analysis* an);
 const char* tch_error(void); /* thread-local message of the last tch_* failure */
 void tch_analysis_perm(const tch_analysis* an, const int32_t** perm, const int32_t** iperm);
 int32_t tch_analysis_ranges(const tch_analysis* an, const int32_t** bounds); /* returns count */
+/* Row spans [lo, hi) of the ND subtrees at `depth` (a shallower leaf stands for itself);
+ * writes at most `cap` of them and returns their count. Rows outside every span are the
+ * separators above them. */
+int32_t tch_analysis_subtrees(const tch_analysis* an, int32_t depth, int32_t cap, int32_t* lo, int32_t* hi);
 void tch_analysis_permuted(const tch_analysis* an, tcg_csr_view* out);
 void tch_analysis_pattern(const tch_analysis* an, tcg_csr_view* out);
 void tch_analysis_times(const tch_analysis* an, double* ordering_s, double* symbolic_s);

@@ -160,6 +160,7 @@ SIGNATURES = [
     ("tcg_plan_error", C.c_char_p, []),
     ("tcg_plan_problem", C.c_int, [C.c_void_p, C.POINTER(Problem)]),
     ("tcg_plan_get_stats", C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
+    ("tcg_plan_part_problem", C.c_int, [C.c_void_p, C.c_int32, i32p, C.c_int32, C.POINTER(Problem), i64p]),
     ("tcg_plan_dag", C.c_int, [C.c_void_p, i64p, C.POINTER(i32p), C.POINTER(i32p), C.POINTER(i32p),
                                 i64p, C.POINTER(i32p), C.POINTER(i32p)]),
     ("tcg_plan_blocks", C.c_int, [C.c_void_p, i32p, C.POINTER(i64p), i64p, C.POINTER(i32p)]),
@@ -181,6 +182,10 @@ SIGNATURES = [
     ("tcg_batch_breakdown", C.c_int, [C.c_void_p, i32p, f64p]),
     ("tcg_device_values", C.c_int, [C.c_void_p, C.POINTER(f64p), i64p]),
     ("tcg_arena_bytes", C.c_int64, [C.c_void_p]),
+    ("tcg_set_peers", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64)]),
+    ("tcg_factor_phase", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    ("tcg_ipc_values_handle", C.c_int, [C.c_void_p, C.c_void_p, i64p]),
+    ("tcg_ipc_open", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_uint64)]),
     ("tch_generate", C.c_void_p, [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]),
     ("tch_matrix_from_csr", C.c_void_p, [C.POINTER(CsrView)]),
     ("tch_matrix_free", None, [C.c_void_p]),
@@ -190,6 +195,7 @@ SIGNATURES = [
     ("tch_error", C.c_char_p, []),
     ("tch_analysis_perm", None, [C.c_void_p, C.POINTER(i32p), C.POINTER(i32p)]),
     ("tch_analysis_ranges", C.c_int32, [C.c_void_p, C.POINTER(i32p)]),
+    ("tch_analysis_subtrees", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, i32p, i32p]),
     ("tch_analysis_permuted", None, [C.c_void_p, C.POINTER(CsrView)]),
     ("tch_analysis_pattern", None, [C.c_void_p, C.POINTER(CsrView)]),
     ("tch_analysis_times", None, [C.c_void_p, f64p, f64p]),

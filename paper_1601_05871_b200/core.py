@@ -116,6 +116,23 @@ class Analysis:
     pattern: FillPattern
     ordering_seconds: float = 0.0
     symbolic_seconds: float = 0.0
+    # ND subtree row spans per depth (0..6): {depth: (lo, hi)}; rows outside
+    # every span at a depth are the separators above it
+    subtree_spans: Optional[dict] = None
+
+    def subtree_owners(self, nparts: int, separators: Optional[int] = 0) -> np.ndarray:
+        """Owner part of every row for a sharded run over `nparts` (a power of
+        two): the depth-log2(nparts) subtrees in order, the separators above
+        them to part `separators` (an extra part when it equals nparts)."""
+        depth = max(0, int(nparts).bit_length() - 1)
+        if 1 << depth != nparts or depth not in (self.subtree_spans or {}):
+            raise ValueError("subtree_owners: nparts must be a power of two up to 64")
+        lo, hi = self.subtree_spans[depth]
+        owners = np.full(self.perm.shape[0], separators, dtype=np.int32)
+        # more subtrees than parts (nodes with several children): contiguous groups
+        for i, (a, b) in enumerate(zip(lo, hi)):
+            owners[a:b] = i * nparts // len(lo)
+        return owners
 
 
 @dataclass
@@ -244,10 +261,18 @@ def analyze(a: CsrMatrix, level: int = 0, treecut: int = 0, leaf_size: int = 64,
             nnz_triu = int(np.count_nonzero(
                 a_perm.col_idx >= np.repeat(np.arange(a_perm.nrows, dtype=np.int64),
                                             np.diff(a_perm.row_ptr))))
+            spans = {}
+            for depth in range(7):
+                k = lib.tch_analysis_subtrees(h, depth, 0, None, None)
+                lo = np.zeros(max(k, 1), np.int32)
+                hi = np.zeros(max(k, 1), np.int32)
+                lib.tch_analysis_subtrees(h, depth, k, lo.ctypes.data_as(N.i32p), hi.ctypes.data_as(N.i32p))
+                spans[depth] = (lo[:k].copy(), hi[:k].copy())
             return Analysis(perm=_copy(perm, a.nrows, np.int32), iperm=_copy(iperm, a.nrows, np.int32),
                             ranges=RangeList(_copy(bounds, cnt + 1, np.int32)), a_permuted=a_perm,
                             pattern=FillPattern(pattern, level, nnz_triu),
-                            ordering_seconds=t_ord.value, symbolic_seconds=t_sym.value)
+                            ordering_seconds=t_ord.value, symbolic_seconds=t_sym.value,
+                            subtree_spans=spans)
         finally:
             lib.tch_analysis_free(h)
     finally:
@@ -320,6 +345,18 @@ class Plan:
     def problem(self) -> N.Problem:
         p = N.Problem()
         self._lib.tcg_plan_problem(self.handle, C.byref(p))
+        return p
+
+    def part_problem(self, nparts: int, owners: np.ndarray, part: int) -> N.Problem:
+        """The rows of one part of a sharded run (tcg_plan_part_problem, mode 5)."""
+        own = np.ascontiguousarray(owners, dtype=np.int32)
+        p = N.Problem()
+        remote = C.c_int64()
+        rc = self._lib.tcg_plan_part_problem(self.handle, nparts, own.ctypes.data_as(N.i32p), part,
+                                             C.byref(p), C.byref(remote))
+        if rc != 0:
+            raise ValueError(self._lib.tcg_plan_error().decode())
+        p.remote_operands = remote.value  # python-side annotation
         return p
 
     def dag(self) -> TaskDag:
@@ -412,7 +449,7 @@ class GpuOptions:
 class GpuFactorizer:
     """A device context holding one uploaded plan (tcg_ctx)."""
 
-    def __init__(self, plan: Plan, options: Optional[GpuOptions] = None):
+    def __init__(self, plan: Plan, options: Optional[GpuOptions] = None, problem: Optional[N.Problem] = None):
         self.opt = options or GpuOptions()
         lib = _lib()
         self._lib = lib
@@ -426,7 +463,7 @@ class GpuFactorizer:
                       self.opt.lanes_per_row)
         self._check(lib.tcg_set_options(self.ctx, C.byref(o)))
         self.plan = plan
-        self._problem = plan.problem()
+        self._problem = problem if problem is not None else plan.problem()
         self.nnz = int(self._problem.nnz)
         self.ntasks = int(self._problem.ntasks)
         self._check(lib.tcg_upload(self.ctx, C.byref(self._problem)))
@@ -532,6 +569,35 @@ class GpuFactorizer:
         out = np.zeros(2 * self.ntasks + 4 * ni, dtype=np.uint64)
         self._check(self._lib.tcg_download_trace(self.ctx, out.ctypes.data_as(N.u64p)))
         return out[:2 * self.ntasks].reshape(-1, 2), out[2 * self.ntasks:].reshape(-1, 4)
+
+    # ---- sharded runs (C6): other parts' U through peer memory ----
+    def factor_phase(self, phase: int) -> N.Stats:
+        """1: reset the output; 2: launch (after every part finished phase 1)."""
+        self.last = N.Stats()
+        self._check(self._lib.tcg_factor_phase(self.ctx, phase, C.byref(self.last)))
+        return self.last
+
+    def values_device_ptr(self) -> int:
+        d = N.f64p()
+        n = C.c_int64()
+        self._check(self._lib.tcg_device_values(self.ctx, C.byref(d), C.byref(n)))
+        return C.cast(d, C.c_void_p).value or 0
+
+    def set_peers(self, ptrs):
+        arr = (C.c_uint64 * len(ptrs))(*[int(x) for x in ptrs])
+        self._check(self._lib.tcg_set_peers(self.ctx, len(ptrs), arr))
+
+    def ipc_handle(self):
+        h = (C.c_char * 64)()
+        off = C.c_int64()
+        self._check(self._lib.tcg_ipc_values_handle(self.ctx, h, C.byref(off)))
+        return bytes(h), off.value
+
+    def ipc_open(self, handle: bytes, offset: int) -> int:
+        h = (C.c_char * 64).from_buffer_copy(handle)
+        ptr = C.c_uint64()
+        self._check(self._lib.tcg_ipc_open(self.ctx, h, offset, C.byref(ptr)))
+        return ptr.value
 
     def arena_bytes(self) -> int:
         return int(self._lib.tcg_arena_bytes(self.ctx))

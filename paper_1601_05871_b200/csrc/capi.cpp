@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <new>
 #include <string>
@@ -56,6 +57,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 struct tcg_plan {
   tcb::Plan plan;
   std::vector<std::int32_t> brow_ptr32;  // unused, kept for ABI symmetry
+  std::map<std::int32_t, tcb::FlowPart> parts;  // tcg_plan_part_problem results
 };
 
 struct tcg_ctx {
@@ -114,6 +116,9 @@ struct tcg_ctx {
   int2* m6_upd = nullptr;
   std::int64_t m6_nrows = 0, m6_nunits = 0, m6_smem = 0;
   bool has_units = false;
+  double** peers = nullptr;  // sharded runs: device table of every part's U (own included)
+  int npeers = 0;
+  std::vector<void*> ipc_opened;  // peer arenas mapped by tcg_ipc_open
   int* m_flags = nullptr;    // per member: breakdown latch, row (2 ints) + pivot (below)
   double* m_pivot = nullptr;
   // batch of value sets sharing the pattern (mode 5); separate allocation
@@ -255,6 +260,48 @@ tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   return TCG_OK;
 }
 
+tcg_status tcg_plan_part_problem(tcg_plan* plan, int32_t nparts, const int32_t* part_of_row, int32_t part,
+                                 tcg_problem* o, int64_t* remote_operands) {
+  if (!plan || !o || !part_of_row) return TCG_INVALID;
+  const tcb::Plan& P = plan->plan;
+  try {
+    std::vector<std::int32_t> own(part_of_row, part_of_row + P.n);
+    plan->parts[part] = tcb::build_flow_part(P, own, nparts, part);
+  } catch (const std::exception& e) {
+    g_plan_error = e.what();
+    return TCG_INVALID;
+  }
+  const tcb::FlowPart& F = plan->parts[part];
+  tcg_status st = tcg_plan_problem(plan, o);
+  if (st != TCG_OK) return st;
+  // only the value-flow tables describe a part: every other executor is off
+  o->row_rec = nullptr;
+  o->nrow_edges = 0;
+  o->row_succ = nullptr;
+  o->row_indeg = nullptr;
+  o->nrow_roots = 0;
+  o->row_roots = nullptr;
+  o->row_order = nullptr;
+  o->row_pred_ptr = nullptr;
+  o->row_pred = nullptr;
+  o->pos_rec = nullptr;
+  o->npos_pred = 0;
+  o->pos_pred = nullptr;
+  o->nslots = 0;
+  o->slot_rec = nullptr;
+  o->nupdates = 0;
+  o->upd = nullptr;
+  o->m6_nunits = 0;
+  o->nflow = F.rows;
+  o->flow_rec = F.rec.data();
+  o->flow_item = F.item.data();
+  o->flow_slot = F.slot.data();
+  o->nflow_upd = static_cast<int64_t>(F.upd.size() / 2);
+  o->flow_upd = F.upd.data();
+  if (remote_operands) *remote_operands = F.remote_operands;
+  return TCG_OK;
+}
+
 tcg_status tcg_plan_get_stats(const tcg_plan* plan, tcg_plan_stats* o) {
   if (!plan || !o) return TCG_INVALID;
   const tcb::PlanStats& s = plan->plan.stats;
@@ -338,6 +385,9 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
 
 void tcg_destroy(tcg_ctx* c) {
   if (c && c->batch_arena) cudaFree(c->batch_arena);
+  if (c && c->peers) cudaFree(c->peers);
+  if (c)
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
@@ -612,7 +662,7 @@ tcg_status tcg_restore(tcg_ctx* c) {
 // copy_stream that runs beside the kernel (the kernel polls them, as it
 // polls operands), and the factor is copied back on the launch stream.
 static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* host_in = nullptr,
-                           double* host_out = nullptr) {
+                           double* host_out = nullptr, int phase = 0) {
   int kb = 4, minb = threads == 128 ? 6 : threads == 384 ? 2 : threads == 256 ? 3 : 1;
   if (const char* e = std::getenv("TCG_FLOW_KB")) kb = std::atoi(e);
   if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
@@ -621,8 +671,10 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   int weak = 0, dyn = 0;
   if (const char* e = std::getenv("TCG_FLOW_WEAK")) weak = std::atoi(e);
   if (const char* e = std::getenv("TCG_FLOW_DYN")) dyn = std::atoi(e);
+  int remote = c->npeers > 1 ? 1 : 0;  // sharded: operands of other parts via peers
+  if (const char* e = std::getenv("TCG_FLOW_REMOTE")) remote = std::atoi(e) ? 1 : remote;
   int occ = 0;
-  TCG_CUDA_TRY(c, tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, &occ));
+  TCG_CUDA_TRY(c, tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ));
   if (occ < 1) {
     c->err = "value-flow kernel does not fit on an SM";
     return TCG_INVALID;
@@ -648,6 +700,8 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   q.input_async = host_in != nullptr;
   tcbdev::FlowParams P{};
   P.input_async = host_in != nullptr;
+  P.peers = c->peers;
+  P.npeers = c->npeers;
   P.rec = c->flow_rec;
   P.item = c->flow_item;
   P.slot = c->flow_slot;
@@ -665,13 +719,18 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
   const size_t vbytes = sizeof(double) * static_cast<size_t>(c->nnz) * c->nbatch;
+  if (phase == 1) {  // sharded runs: every part resets its U before any part's kernel starts
+    TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
+    TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    return TCG_OK;
+  }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
-  TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
+  if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
   if (host_in) {  // inputs stream in while the kernel runs
     TCG_CUDA_TRY(c, cudaEventRecord(c->ev_prep, c->stream));
     TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_prep, 0));
   }
-  if (c->nflow > 0) TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, c->stream));
+  if (c->nflow > 0) TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
   if (host_in) {
     TCG_CUDA_TRY(c, cudaMemcpyAsync(q.a, host_in, vbytes, cudaMemcpyHostToDevice, c->copy_stream));
     TCG_CUDA_TRY(c, cudaEventRecord(c->ev_copy, c->copy_stream));
@@ -689,7 +748,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   S.grid_ctas = grid;
   S.threads_per_cta = threads;
   S.staging_cap = kb;  // reported: gather batch
-  S.kernel_launches = c->nflow > 0 ? 2 : 1;
+  S.kernel_launches = (c->nflow > 0 ? 1 : 0) + (phase == 0 ? 1 : 0);
   S.mode = 5;
   S.lanes_per_row = g;
   const int64_t rows = c->nflow * c->nbatch;
@@ -1123,6 +1182,24 @@ tcg_status tcg_download(tcg_ctx* c, double* values) {
   return TCG_OK;
 }
 
+tcg_status tcg_factor_phase(tcg_ctx* c, int32_t phase, tcg_stats* st) {
+  if (!c || !c->uploaded || phase < 0 || phase > 2) return TCG_INVALID;
+  if (phase == 0) return tcg_factor(c, st);
+  if (!c->has_flow || (c->opt.mode != 0 && c->opt.mode != 5)) {
+    c->err = "tcg_factor_phase: split phases exist in mode 5 only";
+    return TCG_INVALID;
+  }
+  tcg_stats local{};
+  tcg_stats& S = st ? *st : local;
+  S = tcg_stats{};
+  S.breakdown_row = -1;
+  S.breakdown_member = -1;
+  S.batch = 1;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
+  return run_flow(c, S, threads, nullptr, nullptr, phase);
+}
+
 tcg_status tcg_factor_host(tcg_ctx* c, const double* values_in, double* values_out, tcg_stats* st) {
   if (!c || !c->uploaded || ((!values_in || !values_out) && c->nnz > 0)) return TCG_INVALID;
   int mode = c->opt.mode;
@@ -1234,6 +1311,43 @@ tcg_status tcg_device_values(tcg_ctx* c, double** dptr, int64_t* nnz) {
 
 int64_t tcg_arena_bytes(const tcg_ctx* c) { return c ? static_cast<int64_t>(c->arena_bytes) : 0; }
 
+tcg_status tcg_set_peers(tcg_ctx* c, int32_t nparts, const uint64_t* values_ptrs) {
+  if (!c || nparts < 0 || nparts > 64 || (nparts > 0 && !values_ptrs)) return TCG_INVALID;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  if (c->peers) {
+    TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    TCG_CUDA_TRY(c, cudaFree(c->peers));
+    c->peers = nullptr;
+  }
+  c->npeers = nparts;
+  if (nparts == 0) return TCG_OK;
+  TCG_CUDA_TRY(c, cudaMalloc(&c->peers, sizeof(double*) * nparts));
+  TCG_CUDA_TRY(c, cudaMemcpy(c->peers, values_ptrs, sizeof(double*) * nparts, cudaMemcpyHostToDevice));
+  return TCG_OK;
+}
+
+tcg_status tcg_ipc_values_handle(tcg_ctx* c, void* handle, int64_t* offset) {
+  if (!c || !c->uploaded || !handle || !offset) return TCG_INVALID;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  TCG_CUDA_TRY(c, cudaIpcGetMemHandle(&h, c->arena));
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = static_cast<int64_t>(reinterpret_cast<char*>(c->vals) - static_cast<char*>(c->arena));
+  return TCG_OK;
+}
+
+tcg_status tcg_ipc_open(tcg_ctx* c, const void* handle, int64_t offset, uint64_t* values_ptr) {
+  if (!c || !handle || !values_ptr || offset < 0) return TCG_INVALID;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  TCG_CUDA_TRY(c, cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  c->ipc_opened.push_back(p);
+  *values_ptr = reinterpret_cast<uint64_t>(static_cast<char*>(p) + offset);
+  return TCG_OK;
+}
+
 // ------------------------------------------------------------ analysis ----
 
 struct tch_matrix {
@@ -1314,6 +1428,27 @@ void tch_analysis_perm(const tch_analysis* an, const int32_t** perm, const int32
   if (!an) return;
   if (perm) *perm = an->an.perm.perm.data();
   if (iperm) *iperm = an->an.perm.iperm.data();
+}
+
+int32_t tch_analysis_subtrees(const tch_analysis* an, int32_t depth, int32_t cap, int32_t* lo, int32_t* hi) {
+  if (!an || depth < 0 || depth > 20) return -1;
+  const tcb::NdTree& T = an->an.tree;
+  if (T.root < 0) return 0;
+  std::vector<tcb::index_t> level{T.root};
+  for (int32_t d = 0; d < depth; ++d) {  // a leaf above `depth` stands for itself
+    std::vector<tcb::index_t> next;
+    for (tcb::index_t id : level) {
+      const auto& ch = T.nodes[id].children;
+      if (ch.empty()) next.push_back(id);
+      else next.insert(next.end(), ch.begin(), ch.end());
+    }
+    level.swap(next);
+  }
+  for (size_t i = 0; i < level.size() && static_cast<int32_t>(i) < cap; ++i) {
+    if (lo) lo[i] = T.span_begin(level[i]);
+    if (hi) hi[i] = T.span_end(level[i]);
+  }
+  return static_cast<int32_t>(level.size());
 }
 
 int32_t tch_analysis_ranges(const tch_analysis* an, const int32_t** bounds) {

@@ -20,10 +20,11 @@ cudaError_t launch_rows(const RowParams& p, int grid, int threads, int minb, cud
 cudaError_t static_occupancy(int threads, int group, int* ctas_per_sm);
 cudaError_t launch_static(const StaticParams& p, int grid, int threads, int group, cudaStream_t st);
 
-cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int dyn, int* ctas_per_sm);
+cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int dyn, int remote,
+                           int* ctas_per_sm);
 cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStream_t st);
 cudaError_t launch_flow(const FlowParams& p, int grid, int threads, int kb, int minb, int g,
-                        int weak, int dyn, cudaStream_t st);
+                        int weak, int dyn, int remote, cudaStream_t st);
 
 cudaError_t unit_occupancy(int threads, int kb, int minb, int weak, size_t smem, int* ctas_per_sm);
 cudaError_t launch_units(const FlowParams& p, const UnitParams& u, int grid, int threads, int kb, int minb,

@@ -121,6 +121,8 @@ struct FlowParams {
   int nrows;             // schedule rows (per member)
   int nbatch;            // members sharing the pattern
   int input_async;       // the inputs `a` arrive during the launch (kUnset until copied): poll them
+  double* const* peers;  // sharded (C6): every part's U, indexed by part; operands of other parts
+  int npeers;            //   arrive as kRemoteBit | part << 25 | position (plan.hpp build_flow_part)
   unsigned long long timeout_ns;
 };
 

@@ -48,6 +48,24 @@ __device__ __forceinline__ unsigned long long wait_value(const double* p, Ctrl* 
   }
 }
 
+// The same poll at system scope: a value owned by a part on another GPU.
+__device__ __forceinline__ unsigned long long wait_value_sys(const double* p, Ctrl* ctrl,
+                                                          unsigned long long t0,
+                                                          unsigned long long tmo) {
+  unsigned spins = 0;
+  for (;;) {
+    const unsigned long long x = ld_relaxed_sys_u64(p);
+    if (x != kUnset) return x;
+    if (++spins == 1024u) {
+      spins = 0;
+      if (ld_relaxed(&ctrl->error.v) || gtimer() - t0 > tmo) {
+        atomicCAS(&ctrl->error.v, 0, 1);
+        return 0ull;
+      }
+    }
+  }
+}
+
 // WEAK: first attempt of every gather is a plain (L1-cached) load; only a
 // kUnset answer falls back to strong polling. Sound because a location
 // holds kUnset until its single final value is written: any other bits a
@@ -57,7 +75,10 @@ __device__ __forceinline__ unsigned long long wait_value(const double* p, Ctrl* 
 // are nnz apart; the pattern, records and programs are shared).
 // LOCAL (mode 6 units): a negative operand position is kLocalBit | index
 // into the unit's values in shared memory `sv`, final by construction.
-template <int WEAK, int LOCAL = 0>
+// OPS: how a negative operand position is read. 0: never happens; 1 (mode
+// 6): kLocalBit | index into the unit's shared-memory values `sv`; 2
+// (sharded runs): kRemoteBit | part << 25 | position in that part's U.
+template <int WEAK, int OPS = 0>
 struct Ctx {
   const FlowParams& P;
   unsigned long long t0;
@@ -69,11 +90,25 @@ struct Ctx {
     if (x == kUnset) x = wait_value(p, P.ctrl, t0, P.timeout_ns);
     return __longlong_as_double(static_cast<long long>(x));
   }
+  // sharded runs (P.peers): a negative position names another part's value
+  __device__ __forceinline__ const double* remote(int pos) const {
+    return P.peers[(pos >> 25) & 63] + (pos & 0x1FFFFFF);
+  }
   __device__ __forceinline__ unsigned long long ld(int pos) const {
-    if (LOCAL && pos < 0) return static_cast<unsigned long long>(__double_as_longlong(sv[pos & 0x7fffffff]));
+    if (OPS == 1 && pos < 0) return static_cast<unsigned long long>(__double_as_longlong(sv[pos & 0x7fffffff]));
+    if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
     if (WEAK) return ld_weak_u64(vals + pos);
     return ld_relaxed_u64(vals + pos);
   }
+  // settle an operand by its (encoded) position
+  __device__ __forceinline__ double settle_at(int pos, unsigned long long x) const {
+    if (x == kUnset) {
+      if (OPS == 2 && pos < 0) x = wait_value_sys(remote(pos), P.ctrl, t0, P.timeout_ns);
+      else x = wait_value(vals + pos, P.ctrl, t0, P.timeout_ns);
+    }
+    return __longlong_as_double(static_cast<long long>(x));
+  }
+  static constexpr bool kSysPublish = OPS == 2;  // readers on other GPUs
 };
 
 // An input value: immutable during the launch (read-only path), or, when
@@ -103,7 +138,7 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
   int2 p[KB];
 #pragma unroll
   for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
-  v = __dsub_rn(v, __dmul_rn(C.settle(C.vals + sr.z, xa0), C.settle(C.vals + sr.w, xb0)));
+  v = __dsub_rn(v, __dmul_rn(C.settle_at(sr.z, xa0), C.settle_at(sr.w, xb0)));
   while (u < ue) {
     const int n = min(KB, ue - u);
     unsigned long long xa[KB], xb[KB];
@@ -120,8 +155,7 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 #pragma unroll
     for (int j = 0; j < KB; ++j)
       if (j < n)
-        v = __dsub_rn(v, __dmul_rn(C.settle(C.vals + c[j].x, xa[j]),
-                                   C.settle(C.vals + c[j].y, xb[j])));
+        v = __dsub_rn(v, __dmul_rn(C.settle_at(c[j].x, xa[j]), C.settle_at(c[j].y, xb[j])));
   }
   return v;
 }
@@ -134,7 +168,8 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 template <int KIND, int KB, int G, class Cx>
 __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, int t, int gl,
                                          unsigned gmask, int lead, double a0, int4 sr0,
-                                         unsigned long long* stamp, double* local_out = nullptr) {
+                                         unsigned long long* stamp, double* local_out = nullptr,
+                                         bool exported = false) {
   const FlowParams& P = C.P;
   unsigned long long xd = 0;
   if (KIND == kTrsm) xd = C.ld(dpos);
@@ -167,11 +202,16 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
     if (local_out) local_out[k] = y;  // mode 6: the unit's copy for its later rows
     return static_cast<unsigned long long>(__double_as_longlong(y));
   };
-  if (gl < L) st_relaxed_u64(C.vals + tb + gl, finish(gl, v));
+  // sharded runs publish at system scope: readers may sit on other GPUs
+  auto publish = [&](int k, unsigned long long y) {
+    if (Cx::kSysPublish && exported) st_relaxed_sys_u64(C.vals + tb + k, y);
+    else st_relaxed_u64(C.vals + tb + k, y);
+  };
+  if (gl < L) publish(gl, finish(gl, v));
   for (int k = gl + G; k < L; k += G) {
     const double w = flow_slot<KB>(C, input_settle(P, C.a + tb + k, input_ld(P, C.a + tb + k), C.t0),
                                    __ldg(P.slot + tb + k));
-    st_relaxed_u64(C.vals + tb + k, finish(k, w));
+    publish(k, finish(k, w));
   }
 }
 
@@ -186,7 +226,7 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
 //   Still deadlock-free: the lowest unfinished position is either some
 //   group's current row (its operands are final) or was never handed out,
 //   which cannot be while every group of its CTA holds lower rows.
-template <int THREADS, int KB, int MINB, int G, int WEAK, int DYN>
+template <int THREADS, int KB, int MINB, int G, int WEAK, int DYN, int REMOTE>
 __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
   constexpr int kGroups = THREADS / G;
   constexpr int kLenMask = (1 << 30) - 1;
@@ -195,7 +235,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
   const int lead = lane & ~(G - 1);
   const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << lead);
   const int W = gridDim.x * kGroups;
-  Ctx<WEAK> C{P, gtimer(), P.vals, P.a, 0};
+  Ctx<WEAK, REMOTE ? 2 : 0> C{P, gtimer(), P.vals, P.a, 0};
   int ran = 0, executed = 0, anyfail = 0;
   // batch: position pos is schedule row pos / nbatch of member pos % nbatch
   // (the members of one row sit side by side, so level order is kept)
@@ -251,7 +291,8 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
       na0 = input_ld(P, input_of(npos) + na.x + gl);
     }
     const int tb = a.x, L = a.y & kLenMask, dpos = a.z, t = a.w;
-    const bool chol = (static_cast<unsigned>(a.y) >> 30) == kChol;
+    const bool chol = ((a.y >> 30) & 1) == kChol;
+    const bool exported = a.y < 0;  // sharded: bit 31 = some other part reads this row
     int q;
     C.member = member_of(pos, q);
     C.vals = P.vals + static_cast<long long>(C.member) * P.nnz;
@@ -273,9 +314,11 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
     }
     if (!latched) {
       if (chol)
-        flow_row<kChol, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr);
+        flow_row<kChol, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr,
+                               nullptr, exported);
       else
-        flow_row<kTrsm, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr);
+        flow_row<kTrsm, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr,
+                               nullptr, exported);
       ++executed;
     } else {
       // skipped rows keep their input values (readers must not wait forever)
@@ -284,7 +327,8 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
         unsigned long long x = static_cast<unsigned long long>(
             __double_as_longlong(input_settle(P, ap, input_ld(P, ap), C.t0)));
         if (x == kUnset) x = kCanonicalNaN;
-        st_relaxed_u64(C.vals + tb + k, x);
+        if (decltype(C)::kSysPublish && exported) st_relaxed_sys_u64(C.vals + tb + k, x);
+        else st_relaxed_u64(C.vals + tb + k, x);
       }
     }
     if (traced) stamp[3] = gtimer();
@@ -387,7 +431,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_units(FlowParams P, Unit
         na0 = __ldg(P.a + na.x + lane);
       }
       const int tb = a.x, L = a.y & kLenMask, dpos = a.z, t = a.w;
-      const bool chol = (static_cast<unsigned>(a.y) >> 30) == kChol;
+      const bool chol = ((a.y >> 30) & 1) == kChol;
       unsigned long long* stamp = P.trace ? P.trace + 4 * static_cast<long long>(__ldg(P.item + pos)) : nullptr;
       if (stamp && lane == 0) stamp[0] = gtimer();
       if (!latched()) {
@@ -448,21 +492,22 @@ __global__ void flow_prepare(FlowPrepParams Q) {
 // targets; G: lanes per row. Measured on B200 (C1-C5): whole warps per row
 // win everywhere -- the groups of a warp diverge on their polls and product
 // counts, and their rows serialise; G = 8 is kept for experiments.
-#define TCG_FLOW_VARIANTS(X)                                                             \
-  X(256, 4, 3, 32, 0, 0) X(256, 4, 3, 32, 1, 0) X(128, 4, 6, 32, 0, 0) X(512, 4, 1, 32, 0, 0) \
-  X(256, 4, 3, 32, 0, 1) X(768, 4, 1, 32, 0, 1) X(768, 4, 1, 32, 0, 0) X(384, 4, 2, 32, 0, 1)
+#define TCG_FLOW_VARIANTS(X)                                                                   \
+  X(256, 4, 3, 32, 0, 0, 0) X(256, 4, 3, 32, 1, 0, 0) X(128, 4, 6, 32, 0, 0, 0) X(512, 4, 1, 32, 0, 0, 0) \
+  X(256, 4, 3, 32, 0, 1, 0) X(256, 4, 3, 32, 0, 0, 1) X(128, 4, 6, 32, 0, 0, 1) X(512, 4, 1, 32, 0, 0, 1)
 
-static const void* flow_kernel_for(int threads, int kb, int minb, int g, int weak, int dyn) {
-#define X(T, K, M, GG, WK, D)                                                         \
-  if (threads == T && kb == K && minb == M && g == GG && weak == WK && dyn == D)      \
-    return reinterpret_cast<const void*>(&factor_flow<T, K, M, GG, WK, D>);
+static const void* flow_kernel_for(int threads, int kb, int minb, int g, int weak, int dyn, int remote) {
+#define X(T, K, M, GG, WK, D, R)                                                                     \
+  if (threads == T && kb == K && minb == M && g == GG && weak == WK && dyn == D && remote == R)      \
+    return reinterpret_cast<const void*>(&factor_flow<T, K, M, GG, WK, D, R>);
   TCG_FLOW_VARIANTS(X)
 #undef X
   return nullptr;
 }
 
-cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int dyn, int* ctas_per_sm) {
-  const void* k = flow_kernel_for(threads, kb, minb, g, weak, dyn);
+cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int dyn, int remote,
+                           int* ctas_per_sm) {
+  const void* k = flow_kernel_for(threads, kb, minb, g, weak, dyn, remote);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
 }
@@ -506,11 +551,11 @@ cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStrea
 }
 
 cudaError_t launch_flow(const FlowParams& p, int grid, int threads, int kb, int minb, int g,
-                        int weak, int dyn, cudaStream_t st) {
-#define X(T, K, M, GG, WK, D)                                                          \
-  if (threads == T && kb == K && minb == M && g == GG && weak == WK && dyn == D) {     \
-    factor_flow<T, K, M, GG, WK, D><<<grid, T, 0, st>>>(p);                            \
-    return cudaGetLastError();                                                         \
+                        int weak, int dyn, int remote, cudaStream_t st) {
+#define X(T, K, M, GG, WK, D, R)                                                                   \
+  if (threads == T && kb == K && minb == M && g == GG && weak == WK && dyn == D && remote == R) {  \
+    factor_flow<T, K, M, GG, WK, D, R><<<grid, T, 0, st>>>(p);                                     \
+    return cudaGetLastError();                                                                     \
   }
   TCG_FLOW_VARIANTS(X)
 #undef X

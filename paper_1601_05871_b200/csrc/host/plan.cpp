@@ -1009,4 +1009,73 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
   return P;
 }
 
+FlowPart build_flow_part(const Plan& P, const std::vector<std::int32_t>& part_of_row, std::int32_t nparts,
+                         std::int32_t part) {
+  if (P.flow_rec.empty()) throw std::invalid_argument("flow part: the plan has no value-flow tables");
+  if (nparts < 1 || nparts > 64 || part < 0 || part >= nparts)
+    throw std::invalid_argument("flow part: need 1 <= nparts <= 64 and 0 <= part < nparts");
+  if (static_cast<index_t>(part_of_row.size()) != P.n) throw std::invalid_argument("flow part: one owner per row");
+  if (P.nnz >= (std::int64_t{1} << kRemoteShift)) throw std::length_error("flow part: U beyond 2^25 entries");
+  for (std::int32_t o : part_of_row)
+    if (o < 0 || o >= nparts) throw std::invalid_argument("flow part: owner out of range");
+  const std::size_t R = P.flow_item.size();
+  auto owner_of_pos = [&](std::int32_t pos) {
+    const std::int32_t item = P.flow_owner[pos];
+    return part_of_row[P.row_rec[static_cast<std::size_t>(item) * kRowWords + 5]];
+  };
+  // rows of this part that other parts read: they publish at system scope
+  std::vector<char> exported(static_cast<std::size_t>(P.n), 0);
+  for (std::size_t q = 0; q < R; ++q) {
+    const std::int32_t* r = &P.flow_rec[q * kFlowWords];
+    if (part_of_row[r[3]] == part) continue;
+    const std::int32_t L = r[1] & ((1 << kFlowKindShift) - 1);
+    for (std::int32_t j = 0; j < L; ++j) {
+      const std::int32_t* sl = &P.flow_slot[4 * static_cast<std::size_t>(r[0] + j)];
+      for (std::int32_t e = sl[0]; e < sl[1]; ++e)
+        for (int h = 0; h < 2; ++h) {
+          const std::int32_t x = P.flow_upd[2 * static_cast<std::size_t>(e) + h];
+          if (owner_of_pos(x) == part)
+            exported[P.row_rec[static_cast<std::size_t>(P.flow_owner[x]) * kRowWords + 5]] = 1;
+        }
+    }
+  }
+  FlowPart F;
+  F.slot.assign(4 * static_cast<std::size_t>(P.nnz), 0);
+  for (std::size_t q = 0; q < R; ++q) {
+    const std::int32_t* r = &P.flow_rec[q * kFlowWords];
+    if (part_of_row[r[3]] != part) continue;
+    F.rec.insert(F.rec.end(), r, r + kFlowWords);
+    if (exported[r[3]]) {  // bit 31 of the length word: publish at system scope
+      F.rec[F.rec.size() - 3] = static_cast<std::int32_t>(static_cast<std::uint32_t>(F.rec[F.rec.size() - 3]) | 0x80000000u);
+      ++F.exported_rows;
+    }
+    F.item.push_back(P.flow_item[q]);
+    const std::int32_t L = r[1] & ((1 << kFlowKindShift) - 1);
+    for (std::int32_t j = 0; j < L; ++j) {
+      const std::int32_t* sl = &P.flow_slot[4 * static_cast<std::size_t>(r[0] + j)];
+      std::int32_t* o = &F.slot[4 * static_cast<std::size_t>(r[0] + j)];
+      o[0] = static_cast<std::int32_t>(F.upd.size() / 2);
+      for (std::int32_t e = sl[0]; e < sl[1]; ++e)
+        for (int h = 0; h < 2; ++h) {
+          std::int32_t x = P.flow_upd[2 * static_cast<std::size_t>(e) + h];
+          const std::int32_t ow = owner_of_pos(x);
+          if (ow != part) {
+            x = static_cast<std::int32_t>(kRemoteBit | (static_cast<std::uint32_t>(ow) << kRemoteShift) |
+                                          static_cast<std::uint32_t>(x));
+            ++F.remote_operands;
+          }
+          F.upd.push_back(x);
+        }
+      o[1] = static_cast<std::int32_t>(F.upd.size() / 2);
+      if (o[0] < o[1]) {
+        o[2] = F.upd[2 * static_cast<std::size_t>(o[0])];
+        o[3] = F.upd[2 * static_cast<std::size_t>(o[0]) + 1];
+      }
+    }
+    // the Trsm divisor U(t,t) belongs to row t: same part
+  }
+  F.rows = static_cast<std::int64_t>(F.item.size());
+  return F;
+}
+
 }  // namespace tcb

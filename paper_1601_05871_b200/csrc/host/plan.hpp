@@ -162,4 +162,24 @@ Plan build_plan(const CsrMatrix& pattern, const std::vector<double>& init_values
                 const RangeList& ranges, bool with_work = true,
                 const PlanOptions& opt = PlanOptions());
 
+// One part of a sharded value-flow factorization (C6: ND subtrees on
+// different GPUs). The part runs the rows t with part_of_row[t] == part, in
+// the global schedule order; an operand owned by another part is encoded as
+// kRemoteBit | (owner << kRemoteShift) | position and read from the owner's
+// copy of U (peer memory). Programs are compacted to the part's coordinates.
+// A row some other part reads carries bit 31 in its length word and
+// publishes its values at system scope.
+constexpr std::uint32_t kRemoteBit = 0x80000000u;
+constexpr int kRemoteShift = 25;  // positions below 2^25, owners below 64
+struct FlowPart {
+  std::vector<std::int32_t> rec, item;   // kFlowWords per row, schedule order
+  std::vector<std::int32_t> slot;        // 4 per coordinate of U (zero outside the part)
+  std::vector<std::int32_t> upd;         // the part's products
+  std::int64_t remote_operands = 0;      // products reading another part
+  std::int64_t exported_rows = 0;        // rows another part reads (rec word 1, bit 31)
+  std::int64_t rows = 0;
+};
+FlowPart build_flow_part(const Plan& P, const std::vector<std::int32_t>& part_of_row, std::int32_t nparts,
+                         std::int32_t part);
+
 }  // namespace tcb

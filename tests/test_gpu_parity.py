@@ -7,6 +7,7 @@ factor_serial, which is asserted -- and the pattern-restricted residual
 ||A - UᵀU||_P / max|A| equal to the reference's.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -416,3 +417,89 @@ def test_factor_host_batch(T, oracle):
             assert bitwise_equal(out[i], ref), i
     finally:
         fz.close()
+
+
+@pytest.mark.parametrize("name,nparts", [("c5_m0", 2), ("c5_m0", 4), ("c2", 8)])
+def test_sharded_parts_through_peer_pointers(T, golden, oracle, name, nparts):
+    # C6's sharded path on one GPU, made sequential: parts 0..n-1 own the ND
+    # subtrees (independent of each other), part n the separators above them,
+    # which read the subtree parts' U through the peer-pointer table exactly as
+    # they would across GPUs. Each launch only reads parts that have finished,
+    # so no kernel waits on another.
+    _, an = analyzed(name)
+    plan = planned(name)
+    owners = an.subtree_owners(nparts, separators=nparts)
+    total = nparts + 1
+    fzs = [T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30), problem=plan.part_problem(total, owners, k))
+           for k in range(total)]
+    try:
+        ptrs = [f.values_device_ptr() for f in fzs]
+        for f in fzs:
+            f.set_peers(ptrs)
+        for f in fzs:
+            st = f.factor()
+            assert st.mode == 5
+        t = plan.tables()
+        full = np.full(len(t["values"]), np.nan)
+        own_pos = np.repeat(owners, np.diff(an.pattern.pattern.row_ptr))  # owner of every U entry
+        for k, f in enumerate(fzs):
+            v = f.download()
+            full[own_pos == k] = v[own_pos == k]
+        check_against_oracle(name, full, golden, oracle)
+    finally:
+        for f in fzs:
+            f.close()
+
+
+def _ipc_owner(q_out, q_in, name, nparts):
+    """Process A: owns the subtree parts, factors them, exports its U by IPC."""
+    import sys as _s
+    _s.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    import paper_1601_05871_b200 as T
+    from conftest import analyzed, planned
+    _, an = analyzed(name)
+    plan = planned(name)
+    owners = an.subtree_owners(nparts, separators=nparts)
+    fz = T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30),
+                         problem=plan.part_problem(nparts + 1, owners, 0))
+    fz.set_peers([fz.values_device_ptr()] * (nparts + 1))
+    fz.factor()
+    q_out.put((fz.ipc_handle(), fz.download()))
+    q_in.get()  # keep the allocation alive until the reader is done
+    fz.close()
+
+
+def test_ipc_peer_values_across_processes(T, golden, oracle):
+    # the multi-process path of bench.py run_sharded on one GPU, made
+    # sequential: a second process owns part 0 (one ND subtree) and exports
+    # its U by CUDA IPC; this process runs the other parts, whose separator
+    # rows read part 0's values through the IPC mapping
+    import multiprocessing as mp
+    name, nparts = "c5_m0", 2
+    ctx = mp.get_context("spawn")
+    q_out, q_in = ctx.Queue(), ctx.Queue()
+    p = ctx.Process(target=_ipc_owner, args=(q_out, q_in, name, nparts))
+    p.start()
+    try:
+        (handle, offset), part0 = q_out.get(timeout=300)
+        _, an = analyzed(name)
+        plan = planned(name)
+        owners = an.subtree_owners(nparts, separators=nparts)
+        fzs = [T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30), problem=plan.part_problem(nparts + 1, owners, k))
+               for k in range(1, nparts + 1)]
+        remote0 = fzs[0].ipc_open(handle, offset)
+        ptrs = [remote0] + [f.values_device_ptr() for f in fzs]
+        for f in fzs:
+            f.set_peers(ptrs)
+            f.factor()
+        own_pos = np.repeat(owners, np.diff(an.pattern.pattern.row_ptr))
+        full = np.where(own_pos == 0, part0, np.nan)
+        for k, f in enumerate(fzs, start=1):
+            v = f.download()
+            full[own_pos == k] = v[own_pos == k]
+        check_against_oracle(name, full, golden, oracle)
+        for f in fzs:
+            f.close()
+    finally:
+        q_in.put(1)
+        p.join(timeout=120)

@@ -77,3 +77,49 @@ def test_shard_sizes():
         assert [x for p in parts for x in p] == list(range(n))
     with pytest.raises(ValueError):
         batch.shard(4, 2, 2)
+
+
+def shard_worker(rank, world, port, out_dir):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, HERE)
+    import torch.distributed as dist
+
+    from conftest import analyzed, planned
+    from test_plan import part_tables
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    # what bench.py run_sharded does per rank before the GPU work
+    _, an = analyzed("c5_m0")
+    plan = planned("c5_m0")
+    owners = an.subtree_owners(world, separators=0)
+    mine = part_tables(plan.part_problem(world, owners, rank))
+    parts = [None] * world
+    dist.all_gather_object(parts, mine)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "owners.npy"), owners)
+        import pickle
+        with open(os.path.join(out_dir, "parts.pkl"), "wb") as f:
+            pickle.dump(parts, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_subtree_sharding(tmp_path, oracle):
+    # C6 sharding host side over two gloo ranks: each rank builds its part
+    # (rows of its ND subtree, remote operands encoded); rank 0 collects them
+    # and the CPU replay of all parts equals factor_serial bit for bit
+    import pickle
+
+    import torch.multiprocessing as mp
+    sys.path.insert(0, HERE)
+    from conftest import analyzed, bitwise_equal, planned
+    from test_plan import replay_parts
+    mp.spawn(shard_worker, args=(2, free_port(), str(tmp_path)), nprocs=2, join=True)
+    owners = np.load(tmp_path / "owners.npy")
+    parts = pickle.load(open(tmp_path / "parts.pkl", "rb"))
+    assert [int((owners == k).sum()) > 0 for k in range(2)] == [True, True]
+    full, remote, read_remotely, exported = replay_parts(planned("c5_m0").tables(), parts, owners)
+    _, an = analyzed("c5_m0")
+    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
+    assert bitwise_equal(full, ref) and remote > 0 and read_remotely <= exported

@@ -298,3 +298,87 @@ def test_unit_schedule_replays_bitwise(T, name, min_rows, oracle, monkeypatch):
     assert t["m6_smem"] <= 72 * 1024
     ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
     assert bitwise_equal(replay_units(t), ref)
+
+
+def part_tables(p):
+    from paper_1601_05871_b200.core import _copy
+    n = int(p.nflow)
+    return {"rec": _copy(p.flow_rec, 4 * n, np.int32).reshape(-1, 4), "item": _copy(p.flow_item, n, np.int32),
+            "slot": _copy(p.flow_slot, 4 * p.nnz, np.int32).reshape(-1, 4),
+            "upd": _copy(p.flow_upd, 2 * p.nflow_upd, np.int32).reshape(-1, 2)}
+
+
+def replay_parts(t, parts, owners):
+    """Sharded value flow on the CPU: every part's rows in the global order,
+    each part with its own copy of U, remote operands read from their owner's
+    copy. Returns (assembled factor, remote operand count, rows read remotely,
+    rows flagged exported)."""
+    total = len(parts)
+    pos_of_item = {int(it): q for q, it in enumerate(t["flow_item"])}
+    order = sorted((pos_of_item[int(it)], k, i) for k, p in enumerate(parts) for i, it in enumerate(p["item"]))
+    a = t["values"]
+    out = [np.full(len(a), np.nan) for _ in range(total)]
+    done = [np.zeros(len(a), bool) for _ in range(total)]
+    remote = 0
+    exported, read_remotely = set(), set()
+    row_start = {}  # U position -> (part, first position of its row slice)
+    for k, p in enumerate(parts):
+        for tb, lk, _, _ in p["rec"]:
+            for x in range(tb, tb + (lk & ((1 << 30) - 1))):
+                row_start[x] = (k, int(tb))
+    for _, k, i in order:
+        tb, lk, dpos, trow = parts[k]["rec"][i]
+        assert owners[trow] == k
+        L, kind = lk & ((1 << 30) - 1), (lk >> 30) & 1
+        if lk < 0:
+            exported.add((k, int(tb)))
+        v = a[tb:tb + L].copy()
+        for j in range(L):
+            ub, ue = parts[k]["slot"][tb + j, :2]
+            for m, o in parts[k]["upd"][ub:ue]:
+                vals = []
+                for x in (int(m) & 0xFFFFFFFF, int(o) & 0xFFFFFFFF):
+                    if x & 0x80000000:
+                        ow, pos = (x >> 25) & 63, x & 0x1FFFFFF
+                        assert ow != k
+                        remote += 1
+                        read_remotely.add(row_start[pos])
+                    else:
+                        ow, pos = k, x
+                    assert done[ow][pos], "read before written"
+                    vals.append(out[ow][pos])
+                v[j] = v[j] - vals[0] * vals[1]
+        if kind == 0:
+            d = np.sqrt(v[0])
+            v[1:] = v[1:] / d
+            v[0] = d
+        else:
+            assert done[k][dpos]
+            v = v / out[k][dpos]
+        out[k][tb:tb + L] = v
+        done[k][tb:tb + L] = True
+    full = np.full(len(a), np.nan)
+    for k in range(total):
+        full[done[k]] = out[k][done[k]]
+    assert all(not (done[i] & done[j]).any() for i in range(total) for j in range(i + 1, total))
+    return full, remote, read_remotely, exported
+
+
+@pytest.mark.parametrize("name,nparts,extra", [("c5_m0", 2, False), ("c5_m0", 4, True),
+                                               ("s27_16_k2", 2, True), ("c1", 8, False)])
+def test_sharded_parts_replay_bitwise(T, name, nparts, extra, oracle):
+    # C6-style sharding: each part owns the rows of its ND subtree (separators
+    # to part 0, or to an extra last part); every part has its own copy of U
+    # and reads other parts' values through remote (peer) operands
+    _, an = analyzed(name)
+    plan = planned(name)
+    owners = an.subtree_owners(nparts, separators=nparts if extra else 0)
+    total = nparts + (1 if extra else 0)
+    parts = [part_tables(plan.part_problem(total, owners, k)) for k in range(total)]
+    t = plan.tables()
+    assert sum(len(p["item"]) for p in parts) == len(t["flow_item"])
+    full, remote, read_remotely, exported = replay_parts(t, parts, owners)
+    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
+    assert bitwise_equal(full, ref)
+    assert remote > 0
+    assert read_remotely <= exported  # every row another part reads publishes at system scope
