@@ -122,6 +122,10 @@ typedef struct {
   const int32_t* m6_slot;      /*   flow_slot with intra-unit operands as 0x80000000|index */
   const int32_t* m6_upd;       /*   nflow_upd pairs, same rewrite */
   int64_t m6_smem;             /*   bytes of the largest unit */
+  /* device init_factor_values (optional): per U slot, the position in a_permuted's values it
+   * starts from (-1 = fill, starts at 0.0); absent when A has duplicate entries */
+  int64_t nnz_a;
+  const int32_t* a_map;
 } tcg_problem;
 
 typedef struct {
@@ -237,6 +241,10 @@ tcg_status tcg_device_values(tcg_ctx* ctx, double** dptr, int64_t* nnz);
  * one launch; a breakdown skips the rest of that member only (TCG_BREAKDOWN reports the
  * first; tcg_batch_breakdown gives each member's row, -1 = none, and pivot). */
 tcg_status tcg_set_batch(tcg_ctx* ctx, int32_t nbatch, const double* values);
+/* init_factor_values on the device (reference factorize.hpp:71-89): `a_values` holds nbatch x
+ * nnz(a_permuted) values of PᵀAP in a_permuted's CSR order (host); they are uploaded and
+ * scattered into U (fill = 0.0, bitwise as the host init). Sets the batch size to nbatch. */
+tcg_status tcg_set_a_values(tcg_ctx* ctx, int32_t nbatch, const double* a_values);
 tcg_status tcg_set_batch_values(tcg_ctx* ctx, const double* values); /* same nbatch */
 int32_t tcg_batch_size(const tcg_ctx* ctx);
 tcg_status tcg_download_batch(tcg_ctx* ctx, double* values);

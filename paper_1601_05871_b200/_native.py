@@ -88,6 +88,8 @@ class Problem(C.Structure):
         ("m6_slot", i32p),
         ("m6_upd", i32p),
         ("m6_smem", C.c_int64),
+        ("nnz_a", C.c_int64),
+        ("a_map", i32p),
     ]
 
 
@@ -177,6 +179,7 @@ SIGNATURES = [
     ("tcg_download_trace", C.c_int, [C.c_void_p, u64p]),
     ("tcg_set_batch", C.c_int, [C.c_void_p, C.c_int32, f64p]),
     ("tcg_set_batch_values", C.c_int, [C.c_void_p, f64p]),
+    ("tcg_set_a_values", C.c_int, [C.c_void_p, C.c_int32, f64p]),
     ("tcg_batch_size", C.c_int32, [C.c_void_p]),
     ("tcg_download_batch", C.c_int, [C.c_void_p, f64p]),
     ("tcg_batch_breakdown", C.c_int, [C.c_void_p, i32p, f64p]),

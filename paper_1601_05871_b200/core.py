@@ -417,6 +417,7 @@ class Plan:
             "m6_upd": (_copy(p.m6_upd, 2 * p.nflow_upd, np.int32).reshape(-1, 2) if p.m6_upd
                        else np.zeros((0, 2), np.int32)),
             "m6_smem": int(p.m6_smem),
+            "a_map": _copy(p.a_map, p.nnz, np.int32) if p.a_map else np.zeros(0, np.int32),
             "flow_slot": (_copy(p.flow_slot, 4 * p.nnz, np.int32).reshape(-1, 4)
                           if p.flow_slot else np.zeros((0, 4), np.int32)),
             "flow_upd": (_copy(p.flow_upd, 2 * p.nflow_upd, np.int32).reshape(-1, 2)
@@ -537,6 +538,13 @@ class GpuFactorizer:
         if v.ndim != 2 or v.shape[1] != self.nnz:
             raise ValueError(f"batch values must be [nbatch, {self.nnz}]")
         self._check(self._lib.tcg_set_batch(self.ctx, v.shape[0], v.ctypes.data_as(N.f64p)))
+
+    def set_a_values(self, a_values: np.ndarray):
+        """init_factor_values on the device: PᵀAP's values (a_permuted CSR order),
+        one row per member ([nbatch, nnz_A] or [nnz_A])."""
+        v = np.ascontiguousarray(a_values, dtype=np.float64)
+        nb = 1 if v.ndim == 1 else v.shape[0]
+        self._check(self._lib.tcg_set_a_values(self.ctx, nb, v.ctypes.data_as(N.f64p)))
 
     def set_batch_values_ptr(self, host_ptr: int):
         self._check(self._lib.tcg_set_batch_values(self.ctx, C.cast(C.c_void_p(host_ptr), N.f64p)))

@@ -58,6 +58,8 @@ struct tcg_plan {
   tcb::Plan plan;
   std::vector<std::int32_t> brow_ptr32;  // unused, kept for ABI symmetry
   std::map<std::int32_t, tcb::FlowPart> parts;  // tcg_plan_part_problem results
+  std::vector<std::int32_t> a_map;  // device init_factor_values: U slot -> A position (-1 fill)
+  std::int64_t nnz_a = 0;
 };
 
 struct tcg_ctx {
@@ -116,6 +118,9 @@ struct tcg_ctx {
   int2* m6_upd = nullptr;
   std::int64_t m6_nrows = 0, m6_nunits = 0, m6_smem = 0;
   bool has_units = false;
+  int* a_map = nullptr;      // device init_factor_values (in the arena)
+  double* a_stage = nullptr; // staging for A's values (separate allocation, grown on demand)
+  std::int64_t nnz_a = 0, a_stage_len = 0;
   double** peers = nullptr;  // sharded runs: device table of every part's U (own included)
   int npeers = 0;
   std::vector<void*> ipc_opened;  // peer arenas mapped by tcg_ipc_open
@@ -182,6 +187,12 @@ tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pa
     if (const char* e = std::getenv("TCG_UNIT_MIN_ROWS")) po.unit_min_rows = std::atoi(e);
     if (const char* e = std::getenv("TCG_UNIT_SMEM")) po.unit_smem_cap = std::atoll(e);
     p->plan = tcb::build_plan(u, init, rl, true, po);
+    try {
+      p->a_map = tcb::init_factor_map(a, u);
+      p->nnz_a = a.nnz();
+    } catch (const std::invalid_argument&) {
+      p->a_map.clear();  // duplicates in A: no device init (host init_factor_values only)
+    }
     *out = p.release();
     return TCG_OK;
   } catch (const std::bad_alloc&) {
@@ -215,6 +226,8 @@ tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   o->indeg = P.indeg.data();
   o->nroots = static_cast<int64_t>(P.roots.size());
   o->roots = P.roots.data();
+  o->nnz_a = plan->a_map.empty() ? 0 : plan->nnz_a;
+  o->a_map = plan->a_map.empty() ? nullptr : plan->a_map.data();
   o->max_target_len = P.stats.max_target_len;
   o->max_flag_rows = P.stats.max_flag_rows;
   o->nhelpers = P.stats.helpers;
@@ -385,6 +398,7 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
 
 void tcg_destroy(tcg_ctx* c) {
   if (c && c->batch_arena) cudaFree(c->batch_arena);
+  if (c && c->a_stage) cudaFree(c->a_stage);
   if (c && c->peers) cudaFree(c->peers);
   if (c)
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -497,6 +511,8 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_m6lv = take(units ? sizeof(int) * p->m6_nlev : 0);
   const size_t o_m6sl = take(units ? sizeof(int4) * p->nnz : 0);
   const size_t o_m6up = take(units ? sizeof(int2) * p->nflow_upd : 0);
+  const bool amap = p->nnz_a > 0 && p->a_map;
+  const size_t o_amap = take(amap ? sizeof(int) * p->nnz : 0);
   const size_t o_mflags = take(sizeof(int) * 2);
   const size_t o_mpivot = take(sizeof(double));
   const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
@@ -549,6 +565,8 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->m6_nunits = units ? p->m6_nunits : 0;
   c->m6_smem = units ? p->m6_smem : 0;
   c->has_units = units;
+  c->a_map = amap ? reinterpret_cast<int*>(base + o_amap) : nullptr;
+  c->nnz_a = amap ? p->nnz_a : 0;
   c->m_flags = reinterpret_cast<int*>(base + o_mflags);
   c->m_pivot = reinterpret_cast<double*>(base + o_mpivot);
   c->flow_slot = reinterpret_cast<int4*>(base + o_fslot);
@@ -609,6 +627,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     TCG_CUDA_TRY(c, put(c->m6_slot, p->m6_slot, sizeof(int4) * p->nnz));
     TCG_CUDA_TRY(c, put(c->m6_upd, p->m6_upd, sizeof(int2) * p->nflow_upd));
   }
+  if (amap) TCG_CUDA_TRY(c, put(c->a_map, p->a_map, sizeof(int) * p->nnz));
   if (p->nitems > 0)
     TCG_CUDA_TRY(c, cudaMemsetAsync(c->iflag, 0, sizeof(int) * p->nitems, c->stream));
   if (p->nnz > 0)
@@ -1252,6 +1271,56 @@ tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals0, values, vb, cudaMemcpyHostToDevice, c->stream));
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals, c->bvals0, vb, cudaMemcpyDeviceToDevice, c->stream));
   }
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_set_a_values(tcg_ctx* c, int32_t nbatch, const double* a_values) {
+  if (!c || !c->uploaded || nbatch < 1 || (!a_values && c->nnz_a > 0)) return TCG_INVALID;
+  if (!c->a_map) {
+    c->err = "tcg_set_a_values: the problem has no A -> U map (duplicate entries in A?)";
+    return TCG_INVALID;
+  }
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  if (nbatch != c->nbatch) {  // resize the batch (values are overwritten below)
+    if (nbatch > 1) {
+      std::vector<double> zeros;  // tcg_set_batch needs host values; use a cheap device path instead
+      TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      if (c->batch_arena) {
+        TCG_CUDA_TRY(c, cudaFree(c->batch_arena));
+        c->batch_arena = nullptr;
+      }
+      const size_t vb = sizeof(double) * static_cast<size_t>(c->nnz) * nbatch;
+      const size_t fb = align_up(sizeof(int) * 2 * nbatch, 256);
+      TCG_CUDA_TRY(c, cudaMalloc(&c->batch_arena, 3 * align_up(vb, 256) + fb + sizeof(double) * nbatch));
+      char* base = static_cast<char*>(c->batch_arena);
+      c->bvals = reinterpret_cast<double*>(base);
+      c->bvals0 = reinterpret_cast<double*>(base + align_up(vb, 256));
+      c->ba = reinterpret_cast<double*>(base + 2 * align_up(vb, 256));
+      c->bm_flags = reinterpret_cast<int*>(base + 3 * align_up(vb, 256));
+      c->bm_pivot = reinterpret_cast<double*>(base + 3 * align_up(vb, 256) + fb);
+    } else if (c->batch_arena) {
+      TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      TCG_CUDA_TRY(c, cudaFree(c->batch_arena));
+      c->batch_arena = nullptr;
+    }
+    c->nbatch = nbatch;
+  }
+  const int64_t need = c->nnz_a * nbatch;
+  if (need > c->a_stage_len) {
+    TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->a_stage) TCG_CUDA_TRY(c, cudaFree(c->a_stage));
+    c->a_stage = nullptr;
+    TCG_CUDA_TRY(c, cudaMalloc(&c->a_stage, sizeof(double) * std::max<int64_t>(need, 1)));
+    c->a_stage_len = need;
+  }
+  if (need > 0)
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(c->a_stage, a_values, sizeof(double) * need, cudaMemcpyHostToDevice,
+                                    c->stream));
+  double* v = nbatch > 1 ? c->bvals : c->vals;
+  double* v0 = nbatch > 1 ? c->bvals0 : c->vals0;
+  TCG_CUDA_TRY(c, tcbdev::launch_init_values(c->a_stage, c->a_map, v, v0, c->nnz, c->nnz_a, nbatch,
+                                             c->sm_count, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return TCG_OK;
 }

@@ -542,6 +542,31 @@ cudaError_t launch_units(const FlowParams& p, const UnitParams& u, int grid, int
   return cudaErrorInvalidValue;
 }
 
+// init_factor_values on the device: U slot t <- 0.0 + A[map[t]] (the host
+// version's `vals[t] += a` from zero, so -0.0 becomes +0.0 exactly as there),
+// 0.0 for fill; for every member of a batch; also into the restore copy.
+__global__ void init_values(const double* a, const int* map, double* vals, double* vals0, long long nnz,
+                            long long nnz_a, int nbatch) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const long long total = nnz * nbatch;
+  for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < total; x += stride) {
+    const long long b = x / nnz, t = x - b * nnz;
+    const int m = __ldg(map + t);
+    const double v = m >= 0 ? __dadd_rn(0.0, __ldg(a + b * nnz_a + m)) : 0.0;
+    vals[x] = v;
+    vals0[x] = v;
+  }
+}
+
+cudaError_t launch_init_values(const double* a, const int* map, double* vals, double* vals0, long long nnz,
+                               long long nnz_a, int nbatch, int sm_count, cudaStream_t st) {
+  const long long total = nnz * nbatch;
+  long long blocks = (total + 255) / 256;
+  blocks = blocks < 1 ? 1 : (blocks > 8LL * sm_count ? 8LL * sm_count : blocks);
+  init_values<<<static_cast<int>(blocks), 256, 0, st>>>(a, map, vals, vals0, nnz, nnz_a, nbatch);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStream_t st) {
   const long long h = q.nnz / 2;
   long long blocks = (h + 255) / 256;

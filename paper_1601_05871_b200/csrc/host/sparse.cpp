@@ -139,4 +139,26 @@ std::vector<double> init_factor_values(const CsrMatrix& a, const CsrMatrix& u) {
   return vals;
 }
 
+std::vector<std::int32_t> init_factor_map(const CsrMatrix& a, const CsrMatrix& u) {
+  // The same merge as init_factor_values, recording the source instead of
+  // adding it: map[t] = position in a.values of the entry U slot t starts
+  // from, -1 for fill. A slot fed by two entries (duplicates) has no map.
+  std::vector<std::int32_t> map(static_cast<std::size_t>(u.nnz()), -1);
+  if (a.nnz() > 0x7fffffffLL) throw std::length_error("init map: A beyond 2^31 entries");
+  for (index_t i = 0; i < a.nrows; ++i) {
+    offset_t t = u.row_begin(i);
+    const offset_t te = u.row_end(i);
+    for (offset_t q = a.row_begin(i); q < a.row_end(i); ++q) {
+      const index_t c = a.col_idx[q];
+      if (c < i) continue;
+      while (t < te && u.col_idx[t] < c) ++t;
+      if (t < te && u.col_idx[t] == c) {
+        if (map[t] >= 0) throw std::invalid_argument("init map: duplicate entry in A");
+        map[t] = static_cast<std::int32_t>(q);
+      }
+    }
+  }
+  return map;
+}
+
 }  // namespace tcb

@@ -105,6 +105,9 @@ offset_t count_upper(const CsrMatrix& a);
 // (reference factorize.hpp:71-89).
 std::vector<double> init_factor_values(const CsrMatrix& a_permuted,
                                        const CsrMatrix& pattern);
+// Per U slot, the position in a_permuted.values init_factor_values draws it
+// from (-1: fill); throws std::invalid_argument when a slot has two sources.
+std::vector<std::int32_t> init_factor_map(const CsrMatrix& a_permuted, const CsrMatrix& pattern);
 
 // --- analysis (analysis.cpp) -----------------------------------------------
 std::pair<Permutation, NdTree> nested_dissection(const CsrMatrix& a,

@@ -503,3 +503,36 @@ def test_ipc_peer_values_across_processes(T, golden, oracle):
     finally:
         q_in.put(1)
         p.join(timeout=120)
+
+
+@pytest.mark.parametrize("name", ["c1", "c5_m0", "c2", "elast6_k1"])
+def test_device_init_factor_values(T, golden, oracle, name):
+    # init_factor_values on the device from PᵀAP's values equals the host one
+    # bit for bit, and the factor from it equals the golden factor
+    _, an = analyzed(name)
+    plan = planned(name)
+    fz = T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30))
+    try:
+        fz.set_a_values(an.a_permuted.values)
+        fz.restore()
+        init = fz.download()
+        assert bitwise_equal(init, plan.tables()["values"])
+        fz.factor()
+        check_against_oracle(name, fz.download(), golden, oracle)
+    finally:
+        fz.close()
+
+
+def test_device_init_batch(T, oracle):
+    an, vals, perms = c5_members(T, [0, 5])
+    fz = T.GpuFactorizer(planned("c5_m0"), T.GpuOptions(timeout_s=30))
+    try:
+        fz.set_a_values(np.stack([ap.values for ap in perms]))
+        assert fz.batch == 2
+        fz.factor()
+        out = fz.download_batch()
+        for i, ap in enumerate(perms):
+            ref, _, _, _ = oracle.factor_serial(ap, an.pattern.pattern)
+            assert bitwise_equal(out[i], ref), i
+    finally:
+        fz.close()

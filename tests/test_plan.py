@@ -382,3 +382,15 @@ def test_sharded_parts_replay_bitwise(T, name, nparts, extra, oracle):
     assert bitwise_equal(full, ref)
     assert remote > 0
     assert read_remotely <= exported  # every row another part reads publishes at system scope
+
+
+@pytest.mark.parametrize("name", ["c1", "c5_m0", "s27_16_k2", "elast6_k1", "rand_spd_200"])
+def test_init_factor_map_reproduces_host_init(name):
+    # device init_factor_values (tcg_set_a_values) is a gather through this map
+    _, an = analyzed(name)
+    t = planned(name).tables()
+    m = t["a_map"]
+    assert len(m) == len(t["values"])
+    got = np.where(m >= 0, 0.0 + an.a_permuted.values[np.maximum(m, 0)], 0.0)
+    assert bitwise_equal(got, t["values"])
+    assert len(np.unique(m[m >= 0])) == int((m >= 0).sum())  # every A entry feeds one slot at most
