@@ -108,6 +108,26 @@ struct Ctx {
     }
     return __longlong_as_double(static_cast<long long>(x));
   }
+  // both operands of one product: U(r,t) and U(r,c) come from the same
+  // source row r, so when r has just been written both still read kUnset;
+  // re-polling them together costs one round trip instead of two
+  __device__ __forceinline__ double product(int pa, unsigned long long xa, int pb, unsigned long long xb) const {
+    if (OPS != 2 && (xa == kUnset || xb == kUnset)) {
+      unsigned spins = 0;
+      do {
+        if (xa == kUnset) xa = ld(pa);
+        if (xb == kUnset) xb = ld(pb);
+        if (++spins == 1024u) {
+          spins = 0;
+          if (ld_relaxed(&P.ctrl->error.v) || gtimer() - t0 > P.timeout_ns) {
+            atomicCAS(&P.ctrl->error.v, 0, 1);  // abandoned: the host reports TCG_TIMEOUT
+            xa = xb = 0ull;
+          }
+        }
+      } while (xa == kUnset || xb == kUnset);
+    }
+    return __dmul_rn(settle_at(pa, xa), settle_at(pb, xb));
+  }
   static constexpr bool kSysPublish = OPS == 2;  // readers on other GPUs
 };
 
@@ -138,7 +158,7 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
   int2 p[KB];
 #pragma unroll
   for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
-  v = __dsub_rn(v, __dmul_rn(C.settle_at(sr.z, xa0), C.settle_at(sr.w, xb0)));
+  v = __dsub_rn(v, C.product(sr.z, xa0, sr.w, xb0));
   while (u < ue) {
     const int n = min(KB, ue - u);
     unsigned long long xa[KB], xb[KB];
@@ -155,7 +175,7 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 #pragma unroll
     for (int j = 0; j < KB; ++j)
       if (j < n)
-        v = __dsub_rn(v, __dmul_rn(C.settle_at(c[j].x, xa[j]), C.settle_at(c[j].y, xb[j])));
+        v = __dsub_rn(v, C.product(c[j].x, xa[j], c[j].y, xb[j]));
   }
   return v;
 }
