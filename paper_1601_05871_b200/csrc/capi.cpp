@@ -137,7 +137,7 @@ struct tcg_ctx {
   int4* flow_slot = nullptr;
   int2* flow_upd = nullptr;
   double* flow_a = nullptr;  // snapshot of the input values
-  std::int64_t nflow = 0;
+  std::int64_t nflow = 0, nflow_upd = 0;
   bool has_flow = false;
   std::int64_t nslots = 0, nupdates = 0;
   tcbdev::Ctrl* ctrl = nullptr;
@@ -573,6 +573,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->flow_upd = reinterpret_cast<int2*>(base + o_fupd);
   c->flow_a = reinterpret_cast<double*>(base + o_fa);
   c->nflow = flow ? p->nflow : 0;
+  c->nflow_upd = flow ? p->nflow_upd : 0;
   c->has_flow = flow;
 
   c->nslots = programs ? p->nslots : 0;
@@ -682,7 +683,10 @@ tcg_status tcg_restore(tcg_ctx* c) {
 // polls operands), and the factor is copied back on the launch stream.
 static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* host_in = nullptr,
                            double* host_out = nullptr, int phase = 0) {
-  int kb = 4, minb = threads == 128 ? 6 : threads == 384 ? 2 : threads == 256 ? 3 : 1;
+  // gather batch from the mean products per coordinate (flow_kernel.cu variants)
+  const double mean = c->nnz > 0 ? static_cast<double>(c->nflow_upd) / static_cast<double>(c->nnz) : 0.0;
+  int kb = mean <= 4.0 ? 2 : mean <= 16.0 ? 3 : 4;
+  int minb = threads == 128 ? 6 : threads == 384 ? 2 : threads == 256 ? 3 : 1;
   if (const char* e = std::getenv("TCG_FLOW_KB")) kb = std::atoi(e);
   if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
   // lanes per row: a whole warp unless asked otherwise (flow_kernel.cu)
@@ -692,8 +696,14 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (const char* e = std::getenv("TCG_FLOW_DYN")) dyn = std::atoi(e);
   int remote = c->npeers > 1 ? 1 : 0;  // sharded: operands of other parts via peers
   if (const char* e = std::getenv("TCG_FLOW_REMOTE")) remote = std::atoi(e) ? 1 : remote;
+  if (weak || dyn || g != 32) kb = 4;  // those variants exist with KB = 4 only
   int occ = 0;
-  TCG_CUDA_TRY(c, tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ));
+  cudaError_t oe = tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
+  if (oe == cudaErrorInvalidValue && kb != 4) {  // no such variant: the KB = 4 one
+    kb = 4;
+    oe = tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
+  }
+  TCG_CUDA_TRY(c, oe);
   if (occ < 1) {
     c->err = "value-flow kernel does not fit on an SM";
     return TCG_INVALID;

@@ -100,6 +100,12 @@ struct Ctx {
     if (WEAK) return ld_weak_u64(vals + pos);
     return ld_relaxed_u64(vals + pos);
   }
+  // re-polls are always strong: a weak (L1) copy of the marker may be stale
+  __device__ __forceinline__ unsigned long long ld_strong(int pos) const {
+    if (OPS == 1 && pos < 0) return static_cast<unsigned long long>(__double_as_longlong(sv[pos & 0x7fffffff]));
+    if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
+    return ld_relaxed_u64(vals + pos);
+  }
   // settle an operand by its (encoded) position
   __device__ __forceinline__ double settle_at(int pos, unsigned long long x) const {
     if (x == kUnset) {
@@ -115,8 +121,8 @@ struct Ctx {
     if (OPS != 2 && (xa == kUnset || xb == kUnset)) {
       unsigned spins = 0;
       do {
-        if (xa == kUnset) xa = ld(pa);
-        if (xb == kUnset) xb = ld(pb);
+        if (xa == kUnset) xa = ld_strong(pa);
+        if (xb == kUnset) xb = ld_strong(pb);
         if (++spins == 1024u) {
           spins = 0;
           if (ld_relaxed(&P.ctrl->error.v) || gtimer() - t0 > P.timeout_ns) {
@@ -512,9 +518,17 @@ __global__ void flow_prepare(FlowPrepParams Q) {
 // targets; G: lanes per row. Measured on B200 (C1-C5): whole warps per row
 // win everywhere -- the groups of a warp diverge on their polls and product
 // counts, and their rows serialise; G = 8 is kept for experiments.
+// Measured on B200 (one session, mode 5): gather batch KB 2 beats 4 where
+// programs are short (C2 0.69 -> 0.65 ms, C5 0.23 -> 0.20 ms) and 3 where
+// they are long (C4 2.26 -> 2.01 ms); the host picks KB from the mean
+// products per coordinate.
 #define TCG_FLOW_VARIANTS(X)                                                                   \
-  X(256, 4, 3, 32, 0, 0, 0) X(256, 4, 3, 32, 1, 0, 0) X(128, 4, 6, 32, 0, 0, 0) X(512, 4, 1, 32, 0, 0, 0) \
-  X(256, 4, 3, 32, 0, 1, 0) X(256, 4, 3, 32, 0, 0, 1) X(128, 4, 6, 32, 0, 0, 1) X(512, 4, 1, 32, 0, 0, 1)
+  X(256, 1, 3, 32, 0, 0, 0) X(256, 2, 3, 32, 0, 0, 0) X(256, 3, 3, 32, 0, 0, 0) X(256, 4, 3, 32, 0, 0, 0) \
+  X(256, 1, 4, 32, 0, 0, 0) X(256, 2, 4, 32, 0, 0, 0) X(256, 4, 3, 32, 1, 0, 0) X(256, 4, 3, 32, 0, 1, 0) \
+  X(128, 2, 6, 32, 0, 0, 0) X(128, 3, 6, 32, 0, 0, 0) X(128, 4, 6, 32, 0, 0, 0)                         \
+  X(512, 2, 1, 32, 0, 0, 0) X(512, 3, 1, 32, 0, 0, 0) X(512, 4, 1, 32, 0, 0, 0)                         \
+  X(256, 2, 3, 32, 0, 0, 1) X(256, 3, 3, 32, 0, 0, 1) X(256, 4, 3, 32, 0, 0, 1)                         \
+  X(128, 4, 6, 32, 0, 0, 1) X(512, 4, 1, 32, 0, 0, 1) X(256, 4, 3, 8, 0, 0, 0)
 
 static const void* flow_kernel_for(int threads, int kb, int minb, int g, int weak, int dyn, int remote) {
 #define X(T, K, M, GG, WK, D, R)                                                                     \

@@ -1,6 +1,4 @@
-set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "sharded or row_modes" 2>&1 | tail -2
 for r in 1 2; do
-timeout 600 python tests/gpu_probe.py c5 c2 c4 reps=5 mode=5 2>&1 | grep -oE '^c[0-9]|med_ms=[0-9.]+' | paste - -
-TCG_FLOW_REMOTE=1 timeout 600 python tests/gpu_probe.py c5 c2 c4 reps=5 mode=5 2>&1 | grep -oE '^c[0-9]|med_ms=[0-9.]+' | paste - -
-done
+for cfg in "3 2" "3 1" "4 1" "4 2" "5 2" "5 1" "3 3"; do set -- $cfg
+echo "minb=$1 kb=$2"; TCG_FLOW_MINB=$1 TCG_FLOW_KB=$2 timeout 600 python tests/gpu_probe.py c5 c2 c4 c3 reps=5 mode=5 2>&1 | grep -oE '^c[0-9]|med_ms=[0-9.]+' | paste - - | tr '\n' ' '; echo
+done; done
