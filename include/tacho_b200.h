@@ -223,11 +223,9 @@ tcg_status tcg_restore(tcg_ctx* ctx);
 /* Factor the working values in place. TCG_BREAKDOWN sets stats->breakdown_*. */
 tcg_status tcg_factor(tcg_ctx* ctx, tcg_stats* stats);
 tcg_status tcg_download(tcg_ctx* ctx, double* values);
-/* End-to-end refactorization from host buffers (nnz x nbatch doubles each; pinned memory
- * lets the copies overlap): set the initial values, factor, download the factor. In mode 5
- * the input copy runs beside the kernel, which polls each input value like an operand, so
- * the upload hides behind the factorization; other modes run the three steps in turn.
- * The device copy of the initial values (tcg_restore) is not updated. */
+/* End-to-end refactorization from host buffers (nnz x nbatch doubles each; pinned memory for
+ * full PCIe speed): upload the initial values, factor, download the factor, stream-ordered
+ * in one call. The device copy of the initial values (tcg_restore) is not updated. */
 tcg_status tcg_factor_host(tcg_ctx* ctx, const double* values_in, double* values_out, tcg_stats* stats);
 /* Stamps of the last traced factor: per task {start, end} (2*ntasks words), then per
  * item {claimed, sources ready, merged, published} (4*nitems words); globaltimer ns. */

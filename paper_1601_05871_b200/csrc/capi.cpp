@@ -67,8 +67,6 @@ struct tcg_ctx {
   int sm_count = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaStream_t copy_stream = nullptr;  // host-buffer factorization: H2D beside the kernel
-  cudaEvent_t ev_prep = nullptr, ev_copy = nullptr;
   void* arena = nullptr;
   size_t arena_bytes = 0;
   tcbdev::Ctrl* host_ctrl = nullptr;
@@ -383,9 +381,6 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_prep, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_copy, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c->host_ctrl), sizeof(tcbdev::Ctrl));
   if (e != cudaSuccess) {
     g_plan_error = std::string("tcg_create: ") + cudaGetErrorString(e);
@@ -409,10 +404,6 @@ void tcg_destroy(tcg_ctx* c) {
   if (c->host_ctrl) cudaFreeHost(c->host_ctrl);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
-  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
-  if (c->ev_prep) cudaEventDestroy(c->ev_prep);
-  if (c->ev_copy) cudaEventDestroy(c->ev_copy);
-  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -678,9 +669,8 @@ tcg_status tcg_restore(tcg_ctx* c) {
 // Value-flow execution (mode 5, flow_kernel.cu): prelude (snapshot the
 // input, mark the output unwritten, reset the status words) + one persistent
 // launch; both inside the timed region.
-// host_in/host_out (tcg_factor_host): the inputs arrive by a copy on
-// copy_stream that runs beside the kernel (the kernel polls them, as it
-// polls operands), and the factor is copied back on the launch stream.
+// host_in/host_out (tcg_factor_host): upload, factor and download on the
+// launch stream.
 static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* host_in = nullptr,
                            double* host_out = nullptr, int phase = 0) {
   // gather batch from the mean products per coordinate (flow_kernel.cu variants)
@@ -726,9 +716,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   q.m_row = q.m_failed + c->nbatch;
   q.m_pivot = batch ? c->bm_pivot : c->m_pivot;
   q.nbatch = c->nbatch;
-  q.input_async = host_in != nullptr;
   tcbdev::FlowParams P{};
-  P.input_async = host_in != nullptr;
   P.peers = c->peers;
   P.npeers = c->npeers;
   P.rec = c->flow_rec;
@@ -754,17 +742,13 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
     return TCG_OK;
   }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  // host buffers: the upload goes first on the same stream. (Overlapping it
+  // with the kernel, which then polled its inputs, saved ~5% but relied on
+  // the copy running concurrently with the kernel, which CUDA does not
+  // promise -- under a profiler it serialised and the launch stalled.)
+  if (host_in) TCG_CUDA_TRY(c, cudaMemcpyAsync(vals, host_in, vbytes, cudaMemcpyHostToDevice, c->stream));
   if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
-  if (host_in) {  // inputs stream in while the kernel runs
-    TCG_CUDA_TRY(c, cudaEventRecord(c->ev_prep, c->stream));
-    TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->copy_stream, c->ev_prep, 0));
-  }
   if (c->nflow > 0) TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
-  if (host_in) {
-    TCG_CUDA_TRY(c, cudaMemcpyAsync(q.a, host_in, vbytes, cudaMemcpyHostToDevice, c->copy_stream));
-    TCG_CUDA_TRY(c, cudaEventRecord(c->ev_copy, c->copy_stream));
-    TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev_copy, 0));
-  }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
   if (host_out) TCG_CUDA_TRY(c, cudaMemcpyAsync(host_out, vals, vbytes, cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),

@@ -120,7 +120,6 @@ struct FlowParams {
   long long nnz;         // values per member
   int nrows;             // schedule rows (per member)
   int nbatch;            // members sharing the pattern
-  int input_async;       // the inputs `a` arrive during the launch (kUnset until copied): poll them
   double* const* peers;  // sharded (C6): every part's U, indexed by part; operands of other parts
   int npeers;            //   arrive as kRemoteBit | part << 25 | position (plan.hpp build_flow_part)
   unsigned long long timeout_ns;
@@ -147,7 +146,7 @@ struct FlowPrepParams {
   int* m_row;
   double* m_pivot;
   int nbatch;
-  int input_async;       // mark `a` kUnset (a copy fills it beside the kernel) instead of snapshotting
+
   Ctrl* ctrl;
 };
 

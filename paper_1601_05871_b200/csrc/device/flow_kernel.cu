@@ -137,18 +137,10 @@ struct Ctx {
   static constexpr bool kSysPublish = OPS == 2;  // readers on other GPUs
 };
 
-// An input value: immutable during the launch (read-only path), or, when
-// the inputs are still being copied in (input_async), polled like an operand.
-__device__ __forceinline__ double input_ld(const FlowParams& P, const double* p) {
-  if (!P.input_async) return __ldg(p);
-  return __longlong_as_double(static_cast<long long>(ld_relaxed_u64(p)));
-}
-__device__ __forceinline__ double input_settle(const FlowParams& P, const double* p, double x,
-                                               unsigned long long t0) {
-  if (!P.input_async) return x;
-  unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
-  if (b == kUnset) b = wait_value(p, P.ctrl, t0, P.timeout_ns);
-  return __longlong_as_double(static_cast<long long>(b));
+// An input value: the prelude's snapshot, immutable during the launch.
+__device__ __forceinline__ double input_ld(const FlowParams&, const double* p) { return __ldg(p); }
+__device__ __forceinline__ double input_settle(const FlowParams&, const double*, double x, unsigned long long) {
+  return x;
 }
 
 // One coordinate: v -= U[m]*U[o] over its merged program, in order. The
@@ -494,7 +486,7 @@ __global__ void flow_prepare(FlowPrepParams Q) {
   double2* o2 = reinterpret_cast<double2*>(Q.out);
   const double unset = __longlong_as_double(static_cast<long long>(kUnset));
   for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < h; x += stride) {
-    a2[x] = Q.input_async ? make_double2(unset, unset) : in2[x];
+    a2[x] = in2[x];
     o2[x] = make_double2(unset, unset);
   }
   for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < Q.nbatch; x += stride) {
@@ -504,7 +496,7 @@ __global__ void flow_prepare(FlowPrepParams Q) {
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (Q.nnz & 1) {
-      Q.a[Q.nnz - 1] = Q.input_async ? unset : Q.vals[Q.nnz - 1];
+      Q.a[Q.nnz - 1] = Q.vals[Q.nnz - 1];
       Q.out[Q.nnz - 1] = unset;
     }
     Ctrl c = {};
