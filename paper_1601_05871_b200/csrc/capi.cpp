@@ -687,8 +687,15 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   int remote = c->npeers > 1 ? 1 : 0;  // sharded: operands of other parts via peers
   if (const char* e = std::getenv("TCG_FLOW_REMOTE")) remote = std::atoi(e) ? 1 : remote;
   if (weak || dyn || g != 32) kb = 4;  // those variants exist with KB = 4 only
+  // shared-memory staged metadata (factor_flow_pipe) where it exists
+  bool pipe = !weak && !dyn && g == 32;
+  if (const char* e = std::getenv("TCG_FLOW_PIPE")) pipe = pipe && std::atoi(e) != 0;
   int occ = 0;
-  cudaError_t oe = tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
+  if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, &occ) != cudaSuccess) {
+    cudaGetLastError();
+    pipe = false;
+  }
+  cudaError_t oe = pipe ? cudaSuccess : tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
   if (oe == cudaErrorInvalidValue && kb != 4) {  // no such variant: the KB = 4 one
     kb = 4;
     oe = tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
@@ -748,7 +755,10 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // promise -- under a profiler it serialised and the launch stalled.)
   if (host_in) TCG_CUDA_TRY(c, cudaMemcpyAsync(vals, host_in, vbytes, cudaMemcpyHostToDevice, c->stream));
   if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
-  if (c->nflow > 0) TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
+  if (c->nflow > 0) {
+    if (pipe) TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, c->stream));
+    else TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
+  }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
   if (host_out) TCG_CUDA_TRY(c, cudaMemcpyAsync(host_out, vals, vbytes, cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),

@@ -364,6 +364,119 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
   }
 }
 
+// factor_flow with the per-row metadata staged in shared memory (PIPE): a
+// row of a short program is shorter than an L2 round trip, so prefetching its
+// record and first slot one row ahead in registers still exposes the round
+// trip (the loop-carried register copies wait for the loads). Here each warp
+// keeps rings in shared memory filled by cp.async (LDGSTS): the record four
+// rows ahead, the lanes' first slot records and input values two rows ahead;
+// iteration k waits only for the copies issued at iteration k-2.
+// (G = 32, static hand-out.)
+template <int THREADS, int KB, int MINB, int REMOTE>
+__global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) {
+  constexpr int kWarps = THREADS / 32;
+  constexpr int kLenMask = (1 << 30) - 1;
+  struct Ring {
+    int4 rec[8];
+    int4 slot[4][32];
+    double in[4][32];
+  };
+  __shared__ Ring rings[kWarps];
+  const int lane = threadIdx.x & 31;
+  Ring& R = rings[threadIdx.x >> 5];
+  const int W = gridDim.x * kWarps;
+  const int w0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  Ctx<0, REMOTE ? 2 : 0> C{P, gtimer(), P.vals, P.a, 0};
+  int ran = 0, executed = 0, anyfail = 0;
+  const int nrows = P.nrows * P.nbatch;
+  auto member_of = [&](int p, int& q) {
+    q = P.nbatch == 1 ? p : p / P.nbatch;
+    return p - q * P.nbatch;
+  };
+  auto position = [&](int k) { return w0 + k * W; };
+  auto fetch_rec = [&](int k) {
+    const int p = position(k);
+    if (lane == 0 && p < nrows) {
+      int q;
+      member_of(p, q);
+      cp_async16(&R.rec[k & 7], P.rec + q);
+    }
+  };
+  auto fetch_slot = [&](int k) {  // needs R.rec[k & 7] visible
+    const int p = position(k);
+    if (p >= nrows) return;
+    const int4 r = R.rec[k & 7];
+    if (lane < (r.y & kLenMask)) {
+      int q;
+      const long long m = member_of(p, q);
+      cp_async16(&R.slot[k & 3][lane], P.slot + r.x + lane);
+      cp_async8(&R.in[k & 3][lane], P.a + m * P.nnz + r.x + lane);
+    }
+  };
+  // prologue: records of rows 0..3, then the slots of rows 0 and 1
+  for (int k = 0; k < 4; ++k) fetch_rec(k);
+  cp_async_commit();
+  cp_async_wait_all();
+  __syncwarp();
+  fetch_slot(0);
+  fetch_slot(1);
+  cp_async_commit();
+  cp_async_wait_all();
+  cp_async_commit();  // an empty group: the steady state waits for "all but the newest"
+  __syncwarp();
+  for (int k = 0; position(k) < nrows; ++k) {
+    const int pos = position(k);
+    cp_async_wait_group<1>();  // the copies of iteration k-2: slots of row k, record of row k+2
+    __syncwarp();
+    const int4 a = R.rec[k & 7];
+    const int tb = a.x, L = a.y & kLenMask, dpos = a.z, t = a.w;
+    int4 sr0 = make_int4(0, 0, 0, 0);
+    double a0 = 0.0;
+    if (lane < L) {
+      sr0 = R.slot[k & 3][lane];
+      a0 = R.in[k & 3][lane];
+    }
+    fetch_rec(k + 4);
+    fetch_slot(k + 2);
+    cp_async_commit();
+    const bool chol = ((a.y >> 30) & 1) == kChol;
+    const bool exported = a.y < 0;
+    int q;
+    C.member = member_of(pos, q);
+    C.vals = P.vals + static_cast<long long>(C.member) * P.nnz;
+    C.a = P.a + static_cast<long long>(C.member) * P.nnz;
+    const bool traced = P.trace && lane == 0 && C.member == 0;
+    unsigned long long* stamp = P.trace && C.member == 0 ? P.trace + 4 * static_cast<long long>(P.item[q]) : nullptr;
+    if (traced) stamp[0] = gtimer();
+    if ((ran & 15) == 0) anyfail = __shfl_sync(kFull, lane == 0 ? ld_relaxed(&P.ctrl->failed.v) : 0, 0);
+    int latched = 0;
+    if (anyfail) latched = __shfl_sync(kFull, lane == 0 ? ld_relaxed(P.m_failed + C.member) : 0, 0);
+    if (!latched) {
+      if (chol)
+        flow_row<kChol, KB, 32>(C, tb, L, dpos, t, lane, kFull, 0, a0, sr0, stamp ? stamp + 1 : nullptr,
+                                nullptr, exported);
+      else
+        flow_row<kTrsm, KB, 32>(C, tb, L, dpos, t, lane, kFull, 0, a0, sr0, stamp ? stamp + 1 : nullptr,
+                                nullptr, exported);
+      ++executed;
+    } else {
+      for (int k2 = lane; k2 < L; k2 += 32) {
+        unsigned long long x = static_cast<unsigned long long>(__double_as_longlong(__ldg(C.a + tb + k2)));
+        if (x == kUnset) x = kCanonicalNaN;
+        if (decltype(C)::kSysPublish && exported) st_relaxed_sys_u64(C.vals + tb + k2, x);
+        else st_relaxed_u64(C.vals + tb + k2, x);
+      }
+    }
+    if (traced) stamp[3] = gtimer();
+    ++ran;
+  }
+  cp_async_wait_all();
+  if (lane == 0) {
+    if (ran) atomicAdd(&P.ctrl->done.v, ran);
+    if (executed) atomicAdd(&P.ctrl->executed.v, executed);
+  }
+}
+
 // Block units (mode 6; plan.cpp build_units). CTAs [0, nu_ctas) run the
 // units: a unit's rows level by level (warps take the rows of a level
 // round-robin, one __syncthreads between levels), the unit's own values in
@@ -591,6 +704,35 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
   blocks = blocks < 1 ? 1 : (blocks > 8LL * sm_count ? 8LL * sm_count : blocks);
   init_values<<<static_cast<int>(blocks), 256, 0, st>>>(a, map, vals, vals0, nnz, nnz_a, nbatch);
   return cudaGetLastError();
+}
+
+#define TCG_PIPE_VARIANTS(X) X(256, 2, 3, 0) X(256, 3, 3, 0) X(256, 4, 3, 0) X(256, 2, 4, 0) X(256, 2, 3, 1) \
+  X(256, 3, 3, 1) X(256, 4, 3, 1)
+
+static const void* pipe_kernel_for(int threads, int kb, int minb, int remote) {
+#define X(T, K, M, R) \
+  if (threads == T && kb == K && minb == M && remote == R) return reinterpret_cast<const void*>(&factor_flow_pipe<T, K, M, R>);
+  TCG_PIPE_VARIANTS(X)
+#undef X
+  return nullptr;
+}
+
+cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int* ctas_per_sm) {
+  const void* k = pipe_kernel_for(threads, kb, minb, remote);
+  if (!k) return cudaErrorInvalidValue;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
+}
+
+cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb, int minb, int remote,
+                             cudaStream_t st) {
+#define X(T, K, M, R)                                                 \
+  if (threads == T && kb == K && minb == M && remote == R) {          \
+    factor_flow_pipe<T, K, M, R><<<grid, T, 0, st>>>(p);              \
+    return cudaGetLastError();                                        \
+  }
+  TCG_PIPE_VARIANTS(X)
+#undef X
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStream_t st) {
