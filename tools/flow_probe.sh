@@ -1,5 +1,3 @@
-timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1
 for r in 1 2; do
-for pp in 0 1; do echo "pipe=$pp"; TCG_FLOW_PIPE=$pp timeout 600 python tests/gpu_probe.py c1 c5 c2 c4 reps=5 mode=5 2>&1 | grep -oE '^c[0-9]|med_ms=[0-9.]+|grid=[0-9]+' | paste - - - | tr '\n' ' '; echo; done
+for o in "" "0.8,1.0,0.3" "1.5,1.0,0.3" "0.8,0.5,0.5" "2,1,0.2"; do echo "order=$o"; env ${o:+TCG_FLOW_ORDER=$o} timeout 600 python tests/gpu_probe.py c5 c2 c4 reps=5 mode=5 2>&1 | grep -oE '^c[0-9]|med_ms=[0-9.]+|bitwise=[A-Za-z]+' | paste - - - | tr '\n' ' '; echo; done
 done
-for pp in 0 1; do TCG_FLOW_PIPE=$pp timeout 300 python tests/gpu_overhead_probe.py 2>&1 | tail -1; TCG_FLOW_PIPE=$pp timeout 300 python tests/gpu_chain_probe.py 2>&1 | grep "mode=5" | head -1; done
