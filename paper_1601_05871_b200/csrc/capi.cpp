@@ -690,8 +690,10 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // shared-memory staged metadata (factor_flow_pipe) where it exists
   bool pipe = !weak && !dyn && g == 32;
   if (const char* e = std::getenv("TCG_FLOW_PIPE")) pipe = pipe && std::atoi(e) != 0;
+  int extras = (c->nbatch > 1 || c->opt.trace) ? 1 : 0;
+  if (const char* e = std::getenv("TCG_FLOW_EXTRAS")) extras = std::atoi(e) ? 1 : extras;
   int occ = 0;
-  if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, &occ) != cudaSuccess) {
+  if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ) != cudaSuccess) {
     cudaGetLastError();
     pipe = false;
   }
@@ -756,7 +758,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (host_in) TCG_CUDA_TRY(c, cudaMemcpyAsync(vals, host_in, vbytes, cudaMemcpyHostToDevice, c->stream));
   if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
   if (c->nflow > 0) {
-    if (pipe) TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, c->stream));
+    if (pipe) TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, extras, c->stream));
     else TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
   }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));

@@ -372,7 +372,9 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
 // rows ahead, the lanes' first slot records and input values two rows ahead;
 // iteration k waits only for the copies issued at iteration k-2.
 // (G = 32, static hand-out.)
-template <int THREADS, int KB, int MINB, int REMOTE>
+// EXTRAS = 0: a single matrix without trace stamps (no batch member
+// arithmetic, no stamp branches); 1: batches and traces.
+template <int THREADS, int KB, int MINB, int REMOTE, int EXTRAS>
 __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) {
   constexpr int kWarps = THREADS / 32;
   constexpr int kLenMask = (1 << 30) - 1;
@@ -388,8 +390,12 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
   const int w0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
   Ctx<0, REMOTE ? 2 : 0> C{P, gtimer(), P.vals, P.a, 0};
   int ran = 0, executed = 0, anyfail = 0;
-  const int nrows = P.nrows * P.nbatch;
+  const int nrows = EXTRAS ? P.nrows * P.nbatch : P.nrows;
   auto member_of = [&](int p, int& q) {
+    if (!EXTRAS) {
+      q = p;
+      return 0;
+    }
     q = P.nbatch == 1 ? p : p / P.nbatch;
     return p - q * P.nbatch;
   };
@@ -442,12 +448,16 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
     const bool chol = ((a.y >> 30) & 1) == kChol;
     const bool exported = a.y < 0;
     int q;
-    C.member = member_of(pos, q);
-    C.vals = P.vals + static_cast<long long>(C.member) * P.nnz;
-    C.a = P.a + static_cast<long long>(C.member) * P.nnz;
-    const bool traced = P.trace && lane == 0 && C.member == 0;
-    unsigned long long* stamp = P.trace && C.member == 0 ? P.trace + 4 * static_cast<long long>(P.item[q]) : nullptr;
-    if (traced) stamp[0] = gtimer();
+    unsigned long long* stamp = nullptr;
+    bool traced = false;
+    if (EXTRAS) {
+      C.member = member_of(pos, q);
+      C.vals = P.vals + static_cast<long long>(C.member) * P.nnz;
+      C.a = P.a + static_cast<long long>(C.member) * P.nnz;
+      traced = P.trace && lane == 0 && C.member == 0;
+      stamp = P.trace && C.member == 0 ? P.trace + 4 * static_cast<long long>(P.item[q]) : nullptr;
+      if (traced) stamp[0] = gtimer();
+    }
     if ((ran & 15) == 0) anyfail = __shfl_sync(kFull, lane == 0 ? ld_relaxed(&P.ctrl->failed.v) : 0, 0);
     int latched = 0;
     if (anyfail) latched = __shfl_sync(kFull, lane == 0 ? ld_relaxed(P.m_failed + C.member) : 0, 0);
@@ -706,29 +716,31 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
   return cudaGetLastError();
 }
 
-#define TCG_PIPE_VARIANTS(X) X(256, 2, 3, 0) X(256, 3, 3, 0) X(256, 4, 3, 0) X(256, 2, 4, 0) X(256, 2, 3, 1) \
-  X(256, 3, 3, 1) X(256, 4, 3, 1)
+#define TCG_PIPE_VARIANTS(X)                                                                       \
+  X(256, 2, 3, 0, 0) X(256, 3, 3, 0, 0) X(256, 4, 3, 0, 0) X(256, 2, 3, 0, 1) X(256, 3, 3, 0, 1) \
+  X(256, 4, 3, 0, 1) X(256, 2, 3, 1, 1) X(256, 3, 3, 1, 1) X(256, 4, 3, 1, 1)
 
-static const void* pipe_kernel_for(int threads, int kb, int minb, int remote) {
-#define X(T, K, M, R) \
-  if (threads == T && kb == K && minb == M && remote == R) return reinterpret_cast<const void*>(&factor_flow_pipe<T, K, M, R>);
+static const void* pipe_kernel_for(int threads, int kb, int minb, int remote, int extras) {
+#define X(T, K, M, R, E)                                                     \
+  if (threads == T && kb == K && minb == M && remote == R && extras == E)    \
+    return reinterpret_cast<const void*>(&factor_flow_pipe<T, K, M, R, E>);
   TCG_PIPE_VARIANTS(X)
 #undef X
   return nullptr;
 }
 
-cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int* ctas_per_sm) {
-  const void* k = pipe_kernel_for(threads, kb, minb, remote);
+cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm) {
+  const void* k = pipe_kernel_for(threads, kb, minb, remote, extras);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
 }
 
 cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb, int minb, int remote,
-                             cudaStream_t st) {
-#define X(T, K, M, R)                                                 \
-  if (threads == T && kb == K && minb == M && remote == R) {          \
-    factor_flow_pipe<T, K, M, R><<<grid, T, 0, st>>>(p);              \
-    return cudaGetLastError();                                        \
+                             int extras, cudaStream_t st) {
+#define X(T, K, M, R, E)                                                          \
+  if (threads == T && kb == K && minb == M && remote == R && extras == E) {       \
+    factor_flow_pipe<T, K, M, R, E><<<grid, T, 0, st>>>(p);                       \
+    return cudaGetLastError();                                                    \
   }
   TCG_PIPE_VARIANTS(X)
 #undef X
