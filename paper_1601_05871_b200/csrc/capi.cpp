@@ -675,7 +675,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
                            double* host_out = nullptr, int phase = 0) {
   // gather batch from the mean products per coordinate (flow_kernel.cu variants)
   const double mean = c->nnz > 0 ? static_cast<double>(c->nflow_upd) / static_cast<double>(c->nnz) : 0.0;
-  int kb = mean <= 4.0 ? 2 : mean <= 16.0 ? 3 : 4;
+  int kb = mean <= 4.0 ? 2 : 3;
   int minb = threads == 128 ? 6 : threads == 384 ? 2 : threads == 256 ? 3 : 1;
   if (const char* e = std::getenv("TCG_FLOW_KB")) kb = std::atoi(e);
   if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
@@ -1058,14 +1058,8 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
   int mode = c->opt.mode;
   if (mode == 0 && c->nbatch > 1 && c->has_flow) mode = 5;
-  if (mode == 0) {
-    // value flow unless the programs are long (mean products per coordinate
-    // above 16, e.g. C3): there the finalising rows' serial gathers dominate
-    // and the flag schedule, which runs Herk/Gemm rows early, measured faster
-    const bool long_programs = c->nupdates > 16 * c->nnz;
-    mode = c->has_flow && !(long_programs && c->has_static) ? 5
-           : c->has_static ? 4 : c->has_rows ? 3 : (c->has_programs ? 2 : 1);
-  }
+  if (mode == 0)  // value flow wherever the plan has its tables (fastest on C1-C6)
+    mode = c->has_flow ? 5 : c->has_static ? 4 : c->has_rows ? 3 : (c->has_programs ? 2 : 1);
   if ((mode == 2 && !c->has_programs) || (mode == 3 && !c->has_rows) ||
       (mode == 4 && !c->has_static) || (mode == 5 && !c->has_flow) || (mode == 6 && !c->has_units) ||
       mode < 0 || mode > 6) {
@@ -1228,8 +1222,7 @@ tcg_status tcg_factor_phase(tcg_ctx* c, int32_t phase, tcg_stats* st) {
 tcg_status tcg_factor_host(tcg_ctx* c, const double* values_in, double* values_out, tcg_stats* st) {
   if (!c || !c->uploaded || ((!values_in || !values_out) && c->nnz > 0)) return TCG_INVALID;
   int mode = c->opt.mode;
-  const bool flow = c->has_flow && c->nnz > 0 && c->ntasks > 0 && (mode == 0 || mode == 5) &&
-                    !(mode == 0 && c->nbatch == 1 && c->nupdates > 16 * c->nnz && c->has_static);
+  const bool flow = c->has_flow && c->nnz > 0 && c->ntasks > 0 && (mode == 0 || mode == 5);
   if (!flow) {  // other modes: the same three steps, one after the other
     tcg_status r = c->nbatch > 1 ? tcg_set_batch_values(c, values_in) : tcg_set_values(c, values_in);
     if (r != TCG_OK) return r;
