@@ -146,6 +146,10 @@ struct tcg_ctx {
   int epoch = 0;
   int max_target_len = 0, max_flag_rows = 0;
   bool uploaded = false;
+  // the working values equal their restore copy (after upload, set_values,
+  // restore): mode 5 then reads its input from the copy instead of
+  // snapshotting the working values first
+  bool pristine = false;
   tcg_options opt{};
   std::string err;
 };
@@ -638,6 +642,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->max_target_len = p->max_target_len;
   c->max_flag_rows = p->max_flag_rows;
   c->uploaded = true;
+  c->pristine = true;
   return TCG_OK;
 }
 
@@ -650,6 +655,7 @@ tcg_status tcg_set_values(tcg_ctx* c, const double* values) {
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals, c->vals0, sizeof(double) * c->nnz,
                                   cudaMemcpyDeviceToDevice, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->pristine = true;
   return TCG_OK;
 }
 
@@ -663,6 +669,7 @@ tcg_status tcg_restore(tcg_ctx* c) {
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals, c->vals0, sizeof(double) * c->nnz,
                                   cudaMemcpyDeviceToDevice, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->pristine = true;
   return TCG_OK;
 }
 
@@ -718,6 +725,8 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   tcbdev::FlowPrepParams q{};
   q.vals = vals;
   q.a = batch ? c->ba : c->flow_a;
+  const bool from_copy = c->pristine && !host_in;
+  if (from_copy) q.a = batch ? c->bvals0 : c->vals0;
   q.out = vals;
   q.nnz = c->nnz * c->nbatch;
   q.ctrl = c->ctrl;
@@ -733,6 +742,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   P.slot = c->flow_slot;
   P.upd = c->flow_upd;
   P.a = q.a;
+  if (from_copy) q.a = const_cast<double*>(q.vals);  // tells the prelude not to copy
   P.vals = vals;
   P.ctrl = c->ctrl;
   P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
@@ -762,6 +772,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
     else TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
   }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  c->pristine = false;  // the working values now hold the factor
   if (host_out) TCG_CUDA_TRY(c, cudaMemcpyAsync(host_out, vals, vbytes, cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
                                   cudaMemcpyDeviceToHost, c->stream));
@@ -1074,6 +1085,7 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
     c->err = "threads_per_cta 384 and 768 are for mode 5 only";
     return TCG_INVALID;
   }
+  if (mode != 5) c->pristine = false;  // every other executor factors the working values in place
   if (mode == 3) return run_rows(c, S, threads);
   if (mode == 4) return run_static(c, S, threads);
   if (mode == 5) return run_flow(c, S, threads);
@@ -1271,6 +1283,7 @@ tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals, c->bvals0, vb, cudaMemcpyDeviceToDevice, c->stream));
   }
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->pristine = true;
   return TCG_OK;
 }
 
@@ -1321,6 +1334,7 @@ tcg_status tcg_set_a_values(tcg_ctx* c, int32_t nbatch, const double* a_values) 
   TCG_CUDA_TRY(c, tcbdev::launch_init_values(c->a_stage, c->a_map, v, v0, c->nnz, c->nnz_a, nbatch,
                                              c->sm_count, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->pristine = true;
   return TCG_OK;
 }
 
@@ -1332,6 +1346,7 @@ tcg_status tcg_set_batch_values(tcg_ctx* c, const double* values) {
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals0, values, vb, cudaMemcpyHostToDevice, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals, c->bvals0, vb, cudaMemcpyDeviceToDevice, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->pristine = true;
   return TCG_OK;
 }
 
@@ -1372,6 +1387,7 @@ tcg_status tcg_download_trace(tcg_ctx* c, uint64_t* stamps) {
 
 tcg_status tcg_device_values(tcg_ctx* c, double** dptr, int64_t* nnz) {
   if (!c || !c->uploaded) return TCG_INVALID;
+  c->pristine = false;  // the caller may write the working values
   if (dptr) *dptr = c->vals;
   if (nnz) *nnz = c->nnz;
   return TCG_OK;

@@ -139,7 +139,7 @@ struct UnitParams {
 
 struct FlowPrepParams {
   const double* vals;    // working values (input of the factorization)
-  double* a;             // snapshot of them
+  double* a;             // snapshot of them; == vals: no copy (the input already lives in `a`)
   double* out;           // = vals in place: set to kUnset
   long long nnz;         // all members
   int* m_failed;         // reset per member

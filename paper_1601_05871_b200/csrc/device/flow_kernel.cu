@@ -609,7 +609,7 @@ __global__ void flow_prepare(FlowPrepParams Q) {
   double2* o2 = reinterpret_cast<double2*>(Q.out);
   const double unset = __longlong_as_double(static_cast<long long>(kUnset));
   for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < h; x += stride) {
-    a2[x] = in2[x];
+    if (Q.a != Q.vals) a2[x] = in2[x];  // (the pristine copy serves as input when it is current)
     o2[x] = make_double2(unset, unset);
   }
   for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < Q.nbatch; x += stride) {
@@ -619,7 +619,7 @@ __global__ void flow_prepare(FlowPrepParams Q) {
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (Q.nnz & 1) {
-      Q.a[Q.nnz - 1] = Q.vals[Q.nnz - 1];
+      if (Q.a != Q.vals) Q.a[Q.nnz - 1] = Q.vals[Q.nnz - 1];
       Q.out[Q.nnz - 1] = unset;
     }
     Ctrl c = {};
