@@ -132,6 +132,8 @@ struct Ctx {
         }
       } while (xa == kUnset || xb == kUnset);
     }
+    if (OPS != 2)  // settled by the loop above
+      return __dmul_rn(__longlong_as_double(static_cast<long long>(xa)), __longlong_as_double(static_cast<long long>(xb)));
     return __dmul_rn(settle_at(pa, xa), settle_at(pb, xb));
   }
   static constexpr bool kSysPublish = OPS == 2;  // readers on other GPUs
