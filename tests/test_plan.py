@@ -28,7 +28,7 @@ def test_plan_dag_and_blocks_match_reference(name, golden, oracle):
     assert list(s.tasks) == g["dag"]["tasks"]
 
 
-@pytest.mark.parametrize("name", ["c1", "s27_16_k2", "grid20_k2_leaf4", "rand_spd_200"])
+@pytest.mark.parametrize("name", ["c1", "elast6_k1", "grid20_k2_leaf4", "rand_spd_200"])
 def test_replays_are_bitwise_serial(name, golden, oracle):
     plan = planned(name)
     _, an = analyzed(name)
@@ -192,7 +192,7 @@ def replay_flow(t, order=None):
     return out
 
 
-@pytest.mark.parametrize("name", ["c1", "s27_16_k2", "rand_spd_200", "grid20_k2_leaf4", "elast6_k1"])
+@pytest.mark.parametrize("name", ["c1", "rand_spd_200", "grid20_k2_leaf4", "elast6_k1"])
 def test_flow_schedule_partitions_u_and_replays_bitwise(name, oracle):
     # mode 5: the Chol/Trsm rows own every coordinate once; merged programs
     # keep the per-coordinate product order, so replays equal factor_serial
@@ -285,7 +285,7 @@ def replay_units(t):
 
 
 @pytest.mark.parametrize("name,min_rows", [("c5_m0", 64), ("c5_m0", 16), ("grid20_k2_leaf4", 8),
-                                           ("s27_16_k2", 32), ("rand_spd_200", 4)])
+                                           ("elast6_k1", 32), ("rand_spd_200", 4)])
 def test_unit_schedule_replays_bitwise(T, name, min_rows, oracle, monkeypatch):
     monkeypatch.setenv("TCG_UNIT_MIN_ROWS", str(min_rows))
     _, an = analyzed(name)
@@ -365,7 +365,7 @@ def replay_parts(t, parts, owners):
 
 
 @pytest.mark.parametrize("name,nparts,extra", [("c5_m0", 2, False), ("c5_m0", 4, True),
-                                               ("s27_16_k2", 2, True), ("c1", 8, False)])
+                                               ("elast6_k1", 2, True), ("c1", 8, False)])
 def test_sharded_parts_replay_bitwise(T, name, nparts, extra, oracle):
     # C6-style sharding: each part owns the rows of its ND subtree (separators
     # to part 0, or to an extra last part); every part has its own copy of U
