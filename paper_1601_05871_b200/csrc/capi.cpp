@@ -187,6 +187,7 @@ tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pa
     if (const char* e = std::getenv("TCG_DEP_WIDE_COST")) po.dep_wide_cost = std::max(1.0, std::atof(e));
     if (const char* e = std::getenv("TCG_HOT_FRACTION")) po.hot_fraction = std::atof(e);
     if (const char* e = std::getenv("TCG_UNIT_MIN_ROWS")) po.unit_min_rows = std::atoi(e);
+    if (const char* e = std::getenv("TCG_FLOW_MERGE_ROWS")) po.flow_merge_rows = std::atoi(e) != 0;
     if (const char* e = std::getenv("TCG_UNIT_SMEM")) po.unit_smem_cap = std::atoll(e);
     p->plan = tcb::build_plan(u, init, rl, true, po);
     try {

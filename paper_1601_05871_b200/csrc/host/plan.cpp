@@ -428,22 +428,58 @@ void build_item_deps(Plan& P, const RangeList& ranges, double opt_hot_fraction) 
 // work runs early. On B200 it lost on every acceptance config -- C2 0.69 ->
 // 0.83 ms, C3 7.6 -> 17 ms -- the extra rows cost more than the shorter
 // finaliser programs saved.)
-void build_flow(Plan& P) {
+void build_flow(Plan& P, const CsrMatrix& u, bool merge_rows) {
   const std::size_t I = P.item_rec.size() / kItemWords;
   const std::size_t N = static_cast<std::size_t>(P.nnz);
   auto R = [&](std::size_t k, int w) { return P.row_rec[k * kRowWords + w]; };
-  P.flow_owner.assign(N, -1);
-  std::int64_t nfin = 0;
+  // every coordinate's finalising item, and per matrix row its Chol item
+  std::vector<std::int32_t> fin_item(N, -1), chol_of_row(static_cast<std::size_t>(P.n), -1);
   for (std::size_t k = 0; k < I; ++k)
     if (R(k, 4) <= kTrsm) {
-      ++nfin;
+      if (R(k, 4) == kChol) chol_of_row[R(k, 5)] = static_cast<std::int32_t>(k);
       for (std::int32_t x = R(k, 0); x < R(k, 1); ++x) {
-        if (P.flow_owner[x] >= 0) throw std::logic_error("flow: coordinate finalised twice");
-        P.flow_owner[x] = static_cast<std::int32_t>(k);
+        if (fin_item[x] >= 0) throw std::logic_error("flow: coordinate finalised twice");
+        fin_item[x] = static_cast<std::int32_t>(k);
       }
     }
   for (std::size_t x = 0; x < N; ++x)
-    if (P.flow_owner[x] < 0) throw std::logic_error("flow: coordinate without a finaliser");
+    if (fin_item[x] < 0) throw std::logic_error("flow: coordinate without a finaliser");
+  // The rows the schedule runs ("units"). With merge_rows a matrix row whose
+  // whole U row fits one warp pass (<= 32 entries) is one unit: its Chol and
+  // Trsm items share the divisor U(t,t) and nearly all their sources (every
+  // coordinate (t,c) takes U(r,t)*U(r,c) over the same rows r), so one row
+  // pays the per-row cost once. Longer rows keep one unit per item, which
+  // run on different warps. Units are in (row, Chol first) order, which is
+  // topological: every operand comes from a row above.
+  struct Unit {
+    std::int32_t tb, L, dpos, kind, t, item;
+  };
+  std::vector<Unit> units;
+  std::vector<std::int32_t> unit_of(N, -1);
+  std::vector<std::vector<std::int32_t>> items_of_row(static_cast<std::size_t>(P.n));
+  for (std::size_t k = 0; k < I; ++k)
+    if (R(k, 4) == kTrsm) items_of_row[R(k, 5)].push_back(static_cast<std::int32_t>(k));
+  for (index_t t = 0; t < P.n; ++t) {
+    const std::int32_t ck = chol_of_row[t];
+    if (ck < 0) throw std::logic_error("flow: row without a Chol item");
+    const auto rb = static_cast<std::int32_t>(u.row_begin(t)), re = static_cast<std::int32_t>(u.row_end(t));
+    if (merge_rows && re - rb <= 32) {
+      units.push_back({rb, re - rb, rb, kChol, static_cast<std::int32_t>(t), ck});
+      continue;
+    }
+    units.push_back({R(ck, 0), R(ck, 1) - R(ck, 0), R(ck, 2), kChol, static_cast<std::int32_t>(t), ck});
+    for (std::int32_t k : items_of_row[t])
+      units.push_back({R(k, 0), R(k, 1) - R(k, 0), R(k, 2), kTrsm, static_cast<std::int32_t>(t), k});
+  }
+  const std::size_t U = units.size();
+  for (std::size_t g = 0; g < U; ++g)
+    for (std::int32_t x = units[g].tb; x < units[g].tb + units[g].L; ++x) {
+      if (unit_of[x] >= 0) throw std::logic_error("flow: coordinate in two units");
+      unit_of[x] = static_cast<std::int32_t>(g);
+    }
+  // flow_owner (per coordinate): the item representing its unit (build_units / build_flow_part)
+  P.flow_owner.assign(N, -1);
+  for (std::size_t x = 0; x < N; ++x) P.flow_owner[x] = units[unit_of[x]].item;
   // merged programs: per coordinate, the products of every item on it in item order
   std::vector<std::int64_t> cnt(N + 1, 0);
   for (std::size_t k = 0; k < I; ++k)
@@ -475,51 +511,49 @@ void build_flow(Plan& P) {
     }
   }
   // levels (forward) and heights (backward) over "reads a coordinate owned by"
-  std::vector<std::int32_t> level(I, 0), height(I, 0);
-  auto each_src = [&](std::size_t k, auto&& fn) {
-    if (R(k, 4) == kTrsm) fn(P.flow_owner[R(k, 2)]);  // divisor U(t,t)
-    for (std::int32_t x = R(k, 0); x < R(k, 1); ++x)
-      for (std::int64_t u = cnt[x]; u < cnt[x + 1]; ++u) {
-        fn(P.flow_owner[P.flow_upd[2 * u]]);
-        fn(P.flow_owner[P.flow_upd[2 * u + 1]]);
+  std::vector<std::int32_t> level(U, 0), height(U, 0);
+  auto each_src = [&](std::size_t g, auto&& fn) {
+    if (units[g].kind == kTrsm) fn(unit_of[units[g].dpos]);  // divisor U(t,t)
+    for (std::int32_t x = units[g].tb; x < units[g].tb + units[g].L; ++x)
+      for (std::int64_t e = cnt[x]; e < cnt[x + 1]; ++e) {
+        fn(unit_of[P.flow_upd[2 * e]]);
+        fn(unit_of[P.flow_upd[2 * e + 1]]);
       }
   };
   std::int32_t depth = 0;
-  for (std::size_t k = 0; k < I; ++k) {
-    if (R(k, 4) > kTrsm) continue;
+  for (std::size_t g = 0; g < U; ++g) {
     std::int32_t lv = 1;
-    each_src(k, [&](std::int32_t s) {
-      if (s < 0 || static_cast<std::size_t>(s) >= k) throw std::logic_error("flow: dependence out of order");
-      lv = std::max(lv, level[s] + 1);
+    each_src(g, [&](std::int32_t sidx) {
+      if (sidx < 0 || static_cast<std::size_t>(sidx) >= g) throw std::logic_error("flow: dependence out of order");
+      lv = std::max(lv, level[sidx] + 1);
     });
-    level[k] = lv;
+    level[g] = lv;
     depth = std::max(depth, lv);
   }
-  for (std::size_t k = I; k-- > 0;) {
-    if (R(k, 4) > kTrsm) continue;
-    height[k] = std::max(height[k], 1);
-    const std::int32_t h = height[k] + 1;
-    each_src(k, [&](std::int32_t s) { height[s] = std::max(height[s], h); });
+  for (std::size_t g = U; g-- > 0;) {
+    height[g] = std::max(height[g], 1);
+    const std::int32_t h = height[g] + 1;
+    each_src(g, [&](std::int32_t sidx) { height[sidx] = std::max(height[sidx], h); });
   }
-  std::vector<std::int32_t> order;
-  order.reserve(static_cast<std::size_t>(nfin));
-  for (std::size_t k = 0; k < I; ++k)
-    if (R(k, 4) <= kTrsm) order.push_back(static_cast<std::int32_t>(k));
+  std::vector<std::int32_t> order(U);
+  for (std::size_t g = 0; g < U; ++g) order[g] = static_cast<std::int32_t>(g);
   std::stable_sort(order.begin(), order.end(), [&](std::int32_t x, std::int32_t y) {
     if (level[x] != level[y]) return level[x] < level[y];
     return height[x] > height[y];
   });
-  P.flow_rec.assign(order.size() * kFlowWords, 0);
-  P.flow_item = order;
-  for (std::size_t q = 0; q < order.size(); ++q) {
-    const std::size_t k = static_cast<std::size_t>(order[q]);
+  P.flow_rec.assign(U * kFlowWords, 0);
+  P.flow_item.assign(U, 0);
+  for (std::size_t q = 0; q < U; ++q) {
+    const Unit& un = units[static_cast<std::size_t>(order[q])];
+    if (un.L >= (1 << kFlowKindShift)) throw std::length_error("flow: row slice too long");
     std::int32_t* o = &P.flow_rec[q * kFlowWords];
-    if (R(k, 1) - R(k, 0) >= (1 << kFlowKindShift)) throw std::length_error("flow: row slice too long");
-    o[0] = R(k, 0);
-    o[1] = (R(k, 1) - R(k, 0)) | (R(k, 4) << kFlowKindShift);
-    o[2] = R(k, 2);
-    o[3] = R(k, 5);
+    o[0] = un.tb;
+    o[1] = un.L | (un.kind << kFlowKindShift);
+    o[2] = un.dpos;
+    o[3] = un.t;
+    P.flow_item[q] = un.item;
   }
+  const std::int64_t nfin = static_cast<std::int64_t>(U);
   P.stats.flow_rows = nfin;
   P.stats.flow_depth = depth;
 }
@@ -551,13 +585,22 @@ void build_units(Plan& P, const RangeList& ranges, std::int32_t min_rows, std::i
   std::vector<std::int32_t> pos_of_item(I, -1);
   for (std::size_t q = 0; q < R; ++q) pos_of_item[P.flow_item[q]] = static_cast<std::int32_t>(q);
   // candidate units: Chol rows of large diagonal blocks whose values fit
+  // (only blocks whose Chol rows are the diagonal-block slices: a whole
+  // matrix row run as one flow row, build_flow merge_rows, reaches into
+  // blocks other rows of the chain read, which would tie a unit into a cycle)
   std::vector<std::int64_t> nloc(static_cast<std::size_t>(ranges.count()), 0);
+  std::vector<char> whole_rows(static_cast<std::size_t>(ranges.count()), 0);
   for (std::size_t q = 0; q < R; ++q)
-    if (kind(q) == kChol) nloc[range_of[F(q, 3)]] += len(q);
+    if (kind(q) == kChol) {
+      nloc[range_of[F(q, 3)]] += len(q);
+      const std::size_t it = static_cast<std::size_t>(P.flow_item[q]);
+      if (len(q) != P.row_rec[it * kRowWords + 1] - P.row_rec[it * kRowWords]) whole_rows[range_of[F(q, 3)]] = 1;
+    }
   std::vector<std::int32_t> unit_of_range(static_cast<std::size_t>(ranges.count()), -1);
   std::int32_t nunits = 0;
   for (index_t r = 0; r < ranges.count(); ++r)
-    if (min_rows > 0 && ranges.ranges[r].size() > min_rows && nloc[r] > 0 && nloc[r] * 8 <= smem_cap)
+    if (min_rows > 0 && ranges.ranges[r].size() > min_rows && nloc[r] > 0 && nloc[r] * 8 <= smem_cap &&
+        !whole_rows[r])
       unit_of_range[r] = nunits++;
   std::vector<std::int32_t> unit_of_pos(R, -1);
   for (std::size_t q = 0; q < R; ++q)
@@ -969,7 +1012,7 @@ Plan build_plan(const CsrMatrix& u, const std::vector<double>& init_values,
 
   if (with_work && opt.programs) build_programs(P, opt.threads);
   if (with_work) build_item_deps(P, ranges, opt.hot_fraction);
-  if (with_work && opt.programs) build_flow(P);
+  if (with_work && opt.programs) build_flow(P, u, opt.flow_merge_rows);
   if (with_work && opt.programs) build_units(P, ranges, opt.unit_min_rows, opt.unit_smem_cap);
 
   // successors + in-degrees (edge multiplicity preserved)

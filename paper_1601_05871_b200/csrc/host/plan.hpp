@@ -56,6 +56,7 @@ struct PlanOptions {
   double dep_wide_cost = 64.0;  // Chol/Trsm go multi-CTA only above this cost per level
   double hot_fraction = 0.6;    // rows with height >= this fraction of the max are "hot"
   bool programs = true;    // precompute per-row update programs (slot_rec / upd)
+  bool flow_merge_rows = true;  // mode 5: one unit per matrix row when its U row has <= 32 entries
   int unit_min_rows = 64;  // mode 6: diagonal blocks above this many rows become units
   std::int64_t unit_smem_cap = 72 * 1024;  // ... if their values fit in this many bytes
   int threads = 0;         // host threads for the program build (0 = all)

@@ -356,6 +356,7 @@ def test_c5_batch_breakdown_is_per_member(T, oracle):
 def test_block_units(T, golden, oracle, name, min_rows, monkeypatch):
     # mode 6: diagonal blocks above min_rows run as CTA units (shared-memory values)
     monkeypatch.setenv("TCG_UNIT_MIN_ROWS", str(min_rows))
+    monkeypatch.setenv("TCG_FLOW_MERGE_ROWS", "0")  # units are built from diagonal-block rows
     _, an = analyzed(name)
     plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
     if plan.stats().unit_count == 0:
@@ -368,12 +369,13 @@ def test_block_units(T, golden, oracle, name, min_rows, monkeypatch):
 def test_block_units_breakdown(T):
     a, fp, rl = small(T, 4, sym([(0, 0, 1.0), (1, 1, 1.0), (2, 2, 1.0), (2, 3, 4.0), (3, 3, 1.0)]),
                       bounds=[0, 4])
-    import os
     os.environ["TCG_UNIT_MIN_ROWS"] = "1"
+    os.environ["TCG_FLOW_MERGE_ROWS"] = "0"
     try:
         plan = T.Plan(a, fp, rl)
     finally:
         del os.environ["TCG_UNIT_MIN_ROWS"]
+        del os.environ["TCG_FLOW_MERGE_ROWS"]
     assert plan.stats().unit_count == 1
     fz = T.GpuFactorizer(plan, T.GpuOptions(mode=6))
     try:

@@ -192,24 +192,36 @@ def replay_flow(t, order=None):
     return out
 
 
+@pytest.mark.parametrize("merge", [True, False])
 @pytest.mark.parametrize("name", ["c1", "rand_spd_200", "grid20_k2_leaf4", "elast6_k1"])
-def test_flow_schedule_partitions_u_and_replays_bitwise(name, oracle):
-    # mode 5: the Chol/Trsm rows own every coordinate once; merged programs
-    # keep the per-coordinate product order, so replays equal factor_serial
-    plan = planned(name)
+def test_flow_schedule_partitions_u_and_replays_bitwise(T, name, merge, oracle, monkeypatch):
+    # mode 5: the rows of the schedule own every coordinate once -- whole
+    # matrix rows of <= 32 entries (merge) or one Chol/Trsm item each; merged
+    # programs keep the per-coordinate product order, so replays equal
+    # factor_serial
+    monkeypatch.setenv("TCG_FLOW_MERGE_ROWS", "1" if merge else "0")
+    _, an = analyzed(name)
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
     t = plan.tables()
     s = plan.stats()
-    assert s.flow_rows == len(t["flow_rec"]) == int((t["row_rec"][:, 4] <= 1).sum())
+    fin = int((t["row_rec"][:, 4] <= 1).sum())
+    rec = t["flow_rec"]
+    L = rec[:, 1] & ((1 << 30) - 1)
+    assert s.flow_rows == len(rec) and int(L.sum()) == len(t["values"])  # a partition of U
+    u = an.pattern.pattern
+    if merge:
+        long_rows = int((np.diff(u.row_ptr) > 32).sum())
+        assert s.flow_rows <= fin and (long_rows > 0 or s.flow_rows == u.nrows)
+    else:
+        assert s.flow_rows == fin
+        assert np.array_equal(np.sort(t["flow_item"]), np.flatnonzero(t["row_rec"][:, 4] <= 1))
     assert len(t["flow_upd"]) == len(t["upd"])  # every product folded in exactly once
     assert s.flow_depth <= s.item_depth
-    items = t["flow_item"]
-    assert np.array_equal(np.sort(items), np.flatnonzero(t["row_rec"][:, 4] <= 1))
-    _, an = analyzed(name)
     ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
     assert bitwise_equal(replay_flow(t), ref)
     # any order that respects "reads only written values" gives the same bits:
-    # item order (generation order) is one
-    assert bitwise_equal(replay_flow(t, np.argsort(items, kind="stable")), ref)
+    # matrix-row order is one
+    assert bitwise_equal(replay_flow(t, np.lexsort(((rec[:, 1] >> 30) & 1, rec[:, 3]))), ref)
 
 
 LOCAL = 0x80000000
@@ -288,6 +300,7 @@ def replay_units(t):
                                            ("elast6_k1", 32), ("rand_spd_200", 4)])
 def test_unit_schedule_replays_bitwise(T, name, min_rows, oracle, monkeypatch):
     monkeypatch.setenv("TCG_UNIT_MIN_ROWS", str(min_rows))
+    monkeypatch.setenv("TCG_FLOW_MERGE_ROWS", "0")  # units are built from diagonal-block rows
     _, an = analyzed(name)
     plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
     t = plan.tables()
