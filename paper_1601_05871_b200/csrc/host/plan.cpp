@@ -444,12 +444,14 @@ void build_flow(Plan& P, const CsrMatrix& u, bool merge_rows) {
     }
   for (std::size_t x = 0; x < N; ++x)
     if (fin_item[x] < 0) throw std::logic_error("flow: coordinate without a finaliser");
-  // The rows the schedule runs ("units"). With merge_rows a matrix row whose
-  // whole U row fits one warp pass (<= 32 entries) is one unit: its Chol and
-  // Trsm items share the divisor U(t,t) and nearly all their sources (every
-  // coordinate (t,c) takes U(r,t)*U(r,c) over the same rows r), so one row
-  // pays the per-row cost once. Longer rows keep one unit per item, which
-  // run on different warps. Units are in (row, Chol first) order, which is
+  // The rows the schedule runs ("units"). The Chol and Trsm items of a
+  // matrix row share the divisor U(t,t) and nearly all their sources (every
+  // coordinate (t,c) takes U(r,t)*U(r,c) over the same rows r), so with
+  // merge_rows a U row of at most 32 entries is one unit (one warp pass, the
+  // per-row cost paid once); a longer row keeps its diagonal-block slice (the
+  // Chol item, which the next rows of the block chain read) and cuts the rest
+  // into warp-wide chunks that divide by U(t,t). Without merge_rows, one unit
+  // per Chol/Trsm item. Units are in (row, Chol first) order, which is
   // topological: every operand comes from a row above.
   struct Unit {
     std::int32_t tb, L, dpos, kind, t, item;
@@ -463,8 +465,15 @@ void build_flow(Plan& P, const CsrMatrix& u, bool merge_rows) {
     const std::int32_t ck = chol_of_row[t];
     if (ck < 0) throw std::logic_error("flow: row without a Chol item");
     const auto rb = static_cast<std::int32_t>(u.row_begin(t)), re = static_cast<std::int32_t>(u.row_end(t));
-    if (merge_rows && re - rb <= 32) {
+    if (merge_rows && re - rb <= 32) {  // the whole row in one warp pass
       units.push_back({rb, re - rb, rb, kChol, static_cast<std::int32_t>(t), ck});
+      continue;
+    }
+    if (merge_rows) {  // the diagonal-block slice, then the rest of the row in warp-wide chunks
+      units.push_back({R(ck, 0), R(ck, 1) - R(ck, 0), R(ck, 2), kChol, static_cast<std::int32_t>(t), ck});
+      for (std::int32_t c0 = R(ck, 1); c0 < re; c0 += 32)
+        units.push_back({c0, std::min(re - c0, 32), R(ck, 2), kTrsm, static_cast<std::int32_t>(t),
+                         fin_item[static_cast<std::size_t>(c0)]});
       continue;
     }
     units.push_back({R(ck, 0), R(ck, 1) - R(ck, 0), R(ck, 2), kChol, static_cast<std::int32_t>(t), ck});

@@ -209,9 +209,9 @@ def test_flow_schedule_partitions_u_and_replays_bitwise(T, name, merge, oracle, 
     L = rec[:, 1] & ((1 << 30) - 1)
     assert s.flow_rows == len(rec) and int(L.sum()) == len(t["values"])  # a partition of U
     u = an.pattern.pattern
-    if merge:
-        long_rows = int((np.diff(u.row_ptr) > 32).sum())
-        assert s.flow_rows <= fin and (long_rows > 0 or s.flow_rows == u.nrows)
+    if merge:  # rows of <= 32 entries whole; longer ones: the diagonal-block slice + chunks of <= 32
+        assert s.flow_rows <= fin
+        assert int((np.diff(u.row_ptr) <= 32).sum()) <= s.flow_rows
     else:
         assert s.flow_rows == fin
         assert np.array_equal(np.sort(t["flow_item"]), np.flatnonzero(t["row_rec"][:, 4] <= 1))
