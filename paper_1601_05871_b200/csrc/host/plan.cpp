@@ -562,6 +562,12 @@ void build_flow(Plan& P, const CsrMatrix& u, bool merge_rows) {
     o[3] = un.t;
     P.flow_item[q] = un.item;
   }
+  // the schedule position writing each coordinate (a long item's chunks share
+  // the item, so the item alone does not name the writing row)
+  std::vector<std::int32_t> pos_of_unit(U);
+  for (std::size_t q = 0; q < U; ++q) pos_of_unit[static_cast<std::size_t>(order[q])] = static_cast<std::int32_t>(q);
+  P.flow_pos.assign(N, -1);
+  for (std::size_t x = 0; x < N; ++x) P.flow_pos[x] = pos_of_unit[static_cast<std::size_t>(unit_of[x])];
   const std::int64_t nfin = static_cast<std::int64_t>(U);
   P.stats.flow_rows = nfin;
   P.stats.flow_depth = depth;
@@ -584,15 +590,12 @@ void build_flow(Plan& P, const CsrMatrix& u, bool merge_rows) {
 void build_units(Plan& P, const RangeList& ranges, std::int32_t min_rows, std::int64_t smem_cap) {
   const std::size_t R = P.flow_item.size();
   const std::size_t N = static_cast<std::size_t>(P.nnz);
-  const std::size_t I = P.item_rec.size() / kItemWords;
   auto F = [&](std::size_t q, int w) { return P.flow_rec[q * kFlowWords + w]; };
   auto len = [&](std::size_t q) { return F(q, 1) & ((1 << kFlowKindShift) - 1); };
   auto kind = [&](std::size_t q) { return static_cast<std::int32_t>(static_cast<std::uint32_t>(F(q, 1)) >> kFlowKindShift); };
   std::vector<std::int32_t> range_of(static_cast<std::size_t>(P.n));
   for (index_t r = 0; r < ranges.count(); ++r)
     for (index_t c = ranges.ranges[r].begin; c < ranges.ranges[r].end; ++c) range_of[c] = r;
-  std::vector<std::int32_t> pos_of_item(I, -1);
-  for (std::size_t q = 0; q < R; ++q) pos_of_item[P.flow_item[q]] = static_cast<std::int32_t>(q);
   // candidate units: Chol rows of large diagonal blocks whose values fit
   // (only blocks whose Chol rows are the diagonal-block slices: a whole
   // matrix row run as one flow row, build_flow merge_rows, reaches into
@@ -627,7 +630,7 @@ void build_units(Plan& P, const RangeList& ranges, std::int32_t min_rows, std::i
   // programs with intra-unit operands rewritten
   P.m6_slot = P.flow_slot;
   P.m6_upd = P.flow_upd;
-  auto unit_of_value = [&](std::int32_t pos) { return unit_of_pos[pos_of_item[P.flow_owner[pos]]]; };
+  auto unit_of_value = [&](std::int32_t pos) { return unit_of_pos[P.flow_pos[pos]]; };
   for (std::size_t q = 0; q < R; ++q) {
     const std::int32_t u = unit_of_pos[q];
     if (u < 0) continue;
@@ -655,7 +658,7 @@ void build_units(Plan& P, const RangeList& ranges, std::int32_t min_rows, std::i
     const std::int32_t me = node_of_pos[q];
     std::int32_t lv = 1;
     auto src = [&](std::int32_t pos) {
-      const std::int32_t sq = pos_of_item[P.flow_owner[pos]];
+      const std::int32_t sq = P.flow_pos[pos];
       const std::int32_t sn = node_of_pos[sq];
       if (sn == me) lv = std::max(lv, ulevel[sq] + 1);
       else deps[me].push_back(sn);

@@ -131,6 +131,7 @@ struct Plan {
   std::vector<std::int32_t> flow_slot;  // per coordinate of U: {u_b, u_e, m0, o0}
   std::vector<std::int32_t> flow_upd;   // (m, o) pairs
   std::vector<std::int32_t> flow_owner; // per coordinate of U: the item writing it
+  std::vector<std::int32_t> flow_pos;   // per coordinate of U: the schedule position writing it
   // mode 6 (block units): rows outside units in schedule order; units with
   // their rows by intra-unit level; programs with local operands rewritten
   std::vector<std::int32_t> m6_row_rec;   // kFlowWords per row
