@@ -456,6 +456,145 @@ def run_sharded(args):
     dist.destroy_process_group()
 
 
+def run_symbolic(args):
+    """--path symbolic: the level-k fill pattern on the device (tcg_sym_*, the
+    reference's levelk_pattern_bfs, symbolic.hpp:57-120)
+    on the config's PᵀAP. A step = count pass + scan + fill pass; value =
+    nnz_u / device time; e2e = upload of PᵀAP's pattern + the step + download
+    of the pattern through the C ABI from host buffers. Replicas for N > 1."""
+    import numpy as np
+    import torch
+
+    import paper_1601_05871_b200 as T
+
+    rank, local_rank, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    name = "c5" if args.config in ("c5", "c5b") else args.config
+    a, level = T.config_matrix(name)
+    an = T.analyze(a, level=level)
+    ap_ = an.a_permuted
+    n, nnz_a = ap_.nrows, ap_.nnz()
+    g = T.GpuSymbolic(ap_, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(dev).__enter__()
+    for _ in range(args.warmup):
+        g.levelk(level)
+    dev_ms = []
+    barrier()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        fp, st = g.levelk(level)
+        dev_ms.append(st.device_ms)
+    barrier()
+    step_ms = statistics.mean(dev_ms)
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        g.upload(ap_)                         # H2D: PᵀAP's row_ptr + col_idx
+        fp_e, _ = g.levelk(level)             # D2H: U's row_ptr + col_idx
+        if i >= args.warmup:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    clocks.__exit__(None, None, None)
+    e2e = statistics.mean(e2e_ms)
+    g.close()
+    if world > 1:
+        step_ms, e2e = max_over(step_ms, dev), max_over(e2e, dev)
+    same_e2e = np.array_equal(fp_e.pattern.col_idx, fp.pattern.col_idx)
+    u = fp.pattern
+    nnz_u = u.nnz()
+    parity = None
+    if rank == 0:
+        same = np.array_equal(u.row_ptr, an.pattern.pattern.row_ptr) and \
+            np.array_equal(u.col_idx, an.pattern.pattern.col_idx)
+        parity = ("bit-exact vs host levelk (pinned to the reference's golden hashes)"
+                  if same and same_e2e else "MISMATCH")
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from checkers import Reference, reference_available
+        if reference_available():
+            R = Reference()
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                R.levelk(ap_, level)
+                ts.append(time.perf_counter() - t0)
+            cpu = {"value": nnz_u / statistics.median(ts), "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": "3 x levelk_pattern_bfs on the full PaP (reference, oracle/_ref), median"}
+    peak, peak_kind = measured_peak()
+    bytes_alg = 8 * (n + 1) + 4 * nnz_a + 8 * (n + 1) + 4 * nnz_u
+    achieved = bytes_alg / (step_ms / 1e3) / 1e9
+    line = {
+        "metric": "levelk_pattern_nnz_per_s", "value": world * nnz_u / (step_ms / 1e3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (seeded generator, SURVEY.md Appendix B)",
+        "config": {"workload": WORKLOADS[args.config] + ": level-k symbolic of PaP", "path": "symbolic",
+                   "n": n, "nnz_a": nnz_a, "nnz_u": nnz_u, "level": level, "slow_rows": st.slow_rows,
+                   "grid_ctas": st.grid_ctas,
+                   "l2": "flushed before every step (256 MiB write)", "parity": parity},
+        "e2e": {"value": world * nnz_u / (e2e / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": 8 * (n + 1) + 4 * nnz_a, "d2h_bytes_per_step": 8 * (n + 1) + 4 * nnz_u,
+                "ms_per_step": e2e},
+        "gpu_launches": st.kernel_launches * args.steps,
+        "launches_per_step": {"levelk_fast count": 1, "device scan": 1, "levelk_fast fill": 1},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_alg,
+                     "note": "whole symbolic step (3 launches): PaP pattern read once, U pattern written once"},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_reference_symbolic(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from checkers import Reference, reference_available
+
+    import paper_1601_05871_b200 as T
+    if not reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref was not built"}))
+        return
+    name = "c5" if args.config in ("c5", "c5b") else args.config
+    a, level = T.config_matrix(name)
+    an = T.analyze(a, level=level)
+    R = Reference()
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        ptr, _ = R.levelk(an.a_permuted, level)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    nnz_u = int(ptr[-1])
+    t = statistics.mean(times)
+    print(json.dumps({
+        "impl": "reference", "metric": "levelk_pattern_nnz_per_s", "value": nnz_u / t, "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.config] + ": level-k symbolic of PaP", "path": "symbolic",
+                   "nnz_u": nnz_u},
+        "cpu_baseline": {"value": nnz_u / t, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": f"{args.steps} x levelk_pattern_bfs (sequential in the reference)"},
+        "e2e": {"value": nnz_u / t, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
 def max_over(x, dev):
     import torch
     import torch.distributed as dist
@@ -473,11 +612,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", type=int, default=0, help="0 auto, 1/2 task DAG, 3 row DAG")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--path", default="factor", choices=["factor", "symbolic"],
+                    help="factor: the numeric factorization (headline); symbolic: level-k pattern on the device")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warm-up raised to 3 (timing rule)")
         args.warmup = 3
-    if args.impl == "reference":
+    if args.path == "symbolic":
+        run_reference_symbolic(args) if args.impl == "reference" else run_symbolic(args)
+    elif args.impl == "reference":
         run_reference(args)
     elif args.config == "c6" and dist_env()[2] > 1:
         run_sharded(args)

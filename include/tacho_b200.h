@@ -260,6 +260,32 @@ tcg_status tcg_ipc_open(tcg_ctx* ctx, const void* handle, int64_t offset, uint64
 /* Bytes of the device arena. */
 int64_t tcg_arena_bytes(const tcg_ctx* ctx);
 
+/* ---- level-k symbolic on the device ------------------------------------- */
+/* The fill pattern of U, levelk_pattern_bfs (reference symbolic.hpp:57-120), one warp per
+ * source row: same FillPattern.pattern arrays as the reference
+ * (row i = {i} then its targets ascending), bit-exact. Separate handle: it needs no plan. */
+typedef struct tcg_sym tcg_sym;
+typedef struct {
+  double device_ms;          /* count + scan + fill, CUDA events on the handle's stream */
+  double host_ms;            /* wall time of tcg_sym_levelk (includes the nnz_u readback) */
+  int64_t nnz_u;             /* FillPattern.pattern.nnz() */
+  int64_t nnz_triu_input;    /* FillPattern.nnz_triu_input (count_upper, csr_matrix.hpp:219-225) */
+  int64_t slow_rows;         /* rows whose search outgrew shared memory (global-memory path) */
+  int64_t tier2_rows;        /* rows that outgrew the 512-slot tables (then 2,048 slots) */
+  int32_t kernel_launches;
+  int32_t grid_ctas;
+} tcg_sym_stats;
+enum { TCG_SYM_ALL_SLOW = 1 };  /* tcg_sym_levelk flag: every row on the global-memory path */
+tcg_status tcg_sym_create(int device, tcg_sym** out);
+void tcg_sym_destroy(tcg_sym* s);
+const char* tcg_sym_error(const tcg_sym* s);
+/* a_permuted: PᵀAP's pattern (values unused); square, row_ptr 0..nnz, columns in range. */
+tcg_status tcg_sym_upload(tcg_sym* s, const tcg_csr_view* a_permuted);
+tcg_status tcg_sym_levelk(tcg_sym* s, int32_t level, int32_t flags, tcg_sym_stats* stats);
+int64_t tcg_sym_nnz(const tcg_sym* s); /* nnz of the last pattern, -1 before the first */
+/* row_ptr: n + 1, col_idx: tcg_sym_nnz entries (host). */
+tcg_status tcg_sym_download(tcg_sym* s, int64_t* row_ptr, int32_t* col_idx);
+
 /* ---- host input side (analysis) ---------------------------------------- */
 /* Own implementations of the reference's analysis chain (pipeline.hpp:35-55),
  * kept bit-exact with it; they produce the inputs of tcg_plan_build. */

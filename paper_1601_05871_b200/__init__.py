@@ -14,6 +14,7 @@ from .core import (  # noqa: F401
     FillPattern,
     GpuFactorizer,
     GpuOptions,
+    GpuSymbolic,
     KIND_NAMES,
     Plan,
     RangeList,
@@ -26,4 +27,5 @@ from .core import (  # noqa: F401
     generate,
     init_factor_values,
     levelk_pattern,
+    levelk_pattern_gpu,
 )

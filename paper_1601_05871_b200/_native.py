@@ -155,6 +155,21 @@ class PlanStats(C.Structure):
     ]
 
 
+class SymStats(C.Structure):
+    _fields_ = [
+        ("device_ms", C.c_double),
+        ("host_ms", C.c_double),
+        ("nnz_u", C.c_int64),
+        ("nnz_triu_input", C.c_int64),
+        ("slow_rows", C.c_int64),
+        ("tier2_rows", C.c_int64),
+        ("kernel_launches", C.c_int32),
+        ("grid_ctas", C.c_int32),
+    ]
+
+
+TCG_SYM_ALL_SLOW = 1
+
 # (name, restype, argtypes) for every symbol declared in include/tacho_b200.h
 SIGNATURES = [
     ("tcg_plan_build", C.c_int, [C.POINTER(CsrView), C.POINTER(CsrView), C.c_int32, i32p, C.POINTER(C.c_void_p)]),
@@ -189,6 +204,13 @@ SIGNATURES = [
     ("tcg_factor_phase", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     ("tcg_ipc_values_handle", C.c_int, [C.c_void_p, C.c_void_p, i64p]),
     ("tcg_ipc_open", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_uint64)]),
+    ("tcg_sym_create", C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    ("tcg_sym_destroy", None, [C.c_void_p]),
+    ("tcg_sym_error", C.c_char_p, [C.c_void_p]),
+    ("tcg_sym_upload", C.c_int, [C.c_void_p, C.POINTER(CsrView)]),
+    ("tcg_sym_levelk", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(SymStats)]),
+    ("tcg_sym_nnz", C.c_int64, [C.c_void_p]),
+    ("tcg_sym_download", C.c_int, [C.c_void_p, i64p, i32p]),
     ("tch_generate", C.c_void_p, [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]),
     ("tch_matrix_from_csr", C.c_void_p, [C.POINTER(CsrView)]),
     ("tch_matrix_free", None, [C.c_void_p]),

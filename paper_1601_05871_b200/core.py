@@ -298,6 +298,78 @@ def levelk_pattern(a_permuted: CsrMatrix, level: int, threads: int = 0) -> FillP
         lib.tch_matrix_free(m)
 
 
+@dataclass
+class SymbolicStats:
+    device_ms: float
+    host_ms: float
+    nnz_u: int
+    nnz_triu_input: int
+    slow_rows: int
+    tier2_rows: int
+    kernel_launches: int
+    grid_ctas: int
+
+
+class GpuSymbolic:
+    """levelk_pattern_bfs (reference symbolic.hpp:57-120) on the device, one
+    warp per source row: upload PᵀAP's pattern once, compute the level-k
+    pattern for any k, download it as the reference's FillPattern."""
+
+    def __init__(self, a_permuted: CsrMatrix, device: int = 0):
+        self._lib = _lib()
+        h = C.c_void_p()
+        if self._lib.tcg_sym_create(device, C.byref(h)) != N.TCG_OK:
+            raise DeviceError("tcg_sym_create failed (no CUDA device?)")
+        self.h = h
+        self.upload(a_permuted)
+
+    def upload(self, a_permuted: CsrMatrix):
+        """Copy PᵀAP's pattern to the device (buffers are reused when large enough)."""
+        self.a = a_permuted
+        self._check(self._lib.tcg_sym_upload(self.h, C.byref(a_permuted.view())))
+
+    def _check(self, st):
+        if st == N.TCG_OK:
+            return
+        msg = self._lib.tcg_sym_error(self.h).decode()
+        if st == N.TCG_INVALID:
+            raise ValueError(msg)
+        raise DeviceError(msg)
+
+    def levelk(self, level: int, all_slow: bool = False) -> Tuple[FillPattern, SymbolicStats]:
+        s = N.SymStats()
+        self._check(self._lib.tcg_sym_levelk(self.h, level, N.TCG_SYM_ALL_SLOW if all_slow else 0, C.byref(s)))
+        n = self.a.nrows
+        rp = np.zeros(n + 1, np.int64)
+        ci = np.zeros(max(int(s.nnz_u), 1), np.int32)
+        self._check(self._lib.tcg_sym_download(self.h, rp.ctypes.data_as(N.i64p), ci.ctypes.data_as(N.i32p)))
+        pat = CsrMatrix(n, n, rp, ci[:int(s.nnz_u)].copy(), np.ones(int(s.nnz_u)))
+        st = SymbolicStats(s.device_ms, s.host_ms, int(s.nnz_u), int(s.nnz_triu_input), int(s.slow_rows), int(s.tier2_rows),
+                           int(s.kernel_launches), int(s.grid_ctas))
+        return FillPattern(pat, level, int(s.nnz_triu_input)), st
+
+    def close(self):
+        if self.h:
+            self._lib.tcg_sym_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def levelk_pattern_gpu(a_permuted: CsrMatrix, level: int, device: int = 0) -> FillPattern:
+    """The level-k fill pattern computed on the GPU; same arrays as
+    levelk_pattern / the reference's levelk_pattern_bfs."""
+    g = GpuSymbolic(a_permuted, device)
+    try:
+        return g.levelk(level)[0]
+    finally:
+        g.close()
+
+
 def init_factor_values(a_permuted: CsrMatrix, fp: FillPattern) -> np.ndarray:
     lib = _lib()
     out = np.zeros(fp.pattern.nnz(), dtype=np.float64)

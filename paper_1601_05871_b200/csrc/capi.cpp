@@ -33,7 +33,7 @@ tcb::CsrMatrix csr_from_view(const tcg_csr_view* v, bool need_values) {
   }
   if (v->values && v->nnz > 0)
     m.values.assign(v->values, v->values + v->nnz);
-  else if (need_values)
+  else if (need_values && v->nnz > 0)
     throw std::invalid_argument("csr view: values required");
   else
     m.values.assign(static_cast<std::size_t>(v->nnz), 1.0);

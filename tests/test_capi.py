@@ -36,7 +36,8 @@ def test_struct_layouts_match_the_header():
     text = open(os.path.join(ROOT, "include", "tacho_b200.h")).read()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     for cname, py in (("tcg_problem", N.Problem), ("tcg_options", N.Options),
-                      ("tcg_stats", N.Stats), ("tcg_plan_stats", N.PlanStats)):
+                      ("tcg_stats", N.Stats), ("tcg_plan_stats", N.PlanStats),
+                      ("tcg_sym_stats", N.SymStats)):
         body = re.search(r"typedef struct \{([^{}]*)\}\s*" + cname + ";", text, flags=re.S).group(1)
         decls = [d for d in body.split(";") if d.strip()]
         nfields = sum(len(d.split(",")) for d in decls)
@@ -51,6 +52,9 @@ def test_device_calls_fail_cleanly_without_a_gpu():
     lib = N.load()
     h = C.c_void_p()
     st = lib.tcg_create(0, C.byref(h))
+    assert st == N.TCG_CUDA
+    assert not h.value
+    st = lib.tcg_sym_create(0, C.byref(h))
     assert st == N.TCG_CUDA
     assert not h.value
 
