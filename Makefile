@@ -19,17 +19,18 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas
 CXXFLAGS := -O2 -std=c++17 -fPIC -pthread -Wall -Wextra -ffp-contract=off
 
 HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generators.cpp \
-             $(SRC)/host/plan.cpp $(SRC)/capi.cpp $(SRC)/symbolic_capi.cpp
+             $(SRC)/host/plan.cpp $(SRC)/capi.cpp $(SRC)/symbolic_capi.cpp $(SRC)/solve_capi.cpp
 HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
 DEV_OBJS := $(OBJ)/device/factor_kernel.o $(OBJ)/device/row_kernel.o $(OBJ)/device/static_kernel.o \
-            $(OBJ)/device/flow_kernel.o $(OBJ)/device/symbolic_kernel.o
+            $(OBJ)/device/flow_kernel.o $(OBJ)/device/symbolic_kernel.o \
+            $(OBJ)/device/solve_kernel.o
 
 .PHONY: all lib oracle ref clean
 all: lib oracle
 
 lib: $(OUT)/libtacho_b200.so
 
-$(OBJ)/%.o: $(SRC)/%.cpp $(wildcard $(SRC)/host/*.hpp) $(SRC)/device/device_api.hpp $(SRC)/device/symbolic_api.hpp \
+$(OBJ)/%.o: $(SRC)/%.cpp $(wildcard $(SRC)/host/*.hpp) $(SRC)/device/device_api.hpp $(SRC)/device/symbolic_api.hpp $(SRC)/device/solve_api.hpp \
             $(SRC)/device/factor_kernel.cuh include/tacho_b200.h
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -I/usr/local/cuda/include -c $< -o $@
@@ -67,3 +68,7 @@ $(OBJ)/device/flow_kernel.o: $(SRC)/device/flow_kernel.cu $(SRC)/device/factor_k
 $(OBJ)/device/symbolic_kernel.o: $(SRC)/device/symbolic_kernel.cu $(SRC)/device/symbolic_api.hpp
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_symbolic_kernel.txt || (cat build/ptxas_symbolic_kernel.txt; false)
+
+$(OBJ)/device/solve_kernel.o: $(SRC)/device/solve_kernel.cu $(SRC)/device/solve_api.hpp $(SRC)/device/sync.cuh
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_solve_kernel.txt || (cat build/ptxas_solve_kernel.txt; false)

@@ -562,6 +562,114 @@ def run_symbolic(args):
         torch.distributed.destroy_process_group()
 
 
+def run_solve(args):
+    """--path solve: the IC(k) preconditioner apply z = (UᵀU)⁻¹ r with the GPU
+    factor (tcg_solve_*): forward Uᵀ y = r then
+    backward U z = y in one launch. A step = one apply with r resident in HBM;
+    e2e = the apply through the C ABI from host buffers (H2D r, D2H z)."""
+    import numpy as np
+    import torch
+
+    import paper_1601_05871_b200 as T
+
+    rank, local_rank, world = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = local_rank
+    a, an, plan, t_an = build_problem(args.config)
+    u = an.pattern.pattern
+    n, nnz = u.nrows, u.nnz()
+    fz = T.GpuFactorizer(plan, T.GpuOptions(device=dev, timeout_s=60))
+    fz.factor()
+    s = T.GpuTriSolve(fz)
+    r = np.random.default_rng(11).standard_normal(n)
+    rd = torch.from_numpy(r).to(f"cuda:{dev}")
+    zd = torch.empty_like(rd)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{dev}")
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(dev).__enter__()
+    for _ in range(args.warmup):
+        s.apply_device_ptr(rd.data_ptr(), zd.data_ptr(), 3)
+    dev_ms = []
+    barrier()
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        st = s.apply_device_ptr(rd.data_ptr(), zd.data_ptr(), 3)
+        dev_ms.append(st.device_ms)
+    barrier()
+    step_ms = statistics.mean(dev_ms)
+    host_r = torch.from_numpy(r).pin_memory()
+    host_z = torch.empty(n, dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        s.apply_host_ptr(host_r.data_ptr(), host_z.data_ptr(), 3)
+        if i >= args.warmup:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    clocks.__exit__(None, None, None)
+    e2e = statistics.mean(e2e_ms)
+    if world > 1:
+        step_ms, e2e = max_over(step_ms, dev), max_over(e2e, dev)
+    parity, cpu = None, None
+    if rank == 0:
+        from checkers import Oracle
+        O = Oracle()
+        vals = fz.download()
+        t0 = time.perf_counter()
+        ref = O.trisolve(u, vals, r, 3)
+        t_cpu = time.perf_counter() - t0
+        got = host_z.numpy()
+        parity = "bitwise vs oracle orc_trisolve" if np.array_equal(got.view(np.int64), ref.view(np.int64)) \
+            else f"max_rel={float(np.max(np.abs(got - ref) / (np.abs(ref) + 1e-300))):.3e}"
+        if world == 1 and not args.no_cpu:
+            ts = [t_cpu]
+            for _ in range(2):
+                t0 = time.perf_counter()
+                O.trisolve(u, vals, r, 3)
+                ts.append(time.perf_counter() - t0)
+            cpu = {"value": nnz / statistics.median(ts), "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": "3 x orc_trisolve (oracle's sequential forward + backward substitution; the "
+                             "reference has no solve), median"}
+    s.close()
+    fz.close()
+    peak, peak_kind = measured_peak()
+    bytes_alg = 2 * 12 * nnz + 32 * n
+    achieved = bytes_alg / (step_ms / 1e3) / 1e9
+    line = {
+        "metric": "ic_apply_factor_nnz_per_s", "value": world * nnz / (step_ms / 1e3), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md Appendix B); r ~ N(0,1) seed 11",
+        "config": {"workload": WORKLOADS[args.config] + ": preconditioner apply (UᵀU)^-1 r", "path": "solve",
+                   "n": n, "nnz_u": nnz, "depth_forward": st.depth_forward, "depth_backward": st.depth_backward,
+                   "grid_ctas": st.grid_ctas, "l2": "flushed before every step (256 MiB write)",
+                   "parity_vs_oracle": parity},
+        "e2e": {"value": world * nnz / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+                "d2h_bytes_per_step": 8 * n, "ms_per_step": e2e},
+        "gpu_launches": st.kernel_launches * args.steps,
+        "launches_per_step": {"trisolve_flow": 1, "memset (marker)": 2, "copy (result)": 1},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_alg,
+                     "note": "U values + an int32 index per entry, once per direction; 4 vectors of n"},
+        "cpu_baseline": cpu,
+        "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def run_reference_symbolic(args):
     rank, _, world = dist_env()
     if rank != 0:
@@ -612,14 +720,22 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", type=int, default=0, help="0 auto, 1/2 task DAG, 3 row DAG")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--path", default="factor", choices=["factor", "symbolic"],
-                    help="factor: the numeric factorization (headline); symbolic: level-k pattern on the device")
+    ap.add_argument("--path", default="factor", choices=["factor", "symbolic", "solve"],
+                    help="factor: the numeric factorization (headline); symbolic: level-k pattern on the "
+                         "device; solve: the preconditioner apply with the factor")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warm-up raised to 3 (timing rule)")
         args.warmup = 3
     if args.path == "symbolic":
         run_reference_symbolic(args) if args.impl == "reference" else run_symbolic(args)
+    elif args.path == "solve":
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "path": "solve",
+                              "unavailable": "the reference has no triangular solve (SPEC.md:477); "
+                                             "bench --path solve reports the oracle port as cpu_baseline"}))
+        else:
+            run_solve(args)
     elif args.impl == "reference":
         run_reference(args)
     elif args.config == "c6" and dist_env()[2] > 1:

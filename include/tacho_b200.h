@@ -286,6 +286,37 @@ int64_t tcg_sym_nnz(const tcg_sym* s); /* nnz of the last pattern, -1 before the
 /* row_ptr: n + 1, col_idx: tcg_sym_nnz entries (host). */
 tcg_status tcg_sym_download(tcg_sym* s, int64_t* row_ptr, int32_t* col_idx);
 
+/* ---- triangular solves with the factor ----------------------------------- */
+/* The preconditioner apply of IC(k)-preconditioned CG: with the
+ * factor U held by a context (after tcg_factor), forward Uᵀ y = b and backward U x = y on
+ * the device, one warp per unknown in a static level order, operands polled in place
+ * (no per-level launches). The reference has no solve; the order of
+ * operations is fixed: per unknown, products in ascending source index subtracted in that
+ * order, then one division (oracle.c orc_trisolve), so results are reproducible bitwise. */
+typedef struct tcg_solve tcg_solve;
+typedef struct {
+  double device_ms;          /* marker reset + solve kernel + result copy, CUDA events */
+  int32_t depth_forward;     /* longest dependence chain of Uᵀ y = b, in unknowns */
+  int32_t depth_backward;    /* ... of U x = y */
+  int32_t grid_ctas;
+  int32_t kernel_launches;
+} tcg_solve_stats;
+enum { TCG_SOLVE_FORWARD = 1, TCG_SOLVE_BACKWARD = 2, TCG_SOLVE_BOTH = 3 };
+/* u_pattern: the factor's pattern (FillPattern.pattern of the uploaded problem); the values
+ * are read from the context at every apply, so a refactorization is picked up. */
+tcg_status tcg_solve_create(tcg_ctx* ctx, const tcg_csr_view* u_pattern, tcg_solve** out);
+void tcg_solve_destroy(tcg_solve* s);
+const char* tcg_solve_error(const tcg_solve* s);
+/* host vectors of n doubles (b and x may alias); which: TCG_SOLVE_* */
+tcg_status tcg_solve_apply(tcg_solve* s, const double* b, double* x, int32_t which, tcg_solve_stats* stats);
+/* device vectors (b_dev and x_dev may alias), on the context's stream */
+tcg_status tcg_solve_apply_device(tcg_solve* s, const double* b_dev, double* x_dev, int32_t which,
+                                  tcg_solve_stats* stats);
+/* With TCG_SOLVE_TRACE=1 in the environment: per schedule position (2 n) the globaltimer
+ * stamps {start, operands final, end} of the last apply, and (recs != NULL) the position
+ * records {entry begin, length | backward << 31, diagonal position, row} (16 bytes each). */
+tcg_status tcg_solve_trace(tcg_solve* s, uint64_t* stamps, void* recs);
+
 /* ---- host input side (analysis) ---------------------------------------- */
 /* Own implementations of the reference's analysis chain (pipeline.hpp:35-55),
  * kept bit-exact with it; they produce the inputs of tcg_plan_build. */

@@ -470,3 +470,40 @@ void orc_levelk_dense(int32_t n, const int64_t* ap, const int32_t* ac, int32_t k
   free(lev);
   free(act);
 }
+
+/* Preconditioner apply (see oracle.h): forward then backward substitution in
+ * a fixed sequential order, every product and difference rounded on its own. */
+int orc_trisolve(int32_t n, const int64_t* up, const int32_t* uc, const double* uv,
+                 const double* b, int32_t which, double* x) {
+  double* t = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  if (!t) return 3;
+  for (int32_t i = 0; i < n; ++i) t[i] = b[i];
+  for (int32_t i = 0; i < n; ++i)
+    if (up[i] >= up[i + 1] || uc[up[i]] != i || uv[up[i]] == 0.0) {
+      free(t);
+      return 2;
+    }
+  if (which & 1) {
+    for (int32_t i = 0; i < n; ++i) {
+      const double yi = t[i] / uv[up[i]];
+      t[i] = yi;
+      for (int64_t q = up[i] + 1; q < up[i + 1]; ++q) {
+        const double p = uv[q] * yi;
+        t[uc[q]] = t[uc[q]] - p;
+      }
+    }
+  }
+  if (which & 2) {
+    for (int32_t i = n - 1; i >= 0; --i) {
+      double s = t[i];
+      for (int64_t q = up[i] + 1; q < up[i + 1]; ++q) {
+        const double p = uv[q] * t[uc[q]];
+        s = s - p;
+      }
+      t[i] = s / uv[up[i]];
+    }
+  }
+  for (int32_t i = 0; i < n; ++i) x[i] = t[i];
+  free(t);
+  return 0;
+}

@@ -53,6 +53,16 @@ double orc_pattern_residual(int32_t n, const int64_t* a_ptr, const int32_t* a_co
                             const double* a_val, const int64_t* u_ptr, const int32_t* u_col,
                             const double* u_val);
 
+/* Triangular solves with the factor U (the
+ * preconditioner apply; a non-goal of the reference, so this
+ * restatement fixes the order): which & 1 -> forward Uᵀ y = b, row-oriented
+ * push over U's rows (t_j -= U(i,j) * y_i for i ascending, y_i = t_i / U(i,i));
+ * which & 2 -> backward U x = y (x_i = (y_i - sum_j U(i,j) x_j) / U(i,i), j
+ * ascending along row i, i descending). `b` and `x` may alias. Returns 0, or 2
+ * for a missing/zero diagonal. */
+int orc_trisolve(int32_t n, const int64_t* u_ptr, const int32_t* u_col, const double* u_val,
+                 const double* b, int32_t which, double* x);
+
 /* Dense level-k DP (symbolic.hpp:124-167); fills a row-major n*n 0/1 mask of
  * the upper pattern. Small n only. */
 void orc_levelk_dense(int32_t n, const int64_t* a_ptr, const int32_t* a_col, int32_t k,

@@ -15,6 +15,7 @@ from .core import (  # noqa: F401
     GpuFactorizer,
     GpuOptions,
     GpuSymbolic,
+    GpuTriSolve,
     KIND_NAMES,
     Plan,
     RangeList,

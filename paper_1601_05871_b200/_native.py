@@ -170,6 +170,19 @@ class SymStats(C.Structure):
 
 TCG_SYM_ALL_SLOW = 1
 
+
+class SolveStats(C.Structure):
+    _fields_ = [
+        ("device_ms", C.c_double),
+        ("depth_forward", C.c_int32),
+        ("depth_backward", C.c_int32),
+        ("grid_ctas", C.c_int32),
+        ("kernel_launches", C.c_int32),
+    ]
+
+
+TCG_SOLVE_FORWARD, TCG_SOLVE_BACKWARD, TCG_SOLVE_BOTH = 1, 2, 3
+
 # (name, restype, argtypes) for every symbol declared in include/tacho_b200.h
 SIGNATURES = [
     ("tcg_plan_build", C.c_int, [C.POINTER(CsrView), C.POINTER(CsrView), C.c_int32, i32p, C.POINTER(C.c_void_p)]),
@@ -211,6 +224,12 @@ SIGNATURES = [
     ("tcg_sym_levelk", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(SymStats)]),
     ("tcg_sym_nnz", C.c_int64, [C.c_void_p]),
     ("tcg_sym_download", C.c_int, [C.c_void_p, i64p, i32p]),
+    ("tcg_solve_create", C.c_int, [C.c_void_p, C.POINTER(CsrView), C.POINTER(C.c_void_p)]),
+    ("tcg_solve_destroy", None, [C.c_void_p]),
+    ("tcg_solve_error", C.c_char_p, [C.c_void_p]),
+    ("tcg_solve_apply", C.c_int, [C.c_void_p, f64p, f64p, C.c_int32, C.POINTER(SolveStats)]),
+    ("tcg_solve_trace", C.c_int, [C.c_void_p, u64p, C.c_void_p]),
+    ("tcg_solve_apply_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(SolveStats)]),
     ("tch_generate", C.c_void_p, [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]),
     ("tch_matrix_from_csr", C.c_void_p, [C.POINTER(CsrView)]),
     ("tch_matrix_free", None, [C.c_void_p]),

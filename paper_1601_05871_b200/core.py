@@ -683,6 +683,88 @@ class GpuFactorizer:
         return int(self._lib.tcg_arena_bytes(self.ctx))
 
 
+@dataclass
+class SolveStats:
+    device_ms: float
+    depth_forward: int
+    depth_backward: int
+    grid_ctas: int
+    kernel_launches: int
+
+
+class GpuTriSolve:
+    """Triangular solves with the factor a GpuFactorizer holds (tcg_solve_*):
+    ``apply(b)`` = (UᵀU)⁻¹ b, the IC(k) preconditioner apply; ``forward(b)``
+    solves Uᵀ y = b, ``backward(y)`` solves U x = y. Fixed operation order
+    (oracle.c orc_trisolve), bitwise reproducible."""
+
+    def __init__(self, fz: "GpuFactorizer"):
+        self._lib = _lib()
+        self.fz = fz
+        self.n = fz.plan.n
+        h = C.c_void_p()
+        st = self._lib.tcg_solve_create(fz.ctx, C.byref(fz.plan.pattern.view()), C.byref(h))
+        if st != N.TCG_OK:
+            raise (DeviceError if st == N.TCG_CUDA else ValueError)(
+                self._lib.tcg_solve_error(h).decode() if h else "tcg_solve_create: invalid context or pattern")
+        self.h = h
+        self.last = N.SolveStats()
+
+    def _run(self, b, which) -> np.ndarray:
+        bb = np.ascontiguousarray(b, dtype=np.float64)
+        if bb.shape != (self.n,):
+            raise ValueError(f"expected a vector of {self.n} values")
+        x = np.empty(self.n, np.float64)
+        st = self._lib.tcg_solve_apply(self.h, bb.ctypes.data_as(N.f64p), x.ctypes.data_as(N.f64p), which,
+                                       C.byref(self.last))
+        if st != N.TCG_OK:
+            msg = self._lib.tcg_solve_error(self.h).decode()
+            raise (SchedulerError if st == N.TCG_TIMEOUT else ValueError if st == N.TCG_INVALID
+                   else DeviceError)(msg)
+        return x
+
+    def apply(self, b) -> np.ndarray:
+        return self._run(b, N.TCG_SOLVE_BOTH)
+
+    def forward(self, b) -> np.ndarray:
+        return self._run(b, N.TCG_SOLVE_FORWARD)
+
+    def backward(self, y) -> np.ndarray:
+        return self._run(y, N.TCG_SOLVE_BACKWARD)
+
+    def apply_device_ptr(self, b_ptr: int, x_ptr: int, which: int = 3) -> SolveStats:
+        """Device vectors (e.g. torch CUDA tensors' data_ptr()), on the context's stream."""
+        st = self._lib.tcg_solve_apply_device(self.h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), which,
+                                              C.byref(self.last))
+        if st != N.TCG_OK:
+            raise (SchedulerError if st == N.TCG_TIMEOUT else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
+        return self.stats()
+
+    def apply_host_ptr(self, b_ptr: int, x_ptr: int, which: int = 3) -> SolveStats:
+        """Host vectors by address (pinned memory for full PCIe speed)."""
+        st = self._lib.tcg_solve_apply(self.h, C.cast(b_ptr, N.f64p), C.cast(x_ptr, N.f64p), which,
+                                       C.byref(self.last))
+        if st != N.TCG_OK:
+            raise (SchedulerError if st == N.TCG_TIMEOUT else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
+        return self.stats()
+
+    def stats(self) -> SolveStats:
+        s = self.last
+        return SolveStats(s.device_ms, int(s.depth_forward), int(s.depth_backward), int(s.grid_ctas),
+                          int(s.kernel_launches))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.tcg_solve_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def factor_by_blocks_gpu(a_permuted: CsrMatrix, fp: FillPattern, ranges: RangeList,
                          options: Optional[GpuOptions] = None) -> FactorResult:
     """GPU drop-in for ``factor_by_blocks`` (reference factorize.hpp:134-235).

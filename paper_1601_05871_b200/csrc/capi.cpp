@@ -1580,3 +1580,18 @@ tcg_status tch_init_values(const tcg_csr_view* a_permuted, const tcg_csr_view* p
 }
 
 }  // extern "C"
+
+// Internal accessor for the other C-ABI units (solve_capi.cpp): the device,
+// stream and factor values of a context, without touching its state.
+namespace tcb_internal {
+bool ctx_factor(tcg_ctx* c, int member, int* device, cudaStream_t* stream, const double** vals,
+                std::int64_t* n, std::int64_t* nnz) {
+  if (!c || !c->uploaded || member < 0 || member >= c->nbatch) return false;
+  *device = c->device;
+  *stream = c->stream;
+  *vals = c->nbatch == 1 ? c->vals : c->bvals + static_cast<std::int64_t>(member) * c->nnz;
+  *n = c->n;
+  *nnz = c->nnz;
+  return true;
+}
+}  // namespace tcb_internal

@@ -1,0 +1,148 @@
+// Triangular solves with the factor U on the device (SURVEY.md §8(f) rank 3:
+// the preconditioner apply z = (UᵀU)⁻¹ r of an IC(k)-preconditioned CG).
+//
+// The same value-flow schedule as the factorization (flow_kernel.cu): the
+// outputs y (forward, Uᵀ y = b) and x (backward, U x = y) start as a marker
+// NaN; one warp per unknown gathers its operands with strong loads and
+// re-polls any that still read the marker; the data is its own flag. Rows run
+// in a static topological order (forward rows by level, then backward rows by
+// level) dealt round-robin to the co-resident warps, so the lowest unfinished
+// position only reads final values and the launch cannot deadlock.
+//
+// Per unknown the products U(i,j)*v_i are formed in parallel by the lanes
+// (each rounded on its own) and subtracted in ascending source order by a
+// broadcast chain -- the oracle's sequential order (oracle.c orc_trisolve),
+// so the solution is bitwise equal to it.
+#include <cuda_runtime.h>
+
+#include "solve_api.hpp"
+#include "sync.cuh"
+
+namespace tcbdev {
+
+namespace {
+
+constexpr unsigned long long kSolveUnset = ~0ull;  // memset 0xFF; a NaN arithmetic never yields
+constexpr unsigned long long kCanonNaN = 0x7FFFFFFFFFFFFFFFull;
+
+__device__ __forceinline__ double poll(const double* p, const SolveParams& P, unsigned long long t0) {
+  unsigned long long x = ld_relaxed_u64(p);
+  if (x == kSolveUnset) {
+    unsigned spins = 0;
+    do {
+      x = ld_relaxed_u64(p);
+      if (++spins == 1024u) {
+        spins = 0;
+        if (ld_relaxed(P.error) || gtimer() - t0 > P.timeout_ns) {
+          atomicCAS(P.error, 0, 1);  // abandoned: the host reports TCG_TIMEOUT
+          return 0.0;
+        }
+      }
+    } while (x == kSolveUnset);
+  }
+  return __longlong_as_double(static_cast<long long>(x));
+}
+
+}  // namespace
+
+// One unknown per warp; the record, operand indices, values, diagonal and
+// right-hand side of the warp's next row are loaded while the current row
+// polls (all immutable during the launch), so only the operand hand-off is on
+// a row's critical path.
+template <int THREADS>
+__global__ void __launch_bounds__(THREADS) trisolve_flow(SolveParams P) {
+  constexpr int kWarps = THREADS / 32;
+  const int lane = threadIdx.x & 31;
+  const int W = gridDim.x * kWarps;
+  const unsigned long long t0 = gtimer();
+  struct Row {
+    int4 r;
+    int i;       // lane's operand index (first 32 entries)
+    double v;    // lane's value
+    double d;    // diagonal
+    double b;    // right-hand side (forward rows, and backward rows without poll_y)
+  };
+  auto fetch = [&](int q) {
+    Row w{};
+    if (q >= P.pos_end) return w;
+    w.r = __ldg(P.rec + q);
+    const bool back = w.r.y < 0;
+    const int len = w.r.y & 0x7fffffff;
+    if (lane < len) {
+      w.i = __ldg(P.idx + w.r.x + lane);
+      w.v = back ? __ldg(P.u + w.r.z + 1 + lane) : __ldg(P.fval + w.r.x + lane);
+    }
+    w.d = __ldg(P.u + w.r.z);
+    if (!back || !P.poll_y) w.b = __ldg(P.b + w.r.w);
+    return w;
+  };
+  int q = P.pos_begin + blockIdx.x * kWarps + (threadIdx.x >> 5);
+  Row cur = fetch(q);
+  for (; q < P.pos_end; q += W) {
+    const Row nxt = fetch(q + W);  // in flight while this row polls
+    const bool back = cur.r.y < 0;
+    const int len = cur.r.y & 0x7fffffff, row = cur.r.w;
+    const double* src = back ? P.x : P.y;
+    double* dst = back ? P.x : P.y;
+    unsigned long long* stamp = P.trace ? P.trace + 3 * static_cast<long long>(q) : nullptr;
+    if (stamp && lane == 0) stamp[0] = gtimer();
+    double t = (back && P.poll_y) ? poll(P.y + row, P, t0) : cur.b;  // backward: this row's forward result
+    // 32 entries per round, one per lane; the next round's entry loads
+    // overlap this round's chain. (Issuing several rounds' operand loads
+    // together was slower overall on B200: C2-C6 +8-20%, C3 backward -17%.)
+    int i = cur.i;
+    double v = cur.v;
+    for (int c0 = 0; c0 < len; c0 += 32) {
+      const int k = c0 + lane;
+      double p = 0.0;
+      if (k < len) p = __dmul_rn(v, poll(src + i, P, t0));
+      // reconverge before the chain: without it the lanes that found their
+      // operand final park at the first shuffle while the others spin, and
+      // the apply ran 2.7-4x slower on B200 (C2 forward 1.06 -> 0.26 ms)
+      __syncwarp();
+      if (stamp && c0 == 0 && lane == 0) stamp[1] = gtimer();
+      if (k + 32 < len) {
+        i = __ldg(P.idx + cur.r.x + k + 32);
+        v = back ? __ldg(P.u + cur.r.z + 1 + k + 32) : __ldg(P.fval + cur.r.x + k + 32);
+      }
+      const int m = min(32, len - c0);
+      for (int j = 0; j < m; ++j) t = __dsub_rn(t, __shfl_sync(0xffffffffu, p, j));
+    }
+    if (stamp && len == 0 && lane == 0) stamp[1] = gtimer();
+    if (lane == 0) {
+      unsigned long long bits = static_cast<unsigned long long>(__double_as_longlong(__ddiv_rn(t, cur.d)));
+      if (bits == kSolveUnset) bits = kCanonNaN;
+      st_relaxed_u64(dst + row, bits);
+      if (stamp) stamp[2] = gtimer();
+    }
+    cur = nxt;
+  }
+}
+
+__global__ void solve_gather(const double* __restrict__ u, const int* __restrict__ pos, double* __restrict__ fval,
+                             long long n) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long e = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += stride)
+    fval[e] = __ldg(u + __ldg(pos + e));
+}
+
+cudaError_t launch_solve_gather(const double* u, const int* pos, double* fval, long long n, int sm_count,
+                                cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  long long blocks = (n + 255) / 256;
+  blocks = blocks > 8LL * sm_count ? 8LL * sm_count : blocks;
+  solve_gather<<<static_cast<int>(blocks), 256, 0, st>>>(u, pos, fval, n);
+  return cudaGetLastError();
+}
+
+cudaError_t solve_occupancy(int* ctas_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, trisolve_flow<kSolveThreads>, kSolveThreads,
+                                                       0);
+}
+
+cudaError_t launch_trisolve(const SolveParams& p, int grid, cudaStream_t st) {
+  trisolve_flow<kSolveThreads><<<grid, kSolveThreads, 0, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace tcbdev

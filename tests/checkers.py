@@ -45,6 +45,8 @@ class Oracle:
         L.orc_pattern_residual.restype = C.c_double
         L.orc_pattern_residual.argtypes = [C.c_int32, i64p, i32p, f64p, i64p, i32p, f64p]
         L.orc_levelk_dense.argtypes = [C.c_int32, i64p, i32p, C.c_int32, u8p]
+        L.orc_trisolve.argtypes = [C.c_int32, i64p, i32p, f64p, f64p, C.c_int32, f64p]
+        L.orc_trisolve.restype = C.c_int
         self.L = L
 
     # hashes ---------------------------------------------------------------
@@ -107,6 +109,17 @@ class Oracle:
         return self.L.orc_pattern_residual(a.nrows, _p(a.row_ptr, i64p), _p(a.col_idx, i32p),
                                            _p(a.values, f64p), _p(u.row_ptr, i64p),
                                            _p(u.col_idx, i32p), _p(v, f64p))
+
+    def trisolve(self, u, vals, b, which=3) -> np.ndarray:
+        """x with Uᵀ y = b (which & 1) and U x = y (which & 2), oracle order."""
+        v = np.ascontiguousarray(vals, dtype=np.float64)
+        bb = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.zeros(u.nrows, np.float64)
+        st = self.L.orc_trisolve(u.nrows, _p(u.row_ptr, i64p), _p(u.col_idx, i32p), _p(v, f64p),
+                                 _p(bb, f64p), which, _p(x, f64p))
+        if st != 0:
+            raise ValueError(f"orc_trisolve status {st}")
+        return x
 
     def levelk_dense(self, a, k) -> np.ndarray:
         m = np.zeros(a.nrows * a.nrows, dtype=np.uint8)

@@ -37,7 +37,7 @@ def test_struct_layouts_match_the_header():
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
     for cname, py in (("tcg_problem", N.Problem), ("tcg_options", N.Options),
                       ("tcg_stats", N.Stats), ("tcg_plan_stats", N.PlanStats),
-                      ("tcg_sym_stats", N.SymStats)):
+                      ("tcg_sym_stats", N.SymStats), ("tcg_solve_stats", N.SolveStats)):
         body = re.search(r"typedef struct \{([^{}]*)\}\s*" + cname + ";", text, flags=re.S).group(1)
         decls = [d for d in body.split(";") if d.strip()]
         nfields = sum(len(d.split(",")) for d in decls)
