@@ -15,7 +15,8 @@ OBJ := build/obj
 ARCH := -gencode arch=compute_100a,code=sm_100a
 # -fmad=false: no FMA contraction anywhere (bitwise parity with the reference);
 # the kernel also spells every product/difference with __dmul_rn/__dsub_rn.
-NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v
+NVEXTRA ?=
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v $(NVEXTRA)
 CXXFLAGS := -O2 -std=c++17 -fPIC -pthread -Wall -Wextra -ffp-contract=off
 
 HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generators.cpp \
