@@ -19,7 +19,7 @@ NVEXTRA ?=
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas -v $(NVEXTRA)
 CXXFLAGS := -O2 -std=c++17 -fPIC -pthread -Wall -Wextra -ffp-contract=off
 
-HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generators.cpp \
+HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generators.cpp $(SRC)/host/io.cpp \
              $(SRC)/host/plan.cpp $(SRC)/capi.cpp $(SRC)/symbolic_capi.cpp $(SRC)/solve_capi.cpp
 HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
 DEV_OBJS := $(OBJ)/device/factor_kernel.o $(OBJ)/device/row_kernel.o $(OBJ)/device/static_kernel.o \

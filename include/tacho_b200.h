@@ -346,6 +346,20 @@ void tch_analysis_pattern(const tch_analysis* an, tcg_csr_view* out);
 void tch_analysis_times(const tch_analysis* an, double* ordering_s, double* symbolic_s);
 /* Fill pattern for an arbitrary permuted matrix (levelk_pattern_bfs). */
 tch_matrix* tch_levelk_pattern(const tch_matrix* a_permuted, int32_t level, int32_t threads);
+/* File formats. Matrix Market coordinate files, reference
+ * matrix_market.hpp:61-176: real/integer/pattern, general/symmetric (mirrored), duplicates
+ * summed; NULL / TCG_INVALID with tch_error() = the reference's MatrixMarketError text. The
+ * writer emits the reference's bytes (general storage, shortest round-trip values). */
+tch_matrix* tch_load_matrix_market(const char* path);
+tcg_status tch_write_matrix_market(const tcg_csr_view* m, const char* path);
+/* Ordering file, reference load_ordering (ordering.hpp:355-399): n, perm (new index of old),
+ * range count, "begin end" per range. Writes perm (n) and, when cap >= count, count + 1
+ * bounds; returns the range count, or -1 (tch_error() = the reference's message). */
+int32_t tch_load_ordering(const char* path, int32_t n, int32_t* perm, int32_t cap, int32_t* bounds);
+/* analyze() with an imported ordering (reference pipeline.hpp:39-44): PᵀAP and the
+ * level-k pattern for the given permutation and ranges. */
+tch_analysis* tch_analyze_with_ordering(const tch_matrix* a, const int32_t* perm, int32_t nranges,
+                                        const int32_t* bounds, int32_t level, int32_t threads);
 /* init_factor_values (factorize.hpp:71-89): out has pattern->nnz doubles. */
 tcg_status tch_init_values(const tcg_csr_view* a_permuted, const tcg_csr_view* pattern, double* out);
 

@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "taskchol/factorize.hpp"
+#include "taskchol/matrix_market.hpp"
 #include "taskchol/pipeline.hpp"
 #include "taskchol/symbolic.hpp"
 
@@ -55,6 +56,9 @@ struct ref_analysis {
 };
 struct ref_dag {
   std::vector<int32_t> kind, bi, bj, from, to;
+};
+struct ref_csr {
+  CsrMatrix m;
 };
 
 extern "C" {
@@ -213,6 +217,52 @@ int64_t ref_blocks(int32_t n, const int64_t* u_ptr, const int32_t* u_col, int32_
     std::memcpy(bcol, bm.bcol_idx.data(), sizeof(int32_t) * nb);
   }
   return nb;
+}
+
+// matrix_market.hpp:159-176 (0 ok, 1 error with ref_error()).
+int ref_write_mm(int32_t n, const int64_t* ptr, const int32_t* col, const double* val, const char* path) {
+  try {
+    write_matrix_market(make_csr(n, ptr, col, val), path);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// matrix_market.hpp:61-157 (NULL with ref_error() on failure).
+ref_csr* ref_load_mm(const char* path) {
+  try {
+    auto out = std::make_unique<ref_csr>();
+    out->m = load_matrix_market(path);
+    return out.release();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+void ref_csr_free(ref_csr* c) { delete c; }
+int32_t ref_csr_n(const ref_csr* c) { return c->m.nrows; }
+int64_t ref_csr_nnz(const ref_csr* c) { return c->m.nnz(); }
+const int64_t* ref_csr_ptr(const ref_csr* c) { return c->m.row_ptr.data(); }
+const int32_t* ref_csr_col(const ref_csr* c) { return c->m.col_idx.data(); }
+const double* ref_csr_val(const ref_csr* c) { return c->m.values.data(); }
+
+// ordering.hpp:355-399: range count (bounds written when cap >= count), or -1.
+int32_t ref_load_ordering(const char* path, int32_t n, int32_t* perm, int32_t cap, int32_t* bounds) {
+  try {
+    auto [p, rl] = load_ordering(path, n);
+    if (perm) std::memcpy(perm, p.perm.data(), sizeof(int32_t) * static_cast<std::size_t>(n));
+    const int32_t cnt = rl.count();
+    if (bounds && cap >= cnt) {
+      bounds[0] = cnt ? rl.ranges[0].begin : 0;
+      for (int32_t k = 0; k < cnt; ++k) bounds[k + 1] = rl.ranges[static_cast<std::size_t>(k)].end;
+    }
+    return cnt;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
 }
 
 }  // extern "C"

@@ -17,6 +17,7 @@ from .core import (  # noqa: F401
     GpuSymbolic,
     GpuTriSolve,
     KIND_NAMES,
+    MatrixMarketError,
     Plan,
     RangeList,
     SchedulerError,
@@ -29,4 +30,7 @@ from .core import (  # noqa: F401
     init_factor_values,
     levelk_pattern,
     levelk_pattern_gpu,
+    load_matrix_market,
+    load_ordering,
+    write_matrix_market,
 )

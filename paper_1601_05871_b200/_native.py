@@ -245,6 +245,10 @@ SIGNATURES = [
     ("tch_analysis_times", None, [C.c_void_p, f64p, f64p]),
     ("tch_levelk_pattern", C.c_void_p, [C.c_void_p, C.c_int32, C.c_int32]),
     ("tch_init_values", C.c_int, [C.POINTER(CsrView), C.POINTER(CsrView), f64p]),
+    ("tch_load_matrix_market", C.c_void_p, [C.c_char_p]),
+    ("tch_write_matrix_market", C.c_int, [C.POINTER(CsrView), C.c_char_p]),
+    ("tch_load_ordering", C.c_int32, [C.c_char_p, C.c_int32, i32p, C.c_int32, i32p]),
+    ("tch_analyze_with_ordering", C.c_void_p, [C.c_void_p, i32p, C.c_int32, i32p, C.c_int32, C.c_int32]),
 ]
 
 _lib = None

@@ -236,14 +236,21 @@ def config_matrix(name: str, member: int = 0) -> Tuple[CsrMatrix, int]:
 
 
 def analyze(a: CsrMatrix, level: int = 0, treecut: int = 0, leaf_size: int = 64,
-            max_depth: int = 100, threads: int = 0) -> Analysis:
-    """ND ordering -> prune -> PᵀAP -> level-k pattern (reference pipeline.hpp:35-55)."""
+            max_depth: int = 100, threads: int = 0, ordering_path: Optional[str] = None) -> Analysis:
+    """ND ordering -> prune -> PᵀAP -> level-k pattern (reference pipeline.hpp:35-55);
+    with ``ordering_path`` the ordering and ranges are imported instead
+    (load_ordering, pipeline.hpp:39-44)."""
     lib = _lib()
     m = lib.tch_matrix_from_csr(C.byref(a.view()))
     if not m:
         raise ValueError(lib.tch_error().decode())
     try:
-        h = lib.tch_analyze(m, level, treecut, leaf_size, max_depth, threads)
+        if ordering_path is not None:
+            perm_in, b_in = load_ordering(ordering_path, a.nrows)
+            h = lib.tch_analyze_with_ordering(m, perm_in.ctypes.data_as(N.i32p), int(b_in.shape[0]) - 1,
+                                              b_in.ctypes.data_as(N.i32p), level, threads)
+        else:
+            h = lib.tch_analyze(m, level, treecut, leaf_size, max_depth, threads)
         if not h:
             raise ValueError(lib.tch_error().decode())
         try:
@@ -277,6 +284,43 @@ def analyze(a: CsrMatrix, level: int = 0, treecut: int = 0, leaf_size: int = 64,
             lib.tch_analysis_free(h)
     finally:
         lib.tch_matrix_free(m)
+
+
+class MatrixMarketError(RuntimeError):
+    """Reference MatrixMarketError (matrix_market.hpp:24-27)."""
+
+
+def load_matrix_market(path: str) -> CsrMatrix:
+    """Reference load_matrix_market (matrix_market.hpp:61-157)."""
+    lib = _lib()
+    h = lib.tch_load_matrix_market(str(path).encode())
+    if not h:
+        raise MatrixMarketError(lib.tch_error().decode())
+    try:
+        v = N.CsrView()
+        lib.tch_matrix_view(h, C.byref(v))
+        return _from_view(v)
+    finally:
+        lib.tch_matrix_free(h)
+
+
+def write_matrix_market(m: CsrMatrix, path: str) -> None:
+    """Reference write_matrix_market (matrix_market.hpp:159-176): the same bytes."""
+    lib = _lib()
+    if lib.tch_write_matrix_market(C.byref(m.view()), str(path).encode()) != N.TCG_OK:
+        raise MatrixMarketError(lib.tch_error().decode())
+
+
+def load_ordering(path: str, n: int) -> Tuple[np.ndarray, np.ndarray]:
+    """Reference load_ordering (ordering.hpp:355-399): (perm, range bounds)."""
+    lib = _lib()
+    perm = np.zeros(max(n, 1), np.int32)
+    cnt = lib.tch_load_ordering(str(path).encode(), n, perm.ctypes.data_as(N.i32p), 0, None)
+    if cnt < 0:
+        raise RuntimeError(lib.tch_error().decode())
+    bounds = np.zeros(cnt + 1, np.int32)
+    lib.tch_load_ordering(str(path).encode(), n, perm.ctypes.data_as(N.i32p), cnt, bounds.ctypes.data_as(N.i32p))
+    return perm[:n].copy(), bounds
 
 
 def levelk_pattern(a_permuted: CsrMatrix, level: int, threads: int = 0) -> FillPattern:

@@ -1506,6 +1506,76 @@ tch_analysis* tch_analyze(const tch_matrix* a, int32_t level, int32_t treecut, i
   }
 }
 
+tch_matrix* tch_load_matrix_market(const char* path) {
+  try {
+    if (!path) throw std::invalid_argument("null path");
+    auto out = std::make_unique<tch_matrix>();
+    out->m = tcb::load_matrix_market(path);
+    return out.release();
+  } catch (const std::exception& e) {
+    g_tch_error = e.what();
+    return nullptr;
+  }
+}
+
+tcg_status tch_write_matrix_market(const tcg_csr_view* m, const char* path) {
+  try {
+    if (!path) throw std::invalid_argument("null path");
+    tcb::write_matrix_market(csr_from_view(m, true), path);
+    return TCG_OK;
+  } catch (const std::invalid_argument& e) {
+    g_tch_error = e.what();
+    return TCG_INVALID;
+  } catch (const std::exception& e) {
+    g_tch_error = e.what();
+    return TCG_INVALID;
+  }
+}
+
+int32_t tch_load_ordering(const char* path, int32_t n, int32_t* perm, int32_t cap, int32_t* bounds) {
+  try {
+    if (!path) throw std::invalid_argument("null path");
+    auto [p, rl] = tcb::load_ordering(path, n);
+    if (perm) std::copy(p.perm.begin(), p.perm.end(), perm);
+    const int32_t count = rl.count();
+    if (bounds && cap >= count) {
+      bounds[0] = count ? rl.ranges[0].begin : 0;
+      for (int32_t k = 0; k < count; ++k) bounds[k + 1] = rl.ranges[static_cast<size_t>(k)].end;
+    }
+    return count;
+  } catch (const std::exception& e) {
+    g_tch_error = e.what();
+    return -1;
+  }
+}
+
+tch_analysis* tch_analyze_with_ordering(const tch_matrix* a, const int32_t* perm, int32_t nranges,
+                                        const int32_t* bounds, int32_t level, int32_t threads) {
+  try {
+    if (!a || (!perm && a->m.nrows > 0) || nranges < 0 || !bounds) throw std::invalid_argument("null input");
+    const tcb::index_t n = a->m.nrows;
+    tcb::Permutation p;
+    p.perm.assign(perm, perm + n);
+    p.iperm.assign(static_cast<size_t>(n), -1);
+    for (tcb::index_t i = 0; i < n; ++i) {
+      const tcb::index_t q = p.perm[static_cast<size_t>(i)];
+      if (q < 0 || q >= n || p.iperm[static_cast<size_t>(q)] >= 0)
+        throw std::invalid_argument("permutation: not a bijection");
+      p.iperm[static_cast<size_t>(q)] = i;
+    }
+    tcb::RangeList rl;
+    for (int32_t k = 0; k < nranges; ++k) rl.ranges.push_back({bounds[k], bounds[k + 1]});
+    tcb::validate_ranges(rl, n);
+    auto out = std::make_unique<tch_analysis>();
+    out->an = tcb::analyze_with_ordering(a->m, std::move(p), std::move(rl), level, threads);
+    out->bounds.assign(bounds, bounds + nranges + 1);
+    return out.release();
+  } catch (const std::exception& e) {
+    g_tch_error = e.what();
+    return nullptr;
+  }
+}
+
 void tch_analysis_free(tch_analysis* an) { delete an; }
 const char* tch_error(void) { return g_tch_error.c_str(); }
 

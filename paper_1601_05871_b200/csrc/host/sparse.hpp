@@ -119,6 +119,19 @@ FillPattern levelk_pattern(const CsrMatrix& a_permuted, index_t k,
 Analysis analyze(const CsrMatrix& a, const AnalyzeOptions& opt,
                  int threads = 0);
 
+// --- file formats (io.cpp) --------------------------------------------------
+// Matrix Market coordinate files (reference matrix_market.hpp:61-176): real,
+// integer or pattern; general or symmetric (mirrored); duplicates summed.
+// Errors are std::runtime_error with the reference's messages.
+CsrMatrix load_matrix_market(const std::string& path);
+void write_matrix_market(const CsrMatrix& m, const std::string& path);
+// Ordering file (reference ordering.hpp:355-399): n, n values of perm
+// (new index of old), the range count, then "begin end" per range.
+std::pair<Permutation, RangeList> load_ordering(const std::string& path, index_t n);
+// The pipeline with an imported ordering (reference pipeline.hpp:39-44).
+Analysis analyze_with_ordering(const CsrMatrix& a, Permutation perm, RangeList ranges, index_t level,
+                               int threads = 0);
+
 // --- generators (generators.cpp) -------------------------------------------
 CsrMatrix grid_laplacian_2d(index_t nx, index_t ny);           // C1
 CsrMatrix laplacian_7pt(index_t n);                            // C2, C6

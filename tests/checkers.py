@@ -163,6 +163,18 @@ class Reference:
         L.ref_factor_serial.argtypes = [C.c_int32, i64p, i32p, f64p, i64p, i32p, f64p, f64p, i32p, f64p]
         L.ref_factor_by_blocks.argtypes = [C.c_int32, i64p, i32p, f64p, i64p, i32p, C.c_int32, i32p,
                                            C.c_int32, f64p, f64p, f64p, i64p, i32p, f64p]
+        L.ref_write_mm.argtypes = [C.c_int32, i64p, i32p, f64p, C.c_char_p]
+        L.ref_load_mm.restype = vp
+        L.ref_load_mm.argtypes = [C.c_char_p]
+        L.ref_csr_free.argtypes = [vp]
+        L.ref_csr_n.restype = C.c_int32
+        L.ref_csr_nnz.restype = C.c_int64
+        for name, rt in (("ptr", i64p), ("col", i32p), ("val", f64p)):
+            getattr(L, "ref_csr_" + name).restype = rt
+        for name in ("n", "nnz", "ptr", "col", "val"):
+            getattr(L, "ref_csr_" + name).argtypes = [vp]
+        L.ref_load_ordering.restype = C.c_int32
+        L.ref_load_ordering.argtypes = [C.c_char_p, C.c_int32, i32p, C.c_int32, i32p]
         L.ref_export_dag.restype = vp
         L.ref_export_dag.argtypes = [C.c_int32, i64p, i32p, C.c_int32, i32p]
         L.ref_dag_free.argtypes = [vp]
@@ -207,6 +219,32 @@ class Reference:
             }
         finally:
             self.L.ref_analysis_free(h)
+
+    def write_mm(self, m, path) -> None:
+        if self.L.ref_write_mm(m.nrows, _p(m.row_ptr, i64p), _p(m.col_idx, i32p), _p(m.values, f64p),
+                               str(path).encode()) != 0:
+            raise RuntimeError(self.L.ref_error().decode())
+
+    def load_mm(self, path):
+        """(row_ptr, col_idx, values) or raises RuntimeError(reference message)."""
+        h = self.L.ref_load_mm(str(path).encode())
+        if not h:
+            raise RuntimeError(self.L.ref_error().decode())
+        try:
+            n, nnz = self.L.ref_csr_n(h), self.L.ref_csr_nnz(h)
+            return (self._arr(self.L.ref_csr_ptr(h), n + 1, np.int64), self._arr(self.L.ref_csr_col(h), nnz, np.int32),
+                    self._arr(self.L.ref_csr_val(h), nnz, np.float64))
+        finally:
+            self.L.ref_csr_free(h)
+
+    def load_ordering(self, path, n):
+        perm = np.zeros(max(n, 1), np.int32)
+        cnt = self.L.ref_load_ordering(str(path).encode(), n, _p(perm, i32p), 0, C.cast(None, i32p))
+        if cnt < 0:
+            raise RuntimeError(self.L.ref_error().decode())
+        b = np.zeros(cnt + 1, np.int32)
+        self.L.ref_load_ordering(str(path).encode(), n, _p(perm, i32p), cnt, _p(b, i32p))
+        return perm[:n], b
 
     def levelk(self, a, k):
         nnz = self.L.ref_levelk(a.nrows, _p(a.row_ptr, i64p), _p(a.col_idx, i32p), k,
