@@ -27,97 +27,165 @@ namespace tcb {
 
 namespace {
 
+// The recursion of the reference's nested_dissection, with disjoint subtrees
+// run on separate host threads near the top of the tree. A subtree's numbers
+// are known before it is dissected (the lower part first, then the upper,
+// then the separator: ordering.hpp:239-300), so each subtree numbers its
+// vertices from its own base; its tree nodes are built in a private list and
+// appended in the sequential post-order, so perm, iperm and the tree are the
+// sequential ones whatever the thread count.
 class Dissector {
  public:
-  Dissector(const CsrMatrix& a, index_t leaf, index_t max_depth)
-      : a_(a), leaf_(std::max<index_t>(leaf, 1)), max_depth_(max_depth),
-        member_(a.nrows, 0), mark_(a.nrows, 0), side_(a.nrows, 0) {
+  Dissector(const CsrMatrix& a, index_t leaf, index_t max_depth, int threads)
+      : a_(a), leaf_(std::max<index_t>(leaf, 1)), max_depth_(max_depth) {
     perm_.perm.assign(a.nrows, -1);
     perm_.iperm.assign(a.nrows, -1);
+    // spawn below the first levels while threads remain (2^d subtrees at depth d)
+    int d = 0;
+    while ((1 << d) < threads && d < 12) ++d;
+    par_depth_ = threads > 1 ? d : 0;
   }
 
   std::pair<Permutation, NdTree> run() {
+    NdTree tree;
     if (a_.nrows == 0) {
-      tree_.nodes.emplace_back();
-      tree_.root = 0;
+      tree.nodes.emplace_back();
+      tree.root = 0;
     } else {
       std::vector<index_t> all(a_.nrows);
       for (index_t v = 0; v < a_.nrows; ++v) all[v] = v;
-      tree_.root = split(all, 0);
+      Scratch S(a_.nrows);
+      tree.root = split(all, 0, 0, S, tree.nodes);
     }
-    return {std::move(perm_), std::move(tree_)};
+    return {std::move(perm_), std::move(tree)};
   }
 
  private:
-  // Returns the node id of the subtree ordering `verts` (ascending ids).
-  index_t split(const std::vector<index_t>& verts, index_t depth) {
-    if (static_cast<index_t>(verts.size()) <= leaf_ || depth >= max_depth_)
-      return leaf(verts, depth);
+  // per-thread marks; stamps only grow, so a thread's stale marks never match
+  struct Scratch {
+    explicit Scratch(index_t n) : member(n, 0), mark(n, 0), side(n, 0) {}
+    std::vector<index_t> member, mark;
+    std::vector<unsigned char> side;
+    index_t member_stamp = 0, mark_stamp = 0;
+    void enter(const std::vector<index_t>& verts) {
+      ++member_stamp;
+      for (index_t v : verts) member[v] = member_stamp;
+    }
+    bool inside(index_t v) const { return member[v] == member_stamp; }
+  };
 
-    std::vector<std::vector<index_t>> comps = components(verts);
+  // Dissects `verts` (ascending ids), numbering them from `base`; appends the
+  // subtree's nodes to `out` in post-order and returns the root's index there.
+  index_t split(const std::vector<index_t>& verts, index_t depth, index_t base, Scratch& S,
+                std::vector<NdNode>& out) {
+    if (static_cast<index_t>(verts.size()) <= leaf_ || depth >= max_depth_)
+      return leaf(verts, depth, base, out);
+
+    std::vector<std::vector<index_t>> comps = components(verts, S);
     if (comps.size() > 1) {
       NdNode nd;
       nd.depth = depth;
-      for (auto& c : comps) nd.children.push_back(split(c, depth + 1));
-      nd.range = {next_, next_};
-      return push(std::move(nd));
+      std::vector<index_t> bases(comps.size());
+      index_t at = base;
+      for (std::size_t c = 0; c < comps.size(); ++c) {
+        bases[c] = at;
+        at += static_cast<index_t>(comps[c].size());
+      }
+      children(comps, depth + 1, bases, S, out, nd);
+      nd.range = {at, at};
+      return push(out, std::move(nd));
     }
 
     std::vector<index_t> lo, hi, sep;
-    if (!bisect(verts, lo, hi, sep) || sep.empty() || (lo.empty() && hi.empty()))
-      return leaf(verts, depth);
+    if (!bisect(verts, lo, hi, sep, S) || sep.empty() || (lo.empty() && hi.empty()))
+      return leaf(verts, depth, base, out);
 
     NdNode nd;
     nd.depth = depth;
-    if (!lo.empty()) nd.children.push_back(split(lo, depth + 1));
-    if (!hi.empty()) nd.children.push_back(split(hi, depth + 1));
-    nd.range.begin = next_;
-    for (index_t v : sep) number(v);
-    nd.range.end = next_;
-    return push(std::move(nd));
+    const index_t lo_n = static_cast<index_t>(lo.size()), hi_n = static_cast<index_t>(hi.size());
+    std::vector<std::vector<index_t>> parts;
+    std::vector<index_t> bases;
+    if (!lo.empty()) {
+      parts.push_back(std::move(lo));
+      bases.push_back(base);
+    }
+    if (!hi.empty()) {
+      parts.push_back(std::move(hi));
+      bases.push_back(base + lo_n);
+    }
+    children(parts, depth + 1, bases, S, out, nd);
+    nd.range.begin = base + lo_n + hi_n;
+    index_t next = nd.range.begin;
+    for (index_t v : sep) number(v, next);
+    nd.range.end = next;
+    return push(out, std::move(nd));
   }
 
-  index_t leaf(const std::vector<index_t>& verts, index_t depth) {
+  // the child subtrees in order; near the top, all but the last on new threads
+  void children(const std::vector<std::vector<index_t>>& parts, index_t depth,
+                const std::vector<index_t>& bases, Scratch& S, std::vector<NdNode>& out, NdNode& nd) {
+    const std::size_t np = parts.size();
+    if (depth > par_depth_ || np < 2) {
+      for (std::size_t c = 0; c < np; ++c) nd.children.push_back(split(parts[c], depth, bases[c], S, out));
+      return;
+    }
+    std::vector<std::vector<NdNode>> sub(np);
+    std::vector<index_t> roots(np, -1);
+    std::vector<std::thread> pool;
+    for (std::size_t c = 0; c + 1 < np; ++c)
+      pool.emplace_back([&, c] {
+        Scratch own(a_.nrows);
+        roots[c] = split(parts[c], depth, bases[c], own, sub[c]);
+      });
+    roots[np - 1] = split(parts[np - 1], depth, bases[np - 1], S, sub[np - 1]);
+    for (auto& t : pool) t.join();
+    for (std::size_t c = 0; c < np; ++c) {  // append in order, child indices shifted
+      const index_t shift = static_cast<index_t>(out.size());
+      for (NdNode& x : sub[c]) {
+        for (index_t& ch : x.children) ch += shift;
+        out.push_back(std::move(x));
+      }
+      nd.children.push_back(roots[c] + shift);
+    }
+  }
+
+  index_t leaf(const std::vector<index_t>& verts, index_t depth, index_t base, std::vector<NdNode>& out) {
     NdNode nd;
     nd.depth = depth;
-    nd.range.begin = next_;
-    for (index_t v : verts) number(v);
-    nd.range.end = next_;
-    return push(std::move(nd));
+    nd.range.begin = base;
+    index_t next = base;
+    for (index_t v : verts) number(v, next);
+    nd.range.end = next;
+    return push(out, std::move(nd));
   }
 
-  void number(index_t v) {
-    perm_.perm[v] = next_;
-    perm_.iperm[next_] = v;
-    ++next_;
+  // subtrees write disjoint positions of the shared permutation
+  void number(index_t v, index_t& next) {
+    perm_.perm[v] = next;
+    perm_.iperm[next] = v;
+    ++next;
   }
 
-  index_t push(NdNode&& nd) {
-    tree_.nodes.push_back(std::move(nd));
-    return static_cast<index_t>(tree_.nodes.size()) - 1;
+  static index_t push(std::vector<NdNode>& out, NdNode&& nd) {
+    out.push_back(std::move(nd));
+    return static_cast<index_t>(out.size()) - 1;
   }
-
-  void enter(const std::vector<index_t>& verts) {
-    ++member_stamp_;
-    for (index_t v : verts) member_[v] = member_stamp_;
-  }
-  bool inside(index_t v) const { return member_[v] == member_stamp_; }
 
   // Connected pieces, each sorted, ordered by their smallest vertex.
-  std::vector<std::vector<index_t>> components(const std::vector<index_t>& verts) {
-    enter(verts);
-    ++mark_stamp_;
+  std::vector<std::vector<index_t>> components(const std::vector<index_t>& verts, Scratch& S) {
+    S.enter(verts);
+    ++S.mark_stamp;
     std::vector<std::vector<index_t>> out;
     for (index_t s : verts) {
-      if (mark_[s] == mark_stamp_) continue;
+      if (S.mark[s] == S.mark_stamp) continue;
       std::vector<index_t> piece{s};
-      mark_[s] = mark_stamp_;
+      S.mark[s] = S.mark_stamp;
       for (std::size_t h = 0; h < piece.size(); ++h) {
         const index_t v = piece[h];
         for (offset_t q = a_.row_begin(v); q < a_.row_end(v); ++q) {
           const index_t w = a_.col_idx[q];
-          if (w != v && inside(w) && mark_[w] != mark_stamp_) {
-            mark_[w] = mark_stamp_;
+          if (w != v && S.inside(w) && S.mark[w] != S.mark_stamp) {
+            S.mark[w] = S.mark_stamp;
             piece.push_back(w);
           }
         }
@@ -132,13 +200,13 @@ class Dissector {
 
   // BFS from `root` over the member set; `order` receives the vertices level
   // by level (each level sorted) and `level_start` the level offsets.
-  void levels_from(index_t root, std::vector<index_t>& order,
-                   std::vector<std::size_t>& level_start) {
-    ++mark_stamp_;
+  void levels_from(index_t root, std::vector<index_t>& order, std::vector<std::size_t>& level_start,
+                   Scratch& S) {
+    ++S.mark_stamp;
     order.clear();
     level_start.clear();
     order.push_back(root);
-    mark_[root] = mark_stamp_;
+    S.mark[root] = S.mark_stamp;
     std::size_t lb = 0, le = 1;
     level_start.push_back(0);
     while (lb < le) {
@@ -146,8 +214,8 @@ class Dissector {
         const index_t v = order[h];
         for (offset_t q = a_.row_begin(v); q < a_.row_end(v); ++q) {
           const index_t w = a_.col_idx[q];
-          if (w != v && inside(w) && mark_[w] != mark_stamp_) {
-            mark_[w] = mark_stamp_;
+          if (w != v && S.inside(w) && S.mark[w] != S.mark_stamp) {
+            S.mark[w] = S.mark_stamp;
             order.push_back(w);
           }
         }
@@ -160,14 +228,14 @@ class Dissector {
     level_start.push_back(order.size());
   }
 
-  bool bisect(const std::vector<index_t>& verts, std::vector<index_t>& lo,
-              std::vector<index_t>& hi, std::vector<index_t>& sep) {
-    enter(verts);
+  bool bisect(const std::vector<index_t>& verts, std::vector<index_t>& lo, std::vector<index_t>& hi,
+              std::vector<index_t>& sep, Scratch& S) {
+    S.enter(verts);
     std::vector<index_t> order;
     std::vector<std::size_t> ls;
-    levels_from(verts.front(), order, ls);
+    levels_from(verts.front(), order, ls, S);
     const index_t far = order[ls[ls.size() - 2]];  // smallest vertex of the last level
-    levels_from(far, order, ls);
+    levels_from(far, order, ls, S);
     const index_t nlev = static_cast<index_t>(ls.size()) - 1;
     if (nlev < 2) return false;
 
@@ -180,7 +248,7 @@ class Dissector {
       if (acc >= need) break;
     }
     const std::size_t split_at = ls[cut + 1];
-    for (std::size_t h = 0; h < order.size(); ++h) side_[order[h]] = h < split_at ? 1 : 2;
+    for (std::size_t h = 0; h < order.size(); ++h) S.side[order[h]] = h < split_at ? 1 : 2;
     lo.assign(order.begin(), order.begin() + split_at);
     hi.assign(order.begin() + split_at, order.end());
 
@@ -193,7 +261,7 @@ class Dissector {
       bool touches = false;
       for (offset_t q = a_.row_begin(v); q < a_.row_end(v) && !touches; ++q) {
         const index_t w = a_.col_idx[q];
-        touches = (w != v && inside(w) && side_[w] == other);
+        touches = (w != v && S.inside(w) && S.side[w] == other);
       }
       (touches ? sep : keep).push_back(v);
     }
@@ -207,11 +275,8 @@ class Dissector {
 
   const CsrMatrix& a_;
   index_t leaf_, max_depth_;
-  std::vector<index_t> member_, mark_;
-  std::vector<unsigned char> side_;
-  index_t member_stamp_ = 0, mark_stamp_ = 0, next_ = 0;
+  index_t par_depth_ = 0;
   Permutation perm_;
-  NdTree tree_;
 };
 
 double since(std::chrono::steady_clock::time_point t0) {
@@ -227,9 +292,11 @@ int pick_threads(int threads) {
 }  // namespace
 
 std::pair<Permutation, NdTree> nested_dissection(const CsrMatrix& a, index_t leaf_size,
-                                                 index_t max_depth) {
+                                                 index_t max_depth, int threads) {
   if (a.nrows != a.ncols) throw std::invalid_argument("nested_dissection: matrix not square");
-  return Dissector(a, leaf_size, max_depth).run();
+  // small graphs stay on one thread (a thread's scratch is three n-arrays)
+  const int nt = a.nrows < 4096 ? 1 : pick_threads(threads);
+  return Dissector(a, leaf_size, max_depth, nt).run();
 }
 
 RangeList prune_tree(const NdTree& tree, index_t t) {
@@ -327,7 +394,7 @@ FillPattern levelk_pattern(const CsrMatrix& a, index_t k, int threads) {
 Analysis analyze(const CsrMatrix& a, const AnalyzeOptions& opt, int threads) {
   Analysis out;
   auto t0 = std::chrono::steady_clock::now();
-  auto nd = nested_dissection(a, opt.leaf_size, opt.max_depth);
+  auto nd = nested_dissection(a, opt.leaf_size, opt.max_depth, threads);
   out.perm = std::move(nd.first);
   out.tree = std::move(nd.second);
   out.ranges = prune_tree(out.tree, opt.treecut);

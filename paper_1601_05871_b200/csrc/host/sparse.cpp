@@ -1,5 +1,6 @@
 // CSR utilities for the host input side of the IC(k) path.
 #include <algorithm>
+#include <thread>
 #include <numeric>
 
 #include "sparse.hpp"
@@ -96,21 +97,32 @@ CsrMatrix permute_symmetric(const CsrMatrix& a, const Permutation& p) {
   for (index_t i = 0; i < n; ++i) b.row_ptr[i + 1] += b.row_ptr[i];
   b.col_idx.resize(static_cast<std::size_t>(a.nnz()));
   b.values.resize(static_cast<std::size_t>(a.nnz()));
-  std::vector<std::pair<index_t, double>> row;
-  for (index_t r = 0; r < n; ++r) {
-    const index_t src = p.iperm[r];
-    row.clear();
-    for (offset_t q = a.row_begin(src); q < a.row_end(src); ++q)
-      row.emplace_back(p.perm[a.col_idx[q]], a.values[q]);
-    std::sort(row.begin(), row.end(),
-              [](const auto& x, const auto& y) { return x.first < y.first; });
-    offset_t o = b.row_ptr[r];
-    for (const auto& e : row) {
-      b.col_idx[o] = e.first;
-      b.values[o] = e.second;
-      ++o;
+  // rows are independent: blocks of rows on the host threads
+  auto rows = [&](index_t r0, index_t r1) {
+    std::vector<std::pair<index_t, double>> row;
+    for (index_t r = r0; r < r1; ++r) {
+      const index_t src = p.iperm[r];
+      row.clear();
+      for (offset_t q = a.row_begin(src); q < a.row_end(src); ++q)
+        row.emplace_back(p.perm[a.col_idx[q]], a.values[q]);
+      std::sort(row.begin(), row.end(),
+                [](const auto& x, const auto& y) { return x.first < y.first; });
+      offset_t o = b.row_ptr[r];
+      for (const auto& e : row) {
+        b.col_idx[o] = e.first;
+        b.values[o] = e.second;
+        ++o;
+      }
     }
-  }
+  };
+  const unsigned hc = std::thread::hardware_concurrency();
+  const index_t nt = n < 65536 ? 1 : static_cast<index_t>(std::max(1u, std::min(hc, 32u)));
+  std::vector<std::thread> pool;
+  for (index_t t = 1; t < nt; ++t)
+    pool.emplace_back(rows, static_cast<index_t>(static_cast<long long>(n) * t / nt),
+                      static_cast<index_t>(static_cast<long long>(n) * (t + 1) / nt));
+  rows(0, static_cast<index_t>(n / nt));
+  for (auto& th : pool) th.join();
   return b;
 }
 

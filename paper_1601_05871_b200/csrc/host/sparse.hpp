@@ -110,9 +110,11 @@ std::vector<double> init_factor_values(const CsrMatrix& a_permuted,
 std::vector<std::int32_t> init_factor_map(const CsrMatrix& a_permuted, const CsrMatrix& pattern);
 
 // --- analysis (analysis.cpp) -----------------------------------------------
+// threads: 0 = all hardware threads (disjoint subtrees in parallel; the
+// result is the sequential one whatever the count)
 std::pair<Permutation, NdTree> nested_dissection(const CsrMatrix& a,
                                                  index_t leaf_size,
-                                                 index_t max_depth);
+                                                 index_t max_depth, int threads = 1);
 RangeList prune_tree(const NdTree& tree, index_t t);
 FillPattern levelk_pattern(const CsrMatrix& a_permuted, index_t k,
                            int threads = 0);
