@@ -12,10 +12,10 @@ from its device copy and L2 is flushed (256 MiB write), both untimed.
          device time of one step); device time = CUDA events around the
          persistent kernel on the stream it is launched on.
   e2e    the same metric through the C ABI with host buffers
-         (tcg_factor_host): H2D of the initial values from pinned memory --
-         in mode 5 on a second stream beside the kernel, which polls the
-         inputs as they land --, factor, D2H of the factor; the symbolic
-         structure (plan) stays resident, as in a refactorization.
+         (tcg_factor_host_a): H2D of PaP's values (the reference call's
+         input) from pinned memory, init_factor_values on the device, factor,
+         D2H of the factor, one stream-ordered call; the symbolic structure
+         (plan) stays resident, as in a refactorization.
   roofline  algorithmic bytes 20*nnz_u + 8*(n+1) per
          launch / kernel time, against the measured HBM copy bandwidth.
 
@@ -258,11 +258,15 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         step_ms = float(t.item())
 
-    # end to end through the C ABI with host buffers (pinned)
+    # end to end through the C ABI with host buffers (pinned): the reference's inputs,
+    # PᵀAP's values, in; the factor out (tcg_factor_host_a: H2D of A, init_factor_values
+    # on the device, prelude, factor, D2H)
     if batched:
-        host_in = torch.from_numpy(batch_vals.reshape(-1)).pin_memory()
+        a_vals = np.stack([ap.values for ap in batch_perms]).reshape(-1)
     else:
-        host_in = torch.from_numpy(plan.tables()["values"]).pin_memory()
+        a_vals = an.a_permuted.values
+    host_in = torch.from_numpy(np.ascontiguousarray(a_vals)).pin_memory()
+    nnz_a = an.a_permuted.nnz()
     host_out = torch.empty(nnz * per_rank, dtype=torch.float64).pin_memory()
     e2e_ms = []
     barrier()
@@ -270,12 +274,12 @@ def run_ours(args):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        # tcg_factor_host: H2D of the initial values (8*nnz_u per member, overlapped with
-        # the mode-5 kernel, which polls them), factor, D2H of the factor (8*nnz_u per member)
-        fz.factor_host_ptr(host_in.data_ptr(), host_out.data_ptr())
+        st_e2e = fz.factor_host_a_ptr(host_in.data_ptr(), host_out.data_ptr())
         if i >= args.warmup:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
     barrier()
+    if batched:  # back to the initialised batch for anything after
+        fz.set_batch(batch_vals)
     clocks.__exit__(None, None, None)
     e2e = statistics.mean(e2e_ms)
     if world > 1:
@@ -330,8 +334,10 @@ def run_ours(args):
                    "l2": "flushed between steps (256 MiB write), U restored from device copy (untimed)",
                    "analysis_s": round(t_an, 3), "plan_s": round(ps.plan_seconds + ps.block_build_seconds, 3),
                    "parity_vs_oracle": parity},
-        "e2e": {"value": units / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz * per_rank,
-                "d2h_bytes_per_step": 8 * nnz * per_rank, "ms_per_step": e2e},
+        "e2e": {"value": units / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz_a * per_rank,
+                "d2h_bytes_per_step": 8 * nnz * per_rank, "ms_per_step": e2e,
+                "call": "tcg_factor_host_a: PaP values in (host), device init_factor_values, factor, factor out",
+                "launches": int(st_e2e.kernel_launches)},
         "gpu_launches": launches_per_step * args.steps,
         "launches_per_step": ({"flow_prepare (timed)": 1, "factor_flow (timed)": 1} if st.mode == 5 else
                               {"prepare (untimed)": 1, "factor": 1}),

@@ -227,6 +227,12 @@ tcg_status tcg_download(tcg_ctx* ctx, double* values);
  * full PCIe speed): upload the initial values, factor, download the factor, stream-ordered
  * in one call. The device copy of the initial values (tcg_restore) is not updated. */
 tcg_status tcg_factor_host(tcg_ctx* ctx, const double* values_in, double* values_out, tcg_stats* stats);
+/* End to end from the matrix, as the reference's call takes it: PᵀAP's values (host,
+ * nbatch x nnz(a_permuted) in a_permuted's CSR order) are uploaded, scattered into U on the
+ * device (init_factor_values, factorize.hpp:71-89; needs the A -> U map, see
+ * tcg_set_a_values), factored, and the factor downloaded -- one stream-ordered call. The
+ * restore copy is updated too. */
+tcg_status tcg_factor_host_a(tcg_ctx* ctx, const double* a_values, double* values_out, tcg_stats* stats);
 /* Stamps of the last traced factor: per task {start, end} (2*ntasks words), then per
  * item {claimed, sources ready, merged, published} (4*nitems words); globaltimer ns. */
 tcg_status tcg_download_trace(tcg_ctx* ctx, uint64_t* stamps);

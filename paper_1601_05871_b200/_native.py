@@ -204,6 +204,7 @@ SIGNATURES = [
     ("tcg_factor", C.c_int, [C.c_void_p, C.POINTER(Stats)]),
     ("tcg_download", C.c_int, [C.c_void_p, f64p]),
     ("tcg_factor_host", C.c_int, [C.c_void_p, f64p, f64p, C.c_void_p]),
+    ("tcg_factor_host_a", C.c_int, [C.c_void_p, f64p, f64p, C.c_void_p]),
     ("tcg_download_trace", C.c_int, [C.c_void_p, u64p]),
     ("tcg_set_batch", C.c_int, [C.c_void_p, C.c_int32, f64p]),
     ("tcg_set_batch_values", C.c_int, [C.c_void_p, f64p]),

@@ -622,9 +622,27 @@ class GpuFactorizer:
         self._check(st)
         return self.last
 
+    def factor_host_a_ptr(self, a_ptr: int, out_ptr: int) -> N.Stats:
+        """PᵀAP's values in (nnz(A) x batch doubles, a_permuted's CSR order),
+        factor out (nnz x batch), through tcg_factor_host_a: upload, device
+        init_factor_values, factor, download in one call. Pinned memory."""
+        self.last = N.Stats()
+        st = self._lib.tcg_factor_host_a(self.ctx, C.cast(C.c_void_p(a_ptr), N.f64p),
+                                         C.cast(C.c_void_p(out_ptr), N.f64p), C.byref(self.last))
+        self._check(st)
+        return self.last
+
+    def factor_host_a(self, a_values: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """factor_host_a_ptr with numpy arrays (one member: a_permuted.values)."""
+        v = np.ascontiguousarray(a_values, dtype=np.float64)
+        if out is None:
+            out = np.empty(self.nnz * max(1, v.size // max(1, self._problem.nnz_a)), np.float64)
+        self.factor_host_a_ptr(v.ctypes.data, out.ctypes.data)
+        return out
+
     def factor_host_ptr(self, in_ptr: int, out_ptr: int) -> N.Stats:
-        """Host buffers in, factor out (tcg_factor_host): in mode 5 the upload
-        overlaps the factorization. Pointers to nnz x batch doubles (pinned)."""
+        """Host buffers in, factor out (tcg_factor_host): upload, factor and
+        download on one stream. Pointers to nnz x batch doubles (pinned)."""
         self.last = N.Stats()
         st = self._lib.tcg_factor_host(self.ctx, C.cast(C.c_void_p(in_ptr), N.f64p),
                                        C.cast(C.c_void_p(out_ptr), N.f64p), C.byref(self.last))

@@ -680,7 +680,7 @@ tcg_status tcg_restore(tcg_ctx* c) {
 // host_in/host_out (tcg_factor_host): upload, factor and download on the
 // launch stream.
 static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* host_in = nullptr,
-                           double* host_out = nullptr, int phase = 0) {
+                           double* host_out = nullptr, int phase = 0, const double* host_a = nullptr) {
   // gather batch from the mean products per coordinate (flow_kernel.cu variants)
   const double mean = c->nnz > 0 ? static_cast<double>(c->nflow_upd) / static_cast<double>(c->nnz) : 0.0;
   int kb = mean <= 4.0 ? 2 : 3;
@@ -726,7 +726,9 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   tcbdev::FlowPrepParams q{};
   q.vals = vals;
   q.a = batch ? c->ba : c->flow_a;
-  const bool from_copy = c->pristine && !host_in;
+  // host_a: the device init below writes the restore copy too, which then
+  // serves as the kernel's input
+  const bool from_copy = (c->pristine && !host_in) || host_a;
   if (from_copy) q.a = batch ? c->bvals0 : c->vals0;
   q.out = vals;
   q.nnz = c->nnz * c->nbatch;
@@ -767,6 +769,13 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // the copy running concurrently with the kernel, which CUDA does not
   // promise -- under a profiler it serialised and the launch stalled.)
   if (host_in) TCG_CUDA_TRY(c, cudaMemcpyAsync(vals, host_in, vbytes, cudaMemcpyHostToDevice, c->stream));
+  if (host_a) {  // PᵀAP's values in, init_factor_values on the device (factorize.hpp:71-89)
+    if (c->nnz_a > 0)
+      TCG_CUDA_TRY(c, cudaMemcpyAsync(c->a_stage, host_a, sizeof(double) * c->nnz_a * c->nbatch,
+                                      cudaMemcpyHostToDevice, c->stream));
+    TCG_CUDA_TRY(c, tcbdev::launch_init_values(c->a_stage, c->a_map, vals, batch ? c->bvals0 : c->vals0, c->nnz,
+                                               c->nnz_a, c->nbatch, c->sm_count, c->stream));
+  }
   if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
   if (c->nflow > 0) {
     if (pipe) TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, extras, c->stream));
@@ -785,8 +794,9 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   S.grid_ctas = grid;
   S.threads_per_cta = threads;
   S.staging_cap = kb;  // reported: gather batch
-  S.kernel_launches = (c->nflow > 0 ? 1 : 0) + (phase == 0 ? 1 : 0);
+  S.kernel_launches = (c->nflow > 0 ? 1 : 0) + (phase == 0 ? 1 : 0) + (host_a ? 1 : 0);
   S.mode = 5;
+  if (host_a) c->pristine = false;
   S.lanes_per_row = g;
   const int64_t rows = c->nflow * c->nbatch;
   S.tasks_completed = (h.done.v == rows) ? c->ntasks * c->nbatch : 0;
@@ -1252,6 +1262,39 @@ tcg_status tcg_factor_host(tcg_ctx* c, const double* values_in, double* values_o
   TCG_CUDA_TRY(c, cudaSetDevice(c->device));
   const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
   return run_flow(c, S, threads, values_in, values_out);
+}
+
+tcg_status tcg_factor_host_a(tcg_ctx* c, const double* a_values, double* values_out, tcg_stats* st) {
+  if (!c || !c->uploaded || ((!a_values && c->nnz_a > 0) || (!values_out && c->nnz > 0))) return TCG_INVALID;
+  if (!c->a_map) {
+    c->err = "tcg_factor_host_a: the problem has no A -> U map (duplicate entries in A?)";
+    return TCG_INVALID;
+  }
+  const bool flow = c->has_flow && c->nnz > 0 && c->ntasks > 0 && (c->opt.mode == 0 || c->opt.mode == 5);
+  if (!flow) {  // other modes: the same steps, one after the other
+    tcg_status r = tcg_set_a_values(c, c->nbatch, a_values);
+    if (r != TCG_OK) return r;
+    const tcg_status f = tcg_factor(c, st);
+    r = c->nbatch > 1 ? tcg_download_batch(c, values_out) : tcg_download(c, values_out);
+    return f != TCG_OK ? f : r;
+  }
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  const int64_t need = c->nnz_a * c->nbatch;  // staging for A (outside the timed region)
+  if (need > c->a_stage_len) {
+    TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->a_stage) TCG_CUDA_TRY(c, cudaFree(c->a_stage));
+    c->a_stage = nullptr;
+    TCG_CUDA_TRY(c, cudaMalloc(&c->a_stage, sizeof(double) * std::max<int64_t>(need, 1)));
+    c->a_stage_len = need;
+  }
+  tcg_stats local{};
+  tcg_stats& S = st ? *st : local;
+  S = tcg_stats{};
+  S.breakdown_row = -1;
+  S.breakdown_member = -1;
+  S.batch = c->nbatch;
+  const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
+  return run_flow(c, S, threads, nullptr, values_out, 0, a_values);
 }
 
 tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {

@@ -538,3 +538,33 @@ def test_device_init_batch(T, oracle):
             assert bitwise_equal(out[i], ref), i
     finally:
         fz.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c5_m0", "s27_16_k2", "c2"])
+def test_factor_host_a_end_to_end(T, golden, oracle, name):
+    # PᵀAP's values in, factor out in one call (tcg_factor_host_a): the
+    # reference's factor_by_blocks inputs, bitwise the golden factor
+    _, an = analyzed(name)
+    fz = T.GpuFactorizer(planned(name), T.GpuOptions(timeout_s=30))
+    try:
+        for _ in range(2):  # the restore copy it leaves behind is the initialised U
+            out = fz.factor_host_a(an.a_permuted.values)
+            check_against_oracle(name, out, golden, oracle)
+        assert fz.last.kernel_launches == 3
+        fz.restore()
+        assert bitwise_equal(fz.download(), planned(name).tables()["values"])
+    finally:
+        fz.close()
+
+
+def test_factor_host_a_batch(T, oracle):
+    an, vals, perms = c5_members(T, [0, 3, 7])
+    fz = T.GpuFactorizer(planned("c5_m0"), T.GpuOptions(timeout_s=30))
+    try:
+        fz.set_a_values(np.stack([ap.values for ap in perms]))
+        out = fz.factor_host_a(np.stack([ap.values for ap in perms]).ravel())
+        for i, ap in enumerate(perms):
+            ref, _, _, _ = oracle.factor_serial(ap, an.pattern.pattern)
+            assert bitwise_equal(out[i * fz.nnz:(i + 1) * fz.nnz], ref), i
+    finally:
+        fz.close()
