@@ -13,9 +13,11 @@ from its device copy and L2 is flushed (256 MiB write), both untimed.
          persistent kernel on the stream it is launched on.
   e2e    the same metric through the C ABI with host buffers
          (tcg_factor_host_a): H2D of PaP's values (the reference call's
-         input) from pinned memory, init_factor_values on the device, factor,
-         D2H of the factor, one stream-ordered call; the symbolic structure
-         (plan) stays resident, as in a refactorization.
+         input) from pinned memory, init_factor_values on the device, factor
+         -- with CTAs of the same launch copying each group of factor values
+         to the pinned host buffer as soon as it is final, so the D2H
+         overlaps the factorization --, one stream-ordered call; the symbolic
+         structure (plan) stays resident, as in a refactorization.
   roofline  algorithmic bytes 20*nnz_u + 8*(n+1) per
          launch / kernel time, against the measured HBM copy bandwidth.
 
@@ -336,7 +338,9 @@ def run_ours(args):
                    "parity_vs_oracle": parity},
         "e2e": {"value": units / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz_a * per_rank,
                 "d2h_bytes_per_step": 8 * nnz * per_rank, "ms_per_step": e2e,
-                "call": "tcg_factor_host_a: PaP values in (host), device init_factor_values, factor, factor out",
+                "call": "tcg_factor_host_a: PaP values in (host), device init_factor_values, factor; the factor "
+                        "leaves through CTAs of the same launch as it becomes final (drain)",
+                "drain_ctas": int(st_e2e.drain_ctas),
                 "launches": int(st_e2e.kernel_launches)},
         "gpu_launches": launches_per_step * args.steps,
         "launches_per_step": ({"flow_prepare (timed)": 1, "factor_flow (timed)": 1} if st.mode == 5 else

@@ -162,6 +162,8 @@ typedef struct {
   int32_t lanes_per_row;     /* mode 5: lanes per row used */
   int32_t batch;             /* mode 5: value sets factored by the call */
   int32_t breakdown_member;  /* batch: member of breakdown_row (-1 when none) */
+  int32_t drain_ctas;        /* end to end: CTAs that copied the factor to the host during the
+                                launch (0: a D2H copy after it) */
 } tcg_stats;
 
 typedef struct {

@@ -123,6 +123,7 @@ class Stats(C.Structure):
         ("lanes_per_row", C.c_int32),
         ("batch", C.c_int32),
         ("breakdown_member", C.c_int32),
+        ("drain_ctas", C.c_int32),
     ]
 
 

@@ -118,6 +118,8 @@ struct tcg_ctx {
   bool has_units = false;
   int* a_map = nullptr;      // device init_factor_values (in the arena)
   double* a_stage = nullptr; // staging for A's values (separate allocation, grown on demand)
+  unsigned* drain_done = nullptr;  // end-to-end drain: groups copied per 1,024 values
+  std::int64_t drain_len = 0;
   std::int64_t nnz_a = 0, a_stage_len = 0;
   double** peers = nullptr;  // sharded runs: device table of every part's U (own included)
   int npeers = 0;
@@ -399,6 +401,7 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
 void tcg_destroy(tcg_ctx* c) {
   if (c && c->batch_arena) cudaFree(c->batch_arena);
   if (c && c->a_stage) cudaFree(c->a_stage);
+  if (c && c->drain_done) cudaFree(c->drain_done);
   if (c && c->peers) cudaFree(c->peers);
   if (c)
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -700,10 +703,28 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (const char* e = std::getenv("TCG_FLOW_PIPE")) pipe = pipe && std::atoi(e) != 0;
   int extras = (c->nbatch > 1 || c->opt.trace) ? 1 : 0;
   if (const char* e = std::getenv("TCG_FLOW_EXTRAS")) extras = std::atoi(e) ? 1 : extras;
+  // end to end: CTAs of the launch copy the factor to the host as it becomes
+  // final (the D2H overlaps the factorization); needs a pinned, mapped buffer
+  double* drain_out = nullptr;
+  // about one drain CTA per 128 K values of U, 4 to 32 (B200: C2 16, C6 32)
+  int drain_ctas = static_cast<int>(std::min<int64_t>(32, std::max<int64_t>(4, c->nnz >> 17)));
+  if (const char* e = std::getenv("TCG_DRAIN_CTAS")) drain_ctas = std::max(1, std::atoi(e));
+  bool drain = host_out && pipe && !remote && extras == 0 && c->nbatch == 1 && c->nflow > 0 && phase == 0;
+  if (const char* e = std::getenv("TCG_DRAIN")) drain = drain && std::atoi(e) != 0;
+  if (drain) {
+    cudaPointerAttributes attr{};
+    if (cudaPointerGetAttributes(&attr, host_out) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+        attr.devicePointer)
+      drain_out = static_cast<double*>(attr.devicePointer);
+    else
+      cudaGetLastError();
+    drain = drain_out != nullptr;
+  }
   int occ = 0;
-  if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ) != cudaSuccess) {
+  if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0) != cudaSuccess) {
     cudaGetLastError();
     pipe = false;
+    drain = false;
   }
   cudaError_t oe = pipe ? cudaSuccess : tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
   if (oe == cudaErrorInvalidValue && kb != 4) {  // no such variant: the KB = 4 one
@@ -717,6 +738,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   }
   if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
   const int grid = std::max(1, occ * c->sm_count);
+  if (drain && grid <= drain_ctas) drain = false;
   const bool batch = c->nbatch > 1;
   if (static_cast<int64_t>(c->nflow) * c->nbatch > 0x7fffffffLL) {
     c->err = "value-flow batch: rows x members beyond 2^31";
@@ -755,6 +777,19 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   P.nnz = c->nnz;
   P.nbatch = c->nbatch;
   P.nrows = static_cast<int>(c->nflow);
+  P.row_ctas = drain ? grid - drain_ctas : grid;
+  const long long drain_words = (c->nnz + 1023) / 1024;
+  if (drain) {
+    if (drain_words > c->drain_len) {
+      TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+      if (c->drain_done) TCG_CUDA_TRY(c, cudaFree(c->drain_done));
+      c->drain_done = nullptr;
+      TCG_CUDA_TRY(c, cudaMalloc(&c->drain_done, sizeof(unsigned) * drain_words));
+      c->drain_len = drain_words;
+    }
+    P.drain_out = drain_out;
+    P.drain_done = c->drain_done;
+  }
   const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
   const size_t vbytes = sizeof(double) * static_cast<size_t>(c->nnz) * c->nbatch;
@@ -777,13 +812,17 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
                                                c->nnz_a, c->nbatch, c->sm_count, c->stream));
   }
   if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
+  if (drain) TCG_CUDA_TRY(c, cudaMemsetAsync(c->drain_done, 0, sizeof(unsigned) * drain_words, c->stream));
   if (c->nflow > 0) {
-    if (pipe) TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, extras, c->stream));
+    if (pipe)
+      TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, extras, c->stream,
+                                               drain ? 1 : 0));
     else TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
   }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
   c->pristine = false;  // the working values now hold the factor
-  if (host_out) TCG_CUDA_TRY(c, cudaMemcpyAsync(host_out, vals, vbytes, cudaMemcpyDeviceToHost, c->stream));
+  if (host_out && !drain)
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(host_out, vals, vbytes, cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
                                   cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -796,6 +835,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   S.staging_cap = kb;  // reported: gather batch
   S.kernel_launches = (c->nflow > 0 ? 1 : 0) + (phase == 0 ? 1 : 0) + (host_a ? 1 : 0);
   S.mode = 5;
+  S.drain_ctas = drain ? drain_ctas : 0;
   if (host_a) c->pristine = false;
   S.lanes_per_row = g;
   const int64_t rows = c->nflow * c->nbatch;

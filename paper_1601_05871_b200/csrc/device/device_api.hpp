@@ -26,9 +26,10 @@ cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStrea
 cudaError_t launch_flow(const FlowParams& p, int grid, int threads, int kb, int minb, int g,
                         int weak, int dyn, int remote, cudaStream_t st);
 
-cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm);
+cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm,
+                           int drain = 0);
 cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb, int minb, int remote,
-                             int extras, cudaStream_t st);
+                             int extras, cudaStream_t st, int drain = 0);
 cudaError_t launch_init_values(const double* a, const int* map, double* vals, double* vals0, long long nnz,
                                long long nnz_a, int nbatch, int sm_count, cudaStream_t st);
 cudaError_t unit_occupancy(int threads, int kb, int minb, int weak, size_t smem, int* ctas_per_sm);

@@ -123,6 +123,11 @@ struct FlowParams {
   double* const* peers;  // sharded (C6): every part's U, indexed by part; operands of other parts
   int npeers;            //   arrive as kRemoteBit | part << 25 | position (plan.hpp build_flow_part)
   unsigned long long timeout_ns;
+  // drain (end to end, factor_flow_pipe DRAIN = 1): CTAs [row_ctas, grid) copy
+  // final values to the host while the rows run
+  double* drain_out;     // device-accessible pinned host buffer (nnz values)
+  unsigned* drain_done;  // per batch of 32 groups of 32 values: groups copied (zeroed per launch)
+  int row_ctas;          // CTAs that run rows
 };
 
 // Block units (mode 6, flow_kernel.cu factor_units); rows outside units use

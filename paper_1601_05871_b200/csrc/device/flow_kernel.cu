@@ -366,6 +366,52 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
   }
 }
 
+// Drain (end to end): the warps of the CTAs past P.row_ctas copy U to the
+// host while the rows run. A value is final as soon as it no longer reads
+// kUnset (it is written once), so a warp copies every group of 32 values
+// whose 32 loads all see final values -- 256-byte coalesced stores into the
+// pinned host buffer -- and comes back later for groups that are not final
+// yet (a bit per group in P.drain_done; a sweep that copies nothing backs
+// off for a microsecond, so its re-reads do not crowd the lines the rows are
+// writing). Warp d owns a contiguous slice of the 1,024-value batches.
+// (16-byte loads and stores with eight groups in flight per warp raised the
+// kernel to 80 registers and re-read unfinished lines harder: C2 end to end
+// 0.83 -> 1.99 ms with 16 drain CTAs.)
+__device__ void drain_values(const FlowParams& P, int dw, int DW) {
+  const int lane = threadIdx.x & 31;
+  const long long nb = (P.nnz + 1023) / 1024;
+  const long long b0 = nb * dw / DW, b1 = nb * (dw + 1) / DW;
+  const unsigned long long t0 = gtimer();
+  long long low = b0;  // batches below are copied
+  while (low < b1) {
+    bool progressed = false;
+    for (long long b = low; b < b1; ++b) {
+      unsigned done = P.drain_done[b];
+      if (done == 0xffffffffu) {
+        if (b == low) ++low;
+        continue;
+      }
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        if ((done >> j) & 1u) continue;
+        const long long x = (b * 32 + j) * 32 + lane;
+        const unsigned long long v = x < P.nnz ? ld_relaxed_u64(P.vals + x) : 0ull;
+        if (__ballot_sync(kFull, v != kUnset) != kFull) continue;
+        if (x < P.nnz) P.drain_out[x] = __longlong_as_double(static_cast<long long>(v));
+        done |= 1u << j;
+        progressed = true;
+      }
+      if (lane == 0) P.drain_done[b] = done;
+      __syncwarp();
+      if (done == 0xffffffffu && b == low) ++low;
+    }
+    if (!progressed && low < b1) {
+      if (ld_relaxed(&P.ctrl->error.v) || gtimer() - t0 > P.timeout_ns) return;  // the rows report it
+      __nanosleep(1000);
+    }
+  }
+}
+
 // factor_flow with the per-row metadata staged in shared memory (PIPE): a
 // row of a short program is shorter than an L2 round trip, so prefetching its
 // record and first slot one row ahead in registers still exposes the round
@@ -376,7 +422,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
 // (G = 32, static hand-out.)
 // EXTRAS = 0: a single matrix without trace stamps (no batch member
 // arithmetic, no stamp branches); 1: batches and traces.
-template <int THREADS, int KB, int MINB, int REMOTE, int EXTRAS>
+template <int THREADS, int KB, int MINB, int REMOTE, int EXTRAS, int DRAIN = 0>
 __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) {
   constexpr int kWarps = THREADS / 32;
   constexpr int kLenMask = (1 << 30) - 1;
@@ -388,7 +434,12 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
   __shared__ Ring rings[kWarps];
   const int lane = threadIdx.x & 31;
   Ring& R = rings[threadIdx.x >> 5];
-  const int W = gridDim.x * kWarps;
+  if (DRAIN && static_cast<int>(blockIdx.x) >= P.row_ctas) {
+    drain_values(P, (blockIdx.x - P.row_ctas) * kWarps + (threadIdx.x >> 5),
+                 (gridDim.x - P.row_ctas) * kWarps);
+    return;
+  }
+  const int W = (DRAIN ? P.row_ctas : static_cast<int>(gridDim.x)) * kWarps;
   const int w0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
   Ctx<0, REMOTE ? 2 : 0> C{P, gtimer(), P.vals, P.a, 0};
   int ran = 0, executed = 0, anyfail = 0;
@@ -718,31 +769,33 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
   return cudaGetLastError();
 }
 
-#define TCG_PIPE_VARIANTS(X)                                                                       \
-  X(256, 2, 3, 0, 0) X(256, 3, 3, 0, 0) X(256, 4, 3, 0, 0) X(256, 2, 3, 0, 1) X(256, 3, 3, 0, 1) \
-  X(256, 4, 3, 0, 1) X(256, 2, 3, 1, 1) X(256, 3, 3, 1, 1) X(256, 4, 3, 1, 1)
+// (threads, KB, CTAs/SM, remote operands, extras, drain)
+#define TCG_PIPE_VARIANTS(X)                                                                               \
+  X(256, 2, 3, 0, 0, 0) X(256, 3, 3, 0, 0, 0) X(256, 4, 3, 0, 0, 0) X(256, 2, 3, 0, 1, 0) X(256, 3, 3, 0, 1, 0) \
+  X(256, 4, 3, 0, 1, 0) X(256, 2, 3, 1, 1, 0) X(256, 3, 3, 1, 1, 0) X(256, 4, 3, 1, 1, 0)                     \
+  X(256, 2, 3, 0, 0, 1) X(256, 3, 3, 0, 0, 1) X(256, 4, 3, 0, 0, 1)
 
-static const void* pipe_kernel_for(int threads, int kb, int minb, int remote, int extras) {
-#define X(T, K, M, R, E)                                                     \
-  if (threads == T && kb == K && minb == M && remote == R && extras == E)    \
-    return reinterpret_cast<const void*>(&factor_flow_pipe<T, K, M, R, E>);
+static const void* pipe_kernel_for(int threads, int kb, int minb, int remote, int extras, int drain) {
+#define X(T, K, M, R, E, D)                                                                 \
+  if (threads == T && kb == K && minb == M && remote == R && extras == E && drain == D)     \
+    return reinterpret_cast<const void*>(&factor_flow_pipe<T, K, M, R, E, D>);
   TCG_PIPE_VARIANTS(X)
 #undef X
   return nullptr;
 }
 
-cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm) {
-  const void* k = pipe_kernel_for(threads, kb, minb, remote, extras);
+cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm, int drain) {
+  const void* k = pipe_kernel_for(threads, kb, minb, remote, extras, drain);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
 }
 
 cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb, int minb, int remote,
-                             int extras, cudaStream_t st) {
-#define X(T, K, M, R, E)                                                          \
-  if (threads == T && kb == K && minb == M && remote == R && extras == E) {       \
-    factor_flow_pipe<T, K, M, R, E><<<grid, T, 0, st>>>(p);                       \
-    return cudaGetLastError();                                                    \
+                             int extras, cudaStream_t st, int drain) {
+#define X(T, K, M, R, E, D)                                                                   \
+  if (threads == T && kb == K && minb == M && remote == R && extras == E && drain == D) {     \
+    factor_flow_pipe<T, K, M, R, E, D><<<grid, T, 0, st>>>(p);                                \
+    return cudaGetLastError();                                                                \
   }
   TCG_PIPE_VARIANTS(X)
 #undef X

@@ -568,3 +568,52 @@ def test_factor_host_a_batch(T, oracle):
             assert bitwise_equal(out[i * fz.nnz:(i + 1) * fz.nnz], ref), i
     finally:
         fz.close()
+
+
+@pytest.mark.parametrize("name", ["c1", "c5_m0", "s27_16_k2", "elast6_k1", "c2", "c4"])
+def test_drained_end_to_end(T, golden, oracle, name, monkeypatch):
+    # pinned host output: CTAs of the launch copy the factor out while the rows
+    # run (tcg_factor_host[_a] drain); the result is the golden factor bit for bit
+    import torch
+    _, an = analyzed(name)
+    plan = planned(name)
+    fz = T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30))
+    try:
+        a_in = torch.from_numpy(an.a_permuted.values.copy()).pin_memory()
+        u_in = torch.from_numpy(plan.tables()["values"]).pin_memory()
+        for ctas in ("1", "2", "4"):
+            monkeypatch.setenv("TCG_DRAIN_CTAS", ctas)
+            out = torch.full((fz.nnz,), float("nan"), dtype=torch.float64).pin_memory()
+            st = fz.factor_host_a_ptr(a_in.data_ptr(), out.data_ptr())
+            assert st.drain_ctas == int(ctas)
+            check_against_oracle(name, out.numpy().copy(), golden, oracle)
+            out.fill_(float("nan"))
+            st = fz.factor_host_ptr(u_in.data_ptr(), out.data_ptr())
+            assert st.drain_ctas == int(ctas)
+            check_against_oracle(name, out.numpy().copy(), golden, oracle)
+        monkeypatch.setenv("TCG_DRAIN", "0")
+        out = torch.zeros(fz.nnz, dtype=torch.float64).pin_memory()
+        assert fz.factor_host_a_ptr(a_in.data_ptr(), out.data_ptr()).drain_ctas == 0
+        check_against_oracle(name, out.numpy().copy(), golden, oracle)
+        # pageable output: no drain, a copy after the launch
+        monkeypatch.delenv("TCG_DRAIN")
+        assert fz.factor_host_a(an.a_permuted.values) is not None and fz.last.drain_ctas == 0
+    finally:
+        fz.close()
+
+
+def test_drained_end_to_end_breakdown(T):
+    # an indefinite matrix: the rows after the failing pivot are skipped and
+    # keep their inputs, so the drain still finishes; BreakdownError as usual
+    import torch
+    a, fp, rl = small(T, 4, sym([(0, 0, 1.0), (1, 1, 1.0), (2, 2, 1.0), (2, 3, 4.0), (3, 3, 1.0)]),
+                      bounds=[0, 2, 4])
+    fz = T.GpuFactorizer(T.Plan(a, fp, rl), T.GpuOptions(timeout_s=30))
+    try:
+        u_in = torch.from_numpy(T.init_factor_values(a, fp)).pin_memory()
+        out = torch.zeros(fz.nnz, dtype=torch.float64).pin_memory()
+        with pytest.raises(T.BreakdownError) as e:
+            fz.factor_host_ptr(u_in.data_ptr(), out.data_ptr())
+        assert e.value.row == 3 and fz.last.drain_ctas > 0
+    finally:
+        fz.close()
