@@ -205,6 +205,26 @@ def run_reference(args):
     print(json.dumps(line))
 
 
+def chain_hop_us(dev: int) -> float:
+    """Measured latency of one value hand-off between dependent rows: the
+    factor of a 1,000-row tridiagonal matrix (IC(0), one range) is a pure
+    chain of 1,000 finalising rows (SURVEY §8(d)'s latency bound)."""
+    import numpy as np
+
+    import paper_1601_05871_b200 as T
+    n = 1000
+    a = T.generate("path", n)
+    fp = T.levelk_pattern(a, 0)
+    plan = T.Plan(a, fp, T.RangeList(np.array([0, n], np.int32)))
+    fz = T.GpuFactorizer(plan, T.GpuOptions(device=dev, mode=5))
+    ts = []
+    for _ in range(7):
+        fz.restore()
+        ts.append(fz.factor().device_ms)
+    fz.close()
+    return statistics.median(ts) * 1e3 / plan.stats().flow_depth
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -313,6 +333,7 @@ def run_ours(args):
                    "factor_by_blocks_pooled_s": statistics.median(times["pool"]),
                    "pooled_workers": min(os.cpu_count() or 1, 64)}
     peak, peak_kind = measured_peak()
+    hop_us = chain_hop_us(dev)
     bytes_alg = (20 * nnz + 8 * (n + 1)) * per_rank
     achieved = bytes_alg / (step_ms / 1e3) / 1e9
     launches_per_step = st.kernel_launches
@@ -348,6 +369,11 @@ def run_ours(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(args.config),
                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_alg},
+        # what actually binds: the dependence chain. Lower bound = value-flow depth x
+        # the measured hand-off latency of a pure chain on this GPU.
+        "latency_bound": {"flow_depth": int(ps.flow_depth), "hop_us": round(hop_us, 4),
+                          "bound_ms": round(ps.flow_depth * hop_us / 1e3, 4),
+                          "frac": round(ps.flow_depth * hop_us / 1e3 / step_ms, 4)},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }
