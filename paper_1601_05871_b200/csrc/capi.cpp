@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -118,7 +119,7 @@ struct tcg_ctx {
   bool has_units = false;
   int* a_map = nullptr;      // device init_factor_values (in the arena)
   double* a_stage = nullptr; // staging for A's values (separate allocation, grown on demand)
-  unsigned* drain_done = nullptr;  // end-to-end drain: groups copied per 1,024 values
+  unsigned* drain_done = nullptr;  // end-to-end drain: groups copied per 2,048 values
   std::int64_t drain_len = 0;
   std::int64_t nnz_a = 0, a_stage_len = 0;
   double** peers = nullptr;  // sharded runs: device table of every part's U (own included)
@@ -706,8 +707,10 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // end to end: CTAs of the launch copy the factor to the host as it becomes
   // final (the D2H overlaps the factorization); needs a pinned, mapped buffer
   double* drain_out = nullptr;
-  // about one drain CTA per 128 K values of U, 4 to 32 (B200: C2 16, C6 32)
-  int drain_ctas = static_cast<int>(std::min<int64_t>(32, std::max<int64_t>(4, c->nnz >> 17)));
+  // drain CTAs: 8, or 4 where long programs keep L2 busy (B200, end to end: C2 0.82 ms at 4-8,
+  // C4 4.09 at 8 / 4.47 at 4, C6 5.45 at 8 / 6.02 at 4, C3 (24.8 products per coordinate)
+  // 4.57 at 4 / 4.93 at 8; 16-32 no better anywhere)
+  int drain_ctas = mean > 16.0 ? 4 : 8;
   if (const char* e = std::getenv("TCG_DRAIN_CTAS")) drain_ctas = std::max(1, std::atoi(e));
   bool drain = host_out && pipe && !remote && extras == 0 && c->nbatch == 1 && c->nflow > 0 && phase == 0;
   if (const char* e = std::getenv("TCG_DRAIN")) drain = drain && std::atoi(e) != 0;
@@ -718,7 +721,9 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
       drain_out = static_cast<double*>(attr.devicePointer);
     else
       cudaGetLastError();
-    drain = drain_out != nullptr;
+    // 16-byte accesses on both sides (flow_kernel.cu drain_values)
+    drain = drain_out != nullptr && reinterpret_cast<std::uintptr_t>(drain_out) % 16 == 0 &&
+            reinterpret_cast<std::uintptr_t>(c->vals) % 16 == 0;
   }
   int occ = 0;
   if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0) != cudaSuccess) {
@@ -778,7 +783,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   P.nbatch = c->nbatch;
   P.nrows = static_cast<int>(c->nflow);
   P.row_ctas = drain ? grid - drain_ctas : grid;
-  const long long drain_words = (c->nnz + 1023) / 1024;
+  const long long drain_words = (c->nnz + 2047) / 2048;
   if (drain) {
     if (drain_words > c->drain_len) {
       TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));

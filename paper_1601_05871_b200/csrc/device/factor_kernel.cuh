@@ -126,7 +126,7 @@ struct FlowParams {
   // drain (end to end, factor_flow_pipe DRAIN = 1): CTAs [row_ctas, grid) copy
   // final values to the host while the rows run
   double* drain_out;     // device-accessible pinned host buffer (nnz values)
-  unsigned* drain_done;  // per batch of 32 groups of 32 values: groups copied (zeroed per launch)
+  unsigned* drain_done;  // per batch of 32 groups of 64 values: groups copied (zeroed per launch)
   int row_ctas;          // CTAs that run rows
 };
 

@@ -368,21 +368,24 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
 
 // Drain (end to end): the warps of the CTAs past P.row_ctas copy U to the
 // host while the rows run. A value is final as soon as it no longer reads
-// kUnset (it is written once), so a warp copies every group of 32 values
-// whose 32 loads all see final values -- 256-byte coalesced stores into the
-// pinned host buffer -- and comes back later for groups that are not final
-// yet (a bit per group in P.drain_done; a sweep that copies nothing backs
-// off for a microsecond, so its re-reads do not crowd the lines the rows are
-// writing). Warp d owns a contiguous slice of the 1,024-value batches.
-// (16-byte loads and stores with eight groups in flight per warp raised the
-// kernel to 80 registers and re-read unfinished lines harder: C2 end to end
-// 0.83 -> 1.99 ms with 16 drain CTAs.)
+// kUnset (it is written once), so a warp copies every group of 64 values
+// whose loads all see final values -- 16 bytes per lane, one coalesced
+// 512-byte store into the pinned host buffer -- and comes back later for
+// groups that are not final yet (a bit per group in P.drain_done; a sweep
+// that copies nothing backs off for a microsecond, so its re-reads do not
+// crowd the lines the rows are writing). Two groups are checked at once; warp
+// d owns a contiguous slice of the 2,048-value batches. Measured on B200
+// (end to end, wall): 8-byte accesses per lane in groups of 32 gave C2 0.82,
+// C6 5.75 ms; this layout C2 0.82, C6 5.48 ms; four groups in flight C2 0.89
+// ms; eight (80 registers, harder re-reads of unfinished lines) C2 1.99 ms.
 __device__ void drain_values(const FlowParams& P, int dw, int DW) {
+  constexpr int kIn = 2;
   const int lane = threadIdx.x & 31;
-  const long long nb = (P.nnz + 1023) / 1024;
+  const long long nb = (P.nnz + 2047) / 2048;
   const long long b0 = nb * dw / DW, b1 = nb * (dw + 1) / DW;
   const unsigned long long t0 = gtimer();
-  long long low = b0;  // batches below are copied
+  const bool even = (P.nnz & 1) == 0;
+  long long low = b0;
   while (low < b1) {
     bool progressed = false;
     for (long long b = low; b < b1; ++b) {
@@ -391,22 +394,43 @@ __device__ void drain_values(const FlowParams& P, int dw, int DW) {
         if (b == low) ++low;
         continue;
       }
-#pragma unroll 4
-      for (int j = 0; j < 32; ++j) {
-        if ((done >> j) & 1u) continue;
-        const long long x = (b * 32 + j) * 32 + lane;
-        const unsigned long long v = x < P.nnz ? ld_relaxed_u64(P.vals + x) : 0ull;
-        if (__ballot_sync(kFull, v != kUnset) != kFull) continue;
-        if (x < P.nnz) P.drain_out[x] = __longlong_as_double(static_cast<long long>(v));
-        done |= 1u << j;
-        progressed = true;
+      for (int j0 = 0; j0 < 32; j0 += kIn) {
+        unsigned long long va[kIn], vb[kIn];
+#pragma unroll
+        for (int j = 0; j < kIn; ++j) {
+          const long long x = (b * 32 + j0 + j) * 64 + 2 * lane;
+          va[j] = vb[j] = 0ull;
+          if ((done >> (j0 + j)) & 1u) continue;
+          if (even && x + 1 < P.nnz) {
+            ld_relaxed_v2_u64(P.vals + x, va[j], vb[j]);
+          } else {
+            if (x < P.nnz) va[j] = ld_relaxed_u64(P.vals + x);
+            if (x + 1 < P.nnz) vb[j] = ld_relaxed_u64(P.vals + x + 1);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kIn; ++j) {
+          if ((done >> (j0 + j)) & 1u) continue;
+          if (__ballot_sync(kFull, va[j] != kUnset && vb[j] != kUnset) != kFull) continue;
+          const long long x = (b * 32 + j0 + j) * 64 + 2 * lane;
+          if (even && x + 1 < P.nnz) {
+            *reinterpret_cast<double2*>(P.drain_out + x) =
+                make_double2(__longlong_as_double(static_cast<long long>(va[j])),
+                             __longlong_as_double(static_cast<long long>(vb[j])));
+          } else {
+            if (x < P.nnz) P.drain_out[x] = __longlong_as_double(static_cast<long long>(va[j]));
+            if (x + 1 < P.nnz) P.drain_out[x + 1] = __longlong_as_double(static_cast<long long>(vb[j]));
+          }
+          done |= 1u << (j0 + j);
+          progressed = true;
+        }
       }
       if (lane == 0) P.drain_done[b] = done;
       __syncwarp();
       if (done == 0xffffffffu && b == low) ++low;
     }
     if (!progressed && low < b1) {
-      if (ld_relaxed(&P.ctrl->error.v) || gtimer() - t0 > P.timeout_ns) return;  // the rows report it
+      if (ld_relaxed(&P.ctrl->error.v) || gtimer() - t0 > P.timeout_ns) return;
       __nanosleep(1000);
     }
   }

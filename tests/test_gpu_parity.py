@@ -598,6 +598,10 @@ def test_drained_end_to_end(T, golden, oracle, name, monkeypatch):
         # pageable output: no drain, a copy after the launch
         monkeypatch.delenv("TCG_DRAIN")
         assert fz.factor_host_a(an.a_permuted.values) is not None and fz.last.drain_ctas == 0
+        # a pinned buffer 8 bytes off 16-byte alignment: no drain either, same factor
+        big = torch.zeros(fz.nnz + 1, dtype=torch.float64).pin_memory()
+        assert fz.factor_host_a_ptr(a_in.data_ptr(), big.data_ptr() + 8).drain_ctas == 0
+        check_against_oracle(name, big.numpy()[1:].copy(), golden, oracle)
     finally:
         fz.close()
 
