@@ -163,6 +163,8 @@ def cpu_reference_times(an, workers: int, reps: int):
         _, st, secs, _, _, _ = R.factor_by_blocks(an.a_permuted, u, an.ranges.bounds, workers=workers,
                                                   want_values=False)
         out["pool"].append(secs)
+    # TaskPolicy::pooled(1) once (W = 1 and W = all cores)
+    out["pool1"] = [R.factor_by_blocks(an.a_permuted, u, an.ranges.bounds, workers=1, want_values=False)[2]]
     return out
 
 
@@ -331,7 +333,8 @@ def run_ours(args):
                               "the batch rate on 1 core is the same per member") if batched else
                              "3 x factor_serial on the full matrix (reference's fastest CPU path), median",
                    "factor_by_blocks_pooled_s": statistics.median(times["pool"]),
-                   "pooled_workers": min(os.cpu_count() or 1, 64)}
+                   "pooled_workers": min(os.cpu_count() or 1, 64),
+                   "factor_by_blocks_pooled1_s": times["pool1"][0]}
     peak, peak_kind = measured_peak()
     hop_us = chain_hop_us(dev)
     bytes_alg = (20 * nnz + 8 * (n + 1)) * per_rank
