@@ -21,12 +21,13 @@ out = torch.empty(fz.nnz, dtype=torch.float64).pin_memory()
 fz.restore()
 plain = statistics.median([(fz.restore(), fz.factor().device_ms)[1] for _ in range(9)])
 print(f"{name}: factor only {plain:.3f} ms (device)")
-for setting in ["0", "4", "8", "16", "32"]:
-    if setting == "0":
+settings = sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "4", "8", "16"]
+for dr in settings:
+    if dr == "0":
         os.environ["TCG_DRAIN"] = "0"
     else:
         os.environ.pop("TCG_DRAIN", None)
-        os.environ["TCG_DRAIN_CTAS"] = setting
+        os.environ["TCG_DRAIN_CTAS"] = dr
     wall, dev = [], []
     for _ in range(9):
         torch.cuda.synchronize()
