@@ -282,6 +282,9 @@ typedef struct {
   int64_t tier2_rows;        /* rows that outgrew the 512-slot tables (then 2,048 slots) */
   int32_t kernel_launches;
   int32_t grid_ctas;
+  int32_t single_pass;       /* 1: every shared-memory row was searched once (its row copied from
+                                scratch); 0: scratch was short and rows were searched again
+                                (scratch then grows for the next call) */
 } tcg_sym_stats;
 enum { TCG_SYM_ALL_SLOW = 1 };  /* tcg_sym_levelk flag: every row on the global-memory path */
 tcg_status tcg_sym_create(int device, tcg_sym** out);

@@ -166,6 +166,7 @@ class SymStats(C.Structure):
         ("tier2_rows", C.c_int64),
         ("kernel_launches", C.c_int32),
         ("grid_ctas", C.c_int32),
+        ("single_pass", C.c_int32),
     ]
 
 

@@ -352,6 +352,7 @@ class SymbolicStats:
     tier2_rows: int
     kernel_launches: int
     grid_ctas: int
+    single_pass: int = 1
 
 
 class GpuSymbolic:
@@ -389,7 +390,7 @@ class GpuSymbolic:
         self._check(self._lib.tcg_sym_download(self.h, rp.ctypes.data_as(N.i64p), ci.ctypes.data_as(N.i32p)))
         pat = CsrMatrix(n, n, rp, ci[:int(s.nnz_u)].copy(), np.ones(int(s.nnz_u)))
         st = SymbolicStats(s.device_ms, s.host_ms, int(s.nnz_u), int(s.nnz_triu_input), int(s.slow_rows), int(s.tier2_rows),
-                           int(s.kernel_launches), int(s.grid_ctas))
+                           int(s.kernel_launches), int(s.grid_ctas), int(s.single_pass))
         return FillPattern(pat, level, int(s.nnz_triu_input)), st
 
     def close(self):

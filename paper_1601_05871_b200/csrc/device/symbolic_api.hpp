@@ -25,12 +25,20 @@ struct SymParams {
   int* nover;
   int* slow_mark;            // slow path: per slot n stamps
   int* slow_front;           // slow path: per slot 2 n frontier entries
+  // single pass: the count pass also writes each row ({i} then its targets,
+  // sorted) into scratch at a reserved offset; a copy kernel moves the rows
+  // into place after the scan. Rows that found no room (-1) are searched again.
+  int* scratch;
+  long long scratch_cap;
+  unsigned long long* cursor;
+  long long* soff;           // per row: its offset in scratch, or -1
 };
 
 size_t sym_smem_bytes(int hb);
 cudaError_t sym_occupancy(int hb, int* ctas_per_sm);
 cudaError_t launch_levelk_fast(const SymParams& p, int pass, int hb, int grid, cudaStream_t st);
 cudaError_t launch_levelk_slow(const SymParams& p, int pass, int grid, cudaStream_t st);
+cudaError_t launch_levelk_copy(const SymParams& p, int grid, cudaStream_t st);
 cudaError_t sym_scan(const long long* count, long long* u_ptr, int n, void* temp, size_t* temp_bytes,
                      cudaStream_t st);
 

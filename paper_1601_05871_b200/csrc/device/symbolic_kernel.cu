@@ -23,9 +23,13 @@
 // with an n-entry stamp array and n-entry frontier lists in global memory, and
 // targets emitted by scanning the stamps in (i, n) -- no capacity limit.
 //
-// Two passes: count (row lengths; a device scan turns them into row_ptr),
-// then fill (the search again, targets sorted by rank in shared memory). All
-// work is integer; the output is bit-exact by construction.
+// One search per row: the count pass also writes the row ({i}, then the
+// targets rank-sorted in shared memory) into a scratch array at an offset it
+// reserves with an atomic; a device scan turns the lengths into row_ptr and a
+// copy kernel moves the rows into place. Rows that find no room in scratch
+// (its size adapts to the last run) and the global-memory rows are searched
+// again after the scan. All work is integer; the output is bit-exact by
+// construction.
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
@@ -188,6 +192,7 @@ __global__ void __launch_bounds__(kSymThreads) levelk_fast(SymParams P) {
   const int nrows = P.list ? *P.nlist : P.n;
   for (int r = blockIdx.x * (kSymThreads / 32) + (threadIdx.x >> 5); r < nrows; r += nw) {
     const int i = P.list ? P.list[r] : r;
+    if (PASS == 1 && P.soff && P.soff[i] >= 0) continue;  // already written by the count pass
     // overflow is a property of the row, so the fill pass skips exactly the
     // rows the count pass handed on
     const bool ok = search_fast<HB>(P, S, i, lane);
@@ -199,12 +204,24 @@ __global__ void __launch_bounds__(kSymThreads) levelk_fast(SymParams P) {
       continue;
     }
     const int m = drain_targets<HB>(S, i, lane);
+    int* out = nullptr;
     if (PASS == 0) {
-      if (lane == 0) P.count[i] = 1 + m;
-      continue;
+      long long off = -1;
+      if (P.scratch && lane == 0) {
+        off = static_cast<long long>(atomicAdd(P.cursor, static_cast<unsigned long long>(m + 1)));
+        if (off + m + 1 > P.scratch_cap) off = -1;
+      }
+      off = __shfl_sync(kFullMask, off, 0);
+      if (lane == 0) {
+        P.count[i] = 1 + m;
+        if (P.soff) P.soff[i] = off;
+      }
+      if (off < 0) continue;
+      out = P.scratch + off;
+    } else {
+      out = P.u_col + P.u_ptr[i];
     }
     // rank sort (keys are distinct)
-    int* out = P.u_col + P.u_ptr[i];
     if (lane == 0) out[0] = i;
     for (int e = lane; e < m; e += 32) {
       const int x = S.ins[e];
@@ -283,6 +300,23 @@ __global__ void __launch_bounds__(kSymThreads) levelk_slow(SymParams P) {
     }
     __syncwarp();
   }
+}
+
+// Rows the count pass wrote into scratch move into place (warp per row).
+__global__ void __launch_bounds__(kSymThreads) levelk_copy(SymParams P) {
+  const int lane = threadIdx.x & 31;
+  const int nw = gridDim.x * (kSymThreads / 32);
+  for (int i = blockIdx.x * (kSymThreads / 32) + (threadIdx.x >> 5); i < P.n; i += nw) {
+    const long long off = P.soff[i];
+    if (off < 0) continue;
+    const long long b = P.u_ptr[i], len = P.u_ptr[i + 1] - b;
+    for (long long e = lane; e < len; e += 32) P.u_col[b + e] = P.scratch[off + e];
+  }
+}
+
+cudaError_t launch_levelk_copy(const SymParams& p, int grid, cudaStream_t st) {
+  levelk_copy<<<grid, kSymThreads, 0, st>>>(p);
+  return cudaGetLastError();
 }
 
 size_t sym_smem_bytes(int hb) {

@@ -35,6 +35,10 @@ struct tcg_sym {
   int64_t cap_nnz = -1;
   void* scan_tmp = nullptr;
   size_t scan_bytes = 0;
+  long long* soff = nullptr;        // per row: offset of its copy in scratch, or -1
+  unsigned long long* cursor = nullptr;
+  int* scratch = nullptr;           // rows written by the count pass
+  int64_t scratch_cap = 0;          // ints; grown to the last run's need
 };
 
 namespace {
@@ -70,6 +74,10 @@ void free_problem(tcg_sym* s) {
   free_dev(s->mark);
   free_dev(s->front);
   free_dev(s->scan_tmp);
+  free_dev(s->soff);
+  free_dev(s->cursor);
+  free_dev(s->scratch);
+  s->scratch_cap = 0;
   s->u_cap = 0;
   s->slow_slots = 0;
   s->cap_mark = 0;
@@ -152,6 +160,8 @@ tcg_status tcg_sym_upload(tcg_sym* s, const tcg_csr_view* a) {
     SYM_TRY(s, cudaMalloc(&s->count, sizeof(long long) * np1));
     SYM_TRY(s, cudaMalloc(&s->u_ptr, sizeof(long long) * np1));
     SYM_TRY(s, cudaMalloc(&s->over, sizeof(int) * (2 * np1 + 2)));
+    SYM_TRY(s, cudaMalloc(&s->soff, sizeof(long long) * np1));
+    SYM_TRY(s, cudaMalloc(&s->cursor, sizeof(unsigned long long)));
     s->cap_n = a->n;
     s->cap_nnz = a->nnz;
   }
@@ -208,9 +218,20 @@ tcg_status tcg_sym_levelk(tcg_sym* s, int32_t level, int32_t flags, tcg_sym_stat
   const int grid1 = std::max(1, std::min(s->sm_count * std::max(occ1, 1), (n + warps - 1) / warps));
   const int grid2 = std::max(1, s->sm_count * std::max(occ2, 1));
   int launches = 0;
+  if (s->scratch_cap == 0) {  // first run: about the pattern of a level-1 fill; then what the last run used
+    const int64_t want = 2 * s->nnz_a + n + 1024;
+    SYM_TRY(s, cudaMalloc(&s->scratch, sizeof(int) * static_cast<size_t>(want)));
+    s->scratch_cap = want;
+  }
+  P.scratch = s->scratch;
+  P.scratch_cap = s->scratch_cap;
+  P.cursor = s->cursor;
+  P.soff = s->soff;
   SYM_TRY(s, cudaEventRecord(s->ev0, s->stream));
   SYM_TRY(s, cudaMemsetAsync(s->count + n, 0, sizeof(long long), s->stream));
   SYM_TRY(s, cudaMemsetAsync(counters, 0, 2 * sizeof(int), s->stream));
+  SYM_TRY(s, cudaMemsetAsync(s->cursor, 0, sizeof(unsigned long long), s->stream));
+  SYM_TRY(s, cudaMemsetAsync(s->soff, 0xFF, sizeof(long long) * (static_cast<size_t>(n) + 1), s->stream));
   int cnt[2] = {0, 0};
   if (flags & TCG_SYM_ALL_SLOW) {  // test hook: every row through the global-memory path
     std::vector<int> all(static_cast<size_t>(n));
@@ -260,8 +281,12 @@ tcg_status tcg_sym_levelk(tcg_sym* s, int32_t level, int32_t flags, tcg_sym_stat
   SYM_TRY(s, tcbdev::sym_scan(s->count, s->u_ptr, n, s->scan_tmp, &s->scan_bytes, s->stream));
   ++launches;
   long long nnz_u = 0;
+  unsigned long long used = 0;
   SYM_TRY(s, cudaMemcpyAsync(&nnz_u, s->u_ptr + n, sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
+  SYM_TRY(s, cudaMemcpyAsync(&used, s->cursor, sizeof(used), cudaMemcpyDeviceToHost, s->stream));
   SYM_TRY(s, cudaStreamSynchronize(s->stream));
+  // rows that found no room in scratch are searched again below
+  const bool short_scratch = static_cast<int64_t>(used) > s->scratch_cap;
   if (nnz_u >= (int64_t{1} << 31)) {
     s->err = "tcg_sym_levelk: the pattern has 2^31 entries or more";
     return TCG_INVALID;
@@ -273,6 +298,10 @@ tcg_status tcg_sym_levelk(tcg_sym* s, int32_t level, int32_t flags, tcg_sym_stat
   }
   P.u_col = s->u_col;
   if (n > 0 && !(flags & TCG_SYM_ALL_SLOW)) {
+    SYM_TRY(s, tcbdev::launch_levelk_copy(P, grid1, s->stream));
+    ++launches;
+  }
+  if (n > 0 && !(flags & TCG_SYM_ALL_SLOW) && short_scratch) {
     tcbdev::SymParams A = P;
     A.list = nullptr;
     SYM_TRY(s, tcbdev::launch_levelk_fast(A, 1, tcbdev::kSymHashSmall, grid1, s->stream));
@@ -292,6 +321,14 @@ tcg_status tcg_sym_levelk(tcg_sym* s, int32_t level, int32_t flags, tcg_sym_stat
   SYM_TRY(s, cudaEventRecord(s->ev1, s->stream));
   SYM_TRY(s, cudaStreamSynchronize(s->stream));
   s->nnz_u = nnz_u;
+  if (short_scratch) {  // the next run fits in one pass
+    free_dev(s->scratch);
+    s->scratch_cap = 0;
+    const int64_t want = static_cast<int64_t>(used) + static_cast<int64_t>(used) / 8 + 1024;
+    SYM_TRY(s, cudaMalloc(&s->scratch, sizeof(int) * static_cast<size_t>(want)));
+    s->scratch_cap = want;
+  }
+  if (st) st->single_pass = short_scratch ? 0 : 1;
   if (st) {
     float ms = 0.f;
     SYM_TRY(s, cudaEventElapsedTime(&ms, s->ev0, s->ev1));

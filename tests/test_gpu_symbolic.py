@@ -171,3 +171,20 @@ def test_invalid_input_raises(T):
     a = T.CsrMatrix.from_arrays(2, [0, 1, 2], [0, 5])
     with pytest.raises(ValueError, match="out of range"):
         T.GpuSymbolic(a)
+
+
+def test_scratch_grows_to_a_single_pass(T):
+    # level 40 on a random graph fills far more than the first scratch guess:
+    # the short rows are searched again, scratch grows, the next call is one pass
+    a = T.generate("random_spd", 900, 6000, 2)
+    g = T.GpuSymbolic(a)
+    try:
+        first, s1 = g.levelk(40)
+        second, s2 = g.levelk(40)
+        assert s1.single_pass == 0 and s2.single_pass == 1
+        host = T.levelk_pattern(a, 40).pattern
+        assert same_pattern(first.pattern, host) and same_pattern(second.pattern, host)
+        small, s3 = g.levelk(1)  # and back to a small level on the grown scratch
+        assert s3.single_pass == 1 and same_pattern(small.pattern, T.levelk_pattern(a, 1).pattern)
+    finally:
+        g.close()
