@@ -323,6 +323,13 @@ tcg_status tcg_solve_apply(tcg_solve* s, const double* b, double* x, int32_t whi
 /* device vectors (b_dev and x_dev may alias), on the context's stream */
 tcg_status tcg_solve_apply_device(tcg_solve* s, const double* b_dev, double* x_dev, int32_t which,
                                   tcg_solve_stats* stats);
+/* The caller's other step per CG iteration: y = A x with the system matrix (PᵀAP), set once
+ * (host CSR with values, n x n), applied to device vectors on the context's stream; per row
+ * the products are summed in column order. */
+tcg_status tcg_solve_set_matrix(tcg_solve* s, const tcg_csr_view* a);
+tcg_status tcg_solve_spmv(tcg_solve* s, const double* x_dev, double* y_dev);
+/* The context's stream (cudaStream_t): everything above is ordered on it. */
+tcg_status tcg_solve_stream(tcg_solve* s, void** stream);
 /* With TCG_SOLVE_TRACE=1 in the environment: per schedule position (2 n) the globaltimer
  * stamps {start, operands final, end} of the last apply, and (recs != NULL) the position
  * records {entry begin, length | backward << 31, diagonal position, row} (16 bytes each). */

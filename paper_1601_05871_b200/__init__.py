@@ -30,6 +30,7 @@ from .core import (  # noqa: F401
     init_factor_values,
     levelk_pattern,
     levelk_pattern_gpu,
+    pcg,
     load_matrix_market,
     load_ordering,
     write_matrix_market,

@@ -232,6 +232,9 @@ SIGNATURES = [
     ("tcg_solve_error", C.c_char_p, [C.c_void_p]),
     ("tcg_solve_apply", C.c_int, [C.c_void_p, f64p, f64p, C.c_int32, C.POINTER(SolveStats)]),
     ("tcg_solve_trace", C.c_int, [C.c_void_p, u64p, C.c_void_p]),
+    ("tcg_solve_set_matrix", C.c_int, [C.c_void_p, C.POINTER(CsrView)]),
+    ("tcg_solve_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tcg_solve_stream", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     ("tcg_solve_apply_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(SolveStats)]),
     ("tch_generate", C.c_void_p, [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]),
     ("tch_matrix_from_csr", C.c_void_p, [C.POINTER(CsrView)]),

@@ -811,6 +811,24 @@ class GpuTriSolve:
             raise (SchedulerError if st == N.TCG_TIMEOUT else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
         return self.stats()
 
+    def set_matrix(self, a: CsrMatrix):
+        """The system matrix (PᵀAP) for spmv_ptr, uploaded once."""
+        st = self._lib.tcg_solve_set_matrix(self.h, C.byref(a.view()))
+        if st != N.TCG_OK:
+            raise (ValueError if st == N.TCG_INVALID else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
+
+    def spmv_ptr(self, x_ptr: int, y_ptr: int):
+        """y = A x on device vectors, on the context's stream (asynchronous)."""
+        st = self._lib.tcg_solve_spmv(self.h, C.c_void_p(x_ptr), C.c_void_p(y_ptr))
+        if st != N.TCG_OK:
+            raise (ValueError if st == N.TCG_INVALID else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
+
+    def stream_ptr(self) -> int:
+        out = C.c_void_p()
+        if self._lib.tcg_solve_stream(self.h, C.byref(out)) != N.TCG_OK:
+            raise ValueError("tcg_solve_stream failed")
+        return int(out.value or 0)
+
     def stats(self) -> SolveStats:
         s = self.last
         return SolveStats(s.device_ms, int(s.depth_forward), int(s.depth_backward), int(s.grid_ctas),
@@ -826,6 +844,66 @@ class GpuTriSolve:
             self.close()
         except Exception:
             pass
+
+
+@dataclass
+class PcgResult:
+    x: np.ndarray
+    iterations: int
+    converged: bool
+    relative_residual: float
+    seconds: float
+
+
+def pcg(solver: "GpuTriSolve", b, tol: float = 1e-8, maxit: int = 1000, precondition: bool = True,
+        device: int = 0) -> PcgResult:
+    """Conjugate gradients on PᵀAP x = b on the GPU, preconditioned with the
+    IC(k) factor the solver's context holds (z = (UᵀU)⁻¹ r through
+    tcg_solve_apply_device) -- the caller of the factorization. The system
+    matrix must be set (solver.set_matrix). Vectors and the dots live on the
+    device (torch, on the context's stream); one host read per iteration for
+    the convergence test."""
+    import torch
+    dev = torch.device("cuda", device)
+    stream = torch.cuda.ExternalStream(solver.stream_ptr(), device=dev)
+    t0 = time.perf_counter()
+    with torch.cuda.stream(stream):
+        bd = torch.as_tensor(np.ascontiguousarray(b, dtype=np.float64)).to(dev, non_blocking=False)
+        x = torch.zeros_like(bd)
+        r = bd.clone()
+        z = torch.empty_like(bd)
+        ap = torch.empty_like(bd)
+
+        def prec(src, dst):
+            if precondition:
+                solver.apply_device_ptr(src.data_ptr(), dst.data_ptr(), N.TCG_SOLVE_BOTH)
+            else:
+                dst.copy_(src)
+
+        bnorm = float(torch.linalg.vector_norm(bd).item())
+        if bnorm == 0.0:
+            return PcgResult(np.zeros(bd.numel()), 0, True, 0.0, time.perf_counter() - t0)
+        prec(r, z)
+        p = z.clone()
+        rz = torch.dot(r, z)
+        it, rel, converged = 0, 1.0, False
+        while it < maxit:
+            it += 1
+            solver.spmv_ptr(p.data_ptr(), ap.data_ptr())
+            alpha = rz / torch.dot(p, ap)
+            x.add_(alpha * p)
+            r.sub_(alpha * ap)
+            rel = float(torch.linalg.vector_norm(r).item()) / bnorm
+            if rel <= tol:
+                converged = True
+                break
+            prec(r, z)
+            rz_new = torch.dot(r, z)
+            p.mul_(rz_new / rz).add_(z)
+            rz = rz_new
+        out = x.cpu().numpy()
+    torch.cuda.synchronize(dev)
+    return PcgResult(out, it, converged, rel, time.perf_counter() - t0)
 
 
 def factor_by_blocks_gpu(a_permuted: CsrMatrix, fp: FillPattern, ranges: RangeList,

@@ -23,6 +23,10 @@ struct SolveParams {
 };
 
 cudaError_t solve_occupancy(int* ctas_per_sm);
+// y = A x for a CSR matrix (row_ptr int64, col int32, fp64), products summed in
+// column order (one thread per row)
+cudaError_t launch_spmv(int n, const long long* ptr, const int* col, const double* val, const double* x,
+                        double* y, int sm_count, cudaStream_t st);
 // fval[e] = u[pos[e]] for the forward entries (the factor in transposed order)
 cudaError_t launch_solve_gather(const double* u, const int* pos, double* fval, long long n, int sm_count,
                                 cudaStream_t st);

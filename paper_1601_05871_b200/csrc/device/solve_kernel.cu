@@ -135,6 +135,30 @@ cudaError_t launch_solve_gather(const double* u, const int* pos, double* fval, l
   return cudaGetLastError();
 }
 
+// The caller's other operation per CG iteration: y = A x with the system
+// matrix. HBM-bound (12 bytes per entry), one thread per row, sums in column
+// order; a stencil row is 7-81 entries, so the rows of a warp touch
+// neighbouring lines and L2 serves most of the gather of x.
+__global__ void spmv_csr(int n, const long long* __restrict__ ptr, const int* __restrict__ col,
+                         const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double s = 0.0;
+    for (long long q = __ldg(ptr + i), e = __ldg(ptr + i + 1); q < e; ++q)
+      s = __dadd_rn(s, __dmul_rn(__ldg(val + q), __ldg(x + __ldg(col + q))));
+    y[i] = s;
+  }
+}
+
+cudaError_t launch_spmv(int n, const long long* ptr, const int* col, const double* val, const double* x,
+                        double* y, int sm_count, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  int blocks = (n + 255) / 256;
+  blocks = blocks > 16 * sm_count ? 16 * sm_count : blocks;
+  spmv_csr<<<blocks, 256, 0, st>>>(n, ptr, col, val, x, y);
+  return cudaGetLastError();
+}
+
 cudaError_t solve_occupancy(int* ctas_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, trisolve_flow<kSolveThreads>, kSolveThreads,
                                                        0);

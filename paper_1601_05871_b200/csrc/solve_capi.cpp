@@ -42,6 +42,10 @@ struct tcg_solve {
   int* error = nullptr;
   unsigned long long* trace = nullptr;  // TCG_SOLVE_TRACE=1: per position {start, operands final, end}
   double timeout_s = 30.0;
+  void* a_arena = nullptr;  // the system matrix for tcg_solve_spmv (PᵀAP, CSR)
+  long long* a_ptr = nullptr;
+  int* a_col = nullptr;
+  double* a_val = nullptr;
 };
 
 namespace {
@@ -207,6 +211,7 @@ void tcg_solve_destroy(tcg_solve* s) {
   cudaDeviceSynchronize();
   if (s->arena) cudaFree(s->arena);
   if (s->trace) cudaFree(s->trace);
+  if (s->a_arena) cudaFree(s->a_arena);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
   delete s;
@@ -285,6 +290,64 @@ tcg_status tcg_solve_trace(tcg_solve* s, uint64_t* stamps, void* recs) {
   SOLVE_TRY(s, cudaSetDevice(s->device));
   SOLVE_TRY(s, cudaMemcpy(stamps, s->trace, sizeof(uint64_t) * 6 * static_cast<size_t>(s->n), cudaMemcpyDeviceToHost));
   if (recs) SOLVE_TRY(s, cudaMemcpy(recs, s->rec, sizeof(int4) * 2 * static_cast<size_t>(s->n), cudaMemcpyDeviceToHost));
+  return TCG_OK;
+}
+
+tcg_status tcg_solve_set_matrix(tcg_solve* s, const tcg_csr_view* a) {
+  if (!s || !a || a->n != s->n || a->nnz < 0 || !a->row_ptr || (a->nnz > 0 && (!a->col_idx || !a->values)) ||
+      a->row_ptr[0] != 0 || a->row_ptr[a->n] != a->nnz) {
+    if (s) s->err = "tcg_solve_set_matrix: the matrix must be n x n CSR with values";
+    return TCG_INVALID;
+  }
+  for (int32_t i = 0; i < a->n; ++i)
+    for (int64_t q = a->row_ptr[i]; q < a->row_ptr[i + 1]; ++q)
+      if (a->col_idx[q] < 0 || a->col_idx[q] >= a->n) {
+        s->err = "tcg_solve_set_matrix: column index out of range";
+        return TCG_INVALID;
+      }
+  SOLVE_TRY(s, cudaSetDevice(s->device));
+  if (s->a_arena) {
+    SOLVE_TRY(s, cudaDeviceSynchronize());
+    SOLVE_TRY(s, cudaFree(s->a_arena));
+    s->a_arena = nullptr;
+  }
+  const size_t np1 = static_cast<size_t>(a->n) + 1, nz = static_cast<size_t>(std::max<int64_t>(a->nnz, 1));
+  const size_t o_col = align_up(sizeof(long long) * np1, 256), o_val = o_col + align_up(sizeof(int) * nz, 256);
+  SOLVE_TRY(s, cudaMalloc(&s->a_arena, o_val + sizeof(double) * nz));
+  char* base = static_cast<char*>(s->a_arena);
+  s->a_ptr = reinterpret_cast<long long*>(base);
+  s->a_col = reinterpret_cast<int*>(base + o_col);
+  s->a_val = reinterpret_cast<double*>(base + o_val);
+  SOLVE_TRY(s, cudaMemcpy(s->a_ptr, a->row_ptr, sizeof(long long) * np1, cudaMemcpyHostToDevice));
+  if (a->nnz > 0) {
+    SOLVE_TRY(s, cudaMemcpy(s->a_col, a->col_idx, sizeof(int) * a->nnz, cudaMemcpyHostToDevice));
+    SOLVE_TRY(s, cudaMemcpy(s->a_val, a->values, sizeof(double) * a->nnz, cudaMemcpyHostToDevice));
+  }
+  return TCG_OK;
+}
+
+tcg_status tcg_solve_spmv(tcg_solve* s, const double* x_dev, double* y_dev) {
+  if (!s || !s->a_arena || (s->n > 0 && (!x_dev || !y_dev))) {
+    if (s) s->err = "tcg_solve_spmv: no matrix set (tcg_solve_set_matrix) or null vectors";
+    return TCG_INVALID;
+  }
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  const double* vals = nullptr;
+  std::int64_t n = 0, nnz = 0;
+  if (!tcb_internal::ctx_factor(s->ctx, 0, &device, &stream, &vals, &n, &nnz)) return TCG_INVALID;
+  SOLVE_TRY(s, cudaSetDevice(device));
+  SOLVE_TRY(s, tcbdev::launch_spmv(s->n, s->a_ptr, s->a_col, s->a_val, x_dev, y_dev, s->sm_count, stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_solve_stream(tcg_solve* s, void** stream) {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  const double* vals = nullptr;
+  std::int64_t n = 0, nnz = 0;
+  if (!s || !stream || !tcb_internal::ctx_factor(s->ctx, 0, &device, &st, &vals, &n, &nnz)) return TCG_INVALID;
+  *stream = st;
   return TCG_OK;
 }
 

@@ -173,3 +173,52 @@ def test_preconditioned_cg_converges_faster(T):
     finally:
         s.close()
         fz.close()
+
+
+def test_spmv_with_the_system_matrix_is_exact(T):
+    # y = A x on the device: products summed in column order, as np.add.at does
+    import torch
+    _, an = analyzed("c5_m0")
+    ap = an.a_permuted
+    fz = factored(T, "c5_m0")
+    try:
+        s = T.GpuTriSolve(fz)
+        s.set_matrix(ap)
+        x = np.random.default_rng(2).standard_normal(ap.nrows)
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty_like(xd)
+        s.spmv_ptr(xd.data_ptr(), yd.data_ptr())
+        torch.cuda.synchronize()
+        rows = np.repeat(np.arange(ap.nrows), np.diff(ap.row_ptr))
+        ref = np.zeros(ap.nrows)
+        np.add.at(ref, rows, ap.values * x[ap.col_idx])
+        assert bitwise_equal(yd.cpu().numpy(), ref)
+        with pytest.raises(ValueError):
+            s.set_matrix(T.generate("grid2d", 3, 3))  # wrong size
+        s.close()
+    finally:
+        fz.close()
+
+
+@pytest.mark.parametrize("name", ["c5_m0", "c2"])
+def test_gpu_pcg(T, name):
+    # IC(k)-preconditioned CG on the device: converges, in well under half the
+    # iterations of plain CG, to a true residual at the tolerance
+    _, an = analyzed(name)
+    ap = an.a_permuted
+    fz = factored(T, name)
+    try:
+        s = T.GpuTriSolve(fz)
+        s.set_matrix(ap)
+        b = np.ones(ap.nrows)
+        ic = T.pcg(s, b, tol=1e-8, maxit=3000)
+        plain = T.pcg(s, b, tol=1e-8, maxit=3000, precondition=False)
+        assert ic.converged and plain.converged
+        assert ic.iterations * 2 < plain.iterations, (ic.iterations, plain.iterations)
+        rows = np.repeat(np.arange(ap.nrows), np.diff(ap.row_ptr))
+        res = np.zeros(ap.nrows)
+        np.add.at(res, rows, ap.values * ic.x[ap.col_idx])
+        assert np.linalg.norm(res - b) <= 2e-8 * np.linalg.norm(b)
+        s.close()
+    finally:
+        fz.close()
