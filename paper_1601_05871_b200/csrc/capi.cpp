@@ -712,7 +712,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // 4.57 at 4 / 4.93 at 8; 16-32 no better anywhere)
   int drain_ctas = mean > 16.0 ? 4 : 8;
   if (const char* e = std::getenv("TCG_DRAIN_CTAS")) drain_ctas = std::max(1, std::atoi(e));
-  bool drain = host_out && pipe && !remote && extras == 0 && c->nbatch == 1 && c->nflow > 0 && phase == 0;
+  bool drain = host_out && pipe && !remote && !c->opt.trace && c->nflow > 0 && phase == 0;
   if (const char* e = std::getenv("TCG_DRAIN")) drain = drain && std::atoi(e) != 0;
   if (drain) {
     cudaPointerAttributes attr{};
@@ -723,7 +723,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
       cudaGetLastError();
     // 16-byte accesses on both sides (flow_kernel.cu drain_values)
     drain = drain_out != nullptr && reinterpret_cast<std::uintptr_t>(drain_out) % 16 == 0 &&
-            reinterpret_cast<std::uintptr_t>(c->vals) % 16 == 0;
+            reinterpret_cast<std::uintptr_t>(c->nbatch > 1 ? c->bvals : c->vals) % 16 == 0;
   }
   int occ = 0;
   if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0) != cudaSuccess) {
@@ -783,7 +783,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   P.nbatch = c->nbatch;
   P.nrows = static_cast<int>(c->nflow);
   P.row_ctas = drain ? grid - drain_ctas : grid;
-  const long long drain_words = (c->nnz + 2047) / 2048;
+  const long long drain_words = (c->nnz * c->nbatch + 2047) / 2048;
   if (drain) {
     if (drain_words > c->drain_len) {
       TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));

@@ -381,10 +381,11 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
 __device__ void drain_values(const FlowParams& P, int dw, int DW) {
   constexpr int kIn = 2;
   const int lane = threadIdx.x & 31;
-  const long long nb = (P.nnz + 2047) / 2048;
+  const long long total = P.nnz * P.nbatch;  // a batch's members are contiguous
+  const long long nb = (total + 2047) / 2048;
   const long long b0 = nb * dw / DW, b1 = nb * (dw + 1) / DW;
   const unsigned long long t0 = gtimer();
-  const bool even = (P.nnz & 1) == 0;
+  const bool even = (total & 1) == 0;
   long long low = b0;
   while (low < b1) {
     bool progressed = false;
@@ -401,11 +402,11 @@ __device__ void drain_values(const FlowParams& P, int dw, int DW) {
           const long long x = (b * 32 + j0 + j) * 64 + 2 * lane;
           va[j] = vb[j] = 0ull;
           if ((done >> (j0 + j)) & 1u) continue;
-          if (even && x + 1 < P.nnz) {
+          if (even && x + 1 < total) {
             ld_relaxed_v2_u64(P.vals + x, va[j], vb[j]);
           } else {
-            if (x < P.nnz) va[j] = ld_relaxed_u64(P.vals + x);
-            if (x + 1 < P.nnz) vb[j] = ld_relaxed_u64(P.vals + x + 1);
+            if (x < total) va[j] = ld_relaxed_u64(P.vals + x);
+            if (x + 1 < total) vb[j] = ld_relaxed_u64(P.vals + x + 1);
           }
         }
 #pragma unroll
@@ -413,13 +414,13 @@ __device__ void drain_values(const FlowParams& P, int dw, int DW) {
           if ((done >> (j0 + j)) & 1u) continue;
           if (__ballot_sync(kFull, va[j] != kUnset && vb[j] != kUnset) != kFull) continue;
           const long long x = (b * 32 + j0 + j) * 64 + 2 * lane;
-          if (even && x + 1 < P.nnz) {
+          if (even && x + 1 < total) {
             *reinterpret_cast<double2*>(P.drain_out + x) =
                 make_double2(__longlong_as_double(static_cast<long long>(va[j])),
                              __longlong_as_double(static_cast<long long>(vb[j])));
           } else {
-            if (x < P.nnz) P.drain_out[x] = __longlong_as_double(static_cast<long long>(va[j]));
-            if (x + 1 < P.nnz) P.drain_out[x + 1] = __longlong_as_double(static_cast<long long>(vb[j]));
+            if (x < total) P.drain_out[x] = __longlong_as_double(static_cast<long long>(va[j]));
+            if (x + 1 < total) P.drain_out[x + 1] = __longlong_as_double(static_cast<long long>(vb[j]));
           }
           done |= 1u << (j0 + j);
           progressed = true;
@@ -797,7 +798,8 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
 #define TCG_PIPE_VARIANTS(X)                                                                               \
   X(256, 2, 3, 0, 0, 0) X(256, 3, 3, 0, 0, 0) X(256, 4, 3, 0, 0, 0) X(256, 2, 3, 0, 1, 0) X(256, 3, 3, 0, 1, 0) \
   X(256, 4, 3, 0, 1, 0) X(256, 2, 3, 1, 1, 0) X(256, 3, 3, 1, 1, 0) X(256, 4, 3, 1, 1, 0)                     \
-  X(256, 2, 3, 0, 0, 1) X(256, 3, 3, 0, 0, 1) X(256, 4, 3, 0, 0, 1)
+  X(256, 2, 3, 0, 0, 1) X(256, 3, 3, 0, 0, 1) X(256, 4, 3, 0, 0, 1)                                         \
+  X(256, 2, 3, 0, 1, 1) X(256, 3, 3, 0, 1, 1) X(256, 4, 3, 0, 1, 1)
 
 static const void* pipe_kernel_for(int threads, int kb, int minb, int remote, int extras, int drain) {
 #define X(T, K, M, R, E, D)                                                                 \

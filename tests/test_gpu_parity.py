@@ -621,3 +621,23 @@ def test_drained_end_to_end_breakdown(T):
         assert e.value.row == 3 and fz.last.drain_ctas > 0
     finally:
         fz.close()
+
+
+def test_drained_batch_end_to_end(T, oracle):
+    # a C5 batch through tcg_factor_host_a into a pinned buffer: the drain
+    # copies every member's factor during the launch; bitwise per member
+    import torch
+    an, vals, perms = c5_members(T, [0, 9, 21])
+    fz = T.GpuFactorizer(planned("c5_m0"), T.GpuOptions(timeout_s=30))
+    try:
+        fz.set_a_values(np.stack([ap.values for ap in perms]))
+        a_in = torch.from_numpy(np.stack([ap.values for ap in perms]).ravel().copy()).pin_memory()
+        out = torch.full((3 * fz.nnz,), float("nan"), dtype=torch.float64).pin_memory()
+        st = fz.factor_host_a_ptr(a_in.data_ptr(), out.data_ptr())
+        assert st.drain_ctas > 0 and st.batch == 3
+        got = out.numpy().reshape(3, fz.nnz)
+        for i, ap in enumerate(perms):
+            ref, _, _, _ = oracle.factor_serial(ap, an.pattern.pattern)
+            assert bitwise_equal(got[i], ref), i
+    finally:
+        fz.close()
