@@ -294,12 +294,14 @@ def run_ours(args):
     host_out = torch.empty(nnz * per_rank, dtype=torch.float64).pin_memory()
     e2e_ms = []
     barrier()
-    for i in range(args.warmup + args.steps):
+    # 6 more untimed calls: the call decides on this box whether the drain pays
+    # (capi.cpp, first calls alternate with and without it)
+    for i in range(6 + args.warmup + args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         st_e2e = fz.factor_host_a_ptr(host_in.data_ptr(), host_out.data_ptr())
-        if i >= args.warmup:
+        if i >= 6 + args.warmup:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
     barrier()
     if batched:  # back to the initialised batch for anything after

@@ -67,7 +67,11 @@ struct tcg_ctx {
   int device = 0;
   int sm_count = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+  // end to end with a pinned output: best whole-call ms without (0) and with (1)
+  // the drain over the first calls of a problem and batch size (alternating)
+  float drain_ms[2] = {-1.f, -1.f};
+  int drain_calls = 0;
   void* arena = nullptr;
   size_t arena_bytes = 0;
   tcbdev::Ctrl* host_ctrl = nullptr;
@@ -389,6 +393,7 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+  if (e == cudaSuccess) e = cudaEventCreate(&c->ev2);
   if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c->host_ctrl), sizeof(tcbdev::Ctrl));
   if (e != cudaSuccess) {
     g_plan_error = std::string("tcg_create: ") + cudaGetErrorString(e);
@@ -413,6 +418,7 @@ void tcg_destroy(tcg_ctx* c) {
   if (c->host_ctrl) cudaFreeHost(c->host_ctrl);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  if (c->ev2) cudaEventDestroy(c->ev2);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -647,6 +653,8 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->max_target_len = p->max_target_len;
   c->max_flag_rows = p->max_flag_rows;
   c->uploaded = true;
+  c->drain_ms[0] = c->drain_ms[1] = -1.f;
+  c->drain_calls = 0;
   c->pristine = true;
   return TCG_OK;
 }
@@ -724,6 +732,23 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
     // 16-byte accesses on both sides (flow_kernel.cu drain_values)
     drain = drain_out != nullptr && reinterpret_cast<std::uintptr_t>(drain_out) % 16 == 0 &&
             reinterpret_cast<std::uintptr_t>(c->nbatch > 1 ? c->bvals : c->vals) % 16 == 0;
+  }
+  // Whether the drain pays depends on the host: zero-copy writes from the SMs
+  // ran at ~40 GB/s on some B200 boxes (C2 end to end 1.02 -> 0.82 ms) and
+  // far slower on others (1.03 -> 1.44 ms), where the copy engine is the
+  // better path. Unless TCG_DRAIN decides, the first kDrainProbe calls of a
+  // problem alternate between the two (the very first call of a buffer pays
+  // one-time costs, so each side keeps its best), later calls take the faster.
+  constexpr int kDrainProbe = 6;
+  const bool drain_forced = std::getenv("TCG_DRAIN") != nullptr;
+  bool calibrating = false;
+  if (drain && !drain_forced) {
+    if (c->drain_calls < kDrainProbe) {
+      drain = (c->drain_calls & 1) != 0;
+      calibrating = true;
+    } else {
+      drain = c->drain_ms[1] < c->drain_ms[0];
+    }
   }
   int occ = 0;
   if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0) != cudaSuccess) {
@@ -828,11 +853,19 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   c->pristine = false;  // the working values now hold the factor
   if (host_out && !drain)
     TCG_CUDA_TRY(c, cudaMemcpyAsync(host_out, vals, vbytes, cudaMemcpyDeviceToHost, c->stream));
+  if (calibrating) TCG_CUDA_TRY(c, cudaEventRecord(c->ev2, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
                                   cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   float ms = 0.f;
   TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  if (calibrating) {
+    float whole = 0.f;
+    TCG_CUDA_TRY(c, cudaEventElapsedTime(&whole, c->ev0, c->ev2));
+    float& best = c->drain_ms[drain ? 1 : 0];
+    if (best < 0.f || whole < best) best = whole;
+    ++c->drain_calls;
+  }
   const tcbdev::Ctrl& h = *c->host_ctrl;
   S.device_ms = ms;
   S.grid_ctas = grid;
@@ -1367,6 +1400,8 @@ tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {
   c->bm_flags = reinterpret_cast<int*>(base + 3 * align_up(vb, 256));
   c->bm_pivot = reinterpret_cast<double*>(base + 3 * align_up(vb, 256) + fb);
   c->nbatch = nbatch;
+  c->drain_ms[0] = c->drain_ms[1] = -1.f;
+  c->drain_calls = 0;
   if (vb) {
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals0, values, vb, cudaMemcpyHostToDevice, c->stream));
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals, c->bvals0, vb, cudaMemcpyDeviceToDevice, c->stream));
@@ -1406,6 +1441,8 @@ tcg_status tcg_set_a_values(tcg_ctx* c, int32_t nbatch, const double* a_values) 
       c->batch_arena = nullptr;
     }
     c->nbatch = nbatch;
+    c->drain_ms[0] = c->drain_ms[1] = -1.f;
+  c->drain_calls = 0;
   }
   const int64_t need = c->nnz_a * nbatch;
   if (need > c->a_stage_len) {

@@ -581,6 +581,7 @@ def test_drained_end_to_end(T, golden, oracle, name, monkeypatch):
     try:
         a_in = torch.from_numpy(an.a_permuted.values.copy()).pin_memory()
         u_in = torch.from_numpy(plan.tables()["values"]).pin_memory()
+        monkeypatch.setenv("TCG_DRAIN", "1")  # forced: no calibration
         for ctas in ("1", "2", "4"):
             monkeypatch.setenv("TCG_DRAIN_CTAS", ctas)
             out = torch.full((fz.nnz,), float("nan"), dtype=torch.float64).pin_memory()
@@ -606,10 +607,11 @@ def test_drained_end_to_end(T, golden, oracle, name, monkeypatch):
         fz.close()
 
 
-def test_drained_end_to_end_breakdown(T):
+def test_drained_end_to_end_breakdown(T, monkeypatch):
     # an indefinite matrix: the rows after the failing pivot are skipped and
     # keep their inputs, so the drain still finishes; BreakdownError as usual
     import torch
+    monkeypatch.setenv("TCG_DRAIN", "1")
     a, fp, rl = small(T, 4, sym([(0, 0, 1.0), (1, 1, 1.0), (2, 2, 1.0), (2, 3, 4.0), (3, 3, 1.0)]),
                       bounds=[0, 2, 4])
     fz = T.GpuFactorizer(T.Plan(a, fp, rl), T.GpuOptions(timeout_s=30))
@@ -623,10 +625,11 @@ def test_drained_end_to_end_breakdown(T):
         fz.close()
 
 
-def test_drained_batch_end_to_end(T, oracle):
+def test_drained_batch_end_to_end(T, oracle, monkeypatch):
     # a C5 batch through tcg_factor_host_a into a pinned buffer: the drain
     # copies every member's factor during the launch; bitwise per member
     import torch
+    monkeypatch.setenv("TCG_DRAIN", "1")
     an, vals, perms = c5_members(T, [0, 9, 21])
     fz = T.GpuFactorizer(planned("c5_m0"), T.GpuOptions(timeout_s=30))
     try:
@@ -639,5 +642,25 @@ def test_drained_batch_end_to_end(T, oracle):
         for i, ap in enumerate(perms):
             ref, _, _, _ = oracle.factor_serial(ap, an.pattern.pattern)
             assert bitwise_equal(got[i], ref), i
+    finally:
+        fz.close()
+
+
+def test_drain_calibrates_per_problem(T, golden, oracle, monkeypatch):
+    # without TCG_DRAIN: the first six calls alternate between a copy after
+    # the launch and the drain, later calls keep the faster; every result bitwise
+    import torch
+    monkeypatch.delenv("TCG_DRAIN", raising=False)
+    _, an = analyzed("c5_m0")
+    fz = T.GpuFactorizer(planned("c5_m0"), T.GpuOptions(timeout_s=30))
+    try:
+        a_in = torch.from_numpy(an.a_permuted.values.copy()).pin_memory()
+        seen = []
+        for _ in range(9):
+            out = torch.zeros(fz.nnz, dtype=torch.float64).pin_memory()
+            seen.append(fz.factor_host_a_ptr(a_in.data_ptr(), out.data_ptr()).drain_ctas)
+            check_against_oracle("c5_m0", out.numpy().copy(), golden, oracle)
+        assert seen[:6:2] == [0, 0, 0] and min(seen[1:6:2]) > 0  # alternating probe calls
+        assert len(set(seen[6:])) == 1 and seen[6] in (0, seen[1])
     finally:
         fz.close()
