@@ -164,6 +164,8 @@ typedef struct {
   int32_t breakdown_member;  /* batch: member of breakdown_row (-1 when none) */
   int32_t drain_ctas;        /* end to end: CTAs that copied the factor to the host during the
                                 launch (0: a D2H copy after it) */
+  int32_t chunks;            /* end to end, batches: member chunks pipelined with the copies
+                                (0: one launch) */
 } tcg_stats;
 
 typedef struct {

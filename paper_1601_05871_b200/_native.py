@@ -124,6 +124,7 @@ class Stats(C.Structure):
         ("batch", C.c_int32),
         ("breakdown_member", C.c_int32),
         ("drain_ctas", C.c_int32),
+        ("chunks", C.c_int32),
     ]
 
 

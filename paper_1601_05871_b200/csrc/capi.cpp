@@ -122,6 +122,12 @@ struct tcg_ctx {
   std::int64_t m6_nrows = 0, m6_nunits = 0, m6_smem = 0;
   bool has_units = false;
   int* a_map = nullptr;      // device init_factor_values (in the arena)
+  // pipelined batches end to end (run_flow_chunked): copy streams, per-chunk
+  // events and status words
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  tcbdev::Ctrl* host_ctrls = nullptr;
+  int host_ctrls_len = 0;
   double* a_stage = nullptr; // staging for A's values (separate allocation, grown on demand)
   unsigned* drain_done = nullptr;  // end-to-end drain: groups copied per 2,048 values
   std::int64_t drain_len = 0;
@@ -419,6 +425,10 @@ void tcg_destroy(tcg_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->ev2) cudaEventDestroy(c->ev2);
+  for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
+  if (c->host_ctrls) cudaFreeHost(c->host_ctrls);
+  if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+  if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -1342,6 +1352,141 @@ tcg_status tcg_factor_host(tcg_ctx* c, const double* values_in, double* values_o
   return run_flow(c, S, threads, values_in, values_out);
 }
 
+// C5-style batches end to end, pipelined: the members in chunks, one launch
+// per chunk; the upload of chunk i+1 (copy stream) and the download of chunk
+// i-1 (another copy stream) run beside the factorization of chunk i (events
+// order them; if the copies do not overlap, the result is the same, later).
+// Same kernels and arithmetic as one launch over the whole batch.
+static tcg_status run_flow_chunked(tcg_ctx* c, tcg_stats& S, int threads, const double* host_a,
+                                   double* host_out, int chunks) {
+  const double mean = c->nnz > 0 ? static_cast<double>(c->nflow_upd) / static_cast<double>(c->nnz) : 0.0;
+  const int kb = mean <= 4.0 ? 2 : 3, minb = 3;
+  int occ = 0;
+  TCG_CUDA_TRY(c, tcbdev::pipe_occupancy(threads, kb, minb, 0, 1, &occ, 0));
+  if (occ < 1) {
+    c->err = "value-flow kernel does not fit on an SM";
+    return TCG_INVALID;
+  }
+  if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
+  const int grid = std::max(1, occ * c->sm_count);
+  const int nb = c->nbatch;
+  if (!c->h2d_stream) TCG_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
+  if (!c->d2h_stream) TCG_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+  while (static_cast<int>(c->chunk_ev.size()) < 2 * chunks + 1) {
+    cudaEvent_t e = nullptr;
+    TCG_CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->chunk_ev.push_back(e);
+  }
+  if (c->host_ctrls_len < chunks) {
+    if (c->host_ctrls) TCG_CUDA_TRY(c, cudaFreeHost(c->host_ctrls));
+    c->host_ctrls = nullptr;
+    TCG_CUDA_TRY(c, cudaMallocHost(reinterpret_cast<void**>(&c->host_ctrls), sizeof(tcbdev::Ctrl) * chunks));
+    c->host_ctrls_len = chunks;
+  }
+  const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->h2d_stream, c->ev0, 0));
+  for (int k = 0; k < chunks; ++k) {
+    const int m0 = static_cast<int>(static_cast<long long>(nb) * k / chunks);
+    const int m1 = static_cast<int>(static_cast<long long>(nb) * (k + 1) / chunks);
+    const int nk = m1 - m0;
+    cudaEvent_t up = c->chunk_ev[2 * k], done = c->chunk_ev[2 * k + 1];
+    double* vals = c->bvals + static_cast<long long>(m0) * c->nnz;
+    double* vals0 = c->bvals0 + static_cast<long long>(m0) * c->nnz;
+    const double* stage = c->a_stage + static_cast<long long>(m0) * c->nnz_a;
+    if (c->nnz_a > 0)
+      TCG_CUDA_TRY(c, cudaMemcpyAsync(const_cast<double*>(stage), host_a + static_cast<long long>(m0) * c->nnz_a,
+                                      sizeof(double) * c->nnz_a * nk, cudaMemcpyHostToDevice, c->h2d_stream));
+    TCG_CUDA_TRY(c, cudaEventRecord(up, c->h2d_stream));
+    TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, up, 0));
+    TCG_CUDA_TRY(c, tcbdev::launch_init_values(stage, c->a_map, vals, vals0, c->nnz, c->nnz_a, nk, c->sm_count,
+                                               c->stream));
+    tcbdev::FlowPrepParams q{};
+    q.vals = vals;
+    q.a = vals;  // the input is the restore copy the init wrote: no snapshot
+    q.out = vals;
+    q.nnz = c->nnz * nk;
+    q.ctrl = c->ctrl;
+    q.m_failed = c->bm_flags + m0;
+    q.m_row = c->bm_flags + nb + m0;
+    q.m_pivot = c->bm_pivot + m0;
+    q.nbatch = nk;
+    TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
+    tcbdev::FlowParams P{};
+    P.rec = c->flow_rec;
+    P.item = c->flow_item;
+    P.slot = c->flow_slot;
+    P.upd = c->flow_upd;
+    P.a = vals0;
+    P.vals = vals;
+    P.ctrl = c->ctrl;
+    P.m_failed = q.m_failed;
+    P.m_row = q.m_row;
+    P.m_pivot = q.m_pivot;
+    P.nnz = c->nnz;
+    P.nbatch = nk;
+    P.nrows = static_cast<int>(c->nflow);
+    P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
+    P.row_ctas = grid;
+    TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, 0, 1, c->stream, 0));
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrls + k, c->ctrl, sizeof(tcbdev::Ctrl), cudaMemcpyDeviceToHost,
+                                    c->stream));
+    TCG_CUDA_TRY(c, cudaEventRecord(done, c->stream));
+    TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->d2h_stream, done, 0));
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(host_out + static_cast<long long>(m0) * c->nnz, vals,
+                                    sizeof(double) * c->nnz * nk, cudaMemcpyDeviceToHost, c->d2h_stream));
+  }
+  TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
+  TCG_CUDA_TRY(c, cudaEventRecord(c->chunk_ev[2 * chunks], c->d2h_stream));
+  TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->chunk_ev[2 * chunks], 0));  // later work sees the copies done
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->d2h_stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  c->pristine = false;
+  S.device_ms = ms;
+  S.grid_ctas = grid;
+  S.threads_per_cta = threads;
+  S.staging_cap = kb;
+  S.kernel_launches = 3 * chunks;
+  S.mode = 5;
+  S.lanes_per_row = 32;
+  S.batch = nb;
+  S.chunks = chunks;
+  bool error = false;
+  int64_t rows = 0, executed = 0;
+  for (int k = 0; k < chunks; ++k) {
+    const tcbdev::Ctrl& h = c->host_ctrls[k];
+    const int m0 = static_cast<int>(static_cast<long long>(nb) * k / chunks);
+    error = error || h.error.v;
+    rows += h.done.v;
+    executed += h.executed.v;
+    if (h.failed.v && S.breakdown_row < 0) {
+      S.breakdown_row = h.fail_row;
+      S.breakdown_pivot = h.fail_pivot;
+      S.breakdown_member = h.fail_member + m0;
+    }
+  }
+  S.tasks_completed = rows == c->nflow * nb ? c->ntasks * nb : 0;
+  S.tasks_executed = executed;
+  if (error) {
+    c->err = "device watchdog expired: the value-flow schedule stalled";
+    return TCG_TIMEOUT;
+  }
+  if (rows != c->nflow * nb) {
+    c->err = "value-flow schedule finished " + std::to_string(rows) + " of " + std::to_string(c->nflow * nb) +
+             " rows";
+    return TCG_TIMEOUT;
+  }
+  if (S.breakdown_row >= 0) {
+    c->err = "factorization breakdown at row " + std::to_string(S.breakdown_row) + ": pivot " +
+             std::to_string(S.breakdown_pivot) + " is not positive (member " +
+             std::to_string(S.breakdown_member) + ")";
+    return TCG_BREAKDOWN;
+  }
+  return TCG_OK;
+}
+
 tcg_status tcg_factor_host_a(tcg_ctx* c, const double* a_values, double* values_out, tcg_stats* st) {
   if (!c || !c->uploaded || ((!a_values && c->nnz_a > 0) || (!values_out && c->nnz > 0))) return TCG_INVALID;
   if (!c->a_map) {
@@ -1372,6 +1517,12 @@ tcg_status tcg_factor_host_a(tcg_ctx* c, const double* a_values, double* values_
   S.breakdown_member = -1;
   S.batch = c->nbatch;
   const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
+  // batches of 8 or more: pipelined over 4 member chunks (TCG_CHUNKS overrides; 1 = one launch)
+  int chunks = c->nbatch >= 8 ? 4 : 1;
+  if (const char* e = std::getenv("TCG_CHUNKS")) chunks = std::max(1, std::atoi(e));
+  chunks = std::min(chunks, c->nbatch);
+  if (chunks > 1 && threads == 256 && !c->opt.trace && c->npeers <= 1)
+    return run_flow_chunked(c, S, threads, a_values, values_out, chunks);
   return run_flow(c, S, threads, nullptr, values_out, 0, a_values);
 }
 

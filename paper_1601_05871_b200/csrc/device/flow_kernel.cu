@@ -681,6 +681,27 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_units(FlowParams P, Unit
 // the status words.
 __global__ void flow_prepare(FlowPrepParams Q) {
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const double unset1 = __longlong_as_double(static_cast<long long>(kUnset));
+  if (((reinterpret_cast<unsigned long long>(Q.vals) | reinterpret_cast<unsigned long long>(Q.a) |
+        reinterpret_cast<unsigned long long>(Q.out)) & 15ull) != 0) {
+    // a batch chunk starting at an odd member of an odd-sized U: 8-byte accesses
+    for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < Q.nnz; x += stride) {
+      if (Q.a != Q.vals) Q.a[x] = Q.vals[x];
+      Q.out[x] = unset1;
+    }
+    for (long long x = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; x < Q.nbatch; x += stride) {
+      Q.m_failed[x] = 0;
+      Q.m_row[x] = -1;
+      Q.m_pivot[x] = 0.0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      Ctrl c = {};
+      c.fail_row = -1;
+      c.fail_member = -1;
+      *Q.ctrl = c;
+    }
+    return;
+  }
   const long long h = Q.nnz / 2;
   const double2* in2 = reinterpret_cast<const double2*>(Q.vals);
   double2* a2 = reinterpret_cast<double2*>(Q.a);

@@ -664,3 +664,41 @@ def test_drain_calibrates_per_problem(T, golden, oracle, monkeypatch):
         assert len(set(seen[6:])) == 1 and seen[6] in (0, seen[1])
     finally:
         fz.close()
+
+
+@pytest.mark.parametrize("chunks", ["4", "3", "1"])
+def test_pipelined_batch_end_to_end(T, oracle, chunks, monkeypatch):
+    # 10 C5 members through tcg_factor_host_a, pipelined over member chunks
+    # (uploads and downloads beside the launches); member 6 made indefinite:
+    # it breaks down at the oracle's row, the others stay bitwise
+    import torch
+    monkeypatch.setenv("TCG_CHUNKS", chunks)
+    monkeypatch.setenv("TCG_DRAIN", "0")
+    members = list(range(10))
+    an, vals, perms = c5_members(T, members)
+    a_vals = np.stack([ap.values.copy() for ap in perms])
+    ap6 = perms[6]
+    b0, b1 = int(ap6.row_ptr[100]), int(ap6.row_ptr[101])
+    d = b0 + int(np.flatnonzero(ap6.col_idx[b0:b1] == 100)[0])  # the (100, 100) entry
+    a_vals[6, d] = -1.0
+    fz = T.GpuFactorizer(planned("c5_m0"), T.GpuOptions(timeout_s=30))
+    try:
+        fz.set_a_values(a_vals)
+        a_in = torch.from_numpy(a_vals.ravel().copy()).pin_memory()
+        out = torch.full((10 * fz.nnz,), float("nan"), dtype=torch.float64).pin_memory()
+        with pytest.raises(T.BreakdownError) as e:
+            fz.factor_host_a_ptr(a_in.data_ptr(), out.data_ptr())
+        assert fz.last.chunks == (int(chunks) if chunks != "1" else 0)
+        bad = T.CsrMatrix(ap6.nrows, ap6.ncols, ap6.row_ptr, ap6.col_idx, a_vals[6])
+        _, st, row, _ = oracle.factor_serial(bad, an.pattern.pattern)
+        assert st == 1 and e.value.row == row and fz.last.breakdown_member == 6
+        got = out.numpy().reshape(10, fz.nnz)
+        for i, ap in enumerate(perms):
+            if i == 6:
+                continue
+            ref, _, _, _ = oracle.factor_serial(ap, an.pattern.pattern)
+            assert bitwise_equal(got[i], ref), i
+        rows, _ = fz.batch_breakdown()
+        assert [int(r) for r in rows] == [row if i == 6 else -1 for i in range(10)]
+    finally:
+        fz.close()
