@@ -708,6 +708,11 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   int kb = mean <= 4.0 ? 2 : 3;
   int minb = threads == 128 ? 6 : threads == 384 ? 2 : threads == 256 ? 3 : 1;
   if (const char* e = std::getenv("TCG_FLOW_KB")) kb = std::atoi(e);
+  // short programs: 5 CTAs per SM of the single-matrix kernel (48 registers, no spills;
+  // B200: C1 0.049 -> 0.043, C2 0.415 -> 0.402, C5 0.188 -> 0.181, C6 1.79 -> 1.71 ms);
+  // with KB = 3 the fifth CTA costs more than it hides (C3 4.03 -> 4.15, C4 1.47 -> 1.60)
+  const bool single_local = c->nbatch == 1 && !c->opt.trace && c->npeers <= 1;
+  if (threads == 256 && kb == 2 && single_local) minb = 5;
   if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
   // lanes per row: a whole warp unless asked otherwise (flow_kernel.cu)
   const int g = c->opt.lanes_per_row > 0 ? c->opt.lanes_per_row : 32;
@@ -760,6 +765,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
       drain = c->drain_ms[1] < c->drain_ms[0];
     }
   }
+  if (minb == 5 && (remote || extras || !pipe)) minb = 3;  // the 5-CTA kernel exists for one local matrix
   int occ = 0;
   if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0) != cudaSuccess) {
     cudaGetLastError();
