@@ -705,14 +705,17 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
                            double* host_out = nullptr, int phase = 0, const double* host_a = nullptr) {
   // gather batch from the mean products per coordinate (flow_kernel.cu variants)
   const double mean = c->nnz > 0 ? static_cast<double>(c->nflow_upd) / static_cast<double>(c->nnz) : 0.0;
-  int kb = mean <= 4.0 ? 2 : 3;
+  // short programs: one product in flight per lane where the chain binds (B200, KB 1 vs 2: C2
+  // 0.402 -> 0.390, C5 0.183 -> 0.168 ms), two where each warp runs hundreds of rows back to
+  // back and the per-row gather sets the pace (C6, 2.1 M rows: 1.711 vs 1.734 ms)
+  const bool one_local = c->nbatch == 1 && !c->opt.trace && c->npeers <= 1;  // the single-matrix kernels
+  int kb = mean <= 4.0 ? (one_local && c->nflow <= 1000000 ? 1 : 2) : 3;
   int minb = threads == 128 ? 6 : threads == 384 ? 2 : threads == 256 ? 3 : 1;
   if (const char* e = std::getenv("TCG_FLOW_KB")) kb = std::atoi(e);
   // short programs: 5 CTAs per SM of the single-matrix kernel (48 registers, no spills;
   // B200: C1 0.049 -> 0.043, C2 0.415 -> 0.402, C5 0.188 -> 0.181, C6 1.79 -> 1.71 ms);
   // with KB = 3 the fifth CTA costs more than it hides (C3 4.03 -> 4.15, C4 1.47 -> 1.60)
-  const bool single_local = c->nbatch == 1 && !c->opt.trace && c->npeers <= 1;
-  if (threads == 256 && kb == 2 && single_local) minb = 5;
+  if (threads == 256 && kb <= 2 && one_local) minb = 5;
   if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
   // lanes per row: a whole warp unless asked otherwise (flow_kernel.cu)
   const int g = c->opt.lanes_per_row > 0 ? c->opt.lanes_per_row : 32;
@@ -766,7 +769,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
     }
   }
   // the 5-CTA kernel exists for one local matrix (with or without the drain)
-  if (minb == 5 && (remote || extras || !pipe || kb != 2)) minb = 3;
+  if (minb == 5 && (remote || extras || !pipe || kb > 2)) minb = 3;
   int occ = 0;
   if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0) != cudaSuccess) {
     cudaGetLastError();
