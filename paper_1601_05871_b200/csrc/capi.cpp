@@ -1604,7 +1604,7 @@ tcg_status tcg_set_a_values(tcg_ctx* c, int32_t nbatch, const double* a_values) 
     }
     c->nbatch = nbatch;
     c->drain_ms[0] = c->drain_ms[1] = -1.f;
-  c->drain_calls = 0;
+    c->drain_calls = 0;
   }
   const int64_t need = c->nnz_a * nbatch;
   if (need > c->a_stage_len) {
