@@ -1546,6 +1546,8 @@ tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {
     c->batch_arena = nullptr;
   }
   c->nbatch = 1;
+  c->drain_ms[0] = c->drain_ms[1] = -1.f;
+  c->drain_calls = 0;
   if (nbatch == 1) return tcg_set_values(c, values);
   if (!c->has_flow) {
     c->err = "tcg_set_batch: the plan has no value-flow tables (mode 5)";
