@@ -81,6 +81,11 @@ if launches:
     for r in rows[1:]:
         per[r[ki]].append(float(r[vi].replace(",", "")))
     summary["launch_list_mean_ns"] = {k: sum(v) / len(v) for k, v in per.items()}
+    # bench.py also times a 1,000-row chain (the latency bound) with the same
+    # kernel after the C2 steps: the median and the first launches are the C2 ones
+    summary["launch_list_median_ns"] = {k: sorted(v)[len(v) // 2] for k, v in per.items()}
+    summary["launch_list_first5_ns"] = {k: v[:5] for k, v in per.items()}
+    summary["launch_list_count"] = {k: len(v) for k, v in per.items()}
     with open(os.path.join(out_dir, f"launches_bench_{cfg}.csv"), "w") as f:
         f.write(open(launches).read())
 with open(os.path.join(ROOT, "profiles", f"ncu_{cfg}_factor.json"), "w") as f:
