@@ -153,6 +153,12 @@ template <int KB, class Cx>
 __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr) {
   const int ub = sr.x, ue = sr.y;
   if (ub >= ue) return v;
+  // long programs (KB >= 3): pull the rest of the (m, o) pairs into L2 now, so
+  // the batch-ahead loads below hit L2 instead of HBM (C3's programs are
+  // 1.5 GB). B200: C3 4.03 -> 3.88, C4 1.474 -> 1.453 ms; with short programs
+  // it cost 1-2% (C2, C6), so the KB = 1-2 kernels do not do it.
+  if (KB >= 3)
+    for (int q = ub + 1 + 2 * KB; q < ue; q += 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.P.upd + q));
   const unsigned long long xa0 = C.ld(sr.z), xb0 = C.ld(sr.w);
   int u = ub + 1;
   int2 p[KB];
