@@ -316,7 +316,8 @@ typedef struct {
 } tcg_solve_stats;
 enum { TCG_SOLVE_FORWARD = 1, TCG_SOLVE_BACKWARD = 2, TCG_SOLVE_BOTH = 3 };
 /* u_pattern: the factor's pattern (FillPattern.pattern of the uploaded problem); the values
- * are read from the context at every apply, so a refactorization is picked up. */
+ * are read from the context at every apply, so a refactorization is picked up (with a batch,
+ * member 0's factor). Destroy the solve handle before its context. */
 tcg_status tcg_solve_create(tcg_ctx* ctx, const tcg_csr_view* u_pattern, tcg_solve** out);
 void tcg_solve_destroy(tcg_solve* s);
 const char* tcg_solve_error(const tcg_solve* s);
