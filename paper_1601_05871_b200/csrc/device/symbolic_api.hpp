@@ -38,7 +38,7 @@ size_t sym_smem_bytes(int hb);
 cudaError_t sym_occupancy(int hb, int* ctas_per_sm);
 cudaError_t launch_levelk_fast(const SymParams& p, int pass, int hb, int grid, cudaStream_t st);
 cudaError_t launch_levelk_slow(const SymParams& p, int pass, int grid, cudaStream_t st);
-cudaError_t launch_levelk_copy(const SymParams& p, int grid, cudaStream_t st);
+cudaError_t launch_levelk_copy(const SymParams& p, int grid, bool long_rows, cudaStream_t st);
 cudaError_t sym_scan(const long long* count, long long* u_ptr, int n, void* temp, size_t* temp_bytes,
                      cudaStream_t st);
 

@@ -298,7 +298,9 @@ tcg_status tcg_sym_levelk(tcg_sym* s, int32_t level, int32_t flags, tcg_sym_stat
   }
   P.u_col = s->u_col;
   if (n > 0 && !(flags & TCG_SYM_ALL_SLOW)) {
-    SYM_TRY(s, tcbdev::launch_levelk_copy(P, grid1, s->stream));
+    const bool long_rows = nnz_u > 24LL * n;  // mean row length
+    SYM_TRY(s, tcbdev::launch_levelk_copy(P, long_rows ? grid1 : std::max(1, std::min(32 * s->sm_count, (n + 255) / 256)),
+                                          long_rows, s->stream));
     ++launches;
   }
   if (n > 0 && !(flags & TCG_SYM_ALL_SLOW) && short_scratch) {
