@@ -622,10 +622,11 @@ def run_symbolic(args):
                 "h2d_bytes_per_step": 8 * (n + 1) + 4 * nnz_a, "d2h_bytes_per_step": 8 * (n + 1) + 4 * nnz_u,
                 "ms_per_step": e2e},
         "gpu_launches": st.kernel_launches * args.steps,
-        "launches_per_step": {"levelk_fast count": 1, "device scan": 1, "levelk_fast fill": 1},
+        "launches_per_step": {"levelk_fast (tier 1, count + rows into scratch)": 1,
+                              "levelk_fast (tier 2, rows past tier 1)": 1, "device scan": 1, "levelk_copy": 1},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_alg,
-                     "note": "whole symbolic step (3 launches): PaP pattern read once, U pattern written once"},
+                     "note": "whole symbolic step (4 launches): PaP pattern read once, U pattern written once"},
         "cpu_baseline": cpu,
         "clocks": clocks.summary(),
     }

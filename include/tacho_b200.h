@@ -276,7 +276,7 @@ int64_t tcg_arena_bytes(const tcg_ctx* ctx);
  * (row i = {i} then its targets ascending), bit-exact. Separate handle: it needs no plan. */
 typedef struct tcg_sym tcg_sym;
 typedef struct {
-  double device_ms;          /* count + scan + fill, CUDA events on the handle's stream */
+  double device_ms;          /* search (rows into scratch) + scan + copy, CUDA events on the handle's stream */
   double host_ms;            /* wall time of tcg_sym_levelk (includes the nnz_u readback) */
   int64_t nnz_u;             /* FillPattern.pattern.nnz() */
   int64_t nnz_triu_input;    /* FillPattern.nnz_triu_input (count_upper, csr_matrix.hpp:219-225) */

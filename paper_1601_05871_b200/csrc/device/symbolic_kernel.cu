@@ -15,8 +15,9 @@
 //
 // Fast path (two tiers: 512-slot tables at 7 CTAs/SM, then 2,048-slot tables
 // for the rows that outgrow them): the warp's seen-set is an open-addressed
-// hash table in shared memory (interior vertices and targets are disjoint key ranges, one table),
-// the frontier a shared-memory list; the adjacency of 32 frontier vertices is
+// hash table in shared memory (interior vertices and targets are disjoint key
+// ranges, one table) with an insertion list whose depth-d entries are frontier
+// d + 1; the adjacency of 32 frontier vertices is
 // flattened by a warp prefix sum over their degrees so every lane loads a
 // neighbour (7-point stencils have degree 7). A search that outgrows the
 // table or the frontier list is handed to the slow path: one warp per row
