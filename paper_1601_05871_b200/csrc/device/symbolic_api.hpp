@@ -8,6 +8,7 @@
 namespace tcbdev {
 
 constexpr int kSymThreads = 256;              // 8 warps, one source row each
+constexpr int kSymHashTiny = 7;               // tier 1 for small searches: 8 lanes per row, 128 slots (96 keys)
 constexpr int kSymHashSmall = 9;              // tier 1: 512-slot seen-sets (384 keys)
 constexpr int kSymHashLarge = 11;             // tier 2: 2,048 slots (1,536 keys); then global memory
 

@@ -44,15 +44,15 @@ namespace {
 constexpr int kEmpty = -1;
 constexpr unsigned kFullMask = 0xffffffffu;
 
-template <int HB>
+template <int HB, int G = 32>
 struct WarpSym {
   static constexpr int kHash = 1 << HB;
   static constexpr int kLoad = kHash * 3 / 4;  // distinct keys beyond this -> next tier
   int tab[kHash];       // seen-set: interior vertices (< i) and targets (> i)
   int ins[kLoad];       // slots in insertion order: depth by depth, so the
                         // interior keys inserted at depth d are frontier d + 1
-  long long sb[32];     // adjacency begin of the current 32 frontier vertices
-  int sx[32];           // exclusive prefix of their degrees
+  long long sb[G];      // adjacency begin of the current G frontier vertices
+  int sx[G];            // exclusive prefix of their degrees
   int nfill, ovf;
 };
 
@@ -66,9 +66,9 @@ __device__ __forceinline__ unsigned hash_slot(int key) {
 // property of the row, not of the interleaving; the guard at kLoad + 32 (more
 // keys than that imply overflow anyway) and the probe bound keep a table that
 // keeps filling from spinning.
-template <int HB>
-__device__ __forceinline__ bool tab_insert(WarpSym<HB>& S, int key) {
-  using W = WarpSym<HB>;
+template <int HB, int G>
+__device__ __forceinline__ bool tab_insert(WarpSym<HB, G>& S, int key) {
+  using W = WarpSym<HB, G>;
   if (*reinterpret_cast<volatile int*>(&S.nfill) >= W::kLoad + 32) {
     S.ovf = 1;
     return false;
@@ -91,13 +91,13 @@ __device__ __forceinline__ bool tab_insert(WarpSym<HB>& S, int key) {
 
 // The search from row i in shared memory; the table is empty on entry.
 // Returns false on overflow (the table is then cleared whole).
-template <int HB>
-__device__ bool search_fast(const SymParams& P, WarpSym<HB>& S, int i, int lane) {
+template <int HB, int G>
+__device__ bool search_fast(const SymParams& P, WarpSym<HB, G>& S, int i, int lane, unsigned gmask) {
   int lo = 0, hi = 0;  // ins range of the current frontier; depth 0 is {i}
   for (int d = 0; d <= P.kk; ++d) {
     const bool expand = d < P.kk;
     const int ncur = d == 0 ? 1 : hi - lo;
-    for (int c0 = 0; c0 < ncur; c0 += 32) {
+    for (int c0 = 0; c0 < ncur; c0 += G) {
       int v = -1;
       if (c0 + lane < ncur) v = d == 0 ? i : S.tab[S.ins[lo + c0 + lane]];
       if (v > i) v = -1;  // a target: not expanded
@@ -109,32 +109,32 @@ __device__ bool search_fast(const SymParams& P, WarpSym<HB>& S, int i, int lane)
       }
       int incl = deg;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(kFullMask, incl, o);
+      for (int o = 1; o < G; o <<= 1) {
+        const int y = __shfl_up_sync(gmask, incl, o, G);
         if (lane >= o) incl += y;
       }
-      const int total = __shfl_sync(kFullMask, incl, 31);
+      const int total = __shfl_sync(gmask, incl, G - 1, G);
       S.sb[lane] = b;
       S.sx[lane] = incl - deg;
-      __syncwarp();
-      for (int e = lane; e < total; e += 32) {
+      __syncwarp(gmask);
+      for (int e = lane; e < total; e += G) {
         int j = 0;  // last j with sx[j] <= e (a zero degree repeats the prefix; take the last)
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1)
+        for (int step = G / 2; step > 0; step >>= 1)
           if (S.sx[j + step] <= e) j += step;
         const int w = __ldg(P.a_col + S.sb[j] + (e - S.sx[j]));
         if (w > i || (w < i && expand)) tab_insert(S, w);
       }
-      __syncwarp();
+      __syncwarp(gmask);
     }
     if (S.ovf) {
-      for (int s = lane; s < WarpSym<HB>::kHash; s += 32) S.tab[s] = kEmpty;
-      __syncwarp();
+      for (int s = lane; s < WarpSym<HB, G>::kHash; s += G) S.tab[s] = kEmpty;
+      __syncwarp(gmask);
       if (lane == 0) {
         S.nfill = 0;
         S.ovf = 0;
       }
-      __syncwarp();
+      __syncwarp(gmask);
       return false;
     }
     lo = d == 0 ? 0 : hi;
@@ -147,11 +147,11 @@ __device__ bool search_fast(const SymParams& P, WarpSym<HB>& S, int i, int lane)
 // Empties the table through the insertion list and moves the targets
 // (keys > i) to the front of `ins`; returns their count. Every write of the
 // in-place compaction lands at or before the entry being read.
-template <int HB>
-__device__ int drain_targets(WarpSym<HB>& S, int i, int lane) {
+template <int HB, int G>
+__device__ int drain_targets(WarpSym<HB, G>& S, int i, int lane, unsigned gmask, int lead) {
   const int nf = S.nfill;
   int base = 0;
-  for (int p0 = 0; p0 < nf; p0 += 32) {
+  for (int p0 = 0; p0 < nf; p0 += G) {
     const int p = p0 + lane;
     int key = kEmpty;
     if (p < nf) {
@@ -160,14 +160,14 @@ __device__ int drain_targets(WarpSym<HB>& S, int i, int lane) {
       S.tab[slot] = kEmpty;
     }
     const bool t = key > i;
-    const unsigned bal = __ballot_sync(kFullMask, t);
-    __syncwarp();
+    const unsigned bal = (__ballot_sync(gmask, t) >> lead) & (G == 32 ? 0xffffffffu : ((1u << G) - 1u));
+    __syncwarp(gmask);
     if (t) S.ins[base + __popc(bal & ((1u << lane) - 1u))] = key;
     base += __popc(bal);
-    __syncwarp();
+    __syncwarp(gmask);
   }
   if (lane == 0) S.nfill = 0;
-  __syncwarp();
+  __syncwarp(gmask);
   return base;
 }
 
@@ -176,27 +176,30 @@ __device__ int drain_targets(WarpSym<HB>& S, int i, int lane) {
 // PASS 0: count[i] = row length, or (the search outgrew this tier's table)
 // the row joins the next tier's list; PASS 1: write the row. Warp per row,
 // grid-stride over all rows (P.list == nullptr) or over the rows of P.list.
-template <int PASS, int HB>
+template <int PASS, int HB, int G = 32>
 __global__ void __launch_bounds__(kSymThreads) levelk_fast(SymParams P) {
-  using W = WarpSym<HB>;
+  using W = WarpSym<HB, G>;
+  constexpr int kGroups = kSymThreads / G;  // rows in flight per CTA
   extern __shared__ unsigned char smem_raw[];
   W* all = reinterpret_cast<W*>(smem_raw);
-  const int lane = threadIdx.x & 31;
-  W& S = all[threadIdx.x >> 5];
-  for (int s = lane; s < W::kHash; s += 32) S.tab[s] = kEmpty;
+  const int lane_w = threadIdx.x & 31;
+  const int lane = lane_w & (G - 1), lead = lane_w & ~(G - 1);
+  const unsigned gmask = G == 32 ? kFullMask : (((1u << G) - 1u) << lead);
+  W& S = all[threadIdx.x / G];
+  for (int s = lane; s < W::kHash; s += G) S.tab[s] = kEmpty;
   if (lane == 0) {
     S.nfill = 0;
     S.ovf = 0;
   }
-  __syncwarp();
-  const int nw = gridDim.x * (kSymThreads / 32);
+  __syncwarp(gmask);
+  const int nw = gridDim.x * kGroups;
   const int nrows = P.list ? *P.nlist : P.n;
-  for (int r = blockIdx.x * (kSymThreads / 32) + (threadIdx.x >> 5); r < nrows; r += nw) {
+  for (int r = blockIdx.x * kGroups + static_cast<int>(threadIdx.x) / G; r < nrows; r += nw) {
     const int i = P.list ? P.list[r] : r;
     if (PASS == 1 && P.soff && P.soff[i] >= 0) continue;  // already written by the count pass
     // overflow is a property of the row, so the fill pass skips exactly the
     // rows the count pass handed on
-    const bool ok = search_fast<HB>(P, S, i, lane);
+    const bool ok = search_fast<HB, G>(P, S, i, lane, gmask);
     if (!ok) {
       if (PASS == 0 && lane == 0) {
         P.count[i] = -1;
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kSymThreads) levelk_fast(SymParams P) {
       }
       continue;
     }
-    const int m = drain_targets<HB>(S, i, lane);
+    const int m = drain_targets<HB, G>(S, i, lane, gmask, lead);
     int* out = nullptr;
     if (PASS == 0) {
       long long off = -1;
@@ -212,7 +215,7 @@ __global__ void __launch_bounds__(kSymThreads) levelk_fast(SymParams P) {
         off = static_cast<long long>(atomicAdd(P.cursor, static_cast<unsigned long long>(m + 1)));
         if (off + m + 1 > P.scratch_cap) off = -1;
       }
-      off = __shfl_sync(kFullMask, off, 0);
+      off = __shfl_sync(gmask, off, lead);
       if (lane == 0) {
         P.count[i] = 1 + m;
         if (P.soff) P.soff[i] = off;
@@ -224,13 +227,13 @@ __global__ void __launch_bounds__(kSymThreads) levelk_fast(SymParams P) {
     }
     // rank sort (keys are distinct)
     if (lane == 0) out[0] = i;
-    for (int e = lane; e < m; e += 32) {
+    for (int e = lane; e < m; e += G) {
       const int x = S.ins[e];
       int r = 0;
       for (int q = 0; q < m; ++q) r += S.ins[q] < x;
       out[1 + r] = x;
     }
-    __syncwarp();
+    __syncwarp(gmask);
   }
 }
 
@@ -334,35 +337,48 @@ cudaError_t launch_levelk_copy(const SymParams& p, int grid, bool long_rows, cud
 }
 
 size_t sym_smem_bytes(int hb) {
+  if (hb == kSymHashTiny) return sizeof(WarpSym<kSymHashTiny, 8>) * (kSymThreads / 8);
   return hb == kSymHashSmall ? sizeof(WarpSym<kSymHashSmall>) * (kSymThreads / 32)
                              : sizeof(WarpSym<kSymHashLarge>) * (kSymThreads / 32);
 }
 
-template <int PASS, int HB>
+template <int PASS, int HB, int G>
 static cudaError_t fast_attr() {
-  return cudaFuncSetAttribute(levelk_fast<PASS, HB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(levelk_fast<PASS, HB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               static_cast<int>(sym_smem_bytes(HB)));
 }
 
+// hb: kSymHashTiny = 8 lanes per row with 128-slot tables, else a warp per row
 cudaError_t sym_occupancy(int hb, int* ctas_per_sm) {
-  cudaError_t e = hb == kSymHashSmall ? fast_attr<0, kSymHashSmall>() : fast_attr<0, kSymHashLarge>();
-  if (e == cudaSuccess) e = hb == kSymHashSmall ? fast_attr<1, kSymHashSmall>() : fast_attr<1, kSymHashLarge>();
+  cudaError_t e = cudaSuccess;
+  if (hb == kSymHashTiny) {
+    e = fast_attr<0, kSymHashTiny, 8>();
+    if (e == cudaSuccess) e = fast_attr<1, kSymHashTiny, 8>();
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, levelk_fast<0, kSymHashTiny, 8>, kSymThreads,
+                                                         sym_smem_bytes(hb));
+  }
+  e = hb == kSymHashSmall ? fast_attr<0, kSymHashSmall, 32>() : fast_attr<0, kSymHashLarge, 32>();
+  if (e == cudaSuccess) e = hb == kSymHashSmall ? fast_attr<1, kSymHashSmall, 32>() : fast_attr<1, kSymHashLarge, 32>();
   if (e != cudaSuccess) return e;
   return hb == kSymHashSmall
-             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, levelk_fast<0, kSymHashSmall>,
+             ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, levelk_fast<0, kSymHashSmall, 32>,
                                                              kSymThreads, sym_smem_bytes(hb))
-             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, levelk_fast<0, kSymHashLarge>,
+             : cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, levelk_fast<0, kSymHashLarge, 32>,
                                                              kSymThreads, sym_smem_bytes(hb));
 }
 
 cudaError_t launch_levelk_fast(const SymParams& p, int pass, int hb, int grid, cudaStream_t st) {
   const size_t sm = sym_smem_bytes(hb);
-  if (hb == kSymHashSmall) {
-    if (pass == 0) levelk_fast<0, kSymHashSmall><<<grid, kSymThreads, sm, st>>>(p);
-    else levelk_fast<1, kSymHashSmall><<<grid, kSymThreads, sm, st>>>(p);
+  if (hb == kSymHashTiny) {
+    if (pass == 0) levelk_fast<0, kSymHashTiny, 8><<<grid, kSymThreads, sm, st>>>(p);
+    else levelk_fast<1, kSymHashTiny, 8><<<grid, kSymThreads, sm, st>>>(p);
+  } else if (hb == kSymHashSmall) {
+    if (pass == 0) levelk_fast<0, kSymHashSmall, 32><<<grid, kSymThreads, sm, st>>>(p);
+    else levelk_fast<1, kSymHashSmall, 32><<<grid, kSymThreads, sm, st>>>(p);
   } else {
-    if (pass == 0) levelk_fast<0, kSymHashLarge><<<grid, kSymThreads, sm, st>>>(p);
-    else levelk_fast<1, kSymHashLarge><<<grid, kSymThreads, sm, st>>>(p);
+    if (pass == 0) levelk_fast<0, kSymHashLarge, 32><<<grid, kSymThreads, sm, st>>>(p);
+    else levelk_fast<1, kSymHashLarge, 32><<<grid, kSymThreads, sm, st>>>(p);
   }
   return cudaGetLastError();
 }

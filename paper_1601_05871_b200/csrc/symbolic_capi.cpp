@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -213,7 +214,11 @@ tcg_status tcg_sym_levelk(tcg_sym* s, int32_t level, int32_t flags, tcg_sym_stat
   int* counters = s->over + 2 * (n + 1);  // [tier 2 rows, global-path rows]
   const int warps = tcbdev::kSymThreads / 32;
   int occ1 = 0, occ2 = 0;
-  SYM_TRY(s, tcbdev::sym_occupancy(tcbdev::kSymHashSmall, &occ1));
+  // small searches (level <= 1, sparse rows): tier 1 runs 4 rows per warp, 8 lanes each
+  bool tiny = P.kk <= 1 && s->nnz_a <= 10LL * n;
+  if (const char* e = std::getenv("TCG_SYM_TINY")) tiny = std::atoi(e) != 0;
+  const int hb1 = tiny ? tcbdev::kSymHashTiny : tcbdev::kSymHashSmall;
+  SYM_TRY(s, tcbdev::sym_occupancy(hb1, &occ1));
   SYM_TRY(s, tcbdev::sym_occupancy(tcbdev::kSymHashLarge, &occ2));
   const int grid1 = std::max(1, std::min(s->sm_count * std::max(occ1, 1), (n + warps - 1) / warps));
   const int grid2 = std::max(1, s->sm_count * std::max(occ2, 1));
@@ -244,7 +249,7 @@ tcg_status tcg_sym_levelk(tcg_sym* s, int32_t level, int32_t flags, tcg_sym_stat
     tcbdev::SymParams A = P;  // tier 1: every row
     A.over = list1;
     A.nover = counters;
-    SYM_TRY(s, tcbdev::launch_levelk_fast(A, 0, tcbdev::kSymHashSmall, grid1, s->stream));
+    SYM_TRY(s, tcbdev::launch_levelk_fast(A, 0, hb1, grid1, s->stream));
     tcbdev::SymParams B = P;  // tier 2: the rows tier 1 handed on (count read on the device)
     B.list = list1;
     B.nlist = counters;
@@ -306,7 +311,7 @@ tcg_status tcg_sym_levelk(tcg_sym* s, int32_t level, int32_t flags, tcg_sym_stat
   if (n > 0 && !(flags & TCG_SYM_ALL_SLOW) && short_scratch) {
     tcbdev::SymParams A = P;
     A.list = nullptr;
-    SYM_TRY(s, tcbdev::launch_levelk_fast(A, 1, tcbdev::kSymHashSmall, grid1, s->stream));
+    SYM_TRY(s, tcbdev::launch_levelk_fast(A, 1, hb1, grid1, s->stream));
     ++launches;
     if (cnt[0] > 0) {
       tcbdev::SymParams B = P;
