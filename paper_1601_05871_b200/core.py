@@ -856,14 +856,22 @@ class PcgResult:
 
 
 def pcg(solver: "GpuTriSolve", b, tol: float = 1e-8, maxit: int = 1000, precondition: bool = True,
-        device: int = 0) -> PcgResult:
+        device: int = 0, check_every: int = 8) -> PcgResult:
     """Conjugate gradients on PᵀAP x = b on the GPU, preconditioned with the
     IC(k) factor the solver's context holds (z = (UᵀU)⁻¹ r through
     tcg_solve_apply_device) -- the caller of the factorization. The system
     matrix must be set (solver.set_matrix). Vectors and the dots live on the
-    device (torch, on the context's stream); one host read per iteration for
-    the convergence test."""
+    device (torch, on the context's stream).
+
+    Converged means ‖r‖ <= tol·‖b‖. The test runs on the device: a 0/1 mask
+    (1 until the first converged iteration) scales every later step, so x and
+    r freeze at that iteration, and the host reads the residual history once
+    every ``check_every`` iterations instead of syncing on each one. The
+    iterates, the iteration count and x are the same for any check_every (at
+    most check_every - 1 frozen iterations run after convergence)."""
     import torch
+    if check_every < 1:
+        raise ValueError("check_every must be >= 1")
     dev = torch.device("cuda", device)
     stream = torch.cuda.ExternalStream(solver.stream_ptr(), device=dev)
     t0 = time.perf_counter()
@@ -883,24 +891,36 @@ def pcg(solver: "GpuTriSolve", b, tol: float = 1e-8, maxit: int = 1000, precondi
         bnorm = float(torch.linalg.vector_norm(bd).item())
         if bnorm == 0.0:
             return PcgResult(np.zeros(bd.numel()), 0, True, 0.0, time.perf_counter() - t0)
+        thr = tol * bnorm
+        hist = torch.empty(max(maxit, 1), dtype=torch.float64, device=dev)
+        live = torch.ones((), dtype=torch.bool, device=dev)
         prec(r, z)
         p = z.clone()
         rz = torch.dot(r, z)
-        it, rel, converged = 0, 1.0, False
-        while it < maxit:
-            it += 1
-            solver.spmv_ptr(p.data_ptr(), ap.data_ptr())
-            alpha = rz / torch.dot(p, ap)
-            x.add_(alpha * p)
-            r.sub_(alpha * ap)
-            rel = float(torch.linalg.vector_norm(r).item()) / bnorm
-            if rel <= tol:
-                converged = True
-                break
-            prec(r, z)
-            rz_new = torch.dot(r, z)
-            p.mul_(rz_new / rz).add_(z)
-            rz = rz_new
+        done, it, rel, converged = 0, 0, 1.0, False
+        while done < maxit and not converged:
+            k = min(check_every, maxit - done)
+            for _ in range(k):
+                solver.spmv_ptr(p.data_ptr(), ap.data_ptr())
+                alpha = rz / torch.dot(p, ap)
+                # where, not alpha·live: a frozen step may carry 0/0 (r hit 0 exactly)
+                x.add_(torch.where(live, alpha * p, 0.0))
+                r.sub_(torch.where(live, alpha * ap, 0.0))
+                nr = torch.linalg.vector_norm(r)
+                hist[done] = nr
+                done += 1
+                live = live & torch.logical_not(nr <= thr)  # a NaN norm stays live
+                prec(r, z)
+                rz_new = torch.dot(r, z)
+                p.mul_(rz_new / rz).add_(z)
+                rz = rz_new
+            h = hist[done - k:done].cpu().numpy()
+            hit = np.nonzero(h <= thr)[0]
+            if hit.size:
+                it = done - k + int(hit[0]) + 1
+                rel, converged = float(h[hit[0]]) / bnorm, True
+            else:
+                it, rel = done, float(h[-1]) / bnorm
         out = x.cpu().numpy()
     torch.cuda.synchronize(dev)
     return PcgResult(out, it, converged, rel, time.perf_counter() - t0)

@@ -222,3 +222,48 @@ def test_gpu_pcg(T, name):
         s.close()
     finally:
         fz.close()
+
+
+def test_gpu_pcg_check_interval_is_invisible(T):
+    # the device-side convergence mask: reading the residual history every
+    # iteration or every 8 / 64 gives the same iterations and the same x
+    _, an = analyzed("c5_m0")
+    ap = an.a_permuted
+    fz = factored(T, "c5_m0")
+    try:
+        s = T.GpuTriSolve(fz)
+        s.set_matrix(ap)
+        b = np.random.default_rng(4).standard_normal(ap.nrows)
+        runs = [T.pcg(s, b, tol=1e-9, maxit=500, check_every=c) for c in (1, 8, 64)]
+        for r in runs[1:]:
+            assert r.converged and r.iterations == runs[0].iterations
+            assert r.relative_residual == runs[0].relative_residual
+            assert bitwise_equal(r.x, runs[0].x)
+        # maxit not a multiple of the interval; not converged
+        short = T.pcg(s, b, tol=1e-30, maxit=13, check_every=8)
+        assert not short.converged and short.iterations == 13
+        with pytest.raises(ValueError):
+            T.pcg(s, b, check_every=0)
+        s.close()
+    finally:
+        fz.close()
+
+
+def test_gpu_pcg_exact_preconditioner_stops_clean(T):
+    # complete fill: the apply is a direct solve, r reaches (near) zero at once;
+    # the frozen iterations after it must not spoil x
+    a = T.generate("random_spd", 120, 40000, 5)
+    an = T.analyze(a, level=120)
+    fz = T.GpuFactorizer(T.Plan(an.a_permuted, an.pattern, an.ranges))
+    try:
+        fz.factor()
+        s = T.GpuTriSolve(fz)
+        s.set_matrix(an.a_permuted)
+        b = np.random.default_rng(6).standard_normal(an.a_permuted.nrows)
+        res = T.pcg(s, b, tol=1e-8, maxit=50, check_every=16)
+        assert res.converged and res.iterations <= 3 and np.all(np.isfinite(res.x))
+        zero = T.pcg(s, np.zeros_like(b), tol=1e-8)
+        assert zero.converged and zero.iterations == 0
+        s.close()
+    finally:
+        fz.close()

@@ -1,5 +1,6 @@
 """IC(k)-preconditioned vs plain CG on the GPU (paper_1601_05871_b200.pcg):
-iterations and wall time to a 1e-8 relative residual, b = ones."""
+iterations and wall time to a 1e-8 relative residual, b = ones, per
+convergence-check interval (PCG_CHECK, default 1,8)."""
 import os
 import sys
 
@@ -19,9 +20,10 @@ for name in sys.argv[1:] or ["c2", "c6"]:
     s.set_matrix(an.a_permuted)
     b = np.ones(a.nrows)
     for pre in (True, False):
-        T.pcg(s, b, tol=1e-8, maxit=5, precondition=pre)  # warm-up
-        r = T.pcg(s, b, tol=1e-8, maxit=5000, precondition=pre)
-        print(f"{name} {'IC' if pre else 'plain'}: {r.iterations} iterations, converged={r.converged}, "
+      for ce in (int(c) for c in os.environ.get("PCG_CHECK", "1,8").split(",")):
+        T.pcg(s, b, tol=1e-8, maxit=5, precondition=pre, check_every=ce)  # warm-up
+        r = T.pcg(s, b, tol=1e-8, maxit=5000, precondition=pre, check_every=ce)
+        print(f"{name} {'IC' if pre else 'plain'} check_every={ce}: {r.iterations} iterations, converged={r.converged}, "
               f"{r.seconds * 1e3:.1f} ms ({r.seconds * 1e3 / r.iterations:.3f} ms/iteration)", flush=True)
     s.close()
     fz.close()
