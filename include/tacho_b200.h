@@ -326,6 +326,11 @@ tcg_status tcg_solve_apply(tcg_solve* s, const double* b, double* x, int32_t whi
 /* device vectors (b_dev and x_dev may alias), on the context's stream */
 tcg_status tcg_solve_apply_device(tcg_solve* s, const double* b_dev, double* x_dev, int32_t which,
                                   tcg_solve_stats* stats);
+/* The same apply without a host wait (for iterative callers that queue many steps):
+ * enqueued on the context's stream, returns at once. A watchdog expiry is sticky and is
+ * reported by the next tcg_solve_sync (or synchronous apply), which waits for the stream. */
+tcg_status tcg_solve_apply_async(tcg_solve* s, const double* b_dev, double* x_dev, int32_t which);
+tcg_status tcg_solve_sync(tcg_solve* s);
 /* The caller's other step per CG iteration: y = A x with the system matrix (PᵀAP), set once
  * (host CSR with values, n x n), applied to device vectors on the context's stream; per row
  * the products are summed in column order. */

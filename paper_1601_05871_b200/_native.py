@@ -237,6 +237,8 @@ SIGNATURES = [
     ("tcg_solve_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tcg_solve_stream", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     ("tcg_solve_apply_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(SolveStats)]),
+    ("tcg_solve_apply_async", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32]),
+    ("tcg_solve_sync", C.c_int, [C.c_void_p]),
     ("tch_generate", C.c_void_p, [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]),
     ("tch_matrix_from_csr", C.c_void_p, [C.POINTER(CsrView)]),
     ("tch_matrix_free", None, [C.c_void_p]),

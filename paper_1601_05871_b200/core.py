@@ -803,6 +803,18 @@ class GpuTriSolve:
             raise (SchedulerError if st == N.TCG_TIMEOUT else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
         return self.stats()
 
+    def apply_async_ptr(self, b_ptr: int, x_ptr: int, which: int = 3):
+        """apply_device_ptr without the host wait; errors surface at sync()."""
+        st = self._lib.tcg_solve_apply_async(self.h, C.c_void_p(b_ptr), C.c_void_p(x_ptr), which)
+        if st != N.TCG_OK:
+            raise (ValueError if st == N.TCG_INVALID else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
+
+    def sync(self):
+        """Wait for the context's stream; raise SchedulerError if an apply's watchdog expired."""
+        st = self._lib.tcg_solve_sync(self.h)
+        if st != N.TCG_OK:
+            raise (SchedulerError if st == N.TCG_TIMEOUT else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
+
     def apply_host_ptr(self, b_ptr: int, x_ptr: int, which: int = 3) -> SolveStats:
         """Host vectors by address (pinned memory for full PCIe speed)."""
         st = self._lib.tcg_solve_apply(self.h, C.cast(b_ptr, N.f64p), C.cast(x_ptr, N.f64p), which,
@@ -861,7 +873,8 @@ def pcg(solver: "GpuTriSolve", b, tol: float = 1e-8, maxit: int = 1000, precondi
     IC(k) factor the solver's context holds (z = (UᵀU)⁻¹ r through
     tcg_solve_apply_device) -- the caller of the factorization. The system
     matrix must be set (solver.set_matrix). Vectors and the dots live on the
-    device (torch, on the context's stream).
+    device (torch, on the context's stream); the applies are queued without a
+    host wait (tcg_solve_apply_async).
 
     Converged means ‖r‖ <= tol·‖b‖. The test runs on the device: a 0/1 mask
     (1 until the first converged iteration) scales every later step, so x and
@@ -884,7 +897,7 @@ def pcg(solver: "GpuTriSolve", b, tol: float = 1e-8, maxit: int = 1000, precondi
 
         def prec(src, dst):
             if precondition:
-                solver.apply_device_ptr(src.data_ptr(), dst.data_ptr(), N.TCG_SOLVE_BOTH)
+                solver.apply_async_ptr(src.data_ptr(), dst.data_ptr(), N.TCG_SOLVE_BOTH)
             else:
                 dst.copy_(src)
 
@@ -915,6 +928,7 @@ def pcg(solver: "GpuTriSolve", b, tol: float = 1e-8, maxit: int = 1000, precondi
                 p.mul_(rz_new / rz).add_(z)
                 rz = rz_new
             h = hist[done - k:done].cpu().numpy()
+            solver.sync()  # a watchdog expiry in any of the k applies raises here
             hit = np.nonzero(h <= thr)[0]
             if hit.size:
                 it = done - k + int(hit[0]) + 1

@@ -197,6 +197,7 @@ tcg_status tcg_solve_create(tcg_ctx* ctx, const tcg_csr_view* u, tcg_solve** out
     e = cudaMemcpy(s->idx, T.idx.data(), sizeof(int) * T.idx.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !T.fpos.empty())
     e = cudaMemcpy(s->fpos, T.fpos.data(), sizeof(int) * T.fpos.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(s->error, 0, sizeof(int));  // the sticky watchdog flag
   if (e != cudaSuccess) {
     tcg_solve_destroy(s.release());
     return TCG_CUDA;
@@ -219,8 +220,12 @@ void tcg_solve_destroy(tcg_solve* s) {
 
 const char* tcg_solve_error(const tcg_solve* s) { return s ? s->err.c_str() : "null tcg_solve"; }
 
-tcg_status tcg_solve_apply_device(tcg_solve* s, const double* b_dev, double* x_dev, int32_t which,
-                                  tcg_solve_stats* st) {
+namespace {
+
+// Enqueue one apply on the context's stream (no host wait). The watchdog flag
+// is sticky: the kernel only sets it; read_and_clear_error() consumes it.
+tcg_status enqueue_apply(tcg_solve* s, const double* b_dev, double* x_dev, int32_t which, int* grid_out,
+                         cudaStream_t* stream_out) {
   if (!s || which < 1 || which > 3 || (s->n > 0 && (!b_dev || !x_dev))) {
     if (s) s->err = "tcg_solve_apply: which must be 1, 2 or 3 and the vectors non-null";
     return TCG_INVALID;
@@ -260,15 +265,37 @@ tcg_status tcg_solve_apply_device(tcg_solve* s, const double* b_dev, double* x_d
   SOLVE_TRY(s, cudaEventRecord(s->ev0, stream));
   if (s->n > 0) {
     SOLVE_TRY(s, cudaMemsetAsync(s->y, 0xFF, 2 * align_up(nd, 256), stream));  // y and x: the marker
-    SOLVE_TRY(s, cudaMemsetAsync(s->error, 0, sizeof(int), stream));
     if (which & 1) SOLVE_TRY(s, tcbdev::launch_solve_gather(vals, s->fpos, s->fval, s->noff, s->sm_count, stream));
     SOLVE_TRY(s, tcbdev::launch_trisolve(P, grid, stream));
     SOLVE_TRY(s, cudaMemcpyAsync(x_dev, which == 1 ? s->y : s->x, nd, cudaMemcpyDeviceToDevice, stream));
   }
   SOLVE_TRY(s, cudaEventRecord(s->ev1, stream));
-  SOLVE_TRY(s, cudaEventSynchronize(s->ev1));
+  *grid_out = grid;
+  *stream_out = stream;
+  return TCG_OK;
+}
+
+// After the stream is idle: report (and clear) a watchdog expiry of any apply since the last check.
+tcg_status read_and_clear_error(tcg_solve* s) {
+  if (s->n <= 0) return TCG_OK;
   int error = 0;
-  if (s->n > 0) SOLVE_TRY(s, cudaMemcpy(&error, s->error, sizeof(int), cudaMemcpyDeviceToHost));
+  SOLVE_TRY(s, cudaMemcpy(&error, s->error, sizeof(int), cudaMemcpyDeviceToHost));
+  if (!error) return TCG_OK;
+  SOLVE_TRY(s, cudaMemset(s->error, 0, sizeof(int)));
+  s->err = "tcg_solve_apply: device watchdog expired";
+  return TCG_TIMEOUT;
+}
+
+}  // namespace
+
+tcg_status tcg_solve_apply_device(tcg_solve* s, const double* b_dev, double* x_dev, int32_t which,
+                                  tcg_solve_stats* st) {
+  int grid = 0;
+  cudaStream_t stream = nullptr;
+  const tcg_status q = enqueue_apply(s, b_dev, x_dev, which, &grid, &stream);
+  if (q != TCG_OK) return q;
+  SOLVE_TRY(s, cudaEventSynchronize(s->ev1));
+  const tcg_status e = read_and_clear_error(s);
   if (st) {
     float ms = 0.f;
     SOLVE_TRY(s, cudaEventElapsedTime(&ms, s->ev0, s->ev1));
@@ -278,11 +305,25 @@ tcg_status tcg_solve_apply_device(tcg_solve* s, const double* b_dev, double* x_d
     st->grid_ctas = grid;
     st->kernel_launches = s->n > 0 ? ((which & 1) && s->noff > 0 ? 2 : 1) : 0;
   }
-  if (error) {
-    s->err = "tcg_solve_apply: device watchdog expired";
-    return TCG_TIMEOUT;
-  }
-  return TCG_OK;
+  return e;
+}
+
+tcg_status tcg_solve_apply_async(tcg_solve* s, const double* b_dev, double* x_dev, int32_t which) {
+  int grid = 0;
+  cudaStream_t stream = nullptr;
+  return enqueue_apply(s, b_dev, x_dev, which, &grid, &stream);
+}
+
+tcg_status tcg_solve_sync(tcg_solve* s) {
+  if (!s) return TCG_INVALID;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  const double* vals = nullptr;
+  std::int64_t n = 0, nnz = 0;
+  if (!tcb_internal::ctx_factor(s->ctx, 0, &device, &stream, &vals, &n, &nnz)) return TCG_INVALID;
+  SOLVE_TRY(s, cudaSetDevice(device));
+  SOLVE_TRY(s, cudaStreamSynchronize(stream));
+  return read_and_clear_error(s);
 }
 
 tcg_status tcg_solve_trace(tcg_solve* s, uint64_t* stamps, void* recs) {

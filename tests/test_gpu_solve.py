@@ -267,3 +267,28 @@ def test_gpu_pcg_exact_preconditioner_stops_clean(T):
         s.close()
     finally:
         fz.close()
+
+
+def test_async_apply_matches_and_queues(T):
+    # tcg_solve_apply_async: same bits as the synchronous apply; several queued
+    # back to back (chained through one buffer) before one tcg_solve_sync
+    import torch
+    fz = factored(T, "c5_m0")
+    try:
+        s = T.GpuTriSolve(fz)
+        n = planned("c5_m0").pattern.nrows
+        b = np.random.default_rng(8).standard_normal(n)
+        ref = b.copy()
+        for _ in range(4):
+            ref = s.apply(ref)
+        v = torch.from_numpy(b).cuda()
+        torch.cuda.synchronize()
+        for _ in range(4):
+            s.apply_async_ptr(v.data_ptr(), v.data_ptr(), 3)
+        s.sync()
+        assert bitwise_equal(v.cpu().numpy(), ref)
+        with pytest.raises(ValueError):
+            s.apply_async_ptr(v.data_ptr(), v.data_ptr(), 4)
+        s.close()
+    finally:
+        fz.close()
