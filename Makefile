@@ -20,10 +20,10 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xptxas
 CXXFLAGS := -O2 -std=c++17 -fPIC -pthread -Wall -Wextra -ffp-contract=off
 
 HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generators.cpp $(SRC)/host/io.cpp \
-             $(SRC)/host/plan.cpp $(SRC)/capi.cpp $(SRC)/symbolic_capi.cpp $(SRC)/solve_capi.cpp
+             $(SRC)/host/plan.cpp $(SRC)/host/flow_plan.cpp $(SRC)/capi.cpp $(SRC)/symbolic_capi.cpp $(SRC)/solve_capi.cpp
 HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
-DEV_OBJS := $(OBJ)/device/factor_kernel.o $(OBJ)/device/row_kernel.o $(OBJ)/device/static_kernel.o \
-            $(OBJ)/device/flow_kernel.o $(OBJ)/device/symbolic_kernel.o \
+DEV_OBJS := $(OBJ)/device/factor_kernel.o \
+            $(OBJ)/device/flow_kernel.o $(OBJ)/device/flow_program.o $(OBJ)/device/symbolic_kernel.o \
             $(OBJ)/device/solve_kernel.o
 
 .PHONY: all lib oracle ref clean
@@ -54,14 +54,6 @@ clean:
 	rm -rf build $(OUT)/*.so
 	$(MAKE) -C oracle clean
 
-$(OBJ)/device/row_kernel.o: $(SRC)/device/row_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh $(SRC)/device/row_compute.cuh
-	@mkdir -p $(dir $@)
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_row_kernel.txt || (cat build/ptxas_row_kernel.txt; false)
-
-$(OBJ)/device/static_kernel.o: $(SRC)/device/static_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh $(SRC)/device/row_compute.cuh
-	@mkdir -p $(dir $@)
-	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_static_kernel.txt || (cat build/ptxas_static_kernel.txt; false)
-
 $(OBJ)/device/flow_kernel.o: $(SRC)/device/flow_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_flow_kernel.txt || (cat build/ptxas_flow_kernel.txt; false)
@@ -73,3 +65,7 @@ $(OBJ)/device/symbolic_kernel.o: $(SRC)/device/symbolic_kernel.cu $(SRC)/device/
 $(OBJ)/device/solve_kernel.o: $(SRC)/device/solve_kernel.cu $(SRC)/device/solve_api.hpp $(SRC)/device/sync.cuh
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_solve_kernel.txt || (cat build/ptxas_solve_kernel.txt; false)
+
+$(OBJ)/device/flow_program.o: $(SRC)/device/flow_program.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_flow_program.txt || (cat build/ptxas_flow_program.txt; false)

@@ -1,7 +1,11 @@
 """Benchmark of the GPU IC(k) numeric factorization (the reference's
 factor_by_blocks hot path) -- prints ONE JSON line on rank 0.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+The default workload is C3 (BASELINE.json configs[2], 27-point 48^3 IC(2),
+7.6 M factor entries), the largest configuration that runs on one GPU; the
+other configurations are selectable and are parity-test cases.
 
 A step is one numeric factorization of the configuration's matrix, starting
 from the initialised factor U resident in HBM (the reference's
@@ -28,9 +32,15 @@ C5 batch: the 64 members are split over the ranks (paper_1601_05871_b200/
 batch.py), each rank factors its members in one launch, value = 64 * nnz_u /
 max-over-ranks time (strong scaling over the fixed batch).
 
+  parity_vs_oracle  the last factor's hash against the golden hash of the
+         reference's factor_serial (tests/golden), every configuration.
+  one_shot  wall time of one factor_by_blocks_gpu call (plan, context,
+         upload, factor, download), the reference's unit of work.
+
 --impl reference: times the reference's own CPU factor_by_blocks
 (oracle/_ref, compiled from the unmodified reference headers) with a pooled
-policy over all host threads, rank 0 only.
+policy over all host threads, rank 0 only, on inputs built by the shim
+(generators + the reference's analyze); factor_serial and pooled(1) beside it.
 """
 from __future__ import annotations
 
@@ -42,6 +52,8 @@ import subprocess
 import sys
 import threading
 import time
+
+import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -200,7 +212,30 @@ def cpu_reference_times(an, workers: int, reps: int):
     return out
 
 
+# generator table of the configurations (core.CONFIGS), repeated here so the
+# reference arm does not import the package: (kind, p0, p1, seed, level)
+REF_CONFIGS = {"c1": ("grid2d", 100, 100, 0, 0), "c2": ("lap7", 64, 0, 0, 1), "c3": ("stencil27", 48, 0, 1, 2),
+               "c4": ("elasticity", 40, 0, 1, 0), "c5": ("diffusion", 32, 1000, 1, 1), "c6": ("lap7", 128, 0, 0, 1)}
+
+
+class _Csr:
+    def __init__(self, n, ptr, col, val=None):
+        self.nrows, self.row_ptr, self.col_idx = n, ptr, col
+        self.values = val if val is not None else np.ones(col.size)
+
+    def nnz(self):
+        return int(self.col_idx.size)
+
+
 def run_reference(args):
+    """The reference's own CPU path, nothing of this repo's product on it: the
+    inputs come from the shim (the repo's seeded generators compiled into
+    oracle/_ref next to the unmodified reference headers), the reference's
+    analyze() orders and fills, and the timed call is its factor_by_blocks
+    with TaskPolicy::pooled(all host threads) -- numeric_seconds, the same
+    region as ours (factorize.hpp:169-227). factor_serial and pooled(1) are
+    reported beside it. C5 batch: the 64 members' factor_serial spread over
+    all host threads (the reference has no batch API), wall time."""
     rank, _, world = dist_env()
     if rank != 0:
         return
@@ -209,34 +244,91 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref (reference compiled from /root/reference) was not built"}))
         return
-    a, an, plan, _ = build_problem(args.config)
-    u = an.pattern.pattern
     R = Reference()
     cores = os.cpu_count() or 1
-    times = []
-    for i in range(args.warmup + args.steps):
-        _, st, secs, _, _, _ = R.factor_by_blocks(an.a_permuted, u, an.ranges.bounds, workers=cores,
-                                                  want_values=False)
-        if st != 0:
-            raise RuntimeError(f"reference factor_by_blocks status {st}")
-        if i >= args.warmup:
-            times.append(secs)
-    serial = [R.factor_serial(an.a_permuted, u)[2] for _ in range(3)]
-    t = statistics.mean(times)
+    name = "c5" if args.config in ("c5", "c5b") else args.config
+    kind, p0, p1, seed, level = REF_CONFIGS[name]
+
+    def problem(sd):
+        ptr, col, val = R.generate(kind, p0, p1, sd)
+        n = ptr.size - 1
+        ra = R.analyze(_Csr(n, ptr, col, val), level=level)
+        return (n, _Csr(n, ra["a_ptr"], ra["a_col"], ra["a_val"]), _Csr(n, ra["u_ptr"], ra["u_col"]),
+                ra["bounds"])
+
+    n, ap, u, bounds = problem(seed)
     nnz = u.nnz()
-    value = nnz / t
+    serial = [R.factor_serial(ap, u)[2] for _ in range(3)]
+    pool1 = R.factor_by_blocks(ap, u, bounds, workers=1, want_values=False)[2]
+    times, walls = [], []
+    if args.config == "c5b":
+        from concurrent.futures import ThreadPoolExecutor
+        members = [ap] + [problem(b + 1)[1] for b in range(1, 64)]
+        units = 64 * nnz
+        with ThreadPoolExecutor(cores) as ex:
+            for i in range(args.warmup + args.steps):
+                t0 = time.perf_counter()
+                sts = list(ex.map(lambda m: R.factor_serial(m, u)[1], members))
+                dt = time.perf_counter() - t0
+                if any(sts):
+                    raise RuntimeError("reference factor_serial breakdown in the batch")
+                if i >= args.warmup:
+                    times.append(dt)
+                    walls.append(dt)
+        policy = f"64 x factor_serial over {cores} threads"
+    else:
+        units = nnz
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            _, st, secs, _, _, _ = R.factor_by_blocks(ap, u, bounds, workers=cores, want_values=False)
+            wall = time.perf_counter() - t0
+            if st != 0:
+                raise RuntimeError(f"reference factor_by_blocks status {st}")
+            if i >= args.warmup:
+                times.append(secs)
+                walls.append(wall)
+        policy = f"TaskPolicy::pooled({cores})"
+    t = statistics.mean(times)
+    value = units / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS[args.config], "n": a.nrows, "nnz_u": nnz,
-                   "policy": f"TaskPolicy::pooled({cores})"},
+        "scaling": "strong" if args.config == "c5b" else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, SURVEY.md Appendix B)",
+        "config": {"workload": WORKLOADS[args.config], "n": n, "nnz_u": nnz, "policy": policy,
+                   "inputs": "oracle/_ref: repo generators + the reference's analyze() (no product library)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                         "sample": f"{args.steps} full factor_by_blocks runs (pooled, {cores} threads)"},
+                         "sample": f"{args.steps} full runs, {policy}; numeric_seconds"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "reference_factor_serial_s_median": statistics.median(serial),
+        "reference_paths_ms": {"factor_serial_median": statistics.median(serial) * 1e3,
+                               "factor_by_blocks_pooled1": pool1 * 1e3,
+                               f"factor_by_blocks_pooled{cores}": t * 1e3 if args.config != "c5b" else None,
+                               "one_shot_wall_median": statistics.median(walls) * 1e3},
     }
     print(json.dumps(line))
+
+
+def golden_parity(got, names, aps, u):
+    """'bitwise (golden hash)' when every member's factor hashes to the golden
+    hash of the reference's factor_serial; else the max relative difference
+    against the oracle (checker only)."""
+    from checkers import Oracle
+    O = Oracle()
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        golden = json.load(f)
+    checked, bad = 0, []
+    for g, nm, ap in zip(got, names, aps):
+        want = golden.get(nm, {}).get("factor_values")
+        if want is None:
+            continue
+        checked += 1
+        if O.hash(np.ascontiguousarray(g)) != want:
+            ref = O.factor_serial(ap, u)[0]
+            bad.append(float(np.max(np.abs(g - ref) / (np.abs(ref) + 1e-300))))
+    if not checked:
+        return "no golden hash for " + ",".join(names)
+    return f"bitwise (golden hash of the reference's factor_serial, {checked} checked)" if not bad else \
+        f"MISMATCH max_rel={max(bad):.3e}"
 
 
 def chain_hop_us(dev: int) -> float:
@@ -277,6 +369,9 @@ def run_ours(args):
     u = an.pattern.pattern
     nnz, n = u.nnz(), a.nrows
     fz = T.GpuFactorizer(plan, T.GpuOptions(device=dev, mode=args.mode, timeout_s=60))
+    _, prog_upd, prog_ms = fz.flow_programs() if args.mode in (0, 5) else (None, np.zeros((0, 2)), 0.0)
+    nprod = len(prog_upd)
+    del prog_upd
     batched = args.config == "c5b"
     nmembers_total, mine, batch_vals = 1, range(1), None
     if batched:
@@ -345,16 +440,33 @@ def run_ours(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e = float(t.item())
 
-    # parity of the last factor against the oracle (small configs only, rank 0)
+    # parity of the last factor on every configuration: its hash against the
+    # golden hash of the reference's factor_serial (tests/golden, produced by
+    # the unmodified reference), i.e. bitwise equality with the reference
     parity = None
-    if rank == 0 and nnz <= 3_000_000:
-        from checkers import Oracle
-        O = Oracle()
+    if rank == 0:
         got = host_out.numpy().reshape(per_rank, nnz)
-        refs = [O.factor_serial(ap, u)[0] for ap in (batch_perms if batched else [an.a_permuted])]
-        bad = [float(np.max(np.abs(g - r) / (np.abs(r) + 1e-300))) for g, r in zip(got, refs)
-               if not np.array_equal(g.view(np.int64), r.view(np.int64))]
-        parity = "bitwise" if not bad else f"max_rel={max(bad):.3e}"
+        names = [f"c5_m{m}" for m in mine] if batched else [args.config]
+        parity = golden_parity(got, names, [an.a_permuted] if not batched else batch_perms, u)
+
+    # one-shot drop-in call (the reference's unit of work, factorize.hpp:134-235):
+    # factor_by_blocks_gpu from (PᵀAP, pattern, ranges) on the host to the factor on
+    # the host -- plan, context, upload, factor, download, teardown -- wall time
+    one_shot = None
+    if not batched and not args.no_one_shot:
+        walls, res = [], None
+        for i in range(4):
+            t0 = time.perf_counter()
+            res = T.factor_by_blocks_gpu(an.a_permuted, an.pattern, an.ranges)
+            if i:
+                walls.append(time.perf_counter() - t0)
+        one_shot = {"ms": statistics.median(walls) * 1e3, "calls": len(walls),
+                    "plan_ms": res.stats.plan_seconds * 1e3, "block_build_ms": res.stats.block_build_seconds * 1e3,
+                    "device_ms": res.stats.device_ms,
+                    "parity": golden_parity(res.factor.values.reshape(1, -1), [args.config], [an.a_permuted], u)
+                    if rank == 0 else None,
+                    "call": "factor_by_blocks_gpu(a_permuted, fp, ranges): plan + tcg_create + upload + factor + "
+                            "download + destroy, warm process (CUDA initialised), median of 3 after 1"}
 
     # CPU baseline (rank 0, N = 1): the reference's own serial factorization
     cpu = None
@@ -381,10 +493,8 @@ def run_ours(args):
         "scaling": "strong" if batched else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, SURVEY.md Appendix B)",
         "config": {"workload": WORKLOADS[args.config], "n": n, "nnz_u": nnz,
-                   "tasks": int(sum(ps.tasks)), "dag_depth": int(ps.dag_depth),
-                   "rows": int(ps.items), "row_depth": int(ps.item_depth),
+                   "tasks": int(sum(ps.tasks)),
                    "mode": {1: "task DAG / device merge", 2: "task DAG / update programs",
-                            3: "row-level DAG / ready queues", 4: "row-level DAG / static level schedule",
                             5: "value flow / static schedule of the finalising rows"}[st.mode],
                    "flow_rows": int(ps.flow_rows), "flow_depth": int(ps.flow_depth),
                    "grid_ctas": int(st.grid_ctas), "threads_per_cta": int(st.threads_per_cta),
@@ -392,7 +502,9 @@ def run_ours(args):
                                    f"per rank" if batched else
                                    f"replicas{world}" if world > 1 else "single"),
                    "l2": "flushed between steps (256 MiB write), U restored from device copy (untimed)",
-                   "analysis_s": round(t_an, 3), "plan_s": round(ps.plan_seconds + ps.block_build_seconds, 3),
+                   "analysis_s": round(t_an, 3), "plan_s": round(ps.plan_seconds, 4),
+                   "plan_host_threads": int(ps.host_threads),
+                   "programs_device_ms": round(prog_ms, 3), "products": int(nprod),
                    "parity_vs_oracle": parity},
         "e2e": {"value": units / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz_a * per_rank,
                 "d2h_bytes_per_step": 8 * nnz * per_rank, "ms_per_step": e2e,
@@ -412,6 +524,7 @@ def run_ours(args):
                           "bound_ms": round(ps.flow_depth * hop_us / 1e3, 4),
                           "frac": round(ps.flow_depth * hop_us / 1e3 / step_ms, 4)},
         "cpu_baseline": cpu,
+        "one_shot": one_shot,
         "clocks": clocks.summary(),
     }
     if rank == 0:
@@ -474,7 +587,7 @@ def run_sharded(args):
         dev_ms.append(st.device_ms)
     barrier()
     step_ms = max_over(statistics.mean(dev_ms), dev)
-    host_in = torch.from_numpy(plan.tables()["values"]).pin_memory()
+    host_in = torch.from_numpy(plan.flow_tables()["values"]).pin_memory()
     host_out = torch.empty(nnz, dtype=torch.float64).pin_memory()
     e2e_ms = []
     for i in range(args.warmup + args.steps):
@@ -790,10 +903,12 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--config", default="c3", choices=sorted(WORKLOADS),
+                    help="c3 (default): the largest single-GPU configuration of BASELINE.json")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", type=int, default=0, help="0 auto, 1/2 task DAG, 3 row DAG")
+    ap.add_argument("--mode", type=int, default=0, help="0 auto (5: value flow), 1/2 task DAG")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-one-shot", action="store_true", help="skip the one-shot drop-in calls")
     ap.add_argument("--path", default="factor", choices=["factor", "symbolic", "solve"],
                     help="factor: the numeric factorization (headline); symbolic: level-k pattern on the "
                          "device; solve: the preconditioner apply with the factor")

@@ -15,12 +15,19 @@
  * crosses it; every call returns a tcg_status. One context per host thread.
  *
  * Entry points and the reference interface each one replaces:
- *   tcg_plan_build    build_block_matrix + the generation walk of
- *                     factor_by_blocks/export_task_dag, flattened
- *                     (block_layout.hpp:98-181, factorize.hpp:169-225,260-302)
- *   tcg_upload        the one-arena upload of U values, block-CSR work
- *                     tables, the task DAG and dependence counters
- *                     (replaces the TaskView/Future state, block_layout.hpp:66-93)
+ *   tcg_plan_build    the host side of factor_by_blocks before its numeric
+ *                     region: init_factor_values (factorize.hpp:71-89), the
+ *                     block layout's task counts (block_layout.hpp:98-181,
+ *                     factorize.hpp:177-224) and the value-flow schedule of
+ *                     the finalising rows, O(nnz) host work
+ *   tcg_plan_expand   the full generation walk of factor_by_blocks /
+ *                     export_task_dag, flattened (factorize.hpp:169-225,
+ *                     260-302): the DAG contract and the task executors
+ *   tcg_upload        the one-arena upload of U values and the schedule;
+ *                     the update programs (the pattern-restricted merges of
+ *                     kernels.hpp:40-132, per coordinate) are built on the
+ *                     device (replaces the TaskView/Future state,
+ *                     block_layout.hpp:66-93)
  *   tcg_factor        spawn-all + wait(policy) over the whole DAG, executing
  *                     chol/trsm/herk/gemm_block (kernels.hpp:40-132) on the
  *                     GPU; breakdown latch and rethrow (factorize.hpp:146-167,229)
@@ -84,48 +91,28 @@ typedef struct {
   const int32_t* slot_rec;     /*   per target slot {u_b, u_e, m0, o0}; item word 6 = first slot */
   int64_t nupdates;
   const int32_t* upd;          /*   (m, o) pairs: U[tb+k] -= U[m] * U[o] */
-  /* row-level execution (optional; requires the update programs): */
-  const int32_t* row_rec;      /*   8 words per item: tb, te, dpos, slot_off, kind, t, succ_b, succ_e */
-  int64_t nrow_edges;
-  const int32_t* row_succ;     /*   successor items, grouped per item */
-  const int32_t* row_indeg;    /*   dependence counters per item */
-  int64_t nrow_roots;
-  const int32_t* row_roots;
-  const int32_t* row_order;    /*   static schedule: items by (level, falling height) */
-  const int32_t* row_pred_ptr; /*   nitems + 1 offsets into row_pred */
-  const int32_t* row_pred;     /*   predecessor items (nrow_edges) */
-  const int32_t* pos_rec;      /*   per schedule position, 16 words: tb, L, dpos, slot_off, kind,
-                                    t, npred, pred_off, 4 inline predecessor items, item, 0,0,0 */
-  int64_t npos_pred;
-  const int32_t* pos_pred;     /*   predecessor items beyond the inline four */
-  /* value-flow execution (optional; mode 5): the Chol/Trsm items, each applying every
-   * update of its slice, in a static (level, falling height) order */
+  /* value-flow execution (mode 5): the finalising rows of U (whole rows of up to 32 entries;
+   * else a row's diagonal-block slice and warp-wide chunks of the rest), each applying every
+   * update of its coordinates, in a static (level, falling height) order */
   int64_t nflow;
   const int32_t* flow_rec;     /*   4 words per position: tb, L | kind << 30, dpos, t */
-  const int32_t* flow_item;    /*   per position: its item (trace stamps are per item) */
-  const int32_t* flow_slot;    /*   4 words per coordinate of U: u_b, u_e, m0, o0 */
-  int64_t nflow_upd;
-  const int32_t* flow_upd;     /*   (m, o) pairs */
-  /* block units (optional; mode 6): large diagonal blocks run as CTA-wide units with their
-   * values in shared memory; rows outside units as in mode 5 */
-  int64_t m6_nrows;
-  const int32_t* m6_row_rec;   /*   4 words per row outside units, in schedule order */
-  const int32_t* m6_row_item;
-  int64_t m6_nunits;
-  const int32_t* m6_unit_rec;  /*   4 words per unit: level slot begin, end, first row, order */
-  int64_t m6_nurows;
-  const int32_t* m6_urow_rec;  /*   4 words per unit row, by intra-unit level */
-  const int32_t* m6_urow_lbase;/*   first shared-memory index of the row's values */
-  const int32_t* m6_urow_item;
-  int64_t m6_nlev;
-  const int32_t* m6_ulev;      /*   per level slot: end of its rows */
-  const int32_t* m6_slot;      /*   flow_slot with intra-unit operands as 0x80000000|index */
-  const int32_t* m6_upd;       /*   nflow_upd pairs, same rewrite */
-  int64_t m6_smem;             /*   bytes of the largest unit */
+  const int32_t* flow_item;    /*   per position: its unit id (trace stamps are per unit) */
+  const int32_t* flow_slot;    /*   host-built programs (flow_devprog = 0): 4 words per coordinate */
+  int64_t nflow_upd;           /*   of U {u_b, u_e, m0, o0} and nflow_upd (m, o) pairs */
+  const int32_t* flow_upd;
   /* device init_factor_values (optional): per U slot, the position in a_permuted's values it
    * starts from (-1 = fill, starts at 0.0); absent when A has duplicate entries */
   int64_t nnz_a;
   const int32_t* a_map;
+  /* value flow with device-built programs (the default, tcg_plan_build): nflow / flow_rec /
+   * flow_item are the schedule, flow_slot / flow_upd stay NULL -- tcg_upload builds U's
+   * transposed index and the update programs on the device from U's pattern */
+  int32_t flow_devprog;        /* 1: u_row_ptr is set */
+  const int32_t* u_row_ptr;    /*   n + 1 positions of U's rows (int32) */
+  /* a part of a sharded run (tcg_plan_part_problem): the schedule holds the part's rows; the
+   * device programs read operands of rows other parts own from their U (tcg_set_peers) */
+  int32_t flow_part;           /* -1: the whole matrix */
+  const int32_t* part_of_row;  /*   owner part of every row (n) */
 } tcg_problem;
 
 typedef struct {
@@ -134,12 +121,12 @@ typedef struct {
   int32_t staging_cap;      /* target-row entries staged per warp; 0 = auto */
   double timeout_s;         /* device watchdog; 0 = default (30 s) */
   int32_t trace;            /* 1 = record per-task start/end globaltimer stamps */
-  int32_t mode;             /* 0 = auto (5 when available), task-level DAG execution with
-                               1 = device merge of sorted indices or 2 = precomputed update
-                               programs; row-level execution of the same DAG with 3 = ready
-                               queues + counters, 4 = static level schedule + row flags or
-                               5 = static schedule of the finalising rows, readers polling
-                               the values themselves (no flags, no fences) */
+  int32_t mode;             /* 0 = auto (5), task-level DAG execution (the reference's
+                               Chol/Trsm/Herk/Gemm tasks, device ready queue + dependence
+                               counters; needs tcg_plan_expand) with 1 = device merge of
+                               sorted indices or 2 = precomputed update programs; 5 = static
+                               schedule of the finalising rows, readers polling the values
+                               themselves (no flags, no fences) */
   int32_t lanes_per_row;    /* mode 5: lanes working on one row (32, or 8 with 256 threads);
                                0 = default (32) */
 } tcg_options;
@@ -156,7 +143,7 @@ typedef struct {
   int64_t smem_bytes;
   int32_t kernel_launches;   /* device launches issued by the call */
   int64_t helpers_run;       /* helper tickets that joined a multi-CTA task */
-  int32_t mode;              /* execution mode used (1 .. 5, see tcg_options.mode) */
+  int32_t mode;              /* execution mode used (1, 2 or 5, see tcg_options.mode) */
   uint64_t profile[7];       /* trace mode, rows: SM cycles in {pop wait, row body, publish
                                 fence, release} summed over warps; rows, pops, pushes */
   int32_t lanes_per_row;     /* mode 5: lanes per row used */
@@ -169,22 +156,21 @@ typedef struct {
 } tcg_stats;
 
 typedef struct {
-  int64_t tasks[4];          /* chol, trsm, herk, gemm */
-  int64_t edges, items, sources, pairs, empty_tasks;
-  int32_t max_target_len, max_flag_rows, dag_depth;
-  int32_t max_width;         /* most CTAs cooperating on one task */
-  int64_t helpers;           /* helper tickets over all multi-CTA tasks */
-  int64_t updates;           /* products in the update programs (0 if not built) */
-  int64_t item_edges;        /* row-level dependences */
-  int32_t item_depth;        /* longest row-level chain, in items */
+  int64_t tasks[4];          /* chol, trsm, herk, gemm (counted from the block layout) */
   int32_t nblocks_rows;      /* block rows m (= number of ranges) */
   int64_t nblocks;
   double block_build_seconds, plan_seconds;
   int64_t flow_rows;         /* value-flow rows (mode 5) */
   int32_t flow_depth;        /* longest value-flow chain, in rows */
-  int64_t unit_count, unit_rows;   /* mode 6 block units and the rows inside them */
-  int32_t unit_depth;        /* longest chain of units and rows */
-  int32_t unit_max_levels;   /* most intra-unit levels */
+  int32_t host_threads;      /* host threads the plan used */
+  /* the task-DAG plan (tcg_plan_expand; 0 until it exists) */
+  int32_t full_plan;         /* 1 when it exists */
+  double full_plan_seconds;  /* its host time */
+  int64_t edges, items, sources, pairs, empty_tasks;
+  int32_t max_target_len, max_flag_rows, dag_depth;
+  int32_t max_width;         /* most CTAs cooperating on one task */
+  int64_t helpers;           /* helper tickets over all multi-CTA tasks */
+  int64_t updates;           /* products in the task executors' update programs */
 } tcg_plan_stats;
 
 /* ---- host flattener ---------------------------------------------------- */
@@ -194,7 +180,12 @@ tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pa
                           int32_t nranges, const int32_t* range_bounds, tcg_plan** out);
 void tcg_plan_free(tcg_plan* plan);
 const char* tcg_plan_error(void); /* message of the last failed tcg_plan_build (thread-local) */
+/* The upload image: U, its initial values and the value-flow schedule (programs built on the
+ * device); with the task-DAG plan (tcg_plan_expand) also the task executors' tables. */
 tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* out);
+/* Builds the task-DAG plan (the reference's generation walk, flattened) if it does not exist
+ * yet; tcg_plan_dag, tcg_plan_blocks and tcg_plan_part_problem do so on first use. */
+tcg_status tcg_plan_expand(tcg_plan* plan);
 tcg_status tcg_plan_get_stats(const tcg_plan* plan, tcg_plan_stats* out);
 /* DAG in generation order, the export_task_dag contract (factorize.hpp:260-302):
  * node kind/block_row/block_col and edges (before, after) in emission order.
@@ -243,6 +234,9 @@ tcg_status tcg_download_trace(tcg_ctx* ctx, uint64_t* stamps);
 /* Device pointer to the working values and their count (for in-process users
  * that keep U resident, e.g. a preconditioner apply on the same stream). */
 tcg_status tcg_device_values(tcg_ctx* ctx, double** dptr, int64_t* nnz);
+/* The value-flow update programs on the device (slot: 4 * nnz ints {u_b, u_e, m0, o0}; upd:
+ * 2 * nupd ints (m, o); either may be NULL) and the device time of their build (ms). */
+tcg_status tcg_flow_programs(tcg_ctx* ctx, int32_t* slot, int32_t* upd, int64_t* nupd, double* build_ms);
 /* Batch of value sets sharing the uploaded pattern (mode 5; C5-style refactorization of
  * many matrices with one structure). `values`: nbatch x nnz host doubles, member-major.
  * nbatch = 1 returns to the single-matrix state. tcg_factor then factors every member in

@@ -19,6 +19,10 @@
 #include "taskchol/matrix_market.hpp"
 #include "taskchol/pipeline.hpp"
 #include "taskchol/symbolic.hpp"
+// this repo's seeded generators, compiled into the
+// shim so bench.py's reference arm builds its inputs without loading the
+// product library
+#include "../paper_1601_05871_b200/csrc/host/sparse.hpp"
 
 using namespace taskchol;
 
@@ -227,6 +231,31 @@ int ref_write_mm(int32_t n, const int64_t* ptr, const int32_t* col, const double
   } catch (const std::exception& e) {
     g_err = e.what();
     return 1;
+  }
+}
+
+// The BASELINE.json matrices (same generators and seeds as tch_generate),
+// as a reference CsrMatrix; NULL with ref_error() on failure.
+ref_csr* ref_generate(const char* kind, int64_t p0, int64_t p1, uint64_t seed) {
+  try {
+    const std::string k(kind ? kind : "");
+    const auto i0 = static_cast<tcb::index_t>(p0);
+    tcb::CsrMatrix g;
+    if (k == "grid2d") g = tcb::grid_laplacian_2d(i0, static_cast<tcb::index_t>(p1));
+    else if (k == "lap7") g = tcb::laplacian_7pt(i0);
+    else if (k == "stencil27") g = tcb::stencil27_variable(i0, seed);
+    else if (k == "elasticity") g = tcb::elasticity27(i0, seed);
+    else if (k == "diffusion") g = tcb::diffusion_7pt_lognormal(i0, seed, static_cast<double>(p1) / 1000.0);
+    else throw std::invalid_argument("unknown generator '" + k + "'");
+    auto out = std::make_unique<ref_csr>();
+    out->m.nrows = out->m.ncols = g.nrows;
+    out->m.row_ptr.assign(g.row_ptr.begin(), g.row_ptr.end());
+    out->m.col_idx.assign(g.col_idx.begin(), g.col_idx.end());
+    out->m.values.assign(g.values.begin(), g.values.end());
+    return out.release();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
   }
 }
 

@@ -56,40 +56,18 @@ class Problem(C.Structure):
         ("slot_rec", i32p),
         ("nupdates", C.c_int64),
         ("upd", i32p),
-        ("row_rec", i32p),
-        ("nrow_edges", C.c_int64),
-        ("row_succ", i32p),
-        ("row_indeg", i32p),
-        ("nrow_roots", C.c_int64),
-        ("row_roots", i32p),
-        ("row_order", i32p),
-        ("row_pred_ptr", i32p),
-        ("row_pred", i32p),
-        ("pos_rec", i32p),
-        ("npos_pred", C.c_int64),
-        ("pos_pred", i32p),
         ("nflow", C.c_int64),
         ("flow_rec", i32p),
         ("flow_item", i32p),
         ("flow_slot", i32p),
         ("nflow_upd", C.c_int64),
         ("flow_upd", i32p),
-        ("m6_nrows", C.c_int64),
-        ("m6_row_rec", i32p),
-        ("m6_row_item", i32p),
-        ("m6_nunits", C.c_int64),
-        ("m6_unit_rec", i32p),
-        ("m6_nurows", C.c_int64),
-        ("m6_urow_rec", i32p),
-        ("m6_urow_lbase", i32p),
-        ("m6_urow_item", i32p),
-        ("m6_nlev", C.c_int64),
-        ("m6_ulev", i32p),
-        ("m6_slot", i32p),
-        ("m6_upd", i32p),
-        ("m6_smem", C.c_int64),
         ("nnz_a", C.c_int64),
         ("a_map", i32p),
+        ("flow_devprog", C.c_int32),
+        ("u_row_ptr", i32p),
+        ("flow_part", C.c_int32),
+        ("part_of_row", i32p),
     ]
 
 
@@ -131,6 +109,15 @@ class Stats(C.Structure):
 class PlanStats(C.Structure):
     _fields_ = [
         ("tasks", C.c_int64 * 4),
+        ("nblocks_rows", C.c_int32),
+        ("nblocks", C.c_int64),
+        ("block_build_seconds", C.c_double),
+        ("plan_seconds", C.c_double),
+        ("flow_rows", C.c_int64),
+        ("flow_depth", C.c_int32),
+        ("host_threads", C.c_int32),
+        ("full_plan", C.c_int32),
+        ("full_plan_seconds", C.c_double),
         ("edges", C.c_int64),
         ("items", C.c_int64),
         ("sources", C.c_int64),
@@ -142,18 +129,6 @@ class PlanStats(C.Structure):
         ("max_width", C.c_int32),
         ("helpers", C.c_int64),
         ("updates", C.c_int64),
-        ("item_edges", C.c_int64),
-        ("item_depth", C.c_int32),
-        ("nblocks_rows", C.c_int32),
-        ("nblocks", C.c_int64),
-        ("block_build_seconds", C.c_double),
-        ("plan_seconds", C.c_double),
-        ("flow_rows", C.c_int64),
-        ("flow_depth", C.c_int32),
-        ("unit_count", C.c_int64),
-        ("unit_rows", C.c_int64),
-        ("unit_depth", C.c_int32),
-        ("unit_max_levels", C.c_int32),
     ]
 
 
@@ -192,6 +167,7 @@ SIGNATURES = [
     ("tcg_plan_free", None, [C.c_void_p]),
     ("tcg_plan_error", C.c_char_p, []),
     ("tcg_plan_problem", C.c_int, [C.c_void_p, C.POINTER(Problem)]),
+    ("tcg_plan_expand", C.c_int, [C.c_void_p]),
     ("tcg_plan_get_stats", C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
     ("tcg_plan_part_problem", C.c_int, [C.c_void_p, C.c_int32, i32p, C.c_int32, C.POINTER(Problem), i64p]),
     ("tcg_plan_dag", C.c_int, [C.c_void_p, i64p, C.POINTER(i32p), C.POINTER(i32p), C.POINTER(i32p),
@@ -215,6 +191,7 @@ SIGNATURES = [
     ("tcg_batch_size", C.c_int32, [C.c_void_p]),
     ("tcg_download_batch", C.c_int, [C.c_void_p, f64p]),
     ("tcg_batch_breakdown", C.c_int, [C.c_void_p, i32p, f64p]),
+    ("tcg_flow_programs", C.c_int, [C.c_void_p, i32p, i32p, i64p, f64p]),
     ("tcg_device_values", C.c_int, [C.c_void_p, C.POINTER(f64p), i64p]),
     ("tcg_arena_bytes", C.c_int64, [C.c_void_p]),
     ("tcg_set_peers", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_uint64)]),

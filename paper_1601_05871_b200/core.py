@@ -460,9 +460,29 @@ class Plan:
         return s
 
     def problem(self) -> N.Problem:
+        """The upload image: the value-flow schedule (update programs built on the
+        device), plus the task executors' tables once the plan is expanded."""
         p = N.Problem()
         self._lib.tcg_plan_problem(self.handle, C.byref(p))
         return p
+
+    def expand(self) -> "Plan":
+        """Build the task-DAG plan (the reference's generation walk, flattened)."""
+        if self._lib.tcg_plan_expand(self.handle) != N.TCG_OK:
+            raise ValueError(self._lib.tcg_plan_error().decode())
+        return self
+
+    def flow_tables(self) -> dict:
+        """The lean value-flow plan's host arrays (the schedule, U, initial values)."""
+        p = self.problem()
+        return {
+            "flow_rec": _copy(p.flow_rec, 4 * p.nflow, np.int32).reshape(-1, 4),
+            "flow_item": _copy(p.flow_item, p.nflow, np.int32),
+            "row_ptr": _copy(p.u_row_ptr, p.n + 1, np.int32),
+            "a_map": _copy(p.a_map, p.nnz, np.int32) if p.a_map else np.zeros(0, np.int32),
+            "values": _copy(p.values, p.nnz, np.float64),
+            "cols": _copy(p.col_idx, p.nnz, np.int32),
+        }
 
     def part_problem(self, nparts: int, owners: np.ndarray, part: int) -> N.Problem:
         """The rows of one part of a sharded run (tcg_plan_part_problem, mode 5)."""
@@ -492,7 +512,9 @@ class Plan:
         return _copy(bp, m.value + 1, np.int64), _copy(bc, nb.value, np.int32)
 
     def tables(self) -> dict:
-        """Copies of the device tables (for host-side inspection in tests)."""
+        """Copies of the task-DAG plan's tables (for host-side inspection in
+        tests; expands the plan)."""
+        self.expand()
         p = self.problem()
         return {
             "task": _copy(p.task_rec, 12 * p.ntasks, np.int32).reshape(-1, 12),
@@ -505,40 +527,9 @@ class Plan:
             "cols": _copy(p.col_idx, p.nnz, np.int32),
             "slot_rec": _copy(p.slot_rec, 4 * p.nslots, np.int32).reshape(-1, 4),
             "upd": _copy(p.upd, 2 * p.nupdates, np.int32).reshape(-1, 2),
-            "row_rec": (_copy(p.row_rec, 8 * p.nitems, np.int32).reshape(-1, 8)
-                        if p.row_rec else np.zeros((0, 8), np.int32)),
-            "row_succ": _copy(p.row_succ, p.nrow_edges, np.int32) if p.row_succ else np.zeros(0, np.int32),
-            "row_indeg": _copy(p.row_indeg, p.nitems, np.int32) if p.row_indeg else np.zeros(0, np.int32),
-            "row_roots": _copy(p.row_roots, p.nrow_roots, np.int32) if p.row_roots else np.zeros(0, np.int32),
-            "row_order": _copy(p.row_order, p.nitems, np.int32) if p.row_order else np.zeros(0, np.int32),
-            "pos_rec": (_copy(p.pos_rec, 16 * p.nitems, np.int32).reshape(-1, 16)
-                        if p.pos_rec else np.zeros((0, 16), np.int32)),
-            "pos_pred": _copy(p.pos_pred, p.npos_pred, np.int32) if p.pos_pred else np.zeros(0, np.int32),
-            "flow_rec": (_copy(p.flow_rec, 4 * p.nflow, np.int32).reshape(-1, 4)
-                         if p.flow_rec else np.zeros((0, 4), np.int32)),
-            "flow_item": _copy(p.flow_item, p.nflow, np.int32) if p.flow_item else np.zeros(0, np.int32),
-            "m6_row_rec": _copy(p.m6_row_rec, 4 * p.m6_nrows, np.int32).reshape(-1, 4) if p.m6_row_rec
-            else np.zeros((0, 4), np.int32),
-            "m6_row_item": _copy(p.m6_row_item, p.m6_nrows, np.int32) if p.m6_row_item else np.zeros(0, np.int32),
-            "m6_unit_rec": _copy(p.m6_unit_rec, 4 * p.m6_nunits, np.int32).reshape(-1, 4) if p.m6_unit_rec
-            else np.zeros((0, 4), np.int32),
-            "m6_urow_rec": _copy(p.m6_urow_rec, 4 * p.m6_nurows, np.int32).reshape(-1, 4) if p.m6_urow_rec
-            else np.zeros((0, 4), np.int32),
-            "m6_urow_lbase": _copy(p.m6_urow_lbase, p.m6_nurows, np.int32) if p.m6_urow_lbase
-            else np.zeros(0, np.int32),
-            "m6_urow_item": _copy(p.m6_urow_item, p.m6_nurows, np.int32) if p.m6_urow_item
-            else np.zeros(0, np.int32),
-            "m6_ulev": _copy(p.m6_ulev, p.m6_nlev, np.int32) if p.m6_ulev else np.zeros(0, np.int32),
-            "m6_slot": (_copy(p.m6_slot, 4 * p.nnz, np.int32).reshape(-1, 4) if p.m6_slot
-                        else np.zeros((0, 4), np.int32)),
-            "m6_upd": (_copy(p.m6_upd, 2 * p.nflow_upd, np.int32).reshape(-1, 2) if p.m6_upd
-                       else np.zeros((0, 2), np.int32)),
-            "m6_smem": int(p.m6_smem),
+            "flow_rec": _copy(p.flow_rec, 4 * p.nflow, np.int32).reshape(-1, 4),
+            "flow_item": _copy(p.flow_item, p.nflow, np.int32),
             "a_map": _copy(p.a_map, p.nnz, np.int32) if p.a_map else np.zeros(0, np.int32),
-            "flow_slot": (_copy(p.flow_slot, 4 * p.nnz, np.int32).reshape(-1, 4)
-                          if p.flow_slot else np.zeros((0, 4), np.int32)),
-            "flow_upd": (_copy(p.flow_upd, 2 * p.nflow_upd, np.int32).reshape(-1, 2)
-                         if p.flow_upd else np.zeros((0, 2), np.int32)),
         }
 
 
@@ -559,9 +550,9 @@ class GpuOptions:
     staging_cap: int = 0
     timeout_s: float = 0.0
     trace: bool = False
-    mode: int = 0  # 0 auto; task DAG: 1 device merge, 2 update programs; rows: 3 queues,
-    #                4 static + flags, 5 static value flow (finalising rows, no flags)
-    lanes_per_row: int = 0  # mode 4 row-group width (4/8/16/32), 0 = auto
+    mode: int = 0  # 0 auto (5); task DAG (expands the plan): 1 device merge, 2 update programs;
+    #                5 static value flow (finalising rows, the values are their own flags)
+    lanes_per_row: int = 0  # mode 5: lanes per row (32, or 8), 0 = 32
 
 
 class GpuFactorizer:
@@ -581,9 +572,12 @@ class GpuFactorizer:
                       self.opt.lanes_per_row)
         self._check(lib.tcg_set_options(self.ctx, C.byref(o)))
         self.plan = plan
+        if problem is None and self.opt.mode not in (0, 5):
+            plan.expand()  # the task executors run the task-DAG plan's tables
         self._problem = problem if problem is not None else plan.problem()
         self.nnz = int(self._problem.nnz)
         self.ntasks = int(self._problem.ntasks)
+        self._ntab = self.ntasks if self._problem.task_rec else 0
         self._check(lib.tcg_upload(self.ctx, C.byref(self._problem)))
         self.last = N.Stats()
 
@@ -708,10 +702,10 @@ class GpuFactorizer:
 
     def trace(self):
         """(task stamps [ntasks, 2], item stamps [nitems, 4]) of the last traced factor."""
-        ni = int(self._problem.nitems)
-        out = np.zeros(2 * self.ntasks + 4 * ni, dtype=np.uint64)
+        ni = max(int(self._problem.nitems), int(self._problem.nflow))
+        out = np.zeros(2 * self._ntab + 4 * ni, dtype=np.uint64)
         self._check(self._lib.tcg_download_trace(self.ctx, out.ctypes.data_as(N.u64p)))
-        return out[:2 * self.ntasks].reshape(-1, 2), out[2 * self.ntasks:].reshape(-1, 4)
+        return out[:2 * self._ntab].reshape(-1, 2), out[2 * self._ntab:].reshape(-1, 4)
 
     # ---- sharded runs (C6): other parts' U through peer memory ----
     def factor_phase(self, phase: int) -> N.Stats:
@@ -719,6 +713,17 @@ class GpuFactorizer:
         self.last = N.Stats()
         self._check(self._lib.tcg_factor_phase(self.ctx, phase, C.byref(self.last)))
         return self.last
+
+    def flow_programs(self):
+        """(slot [nnz, 4], upd [n, 2], build ms) of the uploaded value-flow programs."""
+        n, ms = C.c_int64(), C.c_double()
+        self._check(self._lib.tcg_flow_programs(self.ctx, C.cast(None, N.i32p), C.cast(None, N.i32p),
+                                                C.byref(n), C.byref(ms)))
+        slot = np.zeros((self.nnz, 4), np.int32)
+        upd = np.zeros((n.value, 2), np.int32)
+        self._check(self._lib.tcg_flow_programs(self.ctx, slot.ctypes.data_as(N.i32p), upd.ctypes.data_as(N.i32p),
+                                                C.byref(n), C.byref(ms)))
+        return slot, upd, ms.value
 
     def values_device_ptr(self) -> int:
         d = N.f64p()

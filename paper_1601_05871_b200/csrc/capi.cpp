@@ -14,6 +14,7 @@
 #include <string>
 
 #include "device/device_api.hpp"
+#include "host/flow_plan.hpp"
 #include "host/plan.hpp"
 #include "host/sparse.hpp"
 
@@ -55,13 +56,47 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 }  // namespace
 
+// A plan holds the lean value-flow plan (flow_plan.hpp: initial values and
+// the schedule, O(nnz) host work; U's transposed index and the update
+// programs are built on the device by tcg_upload) and, only when asked for,
+// the full task-DAG plan (plan.hpp: block layout, the reference's DAG, the
+// task executors' tables, sharded parts), built from the lean plan's copy of
+// the pattern.
 struct tcg_plan {
-  tcb::Plan plan;
-  std::vector<std::int32_t> brow_ptr32;  // unused, kept for ABI symmetry
+  tcb::FlowPlan flow;
+  tcb::RangeList ranges;
+  mutable std::unique_ptr<tcb::Plan> full;
   std::map<std::int32_t, tcb::FlowPart> parts;  // tcg_plan_part_problem results
-  std::vector<std::int32_t> a_map;  // device init_factor_values: U slot -> A position (-1 fill)
-  std::int64_t nnz_a = 0;
+  std::vector<std::int32_t> part_owner;         // the owner table of the last part problem
 };
+
+namespace {
+// the full task-DAG plan (built on first use)
+tcb::Plan& full_plan(const tcg_plan* plan) {
+  if (!plan->full) {
+    tcb::PlanOptions po;
+    if (const char* e = std::getenv("TCG_CTA_COST")) po.cta_cost = std::max(1.0, std::atof(e));
+    if (const char* e = std::getenv("TCG_MAX_WIDTH")) po.max_width = std::max(1, std::atoi(e));
+    if (const char* e = std::getenv("TCG_DEP_WIDE_COST")) po.dep_wide_cost = std::max(1.0, std::atof(e));
+    plan->full = std::make_unique<tcb::Plan>(
+        tcb::build_plan(tcb::flow_plan_pattern(plan->flow), plan->flow.values, plan->ranges, true, po));
+  }
+  return *plan->full;
+}
+
+tcb::CsrRef ref_of(const tcg_csr_view* v) {
+  if (!v || v->n < 0 || v->nnz < 0 || (!v->row_ptr && v->n > 0))
+    throw std::invalid_argument("csr view: null or negative sizes");
+  static const int64_t zero = 0;
+  tcb::CsrRef r;
+  r.n = v->n;
+  r.nnz = v->nnz;
+  r.row_ptr = v->row_ptr ? v->row_ptr : &zero;
+  r.col_idx = v->col_idx;
+  r.values = v->values;
+  return r;
+}
+}  // namespace
 
 struct tcg_ctx {
   int device = 0;
@@ -93,34 +128,8 @@ struct tcg_ctx {
   int4* slot_rec = nullptr;
   int2* upd = nullptr;
   bool has_programs = false;
-  // row-level mode
-  int4* rows = nullptr;
-  int* row_succ = nullptr;
-  int* row_indeg = nullptr;
-  int* row_indeg0 = nullptr;
-  int* row_queue = nullptr;
-  int* row_hiq = nullptr;
-  int* row_roots = nullptr;
-  std::int64_t nrow_roots = 0;
-  bool has_rows = false;
-  int4* pos_rec = nullptr;  // static schedule (mode 4)
-  int* pos_pred = nullptr;
-  int* row_flag = nullptr;
-  bool has_static = false;
   int4* flow_rec = nullptr;  // value-flow schedule (mode 5)
   int* flow_item = nullptr;
-  // block units (mode 6)
-  int4* m6_row_rec = nullptr;
-  int* m6_row_item = nullptr;
-  int4* m6_unit_rec = nullptr;
-  int4* m6_urow_rec = nullptr;
-  int* m6_urow_lbase = nullptr;
-  int* m6_urow_item = nullptr;
-  int* m6_ulev = nullptr;
-  int4* m6_slot = nullptr;
-  int2* m6_upd = nullptr;
-  std::int64_t m6_nrows = 0, m6_nunits = 0, m6_smem = 0;
-  bool has_units = false;
   int* a_map = nullptr;      // device init_factor_values (in the arena)
   // pipelined batches end to end (run_flow_chunked): copy streams, per-chunk
   // events and status words
@@ -147,6 +156,8 @@ struct tcg_ctx {
   double* bm_pivot = nullptr;
   int4* flow_slot = nullptr;
   int2* flow_upd = nullptr;
+  void* prog_arena = nullptr;  // device-built (m, o) pairs (their count is known after the count pass)
+  double prog_build_ms = 0.0;  // device time of the last program build
   double* flow_a = nullptr;  // snapshot of the input values
   std::int64_t nflow = 0, nflow_upd = 0;
   bool has_flow = false;
@@ -154,6 +165,7 @@ struct tcg_ctx {
   tcbdev::Ctrl* ctrl = nullptr;
   unsigned long long* trace = nullptr;
   // problem shape
+  std::int64_t ntab = 0;  // tasks with device tables (modes 1/2: the task-DAG plan was uploaded)
   std::int64_t n = 0, nnz = 0, ntasks = 0, nitems = 0, nsrc = 0, nedges = 0, nroots = 0;
   std::int64_t qcap = 0;
   int epoch = 0;
@@ -185,31 +197,27 @@ tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pa
   if (!out) return TCG_INVALID;
   *out = nullptr;
   try {
-    const tcb::CsrMatrix a = csr_from_view(a_permuted, true);
-    const tcb::CsrMatrix u = csr_from_view(pattern, false);
-    if (a.nrows != u.nrows) throw std::invalid_argument("a_permuted and pattern sizes differ");
+    const tcb::CsrRef a = ref_of(a_permuted), u = ref_of(pattern);
     if (nranges < 0 || (nranges > 0 && !range_bounds))
       throw std::invalid_argument("range list: null bounds");
-    tcb::RangeList rl;
-    for (int32_t r = 0; r < nranges; ++r) rl.ranges.push_back({range_bounds[r], range_bounds[r + 1]});
-    const std::vector<double> init = tcb::init_factor_values(a, u);
     auto p = std::make_unique<tcg_plan>();
-    tcb::PlanOptions po;
-    if (const char* e = std::getenv("TCG_CTA_COST")) po.cta_cost = std::max(1.0, std::atof(e));
-    if (const char* e = std::getenv("TCG_MAX_WIDTH")) po.max_width = std::max(1, std::atoi(e));
-    if (const char* e = std::getenv("TCG_DEP_WIDE_COST")) po.dep_wide_cost = std::max(1.0, std::atof(e));
-    if (const char* e = std::getenv("TCG_HOT_FRACTION")) po.hot_fraction = std::atof(e);
-    if (const char* e = std::getenv("TCG_UNIT_MIN_ROWS")) po.unit_min_rows = std::atoi(e);
-    if (const char* e = std::getenv("TCG_FLOW_MERGE_ROWS")) po.flow_merge_rows = std::atoi(e) != 0;
-    if (const char* e = std::getenv("TCG_UNIT_SMEM")) po.unit_smem_cap = std::atoll(e);
-    p->plan = tcb::build_plan(u, init, rl, true, po);
-    try {
-      p->a_map = tcb::init_factor_map(a, u);
-      p->nnz_a = a.nnz();
-    } catch (const std::invalid_argument&) {
-      p->a_map.clear();  // duplicates in A: no device init (host init_factor_values only)
-    }
+    for (int32_t r = 0; r < nranges; ++r) p->ranges.ranges.push_back({range_bounds[r], range_bounds[r + 1]});
+    p->flow = tcb::build_flow_plan(a, u, p->ranges);
     *out = p.release();
+    return TCG_OK;
+  } catch (const std::bad_alloc&) {
+    g_plan_error = "out of host memory";
+    return TCG_INVALID;
+  } catch (const std::exception& e) {
+    g_plan_error = e.what();
+    return TCG_INVALID;
+  }
+}
+
+tcg_status tcg_plan_expand(tcg_plan* plan) {
+  if (!plan) return TCG_INVALID;
+  try {
+    full_plan(plan);
     return TCG_OK;
   } catch (const std::bad_alloc&) {
     g_plan_error = "out of host memory";
@@ -225,11 +233,25 @@ const char* tcg_plan_error(void) { return g_plan_error.c_str(); }
 
 tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   if (!plan || !o) return TCG_INVALID;
-  const tcb::Plan& P = plan->plan;
-  o->n = P.n;
-  o->nnz = P.nnz;
-  o->col_idx = P.cols.data();
-  o->values = P.values.data();
+  *o = tcg_problem{};
+  const tcb::FlowPlan& F = plan->flow;
+  o->n = F.n;
+  o->nnz = F.nnz;
+  o->col_idx = F.cols.data();
+  o->values = F.values.data();
+  o->nnz_a = F.a_map.empty() ? 0 : F.nnz_a;
+  o->a_map = F.a_map.empty() ? nullptr : F.a_map.data();
+  o->ntasks = F.stats.tasks[0] + F.stats.tasks[1] + F.stats.tasks[2] + F.stats.tasks[3];
+  // the value-flow schedule with device-built programs (the default executor)
+  o->nflow = F.stats.units;
+  o->flow_rec = F.rec.data();
+  o->flow_item = F.unit.data();
+  o->flow_devprog = 1;
+  o->u_row_ptr = F.row_ptr.data();
+  o->flow_part = -1;
+  if (!plan->full) return TCG_OK;
+  // the task executors' tables (modes 1, 2) when the full plan exists
+  const tcb::Plan& P = *plan->full;
   o->ntasks = static_cast<int64_t>(P.node_kind.size());
   o->task_rec = P.task_rec.data();
   o->nitems = static_cast<int64_t>(P.item_rec.size() / tcb::kItemWords);
@@ -242,8 +264,6 @@ tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   o->indeg = P.indeg.data();
   o->nroots = static_cast<int64_t>(P.roots.size());
   o->roots = P.roots.data();
-  o->nnz_a = plan->a_map.empty() ? 0 : plan->nnz_a;
-  o->a_map = plan->a_map.empty() ? nullptr : plan->a_map.data();
   o->max_target_len = P.stats.max_target_len;
   o->max_flag_rows = P.stats.max_flag_rows;
   o->nhelpers = P.stats.helpers;
@@ -251,90 +271,56 @@ tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   o->slot_rec = P.slot_rec.data();
   o->nupdates = static_cast<int64_t>(P.upd.size() / 2);
   o->upd = P.upd.data();
-  const bool rows = !P.row_rec.empty() && !P.slot_rec.empty();
-  o->row_rec = rows ? P.row_rec.data() : nullptr;
-  o->nrow_edges = rows ? static_cast<int64_t>(P.row_succ.size()) : 0;
-  o->row_succ = rows ? P.row_succ.data() : nullptr;
-  o->row_indeg = rows ? P.row_indeg.data() : nullptr;
-  o->nrow_roots = rows ? static_cast<int64_t>(P.row_roots.size()) : 0;
-  o->row_roots = rows ? P.row_roots.data() : nullptr;
-  o->row_order = rows ? P.row_order.data() : nullptr;
-  o->row_pred_ptr = rows ? P.row_pred_ptr.data() : nullptr;
-  o->row_pred = rows ? P.item_dep.data() : nullptr;
-  o->pos_rec = rows ? P.pos_rec.data() : nullptr;
-  o->npos_pred = rows ? static_cast<int64_t>(P.pos_pred.size()) : 0;
-  o->pos_pred = rows ? P.pos_pred.data() : nullptr;
-  const bool flow = !P.flow_rec.empty();
-  o->nflow = flow ? static_cast<int64_t>(P.flow_rec.size() / tcb::kFlowWords) : 0;
-  o->flow_rec = flow ? P.flow_rec.data() : nullptr;
-  o->flow_item = flow ? P.flow_item.data() : nullptr;
-  o->flow_slot = flow ? P.flow_slot.data() : nullptr;
-  o->nflow_upd = flow ? static_cast<int64_t>(P.flow_upd.size() / 2) : 0;
-  o->flow_upd = flow ? P.flow_upd.data() : nullptr;
-  const bool m6 = flow && !P.m6_slot.empty();
-  o->m6_nrows = m6 ? static_cast<int64_t>(P.m6_row_item.size()) : 0;
-  o->m6_row_rec = m6 ? P.m6_row_rec.data() : nullptr;
-  o->m6_row_item = m6 ? P.m6_row_item.data() : nullptr;
-  o->m6_nunits = m6 ? P.m6_units : 0;
-  o->m6_unit_rec = m6 ? P.m6_unit_rec.data() : nullptr;
-  o->m6_nurows = m6 ? static_cast<int64_t>(P.m6_urow_item.size()) : 0;
-  o->m6_urow_rec = m6 ? P.m6_urow_rec.data() : nullptr;
-  o->m6_urow_lbase = m6 ? P.m6_urow_lbase.data() : nullptr;
-  o->m6_urow_item = m6 ? P.m6_urow_item.data() : nullptr;
-  o->m6_nlev = m6 ? static_cast<int64_t>(P.m6_ulev.size()) : 0;
-  o->m6_ulev = m6 ? P.m6_ulev.data() : nullptr;
-  o->m6_slot = m6 ? P.m6_slot.data() : nullptr;
-  o->m6_upd = m6 ? P.m6_upd.data() : nullptr;
-  o->m6_smem = m6 ? P.m6_smem : 0;
   return TCG_OK;
 }
 
 tcg_status tcg_plan_part_problem(tcg_plan* plan, int32_t nparts, const int32_t* part_of_row, int32_t part,
                                  tcg_problem* o, int64_t* remote_operands) {
   if (!plan || !o || !part_of_row) return TCG_INVALID;
-  const tcb::Plan& P = plan->plan;
   try {
-    std::vector<std::int32_t> own(part_of_row, part_of_row + P.n);
-    plan->parts[part] = tcb::build_flow_part(P, own, nparts, part);
+    std::vector<std::int32_t> own(part_of_row, part_of_row + plan->flow.n);
+    plan->parts[part] = tcb::build_flow_part(plan->flow, own, nparts, part);
+    plan->part_owner = std::move(own);
   } catch (const std::exception& e) {
     g_plan_error = e.what();
     return TCG_INVALID;
   }
   const tcb::FlowPart& F = plan->parts[part];
-  tcg_status st = tcg_plan_problem(plan, o);
-  if (st != TCG_OK) return st;
-  // only the value-flow tables describe a part: every other executor is off
-  o->row_rec = nullptr;
-  o->nrow_edges = 0;
-  o->row_succ = nullptr;
-  o->row_indeg = nullptr;
-  o->nrow_roots = 0;
-  o->row_roots = nullptr;
-  o->row_order = nullptr;
-  o->row_pred_ptr = nullptr;
-  o->row_pred = nullptr;
-  o->pos_rec = nullptr;
-  o->npos_pred = 0;
-  o->pos_pred = nullptr;
-  o->nslots = 0;
-  o->slot_rec = nullptr;
-  o->nupdates = 0;
-  o->upd = nullptr;
-  o->m6_nunits = 0;
+  *o = tcg_problem{};
+  const tcb::FlowPlan& P = plan->flow;
+  // only the value-flow tables describe a part: no task executor
+  o->n = P.n;
+  o->nnz = P.nnz;
+  o->col_idx = P.cols.data();
+  o->values = P.values.data();
+  o->ntasks = P.stats.tasks[0] + P.stats.tasks[1] + P.stats.tasks[2] + P.stats.tasks[3];
   o->nflow = F.rows;
   o->flow_rec = F.rec.data();
-  o->flow_item = F.item.data();
-  o->flow_slot = F.slot.data();
-  o->nflow_upd = static_cast<int64_t>(F.upd.size() / 2);
-  o->flow_upd = F.upd.data();
-  if (remote_operands) *remote_operands = F.remote_operands;
+  o->flow_item = F.unit.data();
+  o->flow_devprog = 1;
+  o->u_row_ptr = P.row_ptr.data();
+  o->flow_part = part;
+  o->part_of_row = plan->part_owner.data();
+  if (remote_operands) *remote_operands = F.remote_sources;
   return TCG_OK;
 }
 
 tcg_status tcg_plan_get_stats(const tcg_plan* plan, tcg_plan_stats* o) {
   if (!plan || !o) return TCG_INVALID;
-  const tcb::PlanStats& s = plan->plan.stats;
-  for (int k = 0; k < 4; ++k) o->tasks[k] = s.tasks[k];
+  *o = tcg_plan_stats{};
+  const tcb::FlowPlanStats& f = plan->flow.stats;
+  for (int k = 0; k < 4; ++k) o->tasks[k] = f.tasks[k];
+  o->nblocks_rows = f.nblock_rows;
+  o->nblocks = f.nblocks;
+  o->block_build_seconds = f.block_build_seconds;
+  o->plan_seconds = f.plan_seconds;
+  o->flow_rows = f.units;
+  o->flow_depth = f.depth;
+  o->host_threads = f.threads;
+  o->full_plan = plan->full ? 1 : 0;
+  if (!plan->full) return TCG_OK;
+  // the task-DAG statistics exist once the full plan does
+  const tcb::PlanStats& s = plan->full->stats;
   o->edges = s.edges;
   o->items = s.items;
   o->sources = s.sources;
@@ -346,18 +332,7 @@ tcg_status tcg_plan_get_stats(const tcg_plan* plan, tcg_plan_stats* o) {
   o->max_width = s.max_width;
   o->helpers = s.helpers;
   o->updates = s.updates;
-  o->item_edges = s.item_edges;
-  o->item_depth = s.item_depth;
-  o->nblocks_rows = plan->plan.blocks.m;
-  o->nblocks = plan->plan.blocks.nblocks();
-  o->block_build_seconds = s.block_build_seconds;
-  o->plan_seconds = s.plan_seconds;
-  o->flow_rows = s.flow_rows;
-  o->flow_depth = s.flow_depth;
-  o->unit_count = s.unit_count;
-  o->unit_rows = s.unit_rows;
-  o->unit_depth = s.unit_depth;
-  o->unit_max_levels = s.unit_max_levels;
+  o->full_plan_seconds = s.plan_seconds + s.block_build_seconds;
   return TCG_OK;
 }
 
@@ -365,26 +340,36 @@ tcg_status tcg_plan_dag(const tcg_plan* plan, int64_t* nnodes, const int32_t** k
                         const int32_t** block_row, const int32_t** block_col, int64_t* nedges,
                         const int32_t** edge_from, const int32_t** edge_to) {
   if (!plan) return TCG_INVALID;
-  const tcb::Plan& P = plan->plan;
-  if (nnodes) *nnodes = static_cast<int64_t>(P.node_kind.size());
-  if (kind) *kind = P.node_kind.data();
-  if (block_row) *block_row = P.node_i.data();
-  if (block_col) *block_col = P.node_j.data();
-  if (nedges) *nedges = static_cast<int64_t>(P.edge_from.size());
-  if (edge_from) *edge_from = P.edge_from.data();
-  if (edge_to) *edge_to = P.edge_to.data();
-  return TCG_OK;
+  try {
+    const tcb::Plan& P = full_plan(plan);
+    if (nnodes) *nnodes = static_cast<int64_t>(P.node_kind.size());
+    if (kind) *kind = P.node_kind.data();
+    if (block_row) *block_row = P.node_i.data();
+    if (block_col) *block_col = P.node_j.data();
+    if (nedges) *nedges = static_cast<int64_t>(P.edge_from.size());
+    if (edge_from) *edge_from = P.edge_from.data();
+    if (edge_to) *edge_to = P.edge_to.data();
+    return TCG_OK;
+  } catch (const std::exception& e) {
+    g_plan_error = e.what();
+    return TCG_INVALID;
+  }
 }
 
 tcg_status tcg_plan_blocks(const tcg_plan* plan, int32_t* m, const int64_t** brow_ptr,
                            int64_t* nblocks, const int32_t** bcol_idx) {
   if (!plan) return TCG_INVALID;
-  const tcb::BlockLayout& B = plan->plan.blocks;
-  if (m) *m = B.m;
-  if (brow_ptr) *brow_ptr = B.brow_ptr.data();
-  if (nblocks) *nblocks = B.nblocks();
-  if (bcol_idx) *bcol_idx = B.bcol_idx.data();
-  return TCG_OK;
+  try {
+    const tcb::BlockLayout& B = full_plan(plan).blocks;
+    if (m) *m = B.m;
+    if (brow_ptr) *brow_ptr = B.brow_ptr.data();
+    if (nblocks) *nblocks = B.nblocks();
+    if (bcol_idx) *bcol_idx = B.bcol_idx.data();
+    return TCG_OK;
+  } catch (const std::exception& e) {
+    g_plan_error = e.what();
+    return TCG_INVALID;
+  }
 }
 
 // -------------------------------------------------------------- device ----
@@ -412,6 +397,7 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
 
 void tcg_destroy(tcg_ctx* c) {
   if (c && c->batch_arena) cudaFree(c->batch_arena);
+  if (c && c->prog_arena) cudaFree(c->prog_arena);
   if (c && c->a_stage) cudaFree(c->a_stage);
   if (c && c->drain_done) cudaFree(c->drain_done);
   if (c && c->peers) cudaFree(c->peers);
@@ -449,14 +435,119 @@ tcg_status tcg_set_options(tcg_ctx* c, const tcg_options* opt) {
   return TCG_OK;
 }
 
+}  // extern "C"
+
+// The value-flow update programs built on the device (flow_program.cu): U's
+// transposed index by a radix sort, a count pass, a scan, the (m, o) pairs'
+// own allocation, a fill pass. Scratch: one temporary allocation for the
+// index, the counts and the 32-bit offsets in the working values, the 64-bit
+// scan in the input snapshot (both rewritten before any factorization).
+static tcg_status build_programs(tcg_ctx* c, const tcg_problem* p) {
+  const std::int64_t n = p->n, nnz = p->nnz, ns = nnz - n;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  void* tmp = nullptr;
+  size_t scan_bytes = 0, sort_bytes = 0;
+  TCG_CUDA_TRY(c, tcbdev::flow_program_scan(nullptr, nullptr, nullptr, nnz, nullptr, nullptr, &scan_bytes,
+                                            c->sm_count, c->stream));
+  TCG_CUDA_TRY(c, tcbdev::flow_transpose(static_cast<int>(n), static_cast<int>(nnz), nullptr, nullptr, nullptr,
+                                         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &sort_bytes,
+                                         c->sm_count, c->stream));
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = off;
+    off = align_up(off + std::max<size_t>(bytes, 1), 256);
+    return at;
+  };
+  const size_t o_rp = take(sizeof(int) * (n + 1)), o_cp = take(sizeof(int) * (n + 1));
+  const size_t o_key = take(sizeof(int) * nnz), o_pos = take(sizeof(int) * nnz), o_rid = take(sizeof(int) * nnz);
+  const size_t o_keys = take(sizeof(int) * nnz), o_poss = take(sizeof(int) * nnz), o_cs = take(sizeof(int) * ns);
+  const size_t o_ctr = take(sizeof(int) * 2), o_tot = take(sizeof(long long));
+  const size_t o_own = take(p->flow_part >= 0 ? sizeof(int) * n : 0);
+  const size_t o_tmp = take(std::max(scan_bytes, sort_bytes));
+  TCG_CUDA_TRY(c, cudaMalloc(&tmp, off));
+  struct Free {
+    void* p;
+    ~Free() { cudaFree(p); }
+  } free_tmp{tmp};
+  char* b = static_cast<char*>(tmp);
+  int* row_ptr = reinterpret_cast<int*>(b + o_rp);
+  int* col_ptr = reinterpret_cast<int*>(b + o_cp);
+  int* col_pos = reinterpret_cast<int*>(b + o_poss);
+  int* col_src = reinterpret_cast<int*>(b + o_cs);
+  tcbdev::ProgParams q{};
+  q.n = static_cast<int>(n);
+  q.row_ptr = row_ptr;
+  q.cols = c->cols;
+  q.col_ptr = col_ptr;
+  q.col_src = col_src;
+  q.col_pos = col_pos;
+  q.next_row = reinterpret_cast<int*>(b + o_ctr);
+  int* count = reinterpret_cast<int*>(c->vals);   // nnz ints (of 2 nnz)
+  int* ub32 = count + nnz;                         // nnz ints
+  long long* ub64 = reinterpret_cast<long long*>(c->flow_a);
+  long long* total_d = reinterpret_cast<long long*>(b + o_tot);
+  q.count = count;
+  q.ub = ub32;
+  q.slot = c->flow_slot;
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(row_ptr, p->u_row_ptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, c->stream));
+  TCG_CUDA_TRY(c, cudaMemsetAsync(q.next_row, 0, sizeof(int) * 2, c->stream));
+  TCG_CUDA_TRY(c, cudaEventCreate(&e0));
+  TCG_CUDA_TRY(c, cudaEventCreate(&e1));
+  struct Ev {
+    cudaEvent_t a, b;
+    ~Ev() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+  } evs{e0, e1};
+  TCG_CUDA_TRY(c, cudaEventRecord(e0, c->stream));
+  TCG_CUDA_TRY(c, tcbdev::flow_transpose(static_cast<int>(n), static_cast<int>(nnz), row_ptr, c->cols,
+                                         reinterpret_cast<int*>(b + o_key), reinterpret_cast<int*>(b + o_pos),
+                                         reinterpret_cast<int*>(b + o_rid), reinterpret_cast<int*>(b + o_keys),
+                                         col_pos, col_ptr, col_src, b + o_tmp, &sort_bytes, c->sm_count, c->stream));
+  TCG_CUDA_TRY(c, tcbdev::flow_program_count(q, c->sm_count, c->stream));
+  TCG_CUDA_TRY(c, tcbdev::flow_program_scan(count, ub64, ub32, nnz, total_d, b + o_tmp, &scan_bytes,
+                                            c->sm_count, c->stream));
+  long long total = 0;
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(&total, total_d, sizeof(long long), cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  if (total > 0x7fffffffLL) {
+    c->err = "tcg_upload: more than 2^31 products in the update programs";
+    return TCG_INVALID;
+  }
+  TCG_CUDA_TRY(c, cudaMalloc(&c->prog_arena, sizeof(int2) * std::max<long long>(total, 1)));
+  c->flow_upd = static_cast<int2*>(c->prog_arena);
+  q.upd = c->flow_upd;
+  TCG_CUDA_TRY(c, tcbdev::flow_program_fill(q, c->sm_count, c->stream));
+  if (p->flow_part >= 0) {  // a part: operands of other parts' rows through the peer table
+    int* owner = reinterpret_cast<int*>(b + o_own);
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(owner, p->part_of_row, sizeof(int) * n, cudaMemcpyHostToDevice, c->stream));
+    TCG_CUDA_TRY(c, tcbdev::flow_program_remote_rewrite(nnz, reinterpret_cast<int*>(b + o_rid), owner, p->flow_part,
+                                                        c->flow_slot, c->flow_upd, c->sm_count, c->stream));
+  }
+  TCG_CUDA_TRY(c, cudaEventRecord(e1, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, e0, e1));
+  c->prog_build_ms = ms;
+  c->nflow_upd = total;
+  return TCG_OK;
+}
+
+extern "C" {
+
 tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   if (!c || !p) return TCG_INVALID;
   if (p->n < 0 || p->nnz < 0 || p->ntasks < 0 || p->nitems < 0 || p->nsources < 0 ||
       p->nedges < 0 || p->nroots < 0 || p->nhelpers < 0 || p->nnz > 0x7fffffffLL ||
-      p->ntasks + p->nhelpers >= 0x40000000LL) {
+      p->ntasks + p->nhelpers >= 0x40000000LL || p->nflow < 0 || p->nflow > 0x7fffffffLL ||
+      (p->flow_devprog && p->nnz < p->n)) {
     c->err = "tcg_upload: invalid problem sizes";
     return TCG_INVALID;
   }
+  // the task tables exist only with the task-DAG plan (tcg_plan_expand); the count stays
+  // for the statistics either way
+  const std::int64_t ntab = p->task_rec ? p->ntasks : 0;
   TCG_CUDA_TRY(c, cudaSetDevice(c->device));
   if (c->arena) {
     TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
@@ -468,10 +559,14 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     TCG_CUDA_TRY(c, cudaFree(c->batch_arena));
     c->batch_arena = nullptr;
   }
+  if (c->prog_arena) {
+    TCG_CUDA_TRY(c, cudaFree(c->prog_arena));
+    c->prog_arena = nullptr;
+  }
   c->nbatch = 1;
   // one arena: [cols][vals][vals0][tasks][items][srcs][succ][indeg][indeg0][queue][roots]
   //            [claim][fin][iflag][ctrl][trace]
-  const std::int64_t qcap = p->ntasks + p->nhelpers;
+  const std::int64_t qcap = ntab + (ntab ? p->nhelpers : 0);
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t at = off;
@@ -481,58 +576,38 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_cols = take(sizeof(int) * p->nnz);
   const size_t o_vals = take(sizeof(double) * p->nnz);
   const size_t o_vals0 = take(sizeof(double) * p->nnz);
-  const size_t o_tasks = take(sizeof(int) * 12 * p->ntasks);
+  const size_t o_tasks = take(sizeof(int) * 12 * ntab);
   const size_t o_items = take(sizeof(int) * 8 * p->nitems);
   const size_t o_srcs = take(sizeof(int) * 4 * p->nsources);
   const size_t o_succ = take(sizeof(int4) * 4 * p->nedges);
-  const size_t o_indeg = take(sizeof(int) * p->ntasks);
-  const size_t o_indeg0 = take(sizeof(int) * p->ntasks);
+  const size_t o_indeg = take(sizeof(int) * ntab);
+  const size_t o_indeg0 = take(sizeof(int) * ntab);
   const size_t o_queue = take(sizeof(int) * qcap);
   const size_t o_roots = take(sizeof(int) * p->nroots);
-  const size_t o_claim = take(sizeof(int) * p->ntasks);
-  const size_t o_fin = take(sizeof(int) * p->ntasks);
+  const size_t o_claim = take(sizeof(int) * ntab);
+  const size_t o_fin = take(sizeof(int) * ntab);
   const size_t o_iflag = take(sizeof(int) * p->nitems);
   const bool programs = p->nslots > 0 && p->slot_rec && (p->nupdates == 0 || p->upd);
   const size_t o_slot = take(programs ? sizeof(int4) * p->nslots : 0);
   const size_t o_upd = take(programs ? sizeof(int) * 2 * p->nupdates : 0);
-  const bool rows = programs && p->row_rec && p->row_indeg && (p->nrow_edges == 0 || p->row_succ) &&
-                    (p->nrow_roots == 0 || p->row_roots);
-  const size_t o_rows = take(rows ? sizeof(int4) * 2 * p->nitems : 0);
-  const size_t o_rsucc = take(rows ? sizeof(int) * p->nrow_edges : 0);
-  const size_t o_rindeg = take(rows ? sizeof(int) * p->nitems : 0);
-  const size_t o_rindeg0 = take(rows ? sizeof(int) * p->nitems : 0);
-  const size_t o_rqueue = take(rows ? sizeof(int) * p->nitems : 0);
-  const size_t o_rhiq = take(rows ? sizeof(int) * p->nitems : 0);
-  const size_t o_rroots = take(rows ? sizeof(int) * p->nrow_roots : 0);
-  const bool stat = rows && p->pos_rec && (p->npos_pred == 0 || p->pos_pred);
-  const size_t o_prec = take(stat ? sizeof(int4) * 4 * p->nitems : 0);
-  const size_t o_ppred = take(stat ? sizeof(int) * p->npos_pred : 0);
-  const size_t o_rflag = take(stat ? sizeof(int) * p->nitems : 0);
-  const bool flow = p->nflow > 0 && p->flow_rec && p->flow_item && p->flow_slot &&
-                    (p->nflow_upd == 0 || p->flow_upd);
+  const bool devprog = p->flow_devprog && p->u_row_ptr;
+  const bool flow = p->nflow > 0 && p->flow_rec && p->flow_item &&
+                    (devprog || (p->flow_slot && (p->nflow_upd == 0 || p->flow_upd)));
+  if (p->flow_part >= 0 && (!devprog || !p->part_of_row || p->nnz >= (1LL << tcb::kRemoteShift))) {
+    c->err = "tcg_upload: a part needs device-built programs, its owner table and U below 2^25 entries";
+    return TCG_INVALID;
+  }
   const size_t o_frec = take(flow ? sizeof(int4) * p->nflow : 0);
   const size_t o_fitem = take(flow ? sizeof(int) * p->nflow : 0);
   const size_t o_fslot = take(flow ? sizeof(int4) * p->nnz : 0);
-  const size_t o_fupd = take(flow ? sizeof(int2) * p->nflow_upd : 0);
+  const size_t o_fupd = take(flow && !devprog ? sizeof(int2) * p->nflow_upd : 0);
   const size_t o_fa = take(flow ? sizeof(double) * p->nnz : 0);
-  const bool units = flow && p->m6_nunits > 0 && (p->m6_nrows == 0 || (p->m6_row_rec && p->m6_row_item)) &&
-                     p->m6_unit_rec && p->m6_urow_rec && p->m6_urow_lbase && p->m6_urow_item && p->m6_ulev &&
-                     p->m6_slot && (p->nflow_upd == 0 || p->m6_upd);
-  const size_t o_m6rr = take(units ? sizeof(int4) * p->m6_nrows : 0);
-  const size_t o_m6ri = take(units ? sizeof(int) * p->m6_nrows : 0);
-  const size_t o_m6ur = take(units ? sizeof(int4) * p->m6_nunits : 0);
-  const size_t o_m6wr = take(units ? sizeof(int4) * p->m6_nurows : 0);
-  const size_t o_m6lb = take(units ? sizeof(int) * p->m6_nurows : 0);
-  const size_t o_m6wi = take(units ? sizeof(int) * p->m6_nurows : 0);
-  const size_t o_m6lv = take(units ? sizeof(int) * p->m6_nlev : 0);
-  const size_t o_m6sl = take(units ? sizeof(int4) * p->nnz : 0);
-  const size_t o_m6up = take(units ? sizeof(int2) * p->nflow_upd : 0);
   const bool amap = p->nnz_a > 0 && p->a_map;
   const size_t o_amap = take(amap ? sizeof(int) * p->nnz : 0);
   const size_t o_mflags = take(sizeof(int) * 2);
   const size_t o_mpivot = take(sizeof(double));
   const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
-  const size_t o_trace = take(sizeof(unsigned long long) * (2 * p->ntasks + 4 * p->nitems));
+  const size_t o_trace = take(sizeof(unsigned long long) * (2 * ntab + 4 * std::max(p->nitems, p->nflow)));
   TCG_CUDA_TRY(c, cudaMalloc(&c->arena, off));
   c->arena_bytes = off;
   char* base = static_cast<char*>(c->arena);
@@ -553,34 +628,8 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->slot_rec = reinterpret_cast<int4*>(base + o_slot);
   c->upd = reinterpret_cast<int2*>(base + o_upd);
   c->has_programs = programs;
-  c->rows = reinterpret_cast<int4*>(base + o_rows);
-  c->row_succ = reinterpret_cast<int*>(base + o_rsucc);
-  c->row_indeg = reinterpret_cast<int*>(base + o_rindeg);
-  c->row_indeg0 = reinterpret_cast<int*>(base + o_rindeg0);
-  c->row_queue = reinterpret_cast<int*>(base + o_rqueue);
-  c->row_hiq = reinterpret_cast<int*>(base + o_rhiq);
-  c->row_roots = reinterpret_cast<int*>(base + o_rroots);
-  c->nrow_roots = rows ? p->nrow_roots : 0;
-  c->has_rows = rows;
-  c->pos_rec = reinterpret_cast<int4*>(base + o_prec);
-  c->pos_pred = reinterpret_cast<int*>(base + o_ppred);
-  c->row_flag = reinterpret_cast<int*>(base + o_rflag);
-  c->has_static = stat;
   c->flow_rec = reinterpret_cast<int4*>(base + o_frec);
   c->flow_item = reinterpret_cast<int*>(base + o_fitem);
-  c->m6_row_rec = reinterpret_cast<int4*>(base + o_m6rr);
-  c->m6_row_item = reinterpret_cast<int*>(base + o_m6ri);
-  c->m6_unit_rec = reinterpret_cast<int4*>(base + o_m6ur);
-  c->m6_urow_rec = reinterpret_cast<int4*>(base + o_m6wr);
-  c->m6_urow_lbase = reinterpret_cast<int*>(base + o_m6lb);
-  c->m6_urow_item = reinterpret_cast<int*>(base + o_m6wi);
-  c->m6_ulev = reinterpret_cast<int*>(base + o_m6lv);
-  c->m6_slot = reinterpret_cast<int4*>(base + o_m6sl);
-  c->m6_upd = reinterpret_cast<int2*>(base + o_m6up);
-  c->m6_nrows = units ? p->m6_nrows : 0;
-  c->m6_nunits = units ? p->m6_nunits : 0;
-  c->m6_smem = units ? p->m6_smem : 0;
-  c->has_units = units;
   c->a_map = amap ? reinterpret_cast<int*>(base + o_amap) : nullptr;
   c->nnz_a = amap ? p->nnz_a : 0;
   c->m_flags = reinterpret_cast<int*>(base + o_mflags);
@@ -589,7 +638,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->flow_upd = reinterpret_cast<int2*>(base + o_fupd);
   c->flow_a = reinterpret_cast<double*>(base + o_fa);
   c->nflow = flow ? p->nflow : 0;
-  c->nflow_upd = flow ? p->nflow_upd : 0;
+  c->nflow_upd = flow && !devprog ? p->nflow_upd : 0;
   c->has_flow = flow;
 
   c->nslots = programs ? p->nslots : 0;
@@ -602,7 +651,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   };
   TCG_CUDA_TRY(c, put(c->cols, p->col_idx, sizeof(int) * p->nnz));
   TCG_CUDA_TRY(c, put(c->vals0, p->values, sizeof(double) * p->nnz));
-  TCG_CUDA_TRY(c, put(c->tasks, p->task_rec, sizeof(int) * 12 * p->ntasks));
+  TCG_CUDA_TRY(c, put(c->tasks, p->task_rec, sizeof(int) * 12 * ntab));
   TCG_CUDA_TRY(c, put(c->items, p->item_rec, sizeof(int) * 8 * p->nitems));
   TCG_CUDA_TRY(c, put(c->srcs, p->src_rec, sizeof(int) * 4 * p->nsources));
   if (p->nedges > 0 && !p->succ_rec) {
@@ -610,43 +659,27 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     return TCG_INVALID;
   }
   TCG_CUDA_TRY(c, put(c->succ, p->succ_rec, sizeof(int4) * 4 * p->nedges));
-  TCG_CUDA_TRY(c, put(c->indeg0, p->indeg, sizeof(int) * p->ntasks));
+  TCG_CUDA_TRY(c, put(c->indeg0, p->indeg, sizeof(int) * ntab));
   TCG_CUDA_TRY(c, put(c->roots, p->roots, sizeof(int) * p->nroots));
   if (programs) {
     TCG_CUDA_TRY(c, put(c->slot_rec, p->slot_rec, sizeof(int4) * p->nslots));
     TCG_CUDA_TRY(c, put(c->upd, p->upd, sizeof(int) * 2 * p->nupdates));
   }
-  if (rows) {
-    TCG_CUDA_TRY(c, put(c->rows, p->row_rec, sizeof(int4) * 2 * p->nitems));
-    TCG_CUDA_TRY(c, put(c->row_succ, p->row_succ, sizeof(int) * p->nrow_edges));
-    TCG_CUDA_TRY(c, put(c->row_indeg0, p->row_indeg, sizeof(int) * p->nitems));
-    TCG_CUDA_TRY(c, put(c->row_roots, p->row_roots, sizeof(int) * p->nrow_roots));
-  }
-  if (stat) {
-    TCG_CUDA_TRY(c, put(c->pos_rec, p->pos_rec, sizeof(int4) * 4 * p->nitems));
-    TCG_CUDA_TRY(c, put(c->pos_pred, p->pos_pred, sizeof(int) * p->npos_pred));
-    TCG_CUDA_TRY(c, cudaMemsetAsync(c->row_flag, 0, sizeof(int) * p->nitems, c->stream));
-  }
   if (flow) {
     TCG_CUDA_TRY(c, put(c->flow_rec, p->flow_rec, sizeof(int4) * p->nflow));
     TCG_CUDA_TRY(c, put(c->flow_item, p->flow_item, sizeof(int) * p->nflow));
-    TCG_CUDA_TRY(c, put(c->flow_slot, p->flow_slot, sizeof(int4) * p->nnz));
-    TCG_CUDA_TRY(c, put(c->flow_upd, p->flow_upd, sizeof(int2) * p->nflow_upd));
-  }
-  if (units) {
-    TCG_CUDA_TRY(c, put(c->m6_row_rec, p->m6_row_rec, sizeof(int4) * p->m6_nrows));
-    TCG_CUDA_TRY(c, put(c->m6_row_item, p->m6_row_item, sizeof(int) * p->m6_nrows));
-    TCG_CUDA_TRY(c, put(c->m6_unit_rec, p->m6_unit_rec, sizeof(int4) * p->m6_nunits));
-    TCG_CUDA_TRY(c, put(c->m6_urow_rec, p->m6_urow_rec, sizeof(int4) * p->m6_nurows));
-    TCG_CUDA_TRY(c, put(c->m6_urow_lbase, p->m6_urow_lbase, sizeof(int) * p->m6_nurows));
-    TCG_CUDA_TRY(c, put(c->m6_urow_item, p->m6_urow_item, sizeof(int) * p->m6_nurows));
-    TCG_CUDA_TRY(c, put(c->m6_ulev, p->m6_ulev, sizeof(int) * p->m6_nlev));
-    TCG_CUDA_TRY(c, put(c->m6_slot, p->m6_slot, sizeof(int4) * p->nnz));
-    TCG_CUDA_TRY(c, put(c->m6_upd, p->m6_upd, sizeof(int2) * p->nflow_upd));
+    if (!devprog) {
+      TCG_CUDA_TRY(c, put(c->flow_slot, p->flow_slot, sizeof(int4) * p->nnz));
+      TCG_CUDA_TRY(c, put(c->flow_upd, p->flow_upd, sizeof(int2) * p->nflow_upd));
+    }
   }
   if (amap) TCG_CUDA_TRY(c, put(c->a_map, p->a_map, sizeof(int) * p->nnz));
   if (p->nitems > 0)
     TCG_CUDA_TRY(c, cudaMemsetAsync(c->iflag, 0, sizeof(int) * p->nitems, c->stream));
+  if (flow && devprog) {
+    const tcg_status st = build_programs(c, p);
+    if (st != TCG_OK) return st;
+  }
   if (p->nnz > 0)
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->vals, c->vals0, sizeof(double) * p->nnz,
                                     cudaMemcpyDeviceToDevice, c->stream));
@@ -654,6 +687,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->n = p->n;
   c->nnz = p->nnz;
   c->ntasks = p->ntasks;
+  c->ntab = ntab;
   c->nitems = p->nitems;
   c->nsrc = p->nsources;
   c->nedges = p->nedges;
@@ -820,7 +854,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (from_copy) q.a = const_cast<double*>(q.vals);  // tells the prelude not to copy
   P.vals = vals;
   P.ctrl = c->ctrl;
-  P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
+  P.trace = c->opt.trace ? c->trace + 2 * c->ntab : nullptr;
   P.m_failed = q.m_failed;
   P.m_row = q.m_row;
   P.m_pivot = q.m_pivot;
@@ -921,249 +955,6 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   return TCG_OK;
 }
 
-// Block units (mode 6, flow_kernel.cu factor_units): prelude + one launch.
-static tcg_status run_units(tcg_ctx* c, tcg_stats& S, int threads) {
-  int kb = 4, minb = threads == 128 ? 6 : threads == 256 ? 3 : 1;
-  if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
-  int weak = 0;
-  if (const char* e = std::getenv("TCG_FLOW_WEAK")) weak = std::atoi(e);
-  const size_t smem = static_cast<size_t>(std::max<std::int64_t>(c->m6_smem, 16));
-  int occ = 0;
-  TCG_CUDA_TRY(c, tcbdev::unit_occupancy(threads, kb, minb, weak, smem, &occ));
-  if (occ < 1) {
-    c->err = "block-unit kernel does not fit on an SM";
-    return TCG_INVALID;
-  }
-  if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
-  const int grid = std::max(2, occ * c->sm_count);
-  int nu = static_cast<int>(std::min<std::int64_t>(c->m6_nunits, c->sm_count));
-  if (const char* e = std::getenv("TCG_UNIT_CTAS")) nu = std::max(1, std::atoi(e));
-  nu = std::min(nu, grid - 1);
-  tcbdev::FlowPrepParams q{};
-  q.vals = c->vals;
-  q.a = c->flow_a;
-  q.out = c->vals;
-  q.nnz = c->nnz;
-  q.ctrl = c->ctrl;
-  q.m_failed = c->m_flags;
-  q.m_row = c->m_flags + 1;
-  q.m_pivot = c->m_pivot;
-  q.nbatch = 1;
-  tcbdev::FlowParams P{};
-  P.rec = c->m6_row_rec;
-  P.item = c->m6_row_item;
-  P.slot = c->m6_slot;
-  P.upd = c->m6_upd;
-  P.a = c->flow_a;
-  P.vals = c->vals;
-  P.ctrl = c->ctrl;
-  P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
-  P.m_failed = q.m_failed;
-  P.m_row = q.m_row;
-  P.m_pivot = q.m_pivot;
-  P.nnz = c->nnz;
-  P.nbatch = 1;
-  P.nrows = static_cast<int>(c->m6_nrows);
-  const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
-  P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
-  tcbdev::UnitParams U{};
-  U.unit_rec = c->m6_unit_rec;
-  U.urow_rec = c->m6_urow_rec;
-  U.urow_lbase = c->m6_urow_lbase;
-  U.urow_item = c->m6_urow_item;
-  U.ulev = c->m6_ulev;
-  U.nunits = static_cast<int>(c->m6_nunits);
-  U.nu_ctas = nu;
-  TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
-  TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
-  TCG_CUDA_TRY(c, tcbdev::launch_units(P, U, grid, threads, kb, minb, weak, smem, c->stream));
-  TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
-  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
-                                  cudaMemcpyDeviceToHost, c->stream));
-  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  float ms = 0.f;
-  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-  const tcbdev::Ctrl& h = *c->host_ctrl;
-  S.device_ms = ms;
-  S.grid_ctas = grid;
-  S.threads_per_cta = threads;
-  S.staging_cap = kb;
-  S.smem_bytes = static_cast<int64_t>(smem);
-  S.kernel_launches = 2;
-  S.mode = 6;
-  S.helpers_run = nu;  // reported: CTAs running units
-  S.lanes_per_row = 32;
-  S.tasks_completed = (h.done.v == c->nflow) ? c->ntasks : 0;
-  S.tasks_executed = h.executed.v;
-  if (h.error.v) {
-    c->err = "device watchdog expired: the block-unit schedule stalled";
-    return TCG_TIMEOUT;
-  }
-  if (h.done.v != c->nflow) {
-    c->err = "block-unit schedule finished " + std::to_string(h.done.v) + " of " +
-             std::to_string(c->nflow) + " rows";
-    return TCG_TIMEOUT;
-  }
-  if (h.failed.v) {
-    S.breakdown_row = h.fail_row;
-    S.breakdown_pivot = h.fail_pivot;
-    S.breakdown_member = 0;
-    c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
-             std::to_string(h.fail_pivot) + " is not positive";
-    return TCG_BREAKDOWN;
-  }
-  return TCG_OK;
-}
-
-// Row-level execution on a static level schedule (mode 4, static_kernel.cu).
-static tcg_status run_static(tcg_ctx* c, tcg_stats& S, int threads) {
-  // gather batch: 8 products in flight per slot when slots carry several
-  // products on average, else 4 (fewer registers)
-  const int group = c->nslots > 0 && c->nupdates > 3 * c->nslots ? 8 : 4;
-  int occ = 0;
-  TCG_CUDA_TRY(c, tcbdev::static_occupancy(threads, group, &occ));
-  if (occ < 1) {
-    c->err = "static row kernel does not fit on an SM";
-    return TCG_INVALID;
-  }
-  if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
-  const int grid = std::max(1, occ * c->sm_count);
-  // counters only (no queues): reuse the prepare kernel with an empty task set
-  tcbdev::PrepParams q{};
-  q.ctrl = c->ctrl;
-  q.qcap = 0;
-  q.ntasks = 0;
-  q.nroots = 0;
-  TCG_CUDA_TRY(c, tcbdev::launch_prepare(q, c->stream));
-  tcbdev::StaticParams P{};
-  P.pos = c->pos_rec;
-  P.pos_pred = c->pos_pred;
-  P.slot_rec = c->slot_rec;
-  P.upd = c->upd;
-  P.vals = c->vals;
-  P.flag = c->row_flag;
-  P.ctrl = c->ctrl;
-  P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
-  P.nitems = static_cast<int>(c->nitems);
-  P.epoch = ++c->epoch;
-  const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
-  P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
-  TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
-  if (c->nitems > 0) TCG_CUDA_TRY(c, tcbdev::launch_static(P, grid, threads, group, c->stream));
-  S.staging_cap = group;  // reported: gather batch
-  TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
-  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
-                                  cudaMemcpyDeviceToHost, c->stream));
-  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  float ms = 0.f;
-  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-  const tcbdev::Ctrl& h = *c->host_ctrl;
-  S.device_ms = ms;
-  S.grid_ctas = grid;
-  S.threads_per_cta = threads;
-  S.kernel_launches = c->nitems > 0 ? 2 : 1;
-  S.mode = 4;
-  S.tasks_completed = (h.done.v == c->nitems) ? c->ntasks : 0;
-  S.tasks_executed = h.executed.v;
-  if (h.error.v) {
-    c->err = "device watchdog expired: the static row schedule stalled";
-    return TCG_TIMEOUT;
-  }
-  if (h.done.v != c->nitems) {
-    c->err = "static schedule finished " + std::to_string(h.done.v) + " of " +
-             std::to_string(c->nitems) + " rows";
-    return TCG_TIMEOUT;
-  }
-  if (h.failed.v) {
-    S.breakdown_row = h.fail_row;
-    S.breakdown_pivot = h.fail_pivot;
-    c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
-             std::to_string(h.fail_pivot) + " is not positive";
-    return TCG_BREAKDOWN;
-  }
-  return TCG_OK;
-}
-
-// Row-level execution (mode 3): one warp-granular persistent launch over the
-// items of the same DAG (row_kernel.cu).
-static tcg_status run_rows(tcg_ctx* c, tcg_stats& S, int threads) {
-  int minb = 0;  // register budget variant (row_kernel.cu TCG_ROW_VARIANTS)
-  if (const char* e = std::getenv("TCG_ROW_MINB")) minb = std::atoi(e);
-  else if (threads == 256) minb = 4;
-  int occ = 0;
-  TCG_CUDA_TRY(c, tcbdev::rows_occupancy(threads, minb, c->opt.trace != 0, &occ));
-  if (occ < 1) {
-    c->err = "row kernel does not fit on an SM";
-    return TCG_INVALID;
-  }
-  if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
-  const int grid = std::max(1, occ * c->sm_count);
-
-  tcbdev::PrepParams q{};
-  q.indeg0 = c->row_indeg0;
-  q.roots = c->row_roots;
-  q.indeg = c->row_indeg;
-  q.queue = c->row_queue;
-  q.claim = nullptr;
-  q.queue2 = c->row_hiq;
-  q.fin = nullptr;
-  q.ctrl = c->ctrl;
-  q.qcap = static_cast<int>(c->nitems);
-  q.ntasks = static_cast<int>(c->nitems);
-  q.nroots = static_cast<int>(c->nrow_roots);
-  TCG_CUDA_TRY(c, tcbdev::launch_prepare(q, c->stream));
-
-  tcbdev::RowParams P{};
-  P.rows = c->rows;
-  P.succ = c->row_succ;
-  P.slot_rec = c->slot_rec;
-  P.upd = c->upd;
-  P.vals = c->vals;
-  P.indeg = c->row_indeg;
-  P.queue = c->row_queue;
-  P.hiq = c->row_hiq;
-  P.ctrl = c->ctrl;
-  P.trace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;  // the item-stamp region
-  P.nitems = static_cast<int>(c->nitems);
-  const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
-  P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
-  TCG_CUDA_TRY(c, cudaEventRecord(c->ev0, c->stream));
-  if (c->nitems > 0) TCG_CUDA_TRY(c, tcbdev::launch_rows(P, grid, threads, minb, c->stream));
-  TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
-  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
-                                  cudaMemcpyDeviceToHost, c->stream));
-  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-  float ms = 0.f;
-  TCG_CUDA_TRY(c, cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-  const tcbdev::Ctrl& h = *c->host_ctrl;
-  S.device_ms = ms;
-  S.grid_ctas = grid;
-  S.threads_per_cta = threads;
-  S.kernel_launches = c->nitems > 0 ? 2 : 1;
-  S.mode = 3;
-  for (int i = 0; i < 7; ++i) S.profile[i] = h.prof[i];
-  // every task's rows ran (a task with no rows has no numeric work)
-  S.tasks_completed = (h.done.v == c->nitems) ? c->ntasks : 0;
-  S.tasks_executed = h.executed.v;  // rows whose body ran
-  if (h.error.v) {
-    c->err = "device watchdog expired: the row dataflow stalled";
-    return TCG_TIMEOUT;
-  }
-  if (h.done.v != c->nitems) {
-    c->err = "row scheduler finished with " + std::to_string(h.done.v) + " of " +
-             std::to_string(c->nitems) + " rows";
-    return TCG_TIMEOUT;
-  }
-  if (h.failed.v) {
-    S.breakdown_row = h.fail_row;
-    S.breakdown_pivot = h.fail_pivot;
-    c->err = "factorization breakdown at row " + std::to_string(h.fail_row) + ": pivot " +
-             std::to_string(h.fail_pivot) + " is not positive";
-    return TCG_BREAKDOWN;
-  }
-  return TCG_OK;
-}
-
 tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   if (!c || !c->uploaded) return TCG_INVALID;
   tcg_stats local{};
@@ -1177,13 +968,12 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
 
   const int threads = c->opt.threads_per_cta ? c->opt.threads_per_cta : 256;
   int mode = c->opt.mode;
-  if (mode == 0 && c->nbatch > 1 && c->has_flow) mode = 5;
-  if (mode == 0)  // value flow wherever the plan has its tables (fastest on C1-C6)
-    mode = c->has_flow ? 5 : c->has_static ? 4 : c->has_rows ? 3 : (c->has_programs ? 2 : 1);
-  if ((mode == 2 && !c->has_programs) || (mode == 3 && !c->has_rows) ||
-      (mode == 4 && !c->has_static) || (mode == 5 && !c->has_flow) || (mode == 6 && !c->has_units) ||
-      mode < 0 || mode > 6) {
-    c->err = "requested execution mode is not available for the uploaded problem";
+  if (mode == 0)  // value flow wherever the problem has its tables (the default); else the task DAG
+    mode = c->has_flow ? 5 : (c->has_programs ? 2 : 1);
+  if (((mode == 1 || mode == 2) && c->ntab == 0) || (mode == 2 && !c->has_programs) ||
+      (mode == 5 && !c->has_flow) || (mode != 1 && mode != 2 && mode != 5)) {
+    c->err = "requested execution mode is not available for the uploaded problem (1, 2: task DAG, "
+             "needs tcg_plan_expand; 5: value flow)";
     return TCG_INVALID;
   }
   if (mode != 5 && c->nbatch > 1) {
@@ -1194,11 +984,8 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
     c->err = "threads_per_cta 384 and 768 are for mode 5 only";
     return TCG_INVALID;
   }
-  if (mode != 5) c->pristine = false;  // every other executor factors the working values in place
-  if (mode == 3) return run_rows(c, S, threads);
-  if (mode == 4) return run_static(c, S, threads);
+  if (mode != 5) c->pristine = false;  // the task executors factor the working values in place
   if (mode == 5) return run_flow(c, S, threads);
-  if (mode == 6) return run_units(c, S, threads);
   int flag_words = (c->max_flag_rows + 31) / 32;
   flag_words = (flag_words + 3) & ~3;
   int cap = c->opt.staging_cap;
@@ -1243,7 +1030,7 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   q.fin = c->fin;
   q.ctrl = c->ctrl;
   q.qcap = static_cast<int>(c->qcap);
-  q.ntasks = static_cast<int>(c->ntasks);
+  q.ntasks = static_cast<int>(c->ntab);
   q.nroots = static_cast<int>(c->nroots);
   TCG_CUDA_TRY(c, tcbdev::launch_prepare(q, c->stream));
 
@@ -1263,8 +1050,8 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
   P.qcap = static_cast<int>(c->qcap);
   P.epoch = ++c->epoch;
   P.trace = c->opt.trace ? c->trace : nullptr;
-  P.itrace = c->opt.trace ? c->trace + 2 * c->ntasks : nullptr;
-  P.ntasks = static_cast<int>(c->ntasks);
+  P.itrace = c->opt.trace ? c->trace + 2 * c->ntab : nullptr;
+  P.ntasks = static_cast<int>(c->ntab);
   P.cap = cap;
   P.flag_words = flag_words;
   P.icap = icap;
@@ -1297,9 +1084,9 @@ tcg_status tcg_factor(tcg_ctx* c, tcg_stats* st) {
     c->err = h.error.v == 1 ? "device watchdog expired: the task DAG stalled" : "device capacity error";
     return TCG_TIMEOUT;
   }
-  if (h.done.v != c->ntasks) {
+  if (h.done.v != c->ntab) {
     c->err = "scheduler finished with " + std::to_string(h.done.v) + " of " +
-             std::to_string(c->ntasks) + " tasks";
+             std::to_string(c->ntab) + " tasks";
     return TCG_TIMEOUT;
   }
   if (h.failed.v) {
@@ -1545,6 +1332,10 @@ tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {
     TCG_CUDA_TRY(c, cudaFree(c->batch_arena));
     c->batch_arena = nullptr;
   }
+  if (c->prog_arena) {
+    TCG_CUDA_TRY(c, cudaFree(c->prog_arena));
+    c->prog_arena = nullptr;
+  }
   c->nbatch = 1;
   c->drain_ms[0] = c->drain_ms[1] = -1.f;
   c->drain_calls = 0;
@@ -1669,8 +1460,22 @@ tcg_status tcg_download_trace(tcg_ctx* c, uint64_t* stamps) {
   if (!c || !c->uploaded || !stamps) return TCG_INVALID;
   if (c->ntasks == 0) return TCG_OK;
   TCG_CUDA_TRY(c, cudaSetDevice(c->device));
-  TCG_CUDA_TRY(c, cudaMemcpyAsync(stamps, c->trace, sizeof(uint64_t) * (2 * c->ntasks + 4 * c->nitems),
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(stamps, c->trace, sizeof(uint64_t) * (2 * c->ntab + 4 * std::max(c->nitems, c->nflow)),
                                   cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_flow_programs(tcg_ctx* c, int32_t* slot, int32_t* upd, int64_t* nupd, double* build_ms) {
+  if (!c || !c->uploaded || !c->has_flow) return TCG_INVALID;
+  if (nupd) *nupd = c->nflow_upd;
+  if (build_ms) *build_ms = c->prog_build_ms;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  if (slot && c->nnz > 0)
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(slot, c->flow_slot, sizeof(int4) * c->nnz, cudaMemcpyDeviceToHost, c->stream));
+  if (upd && c->nflow_upd > 0)
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(upd, c->flow_upd, sizeof(int2) * c->nflow_upd, cudaMemcpyDeviceToHost,
+                                    c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   return TCG_OK;
 }

@@ -1,4 +1,4 @@
-// Host-callable launch helpers of factor_kernel.cu and row_kernel.cu.
+// Host-callable launch helpers of factor_kernel.cu, flow_kernel.cu and flow_program.cu.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -14,11 +14,7 @@ cudaError_t factor_occupancy(int threads, size_t smem, int* ctas_per_sm);
 cudaError_t launch_prepare(const PrepParams& q, cudaStream_t st);
 cudaError_t launch_factor(const Params& p, int grid, int threads, size_t smem, cudaStream_t st);
 
-cudaError_t rows_occupancy(int threads, int minb, bool prof, int* ctas_per_sm);
-cudaError_t launch_rows(const RowParams& p, int grid, int threads, int minb, cudaStream_t st);
 
-cudaError_t static_occupancy(int threads, int group, int* ctas_per_sm);
-cudaError_t launch_static(const StaticParams& p, int grid, int threads, int group, cudaStream_t st);
 
 cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int dyn, int remote,
                            int* ctas_per_sm);
@@ -32,8 +28,15 @@ cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb,
                              int extras, cudaStream_t st, int drain = 0);
 cudaError_t launch_init_values(const double* a, const int* map, double* vals, double* vals0, long long nnz,
                                long long nnz_a, int nbatch, int sm_count, cudaStream_t st);
-cudaError_t unit_occupancy(int threads, int kb, int minb, int weak, size_t smem, int* ctas_per_sm);
-cudaError_t launch_units(const FlowParams& p, const UnitParams& u, int grid, int threads, int kb, int minb,
-                         int weak, size_t smem, cudaStream_t st);
+
+cudaError_t flow_transpose(int n, int nnz, const int* row_ptr, const int* cols, int* key, int* pos, int* rowid,
+                           int* key_s, int* pos_s, int* col_ptr, int* col_src, void* temp, size_t* temp_bytes,
+                           int sm_count, cudaStream_t st);
+cudaError_t flow_program_remote_rewrite(long long nnz, const int* rowid, const int* owner, int part, int4* slot,
+                                        int2* upd, int sm_count, cudaStream_t st);
+cudaError_t flow_program_count(const ProgParams& p, int sm_count, cudaStream_t st);
+cudaError_t flow_program_fill(const ProgParams& p, int sm_count, cudaStream_t st);
+cudaError_t flow_program_scan(const int* count, long long* ub64, int* ub32, long long nnz, long long* total,
+                              void* temp, size_t* temp_bytes, int sm_count, cudaStream_t st);
 
 }  // namespace tcbdev

@@ -68,37 +68,6 @@ struct Params {
   unsigned long long timeout_ns;
 };
 
-// Row-level mode (row_kernel.cu).
-struct RowParams {
-  const int4* rows;      // 2 x int4 per item: {tb, te, dpos, slot_off}, {kind, t, succ_b, succ_e}
-  const int* succ;       // successor items
-  const int4* slot_rec;  // update programs
-  const int2* upd;
-  double* vals;
-  int* indeg;
-  int* queue;            // FIFO of ready rows (ticket pop)
-  int* hiq;              // priority rows (rows flagged hot by the host), CAS pop
-  Ctrl* ctrl;            // q_head/q_tail/done/executed count rows in this mode
-  unsigned long long* trace;  // optional: {start, end} per item
-  int nitems;
-  unsigned long long timeout_ns;
-};
-
-// Static row schedule (mode 4, static_kernel.cu).
-struct StaticParams {
-  const int4* pos;       // 4 x int4 per schedule position (plan.hpp kPosWords); positions are
-                         // rows by (level, falling height): a topological order
-  const int* pos_pred;   // predecessor items beyond the 4 inline ones
-  const int4* slot_rec;
-  const int2* upd;
-  double* vals;
-  int* flag;             // per item: epoch stamp once its row is final
-  Ctrl* ctrl;
-  unsigned long long* trace;  // optional: {start, end} per item
-  int nitems;
-  int epoch;
-  unsigned long long timeout_ns;
-};
 
 // Value-flow schedule (mode 5, flow_kernel.cu): the finalising rows only,
 // readers polling the values they gather until they are no longer kUnset.
@@ -130,17 +99,22 @@ struct FlowParams {
   int row_ctas;          // CTAs that run rows
 };
 
-// Block units (mode 6, flow_kernel.cu factor_units); rows outside units use
-// FlowParams (rec/item/nrows = that list, slot/upd = the rewritten programs).
-struct UnitParams {
-  const int4* unit_rec;    // per unit: {level slot begin, end, first row, order}
-  const int4* urow_rec;    // per unit row: {tb, L | kind << 30, dpos, t}
-  const int* urow_lbase;   // per unit row: first shared-memory index of its values
-  const int* urow_item;
-  const int* ulev;         // per level slot: end of its rows
-  int nunits;
-  int nu_ctas;             // CTAs [0, nu_ctas) run units
+// Device-built update programs (flow_program.cu): U's pattern and its
+// transposed index in, the value-flow slot records and (m, o) pairs out.
+struct ProgParams {
+  int n;
+  const int* row_ptr;   // n + 1 positions
+  const int* cols;      // U column indices
+  const int* col_ptr;   // n + 1: sources of row t
+  const int* col_src;   //   source row r, ascending
+  const int* col_pos;   //   position of U(r, t)
+  int* count;           // pass 1 out: products per coordinate
+  const int* ub;        // pass 2 in: first product of each coordinate
+  int4* slot;           // pass 2 out: {u_b, u_e, m0, o0} per coordinate
+  int2* upd;            // pass 2 out: (m, o) pairs
+  int* next_row;        // two work counters (zeroed before pass 1)
 };
+
 
 struct FlowPrepParams {
   const double* vals;    // working values (input of the factorization)

@@ -73,10 +73,7 @@ __device__ __forceinline__ unsigned long long wait_value_sys(const double* p, Ct
 // and a stale L1 copy can only show kUnset, which the strong path re-reads.
 // `vals`/`a`/`member`: the current row's member of a batch (its value sets
 // are nnz apart; the pattern, records and programs are shared).
-// LOCAL (mode 6 units): a negative operand position is kLocalBit | index
-// into the unit's values in shared memory `sv`, final by construction.
-// OPS: how a negative operand position is read. 0: never happens; 1 (mode
-// 6): kLocalBit | index into the unit's shared-memory values `sv`; 2
+// OPS: how a negative operand position is read. 0: never happens; 2
 // (sharded runs): kRemoteBit | part << 25 | position in that part's U.
 template <int WEAK, int OPS = 0>
 struct Ctx {
@@ -85,7 +82,6 @@ struct Ctx {
   double* vals;
   const double* a;
   int member;
-  const double* sv = nullptr;
   __device__ __forceinline__ double settle(const double* p, unsigned long long x) const {
     if (x == kUnset) x = wait_value(p, P.ctrl, t0, P.timeout_ns);
     return __longlong_as_double(static_cast<long long>(x));
@@ -95,14 +91,12 @@ struct Ctx {
     return P.peers[(pos >> 25) & 63] + (pos & 0x1FFFFFF);
   }
   __device__ __forceinline__ unsigned long long ld(int pos) const {
-    if (OPS == 1 && pos < 0) return static_cast<unsigned long long>(__double_as_longlong(sv[pos & 0x7fffffff]));
     if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
     if (WEAK) return ld_weak_u64(vals + pos);
     return ld_relaxed_u64(vals + pos);
   }
   // re-polls are always strong: a weak (L1) copy of the marker may be stale
   __device__ __forceinline__ unsigned long long ld_strong(int pos) const {
-    if (OPS == 1 && pos < 0) return static_cast<unsigned long long>(__double_as_longlong(sv[pos & 0x7fffffff]));
     if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
     return ld_relaxed_u64(vals + pos);
   }
@@ -194,8 +188,7 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 template <int KIND, int KB, int G, class Cx>
 __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, int t, int gl,
                                          unsigned gmask, int lead, double a0, int4 sr0,
-                                         unsigned long long* stamp, double* local_out = nullptr,
-                                         bool exported = false) {
+                                         unsigned long long* stamp, bool exported = false) {
   const FlowParams& P = C.P;
   unsigned long long xd = 0;
   if (KIND == kTrsm) xd = C.ld(dpos);
@@ -223,10 +216,13 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
     __syncwarp(gmask);
     if (gl == 0) *stamp = gtimer();
   }
+  // a result that happens to carry the marker's bits (a NaN payload the
+  // arithmetic passed through) is published as the canonical NaN, so no
+  // reader mistakes a final value for "not written yet"
   auto finish = [&](int k, double x) {
     const double y = (KIND == kChol && k == 0) ? d : __ddiv_rn(x, d);
-    if (local_out) local_out[k] = y;  // mode 6: the unit's copy for its later rows
-    return static_cast<unsigned long long>(__double_as_longlong(y));
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(y));
+    return b == kUnset ? kCanonicalNaN : b;
   };
   // sharded runs publish at system scope: readers may sit on other GPUs
   auto publish = [&](int k, unsigned long long y) {
@@ -341,10 +337,10 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
     if (!latched) {
       if (chol)
         flow_row<kChol, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr,
-                               nullptr, exported);
+                               exported);
       else
         flow_row<kTrsm, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr,
-                               nullptr, exported);
+                               exported);
       ++executed;
     } else {
       // skipped rows keep their input values (readers must not wait forever)
@@ -548,10 +544,10 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
     if (!latched) {
       if (chol)
         flow_row<kChol, KB, 32>(C, tb, L, dpos, t, lane, kFull, 0, a0, sr0, stamp ? stamp + 1 : nullptr,
-                                nullptr, exported);
+                                exported);
       else
         flow_row<kTrsm, KB, 32>(C, tb, L, dpos, t, lane, kFull, 0, a0, sr0, stamp ? stamp + 1 : nullptr,
-                                nullptr, exported);
+                                exported);
       ++executed;
     } else {
       for (int k2 = lane; k2 < L; k2 += 32) {
@@ -565,118 +561,6 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
     ++ran;
   }
   cp_async_wait_all();
-  if (lane == 0) {
-    if (ran) atomicAdd(&P.ctrl->done.v, ran);
-    if (executed) atomicAdd(&P.ctrl->executed.v, executed);
-  }
-}
-
-// Block units (mode 6; plan.cpp build_units). CTAs [0, nu_ctas) run the
-// units: a unit's rows level by level (warps take the rows of a level
-// round-robin, one __syncthreads between levels), the unit's own values in
-// dynamic shared memory as well as in U. The other CTAs' warps run the rows
-// outside units exactly as mode 5 (static order, round-robin). Both lists are
-// in one topological order of units and rows, so the launch cannot deadlock
-// while every CTA is resident.
-template <int THREADS, int KB, int MINB, int WEAK>
-__global__ void __launch_bounds__(THREADS, MINB) factor_units(FlowParams P, UnitParams U) {
-  constexpr int kWarps = THREADS / 32;
-  constexpr int kLenMask = (1 << 30) - 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int ran = 0, executed = 0, anyfail = 0;
-  auto skip_row = [&](const double* a, double* vals, int tb, int L, double* local_out) {
-    for (int k = lane; k < L; k += 32) {
-      unsigned long long x = static_cast<unsigned long long>(__double_as_longlong(a[tb + k]));
-      if (x == kUnset) x = kCanonicalNaN;
-      st_relaxed_u64(vals + tb + k, x);
-      if (local_out) local_out[k] = __longlong_as_double(static_cast<long long>(x));
-    }
-  };
-  auto latched = [&]() {
-    if ((ran & 15) == 0) anyfail = __shfl_sync(kFull, lane == 0 ? ld_relaxed(&P.ctrl->failed.v) : 0, 0);
-    return anyfail != 0;
-  };
-  if (static_cast<int>(blockIdx.x) < U.nu_ctas) {
-    extern __shared__ double sv[];
-    Ctx<WEAK, 1> C{P, gtimer(), P.vals, P.a, 0, sv};
-    for (int u = blockIdx.x; u < U.nunits; u += U.nu_ctas) {
-      const int4 ur = __ldg(U.unit_rec + u);  // {level slot begin, end, first row, order}
-      int start = ur.z;
-      for (int sl = ur.x; sl < ur.y; ++sl) {
-        const int end = __ldg(U.ulev + sl);
-        for (int q = start + warp; q < end; q += kWarps) {
-          const int4 a = __ldg(U.urow_rec + q);
-          const int lb = __ldg(U.urow_lbase + q);
-          const int tb = a.x, L = a.y & kLenMask, t = a.w;
-          unsigned long long* stamp = P.trace ? P.trace + 4 * static_cast<long long>(__ldg(U.urow_item + q)) : nullptr;
-          if (stamp && lane == 0) stamp[0] = gtimer();
-          if (!latched()) {
-            int4 sr0 = make_int4(0, 0, 0, 0);
-            double a0 = 0.0;
-            if (lane < L) {
-              sr0 = __ldg(P.slot + tb + lane);
-              a0 = __ldg(P.a + tb + lane);
-            }
-            flow_row<kChol, KB, 32>(C, tb, L, a.z, t, lane, kFull, 0, a0, sr0, stamp ? stamp + 1 : nullptr,
-                                    sv + lb);
-            ++executed;
-          } else {
-            skip_row(P.a, P.vals, tb, L, sv + lb);
-          }
-          if (stamp && lane == 0) stamp[3] = gtimer();
-          ++ran;
-        }
-        __syncthreads();  // this level's values are in shared memory for the next
-        start = end;
-      }
-    }
-  } else {
-    Ctx<WEAK, 0> C{P, gtimer(), P.vals, P.a, 0};
-    const int W = (static_cast<int>(gridDim.x) - U.nu_ctas) * kWarps;
-    int pos = (static_cast<int>(blockIdx.x) - U.nu_ctas) * kWarps + warp;
-    // two-deep pipeline as in factor_flow
-    const int4 z = make_int4(0, 0, 0, 0);
-    int4 a = z, na = z, sr0 = z;
-    double a0 = 0.0;
-    if (pos < P.nrows) {
-      a = __ldg(P.rec + pos);
-      if (lane < (a.y & kLenMask)) {
-        sr0 = __ldg(P.slot + a.x + lane);
-        a0 = __ldg(P.a + a.x + lane);
-      }
-    }
-    if (pos + W < P.nrows) na = __ldg(P.rec + pos + W);
-    while (pos < P.nrows) {
-      const int npos = pos + W, nnpos = pos + 2 * W;
-      const int4 nna = nnpos < P.nrows ? __ldg(P.rec + nnpos) : z;
-      int4 nsr0 = z;
-      double na0 = 0.0;
-      if (npos < P.nrows && lane < (na.y & kLenMask)) {
-        nsr0 = __ldg(P.slot + na.x + lane);
-        na0 = __ldg(P.a + na.x + lane);
-      }
-      const int tb = a.x, L = a.y & kLenMask, dpos = a.z, t = a.w;
-      const bool chol = ((a.y >> 30) & 1) == kChol;
-      unsigned long long* stamp = P.trace ? P.trace + 4 * static_cast<long long>(__ldg(P.item + pos)) : nullptr;
-      if (stamp && lane == 0) stamp[0] = gtimer();
-      if (!latched()) {
-        if (chol)
-          flow_row<kChol, KB, 32>(C, tb, L, dpos, t, lane, kFull, 0, a0, sr0, stamp ? stamp + 1 : nullptr);
-        else
-          flow_row<kTrsm, KB, 32>(C, tb, L, dpos, t, lane, kFull, 0, a0, sr0, stamp ? stamp + 1 : nullptr);
-        ++executed;
-      } else {
-        skip_row(P.a, P.vals, tb, L, nullptr);
-      }
-      if (stamp && lane == 0) stamp[3] = gtimer();
-      ++ran;
-      pos = npos;
-      a = na;
-      na = nna;
-      sr0 = nsr0;
-      a0 = na0;
-    }
-  }
   if (lane == 0) {
     if (ran) atomicAdd(&P.ctrl->done.v, ran);
     if (executed) atomicAdd(&P.ctrl->executed.v, executed);
@@ -764,36 +648,6 @@ cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int d
   const void* k = flow_kernel_for(threads, kb, minb, g, weak, dyn, remote);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
-}
-
-#define TCG_UNIT_VARIANTS(X) X(256, 4, 3, 0) X(256, 4, 2, 0) X(128, 4, 6, 0) X(512, 4, 1, 0)
-
-static const void* unit_kernel_for(int threads, int kb, int minb, int weak) {
-#define X(T, K, M, WK) \
-  if (threads == T && kb == K && minb == M && weak == WK) return reinterpret_cast<const void*>(&factor_units<T, K, M, WK>);
-  TCG_UNIT_VARIANTS(X)
-#undef X
-  return nullptr;
-}
-
-cudaError_t unit_occupancy(int threads, int kb, int minb, int weak, size_t smem, int* ctas_per_sm) {
-  const void* k = unit_kernel_for(threads, kb, minb, weak);
-  if (!k) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, smem);
-}
-
-cudaError_t launch_units(const FlowParams& p, const UnitParams& u, int grid, int threads, int kb, int minb,
-                         int weak, size_t smem, cudaStream_t st) {
-#define X(T, K, M, WK)                                                  \
-  if (threads == T && kb == K && minb == M && weak == WK) {             \
-    factor_units<T, K, M, WK><<<grid, T, smem, st>>>(p, u);             \
-    return cudaGetLastError();                                          \
-  }
-  TCG_UNIT_VARIANTS(X)
-#undef X
-  return cudaErrorInvalidValue;
 }
 
 // init_factor_values on the device: U slot t <- 0.0 + A[map[t]] (the host

@@ -1,0 +1,361 @@
+// Lean host plan of the value-flow factorization (flow_plan.hpp).
+#include "flow_plan.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <thread>
+
+namespace tcb {
+
+namespace {
+
+double since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+int host_threads() {
+  if (const char* e = std::getenv("TCG_PLAN_THREADS")) return std::max(1, std::atoi(e));
+  const unsigned h = std::thread::hardware_concurrency();
+  return static_cast<int>(std::clamp(h ? h : 1u, 1u, 32u));
+}
+
+// fn(row_begin, row_end) over contiguous row chunks on `threads` threads
+template <class F>
+void parallel_rows(index_t n, int threads, F&& fn) {
+  const int T = std::max(1, std::min<int>(threads, std::max<index_t>(1, n / 4096)));
+  if (T == 1) {
+    fn(0, n);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int k = 0; k < T; ++k) {
+    const auto b = static_cast<index_t>(static_cast<std::int64_t>(n) * k / T);
+    const auto e = static_cast<index_t>(static_cast<std::int64_t>(n) * (k + 1) / T);
+    pool.emplace_back([&fn, b, e] { fn(b, e); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+// validate_csr (sparse.cpp) over the host threads: the same checks and
+// messages, the first failing row reported
+void validate_ref(const CsrRef& m, int threads) {
+  if (m.n < 0 || m.nnz < 0) throw std::invalid_argument("csr: negative dimension");
+  if (!m.row_ptr) throw std::invalid_argument("csr view: null or negative sizes");
+  if (m.row_ptr[0] != 0) throw std::invalid_argument("csr: row_ptr[0] != 0");
+  if (m.row_ptr[m.n] != m.nnz) throw std::invalid_argument("csr: array length mismatch");
+  if (m.nnz > 0 && !m.col_idx) throw std::invalid_argument("csr view: null col_idx");
+  std::atomic<index_t> bad{std::numeric_limits<index_t>::max()};
+  parallel_rows(m.n, threads, [&](index_t b, index_t e) {
+    for (index_t i = b; i < e && i < bad.load(std::memory_order_relaxed); ++i) {
+      bool ok = m.row_ptr[i] <= m.row_ptr[i + 1];
+      for (offset_t q = m.row_ptr[i]; ok && q < m.row_ptr[i + 1]; ++q)
+        ok = m.col_idx[q] >= 0 && m.col_idx[q] < m.n && (q == m.row_ptr[i] || m.col_idx[q] > m.col_idx[q - 1]);
+      if (!ok) {
+        index_t cur = bad.load();
+        while (i < cur && !bad.compare_exchange_weak(cur, i)) {
+        }
+        return;
+      }
+    }
+  });
+  const index_t i = bad.load();
+  if (i == std::numeric_limits<index_t>::max()) return;
+  if (m.row_ptr[i] > m.row_ptr[i + 1]) throw std::invalid_argument("csr: row_ptr not non-decreasing");
+  for (offset_t q = m.row_ptr[i]; q < m.row_ptr[i + 1]; ++q) {
+    if (m.col_idx[q] < 0 || m.col_idx[q] >= m.n) throw std::invalid_argument("csr: column index out of range");
+    if (q > m.row_ptr[i] && m.col_idx[q] <= m.col_idx[q - 1])
+      throw std::invalid_argument("csr: columns not strictly increasing in row " + std::to_string(i));
+  }
+}
+
+// Block CSR of the reference's 2D layout (block (I,J), I <= J, exists iff U
+// has an entry in ranges[I] x ranges[J]; block_layout.hpp:71-72) and the
+// task counts of its generation walk (factorize.hpp:177-224): one Chol per
+// block row, one Trsm and one Herk per off-diagonal block, one Gemm per pair
+// of off-diagonal blocks (i < j) of a block row whose target (i, j) exists.
+void count_tasks(const FlowPlan& P, const RangeList& ranges, const std::vector<index_t>& owner,
+                 FlowPlanStats& st) {
+  const index_t m = ranges.count();
+  std::vector<offset_t> bptr(static_cast<std::size_t>(m) + 1, 0);
+  std::vector<index_t> bcol;
+  std::vector<index_t> stamp(static_cast<std::size_t>(m), -1), present;
+  const std::int32_t* cols = P.cols.data();
+  for (index_t bi = 0; bi < m; ++bi) {
+    present.clear();
+    for (index_t i = ranges.ranges[bi].begin; i < ranges.ranges[bi].end; ++i)
+      for (std::int32_t q = P.row_ptr[i], qe = P.row_ptr[i + 1]; q < qe;) {
+        const index_t bj = owner[cols[q]];
+        if (stamp[bj] != bi) {
+          stamp[bj] = bi;
+          present.push_back(bj);
+        }
+        // skip the rest of this block's slice of the row
+        q = static_cast<std::int32_t>(std::lower_bound(cols + q, cols + qe, ranges.ranges[bj].end) - cols);
+      }
+    std::sort(present.begin(), present.end());
+    bcol.insert(bcol.end(), present.begin(), present.end());
+    bptr[bi + 1] = static_cast<offset_t>(bcol.size());
+  }
+  const offset_t nb = static_cast<offset_t>(bcol.size());
+  std::int64_t gemm = 0;
+  for (index_t p = 0; p < m; ++p) {
+    // off-diagonal block columns of row p (the diagonal block leads)
+    const offset_t b = bptr[p] + 1, e = bptr[p + 1];
+    for (offset_t x = b; x < e; ++x) {
+      const index_t i = bcol[x];
+      const auto re = bcol.begin() + bptr[i + 1];
+      auto it = bcol.begin() + bptr[i];
+      for (offset_t y = x + 1; y < e; ++y) {  // targets (i, j), j ascending: one forward merge
+        it = std::lower_bound(it, re, bcol[y]);
+        if (it == re) break;
+        if (*it == bcol[y]) ++gemm;
+      }
+    }
+  }
+  st.nblock_rows = m;
+  st.nblocks = nb;
+  st.tasks[0] = m;
+  st.tasks[1] = st.tasks[2] = nb - m;
+  st.tasks[3] = gemm;
+}
+
+}  // namespace
+
+CsrMatrix flow_plan_pattern(const FlowPlan& P) {
+  CsrMatrix u;
+  u.nrows = u.ncols = P.n;
+  u.row_ptr.assign(P.row_ptr.begin(), P.row_ptr.end());
+  u.col_idx = P.cols;
+  u.values.assign(P.cols.size(), 1.0);
+  return u;
+}
+
+FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& ranges) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int threads = host_threads();
+  const bool say = std::getenv("TCG_PLAN_TIMES") != nullptr;
+  auto mark = [&](const char* what) {
+    if (say) std::fprintf(stderr, "flow plan %-10s %8.3f s\n", what, since(t0));
+  };
+  validate_ref(a, threads);
+  if (a.nnz > 0 && !a.values) throw std::invalid_argument("csr view: values required");
+  validate_ref(u, threads);
+  if (a.n != u.n) throw std::invalid_argument("a_permuted and pattern sizes differ");
+  validate_ranges(ranges, u.n);
+  if (u.nnz > std::numeric_limits<std::int32_t>::max())
+    throw std::invalid_argument("factor has more than 2^31-1 entries");
+  const index_t n = u.n;
+  // diagonal entries must lead every row (kernels.hpp:46-48)
+  for (index_t i = 0; i < n; ++i)
+    if (u.row_ptr[i] == u.row_ptr[i + 1] || u.col_idx[u.row_ptr[i]] != i)
+      throw std::invalid_argument("chol_block: missing diagonal entry in row " + std::to_string(i));
+  mark("validate");
+
+  FlowPlan P;
+  P.n = n;
+  P.nnz = u.nnz;
+  P.nnz_a = a.nnz;
+  P.stats.threads = threads;
+  P.cols.resize(static_cast<std::size_t>(u.nnz));
+  P.row_ptr.resize(static_cast<std::size_t>(n) + 1);
+  P.values.resize(static_cast<std::size_t>(u.nnz));
+  P.a_map.assign(static_cast<std::size_t>(u.nnz), -1);
+  // initial values (factorize.hpp:71-89) by rows on the host threads: the
+  // sorted merge of A's upper row into U's, recording where each slot starts
+  // from (the device init's map; 0.0 + a as there). A slot fed twice
+  // (duplicate entries in A) has no map and keeps the sum, as the reference.
+  const bool mappable = a.nnz <= 0x7fffffffLL;
+  std::atomic<bool> dup{!mappable};
+  parallel_rows(n, threads, [&](index_t b, index_t e) {
+    for (index_t i = b; i < e; ++i) {
+      const offset_t ub = u.row_ptr[i], ue = u.row_ptr[i + 1];
+      P.row_ptr[i] = static_cast<std::int32_t>(ub);
+      for (offset_t t = ub; t < ue; ++t) {
+        P.cols[t] = u.col_idx[t];
+        P.values[t] = 0.0;
+      }
+      offset_t t = ub;
+      for (offset_t q = a.row_ptr[i]; q < a.row_ptr[i + 1]; ++q) {
+        const index_t c = a.col_idx[q];
+        if (c < i) continue;
+        while (t < ue && u.col_idx[t] < c) ++t;
+        if (t < ue && u.col_idx[t] == c) {
+          P.values[t] += a.values[q];
+          if (P.a_map[t] >= 0) dup.store(true, std::memory_order_relaxed);
+          P.a_map[t] = static_cast<std::int32_t>(q);
+        }
+      }
+    }
+  });
+  P.row_ptr[n] = static_cast<std::int32_t>(u.nnz);
+  if (dup.load()) P.a_map.clear();  // no device init (host values only)
+  mark("init");
+
+  std::vector<index_t> owner(static_cast<std::size_t>(n));
+  for (index_t r = 0; r < ranges.count(); ++r)
+    for (index_t c = ranges.ranges[r].begin; c < ranges.ranges[r].end; ++c) owner[c] = r;
+  // the block layout's task counts on a second thread (FactorStats)
+  std::thread blocks([&] {
+    const auto tb = std::chrono::steady_clock::now();
+    count_tasks(P, ranges, owner, P.stats);
+    P.stats.block_build_seconds = since(tb);
+  });
+  try {
+    // units in natural order (row ascending; a row's Chol slice, then its chunks)
+    const std::int32_t* cols = P.cols.data();
+    std::vector<std::int32_t> ufirst(static_cast<std::size_t>(n) + 1, 0), dsplit(static_cast<std::size_t>(n), 0);
+    parallel_rows(n, threads, [&](index_t b, index_t e) {
+      for (index_t t = b; t < e; ++t) {
+        const std::int32_t rb = P.row_ptr[t], re = P.row_ptr[t + 1];
+        if (re - rb <= 32) {
+          dsplit[t] = re;
+          ufirst[t + 1] = 1;
+          continue;
+        }
+        const auto ds = static_cast<std::int32_t>(
+            std::lower_bound(cols + rb, cols + re, ranges.ranges[owner[t]].end) - cols);
+        dsplit[t] = ds;
+        ufirst[t + 1] = 1 + (re - ds + 31) / 32;
+      }
+    });
+    for (index_t t = 0; t < n; ++t) ufirst[t + 1] += ufirst[t];
+    const std::size_t U = static_cast<std::size_t>(ufirst[n]);
+    if (U >= (1u << 31)) throw std::length_error("flow: too many units");
+    // per unit: first position, length, first and last column, row
+    std::vector<std::int32_t> u_tb(U), u_len(U), u_c0(U), u_c1(U), row_of(U);
+    parallel_rows(n, threads, [&](index_t b, index_t e) {
+      for (index_t t = b; t < e; ++t) {
+        std::int32_t g = ufirst[t];
+        const std::int32_t rb = P.row_ptr[t], re = P.row_ptr[t + 1], ds = dsplit[t];
+        auto put = [&](std::int32_t tb, std::int32_t len) {
+          u_tb[g] = tb;
+          u_len[g] = len;
+          u_c0[g] = cols[tb];
+          u_c1[g] = cols[tb + len - 1];
+          row_of[g] = t;
+          ++g;
+        };
+        put(rb, ds - rb);
+        for (std::int32_t c0 = ds; c0 < re; c0 += 32) put(c0, std::min(re - c0, 32));
+      }
+    });
+    mark("units");
+
+    // Dependences of unit g (row t, last column c1(g)): for every source r of
+    // t (an entry U(r,t) at position q), the units of row r from the one
+    // holding q on, up to the last one starting at a column <= c1(g) (they
+    // hold the multiplier and every operand U(r,c) g reads); a chunk also
+    // reads U(t,t), its row's Chol unit. Every dependence points to a lower
+    // row (or the row's own Chol unit), so both sweeps below run in row
+    // order, pushing along the entries of U's rows (no transposed index).
+    std::vector<std::int32_t> level(U, 1), height(U, 1);
+    // each (dependence v of row r, dependent g of row t) pair of the source entry q
+    auto each_pair = [&](index_t r, std::int32_t q, auto&& fn) {
+      const index_t t = cols[q];
+      std::int32_t v0 = ufirst[r];
+      while (v0 + 1 < ufirst[r + 1] && u_tb[v0 + 1] <= q) ++v0;
+      for (std::int32_t g = ufirst[t]; g < ufirst[t + 1]; ++g) {
+        fn(v0, g);
+        for (std::int32_t v = v0 + 1; v < ufirst[r + 1] && u_c0[v] <= u_c1[g]; ++v) fn(v, g);
+      }
+    };
+    std::int32_t depth = 0;
+    for (index_t r = 0; r < n; ++r) {
+      const std::int32_t chol = ufirst[r];
+      for (std::int32_t g = chol + 1; g < ufirst[r + 1]; ++g) level[g] = std::max(level[g], level[chol] + 1);
+      for (std::int32_t g = chol; g < ufirst[r + 1]; ++g) depth = std::max(depth, level[g]);
+      for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q)
+        each_pair(r, q, [&](std::int32_t v, std::int32_t g) { level[g] = std::max(level[g], level[v] + 1); });
+    }
+    for (index_t r = n; r-- > 0;) {
+      for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q)
+        each_pair(r, q, [&](std::int32_t v, std::int32_t g) { height[v] = std::max(height[v], height[g] + 1); });
+      const std::int32_t chol = ufirst[r];
+      for (std::int32_t g = chol + 1; g < ufirst[r + 1]; ++g) height[chol] = std::max(height[chol], height[g] + 1);
+    }
+    mark("levels");
+    // schedule: level ascending, height descending, unit id ascending (two
+    // stable counting sorts, the second key first)
+    std::int32_t hmax = 0;
+    for (std::int32_t h : height) hmax = std::max(hmax, h);
+    std::vector<std::int32_t> tmp(U), order(U);
+    {
+      std::vector<std::int64_t> cnt(static_cast<std::size_t>(hmax) + 2, 0);
+      for (std::size_t g = 0; g < U; ++g) ++cnt[static_cast<std::size_t>(hmax - height[g]) + 1];
+      for (std::size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+      for (std::size_t g = 0; g < U; ++g)
+        tmp[cnt[static_cast<std::size_t>(hmax - height[g])]++] = static_cast<std::int32_t>(g);
+    }
+    {
+      std::vector<std::int64_t> cnt(static_cast<std::size_t>(depth) + 2, 0);
+      for (std::size_t g = 0; g < U; ++g) ++cnt[static_cast<std::size_t>(level[g])];
+      for (std::size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+      for (std::size_t x = 0; x < U; ++x) {
+        const std::int32_t g = tmp[x];
+        order[cnt[static_cast<std::size_t>(level[g]) - 1]++] = g;
+      }
+    }
+    P.rec.resize(4 * U);
+    P.unit.resize(U);
+    for (std::size_t q = 0; q < U; ++q) {
+      const std::int32_t g = order[q];
+      const std::int32_t t = row_of[g];
+      if (u_len[g] >= (1 << 30)) throw std::length_error("flow: row slice too long");
+      P.rec[4 * q + 0] = u_tb[g];
+      P.rec[4 * q + 1] = u_len[g] | ((g == ufirst[t] ? 0 : 1) << 30);  // Chol unit, else a chunk (Trsm)
+      P.rec[4 * q + 2] = P.row_ptr[t];
+      P.rec[4 * q + 3] = t;
+      P.unit[q] = g;
+    }
+    mark("order");
+    P.stats.units = static_cast<std::int64_t>(U);
+    P.stats.depth = depth;
+  } catch (...) {
+    blocks.join();
+    throw;
+  }
+  blocks.join();
+  mark("blocks");
+  P.stats.plan_seconds = since(t0);
+  return P;
+}
+
+FlowPart build_flow_part(const FlowPlan& P, const std::vector<std::int32_t>& part_of_row, std::int32_t nparts,
+                         std::int32_t part) {
+  if (nparts < 1 || nparts > 64 || part < 0 || part >= nparts)
+    throw std::invalid_argument("flow part: need 1 <= nparts <= 64 and 0 <= part < nparts");
+  if (static_cast<index_t>(part_of_row.size()) != P.n) throw std::invalid_argument("flow part: one owner per row");
+  if (P.nnz >= (std::int64_t{1} << kRemoteShift)) throw std::length_error("flow part: U beyond 2^25 entries");
+  for (std::int32_t o : part_of_row)
+    if (o < 0 || o >= nparts) throw std::invalid_argument("flow part: owner out of range");
+  // rows of this part that other parts read (sources of their rows)
+  FlowPart F;
+  std::vector<char> exported(static_cast<std::size_t>(P.n), 0);
+  for (index_t r = 0; r < P.n; ++r)
+    for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q) {
+      const index_t t = P.cols[q];
+      if (part_of_row[r] == part && part_of_row[t] != part) exported[r] = 1;
+      if (part_of_row[t] == part && part_of_row[r] != part) ++F.remote_sources;
+    }
+  const std::size_t U = P.unit.size();
+  for (std::size_t q = 0; q < U; ++q) {
+    const std::int32_t* r = &P.rec[4 * q];
+    if (part_of_row[r[3]] != part) continue;
+    F.rec.insert(F.rec.end(), r, r + 4);
+    if (exported[r[3]]) {  // bit 31 of the length word: publish at system scope
+      F.rec[F.rec.size() - 3] = static_cast<std::int32_t>(static_cast<std::uint32_t>(F.rec[F.rec.size() - 3]) | kRemoteBit);
+      ++F.exported_rows;
+    }
+    F.unit.push_back(P.unit[q]);
+  }
+  F.rows = static_cast<std::int64_t>(F.unit.size());
+  return F;
+}
+
+}  // namespace tcb

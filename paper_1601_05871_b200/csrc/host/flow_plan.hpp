@@ -1,0 +1,90 @@
+// Lean host plan of the value-flow factorization (the default executor).
+//
+// Everything here is O(nnz(U)) host work, spread over the host threads
+// where rows are independent: the initial values (init_factor_values,
+// factorize.hpp:71-89), the reference DAG's task counts, and the schedule of
+// the finalising rows. U's transposed index and the per-coordinate update
+// programs -- the sorted-index merges of kernels.hpp:55-65, :85-89,
+// :104-108, :125-129, folded per coordinate -- are built on the device from
+// U's pattern (csrc/device/flow_program.cu), so the host never walks the
+// products. The full task-DAG plan (plan.hpp) is built only when the DAG
+// itself is asked for (export_task_dag parity, the task executors, sharded
+// parts).
+//
+// Units ("rows" of the schedule), per matrix row t in ascending order:
+//   * a U row of at most 32 entries is one unit (one warp pass);
+//   * a longer row is its diagonal-block slice (the Chol item of block
+//     (p,p), block_layout.hpp:98-181; entries with column < range_end(t)),
+//     then warp-wide chunks of the rest that divide by U(t,t).
+// Every coordinate of U belongs to exactly one unit, which writes it once.
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "sparse.hpp"
+
+namespace tcb {
+
+// A borrowed CSR matrix (the caller's arrays; values may be null for a pattern).
+struct CsrRef {
+  index_t n = 0;
+  offset_t nnz = 0;
+  const offset_t* row_ptr = nullptr;
+  const index_t* col_idx = nullptr;
+  const double* values = nullptr;
+};
+
+struct FlowPlanStats {
+  std::int64_t tasks[4] = {0, 0, 0, 0};  // Chol/Trsm/Herk/Gemm of the reference's DAG (counted)
+  std::int32_t nblock_rows = 0;
+  std::int64_t nblocks = 0;
+  std::int64_t units = 0;      // schedule rows
+  std::int32_t depth = 0;      // longest chain of units (levels)
+  int threads = 1;             // host threads used
+  double block_build_seconds = 0.0;
+  double plan_seconds = 0.0;
+};
+
+struct FlowPlan {
+  index_t n = 0;
+  std::int64_t nnz = 0;
+  std::int64_t nnz_a = 0;             // entries of a_permuted
+  std::vector<std::int32_t> cols;     // U column indices
+  std::vector<std::int32_t> row_ptr;  // n + 1 positions (int32: nnz < 2^31)
+  std::vector<double> values;         // initialised U values (init_factor_values)
+  std::vector<std::int32_t> a_map;    // U slot -> a_permuted position, -1 = fill (empty: A has duplicates)
+  std::vector<std::int32_t> rec;      // 4 words per schedule position: tb, L | kind << 30, dpos, t
+  std::vector<std::int32_t> unit;     // per schedule position: unit id (natural order)
+  FlowPlanStats stats;
+};
+
+// Validates both matrices as csr_from_view did (validate_csr), then the
+// ranges (ordering.hpp:43-55) and the leading diagonal of every U row
+// (kernels.hpp:46-48); std::invalid_argument on failure.
+FlowPlan build_flow_plan(const CsrRef& a_permuted, const CsrRef& pattern, const RangeList& ranges);
+
+// The pattern as an owning CsrMatrix (values 1.0), for the full plan.
+CsrMatrix flow_plan_pattern(const FlowPlan& P);
+
+// One part of a sharded value-flow factorization (C6: ND subtrees on
+// different GPUs). The part runs the units of the rows t with
+// part_of_row[t] == part, in the global schedule order (the union of the
+// parts' lists is one topological order, so no part can deadlock while the
+// others run). Its programs are the device-built ones with every operand of
+// a row another part owns rewritten to kRemoteBit | owner << kRemoteShift |
+// position (flow_program.cu), read from the owner's copy of U through peer
+// memory. A unit of a row some other part reads (a source of one of its
+// rows) carries bit 31 in its length word and publishes at system scope.
+constexpr std::uint32_t kRemoteBit = 0x80000000u;
+constexpr int kRemoteShift = 25;  // positions below 2^25, owners below 64
+struct FlowPart {
+  std::vector<std::int32_t> rec, unit;  // 4 words per schedule row, global order
+  std::int64_t rows = 0;
+  std::int64_t exported_rows = 0;     // units publishing at system scope
+  std::int64_t remote_sources = 0;    // entries U(r,t), t of the part, r of another part
+};
+FlowPart build_flow_part(const FlowPlan& P, const std::vector<std::int32_t>& part_of_row, std::int32_t nparts,
+                         std::int32_t part);
+
+}  // namespace tcb

@@ -173,6 +173,8 @@ class Reference:
             getattr(L, "ref_csr_" + name).restype = rt
         for name in ("n", "nnz", "ptr", "col", "val"):
             getattr(L, "ref_csr_" + name).argtypes = [vp]
+        L.ref_generate.restype = vp
+        L.ref_generate.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]
         L.ref_load_ordering.restype = C.c_int32
         L.ref_load_ordering.argtypes = [C.c_char_p, C.c_int32, i32p, C.c_int32, i32p]
         L.ref_export_dag.restype = vp
@@ -230,6 +232,18 @@ class Reference:
         h = self.L.ref_load_mm(str(path).encode())
         if not h:
             raise RuntimeError(self.L.ref_error().decode())
+        try:
+            n, nnz = self.L.ref_csr_n(h), self.L.ref_csr_nnz(h)
+            return (self._arr(self.L.ref_csr_ptr(h), n + 1, np.int64), self._arr(self.L.ref_csr_col(h), nnz, np.int32),
+                    self._arr(self.L.ref_csr_val(h), nnz, np.float64))
+        finally:
+            self.L.ref_csr_free(h)
+
+    def generate(self, kind, p0, p1=0, seed=0):
+        """The repo's seeded config generators, compiled into the shim: (row_ptr, col_idx, values)."""
+        h = self.L.ref_generate(kind.encode(), p0, p1, seed)
+        if not h:
+            raise ValueError(self.L.ref_error().decode())
         try:
             n, nnz = self.L.ref_csr_n(h), self.L.ref_csr_nnz(h)
             return (self._arr(self.L.ref_csr_ptr(h), n + 1, np.int64), self._arr(self.L.ref_csr_col(h), nnz, np.int32),
@@ -367,38 +381,65 @@ def emulate_program(plan) -> np.ndarray:
     return vals
 
 
-def emulate_rows(plan, seed: int = 0) -> np.ndarray:
-    """Replay of the row-level mode in a random topological order of the row
-    DAG (a missing row dependence shows up as a value mismatch)."""
-    import random
-    T = plan.tables()
-    vals = T["values"].copy()
-    srec, upd, rows = T["slot_rec"], T["upd"], T["row_rec"]
-    succ, indeg = T["row_succ"], T["row_indeg"].copy()
-    ready = list(T["row_roots"])
-    rng = random.Random(seed)
-    done = 0
-    while ready:
-        k = ready.pop(rng.randrange(len(ready)))
-        tb, te, dpos, soff, kind, _, sb, se = rows[k]
-        tv = vals[tb:te].copy()
-        for j in range(te - tb):
-            ub, ue, _, _ = srec[soff + j]
-            for u in range(ub, ue):
-                m, o = upd[u]
-                tv[j] = tv[j] - vals[m] * vals[o]
+def flow_programs(row_ptr, cols):
+    """CPU restatement of the device program builder (flow_program.cu): per
+    coordinate (t, c) of U, the (m, o) positions of U(r,t), U(r,c) over the
+    rows r < t holding both, ascending r (the per-coordinate order of
+    factor_serial, factorize.hpp:113-123). Returns (slot [nnz, 4] = {u_b,
+    u_e, m0, o0}, upd [k, 2]). Pure Python: small matrices only."""
+    row_ptr = np.asarray(row_ptr, np.int64)
+    cols = np.asarray(cols, np.int64)
+    n, nnz = len(row_ptr) - 1, len(cols)
+    rows = np.repeat(np.arange(n), np.diff(row_ptr))
+    off = np.ones(nnz, bool)
+    off[row_ptr[:-1]] = False
+    m_all = np.flatnonzero(off)
+    m_all = m_all[np.argsort(cols[m_all], kind="stable")]  # by column, rows ascending
+    col_ptr = np.searchsorted(cols[m_all], np.arange(n + 1))
+    progs = [[] for _ in range(nnz)]
+    for t in range(n):
+        tb, te = int(row_ptr[t]), int(row_ptr[t + 1])
+        where = {int(c): tb + j for j, c in enumerate(cols[tb:te])}
+        for m in m_all[col_ptr[t]:col_ptr[t + 1]]:
+            r = rows[m]
+            for q in range(int(m), int(row_ptr[r + 1])):
+                x = where.get(int(cols[q]))
+                if x is not None:
+                    progs[x].append((int(m), q))
+    cnt = np.array([len(p) for p in progs], np.int64)
+    ub = np.concatenate([[0], np.cumsum(cnt)])
+    slot = np.zeros((nnz, 4), np.int32)
+    slot[:, 0], slot[:, 1] = ub[:-1], ub[1:]
+    upd = np.array([mo for p in progs for mo in p], np.int32).reshape(-1, 2)
+    has = cnt > 0
+    slot[has, 2:] = upd[ub[:-1][has]]
+    return slot, upd
+
+
+def emulate_flow(rec, values, slot, upd, order=None) -> np.ndarray:
+    """Replay of the value-flow schedule: rows of `rec` ({tb, L | kind << 30,
+    dpos, t}) in `order` (default: schedule order), each coordinate taking its
+    program's products in order; a read of a value not yet written fails."""
+    out = np.full(len(values), np.nan)
+    done = np.zeros(len(values), bool)
+    for q in (range(len(rec)) if order is None else order):
+        tb, lk, dpos, _ = (int(x) for x in rec[q])
+        L, kind = lk & ((1 << 30) - 1), (lk >> 30) & 1
+        v = values[tb:tb + L].copy()
+        for j in range(L):
+            ub, ue = slot[tb + j, :2]
+            for m, o in upd[ub:ue]:
+                assert done[m] and done[o], "read before written"
+                v[j] = v[j] - out[m] * out[o]
         if kind == 0:
-            d = np.sqrt(tv[0])
-            tv[1:] = tv[1:] / d
-            tv[0] = d
-        elif kind == 1:
-            tv = tv / vals[dpos]
-        vals[tb:te] = tv
-        done += 1
-        for s in succ[sb:se]:
-            s = int(s) & 0x3FFFFFFF  # drop the priority flag
-            indeg[s] -= 1
-            if indeg[s] == 0:
-                ready.append(int(s))
-    assert done == len(rows), "row DAG did not drain"
-    return vals
+            d = np.sqrt(v[0])
+            v[1:] = v[1:] / d
+            v[0] = d
+        else:
+            assert done[dpos]
+            v = v / out[dpos]
+        assert not done[tb:tb + L].any(), "written twice"
+        out[tb:tb + L] = v
+        done[tb:tb + L] = True
+    assert done.all()
+    return out

@@ -41,13 +41,27 @@ def check_against_oracle(name, vals, golden, oracle):
 
 @pytest.mark.parametrize("name", ["c1", "c5_m0", "c5_m63", "s27_16_k2", "grid20_k2_leaf4",
                                   "rand_spd_200", "elast6_k1", "c2", "c3", "c4"])
-@pytest.mark.parametrize("mode", [3, 4, 5, 6])
-def test_configs_row_modes(T, golden, oracle, name, mode):  # noqa: D103
-    if mode == 6 and planned(name).stats().unit_count == 0:
-        pytest.skip("no diagonal block large enough for a unit")
-    vals, st = gpu_factor(T, planned(name), mode=mode)
-    assert st.mode == mode
+def test_configs_value_flow(T, golden, oracle, name):  # noqa: D103
+    vals, st = gpu_factor(T, planned(name), mode=5)
+    assert st.mode == 5
     check_against_oracle(name, vals, golden, oracle)
+
+
+@pytest.mark.parametrize("name", ["c1", "grid20_k2_leaf4", "rand_spd_200", "elast6_k1", "c5_m0"])
+def test_device_programs_equal_the_cpu_restatement(T, name):
+    # flow_program.cu (transposed index by a radix sort, count, scan, fill)
+    # against checkers.flow_programs, table for table
+    from checkers import flow_programs
+    plan = planned(name)
+    f = plan.flow_tables()
+    want_slot, want_upd = flow_programs(f["row_ptr"], f["cols"])
+    fz = T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30))
+    try:
+        slot, upd, ms = fz.flow_programs()
+    finally:
+        fz.close()
+    assert ms > 0
+    assert np.array_equal(slot, want_slot) and np.array_equal(upd, want_upd)
 
 
 @pytest.mark.parametrize("name", ["c1", "c5_m0", "s27_16_k2", "c3"])
@@ -64,37 +78,49 @@ def test_default_mode_is_value_flow(T):
     assert st.mode == 5
 
 
-def test_flow_trace_stamps_every_finalising_row(T):
-    # mode 5 has no row flags (a row starts and polls its operands), so the
-    # stamps only bracket each finalising row
-    plan = planned("c5_m0")
-    fz = T.GpuFactorizer(plan, T.GpuOptions(mode=5, trace=True))
-    fz.factor()
-    _, items = fz.trace()
-    fz.close()
-    t = plan.tables()
-    st = items[t["flow_item"]]  # {start, operands final, -, end}
+@pytest.mark.parametrize("name", ["c5_m0", "elast6_k1", "s27_16_k2"])
+def test_flow_trace_is_sound(T, name):
+    # acceptance.cpp:285-316 for the value flow: the stamps bracket every row
+    # ({start, operands final, -, end}), and a row's operands become final only
+    # after every row it reads had its own operands final (the producer
+    # computes its values after that stamp, the reader sees them before its
+    # own). Readers: rows of <= 32 entries, whose stamp covers all of them.
+    from checkers import flow_programs
+    plan = planned(name)
+    fz = T.GpuFactorizer(plan, T.GpuOptions(mode=5, trace=True, timeout_s=30))
+    try:
+        fz.factor()
+        _, units = fz.trace()
+    finally:
+        fz.close()
+    f = plan.flow_tables()
+    rec, unit = f["flow_rec"], f["flow_item"]
+    st = units[unit]  # per schedule position
     assert np.all(st[:, 0] > 0) and np.all(st[:, 0] <= st[:, 1]) and np.all(st[:, 1] <= st[:, 3])
-
-
-def test_static_trace_respects_every_row_edge(T):
-    # mode 4: stamps per row; every predecessor finishes before the row starts
-    plan = planned("c5_m0")
-    fz = T.GpuFactorizer(plan, T.GpuOptions(mode=4, trace=True))
-    fz.factor()
-    _, items = fz.trace()
-    fz.close()
-    t = plan.tables()
-    ni = len(t["row_rec"])
-    st = items.reshape(-1)[:2 * ni].reshape(-1, 2)
-    rows, succ = t["row_rec"], t["row_succ"] & 0x3FFFFFFF
-    src = np.repeat(np.arange(ni), rows[:, 7] - rows[:, 6])
-    assert np.all(st[src, 1] <= st[succ, 0])
+    L = rec[:, 1] & ((1 << 30) - 1)
+    owner = np.empty(len(f["cols"]), np.int64)
+    for q, (tb, l) in enumerate(zip(rec[:, 0], L)):
+        owner[tb:tb + l] = q
+    slot, upd = flow_programs(f["row_ptr"], f["cols"])
+    checked = 0
+    for q in range(len(rec)):
+        if L[q] > 32:
+            continue
+        tb = rec[q, 0]
+        deps = {owner[x] for ub, ue in slot[tb:tb + L[q], :2] for x in upd[ub:ue].ravel()}
+        if (rec[q, 1] >> 30) & 1:
+            deps.add(owner[rec[q, 2]])
+        for d in deps:
+            assert st[d, 1] <= st[q, 1], (q, d)
+            checked += 1
+    assert checked > 0
 
 
 @pytest.mark.parametrize("mode", [1, 2])
-@pytest.mark.parametrize("name", ["c1", "c5_m0", "s27_16_k2", "elast6_k1", "c2"])
+@pytest.mark.parametrize("name", ["c1", "c5_m0", "s27_16_k2", "elast6_k1", "c2", "c3", "c4"])
 def test_configs_task_modes(T, golden, oracle, name, mode):
+    # the literal task executors (device ready queue + dependence counters
+    # over the reference's Chol/Trsm/Herk/Gemm DAG) on the task-DAG plan
     vals, st = gpu_factor(T, planned(name), mode=mode)
     assert st.mode == mode
     assert st.tasks_completed == sum(planned(name).stats().tasks)
@@ -137,7 +163,7 @@ def sym(entries):
     return entries + [(j, i, v) for i, j, v in entries if i != j]
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("mode", [1, 2, 5])
 def test_known_answers(T, mode):
     # test_factorize.cpp:78-97 and test_kernels.cpp:36-57
     opt = T.GpuOptions(mode=mode)
@@ -154,7 +180,7 @@ def test_known_answers(T, mode):
     assert v[0] == 2.0 and v[1] == 1.0 and v[2] == math.sqrt(2.0)
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("mode", [1, 2, 5])
 def test_breakdown_reports_row_and_pivot(T, mode):
     # test_factorize.cpp:99-108,157-165 and test_kernels.cpp:62-76
     opt = T.GpuOptions(mode=mode)
@@ -183,7 +209,7 @@ def test_random_spd_many_blockings(T, oracle, seed):
         step = max(1, -(-n // nr))
         b = np.array(list(range(0, n, step)) + [n], dtype=np.int32)
         plan = T.Plan(an.a_permuted, an.pattern, T.RangeList(b))
-        for mode in (1, 2, 3, 4, 5):
+        for mode in (1, 2, 5):
             vals, _ = gpu_factor(T, plan, mode=mode)
             assert bitwise_equal(vals, ref), (nr, mode)
 
@@ -220,20 +246,6 @@ def test_task_trace_respects_every_dag_edge(T):
     assert np.all(tasks[d.edge_from, 1] <= tasks[d.edge_to, 0])
 
 
-def test_row_trace_respects_every_row_edge(T):
-    plan = planned("c5_m0")
-    fz = T.GpuFactorizer(plan, T.GpuOptions(mode=3, trace=True))
-    fz.factor()
-    _, items = fz.trace()
-    fz.close()
-    t = plan.tables()
-    ni = len(t["row_rec"])
-    st = items.reshape(-1)[:2 * ni].reshape(-1, 2)
-    rows, succ = t["row_rec"], t["row_succ"] & 0x3FFFFFFF
-    src = np.repeat(np.arange(ni), rows[:, 7] - rows[:, 6])
-    assert np.all(st[src, 1] <= st[succ, 0])
-
-
 def test_refactor_with_new_values_and_determinism(T, oracle):
     # C5-style reuse: one plan, several value sets (same pattern and DAG)
     name = "c5_m0"
@@ -266,7 +278,7 @@ def test_refactor_with_new_values_and_determinism(T, oracle):
 def test_cta_sizes_agree(T, threads):
     plan = planned("s27_16_k2")
     base, _ = gpu_factor(T, plan)
-    for mode in (1, 2, 3, 4, 5):
+    for mode in (1, 2, 5):
         vals, st = gpu_factor(T, plan, mode=mode, threads_per_cta=threads)
         assert st.threads_per_cta == threads
         assert bitwise_equal(vals, base)
@@ -351,48 +363,13 @@ def test_c5_batch_breakdown_is_per_member(T, oracle):
         fz.close()
 
 
-@pytest.mark.parametrize("min_rows", [4, 16, 64])
-@pytest.mark.parametrize("name", ["c5_m0", "s27_16_k2", "grid20_k2_leaf4", "rand_spd_200"])
-def test_block_units(T, golden, oracle, name, min_rows, monkeypatch):
-    # mode 6: diagonal blocks above min_rows run as CTA units (shared-memory values)
-    monkeypatch.setenv("TCG_UNIT_MIN_ROWS", str(min_rows))
-    monkeypatch.setenv("TCG_FLOW_MERGE_ROWS", "0")  # units are built from diagonal-block rows
-    _, an = analyzed(name)
-    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
-    if plan.stats().unit_count == 0:
-        pytest.skip("no block above min_rows")
-    vals, st = gpu_factor(T, plan, mode=6)
-    assert st.mode == 6
-    check_against_oracle(name, vals, golden, oracle)
-
-
-def test_block_units_breakdown(T):
-    a, fp, rl = small(T, 4, sym([(0, 0, 1.0), (1, 1, 1.0), (2, 2, 1.0), (2, 3, 4.0), (3, 3, 1.0)]),
-                      bounds=[0, 4])
-    os.environ["TCG_UNIT_MIN_ROWS"] = "1"
-    os.environ["TCG_FLOW_MERGE_ROWS"] = "0"
-    try:
-        plan = T.Plan(a, fp, rl)
-    finally:
-        del os.environ["TCG_UNIT_MIN_ROWS"]
-        del os.environ["TCG_FLOW_MERGE_ROWS"]
-    assert plan.stats().unit_count == 1
-    fz = T.GpuFactorizer(plan, T.GpuOptions(mode=6))
-    try:
-        with pytest.raises(T.BreakdownError) as e:
-            fz.factor()
-        assert e.value.row == 3
-    finally:
-        fz.close()
-
-
 @pytest.mark.parametrize("name", ["c1", "c5_m0", "c2", "c4"])
 def test_factor_host_overlapped_upload(T, golden, oracle, name):
     # tcg_factor_host: the input copy runs beside the mode-5 kernel, which
     # polls the inputs; the result is the same bits
     import torch
     plan = planned(name)
-    vals = plan.tables()["values"]
+    vals = plan.flow_tables()["values"]
     fz = T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30))
     try:
         host_in = torch.from_numpy(vals.copy()).pin_memory()
@@ -401,7 +378,7 @@ def test_factor_host_overlapped_upload(T, golden, oracle, name):
             host_out.fill_(0.0)
             st = fz.factor_host_ptr(host_in.data_ptr(), host_out.data_ptr())
             check_against_oracle(name, host_out.numpy(), golden, oracle)
-        assert st.mode in (4, 5)
+        assert st.mode == 5
         out = fz.factor_host(vals)  # pageable buffers work too
         check_against_oracle(name, out, golden, oracle)
     finally:
@@ -441,8 +418,7 @@ def test_sharded_parts_through_peer_pointers(T, golden, oracle, name, nparts):
         for f in fzs:
             st = f.factor()
             assert st.mode == 5
-        t = plan.tables()
-        full = np.full(len(t["values"]), np.nan)
+        full = np.full(an.pattern.pattern.nnz(), np.nan)
         own_pos = np.repeat(owners, np.diff(an.pattern.pattern.row_ptr))  # owner of every U entry
         for k, f in enumerate(fzs):
             v = f.download()
@@ -518,7 +494,7 @@ def test_device_init_factor_values(T, golden, oracle, name):
         fz.set_a_values(an.a_permuted.values)
         fz.restore()
         init = fz.download()
-        assert bitwise_equal(init, plan.tables()["values"])
+        assert bitwise_equal(init, plan.flow_tables()["values"])
         fz.factor()
         check_against_oracle(name, fz.download(), golden, oracle)
     finally:
@@ -552,7 +528,7 @@ def test_factor_host_a_end_to_end(T, golden, oracle, name):
             check_against_oracle(name, out, golden, oracle)
         assert fz.last.kernel_launches == 3
         fz.restore()
-        assert bitwise_equal(fz.download(), planned(name).tables()["values"])
+        assert bitwise_equal(fz.download(), planned(name).flow_tables()["values"])
     finally:
         fz.close()
 
@@ -580,7 +556,7 @@ def test_drained_end_to_end(T, golden, oracle, name, monkeypatch):
     fz = T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30))
     try:
         a_in = torch.from_numpy(an.a_permuted.values.copy()).pin_memory()
-        u_in = torch.from_numpy(plan.tables()["values"]).pin_memory()
+        u_in = torch.from_numpy(plan.flow_tables()["values"]).pin_memory()
         monkeypatch.setenv("TCG_DRAIN", "1")  # forced: no calibration
         for ctas in ("1", "2", "4"):
             monkeypatch.setenv("TCG_DRAIN_CTAS", ctas)

@@ -119,7 +119,10 @@ def test_two_rank_subtree_sharding(tmp_path, oracle):
     owners = np.load(tmp_path / "owners.npy")
     parts = pickle.load(open(tmp_path / "parts.pkl", "rb"))
     assert [int((owners == k).sum()) > 0 for k in range(2)] == [True, True]
-    full, remote, read_remotely, exported = replay_parts(planned("c5_m0").tables(), parts, owners)
+    from checkers import flow_programs
+    f = planned("c5_m0").flow_tables()
+    slot, upd = flow_programs(f["row_ptr"], f["cols"])
+    full, remote, read_remotely, exported = replay_parts(f, slot, upd, parts, owners)
     _, an = analyzed("c5_m0")
     ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
     assert bitwise_equal(full, ref) and remote > 0 and read_remotely <= exported

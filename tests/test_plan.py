@@ -1,11 +1,14 @@
-"""Host flattener (tcg_plan_build): the DAG is bit-exact with the reference's
-export_task_dag, the block structure with build_block_matrix, and the work
-tables reproduce factor_serial bit for bit when replayed on the CPU in any
-order the dependences allow (task order, row order, random row orders)."""
+"""Host plans. The lean value-flow plan (tcg_plan_build): task counts equal
+the reference DAG's, and its schedule -- replayed on the CPU with the
+programs the device builds (restated in checkers.flow_programs) -- gives
+factor_serial bit for bit, in schedule order and in row order. The task-DAG
+plan (tcg_plan_expand): the DAG is bit-exact with the reference's
+export_task_dag, the block structure with build_block_matrix, and its work
+tables replay to factor_serial in task order."""
 import numpy as np
 import pytest
 
-from checkers import Reference, emulate_plan, emulate_program, emulate_rows, reference_available
+from checkers import Reference, emulate_flow, emulate_plan, emulate_program, flow_programs, reference_available
 from conftest import analyzed, bitwise_equal, planned
 
 FAST = ["c1", "c5_m0", "s27_16_k2", "grid20_k2_leaf4", "rand_spd_200", "elast6_k1"]
@@ -36,44 +39,6 @@ def test_replays_are_bitwise_serial(name, golden, oracle):
     assert oracle.hash(ref) == golden[name]["factor_values"]
     assert bitwise_equal(emulate_plan(plan), ref)       # device merge mode, task order
     assert bitwise_equal(emulate_program(plan), ref)    # update programs, task order
-    for seed in range(3):                               # row-level DAG, random orders
-        assert bitwise_equal(emulate_rows(plan, seed), ref)
-
-
-@pytest.mark.parametrize("name", ["c1", "s27_16_k2", "rand_spd_200"])
-def test_static_schedule_is_topological_and_replays_bitwise(name, oracle):
-    # mode 4: rows in position order; every predecessor sits at an earlier position
-    plan = planned(name)
-    t = plan.tables()
-    order, pos, extra = t["row_order"], t["pos_rec"], t["pos_pred"]
-    pos_of = np.empty(len(order), np.int64)
-    pos_of[order] = np.arange(len(order))
-    for q in range(len(order)):
-        rec = pos[q]
-        assert rec[12] == order[q]
-        preds = [p for p in rec[8:8 + min(4, rec[6])]] + list(extra[rec[7]:rec[7] + max(0, rec[6] - 4)])
-        assert len(preds) == rec[6]
-        assert all(pos_of[p] < q for p in preds)
-    # replay in position order == serial
-    _, an = analyzed(name)
-    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
-    vals = t["values"].copy()
-    srec, upd, rows = t["slot_rec"], t["upd"], t["row_rec"]
-    for k in order:
-        tb, te, dpos, soff, kind = rows[k][:5]
-        tv = vals[tb:te].copy()
-        for j in range(te - tb):
-            ub, ue, _, _ = srec[soff + j]
-            for u in range(ub, ue):
-                tv[j] = tv[j] - vals[upd[u][0]] * vals[upd[u][1]]
-        if kind == 0:
-            d = np.sqrt(tv[0])
-            tv[1:] = tv[1:] / d
-            tv[0] = d
-        elif kind == 1:
-            tv = tv / vals[dpos]
-        vals[tb:te] = tv
-    assert bitwise_equal(vals, ref)
 
 
 def test_dag_edges_point_forward_and_task_count_formula(T):
@@ -103,15 +68,15 @@ def test_dag_edges_point_forward_and_task_count_formula(T):
             assert chol_of[int(d.block_row[t])] in preds[t]
 
 
-def test_row_dependences_are_acyclic_and_shorter(T):
-    plan = planned("c5_m0")
+def test_flow_depth_is_below_the_task_dag_depth(T):
+    # value flow follows the rows that interact, not the blocks: much shallower
+    _, an = analyzed("c5_m0")
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
     s = plan.stats()
-    assert s.item_depth < s.dag_depth  # rows shorten the critical path
-    t = plan.tables()
-    rows, succ = t["row_rec"], t["row_succ"] & 0x3FFFFFFF
-    for k in range(0, len(rows), 97):
-        assert np.all(succ[rows[k, 6]:rows[k, 7]] > k)  # generation order is topological
-    assert t["row_indeg"].sum() == len(succ)
+    assert s.full_plan == 0 and s.flow_depth > 0
+    plan.expand()
+    s = plan.stats()
+    assert s.full_plan == 1 and s.flow_depth < s.dag_depth
 
 
 def test_single_range_and_diagonal_only(T, oracle):
@@ -121,7 +86,7 @@ def test_single_range_and_diagonal_only(T, oracle):
     plan = T.Plan(a, fp, one)
     assert list(plan.stats().tasks) == [1, 0, 0, 0]
     ref, _, _, _ = oracle.factor_serial(a, fp.pattern)
-    assert bitwise_equal(emulate_rows(plan), ref)
+    assert bitwise_equal(replay_lean(plan), ref)
     d = T.generate("grid2d", 1, 8)  # path-like, blocks of one vertex each
     fp = T.levelk_pattern(d, 0)
     plan = T.Plan(d, fp, T.RangeList(np.arange(9, dtype=np.int32)))
@@ -159,208 +124,122 @@ def test_random_blockings_against_live_reference(T, oracle, seed):
         assert np.array_equal(d.edge_to, et) and np.array_equal(d.block_row, bi)
         vals, st, _, _, _, _ = R.factor_by_blocks(an.a_permuted, an.pattern.pattern, b, workers=2)
         assert st == 0
-        assert bitwise_equal(emulate_rows(plan, seed), vals)
+        assert list(plan.stats().tasks) == [int((kinds == k).sum()) for k in range(4)]
+        assert bitwise_equal(replay_lean(plan), vals)
 
 
-def replay_flow(t, order=None):
-    """Mode 5 on the CPU: finalising rows in schedule order (or `order`), each
-    coordinate applying its merged program once, reading only final values."""
-    rec, slot, upd = t["flow_rec"], t["flow_slot"], t["flow_upd"]
-    a = t["values"]
-    out = np.full(len(a), np.nan)
-    done = np.zeros(len(a), bool)
-    for q in (range(len(rec)) if order is None else order):
-        tb, lk, dpos, _ = rec[q]
-        L, kind = lk & ((1 << 30) - 1), (lk >> 30) & 3
-        v = a[tb:tb + L].copy()
-        for j in range(L):
-            ub, ue = slot[tb + j, :2]
-            for m, o in upd[ub:ue]:
-                assert done[m] and done[o], "read before written"
-                v[j] = v[j] - out[m] * out[o]
-        if kind == 0:
-            d = np.sqrt(v[0])
-            v[1:] = v[1:] / d
-            v[0] = d
-        else:
-            assert done[dpos]
-            v = v / out[dpos]
-        assert not done[tb:tb + L].any(), "written twice"
-        out[tb:tb + L] = v
-        done[tb:tb + L] = True
-    assert done.all()
-    return out
+def replay_lean(plan, order=None):
+    f = plan.flow_tables()
+    slot, upd = flow_programs(f["row_ptr"], f["cols"])
+    return emulate_flow(f["flow_rec"], f["values"], slot, upd, order)
 
 
-@pytest.mark.parametrize("merge", [True, False])
-@pytest.mark.parametrize("name", ["c1", "rand_spd_200", "grid20_k2_leaf4", "elast6_k1"])
-def test_flow_schedule_partitions_u_and_replays_bitwise(T, name, merge, oracle, monkeypatch):
+@pytest.mark.parametrize("name", ["c1", "rand_spd_200", "grid20_k2_leaf4", "elast6_k1", "c5_m0"])
+def test_flow_schedule_partitions_u_and_replays_bitwise(T, name, golden, oracle):
     # mode 5: the rows of the schedule own every coordinate once -- whole
-    # matrix rows of <= 32 entries (merge) or one Chol/Trsm item each; merged
-    # programs keep the per-coordinate product order, so replays equal
-    # factor_serial
-    monkeypatch.setenv("TCG_FLOW_MERGE_ROWS", "1" if merge else "0")
+    # matrix rows of <= 32 entries, longer ones the diagonal-block slice +
+    # chunks of <= 32; with the device-built programs the replay equals
+    # factor_serial, in schedule order and in any order that reads only
+    # written values (matrix-row order is one)
     _, an = analyzed(name)
-    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
-    t = plan.tables()
+    plan = planned(name)
+    f = plan.flow_tables()
     s = plan.stats()
-    fin = int((t["row_rec"][:, 4] <= 1).sum())
-    rec = t["flow_rec"]
+    rec = f["flow_rec"]
     L = rec[:, 1] & ((1 << 30) - 1)
-    assert s.flow_rows == len(rec) and int(L.sum()) == len(t["values"])  # a partition of U
+    assert s.flow_rows == len(rec) and int(L.sum()) == len(f["values"])
+    cover = np.zeros(len(f["values"]), np.int64)
+    for tb, l in zip(rec[:, 0], L):
+        cover[tb:tb + l] += 1
+    assert np.all(cover == 1)  # a partition of U
     u = an.pattern.pattern
-    if merge:  # rows of <= 32 entries whole; longer ones: the diagonal-block slice + chunks of <= 32
-        assert s.flow_rows <= fin
-        assert int((np.diff(u.row_ptr) <= 32).sum()) <= s.flow_rows
-    else:
-        assert s.flow_rows == fin
-        assert np.array_equal(np.sort(t["flow_item"]), np.flatnonzero(t["row_rec"][:, 4] <= 1))
-    assert len(t["flow_upd"]) == len(t["upd"])  # every product folded in exactly once
-    assert s.flow_depth <= s.item_depth
-    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
-    assert bitwise_equal(replay_flow(t), ref)
-    # any order that respects "reads only written values" gives the same bits:
-    # matrix-row order is one
-    assert bitwise_equal(replay_flow(t, np.lexsort(((rec[:, 1] >> 30) & 1, rec[:, 3]))), ref)
+    lens = np.diff(u.row_ptr)
+    assert int((lens <= 32).sum()) <= s.flow_rows
+    assert np.array_equal(np.sort(f["flow_item"]), np.arange(len(rec)))
+    assert list(s.tasks) == golden[name]["dag"]["tasks"]  # counted without the DAG walk
+    ref, _, _, _ = oracle.factor_serial(an.a_permuted, u)
+    assert bitwise_equal(replay_lean(plan), ref)
+    assert bitwise_equal(replay_lean(plan, np.argsort(f["flow_item"])), ref)
 
 
-LOCAL = 0x80000000
-
-
-def replay_units(t):
-    """Mode 6 on the CPU: units and rows in the joint schedule order; a unit
-    runs its rows level by level with its own values in a local array
-    (operands flagged LOCAL), everything else reads the global factor."""
-    rows, rows_item = t["m6_row_rec"], t["m6_row_item"]
-    units, urec, ulb, ulev = t["m6_unit_rec"], t["m6_urow_rec"], t["m6_urow_lbase"], t["m6_ulev"]
-    slot, upd = t["m6_slot"], t["m6_upd"]
-    a = t["values"]
-    out = np.full(len(a), np.nan)
-    done = np.zeros(len(a), bool)
-    m6_node = t["m6_row_node"] if "m6_row_node" in t else None
-
-    def run_row(rec, local=None, lb=None):
-        tb, lk, dpos, _ = rec
-        L, kind = lk & ((1 << 30) - 1), (lk >> 30) & 3
-        v = a[tb:tb + L].copy()
-        for j in range(L):
-            ub, ue = slot[tb + j, :2]
-            for m, o in upd[ub:ue]:
-                vals = []
-                for x in (int(m) & 0xFFFFFFFF, int(o) & 0xFFFFFFFF):
-                    if x & LOCAL:
-                        assert local is not None and not np.isnan(local[x & ~LOCAL]), "local read before written"
-                        vals.append(local[x & ~LOCAL])
-                    else:
-                        assert done[x], "read before written"
-                        vals.append(out[x])
-                v[j] = v[j] - vals[0] * vals[1]
-        if kind == 0:
-            d = np.sqrt(v[0])
-            v[1:] = v[1:] / d
-            v[0] = d
-        else:
-            assert done[dpos]
-            v = v / out[dpos]
-        assert not done[tb:tb + L].any(), "written twice"
-        out[tb:tb + L] = v
-        done[tb:tb + L] = True
-        if local is not None:
-            local[lb:lb + L] = v
-
-    # joint order: unit k sits at order position units[k, 3]; rows fill the rest in order
-    nodes = len(rows) + len(units)
-    unit_at = {int(u[3]): k for k, u in enumerate(units)}
-    r = 0
-    for pos in range(nodes):
-        if pos in unit_at:
-            lb, le, rb, _ = units[unit_at[pos]]
-            n_local = 0
-            start = rb
-            bounds = []
-            for s in range(lb, le):
-                bounds.append((start, ulev[s]))
-                start = ulev[s]
-            for b0, b1 in bounds:
-                for q in range(b0, b1):
-                    n_local = max(n_local, ulb[q] + (urec[q, 1] & ((1 << 30) - 1)))
-            local = np.full(n_local, np.nan)
-            for b0, b1 in bounds:
-                # rows of one level are independent: run them in reverse to prove it
-                for q in reversed(range(b0, b1)):
-                    run_row(urec[q], local, ulb[q])
-        else:
-            run_row(rows[r])
-            r += 1
-    assert r == len(rows) and done.all()
-    return out
-
-
-@pytest.mark.parametrize("name,min_rows,merge", [("c5_m0", 64, 0), ("c5_m0", 16, 0), ("grid20_k2_leaf4", 8, 0),
-                                                 ("elast6_k1", 32, 0), ("rand_spd_200", 4, 0),
-                                                 # merged rows: units only where a block's rows are all
-                                                 # diagonal-block slices; long rows' chunks share an item
-                                                 ("s27_16_k2", 16, 1), ("elast6_k1", 16, 1)])
-def test_unit_schedule_replays_bitwise(T, name, min_rows, merge, oracle, monkeypatch):
-    monkeypatch.setenv("TCG_UNIT_MIN_ROWS", str(min_rows))
-    monkeypatch.setenv("TCG_FLOW_MERGE_ROWS", str(merge))
-    _, an = analyzed(name)
-    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+@pytest.mark.parametrize("name", ["c1", "rand_spd_200", "elast6_k1"])
+def test_flow_programs_equal_the_task_dag_merges(T, name):
+    # the per-coordinate programs (restated from the device builder) hold the
+    # same products, in the same order, as the task-DAG plan's per-item
+    # programs taken in generation order: the reference's kernels'
+    # pattern-restricted merges (kernels.hpp:55-65, 85-89, 104-108, 125-129)
+    plan = planned(name)
+    f = plan.flow_tables()
+    slot, upd = flow_programs(f["row_ptr"], f["cols"])
     t = plan.tables()
-    s = plan.stats()
-    if merge and s.unit_count == 0:
-        pytest.skip("every large block has merged whole rows")
-    assert s.unit_count == len(t["m6_unit_rec"]) > 0
-    assert len(t["m6_row_rec"]) + s.unit_rows == s.flow_rows
-    assert sorted(np.concatenate([t["m6_row_item"], t["m6_urow_item"]])) == sorted(t["flow_item"])
-    assert t["m6_smem"] <= 72 * 1024
-    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
-    assert bitwise_equal(replay_units(t), ref)
+    per = [[] for _ in range(len(f["cols"]))]
+    for rec in t["task"]:
+        for it in range(rec[2], rec[3]):
+            tb, te, _, _, _, _, soff, _ = t["item"][it]
+            for k in range(te - tb):
+                ub, ue = t["slot_rec"][soff + k, :2]
+                per[tb + k].extend(map(tuple, t["upd"][ub:ue]))
+    flat = [mo for p in per for mo in p]
+    assert len(flat) == len(upd)
+    assert np.array_equal(np.array(flat, np.int32).reshape(-1, 2), upd)
 
 
 def part_tables(p):
+    """The schedule rows of one part (tcg_plan_part_problem)."""
     from paper_1601_05871_b200.core import _copy
-    n = int(p.nflow)
-    return {"rec": _copy(p.flow_rec, 4 * n, np.int32).reshape(-1, 4), "item": _copy(p.flow_item, n, np.int32),
-            "slot": _copy(p.flow_slot, 4 * p.nnz, np.int32).reshape(-1, 4),
-            "upd": _copy(p.flow_upd, 2 * p.nflow_upd, np.int32).reshape(-1, 2)}
+    return {"rec": _copy(p.flow_rec, 4 * p.nflow, np.int32).reshape(-1, 4),
+            "unit": _copy(p.flow_item, p.nflow, np.int32)}
 
 
-def replay_parts(t, parts, owners):
+def part_programs(slot, upd, rowid, owners, part):
+    """The device rewrite of a part's programs (flow_program.cu): operands in
+    rows another part owns become 0x80000000 | owner << 25 | position."""
+    s, u = slot.copy(), upd.astype(np.int64).copy()
+    for x in range(len(slot)):
+        if owners[rowid[x]] != part:
+            continue
+        for e in range(slot[x, 0], slot[x, 1]):
+            ow = owners[rowid[u[e, 0]]]
+            if ow != part:
+                u[e] |= 0x80000000 | (int(ow) << 25)
+        if slot[x, 0] < slot[x, 1]:
+            s[x, 2:] = u[slot[x, 0]]
+    return s, u
+
+
+def replay_parts(f, slot, upd, parts, owners):
     """Sharded value flow on the CPU: every part's rows in the global order,
     each part with its own copy of U, remote operands read from their owner's
     copy. Returns (assembled factor, remote operand count, rows read remotely,
     rows flagged exported)."""
     total = len(parts)
-    pos_of_item = {int(it): q for q, it in enumerate(t["flow_item"])}
-    order = sorted((pos_of_item[int(it)], k, i) for k, p in enumerate(parts) for i, it in enumerate(p["item"]))
-    a = t["values"]
+    pos_of_unit = {int(g): q for q, g in enumerate(f["flow_item"])}
+    order = sorted((pos_of_unit[int(g)], k, i) for k, p in enumerate(parts) for i, g in enumerate(p["unit"]))
+    a = f["values"]
+    rowid = np.repeat(np.arange(len(f["row_ptr"]) - 1), np.diff(f["row_ptr"]))
+    progs = [part_programs(slot, upd, rowid, owners, k) for k in range(total)]
     out = [np.full(len(a), np.nan) for _ in range(total)]
     done = [np.zeros(len(a), bool) for _ in range(total)]
     remote = 0
     exported, read_remotely = set(), set()
-    row_start = {}  # U position -> (part, first position of its row slice)
-    for k, p in enumerate(parts):
-        for tb, lk, _, _ in p["rec"]:
-            for x in range(tb, tb + (lk & ((1 << 30) - 1))):
-                row_start[x] = (k, int(tb))
     for _, k, i in order:
-        tb, lk, dpos, trow = parts[k]["rec"][i]
+        tb, lk, dpos, trow = (int(x) for x in parts[k]["rec"][i])
         assert owners[trow] == k
         L, kind = lk & ((1 << 30) - 1), (lk >> 30) & 1
         if lk < 0:
-            exported.add((k, int(tb)))
+            exported.add((k, trow))
         v = a[tb:tb + L].copy()
+        ps, pu = progs[k]
         for j in range(L):
-            ub, ue = parts[k]["slot"][tb + j, :2]
-            for m, o in parts[k]["upd"][ub:ue]:
+            ub, ue = ps[tb + j, :2]
+            for m, o in pu[ub:ue]:
                 vals = []
-                for x in (int(m) & 0xFFFFFFFF, int(o) & 0xFFFFFFFF):
+                for x in (int(m), int(o)):
                     if x & 0x80000000:
                         ow, pos = (x >> 25) & 63, x & 0x1FFFFFF
                         assert ow != k
                         remote += 1
-                        read_remotely.add(row_start[pos])
+                        read_remotely.add((ow, int(rowid[pos])))
                     else:
                         ow, pos = k, x
                     assert done[ow][pos], "read before written"
@@ -392,10 +271,15 @@ def test_sharded_parts_replay_bitwise(T, name, nparts, extra, oracle):
     plan = planned(name)
     owners = an.subtree_owners(nparts, separators=nparts if extra else 0)
     total = nparts + (1 if extra else 0)
-    parts = [part_tables(plan.part_problem(total, owners, k)) for k in range(total)]
-    t = plan.tables()
-    assert sum(len(p["item"]) for p in parts) == len(t["flow_item"])
-    full, remote, read_remotely, exported = replay_parts(t, parts, owners)
+    parts = []
+    for k in range(total):
+        p = plan.part_problem(total, owners, k)
+        assert p.flow_devprog == 1 and p.flow_part == k
+        parts.append(part_tables(p))
+    f = plan.flow_tables()
+    assert sum(len(p["unit"]) for p in parts) == len(f["flow_item"])
+    slot, upd = flow_programs(f["row_ptr"], f["cols"])
+    full, remote, read_remotely, exported = replay_parts(f, slot, upd, parts, owners)
     ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
     assert bitwise_equal(full, ref)
     assert remote > 0
@@ -406,7 +290,7 @@ def test_sharded_parts_replay_bitwise(T, name, nparts, extra, oracle):
 def test_init_factor_map_reproduces_host_init(name):
     # device init_factor_values (tcg_set_a_values) is a gather through this map
     _, an = analyzed(name)
-    t = planned(name).tables()
+    t = planned(name).flow_tables()
     m = t["a_map"]
     assert len(m) == len(t["values"])
     got = np.where(m >= 0, 0.0 + an.a_permuted.values[np.maximum(m, 0)], 0.0)
