@@ -1332,10 +1332,6 @@ tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {
     TCG_CUDA_TRY(c, cudaFree(c->batch_arena));
     c->batch_arena = nullptr;
   }
-  if (c->prog_arena) {
-    TCG_CUDA_TRY(c, cudaFree(c->prog_arena));
-    c->prog_arena = nullptr;
-  }
   c->nbatch = 1;
   c->drain_ms[0] = c->drain_ms[1] = -1.f;
   c->drain_calls = 0;

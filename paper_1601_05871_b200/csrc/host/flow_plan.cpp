@@ -254,30 +254,53 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
     // reads U(t,t), its row's Chol unit. Every dependence points to a lower
     // row (or the row's own Chol unit), so both sweeps below run in row
     // order, pushing along the entries of U's rows (no transposed index).
-    std::vector<std::int32_t> level(U, 1), height(U, 1);
-    // each (dependence v of row r, dependent g of row t) pair of the source entry q
-    auto each_pair = [&](index_t r, std::int32_t q, auto&& fn) {
-      const index_t t = cols[q];
-      std::int32_t v0 = ufirst[r];
-      while (v0 + 1 < ufirst[r + 1] && u_tb[v0 + 1] <= q) ++v0;
-      for (std::int32_t g = ufirst[t]; g < ufirst[t + 1]; ++g) {
-        fn(v0, g);
-        for (std::int32_t v = v0 + 1; v < ufirst[r + 1] && u_c0[v] <= u_c1[g]; ++v) fn(v, g);
-      }
-    };
+    // Both sweeps keep, per source entry, a pointer to the unit of row r
+    // holding it (it only advances along the row) and walk the units of
+    // row t once, the last dependence vmax(g) growing with g's last column.
+    std::vector<std::int32_t> level(U, 1), height(U, 1), vmax;
     std::int32_t depth = 0;
     for (index_t r = 0; r < n; ++r) {
-      const std::int32_t chol = ufirst[r];
-      for (std::int32_t g = chol + 1; g < ufirst[r + 1]; ++g) level[g] = std::max(level[g], level[chol] + 1);
-      for (std::int32_t g = chol; g < ufirst[r + 1]; ++g) depth = std::max(depth, level[g]);
-      for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q)
-        each_pair(r, q, [&](std::int32_t v, std::int32_t g) { level[g] = std::max(level[g], level[v] + 1); });
+      const std::int32_t vr0 = ufirst[r], vr1 = ufirst[r + 1];
+      for (std::int32_t g = vr0 + 1; g < vr1; ++g) level[g] = std::max(level[g], level[vr0] + 1);
+      for (std::int32_t g = vr0; g < vr1; ++g) depth = std::max(depth, level[g]);
+      std::int32_t v0 = vr0;
+      for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q) {
+        while (v0 + 1 < vr1 && u_tb[v0 + 1] <= q) ++v0;
+        const index_t t = cols[q];
+        std::int32_t v = v0, lv = level[v0];
+        for (std::int32_t g = ufirst[t]; g < ufirst[t + 1]; ++g) {
+          while (v + 1 < vr1 && u_c0[v + 1] <= u_c1[g]) lv = std::max(lv, level[++v]);
+          level[g] = std::max(level[g], lv + 1);
+        }
+      }
     }
     for (index_t r = n; r-- > 0;) {
-      for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q)
-        each_pair(r, q, [&](std::int32_t v, std::int32_t g) { height[v] = std::max(height[v], height[g] + 1); });
-      const std::int32_t chol = ufirst[r];
-      for (std::int32_t g = chol + 1; g < ufirst[r + 1]; ++g) height[chol] = std::max(height[chol], height[g] + 1);
+      const std::int32_t vr0 = ufirst[r], vr1 = ufirst[r + 1];
+      std::int32_t v0 = vr0;
+      for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q) {
+        while (v0 + 1 < vr1 && u_tb[v0 + 1] <= q) ++v0;
+        const index_t t = cols[q];
+        const std::int32_t g0 = ufirst[t], g1 = ufirst[t + 1];
+        if (vr1 - vr0 == 1) {  // one unit: every dependent of the entry reads it
+          std::int32_t hm = 0;
+          for (std::int32_t g = g0; g < g1; ++g) hm = std::max(hm, height[g] + 1);
+          height[v0] = std::max(height[v0], hm);
+          continue;
+        }
+        vmax.resize(static_cast<std::size_t>(g1 - g0));
+        for (std::int32_t g = g0, v = v0; g < g1; ++g) {
+          while (v + 1 < vr1 && u_c0[v + 1] <= u_c1[g]) ++v;
+          vmax[g - g0] = v;
+        }
+        // unit v of row r is read by the dependents g with vmax(g) >= v
+        std::int32_t hm = 0;
+        for (std::int32_t g = g1; g-- > g0;) {
+          hm = std::max(hm, height[g] + 1);
+          const std::int32_t lo = g > g0 ? vmax[g - 1 - g0] + 1 : v0;
+          for (std::int32_t v = lo; v <= vmax[g - g0]; ++v) height[v] = std::max(height[v], hm);
+        }
+      }
+      for (std::int32_t g = vr0 + 1; g < vr1; ++g) height[vr0] = std::max(height[vr0], height[g] + 1);
     }
     mark("levels");
     // schedule: level ascending, height descending, unit id ascending (two

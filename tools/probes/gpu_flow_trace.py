@@ -8,7 +8,7 @@ import sys
 
 import numpy as np
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 import paper_1601_05871_b200 as T  # noqa: E402
 
@@ -21,9 +21,10 @@ fz.factor()
 fz.restore()
 st = fz.factor()
 _, items = fz.trace()
+slot, upd, _ = fz.flow_programs()
 fz.close()
-t = plan.tables()
-rec, order, slot, upd = t["flow_rec"], t["flow_item"], t["flow_slot"], t["flow_upd"]
+t = plan.flow_tables()
+rec, order = t["flow_rec"], t["flow_item"]
 stamps = items[order].astype(np.int64)  # per schedule position: start, operands final, -, end
 t0 = stamps[:, 0].min()
 s, r, e = stamps[:, 0] - t0, stamps[:, 1] - t0, stamps[:, 3] - t0
@@ -77,3 +78,24 @@ for k in acc:
     print(f"  {k:48s} {acc[k] / 1e3:8.1f} us  ({n[k]} steps)")
 if len(sys.argv) > 2:
     np.savez_compressed(sys.argv[2], s=s, r=r, e=e, ready=ready, src=src_of, kind=kind, L=L, W=W)
+# the critical path row by row (the last 40 steps): length, products per
+# coordinate (max), and where its time went
+q = int(np.argmax(e))
+path = []
+while q >= 0 and len(path) < 100000:
+    path.append(q)
+    if src_of[q] >= 0 and ready[q] > s[q]:
+        q = src_of[q]
+    elif prev[q] >= 0 and e[prev[q]] <= s[q] + 2000:
+        q = prev[q]
+    else:
+        break
+print(f"critical path: {len(path)} rows")
+prods = np.diff(slot[:, :2], axis=1).ravel()
+for q in path[:40][::-1]:
+    tb = rec[q, 0]
+    pm = int(prods[tb:tb + L[q]].max()) if L[q] else 0
+    ps = int(prods[tb:tb + L[q]].sum())
+    print(f"  pos {q:7d} t={rec[q, 3]:7d} kind={kind[q]} L={L[q]:3d} prod max/sum {pm:4d}/{ps:6d} "
+          f"start->final {(r[q] - s[q]) / 1e3:6.2f} final->end {(e[q] - r[q]) / 1e3:6.2f} "
+          f"ready-start {(ready[q] - s[q]) / 1e3:7.2f} us")
