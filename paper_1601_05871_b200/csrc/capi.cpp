@@ -805,7 +805,11 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // the 5-CTA kernel exists for one local matrix (with or without the drain)
   if (minb == 5 && (remote || extras || !pipe || kb > 2)) minb = 3;
   int occ = 0;
-  if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0) != cudaSuccess) {
+  // poll back-off for long programs (flow_kernel.cu Ctx): thousands of lanes
+  // poll the lines the critical rows write; sleeping between polls frees them
+  int backoff = kb >= 3 ? 200 : 0;
+  if (const char* e = std::getenv("TCG_FLOW_BACKOFF")) backoff = std::atoi(e);
+  if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0, backoff) != cudaSuccess) {
     cudaGetLastError();
     pipe = false;
     drain = false;
@@ -855,6 +859,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   P.vals = vals;
   P.ctrl = c->ctrl;
   P.trace = c->opt.trace ? c->trace + 2 * c->ntab : nullptr;
+
   P.m_failed = q.m_failed;
   P.m_row = q.m_row;
   P.m_pivot = q.m_pivot;
@@ -900,7 +905,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (c->nflow > 0) {
     if (pipe)
       TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, extras, c->stream,
-                                               drain ? 1 : 0));
+                                               drain ? 1 : 0, backoff));
     else TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
   }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
@@ -1159,8 +1164,10 @@ static tcg_status run_flow_chunked(tcg_ctx* c, tcg_stats& S, int threads, const 
   const double mean = c->nnz > 0 ? static_cast<double>(c->nflow_upd) / static_cast<double>(c->nnz) : 0.0;
   // 4 CTAs per SM: a fifth made the batch kernel slower (C5 x 64: 1.81 -> 1.95 ms)
   const int kb = mean <= 4.0 ? 2 : 3, minb = 3;
+  int backoff = kb >= 3 ? 200 : 0;
+  if (const char* e = std::getenv("TCG_FLOW_BACKOFF")) backoff = std::atoi(e);
   int occ = 0;
-  TCG_CUDA_TRY(c, tcbdev::pipe_occupancy(threads, kb, minb, 0, 1, &occ, 0));
+  TCG_CUDA_TRY(c, tcbdev::pipe_occupancy(threads, kb, minb, 0, 1, &occ, 0, backoff));
   if (occ < 1) {
     c->err = "value-flow kernel does not fit on an SM";
     return TCG_INVALID;
@@ -1226,7 +1233,7 @@ static tcg_status run_flow_chunked(tcg_ctx* c, tcg_stats& S, int threads, const 
     P.nrows = static_cast<int>(c->nflow);
     P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
     P.row_ctas = grid;
-    TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, 0, 1, c->stream, 0));
+    TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, 0, 1, c->stream, 0, backoff));
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrls + k, c->ctrl, sizeof(tcbdev::Ctrl), cudaMemcpyDeviceToHost,
                                     c->stream));
     TCG_CUDA_TRY(c, cudaEventRecord(done, c->stream));

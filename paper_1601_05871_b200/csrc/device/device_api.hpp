@@ -23,9 +23,9 @@ cudaError_t launch_flow(const FlowParams& p, int grid, int threads, int kb, int 
                         int weak, int dyn, int remote, cudaStream_t st);
 
 cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm,
-                           int drain = 0);
+                           int drain = 0, int backoff_ns = 0);
 cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb, int minb, int remote,
-                             int extras, cudaStream_t st, int drain = 0);
+                             int extras, cudaStream_t st, int drain = 0, int backoff_ns = 0);
 cudaError_t launch_init_values(const double* a, const int* map, double* vals, double* vals0, long long nnz,
                                long long nnz_a, int nbatch, int sm_count, cudaStream_t st);
 

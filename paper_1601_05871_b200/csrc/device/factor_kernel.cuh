@@ -90,7 +90,7 @@ struct FlowParams {
   int nrows;             // schedule rows (per member)
   int nbatch;            // members sharing the pattern
   double* const* peers;  // sharded (C6): every part's U, indexed by part; operands of other parts
-  int npeers;            //   arrive as kRemoteBit | part << 25 | position (plan.hpp build_flow_part)
+  int npeers;            //   arrive as kRemoteBit | part << 25 | position (flow_plan.hpp build_flow_part)
   unsigned long long timeout_ns;
   // drain (end to end, factor_flow_pipe DRAIN = 1): CTAs [row_ctas, grid) copy
   // final values to the host while the rows run

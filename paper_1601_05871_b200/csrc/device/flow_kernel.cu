@@ -31,6 +31,8 @@ namespace {
 constexpr unsigned long long kCanonicalNaN = 0x7FFFFFFFFFFFFFFFull;
 
 // Slow path of a gather: the value is not written yet.
+// BO: nanoseconds a lane sleeps between re-polls (0: none)
+template <int BO = 0>
 __device__ __forceinline__ unsigned long long wait_value(const double* p, Ctrl* ctrl,
                                                       unsigned long long t0,
                                                       unsigned long long tmo) {
@@ -38,6 +40,7 @@ __device__ __forceinline__ unsigned long long wait_value(const double* p, Ctrl* 
   for (;;) {
     const unsigned long long x = ld_relaxed_u64(p);
     if (x != kUnset) return x;
+    if (BO) __nanosleep(BO);
     if (++spins == 1024u) {
       spins = 0;
       if (ld_relaxed(&ctrl->error.v) || gtimer() - t0 > tmo) {
@@ -75,7 +78,12 @@ __device__ __forceinline__ unsigned long long wait_value_sys(const double* p, Ct
 // are nnz apart; the pattern, records and programs are shared).
 // OPS: how a negative operand position is read. 0: never happens; 2
 // (sharded runs): kRemoteBit | part << 25 | position in that part's U.
-template <int WEAK, int OPS = 0>
+// BO: poll back-off in ns (a lane sleeps between re-polls of a value not yet
+// written). Long programs keep thousands of lanes polling the few lines the
+// critical rows are about to write; sleeping between polls frees the L2
+// slices serving them (B200, C3: 4.33 -> 3.45 ms at 300 ns, C4 1.61 -> 1.48
+// at 100 ns; short programs lose: C2 0.41 -> 0.42-0.45 ms).
+template <int WEAK, int OPS = 0, int BO = 0>
 struct Ctx {
   const FlowParams& P;
   unsigned long long t0;
@@ -83,7 +91,7 @@ struct Ctx {
   const double* a;
   int member;
   __device__ __forceinline__ double settle(const double* p, unsigned long long x) const {
-    if (x == kUnset) x = wait_value(p, P.ctrl, t0, P.timeout_ns);
+    if (x == kUnset) x = wait_value<BO>(p, P.ctrl, t0, P.timeout_ns);
     return __longlong_as_double(static_cast<long long>(x));
   }
   // sharded runs (P.peers): a negative position names another part's value
@@ -104,7 +112,7 @@ struct Ctx {
   __device__ __forceinline__ double settle_at(int pos, unsigned long long x) const {
     if (x == kUnset) {
       if (OPS == 2 && pos < 0) x = wait_value_sys(remote(pos), P.ctrl, t0, P.timeout_ns);
-      else x = wait_value(vals + pos, P.ctrl, t0, P.timeout_ns);
+      else x = wait_value<BO>(vals + pos, P.ctrl, t0, P.timeout_ns);
     }
     return __longlong_as_double(static_cast<long long>(x));
   }
@@ -117,6 +125,7 @@ struct Ctx {
       do {
         if (xa == kUnset) xa = ld_strong(pa);
         if (xb == kUnset) xb = ld_strong(pb);
+        if (BO) __nanosleep(BO);
         if (++spins == 1024u) {
           spins = 0;
           if (ld_relaxed(&P.ctrl->error.v) || gtimer() - t0 > P.timeout_ns) {
@@ -449,7 +458,7 @@ __device__ void drain_values(const FlowParams& P, int dw, int DW) {
 // (G = 32, static hand-out.)
 // EXTRAS = 0: a single matrix without trace stamps (no batch member
 // arithmetic, no stamp branches); 1: batches and traces.
-template <int THREADS, int KB, int MINB, int REMOTE, int EXTRAS, int DRAIN = 0>
+template <int THREADS, int KB, int MINB, int REMOTE, int EXTRAS, int DRAIN = 0, int BO = 0>
 __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) {
   constexpr int kWarps = THREADS / 32;
   constexpr int kLenMask = (1 << 30) - 1;
@@ -468,7 +477,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
   }
   const int W = (DRAIN ? P.row_ctas : static_cast<int>(gridDim.x)) * kWarps;
   const int w0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  Ctx<0, REMOTE ? 2 : 0> C{P, gtimer(), P.vals, P.a, 0};
+  Ctx<0, REMOTE ? 2 : 0, BO> C{P, gtimer(), P.vals, P.a, 0};
   int ran = 0, executed = 0, anyfail = 0;
   const int nrows = EXTRAS ? P.nrows * P.nbatch : P.nrows;
   auto member_of = [&](int p, int& q) {
@@ -675,35 +684,46 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
   return cudaGetLastError();
 }
 
-// (threads, KB, CTAs/SM, remote operands, extras, drain)
-#define TCG_PIPE_VARIANTS(X)                                                                               \
-  X(256, 2, 3, 0, 0, 0) X(256, 3, 3, 0, 0, 0) X(256, 4, 3, 0, 0, 0) X(256, 2, 3, 0, 1, 0) X(256, 3, 3, 0, 1, 0) \
-  X(256, 4, 3, 0, 1, 0) X(256, 2, 3, 1, 1, 0) X(256, 3, 3, 1, 1, 0) X(256, 4, 3, 1, 1, 0)                     \
-  X(256, 2, 3, 0, 0, 1) X(256, 3, 3, 0, 0, 1) X(256, 4, 3, 0, 0, 1)                                         \
-  X(256, 2, 3, 0, 1, 1) X(256, 3, 3, 0, 1, 1) X(256, 4, 3, 0, 1, 1)                                         \
-  X(256, 2, 5, 0, 0, 0) X(256, 2, 5, 0, 0, 1) X(256, 1, 5, 0, 0, 0) X(256, 1, 5, 0, 0, 1)
+// (threads, KB, CTAs/SM, remote operands, extras, drain, poll back-off ns)
+#define TCG_PIPE_VARIANTS(X)                                                                                  \
+  X(256, 2, 3, 0, 0, 0, 0) X(256, 3, 3, 0, 0, 0, 0) X(256, 4, 3, 0, 0, 0, 0) X(256, 2, 3, 0, 1, 0, 0)             \
+  X(256, 3, 3, 0, 1, 0, 0) X(256, 4, 3, 0, 1, 0, 0) X(256, 2, 3, 1, 1, 0, 0) X(256, 3, 3, 1, 1, 0, 0)             \
+  X(256, 4, 3, 1, 1, 0, 0) X(256, 2, 3, 0, 0, 1, 0) X(256, 3, 3, 0, 0, 1, 0) X(256, 4, 3, 0, 0, 1, 0)             \
+  X(256, 2, 3, 0, 1, 1, 0) X(256, 3, 3, 0, 1, 1, 0) X(256, 4, 3, 0, 1, 1, 0)                                     \
+  X(256, 2, 5, 0, 0, 0, 0) X(256, 2, 5, 0, 0, 1, 0) X(256, 1, 5, 0, 0, 0, 0) X(256, 1, 5, 0, 0, 1, 0)             \
+  X(256, 3, 3, 0, 0, 0, 100) X(256, 3, 3, 0, 0, 0, 200) X(256, 3, 3, 0, 0, 0, 400)                              \
+  X(256, 3, 3, 0, 0, 1, 200) X(256, 3, 3, 0, 1, 0, 200) X(256, 3, 3, 0, 1, 1, 200) X(256, 3, 3, 1, 1, 0, 200)     \
+  X(256, 4, 3, 0, 0, 0, 200) X(256, 2, 3, 0, 0, 0, 200) X(256, 2, 3, 0, 1, 0, 200)
 
-static const void* pipe_kernel_for(int threads, int kb, int minb, int remote, int extras, int drain) {
-#define X(T, K, M, R, E, D)                                                                 \
-  if (threads == T && kb == K && minb == M && remote == R && extras == E && drain == D)     \
-    return reinterpret_cast<const void*>(&factor_flow_pipe<T, K, M, R, E, D>);
+static const void* pipe_kernel_for(int threads, int kb, int minb, int remote, int extras, int drain, int bo) {
+#define X(T, K, M, R, E, D, B)                                                                              \
+  if (threads == T && kb == K && minb == M && remote == R && extras == E && drain == D && bo == B)          \
+    return reinterpret_cast<const void*>(&factor_flow_pipe<T, K, M, R, E, D, B>);
   TCG_PIPE_VARIANTS(X)
 #undef X
   return nullptr;
 }
 
-cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm, int drain) {
-  const void* k = pipe_kernel_for(threads, kb, minb, remote, extras, drain);
+// the back-off variant when it exists, else the one without
+static int pipe_backoff(int threads, int kb, int minb, int remote, int extras, int drain, int bo) {
+  return pipe_kernel_for(threads, kb, minb, remote, extras, drain, bo) ? bo : 0;
+}
+
+cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm, int drain,
+                           int bo) {
+  bo = pipe_backoff(threads, kb, minb, remote, extras, drain, bo);
+  const void* k = pipe_kernel_for(threads, kb, minb, remote, extras, drain, bo);
   if (!k) return cudaErrorInvalidValue;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
 }
 
 cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb, int minb, int remote,
-                             int extras, cudaStream_t st, int drain) {
-#define X(T, K, M, R, E, D)                                                                   \
-  if (threads == T && kb == K && minb == M && remote == R && extras == E && drain == D) {     \
-    factor_flow_pipe<T, K, M, R, E, D><<<grid, T, 0, st>>>(p);                                \
-    return cudaGetLastError();                                                                \
+                             int extras, cudaStream_t st, int drain, int bo) {
+  bo = pipe_backoff(threads, kb, minb, remote, extras, drain, bo);
+#define X(T, K, M, R, E, D, B)                                                                              \
+  if (threads == T && kb == K && minb == M && remote == R && extras == E && drain == D && bo == B) {        \
+    factor_flow_pipe<T, K, M, R, E, D, B><<<grid, T, 0, st>>>(p);                                           \
+    return cudaGetLastError();                                                                              \
   }
   TCG_PIPE_VARIANTS(X)
 #undef X

@@ -99,3 +99,23 @@ for q in path[:40][::-1]:
     print(f"  pos {q:7d} t={rec[q, 3]:7d} kind={kind[q]} L={L[q]:3d} prod max/sum {pm:4d}/{ps:6d} "
           f"start->final {(r[q] - s[q]) / 1e3:6.2f} final->end {(e[q] - r[q]) / 1e3:6.2f} "
           f"ready-start {(ready[q] - s[q]) / 1e3:7.2f} us")
+# post-hop work of the critical rows: per lane (coordinate), the products whose
+# operands were published in the last 5 us before the row's operands were
+# final ("late"), and how many products follow the first late one in the
+# lane's program (work that can only start after the hop)
+late_n, after_n = [], []
+for q in path[:60]:
+    tb = rec[q, 0]
+    for j in range(L[q]):
+        u0, u1 = slot[tb + j, :2]
+        if u1 <= u0:
+            continue
+        pr = upd[u0:u1]
+        oe = np.maximum(e[owner[pr[:, 0]]], e[owner[pr[:, 1]]])
+        late = oe > r[q] - 5000
+        late_n.append(int(late.sum()))
+        after_n.append(int(len(late) - np.argmax(late)) if late.any() else 0)
+if late_n:
+    print(f"critical rows, per coordinate: late products mean {np.mean(late_n):.1f} max {max(late_n)}; "
+          f"products from the first late one on: mean {np.mean(after_n):.1f} p90 {np.percentile(after_n, 90):.0f} "
+          f"max {max(after_n)}")
