@@ -105,6 +105,9 @@ FactorResultT factor_by_blocks_gpu(const Csr& a_permuted, const Fp& fp, const Ra
   tcg_status st = tcg_plan_build(&av, &uv, static_cast<int32_t>(bounds.empty() ? 0 : bounds.size() - 1),
                                  bounds.data(), &plan.p);
   if (st != TCG_OK) detail::raise(st, tcg_plan_error());
+  if (opt.mode == 1 || opt.mode == 2) {  // the task executors run the task-DAG plan's tables
+    if ((st = tcg_plan_expand(plan.p)) != TCG_OK) detail::raise(st, tcg_plan_error());
+  }
   const double plan_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   tcg_problem prob{};
   tcg_plan_problem(plan.p, &prob);
@@ -127,6 +130,7 @@ FactorResultT factor_by_blocks_gpu(const Csr& a_permuted, const Fp& fp, const Ra
 
   FactorResultT res{};
   res.factor = fp.pattern;  // fresh CSR with the pattern's arrays (factorize.hpp:139-140)
+  res.factor.values.assign(static_cast<std::size_t>(prob.nnz), 0.0);  // a pattern may carry no values
   if ((st = tcg_download(ctx.c, res.factor.values.data())) != TCG_OK)
     detail::raise(st, tcg_last_error(ctx.c));
   res.stats.block_build_seconds = plan_s;

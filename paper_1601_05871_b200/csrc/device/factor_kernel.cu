@@ -656,12 +656,11 @@ cudaError_t launch_prepare(const PrepParams& q, cudaStream_t st) {
 
 cudaError_t launch_factor(const Params& p, int grid, int threads, size_t smem, cudaStream_t st) {
   switch (threads) {
-    case 128: factor_persistent<128><<<grid, 128, smem, st>>>(p); break;
-    case 256: factor_persistent<256><<<grid, 256, smem, st>>>(p); break;
-    case 512: factor_persistent<512><<<grid, 512, smem, st>>>(p); break;
+    case 128: return launch_resident(reinterpret_cast<const void*>(&factor_persistent<128>), grid, 128, smem, st, p);
+    case 256: return launch_resident(reinterpret_cast<const void*>(&factor_persistent<256>), grid, 256, smem, st, p);
+    case 512: return launch_resident(reinterpret_cast<const void*>(&factor_persistent<512>), grid, 512, smem, st, p);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace tcbdev

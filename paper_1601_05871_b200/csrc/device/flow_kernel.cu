@@ -722,8 +722,8 @@ cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb,
   bo = pipe_backoff(threads, kb, minb, remote, extras, drain, bo);
 #define X(T, K, M, R, E, D, B)                                                                              \
   if (threads == T && kb == K && minb == M && remote == R && extras == E && drain == D && bo == B) {        \
-    factor_flow_pipe<T, K, M, R, E, D, B><<<grid, T, 0, st>>>(p);                                           \
-    return cudaGetLastError();                                                                              \
+    return launch_resident(reinterpret_cast<const void*>(&factor_flow_pipe<T, K, M, R, E, D, B>), grid, T, 0, \
+                           st, p);                                                                          \
   }
   TCG_PIPE_VARIANTS(X)
 #undef X
@@ -742,8 +742,8 @@ cudaError_t launch_flow(const FlowParams& p, int grid, int threads, int kb, int 
                         int weak, int dyn, int remote, cudaStream_t st) {
 #define X(T, K, M, GG, WK, D, R)                                                                   \
   if (threads == T && kb == K && minb == M && g == GG && weak == WK && dyn == D && remote == R) {  \
-    factor_flow<T, K, M, GG, WK, D, R><<<grid, T, 0, st>>>(p);                                     \
-    return cudaGetLastError();                                                                     \
+    return launch_resident(reinterpret_cast<const void*>(&factor_flow<T, K, M, GG, WK, D, R>), grid, T, 0, st, \
+                           p);                                                                             \
   }
   TCG_FLOW_VARIANTS(X)
 #undef X

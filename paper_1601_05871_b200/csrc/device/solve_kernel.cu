@@ -165,8 +165,7 @@ cudaError_t solve_occupancy(int* ctas_per_sm) {
 }
 
 cudaError_t launch_trisolve(const SolveParams& p, int grid, cudaStream_t st) {
-  trisolve_flow<kSolveThreads><<<grid, kSolveThreads, 0, st>>>(p);
-  return cudaGetLastError();
+  return launch_resident(reinterpret_cast<const void*>(&trisolve_flow<kSolveThreads>), grid, kSolveThreads, 0, st, p);
 }
 
 }  // namespace tcbdev

@@ -7,6 +7,28 @@ namespace tcbdev {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Launch of a persistent kernel whose CTAs wait on one another (spin on
+// values, counters or queues): a cooperative launch, so the runtime either
+// makes every CTA co-resident or fails at once (cudaErrorCooperativeLaunchTooLarge,
+// e.g. under MPS or beside another resident kernel) instead of leaving CTAs
+// unscheduled until the watchdog.
+template <class Params>
+inline cudaError_t launch_resident(const void* kernel, int grid, int block, size_t smem, cudaStream_t st,
+                                   const Params& p) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(static_cast<unsigned>(block));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {const_cast<Params*>(&p)};
+  return cudaLaunchKernelExC(&cfg, kernel, args);
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

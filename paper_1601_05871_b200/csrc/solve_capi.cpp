@@ -87,8 +87,9 @@ bool build_tables(const tcg_csr_view* u, Tables& T, std::string& err) {
       }
   }
   const std::int64_t noff = up[n] - n;
-  if (noff > 0x7fffffffLL || up[n] > 0x7fffffffLL) {
-    err = "tcg_solve_create: U beyond 2^31 entries";
+  // the backward records index a table of 2 * noff entries with int32 offsets
+  if (2 * noff > 0x7fffffffLL || up[n] > 0x7fffffffLL) {
+    err = "tcg_solve_create: U beyond 2^30 off-diagonal entries";
     return false;
   }
   // transposed index of the strict upper part

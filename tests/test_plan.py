@@ -14,8 +14,13 @@ from conftest import analyzed, bitwise_equal, planned
 FAST = ["c1", "c5_m0", "s27_16_k2", "grid20_k2_leaf4", "rand_spd_200", "elast6_k1"]
 
 
-@pytest.mark.parametrize("name", FAST + ["c2", "c3", "c4"])
+def an_perm(name):
+    return analyzed(name)[1].perm
+
+
+@pytest.mark.parametrize("name", FAST + ["c2", "c3", "c4", pytest.param("c6", marks=pytest.mark.slow)])
 def test_plan_dag_and_blocks_match_reference(name, golden, oracle):
+    # c6: 1,479,042 tasks and 3,003,864 edges, bit-exact with export_task_dag
     g = golden[name]
     plan = planned(name)
     d = plan.dag()
@@ -29,6 +34,7 @@ def test_plan_dag_and_blocks_match_reference(name, golden, oracle):
     assert oracle.hash(bc) == g["blocks"]["bcol_idx"]
     s = plan.stats()
     assert list(s.tasks) == g["dag"]["tasks"]
+    assert oracle.hash(an_perm(name)) == g["perm"]
 
 
 @pytest.mark.parametrize("name", ["c1", "elast6_k1", "grid20_k2_leaf4", "rand_spd_200"])
