@@ -23,7 +23,7 @@ HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generat
              $(SRC)/host/plan.cpp $(SRC)/host/flow_plan.cpp $(SRC)/capi.cpp $(SRC)/symbolic_capi.cpp $(SRC)/solve_capi.cpp
 HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
 DEV_OBJS := $(OBJ)/device/factor_kernel.o \
-            $(OBJ)/device/flow_kernel.o $(OBJ)/device/flow_program.o $(OBJ)/device/symbolic_kernel.o \
+            $(OBJ)/device/flow_kernel.o $(OBJ)/device/flow_pp_kernel.o $(OBJ)/device/flow_program.o $(OBJ)/device/symbolic_kernel.o \
             $(OBJ)/device/solve_kernel.o
 
 .PHONY: all lib oracle ref clean
@@ -54,7 +54,7 @@ clean:
 	rm -rf build $(OUT)/*.so
 	$(MAKE) -C oracle clean
 
-$(OBJ)/device/flow_kernel.o: $(SRC)/device/flow_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh
+$(OBJ)/device/flow_kernel.o: $(SRC)/device/flow_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/flow_common.cuh $(SRC)/device/sync.cuh
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_flow_kernel.txt || (cat build/ptxas_flow_kernel.txt; false)
 
@@ -69,3 +69,7 @@ $(OBJ)/device/solve_kernel.o: $(SRC)/device/solve_kernel.cu $(SRC)/device/solve_
 $(OBJ)/device/flow_program.o: $(SRC)/device/flow_program.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_flow_program.txt || (cat build/ptxas_flow_program.txt; false)
+
+$(OBJ)/device/flow_pp_kernel.o: $(SRC)/device/flow_pp_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/flow_common.cuh $(SRC)/device/sync.cuh $(SRC)/device/device_api.hpp
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_flow_pp_kernel.txt || (cat build/ptxas_flow_pp_kernel.txt; false)

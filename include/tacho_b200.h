@@ -153,6 +153,8 @@ typedef struct {
                                 launch (0: a D2H copy after it) */
   int32_t chunks;            /* end to end, batches: member chunks pipelined with the copies
                                 (0: one launch) */
+  int32_t row_kernel;        /* mode 5: 1 = one lane per coordinate (factor_flow_pipe / factor_flow),
+                                2 = product-parallel row groups (factor_flow_pp) */
 } tcg_stats;
 
 typedef struct {

@@ -103,6 +103,7 @@ class Stats(C.Structure):
         ("breakdown_member", C.c_int32),
         ("drain_ctas", C.c_int32),
         ("chunks", C.c_int32),
+        ("row_kernel", C.c_int32),
     ]
 
 

@@ -156,8 +156,10 @@ struct tcg_ctx {
   double* bm_pivot = nullptr;
   int4* flow_slot = nullptr;
   int2* flow_upd = nullptr;
+  int* flow_ub = nullptr;      // per coordinate: first product in flow_upd (nnz + 1), in prog_arena
   void* prog_arena = nullptr;  // device-built (m, o) pairs (their count is known after the count pass)
-  double prog_build_ms = 0.0;  // device time of the last program build
+  double prog_build_ms = 0.0;
+  int ub_total = 0;            // host source of flow_ub[nnz]  // device time of the last program build
   double* flow_a = nullptr;  // snapshot of the input values
   std::int64_t nflow = 0, nflow_upd = 0;
   bool has_flow = false;
@@ -515,8 +517,14 @@ static tcg_status build_programs(tcg_ctx* c, const tcg_problem* p) {
     c->err = "tcg_upload: more than 2^31 products in the update programs";
     return TCG_INVALID;
   }
-  TCG_CUDA_TRY(c, cudaMalloc(&c->prog_arena, sizeof(int2) * std::max<long long>(total, 1)));
+  // [(m, o) pairs][per-coordinate offsets, nnz + 1] (the offsets for the product-parallel rows)
+  const size_t upd_bytes = align_up(sizeof(int2) * std::max<long long>(total, 1), 256);
+  TCG_CUDA_TRY(c, cudaMalloc(&c->prog_arena, upd_bytes + sizeof(int) * (nnz + 1)));
   c->flow_upd = static_cast<int2*>(c->prog_arena);
+  c->flow_ub = reinterpret_cast<int*>(static_cast<char*>(c->prog_arena) + upd_bytes);
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->flow_ub, ub32, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, c->stream));
+  c->ub_total = static_cast<int>(total);
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(c->flow_ub + nnz, &c->ub_total, sizeof(int), cudaMemcpyHostToDevice, c->stream));
   q.upd = c->flow_upd;
   TCG_CUDA_TRY(c, tcbdev::flow_program_fill(q, c->sm_count, c->stream));
   if (p->flow_part >= 0) {  // a part: operands of other parts' rows through the peer table
@@ -730,6 +738,32 @@ tcg_status tcg_restore(tcg_ctx* c) {
   return TCG_OK;
 }
 
+// Product-parallel rows (flow_pp_kernel.cu) where programs are short (mean
+// products per coordinate <= 4: C1, C2, C5, C6): a row's products spread over
+// a group of wpr warps, nb batches of kp per thread and chunk. One warp per
+// row for large schedules, two for small ones (B200: C1 0.044 -> 0.040, C2
+// 0.395 -> 0.364, C5 0.168 -> 0.134, C6 1.725 -> 1.424, the C5 batch 1.816 ->
+// 1.412 ms). Long programs (C3, C4) stay on the per-lane kernel.
+// TCG_FLOW_PP=0 turns it off; TCG_FLOW_PP=wpr,kp,nb,minb,d[,backoff] picks a variant.
+static bool pick_pp(const tcg_ctx* c, double mean, int* w, int* k, int* n, int* m, int* d, int* b) {
+  if (!c->flow_ub) return false;
+  if (c->opt.threads_per_cta != 0 && c->opt.threads_per_cta != 256) return false;  // 256-thread CTAs only
+  if (const char* e = std::getenv("TCG_FLOW_PP")) {
+    *b = -1;
+    const int got = std::sscanf(e, "%d,%d,%d,%d,%d,%d", w, k, n, m, d, b);
+    return got >= 5 && *w > 0;
+  }
+  if (mean > 4.0) return false;
+  const long long positions = c->nflow * c->nbatch;
+  if (positions <= 200000) {
+    *w = 2, *k = 2, *n = 2, *m = 3, *d = 1;
+  } else {
+    *w = 1, *k = 2, *n = 1, *m = 4, *d = 2;
+  }
+  *b = 0;
+  return true;
+}
+
 // Value-flow execution (mode 5, flow_kernel.cu): prelude (snapshot the
 // input, mark the output unwritten, reset the status words) + one persistent
 // launch; both inside the timed region.
@@ -809,12 +843,29 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // poll the lines the critical rows write; sleeping between polls frees them
   int backoff = kb >= 3 ? 200 : 0;
   if (const char* e = std::getenv("TCG_FLOW_BACKOFF")) backoff = std::atoi(e);
-  if (pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0, backoff) != cudaSuccess) {
+  int pp_w = 0, pp_k = 0, pp_n = 0, pp_m = 0, pp_d = 0, pp_b = -1;
+  bool pp = !remote && !c->opt.trace && g == 32 && !weak && !dyn && phase == 0 &&
+            pick_pp(c, mean, &pp_w, &pp_k, &pp_n, &pp_m, &pp_d, &pp_b);
+  if (pp) {
+    if (pp_b < 0) pp_b = backoff;
+    size_t pp_smem = 0;
+    cudaError_t pe = tcbdev::pp_occupancy(pp_w, pp_k, pp_n, pp_m, extras, drain ? 1 : 0, pp_b, pp_d, &occ, &pp_smem);
+    if (pe != cudaSuccess && drain) {
+      cudaGetLastError();
+      drain = false;
+      pe = tcbdev::pp_occupancy(pp_w, pp_k, pp_n, pp_m, extras, 0, pp_b, pp_d, &occ, &pp_smem);
+    }
+    if (pe != cudaSuccess) {
+      cudaGetLastError();
+      pp = false;
+    }
+  }
+  if (!pp && pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0, backoff) != cudaSuccess) {
     cudaGetLastError();
     pipe = false;
     drain = false;
   }
-  cudaError_t oe = pipe ? cudaSuccess : tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
+  cudaError_t oe = (pipe || pp) ? cudaSuccess : tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
   if (oe == cudaErrorInvalidValue && kb != 4) {  // no such variant: the KB = 4 one
     kb = 4;
     oe = tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
@@ -902,8 +953,12 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   }
   if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
   if (drain) TCG_CUDA_TRY(c, cudaMemsetAsync(c->drain_done, 0, sizeof(unsigned) * drain_words, c->stream));
+  P.ub = c->flow_ub;
   if (c->nflow > 0) {
-    if (pipe)
+    if (pp)
+      TCG_CUDA_TRY(c, tcbdev::launch_flow_pp(P, grid, pp_w, pp_k, pp_n, pp_m, extras, drain ? 1 : 0, pp_b, pp_d,
+                                             c->stream));
+    else if (pipe)
       TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, extras, c->stream,
                                                drain ? 1 : 0, backoff));
     else TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
@@ -934,7 +989,10 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   S.mode = 5;
   S.drain_ctas = drain ? drain_ctas : 0;
   if (host_a) c->pristine = false;
-  S.lanes_per_row = g;
+  S.lanes_per_row = pp ? 32 * pp_w : g;
+  S.row_kernel = pp ? 2 : 1;
+  if (pp) S.threads_per_cta = 256;
+  if (pp) S.staging_cap = pp_k;
   const int64_t rows = c->nflow * c->nbatch;
   S.tasks_completed = (h.done.v == rows) ? c->ntasks * c->nbatch : 0;
   S.tasks_executed = h.executed.v;
@@ -1167,7 +1225,17 @@ static tcg_status run_flow_chunked(tcg_ctx* c, tcg_stats& S, int threads, const 
   int backoff = kb >= 3 ? 200 : 0;
   if (const char* e = std::getenv("TCG_FLOW_BACKOFF")) backoff = std::atoi(e);
   int occ = 0;
-  TCG_CUDA_TRY(c, tcbdev::pipe_occupancy(threads, kb, minb, 0, 1, &occ, 0, backoff));
+  int pp_w = 0, pp_k = 0, pp_n = 0, pp_m = 0, pp_d = 0, pp_b = -1;
+  bool pp = !c->opt.trace && pick_pp(c, mean, &pp_w, &pp_k, &pp_n, &pp_m, &pp_d, &pp_b);
+  if (pp) {
+    if (pp_b < 0) pp_b = backoff;
+    size_t smem = 0;
+    if (tcbdev::pp_occupancy(pp_w, pp_k, pp_n, pp_m, 1, 0, pp_b, pp_d, &occ, &smem) != cudaSuccess) {
+      cudaGetLastError();
+      pp = false;
+    }
+  }
+  if (!pp) TCG_CUDA_TRY(c, tcbdev::pipe_occupancy(threads, kb, minb, 0, 1, &occ, 0, backoff));
   if (occ < 1) {
     c->err = "value-flow kernel does not fit on an SM";
     return TCG_INVALID;
@@ -1233,7 +1301,11 @@ static tcg_status run_flow_chunked(tcg_ctx* c, tcg_stats& S, int threads, const 
     P.nrows = static_cast<int>(c->nflow);
     P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
     P.row_ctas = grid;
-    TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, 0, 1, c->stream, 0, backoff));
+    P.ub = c->flow_ub;
+    if (pp)
+      TCG_CUDA_TRY(c, tcbdev::launch_flow_pp(P, grid, pp_w, pp_k, pp_n, pp_m, 1, 0, pp_b, pp_d, c->stream));
+    else
+      TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, 0, 1, c->stream, 0, backoff));
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrls + k, c->ctrl, sizeof(tcbdev::Ctrl), cudaMemcpyDeviceToHost,
                                     c->stream));
     TCG_CUDA_TRY(c, cudaEventRecord(done, c->stream));
@@ -1252,10 +1324,11 @@ static tcg_status run_flow_chunked(tcg_ctx* c, tcg_stats& S, int threads, const 
   S.device_ms = ms;
   S.grid_ctas = grid;
   S.threads_per_cta = threads;
-  S.staging_cap = kb;
+  S.staging_cap = pp ? pp_k : kb;
   S.kernel_launches = 3 * chunks;
   S.mode = 5;
-  S.lanes_per_row = 32;
+  S.lanes_per_row = pp ? 32 * pp_w : 32;
+  S.row_kernel = pp ? 2 : 1;
   S.batch = nb;
   S.chunks = chunks;
   bool error = false;

@@ -26,6 +26,11 @@ cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras
                            int drain = 0, int backoff_ns = 0);
 cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb, int minb, int remote,
                              int extras, cudaStream_t st, int drain = 0, int backoff_ns = 0);
+// product-parallel rows (flow_pp_kernel.cu): WPR warps per row group, KP products per thread and chunk
+cudaError_t pp_occupancy(int wpr, int kp, int nb, int minb, int extras, int drain, int bo, int d,
+                         int* ctas_per_sm, size_t* smem);
+cudaError_t launch_flow_pp(const FlowParams& p, int grid, int wpr, int kp, int nb, int minb, int extras, int drain,
+                           int bo, int d, cudaStream_t st);
 cudaError_t launch_init_values(const double* a, const int* map, double* vals, double* vals0, long long nnz,
                                long long nnz_a, int nbatch, int sm_count, cudaStream_t st);
 

@@ -79,6 +79,7 @@ struct FlowParams {
   const int* item;       // per position: its item (trace only)
   const int4* slot;      // per coordinate of U: {u_b, u_e, m0, o0}
   const int2* upd;       // (m, o) pairs
+  const int* ub;         // per coordinate of U: its first product in upd (nnz + 1; product-parallel rows)
   const double* a;       // input values (snapshot taken by the prelude), nbatch x nnz
   double* vals;          // output; kUnset until the owning row writes it; nbatch x nnz
   Ctrl* ctrl;

@@ -22,125 +22,13 @@
 #include <cuda_runtime.h>
 
 #include "factor_kernel.cuh"
+#include "flow_common.cuh"
 #include "sync.cuh"
 
 namespace tcbdev {
 
 namespace {
 
-constexpr unsigned long long kCanonicalNaN = 0x7FFFFFFFFFFFFFFFull;
-
-// Slow path of a gather: the value is not written yet.
-// BO: nanoseconds a lane sleeps between re-polls (0: none)
-template <int BO = 0>
-__device__ __forceinline__ unsigned long long wait_value(const double* p, Ctrl* ctrl,
-                                                      unsigned long long t0,
-                                                      unsigned long long tmo) {
-  unsigned spins = 0;
-  for (;;) {
-    const unsigned long long x = ld_relaxed_u64(p);
-    if (x != kUnset) return x;
-    if (BO) __nanosleep(BO);
-    if (++spins == 1024u) {
-      spins = 0;
-      if (ld_relaxed(&ctrl->error.v) || gtimer() - t0 > tmo) {
-        atomicCAS(&ctrl->error.v, 0, 1);
-        return 0ull;  // abandoned: the host reports TCG_TIMEOUT
-      }
-    }
-  }
-}
-
-// The same poll at system scope: a value owned by a part on another GPU.
-__device__ __forceinline__ unsigned long long wait_value_sys(const double* p, Ctrl* ctrl,
-                                                          unsigned long long t0,
-                                                          unsigned long long tmo) {
-  unsigned spins = 0;
-  for (;;) {
-    const unsigned long long x = ld_relaxed_sys_u64(p);
-    if (x != kUnset) return x;
-    if (++spins == 1024u) {
-      spins = 0;
-      if (ld_relaxed(&ctrl->error.v) || gtimer() - t0 > tmo) {
-        atomicCAS(&ctrl->error.v, 0, 1);
-        return 0ull;
-      }
-    }
-  }
-}
-
-// WEAK: first attempt of every gather is a plain (L1-cached) load; only a
-// kUnset answer falls back to strong polling. Sound because a location
-// holds kUnset until its single final value is written: any other bits a
-// load returns are the final value (8-byte aligned accesses do not tear),
-// and a stale L1 copy can only show kUnset, which the strong path re-reads.
-// `vals`/`a`/`member`: the current row's member of a batch (its value sets
-// are nnz apart; the pattern, records and programs are shared).
-// OPS: how a negative operand position is read. 0: never happens; 2
-// (sharded runs): kRemoteBit | part << 25 | position in that part's U.
-// BO: poll back-off in ns (a lane sleeps between re-polls of a value not yet
-// written). Long programs keep thousands of lanes polling the few lines the
-// critical rows are about to write; sleeping between polls frees the L2
-// slices serving them (B200, C3: 4.33 -> 3.45 ms at 300 ns, C4 1.61 -> 1.48
-// at 100 ns; short programs lose: C2 0.41 -> 0.42-0.45 ms).
-template <int WEAK, int OPS = 0, int BO = 0>
-struct Ctx {
-  const FlowParams& P;
-  unsigned long long t0;
-  double* vals;
-  const double* a;
-  int member;
-  __device__ __forceinline__ double settle(const double* p, unsigned long long x) const {
-    if (x == kUnset) x = wait_value<BO>(p, P.ctrl, t0, P.timeout_ns);
-    return __longlong_as_double(static_cast<long long>(x));
-  }
-  // sharded runs (P.peers): a negative position names another part's value
-  __device__ __forceinline__ const double* remote(int pos) const {
-    return P.peers[(pos >> 25) & 63] + (pos & 0x1FFFFFF);
-  }
-  __device__ __forceinline__ unsigned long long ld(int pos) const {
-    if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
-    if (WEAK) return ld_weak_u64(vals + pos);
-    return ld_relaxed_u64(vals + pos);
-  }
-  // re-polls are always strong: a weak (L1) copy of the marker may be stale
-  __device__ __forceinline__ unsigned long long ld_strong(int pos) const {
-    if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
-    return ld_relaxed_u64(vals + pos);
-  }
-  // settle an operand by its (encoded) position
-  __device__ __forceinline__ double settle_at(int pos, unsigned long long x) const {
-    if (x == kUnset) {
-      if (OPS == 2 && pos < 0) x = wait_value_sys(remote(pos), P.ctrl, t0, P.timeout_ns);
-      else x = wait_value<BO>(vals + pos, P.ctrl, t0, P.timeout_ns);
-    }
-    return __longlong_as_double(static_cast<long long>(x));
-  }
-  // both operands of one product: U(r,t) and U(r,c) come from the same
-  // source row r, so when r has just been written both still read kUnset;
-  // re-polling them together costs one round trip instead of two
-  __device__ __forceinline__ double product(int pa, unsigned long long xa, int pb, unsigned long long xb) const {
-    if (OPS != 2 && (xa == kUnset || xb == kUnset)) {
-      unsigned spins = 0;
-      do {
-        if (xa == kUnset) xa = ld_strong(pa);
-        if (xb == kUnset) xb = ld_strong(pb);
-        if (BO) __nanosleep(BO);
-        if (++spins == 1024u) {
-          spins = 0;
-          if (ld_relaxed(&P.ctrl->error.v) || gtimer() - t0 > P.timeout_ns) {
-            atomicCAS(&P.ctrl->error.v, 0, 1);  // abandoned: the host reports TCG_TIMEOUT
-            xa = xb = 0ull;
-          }
-        }
-      } while (xa == kUnset || xb == kUnset);
-    }
-    if (OPS != 2)  // settled by the loop above
-      return __dmul_rn(__longlong_as_double(static_cast<long long>(xa)), __longlong_as_double(static_cast<long long>(xb)));
-    return __dmul_rn(settle_at(pa, xa), settle_at(pb, xb));
-  }
-  static constexpr bool kSysPublish = OPS == 2;  // readers on other GPUs
-};
 
 // An input value: the prelude's snapshot, immutable during the launch.
 __device__ __forceinline__ double input_ld(const FlowParams&, const double* p) { return __ldg(p); }
@@ -377,76 +265,6 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
   }
 }
 
-// Drain (end to end): the warps of the CTAs past P.row_ctas copy U to the
-// host while the rows run. A value is final as soon as it no longer reads
-// kUnset (it is written once), so a warp copies every group of 64 values
-// whose loads all see final values -- 16 bytes per lane, one coalesced
-// 512-byte store into the pinned host buffer -- and comes back later for
-// groups that are not final yet (a bit per group in P.drain_done; a sweep
-// that copies nothing backs off for a microsecond, so its re-reads do not
-// crowd the lines the rows are writing). Two groups are checked at once; warp
-// d owns a contiguous slice of the 2,048-value batches. Measured on B200
-// (end to end, wall): 8-byte accesses per lane in groups of 32 gave C2 0.82,
-// C6 5.75 ms; this layout C2 0.82, C6 5.48 ms; four groups in flight C2 0.89
-// ms; eight (80 registers, harder re-reads of unfinished lines) C2 1.99 ms.
-__device__ void drain_values(const FlowParams& P, int dw, int DW) {
-  constexpr int kIn = 2;
-  const int lane = threadIdx.x & 31;
-  const long long total = P.nnz * P.nbatch;  // a batch's members are contiguous
-  const long long nb = (total + 2047) / 2048;
-  const long long b0 = nb * dw / DW, b1 = nb * (dw + 1) / DW;
-  const unsigned long long t0 = gtimer();
-  const bool even = (total & 1) == 0;
-  long long low = b0;
-  while (low < b1) {
-    bool progressed = false;
-    for (long long b = low; b < b1; ++b) {
-      unsigned done = P.drain_done[b];
-      if (done == 0xffffffffu) {
-        if (b == low) ++low;
-        continue;
-      }
-      for (int j0 = 0; j0 < 32; j0 += kIn) {
-        unsigned long long va[kIn], vb[kIn];
-#pragma unroll
-        for (int j = 0; j < kIn; ++j) {
-          const long long x = (b * 32 + j0 + j) * 64 + 2 * lane;
-          va[j] = vb[j] = 0ull;
-          if ((done >> (j0 + j)) & 1u) continue;
-          if (even && x + 1 < total) {
-            ld_relaxed_v2_u64(P.vals + x, va[j], vb[j]);
-          } else {
-            if (x < total) va[j] = ld_relaxed_u64(P.vals + x);
-            if (x + 1 < total) vb[j] = ld_relaxed_u64(P.vals + x + 1);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kIn; ++j) {
-          if ((done >> (j0 + j)) & 1u) continue;
-          if (__ballot_sync(kFull, va[j] != kUnset && vb[j] != kUnset) != kFull) continue;
-          const long long x = (b * 32 + j0 + j) * 64 + 2 * lane;
-          if (even && x + 1 < total) {
-            *reinterpret_cast<double2*>(P.drain_out + x) =
-                make_double2(__longlong_as_double(static_cast<long long>(va[j])),
-                             __longlong_as_double(static_cast<long long>(vb[j])));
-          } else {
-            if (x < total) P.drain_out[x] = __longlong_as_double(static_cast<long long>(va[j]));
-            if (x + 1 < total) P.drain_out[x + 1] = __longlong_as_double(static_cast<long long>(vb[j]));
-          }
-          done |= 1u << (j0 + j);
-          progressed = true;
-        }
-      }
-      if (lane == 0) P.drain_done[b] = done;
-      __syncwarp();
-      if (done == 0xffffffffu && b == low) ++low;
-    }
-    if (!progressed && low < b1) {
-      if (ld_relaxed(&P.ctrl->error.v) || gtimer() - t0 > P.timeout_ns) return;
-      __nanosleep(1000);
-    }
-  }
-}
 
 // factor_flow with the per-row metadata staged in shared memory (PIPE): a
 // row of a short program is shorter than an L2 round trip, so prefetching its

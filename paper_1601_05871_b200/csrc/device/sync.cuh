@@ -101,6 +101,17 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
 }
+// 4-byte variant
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+// barrier of the T threads of one row group (named barrier `id`; a warp: __syncwarp)
+template <int T>
+__device__ __forceinline__ void group_sync(int id) {
+  if (T == 32) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(T) : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait_group() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");

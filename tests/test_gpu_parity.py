@@ -47,6 +47,36 @@ def test_configs_value_flow(T, golden, oracle, name):  # noqa: D103
     check_against_oracle(name, vals, golden, oracle)
 
 
+def test_default_row_kernel_follows_program_length(T):
+    # product-parallel rows where programs are short (C1, C2, C5), one lane
+    # per coordinate where they are long (C3: 24.8 products per coordinate)
+    for name, want in (("c1", 2), ("c5_m0", 2), ("c2", 2), ("s27_16_k2", 1)):
+        _, st = gpu_factor(T, planned(name), mode=5)
+        assert st.row_kernel == want, name
+
+
+@pytest.mark.parametrize("name,spec", [("c3", "1,2,1,4,2,0"), ("s27_16_k2", "4,2,4,3,1,0"),
+                                       ("elast6_k1", "2,2,2,3,1,0"), ("c2", "2,1,4,4,1,0"),
+                                       ("c1", "1,2,2,4,2,0"), ("rand_spd_200", "4,4,4,2,1,0"),
+                                       ("c4", "2,2,2,3,1,0"), ("grid20_k2_leaf4", "1,2,1,4,2,0")])
+def test_product_parallel_variants(T, golden, oracle, name, spec, monkeypatch):
+    # flow_pp_kernel.cu: rows longer than the group (passes), programs longer
+    # than a chunk (several chunks, prefetched one ahead), one to four warps
+    # per row: every variant bitwise equal to factor_serial
+    monkeypatch.setenv("TCG_FLOW_PP", spec)
+    vals, st = gpu_factor(T, planned(name), mode=5)
+    assert st.row_kernel == 2 and st.lanes_per_row == 32 * int(spec.split(",")[0])
+    check_against_oracle(name, vals, golden, oracle)
+
+
+@pytest.mark.parametrize("name", ["c1", "c5_m0", "c2", "rand_spd_200"])
+def test_per_lane_kernel_on_short_programs(T, golden, oracle, name, monkeypatch):
+    monkeypatch.setenv("TCG_FLOW_PP", "0")
+    vals, st = gpu_factor(T, planned(name), mode=5)
+    assert st.row_kernel == 1
+    check_against_oracle(name, vals, golden, oracle)
+
+
 @pytest.mark.parametrize("name", ["c1", "grid20_k2_leaf4", "rand_spd_200", "elast6_k1", "c5_m0"])
 def test_device_programs_equal_the_cpu_restatement(T, name):
     # flow_program.cu (transposed index by a radix sort, count, scan, fill)
