@@ -79,7 +79,9 @@ tcb::Plan& full_plan(const tcg_plan* plan) {
     if (const char* e = std::getenv("TCG_MAX_WIDTH")) po.max_width = std::max(1, std::atoi(e));
     if (const char* e = std::getenv("TCG_DEP_WIDE_COST")) po.dep_wide_cost = std::max(1.0, std::atof(e));
     plan->full = std::make_unique<tcb::Plan>(
-        tcb::build_plan(tcb::flow_plan_pattern(plan->flow), plan->flow.values, plan->ranges, true, po));
+        tcb::build_plan(tcb::flow_plan_pattern(plan->flow),
+                        std::vector<double>(plan->flow.values.begin(), plan->flow.values.end()), plan->ranges,
+                        true, po));
   }
   return *plan->full;
 }

@@ -42,6 +42,45 @@ void parallel_rows(index_t n, int threads, F&& fn) {
   for (auto& th : pool) th.join();
 }
 
+// Rows in a topological order of some row DAG, on the host threads: a row
+// is handed out once its counter (its unprocessed predecessors) reaches zero.
+// body(r, release) processes row r and calls release(s) once for every
+// successor s of r. Rows are handed out through a bag of n slots (a taker
+// spins on its slot until a producer fills it); the counters' acq_rel
+// decrements and the slot's release/acquire order a row's writes before
+// every successor's reads. No deadlock: while rows remain, some unprocessed
+// row has a zero counter and was put in the bag by whoever released it last.
+// (Handing out layers between barriers instead was slower on C3, whose
+// layers are narrow: 0.18 -> 0.37 s.)
+template <class Body>
+void ready_rows(index_t n, int threads, std::vector<std::atomic<std::int32_t>>& count, Body&& body) {
+  std::vector<std::atomic<std::int32_t>> slot(static_cast<std::size_t>(n));
+  std::atomic<std::int64_t> head{0}, tail{0};
+  for (index_t r = 0; r < n; ++r) slot[r].store(-1, std::memory_order_relaxed);
+  for (index_t r = 0; r < n; ++r)
+    if (count[r].load(std::memory_order_relaxed) == 0) slot[tail.fetch_add(1)].store(r, std::memory_order_relaxed);
+  auto release = [&](index_t s) {
+    if (count[s].fetch_sub(1, std::memory_order_acq_rel) == 1)
+      slot[tail.fetch_add(1, std::memory_order_relaxed)].store(s, std::memory_order_release);
+  };
+  auto worker = [&] {
+    for (;;) {
+      const std::int64_t k = head.fetch_add(1, std::memory_order_relaxed);
+      if (k >= n) return;
+      std::int32_t r;
+      unsigned spins = 0;
+      while ((r = slot[k].load(std::memory_order_acquire)) < 0)
+        if (++spins > 64) std::this_thread::yield();
+      body(static_cast<index_t>(r), release);
+    }
+  };
+  const int T = std::max(1, std::min<int>(threads, std::max<index_t>(1, n / 4096)));
+  std::vector<std::thread> pool;
+  for (int k = 1; k < T; ++k) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+}
+
 // validate_csr (sparse.cpp) over the host threads: the same checks and
 // messages, the first failing row reported
 void validate_ref(const CsrRef& m, int threads) {
@@ -131,7 +170,7 @@ CsrMatrix flow_plan_pattern(const FlowPlan& P) {
   CsrMatrix u;
   u.nrows = u.ncols = P.n;
   u.row_ptr.assign(P.row_ptr.begin(), P.row_ptr.end());
-  u.col_idx = P.cols;
+  u.col_idx.assign(P.cols.begin(), P.cols.end());
   u.values.assign(P.cols.size(), 1.0);
   return u;
 }
@@ -165,7 +204,7 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
   P.cols.resize(static_cast<std::size_t>(u.nnz));
   P.row_ptr.resize(static_cast<std::size_t>(n) + 1);
   P.values.resize(static_cast<std::size_t>(u.nnz));
-  P.a_map.assign(static_cast<std::size_t>(u.nnz), -1);
+  P.a_map.resize(static_cast<std::size_t>(u.nnz));
   // initial values (factorize.hpp:71-89) by rows on the host threads: the
   // sorted merge of A's upper row into U's, recording where each slot starts
   // from (the device init's map; 0.0 + a as there). A slot fed twice
@@ -179,6 +218,7 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
       for (offset_t t = ub; t < ue; ++t) {
         P.cols[t] = u.col_idx[t];
         P.values[t] = 0.0;
+        P.a_map[t] = -1;
       }
       offset_t t = ub;
       for (offset_t q = a.row_ptr[i]; q < a.row_ptr[i + 1]; ++q) {
@@ -252,62 +292,150 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
     // holding q on, up to the last one starting at a column <= c1(g) (they
     // hold the multiplier and every operand U(r,c) g reads); a chunk also
     // reads U(t,t), its row's Chol unit. Every dependence points to a lower
-    // row (or the row's own Chol unit), so both sweeps below run in row
-    // order, pushing along the entries of U's rows (no transposed index).
-    // Both sweeps keep, per source entry, a pointer to the unit of row r
-    // holding it (it only advances along the row) and walk the units of
-    // row t once, the last dependence vmax(g) growing with g's last column.
-    std::vector<std::int32_t> level(U, 1), height(U, 1), vmax;
+    // row (or the row's own Chol unit). Levels (longest chain from a source)
+    // and heights (longest chain to a sink) are computed row by row, each
+    // row pulling from rows that are final: levels in a topological order of
+    // the rows (ready once all its sources are done, through U's transposed
+    // index), heights in a reverse one (ready once every row it feeds is
+    // done); both on the host threads (ready_rows).
+    hvec<std::int32_t> level(U), height(U);
     std::int32_t depth = 0;
-    for (index_t r = 0; r < n; ++r) {
-      const std::int32_t vr0 = ufirst[r], vr1 = ufirst[r + 1];
-      for (std::int32_t g = vr0 + 1; g < vr1; ++g) level[g] = std::max(level[g], level[vr0] + 1);
-      for (std::int32_t g = vr0; g < vr1; ++g) depth = std::max(depth, level[g]);
-      std::int32_t v0 = vr0;
-      for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q) {
-        while (v0 + 1 < vr1 && u_tb[v0 + 1] <= q) ++v0;
-        const index_t t = cols[q];
-        std::int32_t v = v0, lv = level[v0];
-        for (std::int32_t g = ufirst[t]; g < ufirst[t + 1]; ++g) {
-          while (v + 1 < vr1 && u_c0[v + 1] <= u_c1[g]) lv = std::max(lv, level[++v]);
-          level[g] = std::max(level[g], lv + 1);
-        }
+    // Long rows (C3: 69 entries, three units per row) carry enough work per
+    // row for the parallel traversal (C3 0.39 -> 0.22 s of plan on 8 threads);
+    // shorter ones (C1, C2, C4-C6) sweep faster on one thread than through
+    // any hand-out of their rows (C4: levels and heights 0.14 s on one
+    // thread, 0.20 s in parallel).
+    if (threads > 1 && u.nnz >= 48 * static_cast<offset_t>(n)) {
+      std::vector<std::atomic<std::int32_t>> cnt(static_cast<std::size_t>(n));
+      for (index_t t = 0; t < n; ++t) cnt[t].store(0, std::memory_order_relaxed);
+      parallel_rows(n, threads, [&](index_t b, index_t e) {
+        for (index_t r = b; r < e; ++r)
+          for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q)
+            cnt[cols[q]].fetch_add(1, std::memory_order_relaxed);
+      });
+      // transposed index: the sources (r, q) of every row t, in any order
+      std::vector<std::int64_t> sptr(static_cast<std::size_t>(n) + 1, 0);
+      for (index_t t = 0; t < n; ++t) sptr[t + 1] = sptr[t] + cnt[t].load(std::memory_order_relaxed);
+      hvec<std::int32_t> src_r(static_cast<std::size_t>(sptr[n])), src_q(static_cast<std::size_t>(sptr[n]));
+      {
+        std::vector<std::atomic<std::int64_t>> fill(static_cast<std::size_t>(n));
+        for (index_t t = 0; t < n; ++t) fill[t].store(sptr[t], std::memory_order_relaxed);
+        parallel_rows(n, threads, [&](index_t b, index_t e) {
+          for (index_t r = b; r < e; ++r)
+            for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q) {
+              const std::int64_t k = fill[cols[q]].fetch_add(1, std::memory_order_relaxed);
+              src_r[k] = static_cast<std::int32_t>(r);
+              src_q[k] = q;
+            }
+        });
       }
-    }
-    for (index_t r = n; r-- > 0;) {
-      const std::int32_t vr0 = ufirst[r], vr1 = ufirst[r + 1];
-      std::int32_t v0 = vr0;
-      for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q) {
-        while (v0 + 1 < vr1 && u_tb[v0 + 1] <= q) ++v0;
-        const index_t t = cols[q];
+      mark("transpose");
+      ready_rows(n, threads, cnt, [&](index_t t, auto&& release) {
         const std::int32_t g0 = ufirst[t], g1 = ufirst[t + 1];
-        if (vr1 - vr0 == 1) {  // one unit: every dependent of the entry reads it
+        for (std::int32_t g = g0; g < g1; ++g) level[g] = 1;
+        for (std::int64_t k = sptr[t]; k < sptr[t + 1]; ++k) {
+          const index_t r = src_r[k];
+          const std::int32_t q = src_q[k], vr1 = ufirst[r + 1];
+          std::int32_t v = ufirst[r];
+          while (v + 1 < vr1 && u_tb[v + 1] <= q) ++v;  // the unit of row r holding q
+          std::int32_t lv = level[v];
+          for (std::int32_t g = g0; g < g1; ++g) {
+            while (v + 1 < vr1 && u_c0[v + 1] <= u_c1[g]) lv = std::max(lv, level[++v]);
+            level[g] = std::max(level[g], lv + 1);
+          }
+        }
+        for (std::int32_t g = g0 + 1; g < g1; ++g) level[g] = std::max(level[g], level[g0] + 1);
+        for (std::int32_t q = P.row_ptr[t] + 1; q < P.row_ptr[t + 1]; ++q) release(cols[q]);
+      });
+      for (std::size_t g = 0; g < U; ++g) depth = std::max(depth, level[g]);
+      mark("level");
+      // heights: row r is ready once every row its entries feed is done
+      for (index_t r = 0; r < n; ++r) cnt[r].store(P.row_ptr[r + 1] - P.row_ptr[r] - 1, std::memory_order_relaxed);
+      ready_rows(n, threads, cnt, [&](index_t r, auto&& release) {
+        thread_local std::vector<std::int32_t> vmax;
+        const std::int32_t vr0 = ufirst[r], vr1 = ufirst[r + 1];
+        for (std::int32_t v = vr0; v < vr1; ++v) height[v] = 1;
+        std::int32_t v0 = vr0;
+        for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q) {
+          while (v0 + 1 < vr1 && u_tb[v0 + 1] <= q) ++v0;
+          const index_t t = cols[q];
+          const std::int32_t g0 = ufirst[t], g1 = ufirst[t + 1];
+          if (vr1 - vr0 == 1) {  // one unit: every dependent of the entry reads it
+            std::int32_t hm = 0;
+            for (std::int32_t g = g0; g < g1; ++g) hm = std::max(hm, height[g] + 1);
+            height[v0] = std::max(height[v0], hm);
+            continue;
+          }
+          vmax.resize(static_cast<std::size_t>(g1 - g0));
+          for (std::int32_t g = g0, v = v0; g < g1; ++g) {
+            while (v + 1 < vr1 && u_c0[v + 1] <= u_c1[g]) ++v;
+            vmax[g - g0] = v;
+          }
+          // unit v of row r is read by the dependents g with vmax(g) >= v
           std::int32_t hm = 0;
-          for (std::int32_t g = g0; g < g1; ++g) hm = std::max(hm, height[g] + 1);
-          height[v0] = std::max(height[v0], hm);
-          continue;
+          for (std::int32_t g = g1; g-- > g0;) {
+            hm = std::max(hm, height[g] + 1);
+            const std::int32_t lo = g > g0 ? vmax[g - 1 - g0] + 1 : v0;
+            for (std::int32_t v = lo; v <= vmax[g - g0]; ++v) height[v] = std::max(height[v], hm);
+          }
         }
-        vmax.resize(static_cast<std::size_t>(g1 - g0));
-        for (std::int32_t g = g0, v = v0; g < g1; ++g) {
-          while (v + 1 < vr1 && u_c0[v + 1] <= u_c1[g]) ++v;
-          vmax[g - g0] = v;
-        }
-        // unit v of row r is read by the dependents g with vmax(g) >= v
-        std::int32_t hm = 0;
-        for (std::int32_t g = g1; g-- > g0;) {
-          hm = std::max(hm, height[g] + 1);
-          const std::int32_t lo = g > g0 ? vmax[g - 1 - g0] + 1 : v0;
-          for (std::int32_t v = lo; v <= vmax[g - g0]; ++v) height[v] = std::max(height[v], hm);
+        for (std::int32_t g = vr0 + 1; g < vr1; ++g) height[vr0] = std::max(height[vr0], height[g] + 1);
+        for (std::int64_t k = sptr[r]; k < sptr[r + 1]; ++k) release(src_r[k]);
+      });
+    } else {
+      std::vector<std::int32_t> vmax;
+      std::fill(level.begin(), level.end(), 1);
+      std::fill(height.begin(), height.end(), 1);
+      for (index_t r = 0; r < n; ++r) {
+        const std::int32_t vr0 = ufirst[r], vr1 = ufirst[r + 1];
+        for (std::int32_t g = vr0 + 1; g < vr1; ++g) level[g] = std::max(level[g], level[vr0] + 1);
+        for (std::int32_t g = vr0; g < vr1; ++g) depth = std::max(depth, level[g]);
+        std::int32_t v0 = vr0;
+        for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q) {
+          while (v0 + 1 < vr1 && u_tb[v0 + 1] <= q) ++v0;
+          const index_t t = cols[q];
+          std::int32_t v = v0, lv = level[v0];
+          for (std::int32_t g = ufirst[t]; g < ufirst[t + 1]; ++g) {
+            while (v + 1 < vr1 && u_c0[v + 1] <= u_c1[g]) lv = std::max(lv, level[++v]);
+            level[g] = std::max(level[g], lv + 1);
+          }
         }
       }
-      for (std::int32_t g = vr0 + 1; g < vr1; ++g) height[vr0] = std::max(height[vr0], height[g] + 1);
+      for (index_t r = n; r-- > 0;) {
+        const std::int32_t vr0 = ufirst[r], vr1 = ufirst[r + 1];
+        std::int32_t v0 = vr0;
+        for (std::int32_t q = P.row_ptr[r] + 1; q < P.row_ptr[r + 1]; ++q) {
+          while (v0 + 1 < vr1 && u_tb[v0 + 1] <= q) ++v0;
+          const index_t t = cols[q];
+          const std::int32_t g0 = ufirst[t], g1 = ufirst[t + 1];
+          if (vr1 - vr0 == 1) {  // one unit: every dependent of the entry reads it
+            std::int32_t hm = 0;
+            for (std::int32_t g = g0; g < g1; ++g) hm = std::max(hm, height[g] + 1);
+            height[v0] = std::max(height[v0], hm);
+            continue;
+          }
+          vmax.resize(static_cast<std::size_t>(g1 - g0));
+          for (std::int32_t g = g0, v = v0; g < g1; ++g) {
+            while (v + 1 < vr1 && u_c0[v + 1] <= u_c1[g]) ++v;
+            vmax[g - g0] = v;
+          }
+          // unit v of row r is read by the dependents g with vmax(g) >= v
+          std::int32_t hm = 0;
+          for (std::int32_t g = g1; g-- > g0;) {
+            hm = std::max(hm, height[g] + 1);
+            const std::int32_t lo = g > g0 ? vmax[g - 1 - g0] + 1 : v0;
+            for (std::int32_t v = lo; v <= vmax[g - g0]; ++v) height[v] = std::max(height[v], hm);
+          }
+        }
+        for (std::int32_t g = vr0 + 1; g < vr1; ++g) height[vr0] = std::max(height[vr0], height[g] + 1);
+      }
     }
     mark("levels");
     // schedule: level ascending, height descending, unit id ascending (two
     // stable counting sorts, the second key first)
     std::int32_t hmax = 0;
     for (std::int32_t h : height) hmax = std::max(hmax, h);
-    std::vector<std::int32_t> tmp(U), order(U);
+    hvec<std::int32_t> tmp(U), order(U);
     {
       std::vector<std::int64_t> cnt(static_cast<std::size_t>(hmax) + 2, 0);
       for (std::size_t g = 0; g < U; ++g) ++cnt[static_cast<std::size_t>(hmax - height[g]) + 1];
@@ -326,16 +454,20 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
     }
     P.rec.resize(4 * U);
     P.unit.resize(U);
-    for (std::size_t q = 0; q < U; ++q) {
-      const std::int32_t g = order[q];
-      const std::int32_t t = row_of[g];
-      if (u_len[g] >= (1 << 30)) throw std::length_error("flow: row slice too long");
-      P.rec[4 * q + 0] = u_tb[g];
-      P.rec[4 * q + 1] = u_len[g] | ((g == ufirst[t] ? 0 : 1) << 30);  // Chol unit, else a chunk (Trsm)
-      P.rec[4 * q + 2] = P.row_ptr[t];
-      P.rec[4 * q + 3] = t;
-      P.unit[q] = g;
-    }
+    std::atomic<bool> too_long{false};
+    parallel_rows(static_cast<index_t>(U), threads, [&](index_t b, index_t e) {
+      for (index_t q = b; q < e; ++q) {
+        const std::int32_t g = order[q];
+        const std::int32_t t = row_of[g];
+        if (u_len[g] >= (1 << 30)) too_long.store(true, std::memory_order_relaxed);
+        P.rec[4 * q + 0] = u_tb[g];
+        P.rec[4 * q + 1] = u_len[g] | ((g == ufirst[t] ? 0 : 1) << 30);  // Chol unit, else a chunk (Trsm)
+        P.rec[4 * q + 2] = P.row_ptr[t];
+        P.rec[4 * q + 3] = t;
+        P.unit[q] = g;
+      }
+    });
+    if (too_long.load()) throw std::length_error("flow: row slice too long");
     mark("order");
     P.stats.units = static_cast<std::int64_t>(U);
     P.stats.depth = depth;

@@ -20,11 +20,37 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
+#include <utility>
 #include <vector>
 
 #include "sparse.hpp"
 
 namespace tcb {
+
+// std::vector storage whose resize() leaves new elements default-initialised
+// (no zero fill): the plan's arrays are written in full by the host threads,
+// so a single-threaded memset before that would only add time.
+template <class T>
+struct uninit_alloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = uninit_alloc<U>;
+  };
+  uninit_alloc() = default;
+  template <class U>
+  uninit_alloc(const uninit_alloc<U>&) noexcept {}
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+};
+template <class T>
+using hvec = std::vector<T, uninit_alloc<T>>;
 
 // A borrowed CSR matrix (the caller's arrays; values may be null for a pattern).
 struct CsrRef {
@@ -50,12 +76,12 @@ struct FlowPlan {
   index_t n = 0;
   std::int64_t nnz = 0;
   std::int64_t nnz_a = 0;             // entries of a_permuted
-  std::vector<std::int32_t> cols;     // U column indices
-  std::vector<std::int32_t> row_ptr;  // n + 1 positions (int32: nnz < 2^31)
-  std::vector<double> values;         // initialised U values (init_factor_values)
-  std::vector<std::int32_t> a_map;    // U slot -> a_permuted position, -1 = fill (empty: A has duplicates)
-  std::vector<std::int32_t> rec;      // 4 words per schedule position: tb, L | kind << 30, dpos, t
-  std::vector<std::int32_t> unit;     // per schedule position: unit id (natural order)
+  hvec<std::int32_t> cols;     // U column indices
+  hvec<std::int32_t> row_ptr;  // n + 1 positions (int32: nnz < 2^31)
+  hvec<double> values;         // initialised U values (init_factor_values)
+  hvec<std::int32_t> a_map;    // U slot -> a_permuted position, -1 = fill (empty: A has duplicates)
+  hvec<std::int32_t> rec;      // 4 words per schedule position: tb, L | kind << 30, dpos, t
+  hvec<std::int32_t> unit;     // per schedule position: unit id (natural order)
   FlowPlanStats stats;
 };
 
