@@ -26,7 +26,7 @@ DEV_OBJS := $(OBJ)/device/factor_kernel.o \
             $(OBJ)/device/flow_kernel.o $(OBJ)/device/flow_pp_kernel.o $(OBJ)/device/flow_program.o $(OBJ)/device/symbolic_kernel.o \
             $(OBJ)/device/solve_kernel.o
 
-.PHONY: all lib oracle ref clean
+.PHONY: all lib oracle ref clean checked
 all: lib oracle
 
 lib: $(OUT)/libtacho_b200.so
@@ -46,6 +46,11 @@ $(OUT)/libtacho_b200.so: $(HOST_OBJS) $(DEV_OBJS)
 
 oracle:
 	$(MAKE) -C oracle
+
+# the same library with device-side bounds checks (TCG_CHECK traps on an
+# out-of-range index); tools/gpu_checked.sh runs the GPU tests on it
+checked:
+	$(MAKE) lib OUT=$(PKG)/lib_checked OBJ=build/obj_checked NVEXTRA=-DTCG_DEVICE_CHECKS
 
 ref:
 	$(MAKE) -C oracle ref

@@ -536,8 +536,9 @@ def run_ours(args):
 
 def run_sharded(args):
     """C6 over N GPUs (BASELINE.json configs[4], second half): rank r owns the
-    rows of the r-th level-log2(N) ND subtree, rank 0 also the separators above
-    them; each rank runs its rows (mode 5) and reads the few operands other
+    rows of the r-th level-log2(N) ND subtree; the N-1 separators above them
+    go one per part (--separators spread, the default; rank0 keeps them all on
+    rank 0); each rank runs its rows (mode 5) and reads the few operands other
     ranks own straight from their U through CUDA IPC peer mappings over
     NVLink (tcg_plan_part_problem / tcg_set_peers). Every rank resets its U
     (phase 1) before any rank's kernel starts (phase 2). value = nnz_u of the
@@ -556,7 +557,7 @@ def run_sharded(args):
     ps = plan.stats()
     u = an.pattern.pattern
     nnz, n = u.nnz(), a.nrows
-    owners = an.subtree_owners(world, separators=0)
+    owners = an.subtree_owners(world, separators=0 if args.separators == "rank0" else "spread")
     problem = plan.part_problem(world, owners, rank)
     fz = T.GpuFactorizer(plan, T.GpuOptions(device=dev, mode=5, timeout_s=60), problem=problem)
     handle, offset = fz.ipc_handle()
@@ -622,7 +623,7 @@ def run_sharded(args):
         "config": {"workload": WORKLOADS[args.config] + f", ND subtrees sharded over {world} GPUs",
                    "n": n, "nnz_u": nnz, "flow_rows": int(ps.flow_rows), "flow_depth": int(ps.flow_depth),
                    "rows_rank0": int(problem.nflow), "remote_operands_rank0": int(problem.remote_operands),
-                   "parallelism": f"ND subtrees over {world} ranks, peer reads over NVLink (CUDA IPC)",
+                   "parallelism": f"ND subtrees over {world} ranks, peer reads over NVLink (CUDA IPC), separators {args.separators}",
                    "l2": "flushed between steps (256 MiB write), U restored from device copy (untimed)",
                    "analysis_s": round(t_an, 3), "parity_vs_oracle": parity},
         "e2e": {"value": nnz / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz,
@@ -908,6 +909,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", type=int, default=0, help="0 auto (5: value flow), 1/2 task DAG")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--separators", default="spread", choices=["spread", "rank0"],
+                    help="C6 over N GPUs: ND separators spread over the parts (one each) or all on rank 0")
     ap.add_argument("--no-one-shot", action="store_true", help="skip the one-shot drop-in calls")
     ap.add_argument("--path", default="factor", choices=["factor", "symbolic", "solve"],
                     help="factor: the numeric factorization (headline); symbolic: level-k pattern on the "

@@ -120,18 +120,30 @@ class Analysis:
     # every span at a depth are the separators above it
     subtree_spans: Optional[dict] = None
 
-    def subtree_owners(self, nparts: int, separators: Optional[int] = 0) -> np.ndarray:
+    def subtree_owners(self, nparts: int, separators=0) -> np.ndarray:
         """Owner part of every row for a sharded run over `nparts` (a power of
-        two): the depth-log2(nparts) subtrees in order, the separators above
-        them to part `separators` (an extra part when it equals nparts)."""
+        two): the depth-log2(nparts) subtrees in order; the separators above
+        them to part `separators` (an extra part when it equals nparts), or
+        with separators="spread" each separator to the middle part among the
+        parts its subtree covers (depth 0 -> part N/2, depth 1 -> N/4 and 3N/4,
+        ...), so no part holds more than one separator and the critical
+        separator chain crosses GPUs once per ND level (ordering.hpp:68-86)."""
         depth = max(0, int(nparts).bit_length() - 1)
         if 1 << depth != nparts or depth not in (self.subtree_spans or {}):
             raise ValueError("subtree_owners: nparts must be a power of two up to 64")
+        spread = separators == "spread"
         lo, hi = self.subtree_spans[depth]
-        owners = np.full(self.perm.shape[0], separators, dtype=np.int32)
+        owners = np.full(self.perm.shape[0], -1 if spread else separators, dtype=np.int32)
         # more subtrees than parts (nodes with several children): contiguous groups
         for i, (a, b) in enumerate(zip(lo, hi)):
             owners[a:b] = i * nparts // len(lo)
+        if spread:
+            for d in range(depth - 1, -1, -1):  # deeper separators first
+                for a, b in zip(*self.subtree_spans[d]):
+                    seg = owners[a:b]
+                    parts = np.unique(seg[seg >= 0])
+                    seg[seg < 0] = parts[len(parts) // 2] if len(parts) else 0
+            owners[owners < 0] = 0
         return owners
 
 

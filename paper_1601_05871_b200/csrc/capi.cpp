@@ -907,6 +907,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   P.item = c->flow_item;
   P.slot = c->flow_slot;
   P.upd = c->flow_upd;
+  P.nupd = c->nflow_upd;
   P.a = q.a;
   if (from_copy) q.a = const_cast<double*>(q.vals);  // tells the prelude not to copy
   P.vals = vals;
@@ -1292,6 +1293,7 @@ static tcg_status run_flow_chunked(tcg_ctx* c, tcg_stats& S, int threads, const 
     P.item = c->flow_item;
     P.slot = c->flow_slot;
     P.upd = c->flow_upd;
+    P.nupd = c->nflow_upd;
     P.a = vals0;
     P.vals = vals;
     P.ctrl = c->ctrl;

@@ -88,6 +88,7 @@ struct FlowParams {
   int* m_row;
   double* m_pivot;
   long long nnz;         // values per member
+  long long nupd;        // (m, o) pairs in upd (bounds checks)
   int nrows;             // schedule rows (per member)
   int nbatch;            // members sharing the pattern
   double* const* peers;  // sharded (C6): every part's U, indexed by part; operands of other parts

@@ -44,6 +44,7 @@ template <int KB, class Cx>
 __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr) {
   const int ub = sr.x, ue = sr.y;
   if (ub >= ue) return v;
+  TCG_CHECK((ub >= 0 && ue <= C.P.nupd) || C.P.npeers > 1);
   // long programs (KB >= 3): pull the rest of the (m, o) pairs into L2 now, so
   // the batch-ahead loads below hit L2 instead of HBM (C3's programs are
   // 1.5 GB). B200: C3 4.03 -> 3.88, C4 1.474 -> 1.453 ms; with short programs
@@ -63,6 +64,7 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 #pragma unroll
     for (int j = 0; j < KB; ++j) {
       c[j] = p[j];
+      TCG_CHECK(j >= n || C.P.npeers > 1 || (c[j].x >= 0 && c[j].x <= c[j].y && c[j].y < C.P.nnz));
       xa[j] = (j < n) ? C.ld(c[j].x) : 0ull;
       xb[j] = (j < n) ? C.ld(c[j].y) : 0ull;
     }
@@ -343,6 +345,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
     __syncwarp();
     const int4 a = R.rec[k & 7];
     const int tb = a.x, L = a.y & kLenMask, dpos = a.z, t = a.w;
+    TCG_CHECK(tb >= 0 && L > 0 && static_cast<long long>(tb) + L <= P.nnz && dpos >= 0 && dpos <= tb);
     int4 sr0 = make_int4(0, 0, 0, 0);
     double a0 = 0.0;
     if (lane < L) {

@@ -164,6 +164,8 @@ __global__ void __launch_bounds__(256, MINB) factor_flow_pp(FlowParams P) {
         const int i = base + j + k * T;
         if (i < n) {
           mo[k] = pairs[i];
+          // both operands lie in one earlier row r: m = U(r,t) <= o = U(r,c) < this row
+          TCG_CHECK(mo[k].x >= 0 && mo[k].x <= mo[k].y && mo[k].y < P.nnz);
           xa[k] = Cx.ld(mo[k].x);
           xb[k] = Cx.ld(mo[k].y);
         }
@@ -200,12 +202,15 @@ __global__ void __launch_bounds__(256, MINB) factor_flow_pp(FlowParams P) {
     const int Lp = min(L, T);
     const int* u = ubr + (k % Lay::UR) * Lay::UBW;
     const int pb = u[0], pe = u[Lp];
+    TCG_CHECK(tb >= 0 && L > 0 && static_cast<long long>(tb) + L <= P.nnz && dpos >= 0 && dpos <= tb);
+    TCG_CHECK(pb >= 0 && pb <= pe && pe <= P.nupd);
     int myb = 0, mye = 0;
     double v = 0.0;
     if (j < Lp) {
       myb = u[j];
       mye = u[j + 1];
       v = inr[(k % Lay::UR) * T + j];
+      TCG_CHECK(pb <= myb && myb <= mye && mye <= pe);
     }
     // the pairs of this row's second chunk, then the rings D rows ahead
     if (pe - pb > C) fetch_pairs(xbuf + C, pb + C, min(pe - pb - C, C));

@@ -3,6 +3,21 @@
 
 #include <cuda_runtime.h>
 
+// Device-side bounds checks of the checks build (make checked: -DTCG_DEVICE_CHECKS):
+// an index outside its array traps the kernel, which the host then reports as
+// a CUDA error. (compute-sanitizer is not available on the GPU pool this was
+// measured on; tools/gpu_checked.sh runs the GPU tests on the checks build.)
+#ifdef TCG_DEVICE_CHECKS
+#define TCG_CHECK(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define TCG_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 namespace tcbdev {
 
 constexpr unsigned kFull = 0xffffffffu;
