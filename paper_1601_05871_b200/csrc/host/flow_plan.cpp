@@ -249,6 +249,15 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
   try {
     // units in natural order (row ascending; a row's Chol slice, then its chunks)
     const std::int32_t* cols = P.cols.data();
+    // Chol units hold at most chol_max = 32 coordinates (one warp pass); the
+    // rest of a longer diagonal-block slice runs as chunks dividing by U(t,t),
+    // on other warps, side by side with the Chol unit instead of after it in
+    // the same warp. On the critical path a second pass over a 33-64 wide
+    // slice cost its whole program after the late operand arrived (C3 trace:
+    // 1.8 ms of row tails on a 555-row path). B200: C3 3.25 -> 2.83 ms,
+    // elast6 0.96 -> 0.33, s27 1.11 -> 0.94, C4 unchanged; bitwise.
+    std::int32_t chol_max = 32;
+    if (const char* e = std::getenv("TCG_FLOW_CHOL_MAX")) chol_max = std::max(1, std::atoi(e));
     std::vector<std::int32_t> ufirst(static_cast<std::size_t>(n) + 1, 0), dsplit(static_cast<std::size_t>(n), 0);
     parallel_rows(n, threads, [&](index_t b, index_t e) {
       for (index_t t = b; t < e; ++t) {
@@ -261,13 +270,15 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
         const auto ds = static_cast<std::int32_t>(
             std::lower_bound(cols + rb, cols + re, ranges.ranges[owner[t]].end) - cols);
         dsplit[t] = ds;
-        ufirst[t + 1] = 1 + (re - ds + 31) / 32;
+        const std::int32_t ce = std::min(ds, rb + chol_max);  // end of the Chol unit
+        ufirst[t + 1] = 1 + (ds - ce + 31) / 32 + (re - ds + 31) / 32;
       }
     });
     for (index_t t = 0; t < n; ++t) ufirst[t + 1] += ufirst[t];
     const std::size_t U = static_cast<std::size_t>(ufirst[n]);
     if (U >= (1u << 31)) throw std::length_error("flow: too many units");
     // per unit: first position, length, first and last column, row
+    std::atomic<bool> miscount{false};
     std::vector<std::int32_t> u_tb(U), u_len(U), u_c0(U), u_c1(U), row_of(U);
     parallel_rows(n, threads, [&](index_t b, index_t e) {
       for (index_t t = b; t < e; ++t) {
@@ -281,10 +292,15 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
           row_of[g] = t;
           ++g;
         };
-        put(rb, ds - rb);
+        // (a row of at most 32 entries is one unit: dsplit = re, no chunks)
+        const std::int32_t ce = re - rb <= 32 ? re : std::min(ds, rb + chol_max);
+        put(rb, ce - rb);
+        for (std::int32_t c0 = ce; c0 < ds; c0 += 32) put(c0, std::min(ds - c0, 32));
         for (std::int32_t c0 = ds; c0 < re; c0 += 32) put(c0, std::min(re - c0, 32));
+        if (g != ufirst[t + 1]) miscount.store(true, std::memory_order_relaxed);
       }
     });
+    if (miscount.load()) throw std::logic_error("flow plan: unit count mismatch");
     mark("units");
 
     // Dependences of unit g (row t, last column c1(g)): for every source r of
