@@ -843,7 +843,11 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   int occ = 0;
   // poll back-off for long programs (flow_kernel.cu Ctx): thousands of lanes
   // poll the lines the critical rows write; sleeping between polls frees them
-  int backoff = kb >= 3 ? 200 : 0;
+  // B200, fixed back-off sweep (0-800 ns; the sleep only follows a poll that
+  // still saw kUnset): C3 (24.8 products per coordinate) 4.01 / 2.91 / 2.76 /
+  // 2.66 / 4.01 ms at 0 / 100 / 200 / 400 / 800; s27 (23.4) 1.26 / 0.93 /
+  // 0.89 / 0.88 / 1.25; C4 (12.4) 1.49 / 1.38 / 1.37 / 1.38 / 1.49
+  int backoff = kb >= 3 ? (mean >= 16.0 ? 400 : 200) : 0;
   if (const char* e = std::getenv("TCG_FLOW_BACKOFF")) backoff = std::atoi(e);
   int pp_w = 0, pp_k = 0, pp_n = 0, pp_m = 0, pp_d = 0, pp_b = -1;
   bool pp = !remote && !c->opt.trace && g == 32 && !weak && !dyn && phase == 0 &&
@@ -878,6 +882,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
     return TCG_INVALID;
   }
   if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
+  if (const char* e = std::getenv("TCG_FLOW_CTAS")) occ = std::max(1, std::min(occ, std::atoi(e)));
   const int grid = std::max(1, occ * c->sm_count);
   if (drain && grid <= drain_ctas) drain = false;
   const bool batch = c->nbatch > 1;

@@ -15,16 +15,25 @@ namespace {
 constexpr unsigned long long kCanonicalNaN = 0x7FFFFFFFFFFFFFFFull;
 
 // Slow path of a gather: the value is not written yet.
-// BO: nanoseconds a lane sleeps between re-polls (0: none)
+// Sleep of BO ns between re-polls (0: none). (An exponential back-off, 32 ns
+// doubling up to a cap, was slower everywhere on B200: C3 3.09-3.15 ms
+// against 2.78 at a fixed 400 ns, C4 1.48-1.65 against 1.40 at 100; its
+// extra registers cost a CTA per SM.)
+template <int BO>
+__device__ __forceinline__ void poll_pause(unsigned&) {
+  if (BO > 0) __nanosleep(BO);
+}
+
+// BO: poll back-off (poll_pause)
 template <int BO = 0>
 __device__ __forceinline__ unsigned long long wait_value(const double* p, Ctrl* ctrl,
                                                       unsigned long long t0,
                                                       unsigned long long tmo) {
-  unsigned spins = 0;
+  unsigned spins = 0, ns = 32;
   for (;;) {
     const unsigned long long x = ld_relaxed_u64(p);
     if (x != kUnset) return x;
-    if (BO) __nanosleep(BO);
+    poll_pause<BO>(ns);
     if (++spins == 1024u) {
       spins = 0;
       if (ld_relaxed(&ctrl->error.v) || gtimer() - t0 > tmo) {
@@ -65,8 +74,8 @@ __device__ __forceinline__ unsigned long long wait_value_sys(const double* p, Ct
 // BO: poll back-off in ns (a lane sleeps between re-polls of a value not yet
 // written). Long programs keep thousands of lanes polling the few lines the
 // critical rows are about to write; sleeping between polls frees the L2
-// slices serving them (B200, C3: 4.33 -> 3.45 ms at 300 ns, C4 1.61 -> 1.48
-// at 100 ns; short programs lose: C2 0.41 -> 0.42-0.45 ms).
+// slices serving them (B200, C3: 4.01 ms without, 2.66 ms at 400 ns; C4
+// 1.49 -> 1.37 at 200 ns; short programs lose: C2 0.41 -> 0.42-0.45 ms).
 template <int WEAK, int OPS = 0, int BO = 0>
 struct Ctx {
   const FlowParams& P;
@@ -105,11 +114,15 @@ struct Ctx {
   // re-polling them together costs one round trip instead of two
   __device__ __forceinline__ double product(int pa, unsigned long long xa, int pb, unsigned long long xb) const {
     if (OPS != 2 && (xa == kUnset || xb == kUnset)) {
-      unsigned spins = 0;
-      do {
+      unsigned spins = 0, ns = 32;
+      // re-poll, then sleep only if still unwritten: an operand loaded early
+      // (a batch ahead) is often final by the time it is settled, and must not
+      // pay a back-off for it
+      for (;;) {
         if (xa == kUnset) xa = ld_strong(pa);
         if (xb == kUnset) xb = ld_strong(pb);
-        if (BO) __nanosleep(BO);
+        if (xa != kUnset && xb != kUnset) break;
+        poll_pause<BO>(ns);
         if (++spins == 1024u) {
           spins = 0;
           if (ld_relaxed(&P.ctrl->error.v) || gtimer() - t0 > P.timeout_ns) {
@@ -117,7 +130,7 @@ struct Ctx {
             xa = xb = 0ull;
           }
         }
-      } while (xa == kUnset || xb == kUnset);
+      }
     }
     if (OPS != 2)  // settled by the loop above
       return __dmul_rn(__longlong_as_double(static_cast<long long>(xa)), __longlong_as_double(static_cast<long long>(xb)));
