@@ -962,6 +962,13 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
   if (drain) TCG_CUDA_TRY(c, cudaMemsetAsync(c->drain_done, 0, sizeof(unsigned) * drain_words, c->stream));
   P.ub = c->flow_ub;
+  // the per-lane kernel's Chol pivot through shared memory, the waiting lanes
+  // sleeping P.decouple ns between looks (flow_row): B200, C4 (12.4 products
+  // per coordinate) 1.38 -> 1.30 ms at 100 ns; with long diagonal programs
+  // the waiting lanes slow the diagonal's own (C3 2.65 -> 2.78-2.88, s27
+  // 0.87 -> 0.92), so only below 16 products per coordinate
+  P.decouple = mean < 16.0 ? 100 : 0;
+  if (const char* e = std::getenv("TCG_FLOW_DECOUPLE")) P.decouple = std::atoi(e);
   if (c->nflow > 0) {
     if (pp)
       TCG_CUDA_TRY(c, tcbdev::launch_flow_pp(P, grid, pp_w, pp_k, pp_n, pp_m, extras, drain ? 1 : 0, pp_b, pp_d,

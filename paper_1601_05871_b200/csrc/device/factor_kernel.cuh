@@ -99,6 +99,7 @@ struct FlowParams {
   double* drain_out;     // device-accessible pinned host buffer (nnz values)
   unsigned* drain_done;  // per batch of 32 groups of 64 values: groups copied (zeroed per launch)
   int row_ctas;          // CTAs that run rows
+  int decouple;          // per-lane kernel: Chol pivot through shared memory (lanes publish independently)
 };
 
 // Device-built update programs (flow_program.cu): U's pattern and its

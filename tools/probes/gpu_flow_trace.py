@@ -28,6 +28,7 @@ rec, order = t["flow_rec"], t["flow_item"]
 stamps = items[order].astype(np.int64)  # per schedule position: start, operands final, -, end
 t0 = stamps[:, 0].min()
 s, r, e = stamps[:, 0] - t0, stamps[:, 1] - t0, stamps[:, 3] - t0
+l0 = stamps[:, 2] - t0  # lane 0 (the diagonal of a Chol unit) done with its own program
 npos = len(rec)
 W = st.grid_ctas * st.threads_per_cta // 32
 L = rec[:, 1] & ((1 << 30) - 1)
@@ -77,7 +78,7 @@ while q >= 0:
 for k in acc:
     print(f"  {k:48s} {acc[k] / 1e3:8.1f} us  ({n[k]} steps)")
 if len(sys.argv) > 2:
-    np.savez_compressed(sys.argv[2], s=s, r=r, e=e, ready=ready, src=src_of, kind=kind, L=L, W=W)
+    np.savez_compressed(sys.argv[2], s=s, r=r, e=e, l0=l0, ready=ready, src=src_of, kind=kind, L=L, W=W)
 # the critical path row by row (the last 40 steps): length, products per
 # coordinate (max), and where its time went
 q = int(np.argmax(e))
