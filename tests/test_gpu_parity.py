@@ -69,6 +69,35 @@ def test_product_parallel_variants(T, golden, oracle, name, spec, monkeypatch):
     check_against_oracle(name, vals, golden, oracle)
 
 
+@pytest.mark.parametrize("name,decouple", [("c3", "100"), ("s27_16_k2", "20"), ("c4", "0"), ("elast6_k1", "400")])
+def test_pivot_through_shared_memory(T, golden, oracle, name, decouple, monkeypatch):
+    # per-lane kernel: the Chol pivot handed to the other lanes through shared
+    # memory (each lane publishes as soon as its program and the pivot are
+    # ready) or by a warp shuffle (0); bitwise either way
+    monkeypatch.setenv("TCG_FLOW_DECOUPLE", decouple)
+    monkeypatch.setenv("TCG_FLOW_PP", "0")
+    vals, st = gpu_factor(T, planned(name), mode=5)
+    assert st.row_kernel == 1
+    check_against_oracle(name, vals, golden, oracle)
+
+
+@pytest.mark.parametrize("name,cap", [("c3", "8"), ("elast6_k1", "16"), ("s27_16_k2", "24"), ("c4", "1000")])
+def test_chol_unit_caps(T, golden, oracle, name, cap, monkeypatch):
+    # units of the value flow with Chol units capped at 8..1000 coordinates
+    # (the rest of a wide diagonal slice as chunks dividing by U(t,t)): a
+    # different schedule, the same factor bit for bit
+    monkeypatch.setenv("TCG_FLOW_CHOL_MAX", cap)
+    _, an = analyzed(name)
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    f = plan.flow_tables()
+    L = f["flow_rec"][:, 1] & ((1 << 30) - 1)
+    chol = ((f["flow_rec"][:, 1] >> 30) & 1) == 0
+    long_rows = np.diff(f["row_ptr"])[f["flow_rec"][chol, 3]] > 32
+    assert L[chol][long_rows].max() <= int(cap)
+    vals, _ = gpu_factor(T, plan, mode=5)
+    check_against_oracle(name, vals, golden, oracle)
+
+
 @pytest.mark.parametrize("name", ["c1", "c5_m0", "c2", "rand_spd_200"])
 def test_per_lane_kernel_on_short_programs(T, golden, oracle, name, monkeypatch):
     monkeypatch.setenv("TCG_FLOW_PP", "0")

@@ -302,3 +302,25 @@ def test_init_factor_map_reproduces_host_init(name):
     got = np.where(m >= 0, 0.0 + an.a_permuted.values[np.maximum(m, 0)], 0.0)
     assert bitwise_equal(got, t["values"])
     assert len(np.unique(m[m >= 0])) == int((m >= 0).sum())  # every A entry feeds one slot at most
+
+
+@pytest.mark.parametrize("name,cap", [("elast6_k1", "1"), ("elast6_k1", "8"), ("grid20_k2_leaf4", "4"),
+                                      ("s27_16_k2", "16"), ("elast6_k1", "1000")])
+def test_chol_cap_schedules_replay_bitwise(T, name, cap, oracle, monkeypatch):
+    # Chol units capped at `cap` coordinates (flow_plan.cpp; the default is
+    # 32): still a partition of U, in an order where every read follows its
+    # write (emulate_flow asserts it), and the replay is factor_serial's bits
+    from checkers import emulate_flow, flow_programs
+    monkeypatch.setenv("TCG_FLOW_CHOL_MAX", cap)
+    _, an = analyzed(name)
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    f = plan.flow_tables()
+    rec = f["flow_rec"]
+    L = rec[:, 1] & ((1 << 30) - 1)
+    chol = ((rec[:, 1] >> 30) & 1) == 0
+    lens = np.diff(f["row_ptr"])
+    assert np.all(L[chol & (lens[rec[:, 3]] > 32)] <= int(cap))
+    assert np.all(L <= np.maximum(32, int(cap)))
+    slot, upd = flow_programs(f["row_ptr"], f["cols"])
+    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
+    assert bitwise_equal(emulate_flow(rec, f["values"], slot, upd), ref)
