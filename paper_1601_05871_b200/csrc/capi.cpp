@@ -573,6 +573,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     TCG_CUDA_TRY(c, cudaFree(c->prog_arena));
     c->prog_arena = nullptr;
   }
+  c->flow_ub = nullptr;  // lives in prog_arena (device-built programs only)
   c->nbatch = 1;
   // one arena: [cols][vals][vals0][tasks][items][srcs][succ][indeg][indeg0][queue][roots]
   //            [claim][fin][iflag][ctrl][trace]

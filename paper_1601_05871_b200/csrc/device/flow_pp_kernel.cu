@@ -330,7 +330,10 @@ __global__ void __launch_bounds__(256, MINB) factor_flow_pp(FlowParams P) {
 // by then, while here the whole dsub chain (up to ~200 per diagonal) runs
 // after the last product arrives. A poll back-off (50-200 ns) made every
 // short-program configuration slower (C6 1.426 -> 1.447-1.455, C2 0.362 ->
-// 0.372-0.378 ms).
+// 0.372-0.378 ms). So did 4-byte products ((source index << 16) | in-row
+// offset, the row's source positions staged per unit): C6 1.43 -> 1.55, C5
+// batch 1.41 -> 1.78 ms, DRAM per C6 launch only 1.21 -> 1.19 GB -- the
+// traffic is operand re-reads, not the programs.
 #define TCG_PP_VARIANTS(X)                                                                                   \
   X(1, 2, 1, 4, 0, 0, 0, 2) X(1, 2, 1, 4, 0, 1, 0, 2) X(1, 2, 1, 4, 1, 0, 0, 2) X(1, 2, 1, 4, 1, 1, 0, 2)       \
   X(2, 2, 2, 3, 0, 0, 0, 1) X(2, 2, 2, 3, 0, 1, 0, 1) X(2, 2, 2, 3, 1, 0, 0, 1) X(2, 2, 2, 3, 1, 1, 0, 1)       \
