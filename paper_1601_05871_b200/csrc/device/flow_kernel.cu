@@ -1,12 +1,14 @@
-// Value-flow schedule (mode 5): the static row schedule of mode 4 without
-// flags, fences or any per-row synchronisation.
+// Value-flow schedule (mode 5, the default executor), one lane per
+// coordinate: a static order of the finalising rows without flags, fences or
+// any per-row synchronisation. (flow_pp_kernel.cu runs the same schedule with
+// a unit's products spread over a group of warps, for short programs.)
 //
-// Only the finalising rows run (the Chol/Trsm items; plan.cpp build_flow
-// folds every Herk/Gemm product of a slice into the row that finalises it,
-// in generation order), so every coordinate of U is written exactly once.
+// Only the finalising rows run (the Chol/Trsm units of flow_plan.cpp, which
+// fold every Herk/Gemm product of a slice into the row that finalises it, in
+// generation order), so every coordinate of U is written exactly once.
 // The prelude snapshots the input values and sets the output to kUnset (a
-// signalling NaN, which arithmetic never produces); a row gathers its
-// operands with 64-bit strong loads and re-polls any that still read kUnset.
+// NaN payload arithmetic never produces); a row gathers its operands with
+// 64-bit strong loads and re-polls any that still read kUnset.
 // A value is single-copy atomic, so a reader sees either kUnset or the final
 // value: the data is its own flag, and a hand-off between rows costs one
 // store reaching L2 plus one load, instead of store + release fence + flag
@@ -15,8 +17,8 @@
 // Warp w of the W co-resident warps runs positions w, w+W, ... The order is
 // topological (level, then falling height), so the row at the smallest
 // unfinished position only reads values that are final: the schedule cannot
-// deadlock while all warps are resident (grid = occupancy; a watchdog ends
-// the kernel otherwise). Per coordinate the products arrive in ascending
+// deadlock while all warps are resident (a cooperative launch; a watchdog
+// ends the kernel otherwise). Per coordinate the products arrive in ascending
 // source row, so the factor is bitwise equal to factor_serial
 // (factorize.hpp:94-130; kernels.hpp:40-132 for one target row).
 #include <cuda_runtime.h>
