@@ -116,7 +116,8 @@ typedef struct {
 } tcg_problem;
 
 typedef struct {
-  int32_t threads_per_cta;  /* 128, 256 or 512; 0 = default (256) */
+  int32_t threads_per_cta;  /* task executors (modes 1/2): 128, 256 or 512; 0 = default (256);
+                               mode 5 always runs 256-thread CTAs */
   int32_t ctas_per_sm;      /* 0 = occupancy maximum */
   int32_t staging_cap;      /* target-row entries staged per warp; 0 = auto */
   double timeout_s;         /* device watchdog; 0 = default (30 s) */
@@ -127,8 +128,8 @@ typedef struct {
                                sorted indices or 2 = precomputed update programs; 5 = static
                                schedule of the finalising rows, readers polling the values
                                themselves (no flags, no fences) */
-  int32_t lanes_per_row;    /* mode 5: lanes working on one row (32, or 8 with 256 threads);
-                               0 = default (32) */
+  int32_t lanes_per_row;    /* ignored (kept for the ABI): mode 5 runs whole warps or
+                               groups of warps per row, chosen by program length */
 } tcg_options;
 
 typedef struct {

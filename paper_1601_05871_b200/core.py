@@ -564,7 +564,7 @@ class GpuOptions:
     trace: bool = False
     mode: int = 0  # 0 auto (5); task DAG (expands the plan): 1 device merge, 2 update programs;
     #                5 static value flow (finalising rows, the values are their own flags)
-    lanes_per_row: int = 0  # mode 5: lanes per row (32, or 8), 0 = 32
+    lanes_per_row: int = 0  # ignored (ABI field): mode 5 picks whole warps or warp groups per row
 
 
 class GpuFactorizer:

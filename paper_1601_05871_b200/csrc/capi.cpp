@@ -774,6 +774,9 @@ static bool pick_pp(const tcg_ctx* c, double mean, int* w, int* k, int* n, int* 
 // launch stream.
 static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* host_in = nullptr,
                            double* host_out = nullptr, int phase = 0, const double* host_a = nullptr) {
+  // the value-flow kernels run 256-thread CTAs of whole warps (tcg_options.threads_per_cta
+  // applies to the task executors, lanes_per_row is kept for the ABI and ignored)
+  threads = 256;
   // gather batch from the mean products per coordinate (flow_kernel.cu variants)
   const double mean = c->nnz > 0 ? static_cast<double>(c->nflow_upd) / static_cast<double>(c->nnz) : 0.0;
   // short programs: one product in flight per lane where the chain binds (B200, KB 1 vs 2: C2
@@ -788,17 +791,9 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // with KB = 3 the fifth CTA costs more than it hides (C3 4.03 -> 4.15, C4 1.47 -> 1.60)
   if (threads == 256 && kb <= 2 && one_local) minb = 5;
   if (const char* e = std::getenv("TCG_FLOW_MINB")) minb = std::atoi(e);
-  // lanes per row: a whole warp unless asked otherwise (flow_kernel.cu)
-  const int g = c->opt.lanes_per_row > 0 ? c->opt.lanes_per_row : 32;
-  int weak = 0, dyn = 0;
-  if (const char* e = std::getenv("TCG_FLOW_WEAK")) weak = std::atoi(e);
-  if (const char* e = std::getenv("TCG_FLOW_DYN")) dyn = std::atoi(e);
   int remote = c->npeers > 1 ? 1 : 0;  // sharded: operands of other parts via peers
   if (const char* e = std::getenv("TCG_FLOW_REMOTE")) remote = std::atoi(e) ? 1 : remote;
-  if (weak || dyn || g != 32) kb = 4;  // those variants exist with KB = 4 only
-  // shared-memory staged metadata (factor_flow_pipe) where it exists
-  bool pipe = !weak && !dyn && g == 32;
-  if (const char* e = std::getenv("TCG_FLOW_PIPE")) pipe = pipe && std::atoi(e) != 0;
+  bool pipe = true;  // the per-lane kernel (factor_flow_pipe), unless the product-parallel one runs
   int extras = (c->nbatch > 1 || c->opt.trace) ? 1 : 0;
   if (const char* e = std::getenv("TCG_FLOW_EXTRAS")) extras = std::atoi(e) ? 1 : extras;
   // end to end: CTAs of the launch copy the factor to the host as it becomes
@@ -851,8 +846,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   int backoff = kb >= 3 ? (mean >= 16.0 ? 400 : 200) : 0;
   if (const char* e = std::getenv("TCG_FLOW_BACKOFF")) backoff = std::atoi(e);
   int pp_w = 0, pp_k = 0, pp_n = 0, pp_m = 0, pp_d = 0, pp_b = -1;
-  bool pp = !remote && !c->opt.trace && g == 32 && !weak && !dyn && phase == 0 &&
-            pick_pp(c, mean, &pp_w, &pp_k, &pp_n, &pp_m, &pp_d, &pp_b);
+  bool pp = !remote && !c->opt.trace && phase == 0 && pick_pp(c, mean, &pp_w, &pp_k, &pp_n, &pp_m, &pp_d, &pp_b);
   if (pp) {
     if (pp_b < 0) pp_b = backoff;
     size_t pp_smem = 0;
@@ -867,17 +861,22 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
       pp = false;
     }
   }
-  if (!pp && pipe && tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0, backoff) != cudaSuccess) {
-    cudaGetLastError();
-    pipe = false;
-    drain = false;
+  if (!pp) {
+    pipe = true;
+    cudaError_t oe = tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0, backoff);
+    if (oe != cudaSuccess && drain) {  // no drain variant: a copy after the launch
+      cudaGetLastError();
+      drain = false;
+      oe = tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, 0, backoff);
+    }
+    if (oe == cudaErrorInvalidValue) {
+      cudaGetLastError();
+      c->err = "no value-flow kernel variant for KB " + std::to_string(kb) + ", " + std::to_string(minb) +
+               " CTAs/SM (TCG_FLOW_KB / TCG_FLOW_MINB)";
+      return TCG_INVALID;
+    }
+    TCG_CUDA_TRY(c, oe);
   }
-  cudaError_t oe = (pipe || pp) ? cudaSuccess : tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
-  if (oe == cudaErrorInvalidValue && kb != 4) {  // no such variant: the KB = 4 one
-    kb = 4;
-    oe = tcbdev::flow_occupancy(threads, kb, minb, g, weak, dyn, remote, &occ);
-  }
-  TCG_CUDA_TRY(c, oe);
   if (occ < 1) {
     c->err = "value-flow kernel does not fit on an SM";
     return TCG_INVALID;
@@ -974,10 +973,9 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
     if (pp)
       TCG_CUDA_TRY(c, tcbdev::launch_flow_pp(P, grid, pp_w, pp_k, pp_n, pp_m, extras, drain ? 1 : 0, pp_b, pp_d,
                                              c->stream));
-    else if (pipe)
+    else
       TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, extras, c->stream,
                                                drain ? 1 : 0, backoff));
-    else TCG_CUDA_TRY(c, tcbdev::launch_flow(P, grid, threads, kb, minb, g, weak, dyn, remote, c->stream));
   }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
   c->pristine = false;  // the working values now hold the factor
@@ -1005,7 +1003,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   S.mode = 5;
   S.drain_ctas = drain ? drain_ctas : 0;
   if (host_a) c->pristine = false;
-  S.lanes_per_row = pp ? 32 * pp_w : g;
+  S.lanes_per_row = pp ? 32 * pp_w : 32;
   S.row_kernel = pp ? 2 : 1;
   if (pp) S.threads_per_cta = 256;
   if (pp) S.staging_cap = pp_k;

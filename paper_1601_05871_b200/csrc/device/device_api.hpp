@@ -16,11 +16,7 @@ cudaError_t launch_factor(const Params& p, int grid, int threads, size_t smem, c
 
 
 
-cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int dyn, int remote,
-                           int* ctas_per_sm);
 cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStream_t st);
-cudaError_t launch_flow(const FlowParams& p, int grid, int threads, int kb, int minb, int g,
-                        int weak, int dyn, int remote, cudaStream_t st);
 
 cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm,
                            int drain = 0, int backoff_ns = 0);

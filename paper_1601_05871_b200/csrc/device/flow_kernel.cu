@@ -160,140 +160,10 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
 
 }  // namespace
 
-// G lanes per row: a warp runs 32 / G rows side by side.
-// DYN = 0: row group g of the W co-resident groups runs positions g, g+W, ...
-// DYN = 1: CTA c owns the positions c, c+grid, c+2*grid, ... and its row
-//   groups take them in that order from a shared-memory counter, each
-//   holding at most the row it runs plus two it prefetches; a row blocked on
-//   an operand then holds up only its own group, not the rows dealt after it.
-//   Still deadlock-free: the lowest unfinished position is either some
-//   group's current row (its operands are final) or was never handed out,
-//   which cannot be while every group of its CTA holds lower rows.
-template <int THREADS, int KB, int MINB, int G, int WEAK, int DYN, int REMOTE>
-__global__ void __launch_bounds__(THREADS, MINB) factor_flow(FlowParams P) {
-  constexpr int kGroups = THREADS / G;
-  constexpr int kLenMask = (1 << 30) - 1;
-  const int lane = threadIdx.x & 31;
-  const int gl = lane & (G - 1);
-  const int lead = lane & ~(G - 1);
-  const unsigned gmask = G == 32 ? kFull : (((1u << G) - 1u) << lead);
-  const int W = gridDim.x * kGroups;
-  Ctx<WEAK, REMOTE ? 2 : 0> C{P, gtimer(), P.vals, P.a, 0};
-  int ran = 0, executed = 0, anyfail = 0;
-  // batch: position pos is schedule row pos / nbatch of member pos % nbatch
-  // (the members of one row sit side by side, so level order is kept)
-  const int nrows = P.nrows * P.nbatch;
-  auto member_of = [&](int p, int& q) {
-    q = P.nbatch == 1 ? p : p / P.nbatch;
-    return p - q * P.nbatch;
-  };
-  __shared__ int s_next;
-  if (DYN) {
-    if (threadIdx.x == 0) s_next = 0;
-    __syncthreads();
-  }
-  auto grab = [&](int prev) -> int {
-    if (!DYN) return prev + W;
-    int k = 0;
-    if (gl == 0) k = atomicAdd(&s_next, 1);
-    k = __shfl_sync(gmask, k, lead);
-    return blockIdx.x + k * static_cast<int>(gridDim.x);
-  };
-  int pos = DYN ? grab(0) : blockIdx.x * kGroups + threadIdx.x / G;
-  int npos = grab(pos);
-  // two-deep pipeline of the immutable inputs: the record of the position
-  // after next, and the next position's first slot record and input value,
-  // are in flight while the current row gathers
-  const int4 z = make_int4(0, 0, 0, 0);
-  int4 a = z, na = z, sr0 = z;
-  double a0 = 0.0;
-  auto rec_of = [&](int p) {
-    int q;
-    member_of(p, q);
-    return __ldg(P.rec + q);
-  };
-  auto input_of = [&](int p) {
-    int q;
-    return P.a + static_cast<long long>(member_of(p, q)) * P.nnz;
-  };
-  if (pos < nrows) {
-    a = rec_of(pos);
-    if (gl < (a.y & kLenMask)) {
-      sr0 = __ldg(P.slot + a.x + gl);
-      a0 = input_ld(P, input_of(pos) + a.x + gl);
-    }
-  }
-  if (npos < nrows) na = rec_of(npos);
-  while (pos < nrows) {
-    const int nnpos = npos < nrows ? grab(npos) : npos;
-    const int4 nna = nnpos < nrows ? rec_of(nnpos) : z;
-    int4 nsr0 = z;
-    double na0 = 0.0;
-    if (npos < nrows && gl < (na.y & kLenMask)) {
-      nsr0 = __ldg(P.slot + na.x + gl);
-      na0 = input_ld(P, input_of(npos) + na.x + gl);
-    }
-    const int tb = a.x, L = a.y & kLenMask, dpos = a.z, t = a.w;
-    const bool chol = ((a.y >> 30) & 1) == kChol;
-    const bool exported = a.y < 0;  // sharded: bit 31 = some other part reads this row
-    int q;
-    C.member = member_of(pos, q);
-    C.vals = P.vals + static_cast<long long>(C.member) * P.nnz;
-    C.a = P.a + static_cast<long long>(C.member) * P.nnz;
-    const bool traced = P.trace && gl == 0 && C.member == 0;
-    // trace: per item {start, operands final, 0, end} (4 words, member 0)
-    unsigned long long* stamp = P.trace && C.member == 0 ? P.trace + 4 * static_cast<long long>(P.item[q]) : nullptr;
-    if (traced) stamp[0] = gtimer();
-    // breakdown (reference factorize.hpp:146-167): the member's later rows
-    // are skipped; one decision per group
-    if ((ran & 15) == 0) {
-      anyfail = gl == 0 ? ld_relaxed(&P.ctrl->failed.v) : 0;
-      anyfail = __shfl_sync(gmask, anyfail, lead);
-    }
-    int latched = 0;
-    if (anyfail) {
-      latched = gl == 0 ? ld_relaxed(P.m_failed + C.member) : 0;
-      latched = __shfl_sync(gmask, latched, lead);
-    }
-    if (!latched) {
-      if (chol)
-        flow_row<kChol, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr,
-                               exported);
-      else
-        flow_row<kTrsm, KB, G>(C, tb, L, dpos, t, gl, gmask, lead, a0, sr0, stamp ? stamp + 1 : nullptr,
-                               exported);
-      ++executed;
-    } else {
-      // skipped rows keep their input values (readers must not wait forever)
-      for (int k = gl; k < L; k += G) {
-        const double* ap = C.a + tb + k;
-        unsigned long long x = static_cast<unsigned long long>(
-            __double_as_longlong(input_settle(P, ap, input_ld(P, ap), C.t0)));
-        if (x == kUnset) x = kCanonicalNaN;
-        if (decltype(C)::kSysPublish && exported) st_relaxed_sys_u64(C.vals + tb + k, x);
-        else st_relaxed_u64(C.vals + tb + k, x);
-      }
-    }
-    if (traced) stamp[3] = gtimer();
-    ++ran;
-    pos = npos;
-    npos = nnpos;
-    a = na;
-    na = nna;
-    sr0 = nsr0;
-    a0 = na0;
-  }
-  if (gl == 0) {
-    if (ran) atomicAdd(&P.ctrl->done.v, ran);
-    if (executed) atomicAdd(&P.ctrl->executed.v, executed);
-  }
-}
-
-
-// factor_flow with the per-row metadata staged in shared memory (PIPE): a
+// The per-lane value-flow kernel, per-row metadata staged in shared memory: a
 // row of a short program is shorter than an L2 round trip, so prefetching its
-// record and first slot one row ahead in registers still exposes the round
-// trip (the loop-carried register copies wait for the loads). Here each warp
+// record and first slot one row ahead in registers exposed the round trip
+// (the loop-carried register copies wait for the loads). Here each warp
 // keeps rings in shared memory filled by cp.async (LDGSTS): the record four
 // rows ahead, the lanes' first slot records and input values two rows ahead;
 // iteration k waits only for the copies issued at iteration k-2.
@@ -474,38 +344,6 @@ __global__ void flow_prepare(FlowPrepParams Q) {
   }
 }
 
-// KB: products gathered per batch; MINB: CTAs per SM the register budget
-// targets; G: lanes per row. Measured on B200 (C1-C5): whole warps per row
-// win everywhere -- the groups of a warp diverge on their polls and product
-// counts, and their rows serialise; G = 8 is kept for experiments.
-// Measured on B200 (one session, mode 5): gather batch KB 2 beats 4 where
-// programs are short (C2 0.69 -> 0.65 ms, C5 0.23 -> 0.20 ms) and 3 where
-// they are long (C4 2.26 -> 2.01 ms); the host picks KB from the mean
-// products per coordinate.
-#define TCG_FLOW_VARIANTS(X)                                                                   \
-  X(256, 1, 3, 32, 0, 0, 0) X(256, 2, 3, 32, 0, 0, 0) X(256, 3, 3, 32, 0, 0, 0) X(256, 4, 3, 32, 0, 0, 0) \
-  X(256, 1, 4, 32, 0, 0, 0) X(256, 2, 4, 32, 0, 0, 0) X(256, 4, 3, 32, 1, 0, 0) X(256, 4, 3, 32, 0, 1, 0) \
-  X(128, 2, 6, 32, 0, 0, 0) X(128, 3, 6, 32, 0, 0, 0) X(128, 4, 6, 32, 0, 0, 0)                         \
-  X(512, 2, 1, 32, 0, 0, 0) X(512, 3, 1, 32, 0, 0, 0) X(512, 4, 1, 32, 0, 0, 0)                         \
-  X(256, 2, 3, 32, 0, 0, 1) X(256, 3, 3, 32, 0, 0, 1) X(256, 4, 3, 32, 0, 0, 1)                         \
-  X(128, 4, 6, 32, 0, 0, 1) X(512, 4, 1, 32, 0, 0, 1) X(256, 4, 3, 8, 0, 0, 0)
-
-static const void* flow_kernel_for(int threads, int kb, int minb, int g, int weak, int dyn, int remote) {
-#define X(T, K, M, GG, WK, D, R)                                                                     \
-  if (threads == T && kb == K && minb == M && g == GG && weak == WK && dyn == D && remote == R)      \
-    return reinterpret_cast<const void*>(&factor_flow<T, K, M, GG, WK, D, R>);
-  TCG_FLOW_VARIANTS(X)
-#undef X
-  return nullptr;
-}
-
-cudaError_t flow_occupancy(int threads, int kb, int minb, int g, int weak, int dyn, int remote,
-                           int* ctas_per_sm) {
-  const void* k = flow_kernel_for(threads, kb, minb, g, weak, dyn, remote);
-  if (!k) return cudaErrorInvalidValue;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas_per_sm, k, threads, 0);
-}
-
 // init_factor_values on the device: U slot t <- 0.0 + A[map[t]] (the host
 // version's `vals[t] += a` from zero, so -0.0 becomes +0.0 exactly as there),
 // 0.0 for fill; for every member of a batch; also into the restore copy.
@@ -584,18 +422,6 @@ cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStrea
   blocks = blocks < 1 ? 1 : (blocks > 4LL * sm_count ? 4LL * sm_count : blocks);
   flow_prepare<<<static_cast<int>(blocks), 256, 0, st>>>(q);
   return cudaGetLastError();
-}
-
-cudaError_t launch_flow(const FlowParams& p, int grid, int threads, int kb, int minb, int g,
-                        int weak, int dyn, int remote, cudaStream_t st) {
-#define X(T, K, M, GG, WK, D, R)                                                                   \
-  if (threads == T && kb == K && minb == M && g == GG && weak == WK && dyn == D && remote == R) {  \
-    return launch_resident(reinterpret_cast<const void*>(&factor_flow<T, K, M, GG, WK, D, R>), grid, T, 0, st, \
-                           p);                                                                             \
-  }
-  TCG_FLOW_VARIANTS(X)
-#undef X
-  return cudaErrorInvalidValue;
 }
 
 }  // namespace tcbdev
