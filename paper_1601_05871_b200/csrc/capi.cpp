@@ -794,7 +794,8 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   int remote = c->npeers > 1 ? 1 : 0;  // sharded: operands of other parts via peers
   if (const char* e = std::getenv("TCG_FLOW_REMOTE")) remote = std::atoi(e) ? 1 : remote;
   bool pipe = true;  // the per-lane kernel (factor_flow_pipe), unless the product-parallel one runs
-  int extras = (c->nbatch > 1 || c->opt.trace) ? 1 : 0;
+  // the member / trace arithmetic; sharded runs use those variants too (their remote reads exist there)
+  int extras = (c->nbatch > 1 || c->opt.trace || remote) ? 1 : 0;
   if (const char* e = std::getenv("TCG_FLOW_EXTRAS")) extras = std::atoi(e) ? 1 : extras;
   // end to end: CTAs of the launch copy the factor to the host as it becomes
   // final (the D2H overlaps the factorization); needs a pinned, mapped buffer
