@@ -1,4 +1,4 @@
-O=gpurun_out/${R:-r2e}; mkdir -p $O
+O=gpurun_out/${R:-all}; mkdir -p $O
 R=$R bash tools/gpu_checked.sh
 R=$R bash tools/gpu_round.sh
 for c in c2 c4 c6 c5b c1 c5; do

@@ -1,4 +1,4 @@
-O=gpurun_out/pp4; mkdir -p $O; rm -f $O/*.txt
+O=gpurun_out/sweep_pp; mkdir -p $O; rm -f $O/*.txt
 V='"" 1,2,1,4,2,0 2,2,4,3,1,0 1,2,2,4,2,0 2,2,2,3,1,0 2,2,2,4,1,0 2,1,4,4,1,0 1,2,1,5,1,0 4,2,2,3,1,0'
 for c in c6 c2 c5_m0 c1; do
   eval timeout 600 python tools/probes/pp_sweep.py $c $V >> $O/sweep.txt 2>&1
