@@ -256,22 +256,45 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
     // slice cost its whole program after the late operand arrived (C3 trace:
     // 1.8 ms of row tails on a 555-row path). B200: C3 3.25 -> 2.83 ms,
     // elast6 0.96 -> 0.33, s27 1.11 -> 0.94, C4 unchanged; bitwise.
-    std::int32_t chol_max = 32;
+    // With panel > 0 (TCG_FLOW_PANEL) the diagonal-block slice is cut at fixed
+    // columns instead (block begin + k * panel): the Chol unit of row t ends
+    // at its panel's end, so row t+1 of the same panel finds every operand it
+    // takes from row t in t's Chol unit, never in a chunk finishing one hop
+    // later. B200, panel 32: elast6 0.357 -> 0.312 ms (depth 350 -> 255), but
+    // C3 2.66 -> 2.69 and C4 1.30 -> 1.34 (more units, depth 725 -> 705 only),
+    // so it is off by default.
+    std::int32_t chol_max = 32, panel = 0;
     if (const char* e = std::getenv("TCG_FLOW_CHOL_MAX")) chol_max = std::max(1, std::atoi(e));
-    std::vector<std::int32_t> ufirst(static_cast<std::size_t>(n) + 1, 0), dsplit(static_cast<std::size_t>(n), 0);
+    if (const char* e = std::getenv("TCG_FLOW_PANEL")) panel = std::clamp(std::atoi(e), 0, 32);
+    // the units of row t in order: emit(first position, length)
+    auto split_row = [&](index_t t, auto&& emit) {
+      const std::int32_t rb = P.row_ptr[t], re = P.row_ptr[t + 1];
+      if (re - rb <= 32) {  // one warp pass: the whole row
+        emit(rb, re - rb);
+        return;
+      }
+      const Range blk = ranges.ranges[owner[t]];
+      const auto ds = static_cast<std::int32_t>(std::lower_bound(cols + rb, cols + re, blk.end) - cols);
+      if (panel > 0) {
+        auto panel_end = [&](index_t c) { return std::min<index_t>(blk.end, blk.begin + panel * ((c - blk.begin) / panel + 1)); };
+        for (std::int32_t q = rb; q < ds;) {
+          const auto qe = static_cast<std::int32_t>(std::lower_bound(cols + q, cols + ds, panel_end(cols[q])) - cols);
+          emit(q, qe - q);
+          q = qe;
+        }
+      } else {
+        const std::int32_t ce = std::min(ds, rb + chol_max);
+        emit(rb, ce - rb);
+        for (std::int32_t c0 = ce; c0 < ds; c0 += 32) emit(c0, std::min(ds - c0, 32));
+      }
+      for (std::int32_t c0 = ds; c0 < re; c0 += 32) emit(c0, std::min(re - c0, 32));
+    };
+    std::vector<std::int32_t> ufirst(static_cast<std::size_t>(n) + 1, 0);
     parallel_rows(n, threads, [&](index_t b, index_t e) {
       for (index_t t = b; t < e; ++t) {
-        const std::int32_t rb = P.row_ptr[t], re = P.row_ptr[t + 1];
-        if (re - rb <= 32) {
-          dsplit[t] = re;
-          ufirst[t + 1] = 1;
-          continue;
-        }
-        const auto ds = static_cast<std::int32_t>(
-            std::lower_bound(cols + rb, cols + re, ranges.ranges[owner[t]].end) - cols);
-        dsplit[t] = ds;
-        const std::int32_t ce = std::min(ds, rb + chol_max);  // end of the Chol unit
-        ufirst[t + 1] = 1 + (ds - ce + 31) / 32 + (re - ds + 31) / 32;
+        std::int32_t k = 0;
+        split_row(t, [&](std::int32_t, std::int32_t) { ++k; });
+        ufirst[t + 1] = k;
       }
     });
     for (index_t t = 0; t < n; ++t) ufirst[t + 1] += ufirst[t];
@@ -283,20 +306,14 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
     parallel_rows(n, threads, [&](index_t b, index_t e) {
       for (index_t t = b; t < e; ++t) {
         std::int32_t g = ufirst[t];
-        const std::int32_t rb = P.row_ptr[t], re = P.row_ptr[t + 1], ds = dsplit[t];
-        auto put = [&](std::int32_t tb, std::int32_t len) {
+        split_row(t, [&](std::int32_t tb, std::int32_t len) {
           u_tb[g] = tb;
           u_len[g] = len;
           u_c0[g] = cols[tb];
           u_c1[g] = cols[tb + len - 1];
           row_of[g] = t;
           ++g;
-        };
-        // (a row of at most 32 entries is one unit: dsplit = re, no chunks)
-        const std::int32_t ce = re - rb <= 32 ? re : std::min(ds, rb + chol_max);
-        put(rb, ce - rb);
-        for (std::int32_t c0 = ce; c0 < ds; c0 += 32) put(c0, std::min(ds - c0, 32));
-        for (std::int32_t c0 = ds; c0 < re; c0 += 32) put(c0, std::min(re - c0, 32));
+        });
         if (g != ufirst[t + 1]) miscount.store(true, std::memory_order_relaxed);
       }
     });

@@ -324,3 +324,30 @@ def test_chol_cap_schedules_replay_bitwise(T, name, cap, oracle, monkeypatch):
     slot, upd = flow_programs(f["row_ptr"], f["cols"])
     ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
     assert bitwise_equal(emulate_flow(rec, f["values"], slot, upd), ref)
+
+
+@pytest.mark.parametrize("name,panel", [("elast6_k1", "32"), ("elast6_k1", "8"), ("s27_16_k2", "16"),
+                                        ("grid20_k2_leaf4", "4")])
+def test_panel_schedules_replay_bitwise(T, name, panel, oracle, monkeypatch):
+    # diagonal-block slices cut at fixed column panels (TCG_FLOW_PANEL): every
+    # unit of a long row stays inside one panel of its block, U is still
+    # partitioned, reads follow writes, and the replay is factor_serial's bits
+    from checkers import emulate_flow, flow_programs
+    monkeypatch.setenv("TCG_FLOW_PANEL", panel)
+    _, an = analyzed(name)
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    f = plan.flow_tables()
+    rec, cols = f["flow_rec"], f["cols"]
+    L = rec[:, 1] & ((1 << 30) - 1)
+    b = an.ranges.bounds
+    lens = np.diff(f["row_ptr"])
+    for tb, ln, t in zip(rec[:, 0], L, rec[:, 3]):
+        if lens[t] <= 32:
+            continue
+        k = int(np.searchsorted(b, t, side="right")) - 1  # t's block [b[k], b[k+1])
+        c = cols[tb:tb + ln]
+        if c[-1] < b[k + 1]:  # inside the diagonal block: one panel
+            assert len(set(((c - b[k]) // int(panel)).tolist())) == 1
+    slot, upd = flow_programs(f["row_ptr"], f["cols"])
+    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
+    assert bitwise_equal(emulate_flow(rec, f["values"], slot, upd), ref)
