@@ -98,6 +98,31 @@ def test_chol_unit_caps(T, golden, oracle, name, cap, monkeypatch):
     check_against_oracle(name, vals, golden, oracle)
 
 
+@pytest.mark.parametrize("name,spec", [("c3", "1,2,1,4,2,0"), ("s27_16_k2", "1,2,2,4,2,0"),
+                                       ("elast6_k1", "1,2,1,4,2,0")])
+def test_product_parallel_passes_over_wide_units(T, golden, oracle, name, spec, monkeypatch):
+    # Chol units up to 64-81 coordinates (TCG_FLOW_CHOL_MAX=128) on groups of
+    # 32 or 64 threads: the product-parallel kernel's later passes over a unit
+    # (coordinates past the group, the pivot kept from pass 0)
+    monkeypatch.setenv("TCG_FLOW_CHOL_MAX", "128")
+    monkeypatch.setenv("TCG_FLOW_PP", spec)
+    _, an = analyzed(name)
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    L = plan.flow_tables()["flow_rec"][:, 1] & ((1 << 30) - 1)
+    assert L.max() > 32 * int(spec.split(",")[0])
+    vals, st = gpu_factor(T, plan, mode=5)
+    assert st.row_kernel == 2
+    check_against_oracle(name, vals, golden, oracle)
+
+
+def test_empty_matrix(T):
+    # n = 0: nothing to factor, an empty factor back (factorize.hpp:134-235 with no ranges)
+    a = T.CsrMatrix.from_arrays(0, np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    fp = T.levelk_pattern(a, 0)
+    res = T.factor_by_blocks_gpu(a, fp, T.RangeList(np.array([0], np.int32)))
+    assert res.factor.values.size == 0 and res.factor.nrows == 0
+
+
 @pytest.mark.parametrize("name", ["c1", "c5_m0", "c2", "rand_spd_200"])
 def test_per_lane_kernel_on_short_programs(T, golden, oracle, name, monkeypatch):
     monkeypatch.setenv("TCG_FLOW_PP", "0")
