@@ -23,7 +23,7 @@ HOST_SRCS := $(SRC)/host/sparse.cpp $(SRC)/host/analysis.cpp $(SRC)/host/generat
              $(SRC)/host/plan.cpp $(SRC)/host/flow_plan.cpp $(SRC)/capi.cpp $(SRC)/symbolic_capi.cpp $(SRC)/solve_capi.cpp
 HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
 DEV_OBJS := $(OBJ)/device/factor_kernel.o \
-            $(OBJ)/device/flow_kernel.o $(OBJ)/device/flow_pp_kernel.o $(OBJ)/device/flow_program.o $(OBJ)/device/symbolic_kernel.o \
+            $(OBJ)/device/flow_kernel.o $(OBJ)/device/flow_pp_kernel.o $(OBJ)/device/flow_program.o $(OBJ)/device/flow_schedule.o $(OBJ)/device/symbolic_kernel.o \
             $(OBJ)/device/solve_kernel.o
 
 .PHONY: all lib oracle ref clean checked
@@ -78,3 +78,7 @@ $(OBJ)/device/flow_program.o: $(SRC)/device/flow_program.cu $(SRC)/device/factor
 $(OBJ)/device/flow_pp_kernel.o: $(SRC)/device/flow_pp_kernel.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/flow_common.cuh $(SRC)/device/sync.cuh $(SRC)/device/device_api.hpp
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_flow_pp_kernel.txt || (cat build/ptxas_flow_pp_kernel.txt; false)
+
+$(OBJ)/device/flow_schedule.o: $(SRC)/device/flow_schedule.cu $(SRC)/device/factor_kernel.cuh $(SRC)/device/sync.cuh $(SRC)/device/device_api.hpp
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/ptxas_flow_schedule.txt || (cat build/ptxas_flow_schedule.txt; false)

@@ -347,8 +347,9 @@ def chain_hop_us(dev: int) -> float:
     for _ in range(7):
         fz.restore()
         ts.append(fz.factor().device_ms)
+    fz_depth = fz.flow_records()[2]  # the schedule's depth, built on the device
     fz.close()
-    return statistics.median(ts) * 1e3 / plan.stats().flow_depth
+    return statistics.median(ts) * 1e3 / fz_depth
 
 
 def run_ours(args):
@@ -369,6 +370,8 @@ def run_ours(args):
     u = an.pattern.pattern
     nnz, n = u.nnz(), a.nrows
     fz = T.GpuFactorizer(plan, T.GpuOptions(device=dev, mode=args.mode, timeout_s=60))
+    # the schedule's depth: built on the device at upload (or by the host plan)
+    depth = (fz.flow_records()[2] if args.mode in (0, 5) else 0) or int(ps.flow_depth)
     _, prog_upd, prog_ms = fz.flow_programs() if args.mode in (0, 5) else (None, np.zeros((0, 2)), 0.0)
     nprod = len(prog_upd)
     del prog_upd
@@ -496,7 +499,7 @@ def run_ours(args):
                    "tasks": int(sum(ps.tasks)),
                    "mode": {1: "task DAG / device merge", 2: "task DAG / update programs",
                             5: "value flow / static schedule of the finalising rows"}[st.mode],
-                   "flow_rows": int(ps.flow_rows), "flow_depth": int(ps.flow_depth),
+                   "flow_rows": int(ps.flow_rows), "flow_depth": depth,
                    "grid_ctas": int(st.grid_ctas), "threads_per_cta": int(st.threads_per_cta),
                    "parallelism": (f"batch: {nmembers_total} members, {per_rank} on rank 0, one launch "
                                    f"per rank" if batched else
@@ -520,9 +523,9 @@ def run_ours(args):
                      "peak_kind": peak_kind, "algorithmic_bytes_per_launch": bytes_alg},
         # what actually binds: the dependence chain. Lower bound = value-flow depth x
         # the measured hand-off latency of a pure chain on this GPU.
-        "latency_bound": {"flow_depth": int(ps.flow_depth), "hop_us": round(hop_us, 4),
-                          "bound_ms": round(ps.flow_depth * hop_us / 1e3, 4),
-                          "frac": round(ps.flow_depth * hop_us / 1e3 / step_ms, 4)},
+        "latency_bound": {"flow_depth": depth, "hop_us": round(hop_us, 4),
+                          "bound_ms": round(depth * hop_us / 1e3, 4),
+                          "frac": round(depth * hop_us / 1e3 / step_ms, 4)},
         "cpu_baseline": cpu,
         "one_shot": one_shot,
         "clocks": clocks.summary(),
@@ -554,7 +557,7 @@ def run_sharded(args):
     torch.cuda.set_device(local_rank)
     dev = local_rank
     a, an, plan, t_an = build_problem(args.config)
-    ps = plan.stats()
+    ps = plan.schedule().stats()  # the parts are slices of the host schedule
     u = an.pattern.pattern
     nnz, n = u.nnz(), a.nrows
     owners = an.subtree_owners(world, separators=0 if args.separators == "rank0" else "spread")

@@ -113,6 +113,14 @@ typedef struct {
    * device programs read operands of rows other parts own from their U (tcg_set_peers) */
   int32_t flow_part;           /* -1: the whole matrix */
   const int32_t* part_of_row;  /*   owner part of every row (n) */
+  /* the schedule built on the device (flow_devprog = 1 and flow_rec = NULL, the default of
+   * tcg_plan_build): the nflow units in natural order, from which tcg_upload computes the
+   * levels, heights, order and records on the device (tcg_plan_schedule builds them on the
+   * host instead) */
+  const int32_t* u_first;      /*   n + 1: first unit of every row */
+  const int32_t* u_tb;         /*   per unit: first position in U */
+  const int32_t* u_len;        /*   per unit: coordinates */
+  const int32_t* u_row;        /*   per unit: its row */
 } tcg_problem;
 
 typedef struct {
@@ -154,8 +162,10 @@ typedef struct {
                                 launch (0: a D2H copy after it) */
   int32_t chunks;            /* end to end, batches: member chunks pipelined with the copies
                                 (0: one launch) */
-  int32_t row_kernel;        /* mode 5: 1 = one lane per coordinate (factor_flow_pipe / factor_flow),
+  int32_t row_kernel;        /* mode 5: 1 = one lane per coordinate (factor_flow_pipe),
                                 2 = product-parallel row groups (factor_flow_pp) */
+  int32_t flow_depth;        /* mode 5: longest chain of the schedule when the device built it
+                                (0 when the plan brought a host schedule: tcg_plan_get_stats) */
 } tcg_stats;
 
 typedef struct {
@@ -186,6 +196,9 @@ const char* tcg_plan_error(void); /* message of the last failed tcg_plan_build (
 /* The upload image: U, its initial values and the value-flow schedule (programs built on the
  * device); with the task-DAG plan (tcg_plan_expand) also the task executors' tables. */
 tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* out);
+/* The value-flow schedule (levels, heights, order, records) on the host threads, if it does
+ * not exist yet; tcg_upload otherwise builds it on the device. tcg_plan_part_problem calls it. */
+tcg_status tcg_plan_schedule(tcg_plan* plan);
 /* Builds the task-DAG plan (the reference's generation walk, flattened) if it does not exist
  * yet; tcg_plan_dag, tcg_plan_blocks and tcg_plan_part_problem do so on first use. */
 tcg_status tcg_plan_expand(tcg_plan* plan);
@@ -237,6 +250,9 @@ tcg_status tcg_download_trace(tcg_ctx* ctx, uint64_t* stamps);
 /* Device pointer to the working values and their count (for in-process users
  * that keep U resident, e.g. a preconditioner apply on the same stream). */
 tcg_status tcg_device_values(tcg_ctx* ctx, double** dptr, int64_t* nnz);
+/* The value-flow schedule on the device (nflow records of 4 words, nflow unit ids; depth =
+ * its longest chain when the device built it, else 0); for checks against tcg_plan_schedule. */
+tcg_status tcg_flow_records(tcg_ctx* ctx, int32_t* rec, int32_t* item, int32_t* depth);
 /* The value-flow update programs on the device (slot: 4 * nnz ints {u_b, u_e, m0, o0}; upd:
  * 2 * nupd ints (m, o); either may be NULL) and the device time of their build (ms). */
 tcg_status tcg_flow_programs(tcg_ctx* ctx, int32_t* slot, int32_t* upd, int64_t* nupd, double* build_ms);

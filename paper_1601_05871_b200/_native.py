@@ -68,6 +68,10 @@ class Problem(C.Structure):
         ("u_row_ptr", i32p),
         ("flow_part", C.c_int32),
         ("part_of_row", i32p),
+        ("u_first", i32p),
+        ("u_tb", i32p),
+        ("u_len", i32p),
+        ("u_row", i32p),
     ]
 
 
@@ -104,6 +108,7 @@ class Stats(C.Structure):
         ("drain_ctas", C.c_int32),
         ("chunks", C.c_int32),
         ("row_kernel", C.c_int32),
+        ("flow_depth", C.c_int32),
     ]
 
 
@@ -169,6 +174,7 @@ SIGNATURES = [
     ("tcg_plan_error", C.c_char_p, []),
     ("tcg_plan_problem", C.c_int, [C.c_void_p, C.POINTER(Problem)]),
     ("tcg_plan_expand", C.c_int, [C.c_void_p]),
+    ("tcg_plan_schedule", C.c_int, [C.c_void_p]),
     ("tcg_plan_get_stats", C.c_int, [C.c_void_p, C.POINTER(PlanStats)]),
     ("tcg_plan_part_problem", C.c_int, [C.c_void_p, C.c_int32, i32p, C.c_int32, C.POINTER(Problem), i64p]),
     ("tcg_plan_dag", C.c_int, [C.c_void_p, i64p, C.POINTER(i32p), C.POINTER(i32p), C.POINTER(i32p),
@@ -192,6 +198,7 @@ SIGNATURES = [
     ("tcg_batch_size", C.c_int32, [C.c_void_p]),
     ("tcg_download_batch", C.c_int, [C.c_void_p, f64p]),
     ("tcg_batch_breakdown", C.c_int, [C.c_void_p, i32p, f64p]),
+    ("tcg_flow_records", C.c_int, [C.c_void_p, i32p, i32p, i32p]),
     ("tcg_flow_programs", C.c_int, [C.c_void_p, i32p, i32p, i64p, f64p]),
     ("tcg_device_values", C.c_int, [C.c_void_p, C.POINTER(f64p), i64p]),
     ("tcg_arena_bytes", C.c_int64, [C.c_void_p]),

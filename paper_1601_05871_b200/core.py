@@ -484,8 +484,16 @@ class Plan:
             raise ValueError(self._lib.tcg_plan_error().decode())
         return self
 
+    def schedule(self) -> "Plan":
+        """The value-flow schedule on the host (tcg_plan_schedule); without it the device
+        builds the schedule at upload."""
+        if self._lib.tcg_plan_schedule(self.handle) != N.TCG_OK:
+            raise ValueError(self._lib.tcg_plan_error().decode())
+        return self
+
     def flow_tables(self) -> dict:
         """The lean value-flow plan's host arrays (the schedule, U, initial values)."""
+        self.schedule()
         p = self.problem()
         return {
             "flow_rec": _copy(p.flow_rec, 4 * p.nflow, np.int32).reshape(-1, 4),
@@ -525,8 +533,9 @@ class Plan:
 
     def tables(self) -> dict:
         """Copies of the task-DAG plan's tables (for host-side inspection in
-        tests; expands the plan)."""
+        tests; expands the plan and builds the host schedule)."""
         self.expand()
+        self.schedule()
         p = self.problem()
         return {
             "task": _copy(p.task_rec, 12 * p.ntasks, np.int32).reshape(-1, 12),
@@ -725,6 +734,16 @@ class GpuFactorizer:
         self.last = N.Stats()
         self._check(self._lib.tcg_factor_phase(self.ctx, phase, C.byref(self.last)))
         return self.last
+
+    def flow_records(self):
+        """The schedule the device runs: (records [nflow, 4], unit ids, depth built on the device)."""
+        n = int(self._problem.nflow)
+        rec = np.zeros((n, 4), np.int32)
+        item = np.zeros(n, np.int32)
+        depth = C.c_int32()
+        self._check(self._lib.tcg_flow_records(self.ctx, rec.ctypes.data_as(N.i32p), item.ctypes.data_as(N.i32p),
+                                               C.byref(depth)))
+        return rec, item, int(depth.value)
 
     def flow_programs(self):
         """(slot [nnz, 4], upd [n, 2], build ms) of the uploaded value-flow programs."""

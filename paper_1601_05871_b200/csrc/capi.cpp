@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -161,7 +163,8 @@ struct tcg_ctx {
   int* flow_ub = nullptr;      // per coordinate: first product in flow_upd (nnz + 1), in prog_arena
   void* prog_arena = nullptr;  // device-built (m, o) pairs (their count is known after the count pass)
   double prog_build_ms = 0.0;
-  int ub_total = 0;            // host source of flow_ub[nnz]  // device time of the last program build
+  int ub_total = 0;            // host source of flow_ub[nnz]
+  int flow_depth = 0;          // longest chain of the schedule built on the device (0: built on the host)  // device time of the last program build
   double* flow_a = nullptr;  // snapshot of the input values
   std::int64_t nflow = 0, nflow_upd = 0;
   bool has_flow = false;
@@ -206,12 +209,25 @@ tcg_status tcg_plan_build(const tcg_csr_view* a_permuted, const tcg_csr_view* pa
       throw std::invalid_argument("range list: null bounds");
     auto p = std::make_unique<tcg_plan>();
     for (int32_t r = 0; r < nranges; ++r) p->ranges.ranges.push_back({range_bounds[r], range_bounds[r + 1]});
-    p->flow = tcb::build_flow_plan(a, u, p->ranges);
+    // the schedule is built on the device at upload unless TCG_HOST_SCHEDULE asks for the host
+    const char* hs = std::getenv("TCG_HOST_SCHEDULE");
+    p->flow = tcb::build_flow_plan(a, u, p->ranges, hs && std::atoi(hs) != 0);
     *out = p.release();
     return TCG_OK;
   } catch (const std::bad_alloc&) {
     g_plan_error = "out of host memory";
     return TCG_INVALID;
+  } catch (const std::exception& e) {
+    g_plan_error = e.what();
+    return TCG_INVALID;
+  }
+}
+
+tcg_status tcg_plan_schedule(tcg_plan* plan) {
+  if (!plan) return TCG_INVALID;
+  try {
+    tcb::flow_plan_schedule(plan->flow);
+    return TCG_OK;
   } catch (const std::exception& e) {
     g_plan_error = e.what();
     return TCG_INVALID;
@@ -248,8 +264,12 @@ tcg_status tcg_plan_problem(const tcg_plan* plan, tcg_problem* o) {
   o->ntasks = F.stats.tasks[0] + F.stats.tasks[1] + F.stats.tasks[2] + F.stats.tasks[3];
   // the value-flow schedule with device-built programs (the default executor)
   o->nflow = F.stats.units;
-  o->flow_rec = F.rec.data();
-  o->flow_item = F.unit.data();
+  o->flow_rec = F.scheduled ? F.rec.data() : nullptr;  // else the device builds the schedule
+  o->flow_item = F.scheduled ? F.unit.data() : nullptr;
+  o->u_first = F.ufirst.data();
+  o->u_tb = F.u_tb.data();
+  o->u_len = F.u_len.data();
+  o->u_row = F.u_row.data();
   o->flow_devprog = 1;
   o->u_row_ptr = F.row_ptr.data();
   o->flow_part = -1;
@@ -282,6 +302,7 @@ tcg_status tcg_plan_part_problem(tcg_plan* plan, int32_t nparts, const int32_t* 
                                  tcg_problem* o, int64_t* remote_operands) {
   if (!plan || !o || !part_of_row) return TCG_INVALID;
   try {
+    tcb::flow_plan_schedule(plan->flow);  // a part is a slice of the global schedule
     std::vector<std::int32_t> own(part_of_row, part_of_row + plan->flow.n);
     plan->parts[part] = tcb::build_flow_part(plan->flow, own, nparts, part);
     plan->part_owner = std::move(own);
@@ -456,6 +477,15 @@ static tcg_status build_programs(tcg_ctx* c, const tcg_problem* p) {
   TCG_CUDA_TRY(c, tcbdev::flow_transpose(static_cast<int>(n), static_cast<int>(nnz), nullptr, nullptr, nullptr,
                                          nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, &sort_bytes,
                                          c->sm_count, c->stream));
+  // the schedule on the device when the plan has none (tcg_plan_build's default)
+  const bool dev_sched = !p->flow_rec;
+  const std::int64_t U = dev_sched ? p->nflow : 0;
+  size_t sched_bytes = 0;
+  tcbdev::SchedParams S{};
+  S.nunits = static_cast<int>(U);
+  if (dev_sched)
+    TCG_CUDA_TRY(c, tcbdev::flow_schedule(S, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                          &sched_bytes, c->sm_count, c->stream));
   size_t off = 0;
   auto take = [&](size_t bytes) {
     const size_t at = off;
@@ -467,7 +497,13 @@ static tcg_status build_programs(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_keys = take(sizeof(int) * nnz), o_poss = take(sizeof(int) * nnz), o_cs = take(sizeof(int) * ns);
   const size_t o_ctr = take(sizeof(int) * 2), o_tot = take(sizeof(long long));
   const size_t o_own = take(p->flow_part >= 0 ? sizeof(int) * n : 0);
-  const size_t o_tmp = take(std::max(scan_bytes, sort_bytes));
+  const size_t o_tmp = take(std::max({scan_bytes, sort_bytes, sched_bytes}));
+  const size_t o_uf = take(dev_sched ? sizeof(int) * (n + 1) : 0), o_utb = take(sizeof(int) * U),
+               o_ulen = take(sizeof(int) * U), o_urow = take(sizeof(int) * U), o_lvl = take(sizeof(int) * U),
+               o_hgt = take(sizeof(int) * U), o_acc = take(sizeof(int) * U), o_ids = take(sizeof(int) * (U + 1)),
+               o_ord = take(sizeof(int) * (U + 1)), o_skey = take(sizeof(long long) * U), o_skey2 = take(sizeof(long long) * U),
+               o_words = take(sizeof(int) * 2), o_uc0 = take(sizeof(int) * U), o_uc1 = take(sizeof(int) * U),
+               o_acc2 = take(sizeof(int) * U);
   TCG_CUDA_TRY(c, cudaMalloc(&tmp, off));
   struct Free {
     void* p;
@@ -509,6 +545,55 @@ static tcg_status build_programs(tcg_ctx* c, const tcg_problem* p) {
                                          reinterpret_cast<int*>(b + o_key), reinterpret_cast<int*>(b + o_pos),
                                          reinterpret_cast<int*>(b + o_rid), reinterpret_cast<int*>(b + o_keys),
                                          col_pos, col_ptr, col_src, b + o_tmp, &sort_bytes, c->sm_count, c->stream));
+  const bool say = std::getenv("TCG_PLAN_TIMES") != nullptr;
+  auto wall = [&](const char* what) {  // host wall time of the stream's work so far (TCG_PLAN_TIMES)
+    static thread_local std::chrono::steady_clock::time_point last;
+    if (!say) return;
+    cudaStreamSynchronize(c->stream);
+    const auto now = std::chrono::steady_clock::now();
+    if (what) std::fprintf(stderr, "upload %-12s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+    last = now;
+  };
+  wall(nullptr);
+  if (dev_sched && U > 0) {
+    auto ip = [&](size_t o) { return reinterpret_cast<int*>(b + o); };
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(ip(o_uf), p->u_first, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, c->stream));
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(ip(o_utb), p->u_tb, sizeof(int) * U, cudaMemcpyHostToDevice, c->stream));
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(ip(o_ulen), p->u_len, sizeof(int) * U, cudaMemcpyHostToDevice, c->stream));
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(ip(o_urow), p->u_row, sizeof(int) * U, cudaMemcpyHostToDevice, c->stream));
+    wall("units H2D");
+    S.n = static_cast<int>(n);
+    S.row_ptr = row_ptr;
+    S.cols = c->cols;
+    S.col_ptr = col_ptr;
+    S.col_src = col_src;
+    S.col_pos = col_pos;
+    S.ufirst = ip(o_uf);
+    S.u_tb = ip(o_utb);
+    S.u_len = ip(o_ulen);
+    S.uc0 = ip(o_uc0);
+    S.uc1 = ip(o_uc1);
+    S.level = ip(o_lvl);
+    S.height = ip(o_hgt);
+    S.acc = ip(o_acc);
+    S.acc2 = ip(o_acc2);
+    S.depth = ip(o_words);
+    S.error = ip(o_words) + 1;
+    S.timeout_ns = static_cast<unsigned long long>((c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0) * 1e9);
+    TCG_CUDA_TRY(c, tcbdev::flow_schedule(S, ip(o_urow), c->flow_rec, c->flow_item,
+                                          reinterpret_cast<unsigned long long*>(b + o_skey),
+                                          reinterpret_cast<unsigned long long*>(b + o_skey2), ip(o_ids), ip(o_ord),
+                                          b + o_tmp, &sched_bytes, c->sm_count, c->stream));
+    wall("schedule");
+    int words[2] = {0, 0};
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(words, ip(o_words), sizeof(words), cudaMemcpyDeviceToHost, c->stream));
+    TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (words[1]) {
+      c->err = "tcg_upload: device watchdog expired while building the schedule";
+      return TCG_TIMEOUT;
+    }
+    c->flow_depth = words[0];
+  }
   TCG_CUDA_TRY(c, tcbdev::flow_program_count(q, c->sm_count, c->stream));
   TCG_CUDA_TRY(c, tcbdev::flow_program_scan(count, ub64, ub32, nnz, total_d, b + o_tmp, &scan_bytes,
                                             c->sm_count, c->stream));
@@ -602,7 +687,9 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_slot = take(programs ? sizeof(int4) * p->nslots : 0);
   const size_t o_upd = take(programs ? sizeof(int) * 2 * p->nupdates : 0);
   const bool devprog = p->flow_devprog && p->u_row_ptr;
-  const bool flow = p->nflow > 0 && p->flow_rec && p->flow_item &&
+  const bool dev_sched = devprog && !p->flow_rec && p->u_first && p->u_tb && p->u_len && p->u_row &&
+                         p->flow_part < 0;
+  const bool flow = p->nflow > 0 && ((p->flow_rec && p->flow_item) || dev_sched) &&
                     (devprog || (p->flow_slot && (p->nflow_upd == 0 || p->flow_upd)));
   if (p->flow_part >= 0 && (!devprog || !p->part_of_row || p->nnz >= (1LL << tcb::kRemoteShift))) {
     c->err = "tcg_upload: a part needs device-built programs, its owner table and U below 2^25 entries";
@@ -676,9 +763,12 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
     TCG_CUDA_TRY(c, put(c->slot_rec, p->slot_rec, sizeof(int4) * p->nslots));
     TCG_CUDA_TRY(c, put(c->upd, p->upd, sizeof(int) * 2 * p->nupdates));
   }
+  c->flow_depth = 0;
   if (flow) {
-    TCG_CUDA_TRY(c, put(c->flow_rec, p->flow_rec, sizeof(int4) * p->nflow));
-    TCG_CUDA_TRY(c, put(c->flow_item, p->flow_item, sizeof(int) * p->nflow));
+    if (!dev_sched) {
+      TCG_CUDA_TRY(c, put(c->flow_rec, p->flow_rec, sizeof(int4) * p->nflow));
+      TCG_CUDA_TRY(c, put(c->flow_item, p->flow_item, sizeof(int) * p->nflow));
+    }
     if (!devprog) {
       TCG_CUDA_TRY(c, put(c->flow_slot, p->flow_slot, sizeof(int4) * p->nnz));
       TCG_CUDA_TRY(c, put(c->flow_upd, p->flow_upd, sizeof(int2) * p->nflow_upd));
@@ -1006,6 +1096,8 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (host_a) c->pristine = false;
   S.lanes_per_row = pp ? 32 * pp_w : 32;
   S.row_kernel = pp ? 2 : 1;
+  S.flow_depth = c->flow_depth;
+  S.flow_depth = c->flow_depth;
   if (pp) S.threads_per_cta = 256;
   if (pp) S.staging_cap = pp_k;
   const int64_t rows = c->nflow * c->nbatch;
@@ -1345,6 +1437,7 @@ static tcg_status run_flow_chunked(tcg_ctx* c, tcg_stats& S, int threads, const 
   S.mode = 5;
   S.lanes_per_row = pp ? 32 * pp_w : 32;
   S.row_kernel = pp ? 2 : 1;
+  S.flow_depth = c->flow_depth;
   S.batch = nb;
   S.chunks = chunks;
   bool error = false;
@@ -1555,6 +1648,15 @@ tcg_status tcg_download_trace(tcg_ctx* c, uint64_t* stamps) {
   TCG_CUDA_TRY(c, cudaMemcpyAsync(stamps, c->trace, sizeof(uint64_t) * (2 * c->ntab + 4 * std::max(c->nitems, c->nflow)),
                                   cudaMemcpyDeviceToHost, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  return TCG_OK;
+}
+
+tcg_status tcg_flow_records(tcg_ctx* c, int32_t* rec, int32_t* item, int32_t* depth) {
+  if (!c || !c->uploaded || !c->has_flow) return TCG_INVALID;
+  TCG_CUDA_TRY(c, cudaSetDevice(c->device));
+  if (rec) TCG_CUDA_TRY(c, cudaMemcpy(rec, c->flow_rec, sizeof(int4) * c->nflow, cudaMemcpyDeviceToHost));
+  if (item) TCG_CUDA_TRY(c, cudaMemcpy(item, c->flow_item, sizeof(int) * c->nflow, cudaMemcpyDeviceToHost));
+  if (depth) *depth = c->flow_depth;
   return TCG_OK;
 }
 

@@ -33,6 +33,10 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
 cudaError_t flow_transpose(int n, int nnz, const int* row_ptr, const int* cols, int* key, int* pos, int* rowid,
                            int* key_s, int* pos_s, int* col_ptr, int* col_src, void* temp, size_t* temp_bytes,
                            int sm_count, cudaStream_t st);
+// the value-flow schedule on the device (flow_schedule.cu): levels, heights, order, records
+cudaError_t flow_schedule(SchedParams S, const int* u_row, int4* rec, int* item, unsigned long long* keys,
+                          unsigned long long* keys_sorted, int* ids, int* order, void* temp, size_t* temp_bytes,
+                          int sm_count, cudaStream_t st);
 cudaError_t flow_program_remote_rewrite(long long nnz, const int* rowid, const int* owner, int part, int4* slot,
                                         int2* upd, int sm_count, cudaStream_t st);
 cudaError_t flow_program_count(const ProgParams& p, int sm_count, cudaStream_t st);

@@ -119,6 +119,29 @@ struct ProgParams {
 };
 
 
+// The value-flow schedule built on the device (flow_schedule.cu).
+struct SchedParams {
+  int n;
+  int nunits;
+  const int* row_ptr;   // n + 1
+  const int* cols;
+  const int* col_ptr;   // transposed index: sources of row t
+  const int* col_src;   //   their rows
+  const int* col_pos;   //   positions of U(r, t)
+  const int* ufirst;    // n + 1
+  const int* u_tb;
+  const int* u_len;
+  int* uc0;             // per unit: first and last column (scratch, filled by flow_schedule)
+  int* uc1;
+  int* level;           // 0 until known
+  int* height;
+  int* acc;             // per unit: largest dependence level seen (rows of more than 8 units; zeroed)
+  int* acc2;            // per unit: largest dependent height seen (the same)
+  int* depth;           // out: largest level
+  int* error;           // watchdog
+  unsigned long long timeout_ns;
+};
+
 struct FlowPrepParams {
   const double* vals;    // working values (input of the factorization)
   double* a;             // snapshot of them; == vals: no copy (the input already lives in `a`)

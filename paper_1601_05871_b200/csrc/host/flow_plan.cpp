@@ -175,7 +175,7 @@ CsrMatrix flow_plan_pattern(const FlowPlan& P) {
   return u;
 }
 
-FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& ranges) {
+FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& ranges, bool schedule) {
   const auto t0 = std::chrono::steady_clock::now();
   const int threads = host_threads();
   const bool say = std::getenv("TCG_PLAN_TIMES") != nullptr;
@@ -300,25 +300,59 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
     for (index_t t = 0; t < n; ++t) ufirst[t + 1] += ufirst[t];
     const std::size_t U = static_cast<std::size_t>(ufirst[n]);
     if (U >= (1u << 31)) throw std::length_error("flow: too many units");
-    // per unit: first position, length, first and last column, row
-    std::atomic<bool> miscount{false};
-    std::vector<std::int32_t> u_tb(U), u_len(U), u_c0(U), u_c1(U), row_of(U);
+    // per unit: first position, length, row
+    std::atomic<bool> miscount{false}, too_long{false};
+    P.ufirst.assign(ufirst.begin(), ufirst.end());
+    P.u_tb.resize(U);
+    P.u_len.resize(U);
+    P.u_row.resize(U);
     parallel_rows(n, threads, [&](index_t b, index_t e) {
       for (index_t t = b; t < e; ++t) {
         std::int32_t g = ufirst[t];
         split_row(t, [&](std::int32_t tb, std::int32_t len) {
-          u_tb[g] = tb;
-          u_len[g] = len;
-          u_c0[g] = cols[tb];
-          u_c1[g] = cols[tb + len - 1];
-          row_of[g] = t;
+          P.u_tb[g] = tb;
+          P.u_len[g] = len;
+          P.u_row[g] = static_cast<std::int32_t>(t);
+          if (len >= (1 << 30)) too_long.store(true, std::memory_order_relaxed);
           ++g;
         });
         if (g != ufirst[t + 1]) miscount.store(true, std::memory_order_relaxed);
       }
     });
     if (miscount.load()) throw std::logic_error("flow plan: unit count mismatch");
+    if (too_long.load()) throw std::length_error("flow: row slice too long");
+    P.stats.units = static_cast<std::int64_t>(U);
     mark("units");
+    if (schedule) flow_plan_schedule(P);
+    mark("schedule");
+  } catch (...) {
+    blocks.join();
+    throw;
+  }
+  blocks.join();
+  mark("blocks");
+  P.stats.plan_seconds = since(t0);
+  return P;
+}
+
+void flow_plan_schedule(FlowPlan& P) {
+  if (P.scheduled) return;
+  const index_t n = P.n;
+  const int threads = host_threads();
+  const std::size_t U = P.u_tb.size();
+  const std::int32_t* cols = P.cols.data();
+  const std::int32_t* ufirst = P.ufirst.data();
+  const std::int32_t* u_tb = P.u_tb.data();
+  const std::int32_t* u_len = P.u_len.data();
+  const std::int32_t* row_of = P.u_row.data();
+  hvec<std::int32_t> u_c0(U), u_c1(U);  // first and last column of every unit
+  parallel_rows(static_cast<index_t>(U), threads, [&](index_t b, index_t e) {
+    for (index_t g = b; g < e; ++g) {
+      u_c0[g] = cols[u_tb[g]];
+      u_c1[g] = cols[u_tb[g] + u_len[g] - 1];
+    }
+  });
+  {
 
     // Dependences of unit g (row t, last column c1(g)): for every source r of
     // t (an entry U(r,t) at position q), the units of row r from the one
@@ -338,7 +372,7 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
     // shorter ones (C1, C2, C4-C6) sweep faster on one thread than through
     // any hand-out of their rows (C4: levels and heights 0.14 s on one
     // thread, 0.20 s in parallel).
-    if (threads > 1 && u.nnz >= 48 * static_cast<offset_t>(n)) {
+    if (threads > 1 && P.nnz >= 48 * static_cast<std::int64_t>(n)) {
       std::vector<std::atomic<std::int32_t>> cnt(static_cast<std::size_t>(n));
       for (index_t t = 0; t < n; ++t) cnt[t].store(0, std::memory_order_relaxed);
       parallel_rows(n, threads, [&](index_t b, index_t e) {
@@ -362,7 +396,6 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
             }
         });
       }
-      mark("transpose");
       ready_rows(n, threads, cnt, [&](index_t t, auto&& release) {
         const std::int32_t g0 = ufirst[t], g1 = ufirst[t + 1];
         for (std::int32_t g = g0; g < g1; ++g) level[g] = 1;
@@ -381,7 +414,6 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
         for (std::int32_t q = P.row_ptr[t] + 1; q < P.row_ptr[t + 1]; ++q) release(cols[q]);
       });
       for (std::size_t g = 0; g < U; ++g) depth = std::max(depth, level[g]);
-      mark("level");
       // heights: row r is ready once every row its entries feed is done
       for (index_t r = 0; r < n; ++r) cnt[r].store(P.row_ptr[r + 1] - P.row_ptr[r] - 1, std::memory_order_relaxed);
       ready_rows(n, threads, cnt, [&](index_t r, auto&& release) {
@@ -463,7 +495,6 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
         for (std::int32_t g = vr0 + 1; g < vr1; ++g) height[vr0] = std::max(height[vr0], height[g] + 1);
       }
     }
-    mark("levels");
     // schedule: level ascending, height descending, unit id ascending (two
     // stable counting sorts, the second key first)
     std::int32_t hmax = 0;
@@ -487,12 +518,10 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
     }
     P.rec.resize(4 * U);
     P.unit.resize(U);
-    std::atomic<bool> too_long{false};
     parallel_rows(static_cast<index_t>(U), threads, [&](index_t b, index_t e) {
       for (index_t q = b; q < e; ++q) {
         const std::int32_t g = order[q];
         const std::int32_t t = row_of[g];
-        if (u_len[g] >= (1 << 30)) too_long.store(true, std::memory_order_relaxed);
         P.rec[4 * q + 0] = u_tb[g];
         P.rec[4 * q + 1] = u_len[g] | ((g == ufirst[t] ? 0 : 1) << 30);  // Chol unit, else a chunk (Trsm)
         P.rec[4 * q + 2] = P.row_ptr[t];
@@ -500,18 +529,9 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
         P.unit[q] = g;
       }
     });
-    if (too_long.load()) throw std::length_error("flow: row slice too long");
-    mark("order");
-    P.stats.units = static_cast<std::int64_t>(U);
     P.stats.depth = depth;
-  } catch (...) {
-    blocks.join();
-    throw;
+    P.scheduled = true;
   }
-  blocks.join();
-  mark("blocks");
-  P.stats.plan_seconds = since(t0);
-  return P;
 }
 
 FlowPart build_flow_part(const FlowPlan& P, const std::vector<std::int32_t>& part_of_row, std::int32_t nparts,

@@ -80,6 +80,14 @@ struct FlowPlan {
   hvec<std::int32_t> row_ptr;  // n + 1 positions (int32: nnz < 2^31)
   hvec<double> values;         // initialised U values (init_factor_values)
   hvec<std::int32_t> a_map;    // U slot -> a_permuted position, -1 = fill (empty: A has duplicates)
+  // units in natural order (row ascending; a row's Chol unit, then its chunks)
+  hvec<std::int32_t> ufirst;   // n + 1: first unit of every row
+  hvec<std::int32_t> u_tb;     // per unit: first position in U
+  hvec<std::int32_t> u_len;    // per unit: coordinates
+  hvec<std::int32_t> u_row;    // per unit: its row
+  // the schedule (flow_plan_schedule on the host, or built on the device at
+  // upload, flow_schedule.cu): empty until scheduled
+  bool scheduled = false;
   hvec<std::int32_t> rec;      // 4 words per schedule position: tb, L | kind << 30, dpos, t
   hvec<std::int32_t> unit;     // per schedule position: unit id (natural order)
   FlowPlanStats stats;
@@ -88,7 +96,15 @@ struct FlowPlan {
 // Validates both matrices as csr_from_view did (validate_csr), then the
 // ranges (ordering.hpp:43-55) and the leading diagonal of every U row
 // (kernels.hpp:46-48); std::invalid_argument on failure.
-FlowPlan build_flow_plan(const CsrRef& a_permuted, const CsrRef& pattern, const RangeList& ranges);
+// schedule = false leaves the schedule to the device (tcg_upload) or to a
+// later flow_plan_schedule.
+FlowPlan build_flow_plan(const CsrRef& a_permuted, const CsrRef& pattern, const RangeList& ranges,
+                         bool schedule = true);
+
+// The schedule on the host threads: every unit's level (longest chain from a
+// source) and height (longest chain to a sink), the order (level ascending,
+// height descending, unit id ascending), the records; stats.depth. Idempotent.
+void flow_plan_schedule(FlowPlan& P);
 
 // The pattern as an owning CsrMatrix (values 1.0), for the full plan.
 CsrMatrix flow_plan_pattern(const FlowPlan& P);

@@ -47,6 +47,25 @@ def test_configs_value_flow(T, golden, oracle, name):  # noqa: D103
     check_against_oracle(name, vals, golden, oracle)
 
 
+@pytest.mark.parametrize("name", ["c1", "c5_m0", "s27_16_k2", "elast6_k1", "grid20_k2_leaf4", "rand_spd_200",
+                                  "c2", "c3", "c4"])
+def test_device_schedule_equals_the_host_schedule(T, name):
+    # flow_schedule.cu (levels and heights by polling dry runs, a radix sort,
+    # the records) against flow_plan_schedule on the host: record for record
+    _, an = analyzed(name)
+    fresh = T.Plan(an.a_permuted, an.pattern, an.ranges)  # no host schedule: the device builds it
+    assert fresh.stats().flow_depth == 0
+    fz = T.GpuFactorizer(fresh, T.GpuOptions(timeout_s=30))
+    try:
+        rec, item, depth = fz.flow_records()
+    finally:
+        fz.close()
+    host = T.Plan(an.a_permuted, an.pattern, an.ranges).schedule()
+    f = host.flow_tables()
+    assert np.array_equal(rec, f["flow_rec"]) and np.array_equal(item, f["flow_item"])
+    assert depth == host.stats().flow_depth > 0
+
+
 def test_default_row_kernel_follows_program_length(T):
     # product-parallel rows where programs are short (C1, C2, C5), one lane
     # per coordinate where they are long (C3: 24.8 products per coordinate)

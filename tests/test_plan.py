@@ -78,7 +78,7 @@ def test_flow_depth_is_below_the_task_dag_depth(T):
     # value flow follows the rows that interact, not the blocks: much shallower
     _, an = analyzed("c5_m0")
     plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
-    s = plan.stats()
+    s = plan.schedule().stats()
     assert s.full_plan == 0 and s.flow_depth > 0
     plan.expand()
     s = plan.stats()
