@@ -119,49 +119,80 @@ void validate_ref(const CsrRef& m, int threads) {
 // block row, one Trsm and one Herk per off-diagonal block, one Gemm per pair
 // of off-diagonal blocks (i < j) of a block row whose target (i, j) exists.
 void count_tasks(const FlowPlan& P, const RangeList& ranges, const std::vector<index_t>& owner,
-                 FlowPlanStats& st) {
+                 FlowPlanStats& st, int threads) {
   const index_t m = ranges.count();
+  const std::int32_t* cols = P.cols.data();
+  // block columns of every block row, over contiguous block-row ranges on the
+  // host threads (each with its own stamp array), concatenated in order
+  const int T = std::max(1, std::min<int>(threads, std::max<index_t>(1, m / 256)));
+  std::vector<std::vector<index_t>> part_cols(static_cast<std::size_t>(T));
+  std::vector<std::vector<offset_t>> part_len(static_cast<std::size_t>(T));
+  {
+    std::vector<std::thread> pool;
+    for (int k = 0; k < T; ++k)
+      pool.emplace_back([&, k] {
+        const index_t b0 = static_cast<index_t>(static_cast<std::int64_t>(m) * k / T);
+        const index_t b1 = static_cast<index_t>(static_cast<std::int64_t>(m) * (k + 1) / T);
+        std::vector<index_t> stamp(static_cast<std::size_t>(m), -1), present;
+        auto& out = part_cols[static_cast<std::size_t>(k)];
+        auto& len = part_len[static_cast<std::size_t>(k)];
+        for (index_t bi = b0; bi < b1; ++bi) {
+          present.clear();
+          for (index_t i = ranges.ranges[bi].begin; i < ranges.ranges[bi].end; ++i)
+            for (std::int32_t q = P.row_ptr[i], qe = P.row_ptr[i + 1]; q < qe;) {
+              const index_t bj = owner[cols[q]];
+              if (stamp[bj] != bi) {
+                stamp[bj] = bi;
+                present.push_back(bj);
+              }
+              // skip the rest of this block's slice of the row
+              q = static_cast<std::int32_t>(std::lower_bound(cols + q, cols + qe, ranges.ranges[bj].end) - cols);
+            }
+          std::sort(present.begin(), present.end());
+          out.insert(out.end(), present.begin(), present.end());
+          len.push_back(static_cast<offset_t>(present.size()));
+        }
+      });
+    for (auto& th : pool) th.join();
+  }
   std::vector<offset_t> bptr(static_cast<std::size_t>(m) + 1, 0);
   std::vector<index_t> bcol;
-  std::vector<index_t> stamp(static_cast<std::size_t>(m), -1), present;
-  const std::int32_t* cols = P.cols.data();
-  for (index_t bi = 0; bi < m; ++bi) {
-    present.clear();
-    for (index_t i = ranges.ranges[bi].begin; i < ranges.ranges[bi].end; ++i)
-      for (std::int32_t q = P.row_ptr[i], qe = P.row_ptr[i + 1]; q < qe;) {
-        const index_t bj = owner[cols[q]];
-        if (stamp[bj] != bi) {
-          stamp[bj] = bi;
-          present.push_back(bj);
-        }
-        // skip the rest of this block's slice of the row
-        q = static_cast<std::int32_t>(std::lower_bound(cols + q, cols + qe, ranges.ranges[bj].end) - cols);
-      }
-    std::sort(present.begin(), present.end());
-    bcol.insert(bcol.end(), present.begin(), present.end());
-    bptr[bi + 1] = static_cast<offset_t>(bcol.size());
-  }
-  const offset_t nb = static_cast<offset_t>(bcol.size());
-  std::int64_t gemm = 0;
-  for (index_t p = 0; p < m; ++p) {
-    // off-diagonal block columns of row p (the diagonal block leads)
-    const offset_t b = bptr[p] + 1, e = bptr[p + 1];
-    for (offset_t x = b; x < e; ++x) {
-      const index_t i = bcol[x];
-      const auto re = bcol.begin() + bptr[i + 1];
-      auto it = bcol.begin() + bptr[i];
-      for (offset_t y = x + 1; y < e; ++y) {  // targets (i, j), j ascending: one forward merge
-        it = std::lower_bound(it, re, bcol[y]);
-        if (it == re) break;
-        if (*it == bcol[y]) ++gemm;
+  {
+    index_t bi = 0;
+    for (int k = 0; k < T; ++k) {
+      bcol.insert(bcol.end(), part_cols[static_cast<std::size_t>(k)].begin(), part_cols[static_cast<std::size_t>(k)].end());
+      for (offset_t l : part_len[static_cast<std::size_t>(k)]) {
+        bptr[bi + 1] = bptr[bi] + l;
+        ++bi;
       }
     }
   }
+  const offset_t nb = static_cast<offset_t>(bcol.size());
+  // one Gemm per pair of off-diagonal blocks (i < j) of a block row whose target (i, j) exists
+  std::atomic<std::int64_t> gemm{0};
+  parallel_rows(m, threads, [&](index_t b0, index_t b1) {
+    std::int64_t local = 0;
+    for (index_t p = b0; p < b1; ++p) {
+      // off-diagonal block columns of row p (the diagonal block leads)
+      const offset_t b = bptr[p] + 1, e = bptr[p + 1];
+      for (offset_t x = b; x < e; ++x) {
+        const index_t i = bcol[x];
+        const auto re = bcol.begin() + bptr[i + 1];
+        auto it = bcol.begin() + bptr[i];
+        for (offset_t y = x + 1; y < e; ++y) {  // targets (i, j), j ascending: one forward merge
+          it = std::lower_bound(it, re, bcol[y]);
+          if (it == re) break;
+          if (*it == bcol[y]) ++local;
+        }
+      }
+    }
+    gemm.fetch_add(local, std::memory_order_relaxed);
+  });
   st.nblock_rows = m;
   st.nblocks = nb;
   st.tasks[0] = m;
   st.tasks[1] = st.tasks[2] = nb - m;
-  st.tasks[3] = gemm;
+  st.tasks[3] = gemm.load();
 }
 
 }  // namespace
@@ -243,7 +274,7 @@ FlowPlan build_flow_plan(const CsrRef& a, const CsrRef& u, const RangeList& rang
   // the block layout's task counts on a second thread (FactorStats)
   std::thread blocks([&] {
     const auto tb = std::chrono::steady_clock::now();
-    count_tasks(P, ranges, owner, P.stats);
+    count_tasks(P, ranges, owner, P.stats, threads);
     P.stats.block_build_seconds = since(tb);
   });
   try {
