@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <new>
 #include <string>
@@ -55,6 +56,93 @@ void view_of(const tcb::CsrMatrix& m, tcg_csr_view* out) {
 }
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Device blocks of the arenas, kept for reuse after a context frees them (a
+// one-shot call allocates and frees a few hundred MB to ~2 GB each time;
+// cudaMalloc / cudaFree of that much took 10-300 ms on B200 boxes). A request
+// takes a cached block of at least its size and at most 25% larger; at most
+// 8 GB stay cached per device; TCG_DEVICE_CACHE=0 turns the cache off. A
+// block is only returned once its stream's work is done (callers synchronise).
+struct DeviceCache {
+  std::mutex mu;
+  std::map<int, std::multimap<size_t, void*>> free_blocks;  // device -> size -> block
+  std::map<void*, std::pair<int, size_t>> size_of;          // block -> (device, bytes)
+  std::map<int, size_t> cached;
+  static constexpr size_t kCap = size_t{8} << 30;
+};
+DeviceCache& device_cache() {
+  static DeviceCache* c = new DeviceCache();  // never destroyed: blocks live until the process exits
+  return *c;
+}
+bool cache_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("TCG_DEVICE_CACHE");
+    return !e || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+cudaError_t dev_alloc(int device, void** p, size_t bytes) {
+  bytes = align_up(std::max<size_t>(bytes, 1), size_t{1} << 20);
+  DeviceCache& dc = device_cache();
+  if (cache_on()) {
+    std::lock_guard<std::mutex> lock(dc.mu);
+    auto& fl = dc.free_blocks[device];
+    auto it = fl.lower_bound(bytes);
+    if (it != fl.end() && it->first <= bytes + bytes / 4) {
+      *p = it->second;
+      dc.cached[device] -= it->first;
+      fl.erase(it);
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation && cache_on()) {  // give the cached blocks back and retry
+    cudaGetLastError();
+    std::lock_guard<std::mutex> lock(dc.mu);
+    for (auto& kv : dc.free_blocks[device]) {
+      cudaFree(kv.second);
+      dc.size_of.erase(kv.second);
+    }
+    dc.free_blocks[device].clear();
+    dc.cached[device] = 0;
+    e = cudaMalloc(p, bytes);
+  }
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lock(dc.mu);
+    dc.size_of[*p] = {device, bytes};
+  }
+  return e;
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  DeviceCache& dc = device_cache();
+  std::lock_guard<std::mutex> lock(dc.mu);
+  auto it = dc.size_of.find(p);
+  if (it == dc.size_of.end() || !cache_on()) {
+    if (it != dc.size_of.end()) dc.size_of.erase(it);
+    cudaFree(p);
+    return;
+  }
+  const int device = it->second.first;
+  const size_t bytes = it->second.second;
+  auto& fl = dc.free_blocks[device];
+  while (dc.cached[device] + bytes > DeviceCache::kCap && !fl.empty()) {  // make room: largest first
+    auto big = std::prev(fl.end());
+    dc.cached[device] -= big->first;
+    dc.size_of.erase(big->second);
+    cudaFree(big->second);
+    fl.erase(big);
+  }
+  if (bytes > DeviceCache::kCap) {
+    dc.size_of.erase(it);
+    cudaFree(p);
+    return;
+  }
+  fl.emplace(bytes, p);
+  dc.cached[device] += bytes;
+}
 
 }  // namespace
 
@@ -421,17 +509,18 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
 }
 
 void tcg_destroy(tcg_ctx* c) {
-  if (c && c->batch_arena) cudaFree(c->batch_arena);
-  if (c && c->prog_arena) cudaFree(c->prog_arena);
-  if (c && c->a_stage) cudaFree(c->a_stage);
-  if (c && c->drain_done) cudaFree(c->drain_done);
-  if (c && c->peers) cudaFree(c->peers);
-  if (c)
-    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   if (!c) return;
   cudaSetDevice(c->device);
-  if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->arena) cudaFree(c->arena);
+  if (c->stream) cudaStreamSynchronize(c->stream);  // before any block goes back to the cache
+  if (c->d2h_stream) cudaStreamSynchronize(c->d2h_stream);
+  if (c->h2d_stream) cudaStreamSynchronize(c->h2d_stream);
+  dev_free(c->batch_arena);
+  dev_free(c->prog_arena);
+  if (c->a_stage) cudaFree(c->a_stage);
+  if (c->drain_done) cudaFree(c->drain_done);
+  if (c->peers) cudaFree(c->peers);
+  for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+  dev_free(c->arena);
   if (c->host_ctrl) cudaFreeHost(c->host_ctrl);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -504,11 +593,15 @@ static tcg_status build_programs(tcg_ctx* c, const tcg_problem* p) {
                o_ord = take(sizeof(int) * (U + 1)), o_skey = take(sizeof(long long) * U), o_skey2 = take(sizeof(long long) * U),
                o_words = take(sizeof(int) * 2), o_uc0 = take(sizeof(int) * U), o_uc1 = take(sizeof(int) * U),
                o_acc2 = take(sizeof(int) * U);
-  TCG_CUDA_TRY(c, cudaMalloc(&tmp, off));
+  TCG_CUDA_TRY(c, dev_alloc(c->device, &tmp, off));
   struct Free {
     void* p;
-    ~Free() { cudaFree(p); }
-  } free_tmp{tmp};
+    cudaStream_t st;
+    ~Free() {
+      cudaStreamSynchronize(st);  // (an early return may leave work on the stream)
+      dev_free(p);
+    }
+  } free_tmp{tmp, c->stream};
   char* b = static_cast<char*>(tmp);
   int* row_ptr = reinterpret_cast<int*>(b + o_rp);
   int* col_ptr = reinterpret_cast<int*>(b + o_cp);
@@ -606,7 +699,7 @@ static tcg_status build_programs(tcg_ctx* c, const tcg_problem* p) {
   }
   // [(m, o) pairs][per-coordinate offsets, nnz + 1] (the offsets for the product-parallel rows)
   const size_t upd_bytes = align_up(sizeof(int2) * std::max<long long>(total, 1), 256);
-  TCG_CUDA_TRY(c, cudaMalloc(&c->prog_arena, upd_bytes + sizeof(int) * (nnz + 1)));
+  TCG_CUDA_TRY(c, dev_alloc(c->device, &c->prog_arena, upd_bytes + sizeof(int) * (nnz + 1)));
   c->flow_upd = static_cast<int2*>(c->prog_arena);
   c->flow_ub = reinterpret_cast<int*>(static_cast<char*>(c->prog_arena) + upd_bytes);
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->flow_ub, ub32, sizeof(int) * nnz, cudaMemcpyDeviceToDevice, c->stream));
@@ -646,16 +739,16 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   TCG_CUDA_TRY(c, cudaSetDevice(c->device));
   if (c->arena) {
     TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    TCG_CUDA_TRY(c, cudaFree(c->arena));
+    dev_free(c->arena);
     c->arena = nullptr;
     c->uploaded = false;
   }
   if (c->batch_arena) {
-    TCG_CUDA_TRY(c, cudaFree(c->batch_arena));
+    dev_free(c->batch_arena);
     c->batch_arena = nullptr;
   }
   if (c->prog_arena) {
-    TCG_CUDA_TRY(c, cudaFree(c->prog_arena));
+    dev_free(c->prog_arena);
     c->prog_arena = nullptr;
   }
   c->flow_ub = nullptr;  // lives in prog_arena (device-built programs only)
@@ -706,7 +799,7 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   const size_t o_mpivot = take(sizeof(double));
   const size_t o_ctrl = take(sizeof(tcbdev::Ctrl));
   const size_t o_trace = take(sizeof(unsigned long long) * (2 * ntab + 4 * std::max(p->nitems, p->nflow)));
-  TCG_CUDA_TRY(c, cudaMalloc(&c->arena, off));
+  TCG_CUDA_TRY(c, dev_alloc(c->device, &c->arena, off));
   c->arena_bytes = off;
   char* base = static_cast<char*>(c->arena);
   c->cols = reinterpret_cast<int*>(base + o_cols);
