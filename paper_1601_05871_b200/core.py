@@ -56,7 +56,15 @@ class CsrMatrix:
         v.nnz = self.nnz()
         v.row_ptr = self.row_ptr.ctypes.data_as(N.i64p)
         v.col_idx = self.col_idx.ctypes.data_as(N.i32p)
-        v.values = self.values.ctypes.data_as(N.f64p)
+        vals = self.values
+        if vals.ndim == 1 and vals.size > 1 and vals.strides[0] == 0:
+            # a pattern's broadcast 1.0 values (levelk_pattern_gpu): dense only when C needs them
+            dense = getattr(self, "_dense_values", None)
+            if dense is None or dense.size != vals.size:
+                dense = np.ascontiguousarray(vals)
+                self._dense_values = dense
+            vals = dense
+        v.values = vals.ctypes.data_as(N.f64p)
         return v
 
     @staticmethod
@@ -396,11 +404,13 @@ class GpuSymbolic:
     def levelk(self, level: int, all_slow: bool = False) -> Tuple[FillPattern, SymbolicStats]:
         s = N.SymStats()
         self._check(self._lib.tcg_sym_levelk(self.h, level, N.TCG_SYM_ALL_SLOW if all_slow else 0, C.byref(s)))
-        n = self.a.nrows
-        rp = np.zeros(n + 1, np.int64)
-        ci = np.zeros(max(int(s.nnz_u), 1), np.int32)
+        n, nnz = self.a.nrows, int(s.nnz_u)
+        rp = np.empty(n + 1, np.int64)
+        ci = np.empty(max(nnz, 1), np.int32)
         self._check(self._lib.tcg_sym_download(self.h, rp.ctypes.data_as(N.i64p), ci.ctypes.data_as(N.i32p)))
-        pat = CsrMatrix(n, n, rp, ci[:int(s.nnz_u)].copy(), np.ones(int(s.nnz_u)))
+        # the pattern's values are 1.0 and unused (symbolic.hpp:118): a read-only broadcast,
+        # made dense only if the pattern is handed to C as a matrix (CsrMatrix.view)
+        pat = CsrMatrix(n, n, rp, ci[:nnz], np.broadcast_to(np.float64(1.0), (nnz,)))
         st = SymbolicStats(s.device_ms, s.host_ms, int(s.nnz_u), int(s.nnz_triu_input), int(s.slow_rows), int(s.tier2_rows),
                            int(s.kernel_launches), int(s.grid_ctas), int(s.single_pass))
         return FillPattern(pat, level, int(s.nnz_triu_input)), st

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/tacho_b200.h"
@@ -134,20 +135,48 @@ tcg_status tcg_sym_upload(tcg_sym* s, const tcg_csr_view* a) {
     s->err = "tcg_sym_upload: row_ptr must run from 0 to nnz";
     return TCG_INVALID;
   }
+  // the checks and count_upper (csr_matrix.hpp:219-225) over row blocks on the host threads
+  const int nt = static_cast<int>(std::clamp<int64_t>(a->n / 65536, 1,
+                                                      std::max(1u, std::thread::hardware_concurrency())));
+  std::vector<int64_t> triu_part(static_cast<size_t>(nt), 0);
+  std::vector<int> bad(static_cast<size_t>(nt), 0);  // 1 row_ptr decreases, 2 column out of range
+  auto check = [&](int k) {
+    const int32_t b = static_cast<int32_t>(static_cast<int64_t>(a->n) * k / nt);
+    const int32_t e = static_cast<int32_t>(static_cast<int64_t>(a->n) * (k + 1) / nt);
+    int64_t triu = 0;
+    for (int32_t i = b; i < e; ++i) {
+      if (a->row_ptr[i + 1] < a->row_ptr[i]) {
+        bad[static_cast<size_t>(k)] = 1;
+        return;
+      }
+      for (int64_t q = a->row_ptr[i]; q < a->row_ptr[i + 1]; ++q) {
+        const int32_t c = a->col_idx[q];
+        if (c < 0 || c >= a->n) {
+          bad[static_cast<size_t>(k)] = 2;
+          return;
+        }
+        triu += c >= i;
+      }
+    }
+    triu_part[static_cast<size_t>(k)] = triu;
+  };
+  {
+    std::vector<std::thread> pool;
+    for (int k = 1; k < nt; ++k) pool.emplace_back(check, k);
+    check(0);
+    for (auto& th : pool) th.join();
+  }
   int64_t triu = 0;
-  for (int32_t i = 0; i < a->n; ++i) {
-    if (a->row_ptr[i + 1] < a->row_ptr[i]) {
+  for (int k = 0; k < nt; ++k) {  // the first failing block's error, as the sequential scan reports
+    if (bad[static_cast<size_t>(k)] == 1) {
       s->err = "tcg_sym_upload: row_ptr decreases";
       return TCG_INVALID;
     }
-    for (int64_t q = a->row_ptr[i]; q < a->row_ptr[i + 1]; ++q) {
-      const int32_t c = a->col_idx[q];
-      if (c < 0 || c >= a->n) {
-        s->err = "tcg_sym_upload: column index out of range";
-        return TCG_INVALID;
-      }
-      triu += c >= i;  // count_upper (csr_matrix.hpp:219-225)
+    if (bad[static_cast<size_t>(k)] == 2) {
+      s->err = "tcg_sym_upload: column index out of range";
+      return TCG_INVALID;
     }
+    triu += triu_part[static_cast<size_t>(k)];
   }
   SYM_TRY(s, cudaSetDevice(s->device));
   SYM_TRY(s, cudaStreamSynchronize(s->stream));
