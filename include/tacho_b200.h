@@ -349,6 +349,14 @@ tcg_status tcg_solve_sync(tcg_solve* s);
  * the products are summed in column order. */
 tcg_status tcg_solve_set_matrix(tcg_solve* s, const tcg_csr_view* a);
 tcg_status tcg_solve_spmv(tcg_solve* s, const double* x_dev, double* y_dev);
+/* Conjugate-gradient vector updates on the context's stream (device vectors of n doubles;
+ * state = {rz, live (1/0), threshold} in device memory; dots summed in a fixed order, so
+ * the iterates are the same in every run). cg_step: alpha = rz / (p . ap); where live,
+ * x += alpha p and r -= alpha ap; hist[it] = ||r||; live = 0 once ||r|| <= threshold.
+ * cg_direction: rz' = r . z; p = p (rz' / rz) + z; rz = rz'. */
+tcg_status tcg_solve_cg_step(tcg_solve* s, double* x, double* r, const double* p, const double* ap, double* state,
+                             double* hist, int32_t it);
+tcg_status tcg_solve_cg_direction(tcg_solve* s, const double* r, const double* z, double* p, double* state);
 /* The context's stream (cudaStream_t): everything above is ordered on it. */
 tcg_status tcg_solve_stream(tcg_solve* s, void** stream);
 /* With TCG_SOLVE_TRACE=1 in the environment: per schedule position (2 n) the globaltimer

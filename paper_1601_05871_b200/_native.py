@@ -219,6 +219,9 @@ SIGNATURES = [
     ("tcg_solve_apply", C.c_int, [C.c_void_p, f64p, f64p, C.c_int32, C.POINTER(SolveStats)]),
     ("tcg_solve_trace", C.c_int, [C.c_void_p, u64p, C.c_void_p]),
     ("tcg_solve_set_matrix", C.c_int, [C.c_void_p, C.POINTER(CsrView)]),
+    ("tcg_solve_cg_step", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_int32]),
+    ("tcg_solve_cg_direction", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tcg_solve_spmv", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tcg_solve_stream", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     ("tcg_solve_apply_device", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(SolveStats)]),

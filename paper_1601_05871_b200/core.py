@@ -875,6 +875,20 @@ class GpuTriSolve:
         if st != N.TCG_OK:
             raise (ValueError if st == N.TCG_INVALID else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
 
+    def cg_step_ptr(self, x: int, r: int, p: int, ap: int, state: int, hist: int, it: int):
+        """tcg_solve_cg_step on device vectors (asynchronous, the context's stream)."""
+        st = self._lib.tcg_solve_cg_step(self.h, C.c_void_p(x), C.c_void_p(r), C.c_void_p(p), C.c_void_p(ap),
+                                         C.c_void_p(state), C.c_void_p(hist), it)
+        if st != N.TCG_OK:
+            raise (ValueError if st == N.TCG_INVALID else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
+
+    def cg_direction_ptr(self, r: int, z: int, p: int, state: int):
+        """tcg_solve_cg_direction on device vectors (asynchronous, the context's stream)."""
+        st = self._lib.tcg_solve_cg_direction(self.h, C.c_void_p(r), C.c_void_p(z), C.c_void_p(p),
+                                              C.c_void_p(state))
+        if st != N.TCG_OK:
+            raise (ValueError if st == N.TCG_INVALID else DeviceError)(self._lib.tcg_solve_error(self.h).decode())
+
     def spmv_ptr(self, x_ptr: int, y_ptr: int):
         """y = A x on device vectors, on the context's stream (asynchronous)."""
         st = self._lib.tcg_solve_spmv(self.h, C.c_void_p(x_ptr), C.c_void_p(y_ptr))
@@ -952,27 +966,24 @@ def pcg(solver: "GpuTriSolve", b, tol: float = 1e-8, maxit: int = 1000, precondi
             return PcgResult(np.zeros(bd.numel()), 0, True, 0.0, time.perf_counter() - t0)
         thr = tol * bnorm
         hist = torch.empty(max(maxit, 1), dtype=torch.float64, device=dev)
-        live = torch.ones((), dtype=torch.bool, device=dev)
         prec(r, z)
         p = z.clone()
-        rz = torch.dot(r, z)
+        # {rz, live, threshold} on the device: the vector updates are two fused kernels per
+        # iteration (tcg_solve_cg_step / cg_direction, deterministic dots)
+        state = torch.stack([torch.dot(r, z), torch.ones((), dtype=torch.float64, device=dev),
+                             torch.full((), thr, dtype=torch.float64, device=dev)])
         done, it, rel, converged = 0, 0, 1.0, False
         while done < maxit and not converged:
             k = min(check_every, maxit - done)
             for _ in range(k):
                 solver.spmv_ptr(p.data_ptr(), ap.data_ptr())
-                alpha = rz / torch.dot(p, ap)
-                # where, not alpha·live: a frozen step may carry 0/0 (r hit 0 exactly)
-                x.add_(torch.where(live, alpha * p, 0.0))
-                r.sub_(torch.where(live, alpha * ap, 0.0))
-                nr = torch.linalg.vector_norm(r)
-                hist[done] = nr
+                # alpha = rz / (p.ap); where live: x += alpha p, r -= alpha ap (a frozen step
+                # may carry 0/0); hist[done] = ||r||; live = 0 once ||r|| <= thr (NaN stays live)
+                solver.cg_step_ptr(x.data_ptr(), r.data_ptr(), p.data_ptr(), ap.data_ptr(), state.data_ptr(),
+                                   hist.data_ptr(), done)
                 done += 1
-                live = live & torch.logical_not(nr <= thr)  # a NaN norm stays live
                 prec(r, z)
-                rz_new = torch.dot(r, z)
-                p.mul_(rz_new / rz).add_(z)
-                rz = rz_new
+                solver.cg_direction_ptr(r.data_ptr(), z.data_ptr(), p.data_ptr(), state.data_ptr())
             h = hist[done - k:done].cpu().numpy()
             solver.sync()  # a watchdog expiry in any of the k applies raises here
             hit = np.nonzero(h <= thr)[0]

@@ -62,11 +62,11 @@ __device__ __forceinline__ unsigned long long wait_value_sys(const double* p, Ct
   }
 }
 
-// WEAK: first attempt of every gather is a plain (L1-cached) load; only a
-// kUnset answer falls back to strong polling. Sound because a location
-// holds kUnset until its single final value is written: any other bits a
-// load returns are the final value (8-byte aligned accesses do not tear),
-// and a stale L1 copy can only show kUnset, which the strong path re-reads.
+// The gather context. Every load of a factor value is a strong (L2) load: a
+// location holds kUnset until its single final value is written, so any
+// other bits a load returns are the final value (8-byte aligned accesses do
+// not tear). (L1-cached first loads, validated against kUnset, measured no
+// better in round 1.)
 // `vals`/`a`/`member`: the current row's member of a batch (its value sets
 // are nnz apart; the pattern, records and programs are shared).
 // OPS: how a negative operand position is read. 0: never happens; 2
@@ -76,7 +76,7 @@ __device__ __forceinline__ unsigned long long wait_value_sys(const double* p, Ct
 // critical rows are about to write; sleeping between polls frees the L2
 // slices serving them (B200, C3: 4.01 ms without, 2.66 ms at 400 ns; C4
 // 1.49 -> 1.37 at 200 ns; short programs lose: C2 0.41 -> 0.42-0.45 ms).
-template <int WEAK, int OPS = 0, int BO = 0>
+template <int OPS = 0, int BO = 0>
 struct Ctx {
   const FlowParams& P;
   unsigned long long t0;
@@ -93,10 +93,8 @@ struct Ctx {
   }
   __device__ __forceinline__ unsigned long long ld(int pos) const {
     if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
-    if (WEAK) return ld_weak_u64(vals + pos);
     return ld_relaxed_u64(vals + pos);
   }
-  // re-polls are always strong: a weak (L1) copy of the marker may be stale
   __device__ __forceinline__ unsigned long long ld_strong(int pos) const {
     if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
     return ld_relaxed_u64(vals + pos);

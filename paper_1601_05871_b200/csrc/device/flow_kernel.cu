@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
   }
   const int W = (DRAIN ? P.row_ctas : static_cast<int>(gridDim.x)) * kWarps;
   const int w0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
-  Ctx<0, REMOTE ? 2 : 0, BO> C{P, gtimer(), P.vals, P.a, 0};
+  Ctx<REMOTE ? 2 : 0, BO> C{P, gtimer(), P.vals, P.a, 0};
   int ran = 0, executed = 0, anyfail = 0;
   const int nrows = EXTRAS ? P.nrows * P.nbatch : P.nrows;
   auto member_of = [&](int p, int& q) {

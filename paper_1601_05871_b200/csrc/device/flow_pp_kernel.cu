@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256, MINB) factor_flow_pp(FlowParams P) {
   const int bar = 1 + gi;
   const int W = (DRAIN ? P.row_ctas : static_cast<int>(gridDim.x)) * G;
   const int g0 = blockIdx.x * G + gi;
-  Ctx<0, 0, BO> Cx{P, gtimer(), P.vals, P.a, 0};
+  Ctx<0, BO> Cx{P, gtimer(), P.vals, P.a, 0};
   const int nrows = EXTRAS ? P.nrows * P.nbatch : P.nrows;
   auto split = [&](int p, int& q) -> int {
     if (!EXTRAS) {

@@ -31,5 +31,11 @@ cudaError_t launch_spmv(int n, const long long* ptr, const int* col, const doubl
 cudaError_t launch_solve_gather(const double* u, const int* pos, double* fval, long long n, int sm_count,
                                 cudaStream_t st);
 cudaError_t launch_trisolve(const SolveParams& p, int grid, cudaStream_t st);
+// conjugate-gradient vector updates (cooperative, deterministic dots); state = {rz, live, thr}
+cudaError_t cg_grid(int sm_count, int* grid);
+cudaError_t launch_cg_step(int n, double* x, double* r, const double* p, const double* ap, double* state,
+                           double* hist, int it, double* partial, int grid, cudaStream_t st);
+cudaError_t launch_cg_direction(int n, const double* r, const double* z, double* p, double* state, double* partial,
+                                int grid, cudaStream_t st);
 
 }  // namespace tcbdev

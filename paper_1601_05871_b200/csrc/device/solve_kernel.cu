@@ -13,7 +13,10 @@
 // (each rounded on its own) and subtracted in ascending source order by a
 // broadcast chain -- the oracle's sequential order (oracle.c orc_trisolve),
 // so the solution is bitwise equal to it.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "solve_api.hpp"
 #include "sync.cuh"
@@ -157,6 +160,126 @@ cudaError_t launch_spmv(int n, const long long* ptr, const int* col, const doubl
   blocks = blocks > 16 * sm_count ? 16 * sm_count : blocks;
   spmv_csr<<<blocks, 256, 0, st>>>(n, ptr, col, val, x, y);
   return cudaGetLastError();
+}
+
+// ---- conjugate-gradient vector updates (the caller of the apply) ----------
+// Two cooperative kernels per iteration replace a dozen small launches. The
+// dots are deterministic: every thread sums its strided elements in order,
+// every block reduces its threads in a fixed tree into partial[block], and
+// after a grid barrier every block sums the partials in block order -- the
+// same bits in every block and in every run. state = {rz, live (1/0), thr}.
+namespace {
+
+template <int T>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(kFull, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < T / 32; ++i) s = __dadd_rn(s, red[i]);
+  return s;  // valid in thread 0
+}
+
+// the sum of the blocks' partials in a fixed order (lane l sums blocks l, l+32,
+// ... in order, then a fixed shuffle tree), broadcast to the block
+__device__ __forceinline__ double grid_total(const double* partial, double* red) {
+  if (threadIdx.x < 32) {
+    double s = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) s = __dadd_rn(s, __ldcg(partial + b));
+    for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_down_sync(kFull, s, o));
+    if (threadIdx.x == 0) red[0] = s;
+  }
+  __syncthreads();
+  const double s = red[0];
+  __syncthreads();
+  return s;
+}
+
+// alpha = rz / (p . ap); x += alpha p and r -= alpha ap where live; ||r|| -> hist[it]; live &= ||r|| > thr
+__global__ void __launch_bounds__(256) cg_step(int n, double* x, double* r, const double* p, const double* ap,
+                                               double* state, double* hist, int it, double* partial) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[8];
+  const int stride = gridDim.x * blockDim.x;
+  double d = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) d = __dadd_rn(d, __dmul_rn(p[i], ap[i]));
+  d = block_sum<256>(d, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = d;
+  __threadfence();
+  grid.sync();
+  const double pap = grid_total(partial, red);
+  const bool live = __ldcg(state + 1) != 0.0;
+  const double alpha = __ddiv_rn(__ldcg(state), pap);
+  double q = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double ri = r[i];
+    if (live) {  // (where, not alpha * live: a frozen step may carry 0/0)
+      x[i] = __dadd_rn(x[i], __dmul_rn(alpha, p[i]));
+      ri = __dsub_rn(ri, __dmul_rn(alpha, ap[i]));
+      r[i] = ri;
+    }
+    q = __dadd_rn(q, __dmul_rn(ri, ri));
+  }
+  q = block_sum<256>(q, red);
+  grid.sync();  // every block has read `partial` (pap) before it is reused
+  if (threadIdx.x == 0) partial[blockIdx.x] = q;
+  __threadfence();
+  grid.sync();
+  const double nr = __dsqrt_rn(grid_total(partial, red));
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    hist[it] = nr;
+    if (live && nr <= state[2]) state[1] = 0.0;  // a NaN norm stays live
+  }
+}
+
+// beta = (r . z) / rz; p = p * beta + z; rz = r . z
+__global__ void __launch_bounds__(256) cg_direction(int n, const double* r, const double* z, double* p,
+                                                    double* state, double* partial) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[8];
+  const int stride = gridDim.x * blockDim.x;
+  double d = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) d = __dadd_rn(d, __dmul_rn(r[i], z[i]));
+  d = block_sum<256>(d, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = d;
+  __threadfence();
+  grid.sync();
+  const double rz_new = grid_total(partial, red);
+  const double beta = __ddiv_rn(rz_new, __ldcg(state));
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) p[i] = __dadd_rn(__dmul_rn(p[i], beta), z[i]);
+  grid.sync();  // every block has read the old rz
+  if (blockIdx.x == 0 && threadIdx.x == 0) state[0] = rz_new;
+}
+
+}  // namespace
+
+cudaError_t cg_grid(int sm_count, int* grid) {
+  int occ = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, cg_step, 256, 0);
+  int occ2 = 0;
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, cg_direction, 256, 0);
+  // one block per SM: enough threads for these vectors, and few partials to sum
+  *grid = (std::min(occ, occ2) >= 1 ? 1 : 0) * sm_count;
+  if (*grid < 1) *grid = 1;
+  return e;
+}
+
+cudaError_t launch_cg_step(int n, double* x, double* r, const double* p, const double* ap, double* state,
+                           double* hist, int it, double* partial, int grid, cudaStream_t st) {
+  void* args[] = {&n, &x, &r, const_cast<const double**>(&p), const_cast<const double**>(&ap), &state, &hist, &it,
+                  &partial};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&cg_step), grid, 256, args, 0, st);
+}
+
+cudaError_t launch_cg_direction(int n, const double* r, const double* z, double* p, double* state, double* partial,
+                                int grid, cudaStream_t st) {
+  void* args[] = {&n, const_cast<const double**>(&r), const_cast<const double**>(&z), &p, &state, &partial};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&cg_direction), grid, 256, args, 0, st);
 }
 
 cudaError_t solve_occupancy(int* ctas_per_sm) {

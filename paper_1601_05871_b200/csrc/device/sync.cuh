@@ -94,11 +94,6 @@ __device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const void* p) 
 __device__ __forceinline__ void st_relaxed_sys_u64(void* p, unsigned long long v) {
   asm volatile("st.relaxed.sys.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_weak_u64(const void* p) {
-  unsigned long long v;
-  asm volatile("ld.global.ca.b64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
-}
 __device__ __forceinline__ void st_relaxed_u64(void* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }

@@ -46,6 +46,8 @@ struct tcg_solve {
   long long* a_ptr = nullptr;
   int* a_col = nullptr;
   double* a_val = nullptr;
+  double* cg_partial = nullptr;  // per block of the CG update kernels
+  int cg_grid = 0;
 };
 
 namespace {
@@ -214,6 +216,7 @@ void tcg_solve_destroy(tcg_solve* s) {
   if (s->arena) cudaFree(s->arena);
   if (s->trace) cudaFree(s->trace);
   if (s->a_arena) cudaFree(s->a_arena);
+  if (s->cg_partial) cudaFree(s->cg_partial);
   if (s->ev0) cudaEventDestroy(s->ev0);
   if (s->ev1) cudaEventDestroy(s->ev1);
   delete s;
@@ -380,6 +383,48 @@ tcg_status tcg_solve_spmv(tcg_solve* s, const double* x_dev, double* y_dev) {
   if (!tcb_internal::ctx_factor(s->ctx, 0, &device, &stream, &vals, &n, &nnz)) return TCG_INVALID;
   SOLVE_TRY(s, cudaSetDevice(device));
   SOLVE_TRY(s, tcbdev::launch_spmv(s->n, s->a_ptr, s->a_col, s->a_val, x_dev, y_dev, s->sm_count, stream));
+  return TCG_OK;
+}
+
+namespace {
+
+tcg_status cg_prepare(tcg_solve* s, cudaStream_t* stream) {
+  int device = 0;
+  const double* vals = nullptr;
+  std::int64_t n = 0, nnz = 0;
+  if (!tcb_internal::ctx_factor(s->ctx, 0, &device, stream, &vals, &n, &nnz)) return TCG_INVALID;
+  SOLVE_TRY(s, cudaSetDevice(device));
+  if (!s->cg_partial) {
+    SOLVE_TRY(s, tcbdev::cg_grid(s->sm_count, &s->cg_grid));
+    SOLVE_TRY(s, cudaMalloc(&s->cg_partial, sizeof(double) * static_cast<size_t>(s->cg_grid)));
+  }
+  return TCG_OK;
+}
+
+}  // namespace
+
+tcg_status tcg_solve_cg_step(tcg_solve* s, double* x, double* r, const double* p, const double* ap, double* state,
+                             double* hist, int32_t it) {
+  if (!s || !state || !hist || it < 0 || (s->n > 0 && (!x || !r || !p || !ap))) {
+    if (s) s->err = "tcg_solve_cg_step: null vectors";
+    return TCG_INVALID;
+  }
+  cudaStream_t st = nullptr;
+  const tcg_status ok = cg_prepare(s, &st);
+  if (ok != TCG_OK) return ok;
+  SOLVE_TRY(s, tcbdev::launch_cg_step(s->n, x, r, p, ap, state, hist, it, s->cg_partial, s->cg_grid, st));
+  return TCG_OK;
+}
+
+tcg_status tcg_solve_cg_direction(tcg_solve* s, const double* r, const double* z, double* p, double* state) {
+  if (!s || !state || (s->n > 0 && (!r || !z || !p))) {
+    if (s) s->err = "tcg_solve_cg_direction: null vectors";
+    return TCG_INVALID;
+  }
+  cudaStream_t st = nullptr;
+  const tcg_status ok = cg_prepare(s, &st);
+  if (ok != TCG_OK) return ok;
+  SOLVE_TRY(s, tcbdev::launch_cg_direction(s->n, r, z, p, state, s->cg_partial, s->cg_grid, st));
   return TCG_OK;
 }
 
