@@ -19,6 +19,9 @@
 #include "taskchol/matrix_market.hpp"
 #include "taskchol/pipeline.hpp"
 #include "taskchol/symbolic.hpp"
+// the reference's own test generators (tests/support), compiled where they
+// lie: they pin this repo's grid2d / path / random_spd generators
+#include "test_matrices.hpp"
 // this repo's seeded generators, compiled into the
 // shim so bench.py's reference arm builds its inputs without loading the
 // product library
@@ -252,6 +255,26 @@ ref_csr* ref_generate(const char* kind, int64_t p0, int64_t p1, uint64_t seed) {
     out->m.row_ptr.assign(g.row_ptr.begin(), g.row_ptr.end());
     out->m.col_idx.assign(g.col_idx.begin(), g.col_idx.end());
     out->m.values.assign(g.values.begin(), g.values.end());
+    return out.release();
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+// The reference's test generators (tests/support/test_matrices.hpp:18-82):
+// "grid" (p0 x p1 5-point Laplacian), "path" (p0 vertices), "random_spd"
+// (p0 rows, density p1 / 1e6, a freshly seeded std::mt19937).
+ref_csr* ref_test_matrix(const char* kind, int64_t p0, int64_t p1, uint64_t seed) {
+  try {
+    const std::string k(kind ? kind : "");
+    auto out = std::make_unique<ref_csr>();
+    if (k == "grid") out->m = testing::grid_laplacian(static_cast<index_t>(p0), static_cast<index_t>(p1));
+    else if (k == "path") out->m = testing::path_matrix(static_cast<index_t>(p0));
+    else if (k == "random_spd") {
+      std::mt19937 rng(static_cast<std::uint32_t>(seed));
+      out->m = testing::random_spd(static_cast<index_t>(p0), static_cast<double>(p1) / 1e6, rng);
+    } else throw std::invalid_argument("unknown reference test matrix '" + k + "'");
     return out.release();
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -251,6 +251,20 @@ class Reference:
         finally:
             self.L.ref_csr_free(h)
 
+    def test_matrix(self, kind, p0, p1=0, seed=0):
+        """The reference's own test generators (tests/support/test_matrices.hpp): (row_ptr, col_idx, values)."""
+        self.L.ref_test_matrix.restype = C.c_void_p
+        self.L.ref_test_matrix.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_uint64]
+        h = self.L.ref_test_matrix(kind.encode(), p0, p1, seed)
+        if not h:
+            raise ValueError(self.L.ref_error().decode())
+        try:
+            n, nnz = self.L.ref_csr_n(h), self.L.ref_csr_nnz(h)
+            return (self._arr(self.L.ref_csr_ptr(h), n + 1, np.int64), self._arr(self.L.ref_csr_col(h), nnz, np.int32),
+                    self._arr(self.L.ref_csr_val(h), nnz, np.float64))
+        finally:
+            self.L.ref_csr_free(h)
+
     def load_ordering(self, path, n):
         perm = np.zeros(max(n, 1), np.int32)
         cnt = self.L.ref_load_ordering(str(path).encode(), n, _p(perm, i32p), 0, C.cast(None, i32p))

@@ -51,10 +51,37 @@ CASES = {
 }
 
 
+# The reference's own test generators (tests/support/test_matrices.hpp) against
+# which this repo's grid2d / path / random_spd are pinned: (reference kind,
+# this repo's kind, p0, p1, seed)
+REF_GENERATORS = {
+    "grid_100x100": ("grid", "grid2d", 100, 100, 0),      # BASELINE.json configs[0]
+    "grid_20x20": ("grid", "grid2d", 20, 20, 0),
+    "grid_7x13": ("grid", "grid2d", 7, 13, 0),
+    "path_1000": ("path", "path", 1000, 0, 0),
+    "random_spd_200_s7": ("random_spd", "random_spd", 200, 20000, 7),
+    "random_spd_60_s1": ("random_spd", "random_spd", 60, 150000, 1),
+    "random_spd_333_s42": ("random_spd", "random_spd", 333, 8000, 42),
+}
+
+
+def reference_generators(golden):
+    """Hashes of the matrices the reference's test generators produce."""
+    O, R = Oracle(), Reference()
+    out = {}
+    for name, (rkind, kind, p0, p1, seed) in REF_GENERATORS.items():
+        ptr, col, val = R.test_matrix(rkind, p0, p1, seed)
+        out[name] = {"reference_kind": rkind, "kind": kind, "args": [p0, p1, seed], "n": int(len(ptr) - 1),
+                     "nnz": int(len(col)), "row_ptr": O.hash(ptr), "col_idx": O.hash(col), "values": O.hash(val)}
+        print(f"reference generator {name}: n={out[name]['n']} nnz={out[name]['nnz']} values={out[name]['values']}")
+    golden["reference_generators"] = out
+
+
 def main(names):
     O, R = Oracle(), Reference()
     out_path = os.path.join(HERE, "golden.json")
     golden = json.load(open(out_path)) if os.path.exists(out_path) else {}
+    reference_generators(golden)
     for name in names:
         kind, p0, p1, seed, level, leaf = CASES[name]
         t0 = time.time()
