@@ -424,14 +424,15 @@ def run_ours(args):
     host_out = torch.empty(nnz * per_rank, dtype=torch.float64).pin_memory()
     e2e_ms = []
     barrier()
-    # 6 more untimed calls: the call decides on this box whether the drain pays
-    # (capi.cpp, first calls alternate with and without it)
-    for i in range(6 + args.warmup + args.steps):
+    # 9 more untimed calls: the call decides on this box how the factor leaves
+    # (capi.cpp run_flow: a copy after the launch, the drain CTAs or chunked copies
+    # beside the launch take turns over the first calls of a problem)
+    for i in range(9 + args.warmup + args.steps):
         flush.fill_(1.0)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         st_e2e = fz.factor_host_a_ptr(host_in.data_ptr(), host_out.data_ptr())
-        if i >= 6 + args.warmup:
+        if i >= 9 + args.warmup:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
     barrier()
     if batched:  # back to the initialised batch for anything after
@@ -511,8 +512,11 @@ def run_ours(args):
                    "parity_vs_oracle": parity},
         "e2e": {"value": units / (e2e / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * nnz_a * per_rank,
                 "d2h_bytes_per_step": 8 * nnz * per_rank, "ms_per_step": e2e,
-                "call": "tcg_factor_host_a: PaP values in (host), device init_factor_values, factor; the factor "
-                        "leaves through CTAs of the same launch as it becomes final (drain)",
+                "call": "tcg_factor_host_a: PaP values in (pinned host), device init_factor_values, factor, the "
+                        "factor out (pinned host); how it leaves is calibrated per problem (d2h)",
+                "d2h": ("copy after the launch" if st_e2e.drain_ctas == 0 else
+                        f"{st_e2e.drain_ctas} drain CTAs of the launch (zero-copy stores)" if st_e2e.drain_ctas > 0 else
+                        f"{-st_e2e.drain_ctas} chunks copied by the copy engine beside the launch as they become final"),
                 "drain_ctas": int(st_e2e.drain_ctas),
                 "launches": int(st_e2e.kernel_launches)},
         "gpu_launches": launches_per_step * args.steps,

@@ -159,7 +159,8 @@ typedef struct {
   int32_t batch;             /* mode 5: value sets factored by the call */
   int32_t breakdown_member;  /* batch: member of breakdown_row (-1 when none) */
   int32_t drain_ctas;        /* end to end: CTAs that copied the factor to the host during the
-                                launch (0: a D2H copy after it) */
+                                launch; negative: minus the number of chunks the copy engine took
+                                out beside the launch as they became final; 0: a D2H copy after it */
   int32_t chunks;            /* end to end, batches: member chunks pipelined with the copies
                                 (0: one launch) */
   int32_t row_kernel;        /* mode 5: 1 = one lane per coordinate (factor_flow_pipe),

@@ -194,11 +194,22 @@ struct tcg_ctx {
   int device = 0;
   int sm_count = 0;
   cudaStream_t stream = nullptr;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
-  // end to end with a pinned output: best whole-call ms without (0) and with (1)
-  // the drain over the first calls of a problem and batch size (alternating)
-  float drain_ms[2] = {-1.f, -1.f};
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr, ev3 = nullptr;
+  // end to end with a pinned output: best whole-call ms of a copy after the
+  // launch (0), the drain CTAs (1) and the chunked copies (2) over the first
+  // calls of a problem and batch size (taking turns)
+  float drain_ms[3] = {-1.f, -1.f, -1.f};
   int drain_calls = 0;
+  // chunked download (run_flow, mode 2): chunk starts (host, nchunks + 1), device
+  // counters (units per chunk, and the working copy), host-mapped flags
+  int nchunks = 0;
+  bool chunks_ready = false;
+  std::vector<std::int64_t> chunk_start;
+  int* chunk_units = nullptr;
+  int* chunk_left = nullptr;
+  int* chunk_flag = nullptr;    // pinned, mapped
+  int* chunk_flag_d = nullptr;  // its device address
+  int chunk_seq = 0;
   void* arena = nullptr;
   size_t arena_bytes = 0;
   tcbdev::Ctrl* host_ctrl = nullptr;
@@ -498,6 +509,7 @@ tcg_status tcg_create(int device, tcg_ctx** out) {
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev2);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev3, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMallocHost(reinterpret_cast<void**>(&c->host_ctrl), sizeof(tcbdev::Ctrl));
   if (e != cudaSuccess) {
     g_plan_error = std::string("tcg_create: ") + cudaGetErrorString(e);
@@ -518,6 +530,8 @@ void tcg_destroy(tcg_ctx* c) {
   dev_free(c->prog_arena);
   if (c->a_stage) cudaFree(c->a_stage);
   if (c->drain_done) cudaFree(c->drain_done);
+  if (c->chunk_units) cudaFree(c->chunk_units);
+  if (c->chunk_flag) cudaFreeHost(c->chunk_flag);
   if (c->peers) cudaFree(c->peers);
   for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
   dev_free(c->arena);
@@ -525,6 +539,7 @@ void tcg_destroy(tcg_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->ev2) cudaEventDestroy(c->ev2);
+  if (c->ev3) cudaEventDestroy(c->ev3);
   for (cudaEvent_t e : c->chunk_ev) cudaEventDestroy(e);
   if (c->host_ctrls) cudaFreeHost(c->host_ctrls);
   if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
@@ -891,7 +906,8 @@ tcg_status tcg_upload(tcg_ctx* c, const tcg_problem* p) {
   c->max_target_len = p->max_target_len;
   c->max_flag_rows = p->max_flag_rows;
   c->uploaded = true;
-  c->drain_ms[0] = c->drain_ms[1] = -1.f;
+  c->chunks_ready = false;
+  c->drain_ms[0] = c->drain_ms[1] = c->drain_ms[2] = -1.f;
   c->drain_calls = 0;
   c->pristine = true;
   return TCG_OK;
@@ -921,6 +937,42 @@ tcg_status tcg_restore(tcg_ctx* c) {
                                   cudaMemcpyDeviceToDevice, c->stream));
   TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
   c->pristine = true;
+  return TCG_OK;
+}
+
+// The chunks of the chunked download (run_flow, mode 2): up to 64 ranges of U
+// of at least 512 KB, cut at unit starts; a unit at tb lies in chunk
+// tb * nchunks / nnz. Built once per upload from the schedule's records.
+static tcg_status prepare_chunks(tcg_ctx* c) {
+  if (c->chunks_ready) return TCG_OK;
+  constexpr int kMaxChunks = 64;
+  std::int64_t least = 512 << 10;  // bytes per chunk at least (TCG_D2H_CHUNK_KB)
+  if (const char* e = std::getenv("TCG_D2H_CHUNK_KB")) least = std::max<std::int64_t>(1, std::atoll(e)) << 10;
+  const int n = static_cast<int>(std::min<std::int64_t>(kMaxChunks, c->nnz * 8 / least));
+  c->nchunks = n >= 4 ? n : 0;
+  c->chunks_ready = true;
+  if (!c->nchunks) return TCG_OK;
+  if (!c->chunk_units) {
+    TCG_CUDA_TRY(c, cudaMalloc(&c->chunk_units, sizeof(int) * 3 * kMaxChunks));
+    c->chunk_left = c->chunk_units + kMaxChunks;
+    TCG_CUDA_TRY(c, cudaHostAlloc(reinterpret_cast<void**>(&c->chunk_flag), sizeof(int) * kMaxChunks, cudaHostAllocMapped));
+    std::memset(c->chunk_flag, 0, sizeof(int) * kMaxChunks);
+    TCG_CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->chunk_flag_d), c->chunk_flag, 0));
+  }
+  int* start_d = c->chunk_units + 2 * kMaxChunks;
+  TCG_CUDA_TRY(c, tcbdev::launch_chunk_setup(c->flow_rec, static_cast<int>(c->nflow), c->nnz, c->nchunks, start_d,
+                                             c->chunk_units, c->sm_count, c->stream));
+  int start[kMaxChunks];
+  TCG_CUDA_TRY(c, cudaMemcpyAsync(start, start_d, sizeof(int) * c->nchunks, cudaMemcpyDeviceToHost, c->stream));
+  TCG_CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+  c->chunk_start.assign(static_cast<size_t>(c->nchunks) + 1, c->nnz);
+  for (int k = 0; k < c->nchunks; ++k) {
+    if (start[k] == 0x7f7f7f7f || (k == 0 && start[k] != 0)) {  // a range without a unit start: no chunks
+      c->nchunks = 0;
+      return TCG_OK;
+    }
+    c->chunk_start[static_cast<size_t>(k)] = start[k];
+  }
   return TCG_OK;
 }
 
@@ -989,35 +1041,58 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   int drain_ctas = mean > 16.0 ? 4 : 8;
   if (const char* e = std::getenv("TCG_DRAIN_CTAS")) drain_ctas = std::max(1, std::atoi(e));
   bool drain = host_out && pipe && !remote && !c->opt.trace && c->nflow > 0 && phase == 0;
-  if (const char* e = std::getenv("TCG_DRAIN")) drain = drain && std::atoi(e) != 0;
+  bool chunks = drain && c->nbatch == 1;
+  bool out_pinned = false;
   if (drain) {
     cudaPointerAttributes attr{};
     if (cudaPointerGetAttributes(&attr, host_out) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
-        attr.devicePointer)
+        attr.devicePointer) {
       drain_out = static_cast<double*>(attr.devicePointer);
-    else
+      out_pinned = true;
+    } else {
       cudaGetLastError();
+    }
     // 16-byte accesses on both sides (flow_kernel.cu drain_values)
     drain = drain_out != nullptr && reinterpret_cast<std::uintptr_t>(drain_out) % 16 == 0 &&
             reinterpret_cast<std::uintptr_t>(c->nbatch > 1 ? c->bvals : c->vals) % 16 == 0;
   }
-  // Whether the drain pays depends on the host: zero-copy writes from the SMs
-  // ran at ~40 GB/s on some B200 boxes (C2 end to end 1.02 -> 0.82 ms) and
-  // far slower on others (1.03 -> 1.44 ms), where the copy engine is the
-  // better path. Unless TCG_DRAIN decides, the first kDrainProbe calls of a
-  // problem alternate between the two (the very first call of a buffer pays
-  // one-time costs, so each side keeps its best), later calls take the faster.
-  constexpr int kDrainProbe = 6;
-  const bool drain_forced = std::getenv("TCG_DRAIN") != nullptr;
+  // chunked copies: the copy engine takes each chunk of U to the (pinned) host
+  // buffer as soon as its last unit has run, beside the rest of the launch
+  if (chunks && out_pinned) {
+    const tcg_status cs = prepare_chunks(c);
+    if (cs != TCG_OK) return cs;
+    chunks = c->nchunks > 0;
+    if (chunks && !c->d2h_stream) TCG_CUDA_TRY(c, cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+  } else {
+    chunks = false;
+  }
+  // How the factor should leave depends on the host: zero-copy writes from
+  // the SMs (the drain CTAs) ran at ~40 GB/s on some B200 boxes (C2 end to end
+  // 1.02 -> 0.82 ms) and far slower on others (1.03 -> 1.44 ms); the copy
+  // engine runs at PCIe speed everywhere, after the launch (mode 0) or chunk
+  // by chunk beside it (mode 2). Unless TCG_DRAIN decides (0 / 1 / 2), the
+  // first calls of a problem take turns (the very first call of a buffer pays
+  // one-time costs, so each mode keeps its best of 3), later calls take the fastest.
+  int dmode = 0;
   bool calibrating = false;
-  if (drain && !drain_forced) {
-    if (c->drain_calls < kDrainProbe) {
-      drain = (c->drain_calls & 1) != 0;
+  if (const char* e = std::getenv("TCG_DRAIN")) {
+    const int v = std::atoi(e);
+    dmode = (v == 1 && drain) ? 1 : (v == 2 && chunks) ? 2 : 0;
+  } else if (drain || chunks) {
+    int cand[3], nc = 0;
+    cand[nc++] = 0;
+    if (drain) cand[nc++] = 1;
+    if (chunks) cand[nc++] = 2;
+    if (c->drain_calls < 3 * nc) {
+      dmode = cand[c->drain_calls % nc];
       calibrating = true;
     } else {
-      drain = c->drain_ms[1] < c->drain_ms[0];
+      for (int i = 1; i < nc; ++i)
+        if (c->drain_ms[cand[i]] >= 0.f && c->drain_ms[cand[i]] < c->drain_ms[dmode]) dmode = cand[i];
     }
   }
+  drain = dmode == 1;
+  chunks = dmode == 2;
   // the 5-CTA kernel exists for one local matrix (with or without the drain)
   if (minb == 5 && (remote || extras || !pipe || kb > 2)) minb = 3;
   int occ = 0;
@@ -1034,10 +1109,11 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (pp) {
     if (pp_b < 0) pp_b = backoff;
     size_t pp_smem = 0;
-    cudaError_t pe = tcbdev::pp_occupancy(pp_w, pp_k, pp_n, pp_m, extras, drain ? 1 : 0, pp_b, pp_d, &occ, &pp_smem);
-    if (pe != cudaSuccess && drain) {
+    cudaError_t pe = tcbdev::pp_occupancy(pp_w, pp_k, pp_n, pp_m, extras, dmode, pp_b, pp_d, &occ, &pp_smem);
+    if (pe != cudaSuccess && dmode) {
       cudaGetLastError();
-      drain = false;
+      drain = chunks = false;
+      dmode = 0;
       pe = tcbdev::pp_occupancy(pp_w, pp_k, pp_n, pp_m, extras, 0, pp_b, pp_d, &occ, &pp_smem);
     }
     if (pe != cudaSuccess) {
@@ -1047,10 +1123,11 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   }
   if (!pp) {
     pipe = true;
-    cudaError_t oe = tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, drain ? 1 : 0, backoff);
-    if (oe != cudaSuccess && drain) {  // no drain variant: a copy after the launch
+    cudaError_t oe = tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, dmode, backoff);
+    if (oe != cudaSuccess && dmode) {  // no such variant: a copy after the launch
       cudaGetLastError();
-      drain = false;
+      drain = chunks = false;
+      dmode = 0;
       oe = tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, 0, backoff);
     }
     if (oe == cudaErrorInvalidValue) {
@@ -1068,7 +1145,10 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (c->opt.ctas_per_sm > 0) occ = std::min(occ, c->opt.ctas_per_sm);
   if (const char* e = std::getenv("TCG_FLOW_CTAS")) occ = std::max(1, std::min(occ, std::atoi(e)));
   const int grid = std::max(1, occ * c->sm_count);
-  if (drain && grid <= drain_ctas) drain = false;
+  if (drain && grid <= drain_ctas) {
+    drain = false;
+    dmode = 0;
+  }
   const bool batch = c->nbatch > 1;
   if (static_cast<int64_t>(c->nflow) * c->nbatch > 0x7fffffffLL) {
     c->err = "value-flow batch: rows x members beyond 2^31";
@@ -1122,6 +1202,12 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
     P.drain_out = drain_out;
     P.drain_done = c->drain_done;
   }
+  if (chunks) {
+    P.chunk_left = c->chunk_left;
+    P.chunk_flag = c->chunk_flag_d;
+    P.nchunks = c->nchunks;
+    P.chunk_seq = ++c->chunk_seq;
+  }
   const double tmo = c->opt.timeout_s > 0 ? c->opt.timeout_s : 30.0;
   P.timeout_ns = static_cast<unsigned long long>(tmo * 1e9);
   const size_t vbytes = sizeof(double) * static_cast<size_t>(c->nnz) * c->nbatch;
@@ -1145,6 +1231,9 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   }
   if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));
   if (drain) TCG_CUDA_TRY(c, cudaMemsetAsync(c->drain_done, 0, sizeof(unsigned) * drain_words, c->stream));
+  if (chunks)
+    TCG_CUDA_TRY(c, cudaMemcpyAsync(c->chunk_left, c->chunk_units, sizeof(int) * c->nchunks, cudaMemcpyDeviceToDevice,
+                                    c->stream));
   P.ub = c->flow_ub;
   // the per-lane kernel's Chol pivot through shared memory, the waiting lanes
   // sleeping P.decouple ns between looks (flow_row): B200, C4 (12.4 products
@@ -1155,16 +1244,59 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (const char* e = std::getenv("TCG_FLOW_DECOUPLE")) P.decouple = std::atoi(e);
   if (c->nflow > 0) {
     if (pp)
-      TCG_CUDA_TRY(c, tcbdev::launch_flow_pp(P, grid, pp_w, pp_k, pp_n, pp_m, extras, drain ? 1 : 0, pp_b, pp_d,
+      TCG_CUDA_TRY(c, tcbdev::launch_flow_pp(P, grid, pp_w, pp_k, pp_n, pp_m, extras, dmode, pp_b, pp_d,
                                              c->stream));
     else
       TCG_CUDA_TRY(c, tcbdev::launch_flow_pipe(P, grid, threads, kb, minb, remote, extras, c->stream,
-                                               drain ? 1 : 0, backoff));
+                                               dmode, backoff));
   }
   TCG_CUDA_TRY(c, cudaEventRecord(c->ev1, c->stream));
   c->pristine = false;  // the working values now hold the factor
-  if (host_out && !drain)
+  if (host_out && !drain && !chunks)
     TCG_CUDA_TRY(c, cudaMemcpyAsync(host_out, vals, vbytes, cudaMemcpyDeviceToHost, c->stream));
+  if (chunks) {
+    // the host issues each chunk's copy (adjacent chunks together) on the copy
+    // stream as soon as the launch has flagged it; if the launch ends without
+    // every flag (a watchdog stop), the rest is copied after it
+    std::vector<char> sent(static_cast<size_t>(c->nchunks), 0);
+    const volatile int* flag = c->chunk_flag;
+    int left = c->nchunks;
+    auto copy = [&](int k0, int k1) {  // chunks [k0, k1)
+      const std::int64_t b = c->chunk_start[static_cast<size_t>(k0)], e = c->chunk_start[static_cast<size_t>(k1)];
+      return cudaMemcpyAsync(host_out + b, vals + b, sizeof(double) * static_cast<size_t>(e - b),
+                             cudaMemcpyDeviceToHost, c->d2h_stream);
+    };
+    unsigned idle = 0;
+    while (left > 0) {
+      bool any = false;
+      for (int k = 0; k < c->nchunks; ++k) {
+        if (sent[static_cast<size_t>(k)] || flag[k] != c->chunk_seq) continue;
+        int k1 = k + 1;
+        while (k1 < c->nchunks && !sent[static_cast<size_t>(k1)] && flag[k1] == c->chunk_seq) ++k1;
+        TCG_CUDA_TRY(c, copy(k, k1));
+        for (int x = k; x < k1; ++x) sent[static_cast<size_t>(x)] = 1;
+        left -= k1 - k;
+        any = true;
+        k = k1 - 1;
+      }
+      if (any) {
+        idle = 0;
+      } else if (++idle >= 256) {
+        idle = 0;
+        const cudaError_t qe = cudaStreamQuery(c->stream);
+        if (qe == cudaErrorNotReady) continue;
+        TCG_CUDA_TRY(c, qe);
+        bool all = true;  // the launch is over: its flags are all there, unless it was stopped
+        for (int k = 0; k < c->nchunks; ++k) all = all && (sent[static_cast<size_t>(k)] || flag[k] == c->chunk_seq);
+        if (all) continue;
+        for (int k = 0; k < c->nchunks; ++k)
+          if (!sent[static_cast<size_t>(k)]) TCG_CUDA_TRY(c, copy(k, k + 1));
+        left = 0;
+      }
+    }
+    TCG_CUDA_TRY(c, cudaEventRecord(c->ev3, c->d2h_stream));
+    TCG_CUDA_TRY(c, cudaStreamWaitEvent(c->stream, c->ev3, 0));
+  }
   if (calibrating) TCG_CUDA_TRY(c, cudaEventRecord(c->ev2, c->stream));
   TCG_CUDA_TRY(c, cudaMemcpyAsync(c->host_ctrl, c->ctrl, sizeof(tcbdev::Ctrl),
                                   cudaMemcpyDeviceToHost, c->stream));
@@ -1174,7 +1306,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   if (calibrating) {
     float whole = 0.f;
     TCG_CUDA_TRY(c, cudaEventElapsedTime(&whole, c->ev0, c->ev2));
-    float& best = c->drain_ms[drain ? 1 : 0];
+    float& best = c->drain_ms[dmode];
     if (best < 0.f || whole < best) best = whole;
     ++c->drain_calls;
   }
@@ -1185,7 +1317,7 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   S.staging_cap = kb;  // reported: gather batch
   S.kernel_launches = (c->nflow > 0 ? 1 : 0) + (phase == 0 ? 1 : 0) + (host_a ? 1 : 0);
   S.mode = 5;
-  S.drain_ctas = drain ? drain_ctas : 0;
+  S.drain_ctas = drain ? drain_ctas : chunks ? -c->nchunks : 0;  // (negative: chunked copies, their count)
   if (host_a) c->pristine = false;
   S.lanes_per_row = pp ? 32 * pp_w : 32;
   S.row_kernel = pp ? 2 : 1;
@@ -1615,7 +1747,7 @@ tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {
     c->batch_arena = nullptr;
   }
   c->nbatch = 1;
-  c->drain_ms[0] = c->drain_ms[1] = -1.f;
+  c->drain_ms[0] = c->drain_ms[1] = c->drain_ms[2] = -1.f;
   c->drain_calls = 0;
   if (nbatch == 1) return tcg_set_values(c, values);
   if (!c->has_flow) {
@@ -1633,7 +1765,7 @@ tcg_status tcg_set_batch(tcg_ctx* c, int32_t nbatch, const double* values) {
   c->bm_flags = reinterpret_cast<int*>(base + 3 * align_up(vb, 256));
   c->bm_pivot = reinterpret_cast<double*>(base + 3 * align_up(vb, 256) + fb);
   c->nbatch = nbatch;
-  c->drain_ms[0] = c->drain_ms[1] = -1.f;
+  c->drain_ms[0] = c->drain_ms[1] = c->drain_ms[2] = -1.f;
   c->drain_calls = 0;
   if (vb) {
     TCG_CUDA_TRY(c, cudaMemcpyAsync(c->bvals0, values, vb, cudaMemcpyHostToDevice, c->stream));
@@ -1674,7 +1806,7 @@ tcg_status tcg_set_a_values(tcg_ctx* c, int32_t nbatch, const double* a_values) 
       c->batch_arena = nullptr;
     }
     c->nbatch = nbatch;
-    c->drain_ms[0] = c->drain_ms[1] = -1.f;
+    c->drain_ms[0] = c->drain_ms[1] = c->drain_ms[2] = -1.f;
     c->drain_calls = 0;
   }
   const int64_t need = c->nnz_a * nbatch;

@@ -17,6 +17,9 @@ cudaError_t launch_factor(const Params& p, int grid, int threads, size_t smem, c
 
 
 cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStream_t st);
+// chunked download: chunk starts (first unit start at or after k * nnz / nchunks) and units per chunk
+cudaError_t launch_chunk_setup(const int4* rec, int nrows, long long nnz, int nchunks, int* start, int* units,
+                               int sm_count, cudaStream_t st);
 
 cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm,
                            int drain = 0, int backoff_ns = 0);

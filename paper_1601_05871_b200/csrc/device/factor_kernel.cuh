@@ -100,6 +100,13 @@ struct FlowParams {
   unsigned* drain_done;  // per batch of 32 groups of 64 values: groups copied (zeroed per launch)
   int row_ctas;          // CTAs that run rows
   int decouple;          // per-lane kernel: Chol pivot through shared memory (lanes publish independently)
+  // chunked download (end to end, DRAIN = 2): U in nchunks position ranges cut at unit starts (a unit at
+  // tb lies in chunk tb * nchunks / nnz); the unit that completes a chunk tells the host, whose copy
+  // engine then takes the chunk to the host while the rest of the rows run
+  int* chunk_left;       // per chunk: units still to run (reset per launch)
+  int* chunk_flag;       // per chunk, host-mapped: chunk_seq once the chunk is final
+  int nchunks;
+  int chunk_seq;
 };
 
 // Device-built update programs (flow_program.cu): U's pattern and its

@@ -137,6 +137,24 @@ struct Ctx {
   static constexpr bool kSysPublish = OPS == 2;  // readers on other GPUs
 };
 
+// Chunked download (end to end, DRAIN = 2): the unit starting at tb is done
+// (the whole group `sync`s before its first lane counts it); the unit that
+// completes its chunk tells the host, which then copies the chunk with the
+// copy engine while the rest of the rows run. The fence orders the group's
+// value stores before the count, the system fence the chunk before the flag.
+__device__ __forceinline__ void chunk_count(const FlowParams& P, int tb) {
+  const int k = static_cast<int>(static_cast<long long>(tb) * P.nchunks / P.nnz);
+  __threadfence();
+  if (atomicSub(P.chunk_left + k, 1) == 1) {
+    __threadfence_system();
+    *reinterpret_cast<volatile int*>(P.chunk_flag + k) = P.chunk_seq;
+  }
+}
+__device__ __forceinline__ void chunk_notify(const FlowParams& P, int tb, int lane) {
+  __syncwarp();
+  if (lane == 0) chunk_count(P, tb);
+}
+
 // Drain (end to end): the warps of the CTAs past P.row_ctas copy U to the
 // host while the rows run. A value is final as soon as it no longer reads
 // kUnset (it is written once), so a warp copies every group of 64 values

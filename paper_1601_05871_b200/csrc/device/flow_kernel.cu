@@ -183,12 +183,12 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
   __shared__ Ring rings[kWarps];
   const int lane = threadIdx.x & 31;
   Ring& R = rings[threadIdx.x >> 5];
-  if (DRAIN && static_cast<int>(blockIdx.x) >= P.row_ctas) {
+  if (DRAIN == 1 && static_cast<int>(blockIdx.x) >= P.row_ctas) {
     drain_values(P, (blockIdx.x - P.row_ctas) * kWarps + (threadIdx.x >> 5),
                  (gridDim.x - P.row_ctas) * kWarps);
     return;
   }
-  const int W = (DRAIN ? P.row_ctas : static_cast<int>(gridDim.x)) * kWarps;
+  const int W = (DRAIN == 1 ? P.row_ctas : static_cast<int>(gridDim.x)) * kWarps;
   const int w0 = blockIdx.x * kWarps + (threadIdx.x >> 5);
   Ctx<REMOTE ? 2 : 0, BO> C{P, gtimer(), P.vals, P.a, 0};
   int ran = 0, executed = 0, anyfail = 0;
@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) 
     }
     if (traced) stamp[3] = gtimer();
     ++ran;
+    if (DRAIN == 2) chunk_notify(P, tb, lane);
   }
   cp_async_wait_all();
   if (lane == 0) {
@@ -379,7 +380,9 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
   X(256, 3, 3, 0, 0, 0, 100) X(256, 3, 3, 0, 0, 0, 200) X(256, 3, 3, 0, 0, 0, 400)                              \
   X(256, 3, 3, 0, 0, 1, 200) X(256, 3, 3, 0, 1, 0, 200) X(256, 3, 3, 0, 1, 1, 200) X(256, 3, 3, 1, 1, 0, 200)     \
   X(256, 4, 3, 0, 0, 0, 200) X(256, 2, 3, 0, 0, 0, 200) X(256, 2, 3, 0, 1, 0, 200)                              \
-  X(256, 3, 3, 0, 0, 1, 400) X(256, 3, 3, 0, 1, 0, 400)
+  X(256, 3, 3, 0, 0, 1, 400) X(256, 3, 3, 0, 1, 0, 400)                                                        \
+  X(256, 3, 3, 0, 0, 2, 400) X(256, 3, 3, 0, 0, 2, 200) X(256, 3, 3, 0, 0, 2, 0) X(256, 2, 3, 0, 0, 2, 0)       \
+  X(256, 2, 5, 0, 0, 2, 0) X(256, 1, 5, 0, 0, 2, 0) X(256, 4, 3, 0, 0, 2, 0)
 
 static const void* pipe_kernel_for(int threads, int kb, int minb, int remote, int extras, int drain, int bo) {
 #define X(T, K, M, R, E, D, B)                                                                              \
@@ -414,6 +417,28 @@ cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb,
   TCG_PIPE_VARIANTS(X)
 #undef X
   return cudaErrorInvalidValue;
+}
+
+// Chunks of the chunked download: chunk k starts at the first unit start at or
+// after k * nnz / nchunks (start[] preset to INT_MAX), and counts its units.
+__global__ void flow_chunk_setup(const int4* rec, int nrows, long long nnz, int nchunks, int* start, int* units) {
+  const int stride = gridDim.x * blockDim.x;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nrows; q += stride) {
+    const int tb = rec[q].x;
+    const int k = static_cast<int>(static_cast<long long>(tb) * nchunks / nnz);
+    atomicMin(start + k, tb);
+    atomicAdd(units + k, 1);
+  }
+}
+
+cudaError_t launch_chunk_setup(const int4* rec, int nrows, long long nnz, int nchunks, int* start, int* units,
+                               int sm_count, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(start, 0x7f, sizeof(int) * nchunks, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(units, 0, sizeof(int) * nchunks, st);
+  if (e != cudaSuccess) return e;
+  const int blocks = max(1, min((nrows + 255) / 256, 8 * sm_count));
+  flow_chunk_setup<<<blocks, 256, 0, st>>>(rec, nrows, nnz, nchunks, start, units);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStream_t st) {

@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(256, MINB) factor_flow_pp(FlowParams P) {
   constexpr int C = Lay::C;
   constexpr int kLenMask = (1 << 30) - 1;
   extern __shared__ __align__(16) unsigned char pp_smem[];
-  if (DRAIN && static_cast<int>(blockIdx.x) >= P.row_ctas) {
+  if (DRAIN == 1 && static_cast<int>(blockIdx.x) >= P.row_ctas) {
     drain_values(P, (blockIdx.x - P.row_ctas) * 8 + (threadIdx.x >> 5), (gridDim.x - P.row_ctas) * 8);
     return;
   }
@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(256, MINB) factor_flow_pp(FlowParams P) {
   double* pivw = reinterpret_cast<double*>(S + Lay::o_word);
   int* flagw = reinterpret_cast<int*>(S + Lay::o_word + 16);
   const int bar = 1 + gi;
-  const int W = (DRAIN ? P.row_ctas : static_cast<int>(gridDim.x)) * G;
+  const int W = (DRAIN == 1 ? P.row_ctas : static_cast<int>(gridDim.x)) * G;
   const int g0 = blockIdx.x * G + gi;
   Ctx<0, BO> Cx{P, gtimer(), P.vals, P.a, 0};
   const int nrows = EXTRAS ? P.nrows * P.nbatch : P.nrows;
@@ -231,6 +231,10 @@ __global__ void __launch_bounds__(256, MINB) factor_flow_pp(FlowParams P) {
         if (y == kUnset) y = kCanonicalNaN;
         st_relaxed_u64(Cx.vals + x, y);
       }
+      if (DRAIN == 2) {
+        group_sync<T>(bar);
+        if (j == 0) chunk_count(P, tb);
+      }
       continue;
     }
     ++executed;
@@ -309,6 +313,10 @@ __global__ void __launch_bounds__(256, MINB) factor_flow_pp(FlowParams P) {
       }
       if (j < Lc) publish(cb + j, w, false);
     }
+    if (DRAIN == 2) {  // chunked download: the unit is done once the whole group has published
+      group_sync<T>(bar);
+      if (j == 0) chunk_count(P, tb);
+    }
   }
   cp_async_wait_all();
   if (j == 0) {
@@ -337,7 +345,8 @@ __global__ void __launch_bounds__(256, MINB) factor_flow_pp(FlowParams P) {
 #define TCG_PP_VARIANTS(X)                                                                                   \
   X(1, 2, 1, 4, 0, 0, 0, 2) X(1, 2, 1, 4, 0, 1, 0, 2) X(1, 2, 1, 4, 1, 0, 0, 2) X(1, 2, 1, 4, 1, 1, 0, 2)       \
   X(2, 2, 2, 3, 0, 0, 0, 1) X(2, 2, 2, 3, 0, 1, 0, 1) X(2, 2, 2, 3, 1, 0, 0, 1) X(2, 2, 2, 3, 1, 1, 0, 1)       \
-  X(2, 1, 4, 4, 0, 0, 0, 1) X(1, 2, 2, 4, 0, 0, 0, 2) X(4, 2, 4, 3, 0, 0, 0, 1) X(4, 4, 4, 2, 0, 0, 0, 1)
+  X(2, 1, 4, 4, 0, 0, 0, 1) X(1, 2, 2, 4, 0, 0, 0, 2) X(4, 2, 4, 3, 0, 0, 0, 1) X(4, 4, 4, 2, 0, 0, 0, 1)       \
+  X(1, 2, 1, 4, 0, 2, 0, 2) X(2, 2, 2, 3, 0, 2, 0, 1)
 
 template <int WPR, int KP, int NB, int D>
 static size_t pp_smem_bytes() {

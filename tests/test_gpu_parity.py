@@ -677,6 +677,68 @@ def test_drained_end_to_end(T, golden, oracle, name, monkeypatch):
         fz.close()
 
 
+@pytest.mark.parametrize("name,kb", [("c2", None), ("c4", None), ("c1", "16"), ("elast6_k1", "1"), ("s27_16_k2", "64")])
+def test_chunked_copies_end_to_end(T, golden, oracle, name, kb, monkeypatch):
+    # TCG_DRAIN=2: U in chunks cut at unit starts; the unit that completes a chunk
+    # flags it and the host's copy engine takes it out beside the rest of the
+    # launch (run_flow, chunk_count). Bitwise the golden factor, call after call.
+    import torch
+    monkeypatch.setenv("TCG_DRAIN", "2")
+    if kb:
+        monkeypatch.setenv("TCG_D2H_CHUNK_KB", kb)  # small matrices: small chunks
+    _, an = analyzed(name)
+    plan = planned(name)
+    fz = T.GpuFactorizer(plan, T.GpuOptions(timeout_s=30))
+    try:
+        a_in = torch.from_numpy(an.a_permuted.values.copy()).pin_memory()
+        u_in = torch.from_numpy(plan.flow_tables()["values"]).pin_memory()
+        for _ in range(3):
+            out = torch.full((fz.nnz,), float("nan"), dtype=torch.float64).pin_memory()
+            st = fz.factor_host_a_ptr(a_in.data_ptr(), out.data_ptr())
+            assert st.drain_ctas <= -4  # (minus the number of chunks)
+            check_against_oracle(name, out.numpy().copy(), golden, oracle)
+        out.fill_(float("nan"))
+        assert fz.factor_host_ptr(u_in.data_ptr(), out.data_ptr()).drain_ctas <= -4
+        check_against_oracle(name, out.numpy().copy(), golden, oracle)
+        # pageable output: a copy after the launch
+        assert fz.factor_host_a(an.a_permuted.values) is not None and fz.last.drain_ctas == 0
+    finally:
+        fz.close()
+
+
+def test_chunked_copies_breakdown_and_calibration(T, golden, oracle, monkeypatch):
+    import torch
+    _, an = analyzed("c2")
+    fz = T.GpuFactorizer(planned("c2"), T.GpuOptions(timeout_s=30))
+    try:
+        a_in = torch.from_numpy(an.a_permuted.values.copy()).pin_memory()
+        out = torch.zeros(fz.nnz, dtype=torch.float64).pin_memory()
+        # without TCG_DRAIN the three ways out take turns for nine calls, then the fastest stays
+        monkeypatch.delenv("TCG_DRAIN", raising=False)
+        seen = []
+        for _ in range(12):
+            seen.append(fz.factor_host_a_ptr(a_in.data_ptr(), out.data_ptr()).drain_ctas)
+            check_against_oracle("c2", out.numpy().copy(), golden, oracle)
+        assert all(x == 0 for x in seen[0:9:3]) and all(x > 0 for x in seen[1:9:3]) and all(x < 0 for x in seen[2:9:3])
+        assert len(set(seen[9:])) == 1
+        # an indefinite matrix: the rows after the failing pivot keep their inputs and still
+        # count towards their chunks, so every chunk leaves; BreakdownError as usual
+        monkeypatch.setenv("TCG_DRAIN", "2")
+        bad = an.a_permuted.values.copy()
+        r = an.a_permuted.nrows // 2
+        b0, b1 = int(an.a_permuted.row_ptr[r]), int(an.a_permuted.row_ptr[r + 1])
+        bad[b0 + int(np.flatnonzero(an.a_permuted.col_idx[b0:b1] == r)[0])] = -1.0
+        a_bad = torch.from_numpy(bad).pin_memory()
+        with pytest.raises(T.BreakdownError) as e:
+            fz.factor_host_a_ptr(a_bad.data_ptr(), out.data_ptr())
+        assert e.value.row == r and fz.last.drain_ctas < 0
+        # and the context is good for the next call
+        fz.factor_host_a_ptr(a_in.data_ptr(), out.data_ptr())
+        check_against_oracle("c2", out.numpy().copy(), golden, oracle)
+    finally:
+        fz.close()
+
+
 def test_drained_end_to_end_breakdown(T, monkeypatch):
     # an indefinite matrix: the rows after the failing pivot are skipped and
     # keep their inputs, so the drain still finishes; BreakdownError as usual
