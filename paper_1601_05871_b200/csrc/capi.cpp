@@ -671,6 +671,7 @@ static tcg_status build_programs(tcg_ctx* c, const tcg_problem* p) {
     TCG_CUDA_TRY(c, cudaMemcpyAsync(ip(o_urow), p->u_row, sizeof(int) * U, cudaMemcpyHostToDevice, c->stream));
     wall("units H2D");
     S.n = static_cast<int>(n);
+    S.nnz = nnz;
     S.row_ptr = row_ptr;
     S.cols = c->cols;
     S.col_ptr = col_ptr;

@@ -265,6 +265,13 @@ cudaError_t flow_schedule(SchedParams S, const int* u_row, int4* rec, int* item,
   if (e == cudaSuccess) e = cudaMemsetAsync(up.fsize, 0, sizeof(int) * (S.n + 1), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(down.fsize, 0, sizeof(int) * (S.n + 1), st);
   if (e != cudaSuccess) return e;
+  // Long rows (C3: 69 entries) make narrow frontiers of heavy rows: a round is
+  // the rows' chains of dependent index loads plus the grid barrier, and one
+  // CTA per SM has warps enough while its barrier is the cheapest (B200, C3:
+  // 25.6 -> 19.5 ms). Short rows make wide frontiers that want every warp
+  // (C6: 7.5 ms at full occupancy, 23.3 at one CTA per SM).
+  if (S.nnz >= 48LL * S.n) occ = 1;
+  if (const char* ev = std::getenv("TCG_SCHED_CTAS")) occ = max(1, min(occ, std::atoi(ev)));
   void* args[] = {&S, &up, &down};
   e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(&flow_frontiers), max(1, occ) * sm_count, 256, args,
                                   0, st);
