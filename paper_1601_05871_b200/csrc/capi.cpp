@@ -1224,10 +1224,31 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // promise -- under a profiler it serialised and the launch stalled.)
   if (host_in) TCG_CUDA_TRY(c, cudaMemcpyAsync(vals, host_in, vbytes, cudaMemcpyHostToDevice, c->stream));
   if (host_a) {  // PᵀAP's values in, init_factor_values on the device (factorize.hpp:71-89)
-    if (c->nnz_a > 0)
+    // A pinned, mapped input with long rows is gathered in place:
+    // init_factor_values reads only the entries U starts from (A's upper
+    // triangle, the tail of every row: half of a symmetric A), so the device
+    // pulls those over PCIe instead of the copy engine moving all of A. With
+    // short rows the halves share their 32-byte sectors and nothing is saved.
+    // B200, end to end: C4 (81 entries per row) 3.97 -> 3.31 ms, C3 (27) 3.29 ->
+    // 3.26; C2 / C6 (7) 0.96 -> 0.98 / 5.34 -> 5.70, hence the threshold.
+    const double* a_src = c->a_stage;
+    bool zero_copy = false;
+    if (c->nnz_a > 0) {
+      int want = c->nnz_a >= 16 * c->n ? 1 : 0;
+      if (const char* e = std::getenv("TCG_A_ZEROCOPY")) want = std::atoi(e);
+      cudaPointerAttributes attr{};
+      if (want && cudaPointerGetAttributes(&attr, host_a) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+          attr.devicePointer) {
+        a_src = static_cast<const double*>(attr.devicePointer);
+        zero_copy = true;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    if (c->nnz_a > 0 && !zero_copy)
       TCG_CUDA_TRY(c, cudaMemcpyAsync(c->a_stage, host_a, sizeof(double) * c->nnz_a * c->nbatch,
                                       cudaMemcpyHostToDevice, c->stream));
-    TCG_CUDA_TRY(c, tcbdev::launch_init_values(c->a_stage, c->a_map, vals, batch ? c->bvals0 : c->vals0, c->nnz,
+    TCG_CUDA_TRY(c, tcbdev::launch_init_values(a_src, c->a_map, vals, batch ? c->bvals0 : c->vals0, c->nnz,
                                                c->nnz_a, c->nbatch, c->sm_count, c->stream));
   }
   if (phase == 0) TCG_CUDA_TRY(c, tcbdev::launch_flow_prepare(q, c->sm_count, c->stream));

@@ -706,6 +706,31 @@ def test_chunked_copies_end_to_end(T, golden, oracle, name, kb, monkeypatch):
         fz.close()
 
 
+@pytest.mark.parametrize("name", ["c1", "elast6_k1", "c4"])
+def test_pinned_input_gathered_in_place(T, golden, oracle, name, monkeypatch):
+    # tcg_factor_host_a with a pinned input: the device init gathers the entries U
+    # starts from straight out of host memory (TCG_A_ZEROCOPY=1; the default for
+    # long rows) instead of copying all of A first (0); the same factor bit for bit
+    import torch
+    _, an = analyzed(name)
+    fz = T.GpuFactorizer(planned(name), T.GpuOptions(timeout_s=30))
+    try:
+        a_in = torch.from_numpy(an.a_permuted.values.copy()).pin_memory()
+        for z in ("1", "0", None):
+            if z is None:
+                monkeypatch.delenv("TCG_A_ZEROCOPY")
+            else:
+                monkeypatch.setenv("TCG_A_ZEROCOPY", z)
+            out = torch.full((fz.nnz,), float("nan"), dtype=torch.float64).pin_memory()
+            fz.factor_host_a_ptr(a_in.data_ptr(), out.data_ptr())
+            check_against_oracle(name, out.numpy().copy(), golden, oracle)
+        # a pageable input is copied (no device address to gather from)
+        monkeypatch.setenv("TCG_A_ZEROCOPY", "1")
+        check_against_oracle(name, fz.factor_host_a(an.a_permuted.values), golden, oracle)
+    finally:
+        fz.close()
+
+
 def test_chunked_copies_breakdown_and_calibration(T, golden, oracle, monkeypatch):
     import torch
     _, an = analyzed("c2")
