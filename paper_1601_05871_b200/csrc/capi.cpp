@@ -1099,11 +1099,20 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   int occ = 0;
   // poll back-off for long programs (flow_kernel.cu Ctx): thousands of lanes
   // poll the lines the critical rows write; sleeping between polls frees them
-  // B200, fixed back-off sweep (0-800 ns; the sleep only follows a poll that
-  // still saw kUnset): C3 (24.8 products per coordinate) 4.01 / 2.91 / 2.76 /
-  // 2.66 / 4.01 ms at 0 / 100 / 200 / 400 / 800; s27 (23.4) 1.26 / 0.93 /
-  // 0.89 / 0.88 / 1.25; C4 (12.4) 1.49 / 1.38 / 1.37 / 1.38 / 1.49
-  int backoff = kb >= 3 ? (mean >= 16.0 ? 400 : 200) : 0;
+  // (the sleep only follows a poll that still saw kUnset). B200, fixed
+  // back-off sweep with a compiled variant for every value -- __nanosleep
+  // rounds its argument into coarse steps, so 300-500 ns and 520-1600 ns each
+  // measure as one value: C3 (24.8 products per coordinate) 4.01 / 2.91 / 2.76
+  // / 2.66 / 2.60 / 3.23 ms at 0 / 100 / 200 / 300-500 / 520-1600 / 2400; C4
+  // (12.4) 1.49 / 1.31 / 1.30 / 1.31 / 1.32 / 1.45 at 0 / 100 / 150-250 / 400 /
+  // 600-1000 / 1600. (Two shorter sleeps in a row are worse than one: C3 2.74
+  // at 200 + 200, 2.82 at 400 + 600.)
+  // The longer step pays only where many rows wait at once (C3: 73 units per
+  // warp); with a few units per warp the chain itself binds and the shorter
+  // sleep wins (s27, 2.4 units per warp: 0.88 ms at 400, 0.90 at 600; elast6
+  // 0.35 / 0.43).
+  const bool crowded = c->nflow >= 32LL * 32 * c->sm_count;
+  int backoff = kb >= 3 ? (mean >= 16.0 ? (crowded ? 600 : 400) : 200) : 0;
   if (const char* e = std::getenv("TCG_FLOW_BACKOFF")) backoff = std::atoi(e);
   int pp_w = 0, pp_k = 0, pp_n = 0, pp_m = 0, pp_d = 0, pp_b = -1;
   bool pp = !remote && !c->opt.trace && phase == 0 && pick_pp(c, mean, &pp_w, &pp_k, &pp_n, &pp_m, &pp_d, &pp_b);

@@ -74,8 +74,8 @@ __device__ __forceinline__ unsigned long long wait_value_sys(const double* p, Ct
 // BO: poll back-off in ns (a lane sleeps between re-polls of a value not yet
 // written). Long programs keep thousands of lanes polling the few lines the
 // critical rows are about to write; sleeping between polls frees the L2
-// slices serving them (B200, C3: 4.01 ms without, 2.66 ms at 400 ns; C4
-// 1.49 -> 1.37 at 200 ns; short programs lose: C2 0.41 -> 0.42-0.45 ms).
+// slices serving them (B200, C3: 4.01 ms without, 2.66 ms at 400 ns, 2.60 at
+// 600 ns; C4 1.49 -> 1.30 at 200 ns; short programs lose: C2 0.41 -> 0.42-0.45 ms).
 template <int OPS = 0, int BO = 0>
 struct Ctx {
   const FlowParams& P;

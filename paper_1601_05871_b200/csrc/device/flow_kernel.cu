@@ -377,11 +377,13 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
   X(256, 4, 3, 1, 1, 0, 0) X(256, 2, 3, 0, 0, 1, 0) X(256, 3, 3, 0, 0, 1, 0) X(256, 4, 3, 0, 0, 1, 0)             \
   X(256, 2, 3, 0, 1, 1, 0) X(256, 3, 3, 0, 1, 1, 0) X(256, 4, 3, 0, 1, 1, 0)                                     \
   X(256, 2, 5, 0, 0, 0, 0) X(256, 2, 5, 0, 0, 1, 0) X(256, 1, 5, 0, 0, 0, 0) X(256, 1, 5, 0, 0, 1, 0)             \
-  X(256, 3, 3, 0, 0, 0, 100) X(256, 3, 3, 0, 0, 0, 200) X(256, 3, 3, 0, 0, 0, 400)                              \
+  X(256, 3, 3, 0, 0, 0, 100) X(256, 3, 3, 0, 0, 0, 200) X(256, 3, 3, 0, 0, 0, 400) X(256, 3, 3, 0, 0, 0, 600)   \
+  X(256, 3, 3, 0, 0, 0, 1000) X(256, 3, 3, 0, 0, 0, 2400)                                                       \
   X(256, 3, 3, 0, 0, 1, 200) X(256, 3, 3, 0, 1, 0, 200) X(256, 3, 3, 0, 1, 1, 200) X(256, 3, 3, 1, 1, 0, 200)     \
   X(256, 4, 3, 0, 0, 0, 200) X(256, 2, 3, 0, 0, 0, 200) X(256, 2, 3, 0, 1, 0, 200)                              \
-  X(256, 3, 3, 0, 0, 1, 400) X(256, 3, 3, 0, 1, 0, 400)                                                        \
-  X(256, 3, 3, 0, 0, 2, 400) X(256, 3, 3, 0, 0, 2, 200) X(256, 3, 3, 0, 0, 2, 0) X(256, 2, 3, 0, 0, 2, 0)       \
+  X(256, 3, 3, 0, 0, 1, 600) X(256, 3, 3, 0, 1, 0, 600) X(256, 3, 3, 0, 0, 1, 400) X(256, 3, 3, 0, 1, 0, 400)    \
+  X(256, 3, 3, 0, 0, 2, 400)                                                                                    \
+  X(256, 3, 3, 0, 0, 2, 600) X(256, 3, 3, 0, 0, 2, 200) X(256, 3, 3, 0, 0, 2, 0) X(256, 2, 3, 0, 0, 2, 0)       \
   X(256, 2, 5, 0, 0, 2, 0) X(256, 1, 5, 0, 0, 2, 0) X(256, 4, 3, 0, 0, 2, 0)
 
 static const void* pipe_kernel_for(int threads, int kb, int minb, int remote, int extras, int drain, int bo) {
