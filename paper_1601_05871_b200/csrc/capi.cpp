@@ -1140,6 +1140,14 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
       dmode = 0;
       oe = tcbdev::pipe_occupancy(threads, kb, minb, remote, extras, &occ, 0, backoff);
     }
+    // a back-off asked for by name must exist: a silent fall-back to none once made
+    // every value above 400 ns of a sweep measure as 0
+    if (std::getenv("TCG_FLOW_BACKOFF") && backoff > 0 && oe == cudaSuccess &&
+        !tcbdev::pipe_variant_exists(threads, kb, minb, remote, extras, dmode, backoff)) {
+      c->err = "no value-flow kernel variant with a " + std::to_string(backoff) +
+               " ns back-off for this launch (TCG_FLOW_BACKOFF; see TCG_PIPE_VARIANTS)";
+      return TCG_INVALID;
+    }
     if (oe == cudaErrorInvalidValue) {
       cudaGetLastError();
       c->err = "no value-flow kernel variant for KB " + std::to_string(kb) + ", " + std::to_string(minb) +

@@ -21,6 +21,9 @@ cudaError_t launch_flow_prepare(const FlowPrepParams& q, int sm_count, cudaStrea
 cudaError_t launch_chunk_setup(const int4* rec, int nrows, long long nnz, int nchunks, int* start, int* units,
                                int sm_count, cudaStream_t st);
 
+// whether that exact variant is compiled in (pipe_occupancy / launch_flow_pipe fall back to the
+// variant without a back-off when the requested back-off has none)
+bool pipe_variant_exists(int threads, int kb, int minb, int remote, int extras, int drain, int backoff_ns);
 cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm,
                            int drain = 0, int backoff_ns = 0);
 cudaError_t launch_flow_pipe(const FlowParams& p, int grid, int threads, int kb, int minb, int remote,

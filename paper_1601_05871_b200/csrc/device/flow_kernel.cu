@@ -400,6 +400,10 @@ static int pipe_backoff(int threads, int kb, int minb, int remote, int extras, i
   return pipe_kernel_for(threads, kb, minb, remote, extras, drain, bo) ? bo : 0;
 }
 
+bool pipe_variant_exists(int threads, int kb, int minb, int remote, int extras, int drain, int bo) {
+  return pipe_kernel_for(threads, kb, minb, remote, extras, drain, bo) != nullptr;
+}
+
 cudaError_t pipe_occupancy(int threads, int kb, int minb, int remote, int extras, int* ctas_per_sm, int drain,
                            int bo) {
   bo = pipe_backoff(threads, kb, minb, remote, extras, drain, bo);
