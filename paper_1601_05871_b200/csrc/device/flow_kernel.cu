@@ -81,6 +81,85 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
   return v;
 }
 
+// flow_slot for the first pass of a unit, called by the whole warp (`on`: the
+// lane has a coordinate). Every batch but the last runs as in flow_slot, each
+// lane on its own. The last batch's operands are loaded as each lane gets
+// there, and what is still unwritten then is re-polled by the lanes of the
+// unit together, on one clock. The lanes of a critical row mostly wait for the
+// same source row, whose values arrive together: polling each on its own
+// clock, they saw them up to a sleep plus a round trip apart (C3 trace: 1.7
+// us), and the pivot waits for the last; together the unit is done one poll
+// after the values are. The warp sleeps only after a round in which no lane
+// got further. B200: C3 2.60 -> 2.38 ms, C4 1.30 -> 1.25, bitwise.
+template <int KB, class Cx>
+__device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const int4 sr, bool on, unsigned gmask) {
+  constexpr int BO = Cx::kBackoff;
+  const int ub = sr.x, ue = on ? sr.y : sr.x;
+  int u = ub;
+  int2 p[KB];
+  if (ub < ue) {
+    if (KB >= 3)
+      for (int q = ub + 1 + 2 * KB; q < ue; q += 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.P.upd + q));
+    const unsigned long long xa0 = C.ld(sr.z), xb0 = C.ld(sr.w);
+    u = ub + 1;
+#pragma unroll
+    for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
+    v = __dsub_rn(v, C.product(sr.z, xa0, sr.w, xb0));
+    while (ue - u > KB) {  // (a full batch, and more after it)
+      unsigned long long xa[KB], xb[KB];
+      int2 c[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        c[j] = p[j];
+        xa[j] = C.ld(c[j].x);
+        xb[j] = C.ld(c[j].y);
+      }
+      u += KB;
+#pragma unroll
+      for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
+#pragma unroll
+      for (int j = 0; j < KB; ++j) v = __dsub_rn(v, C.product(c[j].x, xa[j], c[j].y, xb[j]));
+    }
+  }
+  // the last batch
+  const int n = ue - u;  // 0..KB
+  unsigned long long xa[KB], xb[KB];
+#pragma unroll
+  for (int j = 0; j < KB; ++j) {
+    xa[j] = (j < n) ? C.ld(p[j].x) : 0ull;
+    xb[j] = (j < n) ? C.ld(p[j].y) : 0ull;
+  }
+  int j = 0;
+  unsigned spins = 0;
+  for (;;) {
+    bool progressed = false;
+#pragma unroll
+    for (int jj = 0; jj < KB; ++jj)
+      if (jj == j && jj < n && xa[jj] != kUnset && xb[jj] != kUnset) {
+        v = __dsub_rn(v, __dmul_rn(__longlong_as_double(static_cast<long long>(xa[jj])),
+                                   __longlong_as_double(static_cast<long long>(xb[jj]))));
+        ++j;
+        progressed = true;
+      }
+    if (__all_sync(gmask, j >= n)) break;
+    if (BO > 0 && !__any_sync(gmask, progressed)) __nanosleep(BO);
+#pragma unroll
+    for (int jj = 0; jj < KB; ++jj)
+      if (jj == j && jj < n) {
+        if (xa[jj] == kUnset) xa[jj] = C.ld_strong(p[jj].x);
+        if (xb[jj] == kUnset) xb[jj] = C.ld_strong(p[jj].y);
+      }
+    if (++spins == 1024u) {
+      spins = 0;
+      if (ld_relaxed(&C.P.ctrl->error.v) || gtimer() - C.t0 > C.P.timeout_ns) {
+        atomicCAS(&C.P.ctrl->error.v, 0, 1);  // abandoned: the host reports TCG_TIMEOUT
+        j = n;
+      }
+    }
+  }
+  return v;
+}
+
 // One finalising row on a group of G lanes: group lane j owns coordinates
 // tb+j, tb+j+G, ... Chol: pivot test (latch), sqrt, scale
 // (kernels.hpp:49-53); Trsm: divide by U(t,t) (kernels.hpp:76-78). `a0`/`sr0`:
@@ -95,7 +174,9 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
   unsigned long long xd = 0;
   if (KIND == kTrsm) xd = C.ld(dpos);
   double v = 0.0;
-  if (gl < L) v = flow_slot<KB>(C, input_settle(P, C.a + tb + gl, a0, C.t0), sr0);
+  if (G == 32 && !Cx::kSysPublish)  // (sharded parts settle remote operands lane by lane)
+    v = flow_slot_conv<KB>(C, gl < L ? a0 : 0.0, sr0, gl < L, gmask);
+  else if (gl < L) v = flow_slot<KB>(C, input_settle(P, C.a + tb + gl, a0, C.t0), sr0);
   if (stamp && gl == 0) stamp[1] = gtimer();  // trace: the group's first coordinate is done
   double d;
   if (KIND == kChol) {
@@ -171,7 +252,8 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
 // EXTRAS = 0: a single matrix without trace stamps (no batch member
 // arithmetic, no stamp branches); 1: batches and traces.
 template <int THREADS, int KB, int MINB, int REMOTE, int EXTRAS, int DRAIN = 0, int BO = 0>
-__global__ void __launch_bounds__(THREADS, MINB) factor_flow_pipe(FlowParams P) {
+__global__ void __launch_bounds__(THREADS, (MINB == 3 && THREADS == 256 && KB <= 3 && !EXTRAS) ? 4 : MINB)
+    factor_flow_pipe(FlowParams P) {
   constexpr int kWarps = THREADS / 32;
   constexpr int kLenMask = (1 << 30) - 1;
   struct Ring {
@@ -370,7 +452,8 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
   return cudaGetLastError();
 }
 
-// (threads, KB, CTAs/SM, remote operands, extras, drain, poll back-off ns)
+// (threads, KB, CTAs/SM, remote operands, extras, drain, poll back-off ns); the single-matrix
+// variants named with 3 CTAs/SM and KB <= 3 are compiled for 4 (64 registers, no spills)
 #define TCG_PIPE_VARIANTS(X)                                                                                  \
   X(256, 2, 3, 0, 0, 0, 0) X(256, 3, 3, 0, 0, 0, 0) X(256, 4, 3, 0, 0, 0, 0) X(256, 2, 3, 0, 1, 0, 0)             \
   X(256, 3, 3, 0, 1, 0, 0) X(256, 4, 3, 0, 1, 0, 0) X(256, 2, 3, 1, 1, 0, 0) X(256, 3, 3, 1, 1, 0, 0)             \
