@@ -994,6 +994,13 @@ static bool pick_pp(const tcg_ctx* c, double mean, int* w, int* k, int* n, int* 
   }
   if (mean > 4.0) return false;
   const long long positions = c->nflow * c->nbatch;
+  // Between the small matrices (a few units per warp: the group's parallel products win) and the
+  // large ones (hundreds of units per warp: throughput) the chain binds, and the per-lane kernel
+  // with its warp-wide settle of the last batch is the faster one. B200, 7-point Laplacians IC(1),
+  // per-lane / product-parallel ms: 40^3 (64 K units) 0.173 / 0.187, 56^3 (176 K) 0.270 / 0.311,
+  // 64^3 (C2, 262 K) 0.343 / 0.361, 80^3 (512 K) 0.539 / 0.529, 96^3 (885 K) 0.813 / 0.751,
+  // 128^3 (C6) 1.67 / 1.43; C5 (33 K) 0.146 / 0.136, C1 (13 K) 0.052 / 0.043.
+  if (c->nbatch == 1 && positions > 48000 && positions <= 400000) return false;
   if (positions <= 200000) {
     *w = 2, *k = 2, *n = 2, *m = 3, *d = 1;
   } else {

@@ -67,9 +67,10 @@ def test_device_schedule_equals_the_host_schedule(T, name):
 
 
 def test_default_row_kernel_follows_program_length(T):
-    # product-parallel rows where programs are short (C1, C2, C5), one lane
-    # per coordinate where they are long (C3: 24.8 products per coordinate)
-    for name, want in (("c1", 2), ("c5_m0", 2), ("c2", 2), ("s27_16_k2", 1)):
+    # product-parallel rows where programs are short and the matrix small (C1, C5;
+    # large ones too: C6), one lane per coordinate where programs are long (s27,
+    # C3: 24.8 products per coordinate) and on mid-size matrices (C2: 262 K units)
+    for name, want in (("c1", 2), ("c5_m0", 2), ("c2", 1), ("s27_16_k2", 1)):
         _, st = gpu_factor(T, planned(name), mode=5)
         assert st.row_kernel == want, name
 
