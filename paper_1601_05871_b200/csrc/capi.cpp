@@ -1113,13 +1113,14 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
   // / 2.66 / 2.60 / 3.23 ms at 0 / 100 / 200 / 300-500 / 520-1600 / 2400; C4
   // (12.4) 1.49 / 1.31 / 1.30 / 1.31 / 1.32 / 1.45 at 0 / 100 / 150-250 / 400 /
   // 600-1000 / 1600. (Two shorter sleeps in a row are worse than one: C3 2.74
-  // at 200 + 200, 2.82 at 400 + 600.)
+  // at 200 + 200, 2.82 at 400 + 600.) With the last batch settled warp-wide
+  // (flow_slot_conv) C4 takes 1.23 ms at 100 and 1.25 at 200.
   // The longer step pays only where many rows wait at once (C3: 73 units per
   // warp); with a few units per warp the chain itself binds and the shorter
   // sleep wins (s27, 2.4 units per warp: 0.88 ms at 400, 0.90 at 600; elast6
   // 0.35 / 0.43).
   const bool crowded = c->nflow >= 32LL * 32 * c->sm_count;
-  int backoff = kb >= 3 ? (mean >= 16.0 ? (crowded ? 600 : 400) : 200) : 0;
+  int backoff = kb >= 3 ? (mean >= 16.0 ? (crowded ? 600 : 400) : 100) : 0;
   if (const char* e = std::getenv("TCG_FLOW_BACKOFF")) backoff = std::atoi(e);
   int pp_w = 0, pp_k = 0, pp_n = 0, pp_m = 0, pp_d = 0, pp_b = -1;
   bool pp = !remote && !c->opt.trace && phase == 0 && pick_pp(c, mean, &pp_w, &pp_k, &pp_n, &pp_m, &pp_d, &pp_b);
@@ -1282,11 +1283,11 @@ static tcg_status run_flow(tcg_ctx* c, tcg_stats& S, int threads, const double* 
                                     c->stream));
   P.ub = c->flow_ub;
   // the per-lane kernel's Chol pivot through shared memory, the waiting lanes
-  // sleeping P.decouple ns between looks (flow_row): B200, C4 (12.4 products
-  // per coordinate) 1.38 -> 1.30 ms at 100 ns; with long diagonal programs
-  // the waiting lanes slow the diagonal's own (C3 2.65 -> 2.78-2.88, s27
-  // 0.87 -> 0.92), so only below 16 products per coordinate
-  P.decouple = mean < 16.0 ? 100 : 0;
+  // sleeping P.decouple ns between looks (flow_row; TCG_FLOW_DECOUPLE): it let
+  // the lanes of a medium-program unit publish independently (C4 1.38 -> 1.30
+  // ms at 100 ns) until the last batch was settled warp-wide, which brings the
+  // lanes in together anyway (C4 now 1.23 ms without, 1.24 with): off.
+  P.decouple = 0;
   if (const char* e = std::getenv("TCG_FLOW_DECOUPLE")) P.decouple = std::atoi(e);
   if (c->nflow > 0) {
     if (pp)

@@ -96,6 +96,15 @@ struct Ctx {
     if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
     return ld_relaxed_u64(vals + pos);
   }
+  // An operand of an early product: final long ago as a rule, and a final value
+  // is final in any cache (written once), so the SM's L1 may serve it -- the
+  // lanes of a row read the same multiplier and neighbouring operands. A copy
+  // cached before the value was written reads kUnset and is re-read from L2
+  // (product()'s strong re-poll).
+  __device__ __forceinline__ unsigned long long ld_early(int pos) const {
+    if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
+    return ld_cached_u64(vals + pos);
+  }
   __device__ __forceinline__ unsigned long long ld_strong(int pos) const {
     if (OPS == 2 && pos < 0) return ld_relaxed_sys_u64(remote(pos));
     return ld_relaxed_u64(vals + pos);

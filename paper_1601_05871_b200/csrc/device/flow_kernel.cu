@@ -94,13 +94,14 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 template <int KB, class Cx>
 __device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const int4 sr, bool on, unsigned gmask) {
   constexpr int BO = Cx::kBackoff;
+  auto LD = [&](int pos) { return C.ld_early(pos); };
   const int ub = sr.x, ue = on ? sr.y : sr.x;
   int u = ub;
   int2 p[KB];
   if (ub < ue) {
     if (KB >= 3)
       for (int q = ub + 1 + 2 * KB; q < ue; q += 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(C.P.upd + q));
-    const unsigned long long xa0 = C.ld(sr.z), xb0 = C.ld(sr.w);
+    const unsigned long long xa0 = LD(sr.z), xb0 = LD(sr.w);
     u = ub + 1;
 #pragma unroll
     for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
@@ -111,8 +112,8 @@ __device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const in
 #pragma unroll
       for (int j = 0; j < KB; ++j) {
         c[j] = p[j];
-        xa[j] = C.ld(c[j].x);
-        xb[j] = C.ld(c[j].y);
+        xa[j] = LD(c[j].x);
+        xb[j] = LD(c[j].y);
       }
       u += KB;
 #pragma unroll
@@ -463,6 +464,8 @@ cudaError_t launch_init_values(const double* a, const int* map, double* vals, do
   X(256, 3, 3, 0, 0, 0, 100) X(256, 3, 3, 0, 0, 0, 200) X(256, 3, 3, 0, 0, 0, 400) X(256, 3, 3, 0, 0, 0, 600)   \
   X(256, 3, 3, 0, 0, 0, 1000) X(256, 3, 3, 0, 0, 0, 2400)                                                       \
   X(256, 3, 3, 0, 0, 1, 200) X(256, 3, 3, 0, 1, 0, 200) X(256, 3, 3, 0, 1, 1, 200) X(256, 3, 3, 1, 1, 0, 200)     \
+  X(256, 3, 3, 0, 0, 1, 100) X(256, 3, 3, 0, 1, 0, 100) X(256, 3, 3, 0, 1, 1, 100) X(256, 3, 3, 1, 1, 0, 100)     \
+  X(256, 3, 3, 0, 0, 2, 100)                                                                                    \
   X(256, 4, 3, 0, 0, 0, 200) X(256, 2, 3, 0, 0, 0, 200) X(256, 2, 3, 0, 1, 0, 200)                              \
   X(256, 3, 3, 0, 0, 1, 600) X(256, 3, 3, 0, 1, 0, 600) X(256, 3, 3, 0, 0, 1, 400) X(256, 3, 3, 0, 1, 0, 400)    \
   X(256, 3, 3, 0, 0, 2, 400)                                                                                    \

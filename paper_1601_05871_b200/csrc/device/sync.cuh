@@ -82,6 +82,12 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const void* p) {
   asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p));
   return v;
 }
+// a weak load that may be served by the SM's L1 (a stale copy is possible: callers validate)
+__device__ __forceinline__ unsigned long long ld_cached_u64(const void* p) {
+  unsigned long long v;
+  asm volatile("ld.global.ca.b64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
 // two adjacent 64-bit values, each element single-copy atomic (16-byte aligned)
 __device__ __forceinline__ void ld_relaxed_v2_u64(const void* p, unsigned long long& a, unsigned long long& b) {
   asm volatile("ld.relaxed.gpu.global.v2.b64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p));

@@ -89,7 +89,7 @@ def test_product_parallel_variants(T, golden, oracle, name, spec, monkeypatch):
     check_against_oracle(name, vals, golden, oracle)
 
 
-@pytest.mark.parametrize("name,decouple", [("c3", "100"), ("s27_16_k2", "20"), ("c4", "0"), ("elast6_k1", "400")])
+@pytest.mark.parametrize("name,decouple", [("c3", "100"), ("s27_16_k2", "20"), ("c4", "100"), ("elast6_k1", "400")])
 def test_pivot_through_shared_memory(T, golden, oracle, name, decouple, monkeypatch):
     # per-lane kernel: the Chol pivot handed to the other lanes through shared
     # memory (each lane publishes as soon as its program and the pivot are
