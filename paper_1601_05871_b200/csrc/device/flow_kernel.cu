@@ -90,7 +90,10 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 // clock, they saw them up to a sleep plus a round trip apart (C3 trace: 1.7
 // us), and the pivot waits for the last; together the unit is done one poll
 // after the values are. The warp sleeps only after a round in which no lane
-// got further. B200: C3 2.60 -> 2.38 ms, C4 1.30 -> 1.25, bitwise.
+// got further, and a round re-polls every operand of the batch that is still
+// unwritten (the polls of a warp coalesce now; lane by lane the same re-reads
+// made things slower). B200: C3 2.60 -> 2.38 ms, C4 1.30 -> 1.25, then C3
+// 2.34 -> 2.19, s27 0.80 -> 0.72 with the whole batch re-polled; bitwise.
 template <int KB, class Cx>
 __device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const int4 sr, bool on, unsigned gmask) {
   constexpr int BO = Cx::kBackoff;
@@ -146,7 +149,7 @@ __device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const in
     if (BO > 0 && !__any_sync(gmask, progressed)) __nanosleep(BO);
 #pragma unroll
     for (int jj = 0; jj < KB; ++jj)
-      if (jj == j && jj < n) {
+      if (jj >= j && jj < n) {  // every operand of the batch still unwritten, not only the next product's
         if (xa[jj] == kUnset) xa[jj] = C.ld_strong(p[jj].x);
         if (xb[jj] == kUnset) xb[jj] = C.ld_strong(p[jj].y);
       }
