@@ -672,6 +672,7 @@ static tcg_status build_programs(tcg_ctx* c, const tcg_problem* p) {
     wall("units H2D");
     S.n = static_cast<int>(n);
     S.nnz = nnz;
+    S.slack_pct = tcb::flow_slack_pct(n, nnz, U);
     S.row_ptr = row_ptr;
     S.cols = c->cols;
     S.col_ptr = col_ptr;

@@ -129,6 +129,7 @@ struct ProgParams {
 // The value-flow schedule built on the device (flow_schedule.cu).
 struct SchedParams {
   int n;
+  int slack_pct;     // placement between a unit's earliest and latest level, in percent (flow_order_keys)
   long long nnz;     // entries of U (the grid of the frontier kernel is sized by the mean row length)
   int nunits;
   const int* row_ptr;   // n + 1

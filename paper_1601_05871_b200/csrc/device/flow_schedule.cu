@@ -213,10 +213,16 @@ __global__ void flow_frontiers(SchedParams S, Frontier up, Frontier down) {
 }
 
 // ascending level, descending height; the unit ids as values (a stable sort keeps them ascending)
-__global__ void flow_order_keys(int nunits, const int* level, const int* height, unsigned long long* key, int* id) {
+// (slack_pct: a unit is placed slack_pct % of the way from its earliest level to its latest,
+// depth + 1 - height; still a topological key: both ends grow by at least 1 along a dependence)
+__global__ void flow_order_keys(int nunits, const int* level, const int* height, const int* depth, int slack_pct,
+                                unsigned long long* key, int* id) {
   const int stride = gridDim.x * blockDim.x;
+  const int dp = *depth;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < nunits; g += stride) {
-    key[g] = (static_cast<unsigned long long>(level[g]) << 32) | static_cast<unsigned>(0x7fffffff - height[g]);
+    const int slack = dp + 1 - height[g] - level[g];
+    const int place = level[g] + static_cast<int>(static_cast<long long>(slack_pct) * slack / 100);
+    key[g] = (static_cast<unsigned long long>(place) << 32) | static_cast<unsigned>(0x7fffffff - height[g]);
     id[g] = g;
   }
 }
@@ -277,7 +283,7 @@ cudaError_t flow_schedule(SchedParams S, const int* u_row, int4* rec, int* item,
                                   0, st);
   if (e != cudaSuccess) return e;
   const int blocks = max(1, min((S.nunits + 255) / 256, 8 * sm_count));
-  flow_order_keys<<<blocks, 256, 0, st>>>(S.nunits, S.level, S.height, keys, ids);
+  flow_order_keys<<<blocks, 256, 0, st>>>(S.nunits, S.level, S.height, S.depth, S.slack_pct, keys, ids);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   e = cub::DeviceRadixSort::SortPairs(temp, *temp_bytes, keys, keys_sorted, ids, order, S.nunits, 0, 64, st);

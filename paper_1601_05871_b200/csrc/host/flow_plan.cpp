@@ -197,6 +197,13 @@ void count_tasks(const FlowPlan& P, const RangeList& ranges, const std::vector<i
 
 }  // namespace
 
+int flow_slack_pct(std::int64_t n, std::int64_t nnz, std::int64_t units) {
+  if (const char* e = std::getenv("TCG_FLOW_SLACK")) return std::clamp(std::atoi(e), 0, 100);
+  // short rows (so short programs: the product-parallel kernel) and more units
+  // than that kernel's lower size bound (capi.cpp pick_pp)
+  return nnz < 12 * n && units > 400000 ? 100 : 0;
+}
+
 CsrMatrix flow_plan_pattern(const FlowPlan& P) {
   CsrMatrix u;
   u.nrows = u.ncols = P.n;
@@ -539,12 +546,20 @@ void flow_plan_schedule(FlowPlan& P) {
         tmp[cnt[static_cast<std::size_t>(hmax - height[g])]++] = static_cast<std::int32_t>(g);
     }
     {
+      // a unit's place: its level, moved towards its latest level (depth + 1 -
+      // height) by flow_slack_pct percent of its slack (a topological key
+      // still: both ends grow by at least 1 along a dependence)
+      const int pct = flow_slack_pct(n, P.nnz, static_cast<std::int64_t>(U));
+      auto place = [&](std::int32_t g) {
+        const std::int32_t slack = depth + 1 - height[g] - level[g];
+        return level[g] + static_cast<std::int32_t>(static_cast<std::int64_t>(pct) * slack / 100);
+      };
       std::vector<std::int64_t> cnt(static_cast<std::size_t>(depth) + 2, 0);
-      for (std::size_t g = 0; g < U; ++g) ++cnt[static_cast<std::size_t>(level[g])];
+      for (std::size_t g = 0; g < U; ++g) ++cnt[static_cast<std::size_t>(place(static_cast<std::int32_t>(g)))];
       for (std::size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
       for (std::size_t x = 0; x < U; ++x) {
         const std::int32_t g = tmp[x];
-        order[cnt[static_cast<std::size_t>(level[g]) - 1]++] = g;
+        order[cnt[static_cast<std::size_t>(place(g)) - 1]++] = g;
       }
     }
     P.rec.resize(4 * U);

@@ -106,6 +106,16 @@ FlowPlan build_flow_plan(const CsrRef& a_permuted, const CsrRef& pattern, const 
 // height descending, unit id ascending), the records; stats.depth. Idempotent.
 void flow_plan_schedule(FlowPlan& P);
 
+// Where a unit goes between its earliest level and its latest (depth + 1 -
+// height), in percent of its slack; host and device schedules alike. 0: as
+// soon as possible, the placement of the latency-bound runs (any later costs
+// them: C3 2.17 -> 2.80 ms at 100, C2 0.33 -> 0.38). 100: as late as possible,
+// for large matrices with short rows, which run the product-parallel kernel
+// throughput-bound: a value is then produced shortly before its readers run
+// and is still in L2 when they do (B200: C6 1.43 -> 1.15 ms, 7-point 80^3 /
+// 96^3 / 112^3 0.53 / 0.75 / 1.05 -> 0.43 / 0.60 / 0.83). TCG_FLOW_SLACK overrides.
+int flow_slack_pct(std::int64_t n, std::int64_t nnz, std::int64_t units);
+
 // The pattern as an owning CsrMatrix (values 1.0), for the full plan.
 CsrMatrix flow_plan_pattern(const FlowPlan& P);
 

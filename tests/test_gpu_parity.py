@@ -66,6 +66,27 @@ def test_device_schedule_equals_the_host_schedule(T, name):
     assert depth == host.stats().flow_depth > 0
 
 
+@pytest.mark.parametrize("name,slack", [("c1", "100"), ("s27_16_k2", "60"), ("c2", "100")])
+def test_slack_placed_device_schedule(T, golden, oracle, name, slack, monkeypatch):
+    # TCG_FLOW_SLACK: the device and the host place the units alike, and the
+    # factor is the golden one under either row kernel
+    monkeypatch.setenv("TCG_FLOW_SLACK", slack)
+    _, an = analyzed(name)
+    fresh = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    fz = T.GpuFactorizer(fresh, T.GpuOptions(timeout_s=30))
+    try:
+        rec, item, depth = fz.flow_records()
+        for pp in ("0", "1,2,1,4,2"):
+            monkeypatch.setenv("TCG_FLOW_PP", pp)
+            fz.restore()
+            fz.factor()
+            check_against_oracle(name, fz.download(), golden, oracle)
+    finally:
+        fz.close()
+    f = T.Plan(an.a_permuted, an.pattern, an.ranges).schedule().flow_tables()
+    assert np.array_equal(rec, f["flow_rec"]) and np.array_equal(item, f["flow_item"])
+
+
 def test_default_row_kernel_follows_program_length(T):
     # product-parallel rows where programs are short and the matrix small (C1, C5;
     # large ones too: C6), one lane per coordinate where programs are long (s27,

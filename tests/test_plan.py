@@ -326,6 +326,26 @@ def test_chol_cap_schedules_replay_bitwise(T, name, cap, oracle, monkeypatch):
     assert bitwise_equal(emulate_flow(rec, f["values"], slot, upd), ref)
 
 
+@pytest.mark.parametrize("name,slack", [("elast6_k1", "100"), ("grid20_k2_leaf4", "50"), ("s27_16_k2", "100"),
+                                        ("c1", "100"), ("c1", "37")])
+def test_slack_placed_schedules_replay_bitwise(T, name, slack, oracle, monkeypatch):
+    # units placed between their earliest and latest level (flow_slack_pct: the
+    # default for large short-row matrices is as late as possible): still an
+    # order where every read follows its write, and factor_serial's bits
+    from checkers import emulate_flow, flow_programs
+    _, an = analyzed(name)
+    base = T.Plan(an.a_permuted, an.pattern, an.ranges).flow_tables()["flow_rec"]
+    monkeypatch.setenv("TCG_FLOW_SLACK", slack)
+    plan = T.Plan(an.a_permuted, an.pattern, an.ranges)
+    f = plan.flow_tables()
+    rec = f["flow_rec"]
+    assert rec.shape == base.shape and not np.array_equal(rec, base)  # a different order of the same units
+    assert np.array_equal(np.sort(rec[:, 0]), np.sort(base[:, 0]))
+    slot, upd = flow_programs(f["row_ptr"], f["cols"])
+    ref, _, _, _ = oracle.factor_serial(an.a_permuted, an.pattern.pattern)
+    assert bitwise_equal(emulate_flow(rec, f["values"], slot, upd), ref)
+
+
 @pytest.mark.parametrize("name,panel", [("elast6_k1", "32"), ("elast6_k1", "8"), ("s27_16_k2", "16"),
                                         ("grid20_k2_leaf4", "4")])
 def test_panel_schedules_replay_bitwise(T, name, panel, oracle, monkeypatch):
