@@ -78,7 +78,6 @@ __device__ __forceinline__ unsigned long long wait_value_sys(const double* p, Ct
 // 600 ns; C4 1.49 -> 1.30 at 200 ns; short programs lose: C2 0.41 -> 0.42-0.45 ms).
 template <int OPS = 0, int BO = 0>
 struct Ctx {
-  static constexpr int kBackoff = BO;
   const FlowParams& P;
   unsigned long long t0;
   double* vals;

@@ -89,14 +89,15 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 // same source row, whose values arrive together: polling each on its own
 // clock, they saw them up to a sleep plus a round trip apart (C3 trace: 1.7
 // us), and the pivot waits for the last; together the unit is done one poll
-// after the values are. The warp sleeps only after a round in which no lane
-// got further, and a round re-polls every operand of the batch that is still
-// unwritten (the polls of a warp coalesce now; lane by lane the same re-reads
-// made things slower). B200: C3 2.60 -> 2.38 ms, C4 1.30 -> 1.25, then C3
+// after the values are. A round re-polls every operand of the batch that is
+// still unwritten (the polls of a warp coalesce now; lane by lane the same
+// re-reads made things slower), and the rounds follow each other at the pace
+// of the round trip, without a sleep (a warp's coalesced polls are few enough:
+// C3 2.17 -> 2.13 ms, C4 1.21 -> 1.17 against sleeping 100-600 ns after a
+// round without progress). B200: C3 2.60 -> 2.38 ms, C4 1.30 -> 1.25, then C3
 // 2.34 -> 2.19, s27 0.80 -> 0.72 with the whole batch re-polled; bitwise.
 template <int KB, class Cx>
 __device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const int4 sr, bool on, unsigned gmask) {
-  constexpr int BO = Cx::kBackoff;
   auto LD = [&](int pos) { return C.ld_early(pos); };
   const int ub = sr.x, ue = on ? sr.y : sr.x;
   int u = ub;
@@ -136,17 +137,14 @@ __device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const in
   int j = 0;
   unsigned spins = 0;
   for (;;) {
-    bool progressed = false;
 #pragma unroll
     for (int jj = 0; jj < KB; ++jj)
       if (jj == j && jj < n && xa[jj] != kUnset && xb[jj] != kUnset) {
         v = __dsub_rn(v, __dmul_rn(__longlong_as_double(static_cast<long long>(xa[jj])),
                                    __longlong_as_double(static_cast<long long>(xb[jj]))));
         ++j;
-        progressed = true;
       }
     if (__all_sync(gmask, j >= n)) break;
-    if (BO > 0 && !__any_sync(gmask, progressed)) __nanosleep(BO);
 #pragma unroll
     for (int jj = 0; jj < KB; ++jj)
       if (jj >= j && jj < n) {  // every operand of the batch still unwritten, not only the next product's
