@@ -87,6 +87,11 @@ struct Ctx {
     if (x == kUnset) x = wait_value<BO>(p, P.ctrl, t0, P.timeout_ns);
     return __longlong_as_double(static_cast<long long>(x));
   }
+  // the same without a sleep between polls: the whole warp waits for this one value (one sector a poll)
+  __device__ __forceinline__ double settle_now(const double* p, unsigned long long x) const {
+    if (x == kUnset) x = wait_value<0>(p, P.ctrl, t0, P.timeout_ns);
+    return __longlong_as_double(static_cast<long long>(x));
+  }
   // sharded runs (P.peers): a negative position names another part's value
   __device__ __forceinline__ const double* remote(int pos) const {
     return P.peers[(pos >> 25) & 63] + (pos & 0x1FFFFFF);

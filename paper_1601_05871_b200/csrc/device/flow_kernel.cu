@@ -214,7 +214,8 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
     }
     d = __dsqrt_rn(piv);
   } else {
-    d = C.settle(C.vals + dpos, xd);
+    // (a chunk's lanes are through with their products: they poll their row's pivot together)
+    d = (G == 32 && !Cx::kSysPublish) ? C.settle_now(C.vals + dpos, xd) : C.settle(C.vals + dpos, xd);
   }
   if (stamp) {  // trace: every operand of the first G coordinates is final
     __syncwarp(gmask);
