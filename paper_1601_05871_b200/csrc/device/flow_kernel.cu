@@ -97,7 +97,8 @@ __device__ __forceinline__ double flow_slot(const Cx& C, double v, const int4 sr
 // round without progress). B200: C3 2.60 -> 2.38 ms, C4 1.30 -> 1.25, then C3
 // 2.34 -> 2.19, s27 0.80 -> 0.72 with the whole batch re-polled; bitwise.
 template <int KB, class Cx>
-__device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const int4 sr, bool on, unsigned gmask) {
+__device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const int4 sr, bool on, unsigned gmask,
+                                               int dpos = -1, unsigned long long* xd = nullptr) {
   auto LD = [&](int pos) { return C.ld_early(pos); };
   const int ub = sr.x, ue = on ? sr.y : sr.x;
   int u = ub;
@@ -145,6 +146,8 @@ __device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const in
         ++j;
       }
     if (__all_sync(gmask, j >= n)) break;
+    // (a chunk looks for its row's pivot in the same rounds, so it need not start waiting for it afterwards)
+    if (xd && *xd == kUnset) *xd = C.ld_strong(dpos);
 #pragma unroll
     for (int jj = 0; jj < KB; ++jj)
       if (jj >= j && jj < n) {  // every operand of the batch still unwritten, not only the next product's
@@ -177,7 +180,7 @@ __device__ __forceinline__ void flow_row(const Cx& C, int tb, int L, int dpos, i
   if (KIND == kTrsm) xd = C.ld(dpos);
   double v = 0.0;
   if (G == 32 && !Cx::kSysPublish)  // (sharded parts settle remote operands lane by lane)
-    v = flow_slot_conv<KB>(C, gl < L ? a0 : 0.0, sr0, gl < L, gmask);
+    v = flow_slot_conv<KB>(C, gl < L ? a0 : 0.0, sr0, gl < L, gmask, dpos, KIND == kTrsm ? &xd : nullptr);
   else if (gl < L) v = flow_slot<KB>(C, input_settle(P, C.a + tb + gl, a0, C.t0), sr0);
   if (stamp && gl == 0) stamp[1] = gtimer();  // trace: the group's first coordinate is done
   double d;
