@@ -881,3 +881,18 @@ def test_pipelined_batch_end_to_end(T, oracle, chunks, monkeypatch):
         assert [int(r) for r in rows] == [row if i == 6 else -1 for i in range(10)]
     finally:
         fz.close()
+
+
+def test_forced_backoff_without_a_variant_is_an_error(T, monkeypatch):
+    # a sweep value that has no compiled kernel variant must not run silently
+    # without a back-off (that once made every value above 400 ns measure as 0)
+    monkeypatch.setenv("TCG_FLOW_BACKOFF", "777")
+    fz = T.GpuFactorizer(planned("s27_16_k2"), T.GpuOptions(timeout_s=30))
+    try:
+        with pytest.raises(ValueError, match="back-off"):
+            fz.factor()
+        monkeypatch.setenv("TCG_FLOW_BACKOFF", "600")
+        fz.restore()
+        assert fz.factor().row_kernel == 1
+    finally:
+        fz.close()
