@@ -111,20 +111,26 @@ __device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const in
 #pragma unroll
     for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
     v = __dsub_rn(v, C.product(sr.z, xa0, sr.w, xb0));
-    while (ue - u > KB) {  // (a full batch, and more after it)
+    // the short batch goes first, so that the last one -- the one the warp
+    // settles together -- always holds KB products (when there are that many)
+    int take = (ue - u) % KB;
+    if (take == 0) take = KB;
+    while (ue - u > KB) {  // (a batch, and a full one after it)
       unsigned long long xa[KB], xb[KB];
       int2 c[KB];
 #pragma unroll
       for (int j = 0; j < KB; ++j) {
         c[j] = p[j];
-        xa[j] = LD(c[j].x);
-        xb[j] = LD(c[j].y);
+        xa[j] = (j < take) ? LD(c[j].x) : 0ull;
+        xb[j] = (j < take) ? LD(c[j].y) : 0ull;
       }
-      u += KB;
+      u += take;
 #pragma unroll
       for (int j = 0; j < KB; ++j) p[j] = (u + j < ue) ? __ldg(C.P.upd + u + j) : make_int2(0, 0);
 #pragma unroll
-      for (int j = 0; j < KB; ++j) v = __dsub_rn(v, C.product(c[j].x, xa[j], c[j].y, xb[j]));
+      for (int j = 0; j < KB; ++j)
+        if (j < take) v = __dsub_rn(v, C.product(c[j].x, xa[j], c[j].y, xb[j]));
+      take = KB;
     }
   }
   // the last batch
