@@ -138,8 +138,8 @@ __device__ __forceinline__ double flow_slot_conv(const Cx& C, double v, const in
   unsigned long long xa[KB], xb[KB];
 #pragma unroll
   for (int j = 0; j < KB; ++j) {
-    xa[j] = (j < n) ? C.ld(p[j].x) : 0ull;
-    xb[j] = (j < n) ? C.ld(p[j].y) : 0ull;
+    xa[j] = (j < n) ? LD(p[j].x) : 0ull;
+    xb[j] = (j < n) ? LD(p[j].y) : 0ull;
   }
   int j = 0;
   unsigned spins = 0;
